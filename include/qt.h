@@ -1,0 +1,198 @@
+/*
+ * qt.h — C ABI of libqtmm: block-sparse quadtree matrix multiply on B200.
+ *
+ * The operation (arXiv 1501.07800, Rubensson & Rudberg; P:nnn = line of
+ * /root/reference/PAPER.md):
+ *   C = A*B for block-sparse matrices held as sparse quadtrees whose leaves
+ *   are block-sparse submatrices (abstract; §3.1; §4.1
+ *   P:350-357).  Zero submatrices are NIL at every level and every operation
+ *   on them is skipped (§3.2).  C's block pattern is the structural
+ *   product of A's and B's patterns (reading C-1): nothing is dropped
+ *   numerically; only qt_truncate removes blocks.
+ *
+ * Conventions for every entry point:
+ *   - All functions return qt_status; on failure qt_last_error() names the
+ *     problem (thread-local string, valid until the next failing call on the
+ *     same thread).  No function aborts the process.
+ *   - Pointers are plain host or device pointers; the library detects which
+ *     (cudaPointerGetAttributes).  Host pointers may be pageable or pinned.
+ *   - Sizes are element counts unless named *_bytes.
+ *   - Ownership: the library copies every input array before returning (the
+ *     caller keeps its buffers).  Each qt_mat owns its device memory until
+ *     qt_destroy.  qt_mat handles are immutable after creation (chunks are
+ *     read-only after registration), so A and B may be the same
+ *     handle (C = A*A).
+ *   - All device work runs on the stream given to qt_ctx_create, in stream
+ *     order.  Functions that must know a size on the host (qt_create,
+ *     qt_multiply, qt_truncate, qt_read_back) synchronise that stream.
+ *   - Multi-rank: one process per GPU, one qt_ctx per process.  Functions
+ *     marked "collective" must be called by every rank in the same order.
+ */
+#ifndef QT_H_
+#define QT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QT_OK = 0,
+  QT_EINVAL = 1,  /* invalid argument (null handle, bad size, bs does not divide leaf_dim, ...) */
+  QT_ERANGE = 2,  /* a block coordinate is outside [0, ceil(n/bs)) */
+  QT_EDUP = 3,    /* the same (brow, bcol) is listed twice */
+  QT_EDIM = 4,    /* operand dimensions differ */
+  QT_EBS = 5,     /* operand leaf_dim or block_size differ */
+  QT_EDTYPE = 6,  /* operand dtypes differ, or dtype unsupported */
+  QT_ENOMEM = 7,  /* device allocation failed */
+  QT_ECUDA = 8,   /* a CUDA runtime call failed (message kept) */
+  QT_ENCCL = 9,   /* an NCCL call failed or NCCL could not be loaded */
+  QT_ESTATE = 10  /* handles from different contexts, or context misuse */
+} qt_status;
+
+typedef enum { QT_F64 = 0, QT_F32 = 1 } qt_dtype;
+
+typedef struct qt_ctx_s* qt_ctx;  /* device, stream, rank/world, NCCL communicator */
+typedef struct qt_mat_s* qt_mat;  /* immutable matrix (the rank-local part when world > 1) */
+
+#define QT_MAX_LEVELS 40
+
+/* Statistics of one qt_multiply (the paper's instrumentation, §5, §6.3). */
+typedef struct {
+  int32_t nlevels;           /* L+1: levels 0 (root) .. L (blocks) */
+  int32_t leaf_level;        /* the quadtree level of the leaf matrices */
+  int64_t level_tasks[QT_MAX_LEVELS]; /* multiply tasks per level: (A-node, B-node)
+                                         pairs with both non-NIL (C_l) */
+  int64_t level_c_nodes[QT_MAX_LEVELS]; /* C nodes the BFS created per level (task
+                                           groups; a group whose child products
+                                           all vanish is later pruned as NIL) */
+  int64_t block_products;    /* = level_tasks[L]; effective flops = 2*bs^3 each */
+  int64_t c_blocks;          /* local C blocks */
+  int64_t bytes_recv_payload; /* bytes of A/B block values received */
+  int64_t bytes_recv_meta;   /* request/reply metadata received */
+  int64_t bytes_sent_payload;
+  int64_t bytes_sent_meta;
+  int64_t blocks_recv;       /* remote B blocks received */
+  float ms_exchange;         /* device time of the exchange phase (0 when world == 1) */
+  float ms_symbolic;         /* device time of the symbolic BFS (a5-a7) */
+  float ms_numeric;          /* device time of the numeric kernel (a8) */
+  float ms_total;            /* device time of the whole call */
+} qt_stats;
+
+/* ------------------------------------------------------------------ context */
+
+/* Create a context on CUDA device `device`.  `cuda_stream` is a cudaStream_t
+ * (NULL = the legacy default stream).  `rank`/`world`: this process's rank
+ * and the number of ranks.  `nccl_unique_id`: the 128-byte ncclUniqueId made
+ * by qt_nccl_unique_id() on rank 0 and broadcast by the caller; must be NULL
+ * iff world == 1.  Collective when world > 1 (ncclCommInitRank).
+ * Errors: QT_EINVAL (bad rank/world/device), QT_ECUDA, QT_ENCCL. */
+qt_status qt_ctx_create(int device, void* cuda_stream, int rank, int world,
+                        const void* nccl_unique_id, qt_ctx* out);
+qt_status qt_ctx_destroy(qt_ctx ctx);
+
+/* Write a fresh 128-byte ncclUniqueId into `out128` (loads NCCL on demand).
+ * Errors: QT_ENCCL when libnccl.so.2 cannot be loaded. */
+qt_status qt_nccl_unique_id(void* out128);
+
+/* ------------------------------------------------------------------ matrices */
+
+/* Create a quadtree matrix of dimension n (the matrix-parameters chunk,
+ * §3.1: n, leaf dimension, leaf block size) from `nblocks` dense
+ * blocks.  Block t has block coordinates (brow[t], bcol[t]) and values
+ * values[t*bs*bs .. (t+1)*bs*bs) in row-major order, of type `dtype`
+ * (double for QT_F64, float for QT_F32).  brow, bcol, values may be host or
+ * device pointers; order of blocks is arbitrary.  Zero submatrices are never
+ * stored: only the listed blocks exist, a listed all-zero block is
+ * kept (reading C-2).
+ * The quadtree is uniform: 2^L x 2^L blocks with 2^L >= max(2, ceil(n/bs)),
+ * padded children are NIL (reading C-3); the leaf level is
+ * L - log2(leaf_dim/bs) (leaves are block-sparse submatrices, §4.1).
+ * Requirements: block_size == 32 (the built kernels), leaf_dim a power-of-two
+ * multiple of block_size, n % block_size == 0 (reading C-4), nblocks >= 0
+ * (0 gives the NIL matrix).
+ * Multi-rank (world > 1): collective; each rank passes the blocks of its own
+ * block-row range.  `row_bounds` (host, world+1 non-decreasing block-row
+ * boundaries, first 0 and last ceil(n/bs)) gives the ranges; NULL means equal
+ * strips of ceil(nbr/world) rows.  A block outside the rank's range is
+ * QT_ERANGE.  Ignored when world == 1.
+ * Errors: QT_EINVAL, QT_ERANGE (names the block), QT_EDUP (names the block),
+ * QT_EDTYPE, QT_ENOMEM, QT_ECUDA. */
+qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
+                    qt_dtype dtype, int64_t nblocks, const int32_t* brow,
+                    const int32_t* bcol, const void* values,
+                    const int32_t* row_bounds, qt_mat* out);
+
+/* C = A*B (§3.2).  A and B must share ctx, n, leaf_dim, block_size
+ * and dtype.  Runs the symbolic multiply (level-synchronous BFS over the two
+ * quadtrees, skipping NIL children at every level, emitting per level the
+ * compacted queue of (A-node, B-node) tasks grouped by C node), then the
+ * numeric block-sparse multiply (each C block = sum over k ascending of
+ * A(I,k)*B(k,J), accumulated in registers, no atomics).  The result is a new
+ * handle; A and B are unchanged.  `st` may be NULL.
+ * Multi-rank: collective.  C gets A's block-row ranges; each rank receives
+ * from the owners exactly the B block rows its A rows reference (NCCL
+ * send/recv) and reports the bytes in `st`.
+ * Errors: QT_EINVAL, QT_EDIM, QT_EBS, QT_EDTYPE, QT_ESTATE, QT_ENOMEM,
+ * QT_ECUDA, QT_ENCCL. */
+qt_status qt_multiply(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st);
+
+/* Frobenius-norm truncation (reading C-16): remove the longest
+ * prefix of blocks, sorted ascending by Frobenius norm with ties broken by
+ * (brow, bcol), whose accumulated squared norm is < tau^2, so that
+ * ||A - out||_F < tau (or nothing removed).  tau >= 0.  New handle; A
+ * unchanged.  Multi-rank: collective (the prefix is global).
+ * Errors: QT_EINVAL, QT_ENOMEM, QT_ECUDA, QT_ENCCL. */
+qt_status qt_truncate(qt_mat A, double tau, qt_mat* out);
+
+/* Describe a matrix.  Any output pointer may be NULL.  local_nblocks: blocks
+ * held by this rank; global_nblocks: over all ranks; row_lo/row_hi: this
+ * rank's block-row range. */
+qt_status qt_info(qt_mat A, int64_t* n, int32_t* leaf_dim, int32_t* block_size,
+                  qt_dtype* dtype, int64_t* local_nblocks, int64_t* global_nblocks,
+                  int32_t* row_lo, int32_t* row_hi);
+
+/* Per-level non-NIL node counts of the quadtree (levels 0..L), written to
+ * `counts` (host, capacity `cap`); *nlevels receives L+1. */
+qt_status qt_level_nodes(qt_mat A, int64_t* counts, int32_t cap, int32_t* nlevels);
+
+/* Copy this rank's blocks out, sorted by (brow, bcol), values row-major per
+ * block.  brow/bcol: local_nblocks int32 each; values: local_nblocks*bs*bs
+ * elements of the matrix dtype.  Host or device pointers; any may be NULL
+ * to skip it.  Synchronises the stream before returning.
+ * Errors: QT_EINVAL, QT_ECUDA. */
+qt_status qt_read_back(qt_mat A, int32_t* brow, int32_t* bcol, void* values);
+
+/* Release a matrix (stream-ordered; safe right after the last use). */
+qt_status qt_destroy(qt_mat A);
+
+/* Message of the last failure on this thread ("" if none). */
+const char* qt_last_error(void);
+
+/* ---------------------------------------------------------------- diagnostics */
+
+/* The multi-rank multiply of rank g out of P virtual ranks, on this single
+ * (world == 1) context: A and B are whole matrices; the call restricts them
+ * to rank g's block rows [row_bounds[g], row_bounds[g+1]) (A, B and C share
+ * the bounds), determines the remote B rows as qt_multiply does, packs them
+ * from B exactly as their owners would, and runs the same B_ext merge and
+ * local multiply.  Only the NCCL transfers are replaced by device copies.
+ * C holds rank g's block rows of A*B; `st` reports what rank g would receive.
+ * Used to test the distributed path on one GPU. */
+qt_status qt_multiply_virtual(qt_mat A, qt_mat B, int32_t P, int32_t g,
+                              const int32_t* row_bounds, qt_mat* C, qt_stats* st);
+
+/* Number of CUDA kernels this context has launched so far (bench accounting). */
+int64_t qt_kernel_launches(qt_ctx ctx);
+
+/* FP64 peak microbenchmark on the context's device (roofline denominator,
+ * MEASURED_PEAKS.json has no FP64 entry): kind 0 = DMMA (mma.sync m8n8k4 f64),
+ * kind 1 = DFMA.  Runs about `ms` milliseconds of back-to-back work and
+ * returns the achieved FLOP/s in *flops. */
+qt_status qt_fp64_peak(qt_ctx ctx, int kind, float ms, double* flops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QT_H_ */

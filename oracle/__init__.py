@@ -273,9 +273,11 @@ def gamma(k: int, u: float) -> float:
     return k * u / (1.0 - k * u)
 
 
-def higham_bound(nbr: int, bs: int, A, B, k_terms: int, u: float = 2.0 ** -53, nthreads=None):
+def higham_bound(nbr: int, bs: int, A, B, k_terms: int, u: float = 2.0 ** -53, nthreads=None,
+                 rows=None):
     """Elementwise bound 2*gamma_K*(|A||B|) on |C_computed - C_exact| valid for
     any summation order, with or without FMA (Higham, Accuracy and Stability,
     §3.5).  Returns (brow, bcol, bound_vals) aligned with spgemm's output."""
-    r, c, v = spgemm(nbr, bs, (A[0], A[1], np.abs(A[2])), (B[0], B[1], np.abs(B[2])), nthreads)
+    r, c, v = spgemm(nbr, bs, (A[0], A[1], np.abs(A[2])), (B[0], B[1], np.abs(B[2])), nthreads,
+                     rows=rows)
     return r, c, 2.0 * gamma(k_terms, u) * v

@@ -1,0 +1,363 @@
+// C ABI entry points of libqtmm (include/qt.h).  Argument checking, handle
+// management and orchestration only; every step of the path runs in the
+// kernels of qt_tree.cu, qt_symbolic.cu, qt_numeric.cu and qt_dist.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+
+#include "qt_internal.h"
+
+namespace qt {
+
+static thread_local std::string g_last_error;
+
+void fail(qt_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  throw Error(s, buf);
+}
+
+static qt_status handle_exception() {
+  try {
+    throw;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return QT_ENOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return QT_EINVAL;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return QT_EINVAL;
+  }
+}
+
+static int ilog2(int64_t x) {
+  int r = 0;
+  while ((1ll << (r + 1)) <= x) ++r;
+  return r;
+}
+
+}  // namespace qt
+
+using namespace qt;
+
+#define API_TRY try {
+#define API_CATCH              \
+  }                            \
+  catch (...) {                \
+    return handle_exception(); \
+  }                            \
+  return QT_OK;
+
+extern "C" {
+
+const char* qt_last_error(void) { return g_last_error.c_str(); }
+
+qt_status qt_ctx_create(int device, void* cuda_stream, int rank, int world,
+                        const void* nccl_unique_id, qt_ctx* out) {
+  API_TRY
+  if (!out) fail(QT_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) fail(QT_EINVAL, "bad rank %d / world %d", rank, world);
+  if ((world > 1) != (nccl_unique_id != nullptr))
+    fail(QT_EINVAL, "nccl_unique_id must be non-NULL iff world > 1");
+  int ndev = 0;
+  QT_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) fail(QT_EINVAL, "device %d not in [0,%d)", device, ndev);
+  QT_CUDA(cudaSetDevice(device));
+  qt_ctx c = new qt_ctx_s();
+  try {
+    c->device = device;
+    c->stream = (cudaStream_t)cuda_stream;
+    c->rank = rank;
+    c->world = world;
+    QT_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    for (auto& e : c->ev) QT_CUDA(cudaEventCreate(&e));
+    // keep freed blocks of the stream-ordered allocator cached in the pool
+    cudaMemPool_t pool;
+    QT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    QT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    c->counters.alloc(256, c->stream);
+    QT_CUDA(cudaMemsetAsync(c->counters.p, 0, 256, c->stream));
+    c->pinned_bytes = 256;
+    QT_CUDA(cudaMallocHost(&c->pinned, c->pinned_bytes));
+    if (world > 1) dist_init(c, nccl_unique_id);
+    QT_CUDA(cudaStreamSynchronize(c->stream));
+  } catch (...) {
+    if (c->pinned) cudaFreeHost(c->pinned);
+    delete c;
+    throw;
+  }
+  *out = c;
+  API_CATCH
+}
+
+qt_status qt_ctx_destroy(qt_ctx ctx) {
+  API_TRY
+  if (!ctx) return QT_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->world > 1) dist_finalize(ctx);
+  for (auto& e : ctx->ev) cudaEventDestroy(e);
+  ctx->scratch.release();
+  ctx->counters.release();
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  delete ctx;
+  API_CATCH
+}
+
+qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size, qt_dtype dtype,
+                    int64_t nblocks, const int32_t* brow, const int32_t* bcol, const void* values,
+                    const int32_t* row_bounds, qt_mat* out) {
+  API_TRY
+  if (!ctx || !out) fail(QT_EINVAL, "ctx/out is NULL");
+  *out = nullptr;
+  QT_CUDA(cudaSetDevice(ctx->device));
+  if (dtype != QT_F64 && dtype != QT_F32) fail(QT_EDTYPE, "unknown dtype %d", (int)dtype);
+  if (block_size != 32) fail(QT_EINVAL, "block_size %d: only 32 is built", block_size);
+  if (n <= 0 || n % block_size != 0)
+    fail(QT_EINVAL, "n=%lld must be a positive multiple of block_size=%d (reading C-4)",
+         (long long)n, block_size);
+  if (leaf_dim < block_size || leaf_dim % block_size != 0 ||
+      ((leaf_dim / block_size) & (leaf_dim / block_size - 1)) != 0)
+    fail(QT_EINVAL, "leaf_dim=%d must be a power-of-two multiple of block_size=%d", leaf_dim,
+         block_size);
+  if (nblocks < 0 || nblocks >= (1ll << 31)) fail(QT_EINVAL, "nblocks=%lld", (long long)nblocks);
+  if (nblocks > 0 && (!brow || !bcol || !values)) fail(QT_EINVAL, "NULL block arrays");
+  int64_t nbr = n / block_size;
+  if (nbr > (1 << 20)) fail(QT_EINVAL, "n too large (more than 2^20 block rows)");
+  qt_mat M = new qt_mat_s();
+  try {
+    M->ctx = ctx;
+    M->n = n;
+    M->leaf_dim = leaf_dim;
+    M->bs = block_size;
+    M->dtype = dtype;
+    M->nbr = (int32_t)nbr;
+    int L = 1;
+    while ((1ll << L) < nbr) ++L;
+    M->L = L;
+    M->leaf_level = std::max(0, L - ilog2(leaf_dim / block_size));
+    // block-row ownership
+    M->bounds.assign(ctx->world + 1, 0);
+    if (ctx->world == 1) {
+      M->bounds[1] = (int32_t)nbr;
+    } else if (row_bounds) {
+      for (int g = 0; g <= ctx->world; ++g) M->bounds[g] = row_bounds[g];
+      if (M->bounds[0] != 0 || M->bounds[ctx->world] != nbr)
+        fail(QT_EINVAL, "row_bounds must start at 0 and end at %lld", (long long)nbr);
+      for (int g = 0; g < ctx->world; ++g)
+        if (M->bounds[g + 1] < M->bounds[g]) fail(QT_EINVAL, "row_bounds not non-decreasing");
+    } else {
+      int64_t per = (nbr + ctx->world - 1) / ctx->world;
+      for (int g = 0; g <= ctx->world; ++g) M->bounds[g] = (int32_t)std::min<int64_t>(nbr, per * g);
+    }
+    M->row_lo = M->bounds[ctx->rank];
+    M->row_hi = M->bounds[ctx->rank + 1];
+    // inputs to the device (stream-ordered copies from host, pinned or pageable)
+    cudaStream_t st = ctx->stream;
+    size_t es = elem_size(dtype);
+    DevBuf dr, dc, dv;
+    const int32_t* pr = brow;
+    const int32_t* pc = bcol;
+    const void* pv = values;
+    if (nblocks > 0) {
+      if (!is_device_ptr(brow)) {
+        dr.alloc(nblocks * 4, st);
+        QT_CUDA(cudaMemcpyAsync(dr.p, brow, nblocks * 4, cudaMemcpyHostToDevice, st));
+        pr = dr.as<int32_t>();
+      }
+      if (!is_device_ptr(bcol)) {
+        dc.alloc(nblocks * 4, st);
+        QT_CUDA(cudaMemcpyAsync(dc.p, bcol, nblocks * 4, cudaMemcpyHostToDevice, st));
+        pc = dc.as<int32_t>();
+      }
+      if (!is_device_ptr(values)) {
+        dv.alloc(nblocks * 1024 * es, st);
+        QT_CUDA(cudaMemcpyAsync(dv.p, values, nblocks * 1024 * es, cudaMemcpyHostToDevice, st));
+        pv = dv.p;
+      }
+    }
+    build_from_blocks(M, nblocks, pr, pc, pv, M->row_lo, M->row_hi);
+    M->global_nb = M->nb;
+    if (ctx->world > 1) {
+      std::vector<int64_t> all(ctx->world);
+      int64_t mine = M->nb;
+      allgather_i64(ctx, &mine, all.data(), 1);
+      M->global_nb = 0;
+      for (auto v : all) M->global_nb += v;
+    }
+    QT_CUDA(cudaStreamSynchronize(st));
+  } catch (...) {
+    delete M;
+    throw;
+  }
+  *out = M;
+  API_CATCH
+}
+
+qt_status qt_multiply(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st) {
+  API_TRY
+  if (!A || !B || !C) fail(QT_EINVAL, "NULL argument");
+  *C = nullptr;
+  if (A->ctx != B->ctx) fail(QT_ESTATE, "A and B belong to different contexts");
+  if (A->n != B->n) fail(QT_EDIM, "dimension mismatch: %lld vs %lld", (long long)A->n, (long long)B->n);
+  if (A->leaf_dim != B->leaf_dim || A->bs != B->bs)
+    fail(QT_EBS, "leaf_dim/block_size mismatch: (%d,%d) vs (%d,%d)", A->leaf_dim, A->bs,
+         B->leaf_dim, B->bs);
+  if (A->dtype != B->dtype) fail(QT_EDTYPE, "dtype mismatch");
+  qt_ctx ctx = A->ctx;
+  QT_CUDA(cudaSetDevice(ctx->device));
+  ensure_levels(A);
+  ensure_levels(B);
+  qt_stats local;
+  qt_stats& S = st ? *st : local;
+  memset(&S, 0, sizeof(S));
+  QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  qt_mat R;
+  if (ctx->world == 1) {
+    float ms_sym = 0, ms_num = 0;
+    R = multiply_local(A, B, &S, &ms_sym, &ms_num);
+    S.ms_symbolic = ms_sym;
+    S.ms_numeric = ms_num;
+  } else {
+    R = multiply_dist(A, B, &S);
+  }
+  QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+  QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
+  QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
+  R->global_nb = R->nb;
+  *C = R;
+  API_CATCH
+}
+
+qt_status qt_truncate(qt_mat A, double tau, qt_mat* out) {
+  API_TRY
+  if (!A || !out) fail(QT_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (!(tau >= 0)) fail(QT_EINVAL, "tau must be >= 0");
+  QT_CUDA(cudaSetDevice(A->ctx->device));
+  if (A->ctx->world > 1) fail(QT_EINVAL, "multi-rank truncate is not built yet");
+  qt_mat R = truncate(A, tau);
+  R->global_nb = R->nb;
+  QT_CUDA(cudaStreamSynchronize(A->ctx->stream));
+  *out = R;
+  API_CATCH
+}
+
+qt_status qt_info(qt_mat A, int64_t* n, int32_t* leaf_dim, int32_t* block_size, qt_dtype* dtype,
+                  int64_t* local_nblocks, int64_t* global_nblocks, int32_t* row_lo,
+                  int32_t* row_hi) {
+  API_TRY
+  if (!A) fail(QT_EINVAL, "NULL matrix");
+  if (n) *n = A->n;
+  if (leaf_dim) *leaf_dim = A->leaf_dim;
+  if (block_size) *block_size = A->bs;
+  if (dtype) *dtype = A->dtype;
+  if (local_nblocks) *local_nblocks = A->nb;
+  if (global_nblocks) *global_nblocks = A->global_nb;
+  if (row_lo) *row_lo = A->row_lo;
+  if (row_hi) *row_hi = A->row_hi;
+  API_CATCH
+}
+
+qt_status qt_level_nodes(qt_mat A, int64_t* counts, int32_t cap, int32_t* nlevels) {
+  API_TRY
+  if (!A) fail(QT_EINVAL, "NULL matrix");
+  QT_CUDA(cudaSetDevice(A->ctx->device));
+  ensure_levels(A);
+  if (nlevels) *nlevels = A->L + 1;
+  for (int l = 0; l <= A->L && l < cap; ++l) counts[l] = A->cnt[l];
+  API_CATCH
+}
+
+qt_status qt_read_back(qt_mat A, int32_t* brow, int32_t* bcol, void* values) {
+  API_TRY
+  if (!A) fail(QT_EINVAL, "NULL matrix");
+  QT_CUDA(cudaSetDevice(A->ctx->device));
+  read_back(A, brow, bcol, values);
+  API_CATCH
+}
+
+qt_status qt_destroy(qt_mat A) {
+  API_TRY
+  if (!A) return QT_OK;
+  cudaSetDevice(A->ctx->device);
+  delete A;
+  API_CATCH
+}
+
+qt_status qt_nccl_unique_id(void* out128) {
+  API_TRY
+  if (!out128) fail(QT_EINVAL, "out128 is NULL");
+  nccl_unique_id(out128);
+  API_CATCH
+}
+
+qt_status qt_multiply_virtual(qt_mat A, qt_mat B, int32_t P, int32_t g, const int32_t* row_bounds,
+                              qt_mat* C, qt_stats* st) {
+  API_TRY
+  if (!A || !B || !C || !row_bounds) fail(QT_EINVAL, "NULL argument");
+  *C = nullptr;
+  if (A->ctx != B->ctx) fail(QT_ESTATE, "A and B belong to different contexts");
+  if (A->ctx->world != 1) fail(QT_ESTATE, "virtual ranks need a single-rank context");
+  if (A->n != B->n) fail(QT_EDIM, "dimension mismatch");
+  if (A->leaf_dim != B->leaf_dim || A->bs != B->bs) fail(QT_EBS, "leaf_dim/block_size mismatch");
+  if (A->dtype != B->dtype) fail(QT_EDTYPE, "dtype mismatch");
+  if (P < 1 || g < 0 || g >= P) fail(QT_EINVAL, "bad P=%d / g=%d", P, g);
+  if (row_bounds[0] != 0 || row_bounds[P] != A->nbr) fail(QT_EINVAL, "row_bounds must span [0,%d]", A->nbr);
+  for (int q = 0; q < P; ++q)
+    if (row_bounds[q + 1] < row_bounds[q]) fail(QT_EINVAL, "row_bounds not non-decreasing");
+  qt_ctx ctx = A->ctx;
+  QT_CUDA(cudaSetDevice(ctx->device));
+  qt_stats local;
+  qt_stats& S = st ? *st : local;
+  memset(&S, 0, sizeof(S));
+  QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  qt_mat R = multiply_virtual(A, B, row_bounds, P, g, &S);
+  QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+  QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
+  QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
+  R->global_nb = R->nb;
+  R->bounds.assign(row_bounds, row_bounds + P + 1);
+  *C = R;
+  API_CATCH
+}
+
+int64_t qt_kernel_launches(qt_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+qt_status qt_fp64_peak(qt_ctx ctx, int kind, float ms, double* flops) {
+  API_TRY
+  if (!ctx || !flops || (kind != 0 && kind != 1)) fail(QT_EINVAL, "bad arguments");
+  QT_CUDA(cudaSetDevice(ctx->device));
+  const int grid = ctx->num_sms * 2, threads = 256;
+  // calibrate: a short run, then one sized to `ms`
+  int iters = 256;
+  float t = 0;
+  for (int rep = 0; rep < 2; ++rep) {
+    launch_fp64_peak(ctx, kind, 16, grid);  // warm
+    QT_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
+    launch_fp64_peak(ctx, kind, iters, grid);
+    QT_CUDA(cudaEventRecord(ctx->ev[6], ctx->stream));
+    QT_CUDA(cudaEventSynchronize(ctx->ev[6]));
+    QT_CUDA(cudaEventElapsedTime(&t, ctx->ev[5], ctx->ev[6]));
+    if (rep == 0) iters = std::max(16, (int)(iters * (ms / std::max(t, 1e-3f))));
+  }
+  double fl = kind == 0 ? (double)grid * (threads / 32) * iters * 16 * 512
+                        : (double)grid * threads * iters * 4 * 8 * 2;
+  *flops = fl / (t * 1e-3);
+  API_CATCH
+}
+
+}  // extern "C"

@@ -1,0 +1,45 @@
+// Device helpers shared by the libqtmm kernels (Morton keys, internal block
+// layout).  Not shared with the oracle.
+#pragma once
+#include <stdint.h>
+
+namespace qt {
+
+// Morton key of a block: row bits at odd positions, column bits at even
+// positions, so key >> 2 is the parent node and key & 3 = 2*rowbit + colbit is
+// the child slot in row-major order (NW, NE, SW, SE) — the quadtree split of
+// §3.1 addressed by coordinates.
+__host__ __device__ inline uint64_t spread_bits(uint32_t x) {
+  uint64_t v = x;
+  v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+__host__ __device__ inline uint32_t compact_bits(uint64_t v) {
+  v &= 0x5555555555555555ull;
+  v = (v | (v >> 1)) & 0x3333333333333333ull;
+  v = (v | (v >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v >> 4)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v >> 8)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v >> 16)) & 0x00000000FFFFFFFFull;
+  return (uint32_t)v;
+}
+__host__ __device__ inline uint64_t morton(uint32_t row, uint32_t col) {
+  return (spread_bits(row) << 1) | spread_bits(col);
+}
+__host__ __device__ inline uint32_t morton_row(uint64_t k) { return compact_bits(k >> 1); }
+__host__ __device__ inline uint32_t morton_col(uint64_t k) { return compact_bits(k); }
+
+// Internal FP64 block layout (32x32): element (r, c) lives at
+//   r*32 + (c ^ ((r & 3) << 2)),
+// i.e. the eight 32-byte chunks of each 256-byte row are XOR-permuted by
+// (r & 3).  With this layout the warp-wide fragment loads of
+// mma.sync.m8n8k4.f64 — A: (row g, col t), B: (row t, col g), g = lane>>2,
+// t = lane&3 — hit every 8-byte bank pair exactly twice (2 wavefronts, the
+// minimum for 256 bytes), and the accumulator pairs stay 16-byte contiguous.
+__host__ __device__ inline int swz64(int r, int c) { return r * 32 + (c ^ ((r & 3) << 2)); }
+
+}  // namespace qt

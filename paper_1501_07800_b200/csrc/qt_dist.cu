@@ -1,0 +1,616 @@
+// Multi-GPU multiply (X1-X3): locality-aware row strips + NCCL point-to-point
+// exchange of exactly the B block rows a rank's output needs.
+//
+// Paper: output work and data are kept where the data is (the quadtree keeps
+// locality, P:82-97 Fig. fig:random_destruction, §5.2) and each
+// process fetches the remote chunks its tasks need; "data received by each
+// process" is the central measured quantity (§6.3).  CHT-MPI
+// moves chunks by work stealing + MPI fetches; here the mapping
+// is static: rank g owns block rows [b_g, b_{g+1}) of A, B and C (output
+// subtrees aligned to quadtree rows), A stays put, and rank g receives from
+// their owners the B block rows K in cols(A[rows_g, :]) outside its own range
+// — one request/response round over NCCL send/recv (NVLink / NVSwitch).
+//
+// Protocol (all int32 unless noted):
+//   0. allgather of the P x P matrix of requested-row counts (int64)
+//   1. requester -> owner : the sorted list of requested block rows
+//   2. owner -> requester : number of blocks in each requested row
+//   3. owner -> requester : block columns, then the block values (internal
+//      layout, 8 KiB per FP64 block) — the payload
+// The requester merges the received blocks with its local B into B_ext (a
+// quadtree over the union, Morton-sorted; the level L-1 child table stores
+// pool ids, ids >= nb_local point into the received payload) and runs the
+// single-GPU multiply A_local * B_ext.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cub/cub.cuh>
+
+#include "qt_common.cuh"
+#include "qt_internal.h"
+
+namespace qt {
+
+// ------------------------------------------------------------------ NCCL
+
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) {
+    if (!api.ok) fail(QT_ENCCL, "NCCL unavailable: %s", api.why.c_str());
+    return api;
+  }
+  tried = true;
+  api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!api.h) api.h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!api.h) {
+    api.why = dlerror() ? dlerror() : "dlopen failed";
+    fail(QT_ENCCL, "cannot load libnccl.so.2: %s", api.why.c_str());
+  }
+#define LOAD(name)                                                       \
+  api.name = (decltype(api.name))dlsym(api.h, "nccl" #name);             \
+  if (!api.name) {                                                       \
+    api.why = "missing symbol nccl" #name;                               \
+    fail(QT_ENCCL, "%s", api.why.c_str());                               \
+  }
+  LOAD(GetUniqueId)
+  LOAD(CommInitRank)
+  LOAD(CommDestroy)
+  LOAD(Send)
+  LOAD(Recv)
+  LOAD(GroupStart)
+  LOAD(GroupEnd)
+  LOAD(AllGather)
+  LOAD(AllReduce)
+  LOAD(GetErrorString)
+#undef LOAD
+  api.ok = true;
+  return api;
+}
+
+#define NCCL_CALL(x)                                                                       \
+  do {                                                                                     \
+    ncclResult_t r_ = (x);                                                                 \
+    if (r_ != ncclSuccess) fail(QT_ENCCL, "%s: %s", #x, nccl().GetErrorString(r_));        \
+  } while (0)
+
+static ncclComm_t comm(qt_ctx ctx) { return (ncclComm_t)ctx->nccl_comm; }
+
+void dist_init(qt_ctx ctx, const void* uid) {
+  NcclApi& N = nccl();
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof(id));
+  ncclComm_t c;
+  NCCL_CALL(N.CommInitRank(&c, ctx->world, id, ctx->rank));
+  ctx->nccl_comm = c;
+}
+
+void dist_finalize(qt_ctx ctx) {
+  if (ctx->nccl_comm) nccl().CommDestroy(comm(ctx));
+  ctx->nccl_comm = nullptr;
+}
+
+void allgather_i64(qt_ctx ctx, const int64_t* send_host, int64_t* recv_host, int count) {
+  NcclApi& N = nccl();
+  DevBuf s(8 * count, ctx->stream), r(8ll * count * ctx->world, ctx->stream);
+  QT_CUDA(cudaMemcpyAsync(s.p, send_host, 8 * count, cudaMemcpyHostToDevice, ctx->stream));
+  NCCL_CALL(N.AllGather(s.p, r.p, count, ncclInt64, comm(ctx), ctx->stream));
+  QT_CUDA(cudaMemcpyAsync(recv_host, r.p, 8ll * count * ctx->world, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  QT_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+double allreduce_sum_f64(qt_ctx ctx, double v) {
+  NcclApi& N = nccl();
+  DevBuf b(8, ctx->stream);
+  QT_CUDA(cudaMemcpyAsync(b.p, &v, 8, cudaMemcpyHostToDevice, ctx->stream));
+  NCCL_CALL(N.AllReduce(b.p, b.p, 1, ncclFloat64, ncclSum, comm(ctx), ctx->stream));
+  double r;
+  QT_CUDA(cudaMemcpyAsync(&r, b.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  QT_CUDA(cudaStreamSynchronize(ctx->stream));
+  return r;
+}
+
+// ------------------------------------------------------------------ kernels
+
+namespace {
+
+constexpr int kT = 256;
+inline unsigned gfor(int64_t n) { return (unsigned)std::max<int64_t>(1, (n + kT - 1) / kT); }
+
+// flag[K] = 1 for every block column K of A outside [lo, hi)
+__global__ void k_mark_cols(const uint64_t* __restrict__ key, int64_t nb, int32_t lo, int32_t hi,
+                            int32_t* __restrict__ flag) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nb;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int32_t c = (int32_t)morton_col(key[t]);
+    if (c < lo || c >= hi) flag[c] = 1;
+  }
+}
+
+__global__ void k_scatter_flagged(const int32_t* __restrict__ flag, const int32_t* __restrict__ incl,
+                                  int32_t n, int32_t* __restrict__ out) {
+  int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n && flag[t]) out[incl[t] - 1] = t;
+}
+
+// flag[t] = 1 if block t's row is in [lo, hi)
+__global__ void k_flag_rows(const uint64_t* __restrict__ key, int64_t nb, int32_t lo, int32_t hi,
+                            uint8_t* __restrict__ keep) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nb;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int32_t r = (int32_t)morton_row(key[t]);
+    keep[t] = (r >= lo && r < hi) ? 1 : 0;
+  }
+}
+
+__global__ void k_rm_keys(const uint64_t* __restrict__ key, int64_t nb, uint64_t* __restrict__ rm,
+                          int32_t* __restrict__ iota) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nb;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = key[t];
+    rm[t] = ((uint64_t)morton_row(k) << 32) | morton_col(k);
+    iota[t] = (int32_t)t;
+  }
+}
+
+// row_cnt[row] += 1 per block (rows of the whole grid)
+__global__ void k_row_hist(const uint64_t* __restrict__ rm_sorted, int64_t nb,
+                           int32_t* __restrict__ row_cnt) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nb;
+       t += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&row_cnt[(int32_t)(rm_sorted[t] >> 32)], 1);
+}
+
+// counts of requested rows
+__global__ void k_req_counts(const int32_t* __restrict__ rows, int32_t n,
+                             const int32_t* __restrict__ row_cnt, int32_t* __restrict__ out) {
+  int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = row_cnt[rows[t]];
+}
+
+// one warp per requested row: copy its blocks (columns + values) to the
+// packed buffers at the row's offset
+__global__ void k_pack(const int32_t* __restrict__ rows, int32_t n, const int32_t* __restrict__ offs,
+                       const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ order,
+                       const uint64_t* __restrict__ rm_sorted, const uint4* __restrict__ pool,
+                       int vec_per_block, int32_t* __restrict__ cols, uint4* __restrict__ payload) {
+  int lane = threadIdx.x & 31;
+  int64_t w = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  if (w >= n) return;
+  int32_t r = rows[w];
+  int32_t s0 = row_ptr[r], s1 = row_ptr[r + 1];
+  int32_t o = offs[w];
+  for (int32_t s = s0; s < s1; ++s) {
+    int32_t src = order[s];
+    if (lane == 0) cols[o + (s - s0)] = (int32_t)(rm_sorted[s] & 0xffffffffu);
+    const uint4* sp = pool + (int64_t)src * vec_per_block;
+    uint4* dp = payload + (int64_t)(o + (s - s0)) * vec_per_block;
+    for (int e = lane; e < vec_per_block; e += 32) dp[e] = sp[e];
+  }
+}
+
+// Morton keys of the received blocks; ids continue after the local blocks
+__global__ void k_remote_keys(const int32_t* __restrict__ rows, int32_t n,
+                              const int32_t* __restrict__ offs, const int32_t* __restrict__ cols,
+                              uint64_t* __restrict__ key, int32_t* __restrict__ ids, int64_t nb_local) {
+  int lane = threadIdx.x & 31;
+  int64_t w = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  if (w >= n) return;
+  int32_t r = rows[w];
+  for (int32_t e = offs[w] + lane; e < offs[w + 1]; e += 32) {
+    key[e] = morton((uint32_t)r, (uint32_t)cols[e]);
+    ids[e] = (int32_t)(nb_local + e);
+  }
+}
+
+__global__ void k_iota(int32_t* __restrict__ out, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = (int32_t)t;
+}
+
+template <class T>
+void excl_sum(qt_ctx ctx, const T* in, T* out, int64_t n) {
+  size_t tb = 0;
+  QT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, ctx->stream));
+  void* tmp = scratch(ctx, tb);
+  QT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, (int)n, ctx->stream));
+  ctx->launches += 2;
+}
+template <class T>
+void incl_sum(qt_ctx ctx, const T* in, T* out, int64_t n) {
+  size_t tb = 0;
+  QT_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out, (int)n, ctx->stream));
+  void* tmp = scratch(ctx, tb);
+  QT_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, in, out, (int)n, ctx->stream));
+  ctx->launches += 2;
+}
+template <class V>
+void sort_pairs(qt_ctx ctx, const uint64_t* kin, uint64_t* kout, const V* vin, V* vout, int64_t n,
+                int bits) {
+  size_t tb = 0;
+  QT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, (int)n, 0, bits,
+                                          ctx->stream));
+  void* tmp = scratch(ctx, tb);
+  QT_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, vout, (int)n, 0, bits,
+                                          ctx->stream));
+  ctx->launches += 4;
+}
+
+// Row-major view of a matrix for the owner side: blocks sorted by (row, col)
+// and a row pointer over the whole grid.
+struct RowView {
+  DevBuf rm_sorted, order, row_ptr;
+};
+
+void build_row_view(qt_mat B, RowView& v) {
+  qt_ctx ctx = B->ctx;
+  cudaStream_t st = ctx->stream;
+  int64_t nb = B->nb;
+  int32_t nbr = B->nbr;
+  v.row_ptr.alloc(4ll * (nbr + 1), st);
+  DevBuf cnt(4ll * (nbr + 1), st);
+  QT_CUDA(cudaMemsetAsync(cnt.p, 0, 4ll * (nbr + 1), st));
+  if (nb > 0) {
+    DevBuf rm(nb * 8, st), iota(nb * 4, st);
+    v.rm_sorted.alloc(nb * 8, st);
+    v.order.alloc(nb * 4, st);
+    k_rm_keys<<<gfor(nb), kT, 0, st>>>(B->key.as<uint64_t>(), nb, rm.as<uint64_t>(), iota.as<int32_t>());
+    QT_LAUNCH_CHECK(ctx);
+    sort_pairs(ctx, rm.as<uint64_t>(), v.rm_sorted.as<uint64_t>(), iota.as<int32_t>(),
+               v.order.as<int32_t>(), nb, 64);
+    k_row_hist<<<gfor(nb), kT, 0, st>>>(v.rm_sorted.as<uint64_t>(), nb, cnt.as<int32_t>());
+    QT_LAUNCH_CHECK(ctx);
+  }
+  excl_sum(ctx, cnt.as<int32_t>(), v.row_ptr.as<int32_t>(), nbr + 1);
+}
+
+// The block rows a rank with rows [lo, hi) of A needs from others: sorted.
+std::vector<int32_t> needed_rows(qt_mat A, int32_t lo, int32_t hi, DevBuf& d_rows) {
+  qt_ctx ctx = A->ctx;
+  cudaStream_t st = ctx->stream;
+  int32_t nbr = A->nbr;
+  DevBuf flag(4ll * nbr, st), incl(4ll * nbr, st);
+  QT_CUDA(cudaMemsetAsync(flag.p, 0, 4ll * nbr, st));
+  if (A->nb > 0) {
+    k_mark_cols<<<gfor(A->nb), kT, 0, st>>>(A->key.as<uint64_t>(), A->nb, lo, hi, flag.as<int32_t>());
+    QT_LAUNCH_CHECK(ctx);
+  }
+  incl_sum(ctx, flag.as<int32_t>(), incl.as<int32_t>(), nbr);
+  int32_t n = 0;
+  QT_CUDA(cudaMemcpyAsync(&n, incl.as<int32_t>() + nbr - 1, 4, cudaMemcpyDeviceToHost, st));
+  QT_CUDA(cudaStreamSynchronize(st));
+  d_rows.alloc(4ll * std::max(n, 1), st);
+  std::vector<int32_t> h(n);
+  if (n > 0) {
+    k_scatter_flagged<<<gfor(nbr), kT, 0, st>>>(flag.as<int32_t>(), incl.as<int32_t>(), nbr,
+                                                d_rows.as<int32_t>());
+    QT_LAUNCH_CHECK(ctx);
+    QT_CUDA(cudaMemcpyAsync(h.data(), d_rows.p, 4ll * n, cudaMemcpyDeviceToHost, st));
+    QT_CUDA(cudaStreamSynchronize(st));
+  }
+  return h;
+}
+
+// Owner side, step 2: per requested row, its block count (device) -> counts
+void pack_counts(qt_mat B, const RowView& v, const int32_t* d_rows, int32_t n, int32_t* d_counts) {
+  qt_ctx ctx = B->ctx;
+  if (n == 0) return;
+  DevBuf rc(4ll * B->nbr, ctx->stream);
+  // row_cnt[r] = row_ptr[r+1] - row_ptr[r]; computed on the fly by k_req_counts via row_ptr diff
+  // (reuse k_req_counts on an explicit histogram for clarity)
+  QT_CUDA(cudaMemsetAsync(rc.p, 0, 4ll * B->nbr, ctx->stream));
+  if (B->nb > 0) {
+    k_row_hist<<<gfor(B->nb), kT, 0, ctx->stream>>>(v.rm_sorted.as<uint64_t>(), B->nb, rc.as<int32_t>());
+    QT_LAUNCH_CHECK(ctx);
+  }
+  k_req_counts<<<gfor(n), kT, 0, ctx->stream>>>(d_rows, n, rc.as<int32_t>(), d_counts);
+  QT_LAUNCH_CHECK(ctx);
+}
+
+// Owner side, step 3: columns and values of the requested rows, packed at the
+// exclusive-scan offsets of the counts.
+void pack_blocks(qt_mat B, const RowView& v, const int32_t* d_rows, int32_t n, const int32_t* d_offs,
+                 int32_t* d_cols, void* d_payload) {
+  qt_ctx ctx = B->ctx;
+  if (n == 0) return;
+  int vpb = (int)(1024 * elem_size(B->dtype) / 16);
+  unsigned g = (unsigned)((n + 7) / 8);
+  k_pack<<<g, 256, 0, ctx->stream>>>(d_rows, n, d_offs, v.row_ptr.as<int32_t>(), v.order.as<int32_t>(),
+                                     v.rm_sorted.as<uint64_t>(), static_cast<const uint4*>(B->pool_ptr()),
+                                     vpb, d_cols, static_cast<uint4*>(d_payload));
+  QT_LAUNCH_CHECK(ctx);
+}
+
+// What a requester ends up with after the exchange.
+struct Received {
+  int32_t nrows = 0;
+  int64_t nblk = 0;
+  DevBuf rows, counts, offs, cols, payload;
+};
+
+qt_mat clone_shape(qt_mat A) {
+  qt_mat M = new qt_mat_s();
+  M->ctx = A->ctx;
+  M->n = A->n;
+  M->leaf_dim = A->leaf_dim;
+  M->bs = A->bs;
+  M->dtype = A->dtype;
+  M->L = A->L;
+  M->leaf_level = A->leaf_level;
+  M->nbr = A->nbr;
+  M->row_lo = A->row_lo;
+  M->row_hi = A->row_hi;
+  M->bounds = A->bounds;
+  return M;
+}
+
+// B_ext = local B rows + received rows; the received payload is owned by `rx`.
+qt_mat make_b_ext(qt_mat B, Received& rx) {
+  qt_ctx ctx = B->ctx;
+  cudaStream_t st = ctx->stream;
+  qt_mat X = clone_shape(B);
+  try {
+    int64_t nl = B->nb, nr = rx.nblk, nt = nl + nr;
+    X->nb = nt;
+    X->pool1 = B->pool_ptr();
+    X->pool2 = rx.payload.p;
+    X->split = nl;
+    if (nt == 0) {
+      build_levels(X);
+      return X;
+    }
+    DevBuf keys(8 * nt, st), ids(4 * nt, st), sids(4 * nt, st);
+    if (nl > 0) {
+      QT_CUDA(cudaMemcpyAsync(keys.p, B->key.p, 8 * nl, cudaMemcpyDeviceToDevice, st));
+      k_iota<<<gfor(nl), kT, 0, st>>>(ids.as<int32_t>(), nl);
+      QT_LAUNCH_CHECK(ctx);
+    }
+    if (nr > 0) {
+      unsigned g = (unsigned)((rx.nrows + 7) / 8);
+      k_remote_keys<<<g, 256, 0, st>>>(rx.rows.as<int32_t>(), rx.nrows, rx.offs.as<int32_t>(),
+                                       rx.cols.as<int32_t>(), keys.as<uint64_t>() + nl,
+                                       ids.as<int32_t>() + nl, nl);
+      QT_LAUNCH_CHECK(ctx);
+    }
+    X->key.alloc(8 * nt, st);
+    sort_pairs(ctx, keys.as<uint64_t>(), X->key.as<uint64_t>(), ids.as<int32_t>(), sids.as<int32_t>(),
+               nt, 2 * X->L);
+    build_levels(X, sids.as<int32_t>());
+  } catch (...) {
+    delete X;
+    throw;
+  }
+  return X;
+}
+
+qt_mat rows_of(qt_mat A, int32_t lo, int32_t hi) {
+  qt_ctx ctx = A->ctx;
+  DevBuf keep(std::max<int64_t>(A->nb, 1), ctx->stream);
+  if (A->nb > 0) {
+    k_flag_rows<<<gfor(A->nb), kT, 0, ctx->stream>>>(A->key.as<uint64_t>(), A->nb, lo, hi,
+                                                     keep.as<uint8_t>());
+    QT_LAUNCH_CHECK(ctx);
+  }
+  qt_mat M = select_blocks(A, keep.as<uint8_t>());
+  M->row_lo = lo;
+  M->row_hi = hi;
+  return M;
+}
+
+void fill_exchange_stats(qt_stats* S, const Received& rx, size_t block_bytes) {
+  S->blocks_recv = rx.nblk;
+  S->bytes_recv_payload = rx.nblk * (int64_t)block_bytes;
+  S->bytes_recv_meta = 4ll * rx.nrows + 4ll * rx.nblk;
+  S->bytes_sent_meta = 4ll * rx.nrows;
+}
+
+qt_mat finish_multiply(qt_mat A_local, qt_mat Bx, qt_stats* S) {
+  float ms_sym = 0, ms_num = 0;
+  qt_mat C = multiply_local(A_local, Bx, S, &ms_sym, &ms_num);
+  S->ms_symbolic = ms_sym;
+  S->ms_numeric = ms_num;
+  return C;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ NCCL path
+
+qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S) {
+  qt_ctx ctx = A->ctx;
+  cudaStream_t st = ctx->stream;
+  const int P = ctx->world, g = ctx->rank;
+  if (A->bounds != B->bounds) fail(QT_EINVAL, "A and B must have the same block-row bounds");
+  NcclApi& N = nccl();
+  const size_t bb = 1024 * elem_size(A->dtype);
+  QT_CUDA(cudaEventRecord(ctx->ev[5], st));
+  const int32_t lo = A->row_lo, hi = A->row_hi;
+  // 1. rows needed from others, split by owner (bounds are sorted, so is the list)
+  DevBuf d_req;
+  std::vector<int32_t> req = needed_rows(A, lo, hi, d_req);
+  std::vector<int64_t> my_counts(P, 0), seg_off(P + 1, 0);
+  for (int q = 0; q < P; ++q) {
+    auto b = std::lower_bound(req.begin(), req.end(), A->bounds[q]);
+    auto e = std::lower_bound(req.begin(), req.end(), A->bounds[q + 1]);
+    seg_off[q] = b - req.begin();
+    my_counts[q] = e - b;
+  }
+  seg_off[P] = (int64_t)req.size();
+  // 0. P x P request matrix
+  std::vector<int64_t> M((size_t)P * P);
+  allgather_i64(ctx, my_counts.data(), M.data(), P);  // M[r*P+q] = rows r wants from q
+  // 1. request lists
+  std::vector<int64_t> in_off(P + 1, 0);
+  for (int r = 0; r < P; ++r) in_off[r + 1] = in_off[r] + (r == g ? 0 : M[(size_t)r * P + g]);
+  int64_t n_in = in_off[P];
+  DevBuf d_in_rows(4 * std::max<int64_t>(n_in, 1), st);
+  NCCL_CALL(N.GroupStart());
+  for (int q = 0; q < P; ++q) {
+    if (q == g) continue;
+    if (my_counts[q] > 0)
+      NCCL_CALL(N.Send(d_req.as<int32_t>() + seg_off[q], my_counts[q], ncclInt32, q, comm(ctx), st));
+    int64_t cnt = M[(size_t)q * P + g];
+    if (cnt > 0)
+      NCCL_CALL(N.Recv(d_in_rows.as<int32_t>() + in_off[q], cnt, ncclInt32, q, comm(ctx), st));
+  }
+  NCCL_CALL(N.GroupEnd());
+  // 2. owner: block counts of the requested rows; requester: receive counts
+  RowView v;
+  build_row_view(B, v);
+  DevBuf d_out_counts(4 * std::max<int64_t>(n_in, 1), st), d_out_offs(4 * (n_in + 1), st);
+  pack_counts(B, v, d_in_rows.as<int32_t>(), (int32_t)n_in, d_out_counts.as<int32_t>());
+  Received rx;
+  rx.nrows = (int32_t)req.size();
+  rx.rows = std::move(d_req);
+  rx.counts.alloc(4 * std::max<int64_t>(rx.nrows, 1), st);
+  rx.offs.alloc(4 * (rx.nrows + 1), st);
+  NCCL_CALL(N.GroupStart());
+  for (int q = 0; q < P; ++q) {
+    if (q == g) continue;
+    int64_t cnt_out = M[(size_t)q * P + g];
+    if (cnt_out > 0)
+      NCCL_CALL(N.Send(d_out_counts.as<int32_t>() + in_off[q], cnt_out, ncclInt32, q, comm(ctx), st));
+    if (my_counts[q] > 0)
+      NCCL_CALL(N.Recv(rx.counts.as<int32_t>() + seg_off[q], my_counts[q], ncclInt32, q, comm(ctx), st));
+  }
+  NCCL_CALL(N.GroupEnd());
+  // offsets on both sides (host copies decide the message sizes)
+  std::vector<int32_t> h_out_counts(n_in), h_in_counts(rx.nrows);
+  if (n_in > 0) {
+    QT_CUDA(cudaMemcpyAsync(h_out_counts.data(), d_out_counts.p, 4 * n_in, cudaMemcpyDeviceToHost, st));
+  }
+  if (rx.nrows > 0) {
+    QT_CUDA(cudaMemcpyAsync(h_in_counts.data(), rx.counts.p, 4ll * rx.nrows, cudaMemcpyDeviceToHost, st));
+  }
+  QT_CUDA(cudaStreamSynchronize(st));
+  std::vector<int32_t> h_out_offs(n_in + 1, 0), h_in_offs(rx.nrows + 1, 0);
+  for (int64_t i = 0; i < n_in; ++i) h_out_offs[i + 1] = h_out_offs[i] + h_out_counts[i];
+  for (int32_t i = 0; i < rx.nrows; ++i) h_in_offs[i + 1] = h_in_offs[i] + h_in_counts[i];
+  QT_CUDA(cudaMemcpyAsync(d_out_offs.p, h_out_offs.data(), 4 * (n_in + 1), cudaMemcpyHostToDevice, st));
+  QT_CUDA(cudaMemcpyAsync(rx.offs.p, h_in_offs.data(), 4ll * (rx.nrows + 1), cudaMemcpyHostToDevice, st));
+  int64_t nblk_out = h_out_offs[n_in];
+  rx.nblk = h_in_offs[rx.nrows];
+  // 3. owner packs columns + values; exchange
+  DevBuf d_out_cols(4 * std::max<int64_t>(nblk_out, 1), st), d_out_pay(bb * std::max<int64_t>(nblk_out, 1), st);
+  pack_blocks(B, v, d_in_rows.as<int32_t>(), (int32_t)n_in, d_out_offs.as<int32_t>(),
+              d_out_cols.as<int32_t>(), d_out_pay.p);
+  rx.cols.alloc(4 * std::max<int64_t>(rx.nblk, 1), st);
+  rx.payload.alloc(bb * std::max<int64_t>(rx.nblk, 1), st);
+  int64_t sent_payload = 0, sent_meta = 0;
+  NCCL_CALL(N.GroupStart());
+  for (int q = 0; q < P; ++q) {
+    if (q == g) continue;
+    int64_t r0 = in_off[q], r1 = in_off[q + 1];
+    int64_t b0 = h_out_offs[r0], b1 = h_out_offs[r1];
+    if (b1 > b0) {
+      NCCL_CALL(N.Send(d_out_cols.as<int32_t>() + b0, b1 - b0, ncclInt32, q, comm(ctx), st));
+      NCCL_CALL(N.Send((char*)d_out_pay.p + b0 * bb, (b1 - b0) * bb, ncclInt8, q, comm(ctx), st));
+      sent_payload += (b1 - b0) * bb;
+    }
+    sent_meta += 4 * (r1 - r0) + 4 * (b1 - b0);
+    int64_t i0 = h_in_offs[seg_off[q]], i1 = h_in_offs[seg_off[q] + my_counts[q]];
+    if (i1 > i0) {
+      NCCL_CALL(N.Recv(rx.cols.as<int32_t>() + i0, i1 - i0, ncclInt32, q, comm(ctx), st));
+      NCCL_CALL(N.Recv((char*)rx.payload.p + i0 * bb, (i1 - i0) * bb, ncclInt8, q, comm(ctx), st));
+    }
+  }
+  NCCL_CALL(N.GroupEnd());
+  qt_mat Bx = make_b_ext(B, rx);
+  QT_CUDA(cudaEventRecord(ctx->ev[6], st));
+  fill_exchange_stats(S, rx, bb);
+  S->bytes_sent_payload = sent_payload;
+  S->bytes_sent_meta += sent_meta;
+  qt_mat C;
+  try {
+    C = finish_multiply(A, Bx, S);
+  } catch (...) {
+    delete Bx;
+    throw;
+  }
+  delete Bx;
+  QT_CUDA(cudaEventElapsedTime(&S->ms_exchange, ctx->ev[5], ctx->ev[6]));
+  return C;
+}
+
+// ------------------------------------------------------------ virtual ranks
+
+qt_mat multiply_virtual(qt_mat A, qt_mat B, const int32_t* bounds, int P, int g, qt_stats* S) {
+  qt_ctx ctx = A->ctx;
+  cudaStream_t st = ctx->stream;
+  const size_t bb = 1024 * elem_size(A->dtype);
+  const int32_t lo = bounds[g], hi = bounds[g + 1];
+  qt_mat Al = rows_of(A, lo, hi);
+  qt_mat Bl = nullptr, Bx = nullptr, C = nullptr;
+  try {
+    Bl = rows_of(B, lo, hi);
+    QT_CUDA(cudaEventRecord(ctx->ev[5], st));
+    DevBuf d_req;
+    std::vector<int32_t> req = needed_rows(Al, lo, hi, d_req);
+    Received rx;
+    rx.nrows = (int32_t)req.size();
+    rx.rows = std::move(d_req);
+    rx.counts.alloc(4 * std::max<int64_t>(rx.nrows, 1), st);
+    rx.offs.alloc(4 * (rx.nrows + 1), st);
+    // every owner's rows are rows of the whole B: pack from B directly
+    RowView v;
+    build_row_view(B, v);
+    pack_counts(B, v, rx.rows.as<int32_t>(), rx.nrows, rx.counts.as<int32_t>());
+    std::vector<int32_t> hc(rx.nrows), ho(rx.nrows + 1, 0);
+    if (rx.nrows > 0)
+      QT_CUDA(cudaMemcpyAsync(hc.data(), rx.counts.p, 4ll * rx.nrows, cudaMemcpyDeviceToHost, st));
+    QT_CUDA(cudaStreamSynchronize(st));
+    for (int32_t i = 0; i < rx.nrows; ++i) ho[i + 1] = ho[i] + hc[i];
+    QT_CUDA(cudaMemcpyAsync(rx.offs.p, ho.data(), 4ll * (rx.nrows + 1), cudaMemcpyHostToDevice, st));
+    rx.nblk = ho[rx.nrows];
+    rx.cols.alloc(4 * std::max<int64_t>(rx.nblk, 1), st);
+    rx.payload.alloc(bb * std::max<int64_t>(rx.nblk, 1), st);
+    pack_blocks(B, v, rx.rows.as<int32_t>(), rx.nrows, rx.offs.as<int32_t>(), rx.cols.as<int32_t>(),
+                rx.payload.p);
+    Bx = make_b_ext(Bl, rx);
+    QT_CUDA(cudaEventRecord(ctx->ev[6], st));
+    fill_exchange_stats(S, rx, bb);
+    C = finish_multiply(Al, Bx, S);
+    QT_CUDA(cudaEventElapsedTime(&S->ms_exchange, ctx->ev[5], ctx->ev[6]));
+    C->row_lo = lo;
+    C->row_hi = hi;
+  } catch (...) {
+    delete Al;
+    delete Bl;
+    delete Bx;
+    throw;
+  }
+  delete Bx;
+  delete Bl;
+  delete Al;
+  return C;
+}
+
+}  // namespace qt
+
+namespace qt {
+void nccl_unique_id(void* out128) {
+  NcclApi& N = nccl();
+  ncclUniqueId id;
+  NCCL_CALL(N.GetUniqueId(&id));
+  memcpy(out128, &id, sizeof(id));
+}
+}  // namespace qt

@@ -1,0 +1,186 @@
+// Internal declarations of libqtmm (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/qt.h"
+
+namespace qt {
+
+// ----------------------------------------------------------------- errors
+
+struct Error : std::runtime_error {
+  qt_status status;
+  Error(qt_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] void fail(qt_status s, const char* fmt, ...);
+
+#define QT_CUDA(x)                                                                  \
+  do {                                                                              \
+    cudaError_t e_ = (x);                                                           \
+    if (e_ != cudaSuccess)                                                          \
+      ::qt::fail(e_ == cudaErrorMemoryAllocation ? QT_ENOMEM : QT_ECUDA, "%s:%d %s: %s", \
+                 __FILE__, __LINE__, #x, cudaGetErrorString(e_));                   \
+  } while (0)
+
+#define QT_LAUNCH_CHECK(ctx)                                                        \
+  do {                                                                              \
+    (ctx)->launches++;                                                              \
+    cudaError_t e_ = cudaGetLastError();                                            \
+    if (e_ != cudaSuccess)                                                          \
+      ::qt::fail(QT_ECUDA, "%s:%d kernel launch: %s", __FILE__, __LINE__,          \
+                 cudaGetErrorString(e_));                                           \
+  } while (0)
+
+// ----------------------------------------------------------------- memory
+
+// Stream-ordered device buffer (cudaMallocAsync from the device's default
+// pool, which keeps freed memory cached: no OS calls in steady state).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t b, cudaStream_t st) { alloc(b, st); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; s = o.s; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t b, cudaStream_t st) {
+    release();
+    s = st;
+    bytes = b;
+    if (b == 0) return;
+    cudaError_t e = cudaMallocAsync(&p, b, st);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      fail(QT_ENOMEM, "device allocation of %zu bytes failed: %s", b, cudaGetErrorString(e));
+    }
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// ----------------------------------------------------------------- handles
+
+struct NcclApi;  // dynamically loaded NCCL entry points (qt_dist.cu)
+
+}  // namespace qt
+
+struct qt_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  void* nccl_comm = nullptr;
+  int num_sms = 148;
+  int64_t launches = 0;
+  cudaEvent_t ev[8] = {};
+  qt::DevBuf scratch;  // cub temp storage, grown on demand
+  qt::DevBuf counters; // small device counters (scheduler, errors)
+  void* pinned = nullptr;  // small pinned host staging area
+  size_t pinned_bytes = 0;
+};
+
+struct qt_mat_s {
+  qt_ctx ctx = nullptr;
+  int64_t n = 0;
+  int32_t leaf_dim = 0, bs = 0;
+  qt_dtype dtype = QT_F64;
+  int L = 1;           // levels above the block level; level L = blocks
+  int leaf_level = 0;
+  int32_t nbr = 0;     // block rows (= block cols) of the matrix
+  int64_t nb = 0;      // local blocks
+  int64_t global_nb = 0;
+  int32_t row_lo = 0, row_hi = 0;
+  std::vector<int32_t> bounds;  // world+1 block-row boundaries
+  qt::DevBuf key;      // uint64 [nb] Morton keys, ascending
+  qt::DevBuf pool;     // [nb][bs*bs] values in the internal (swizzled) layout
+  std::vector<int64_t> cnt;     // non-NIL nodes per level, l = 0..L (cnt[L] = nb)
+  std::vector<qt::DevBuf> child; // child[l] : int32 [cnt[l]][4], l = 0..L-1 (-1 = NIL)
+  bool levels_built = true;     // false for a fresh product: built on first use
+  // B_ext of a multi-rank multiply: pool1 overrides pool.p (a borrowed view of
+  // the local pool); block ids >= split live in pool2 (the received blocks).
+  const void* pool1 = nullptr;
+  const void* pool2 = nullptr;
+  int64_t split = INT64_MAX;
+  const void* pool_ptr() const { return pool1 ? pool1 : pool.p; }
+};
+
+namespace qt {
+
+inline size_t elem_size(qt_dtype d) { return d == QT_F64 ? 8 : 4; }
+
+// memory kind of a pointer
+bool is_device_ptr(const void* p);
+
+// cub temp storage of at least `bytes` on the ctx
+void* scratch(qt_ctx ctx, size_t bytes);
+
+// ----- kernels / host drivers (qt_tree.cu)
+// keys from coordinates; validation; sort; duplicate check; swizzled pool fill.
+void build_from_blocks(qt_mat M, int64_t nb, const int32_t* d_brow, const int32_t* d_bcol,
+                       const void* d_vals, int32_t row_lo, int32_t row_hi);
+// build levels L-1..0 from the sorted block keys in M->key.  leaf_ids (device,
+// optional): the pool index of each sorted block, stored in the level L-1
+// child table instead of the sorted position (used by the merged B_ext).
+void build_levels(qt_mat M, const int32_t* leaf_ids = nullptr);
+inline void ensure_levels(qt_mat M) {
+  if (!M->levels_built) { build_levels(M); M->levels_built = true; }
+}
+// row-major (brow, bcol) order and un-swizzle into caller buffers
+void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals);
+// truncate
+qt_mat truncate(qt_mat A, double tau);
+// copy `keep` flagged blocks (Morton order preserved) of A into a new matrix
+qt_mat select_blocks(qt_mat A, const uint8_t* d_keep);
+
+// ----- symbolic + numeric multiply (qt_symbolic.cu, qt_numeric.cu)
+qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* st, float* ms_sym, float* ms_num);
+
+struct NumericArgs {
+  int64_t ntiles;            // C nodes at level L-1
+  const int32_t* tile_start; // [ntiles+1] pair ranges
+  const int32_t* pa;         // A node (level L-1) per pair
+  const int32_t* pb;         // B node (level L-1) per pair
+  const int4* childA;        // A child table at level L-1 (block indices)
+  const int4* childB;
+  const int4* childC;        // C child table at level L-1 (C block indices)
+  const void* poolA;
+  const void* poolB;
+  const void* poolB2;        // remote pool for B blocks >= splitB (or null)
+  int64_t splitB;
+  void* poolC;
+  int* counter;              // tile scheduler counter (zeroed before launch)
+};
+void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a);
+void launch_fp64_peak(qt_ctx ctx, int kind, int iters, int grid);
+
+// ----- distributed (qt_dist.cu)
+void dist_init(qt_ctx ctx, const void* uid);
+void nccl_unique_id(void* out128);
+void dist_finalize(qt_ctx ctx);
+qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* st);
+// the same path for virtual rank g of P on one device (D2D copies stand in for
+// the NCCL transfers); A and B are whole matrices on this context.
+qt_mat multiply_virtual(qt_mat A, qt_mat B, const int32_t* bounds, int P, int g, qt_stats* st);
+void allgather_i64(qt_ctx ctx, const int64_t* send_host, int64_t* recv_host, int count);
+double allreduce_sum_f64(qt_ctx ctx, double v);
+
+}  // namespace qt

@@ -1,0 +1,328 @@
+// Numeric block-sparse multiply (K5): C(I,J) = sum_{k ascending} A(I,k) B(k,J)
+// for every C block produced by the symbolic pass.
+//
+// Paper: the leaf multiply is a sum of outer products executed as cuBLAS
+// batched GEMMs, one batch per inner index k (Fig.
+// fig:block-sparse-mmul).  Here the same block products are instead grouped by
+// OUTPUT: a work item ("tile") is a C node at level L-1, i.e. a 2x2 group of
+// 32x32 C blocks, together with its ascending-k task list from the symbolic
+// pass.  Each step of a tile stages A(I0,k), A(I1,k), B(k,J0), B(k,J1) in
+// shared memory with 1-D TMA bulk copies (cp.async.bulk, mbarrier
+// complete_tx); four consumer warps each own one C block and accumulate
+// A(Ii,k)·B(k,Jj) in registers with FP64 tensor-core DMMA
+// (mma.sync.m8n8k4.f64) — every staged block feeds two products.  Each C block
+// is written exactly once, by one warp: no atomics, no batch barriers, and a
+// deterministic summation order (ascending k, reading C-5).
+//
+// CTA = 4 consumer warps + 1 producer warp, persistent (one CTA per SM), tiles
+// handed out by an atomic counter in Morton order (L2 locality), 6-stage
+// smem ring (6 x 32 KiB).
+#include <cuda_runtime.h>
+
+#include "qt_common.cuh"
+#include "qt_internal.h"
+
+namespace qt {
+
+namespace {
+
+constexpr int kStages = 6;
+constexpr int kConsumerWarps = 4;
+constexpr int kNumThreads = (kConsumerWarps + 1) * 32;
+constexpr int kBlockElems = 1024;                // 32 x 32
+constexpr int kStageElems = 4 * kBlockElems;     // A0 A1 B0 B1
+constexpr int kStageBytes = kStageElems * 8;     // 32 KiB (FP64)
+
+enum : int { F_COMPUTE = 1, F_STORE = 2, F_DONE = 4 };
+
+struct __align__(16) StageHdr {
+  int a[2];
+  int b[2];
+  int c[4];
+  int flags;
+  int pad[3];
+};
+
+constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + kStages * sizeof(StageHdr) +
+                              2 * kStages * sizeof(uint64_t);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ int4 shfl_int4(int4 v, int src) {
+  v.x = __shfl_sync(0xffffffffu, v.x, src);
+  v.y = __shfl_sync(0xffffffffu, v.y, src);
+  v.z = __shfl_sync(0xffffffffu, v.z, src);
+  v.w = __shfl_sync(0xffffffffu, v.w, src);
+  return v;
+}
+
+// One 32x32x32 block product on one warp: acc += A·B, A and B in the internal
+// swizzled layout (qt_common.cuh swz64) in shared memory.
+__device__ __forceinline__ void warp_block_mma(double (&acc)[4][4][2], const double* __restrict__ As,
+                                               const double* __restrict__ Bs, int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+  const int xa = g & 3;
+  const int xb = g ^ (t4 << 2);
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    double af[4], bf[4];
+    const int acol = ((ks ^ xa) << 2) | t4;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) af[m] = As[(m * 8 + g) * 32 + acol];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) bf[n] = Bs[(ks * 4 + t4) * 32 + ((n * 8) ^ xb)];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int n = 0; n < 4; ++n) dmma(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+  }
+}
+
+__global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  double* data = reinterpret_cast<double*>(smem);
+  StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + (size_t)kStages * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(hdr + kStages);
+  uint64_t* empty = full + kStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  int stage = 0;
+  uint32_t phase = 0;
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------------ producer
+    const double* poolA = static_cast<const double*>(a.poolA);
+    const double* poolB = static_cast<const double*>(a.poolB);
+    const double* poolB2 = static_cast<const double*>(a.poolB2);
+    for (;;) {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(a.counter, 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= a.ntiles) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) {
+          hdr[stage].flags = F_DONE;
+          mbar_arrive(&full[stage]);
+        }
+        break;
+      }
+      const int p0 = a.tile_start[t], p1 = a.tile_start[t + 1];
+      const int4 cc = a.childC[t];
+      for (int pb0 = p0; pb0 < p1; pb0 += 32) {
+        const int p = pb0 + lane;
+        int4 ca = make_int4(-1, -1, -1, -1), cb = ca;
+        if (p < p1) {
+          ca = a.childA[a.pa[p]];
+          cb = a.childB[a.pb[p]];
+        }
+        const int nloc = min(32, p1 - pb0);
+        for (int u = 0; u < nloc; ++u) {
+          const int4 A4 = shfl_int4(ca, u);
+          const int4 B4 = shfl_int4(cb, u);
+#pragma unroll
+          for (int kb = 0; kb < 2; ++kb) {
+            // A child (i,kb) in slot 2i+kb ; B child (kb,j) in slot 2kb+j
+            const int a0 = kb ? A4.y : A4.x, a1 = kb ? A4.w : A4.z;
+            const int b0 = kb ? B4.z : B4.x, b1 = kb ? B4.w : B4.y;
+            if (!((a0 >= 0 || a1 >= 0) && (b0 >= 0 || b1 >= 0))) continue;
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (lane == 0) {
+              StageHdr& h = hdr[stage];
+              h.a[0] = a0;
+              h.a[1] = a1;
+              h.b[0] = b0;
+              h.b[1] = b1;
+              h.flags = F_COMPUTE;
+              const uint32_t bytes = 8192u * ((a0 >= 0) + (a1 >= 0) + (b0 >= 0) + (b1 >= 0));
+              mbar_arrive_expect_tx(&full[stage], bytes);
+              double* dst = data + (size_t)stage * kStageElems;
+              if (a0 >= 0) bulk_g2s(dst, poolA + (size_t)a0 * kBlockElems, 8192u, &full[stage]);
+              if (a1 >= 0)
+                bulk_g2s(dst + kBlockElems, poolA + (size_t)a1 * kBlockElems, 8192u, &full[stage]);
+              if (b0 >= 0) {
+                const double* src = b0 < a.splitB ? poolB + (size_t)b0 * kBlockElems
+                                                  : poolB2 + (size_t)(b0 - a.splitB) * kBlockElems;
+                bulk_g2s(dst + 2 * kBlockElems, src, 8192u, &full[stage]);
+              }
+              if (b1 >= 0) {
+                const double* src = b1 < a.splitB ? poolB + (size_t)b1 * kBlockElems
+                                                  : poolB2 + (size_t)(b1 - a.splitB) * kBlockElems;
+                bulk_g2s(dst + 3 * kBlockElems, src, 8192u, &full[stage]);
+              }
+            }
+            __syncwarp();
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+      mbar_wait(&empty[stage], phase ^ 1);
+      if (lane == 0) {
+        StageHdr& h = hdr[stage];
+        h.c[0] = cc.x;
+        h.c[1] = cc.y;
+        h.c[2] = cc.z;
+        h.c[3] = cc.w;
+        h.flags = F_STORE;
+        mbar_arrive(&full[stage]);
+      }
+      __syncwarp();
+      if (++stage == kStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    const int wi = warp >> 1, wj = warp & 1;
+    double* poolC = static_cast<double*>(a.poolC);
+    double acc[4][4][2];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+    const int g = lane >> 2, t4 = lane & 3;
+    for (;;) {
+      mbar_wait(&full[stage], phase);
+      const StageHdr& h = hdr[stage];
+      const int flags = h.flags;
+      if (flags & F_DONE) break;
+      if (flags & F_STORE) {
+        const int cb = h.c[warp];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (cb >= 0) {
+          double* Cb = poolC + (size_t)cb * kBlockElems;
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int n = 0; n < 4; ++n) {
+              const int r = m * 8 + g, c = n * 8 + 2 * t4;
+              *reinterpret_cast<double2*>(Cb + swz64(r, c)) = make_double2(acc[m][n][0], acc[m][n][1]);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+      } else {
+        const bool go = h.a[wi] >= 0 && h.b[wj] >= 0;
+        if (go) {
+          const double* st = data + (size_t)stage * kStageElems;
+          warp_block_mma(acc, st + wi * kBlockElems, st + (2 + wj) * kBlockElems, lane);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+      }
+      if (++stage == kStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- FP64 peaks
+
+__global__ void k_peak_dmma(double* out, int iters) {
+  double acc[16][2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
+  const double av = 1.0 + threadIdx.x * 1e-9, bv = 1e-9;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dmma(acc[i][0], acc[i][1], av, bv);
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += acc[i][0] + acc[i][1];
+  if (s == 123.456) out[0] = s;
+}
+
+__global__ void k_peak_dfma(double* out, int iters) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = fma(x[i], 1.0000001, 1e-9);
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 123.456) out[0] = s;
+}
+
+}  // namespace
+
+void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a) {
+  if (dt != QT_F64) fail(QT_EDTYPE, "the FP32 numeric kernel is not built yet");
+  static bool attr_set = false;
+  if (!attr_set) {
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmemBytes));
+    attr_set = true;
+  }
+  QT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), ctx->stream));
+  int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
+  k_numeric_f64<<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
+  QT_LAUNCH_CHECK(ctx);
+}
+
+// kind 0: DMMA (512 flop per mma per warp), kind 1: DFMA (2 flop per lane)
+void launch_fp64_peak(qt_ctx ctx, int kind, int iters, int grid) {
+  double* out = ctx->counters.as<double>() + 12;
+  if (kind == 0)
+    k_peak_dmma<<<grid, 256, 0, ctx->stream>>>(out, iters);
+  else
+    k_peak_dfma<<<grid, 256, 0, ctx->stream>>>(out, iters);
+  QT_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace qt

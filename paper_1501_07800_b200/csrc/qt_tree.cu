@@ -1,0 +1,420 @@
+// Quadtree construction (K1/K2), read-back (K9) and truncation (K8).
+//
+// Matrix chunk = quadtree node (§3.1): every internal node has four
+// child slots, NIL (-1) for a zero submatrix; zero submatrices are never
+// stored.  On the device a level is an array of non-NIL nodes in Morton order
+// and a child table int32[n_l][4]; the block level (l = L) is the block pool
+// itself, sorted by Morton key.  The leaf matrices of the paper (block-sparse
+// submatrices, §4.1) are the subtrees below the leaf level: their
+// "two-dimensional array where only non-zero submatrices are allocated" is
+// represented by the same child tables, which lets the symbolic multiply run
+// the recursion of §3.2 straight through the leaves to block granularity
+// ("merging several of the lowest levels").
+#include <cub/cub.cuh>
+
+#include "qt_common.cuh"
+#include "qt_internal.h"
+
+namespace qt {
+
+namespace {
+
+constexpr int kThreads = 256;
+inline unsigned grid_for(int64_t n, int t = kThreads) {
+  int64_t g = (n + t - 1) / t;
+  return (unsigned)(g < 1 ? 1 : (g > (1 << 30) ? (1 << 30) : g));
+}
+
+__global__ void k_keys(const int32_t* __restrict__ brow, const int32_t* __restrict__ bcol,
+                       int64_t nb, int32_t nbr, int32_t row_lo, int32_t row_hi,
+                       uint64_t* __restrict__ key, int32_t* __restrict__ idx,
+                       unsigned long long* __restrict__ err_range) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nb;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int32_t r = brow[t], c = bcol[t];
+    bool bad = r < 0 || c < 0 || r >= nbr || c >= nbr || r < row_lo || r >= row_hi;
+    if (bad) atomicMin(err_range, (unsigned long long)t);
+    key[t] = bad ? 0 : morton((uint32_t)r, (uint32_t)c);
+    idx[t] = (int32_t)t;
+  }
+}
+
+__global__ void k_dup(const uint64_t* __restrict__ key, int64_t nb,
+                      unsigned long long* __restrict__ err_dup) {
+  for (int64_t t = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nb;
+       t += (int64_t)gridDim.x * blockDim.x)
+    if (key[t] == key[t - 1]) atomicMin(err_dup, (unsigned long long)t);
+}
+
+// pool[t] = layout(vals[idx[t]]) ; one 32x32 block per 256 threads, 4 elements each
+template <class T>
+__global__ void k_fill_pool(const T* __restrict__ vals, const int32_t* __restrict__ idx,
+                            int64_t nb, T* __restrict__ pool) {
+  for (int64_t t = blockIdx.x; t < nb; t += gridDim.x) {
+    const T* src = vals + (int64_t)idx[t] * 1024;
+    T* dst = pool + t * 1024;
+#pragma unroll
+    for (int e = threadIdx.x; e < 1024; e += 256) {
+      int r = e >> 5, c = e & 31;
+      T v = src[e];
+      if (sizeof(T) == 8) dst[swz64(r, c)] = v;
+      else dst[e] = v;
+    }
+  }
+}
+
+__global__ void k_parent_flags(const uint64_t* __restrict__ key, int64_t n,
+                               int32_t* __restrict__ flag) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    flag[t] = (t == 0 || (key[t] >> 2) != (key[t - 1] >> 2)) ? 1 : 0;
+}
+
+__global__ void k_link(const uint64_t* __restrict__ key, const int32_t* __restrict__ incl,
+                       int64_t n, const int32_t* __restrict__ ids, int32_t* __restrict__ child,
+                       uint64_t* __restrict__ pkey) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int32_t p = incl[t] - 1;
+    uint64_t k = key[t];
+    child[(int64_t)p * 4 + (int)(k & 3)] = ids ? ids[t] : (int32_t)t;
+    if (t == 0 || (k >> 2) != (key[t - 1] >> 2)) pkey[p] = k >> 2;
+  }
+}
+
+__global__ void k_rowmajor_keys(const uint64_t* __restrict__ key, int64_t n,
+                                uint64_t* __restrict__ rm, int32_t* __restrict__ iota) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = key[t];
+    rm[t] = ((uint64_t)morton_row(k) << 32) | morton_col(k);
+    iota[t] = (int32_t)t;
+  }
+}
+
+template <class T>
+__global__ void k_unpack(const T* __restrict__ pool, const uint64_t* __restrict__ key,
+                         const int32_t* __restrict__ order, int64_t nb,
+                         int32_t* __restrict__ brow, int32_t* __restrict__ bcol,
+                         T* __restrict__ out) {
+  for (int64_t t = blockIdx.x; t < nb; t += gridDim.x) {
+    int32_t s = order[t];
+    if (threadIdx.x == 0) {
+      uint64_t k = key[s];
+      if (brow) brow[t] = (int32_t)morton_row(k);
+      if (bcol) bcol[t] = (int32_t)morton_col(k);
+    }
+    if (!out) continue;
+    const T* src = pool + (int64_t)s * 1024;
+    T* dst = out + t * 1024;
+#pragma unroll
+    for (int e = threadIdx.x; e < 1024; e += 256) {
+      int r = e >> 5, c = e & 31;
+      dst[e] = (sizeof(T) == 8) ? src[swz64(r, c)] : src[e];
+    }
+  }
+}
+
+template <class T>
+__global__ void k_block_norm2(const T* __restrict__ pool, int64_t nb, double* __restrict__ out) {
+  // one warp per block, fixed reduction order
+  int lane = threadIdx.x & 31;
+  int64_t w = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  for (; w < nb; w += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    const T* b = pool + w * 1024;
+    double s = 0.0;
+    for (int e = lane; e < 1024; e += 32) {
+      double v = (double)b[e];
+      s += v * v;
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[w] = s;
+  }
+}
+
+__global__ void k_gather_f64(const double* __restrict__ in, const int32_t* __restrict__ order,
+                             int64_t n, double* __restrict__ out, uint64_t* __restrict__ bits) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double v = in[order[t]];
+    if (out) out[t] = v;
+    if (bits) bits[t] = (uint64_t)__double_as_longlong(v);  // v >= 0: bit order = value order
+  }
+}
+
+__global__ void k_mark_keep(const double* __restrict__ prefix, const int32_t* __restrict__ order,
+                            int64_t n, double tau2, uint8_t* __restrict__ keep) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    keep[order[t]] = prefix[t] < tau2 ? 0 : 1;
+}
+
+__global__ void k_compact_blocks(const uint8_t* __restrict__ keep, const int32_t* __restrict__ incl,
+                                 const uint64_t* __restrict__ key, const uint4* __restrict__ pool,
+                                 int64_t n, int64_t vec_per_block, uint64_t* __restrict__ okey,
+                                 uint4* __restrict__ opool) {
+  for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+    if (!keep[t]) continue;
+    int64_t d = incl[t] - 1;
+    if (threadIdx.x == 0) okey[d] = key[t];
+    for (int64_t e = threadIdx.x; e < vec_per_block; e += blockDim.x)
+      opool[d * vec_per_block + e] = pool[t * vec_per_block + e];
+  }
+}
+
+__global__ void k_u8_to_i32(const uint8_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = in[t];
+}
+
+template <class T>
+void cub_sort_pairs(qt_ctx ctx, const uint64_t* kin, uint64_t* kout, const T* vin, T* vout,
+                    int64_t n, int end_bit) {
+  size_t tb = 0;
+  QT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, (int)n, 0, end_bit,
+                                          ctx->stream));
+  void* tmp = scratch(ctx, tb);
+  QT_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, vout, (int)n, 0, end_bit,
+                                          ctx->stream));
+  ctx->launches += 4;
+}
+
+template <class T>
+void cub_incl_sum(qt_ctx ctx, const T* in, T* out, int64_t n) {
+  size_t tb = 0;
+  QT_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out, (int)n, ctx->stream));
+  void* tmp = scratch(ctx, tb);
+  QT_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, in, out, (int)n, ctx->stream));
+  ctx->launches += 2;
+}
+
+template <class T>
+T read_scalar(qt_ctx ctx, const T* d) {
+  T h;
+  QT_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+  QT_CUDA(cudaStreamSynchronize(ctx->stream));
+  return h;
+}
+
+}  // namespace
+
+void* scratch(qt_ctx ctx, size_t bytes) {
+  if (ctx->scratch.bytes < bytes) {
+    size_t want = bytes + bytes / 2 + 4096;
+    ctx->scratch.alloc(want, ctx->stream);
+  }
+  return ctx->scratch.p;
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void build_levels(qt_mat M, const int32_t* leaf_ids) {
+  qt_ctx ctx = M->ctx;
+  cudaStream_t st = ctx->stream;
+  M->cnt.assign(M->L + 1, 0);
+  M->child.clear();
+  M->child.resize(M->L);
+  M->cnt[M->L] = M->nb;
+  if (M->nb == 0) return;
+  DevBuf cur_keys(M->nb * 8, st);
+  QT_CUDA(cudaMemcpyAsync(cur_keys.p, M->key.p, M->nb * 8, cudaMemcpyDeviceToDevice, st));
+  for (int l = M->L - 1; l >= 0; --l) {
+    int64_t n = M->cnt[l + 1];
+    DevBuf flag(n * 4, st), incl(n * 4, st);
+    k_parent_flags<<<grid_for(n), kThreads, 0, st>>>(cur_keys.as<uint64_t>(), n, flag.as<int32_t>());
+    QT_LAUNCH_CHECK(ctx);
+    cub_incl_sum(ctx, flag.as<int32_t>(), incl.as<int32_t>(), n);
+    int32_t np = read_scalar(ctx, incl.as<int32_t>() + (n - 1));
+    M->cnt[l] = np;
+    M->child[l].alloc((size_t)np * 16, st);
+    QT_CUDA(cudaMemsetAsync(M->child[l].p, 0xff, (size_t)np * 16, st));
+    DevBuf pkey((size_t)np * 8, st);
+    k_link<<<grid_for(n), kThreads, 0, st>>>(cur_keys.as<uint64_t>(), incl.as<int32_t>(), n,
+                                             l == M->L - 1 ? leaf_ids : nullptr,
+                                             M->child[l].as<int32_t>(), pkey.as<uint64_t>());
+    QT_LAUNCH_CHECK(ctx);
+    cur_keys = std::move(pkey);
+  }
+}
+
+void build_from_blocks(qt_mat M, int64_t nb, const int32_t* d_brow, const int32_t* d_bcol,
+                       const void* d_vals, int32_t row_lo, int32_t row_hi) {
+  qt_ctx ctx = M->ctx;
+  cudaStream_t st = ctx->stream;
+  M->nb = nb;
+  if (nb == 0) {
+    build_levels(M);
+    return;
+  }
+  DevBuf key0(nb * 8, st), idx0(nb * 4, st), idx1(nb * 4, st);
+  M->key.alloc(nb * 8, st);
+  unsigned long long* err = ctx->counters.as<unsigned long long>();
+  QT_CUDA(cudaMemsetAsync(err, 0xff, 16, st));
+  k_keys<<<grid_for(nb), kThreads, 0, st>>>(d_brow, d_bcol, nb, M->nbr, row_lo, row_hi,
+                                            key0.as<uint64_t>(), idx0.as<int32_t>(), err);
+  QT_LAUNCH_CHECK(ctx);
+  cub_sort_pairs(ctx, key0.as<uint64_t>(), M->key.as<uint64_t>(), idx0.as<int32_t>(),
+                 idx1.as<int32_t>(), nb, 2 * M->L);
+  k_dup<<<grid_for(nb), kThreads, 0, st>>>(M->key.as<uint64_t>(), nb, err + 1);
+  QT_LAUNCH_CHECK(ctx);
+  unsigned long long e[2];
+  QT_CUDA(cudaMemcpyAsync(e, err, 16, cudaMemcpyDeviceToHost, st));
+  QT_CUDA(cudaStreamSynchronize(st));
+  if (e[0] != ~0ull) {
+    int32_t r, c;
+    QT_CUDA(cudaMemcpy(&r, d_brow + e[0], 4, cudaMemcpyDeviceToHost));
+    QT_CUDA(cudaMemcpy(&c, d_bcol + e[0], 4, cudaMemcpyDeviceToHost));
+    fail(QT_ERANGE, "block %llu at (brow=%d, bcol=%d) is outside the block grid [0,%d) or this "
+         "rank's block rows [%d,%d)", e[0], r, c, M->nbr, row_lo, row_hi);
+  }
+  if (e[1] != ~0ull) {
+    uint64_t k;
+    QT_CUDA(cudaMemcpy(&k, M->key.as<uint64_t>() + e[1], 8, cudaMemcpyDeviceToHost));
+    fail(QT_EDUP, "block (brow=%u, bcol=%u) is listed twice", morton_row(k), morton_col(k));
+  }
+  size_t es = elem_size(M->dtype);
+  M->pool.alloc(nb * 1024 * es, st);
+  unsigned g = (unsigned)std::min<int64_t>(nb, 148 * 16);
+  if (M->dtype == QT_F64)
+    k_fill_pool<double><<<g, 256, 0, st>>>((const double*)d_vals, idx1.as<int32_t>(), nb,
+                                           M->pool.as<double>());
+  else
+    k_fill_pool<float><<<g, 256, 0, st>>>((const float*)d_vals, idx1.as<int32_t>(), nb,
+                                          M->pool.as<float>());
+  QT_LAUNCH_CHECK(ctx);
+  build_levels(M);
+}
+
+void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals) {
+  qt_ctx ctx = M->ctx;
+  cudaStream_t st = ctx->stream;
+  int64_t nb = M->nb;
+  if (nb == 0) return;
+  size_t es = elem_size(M->dtype);
+  DevBuf rm(nb * 8, st), rm2(nb * 8, st), iota(nb * 4, st), order(nb * 4, st);
+  k_rowmajor_keys<<<grid_for(nb), kThreads, 0, st>>>(M->key.as<uint64_t>(), nb, rm.as<uint64_t>(),
+                                                     iota.as<int32_t>());
+  QT_LAUNCH_CHECK(ctx);
+  int bits = 32 + 32 - __builtin_clz((unsigned)std::max(M->nbr, 2));
+  cub_sort_pairs(ctx, rm.as<uint64_t>(), rm2.as<uint64_t>(), iota.as<int32_t>(),
+                 order.as<int32_t>(), nb, std::min(64, bits));
+  bool dr = brow && is_device_ptr(brow), dc = bcol && is_device_ptr(bcol),
+       dv = vals && is_device_ptr(vals);
+  DevBuf sr, sc, sv;
+  int32_t* obr = brow ? (dr ? brow : (sr.alloc(nb * 4, st), sr.as<int32_t>())) : nullptr;
+  int32_t* obc = bcol ? (dc ? bcol : (sc.alloc(nb * 4, st), sc.as<int32_t>())) : nullptr;
+  void* ov = vals ? (dv ? vals : (sv.alloc(nb * 1024 * es, st), sv.p)) : nullptr;
+  unsigned g = (unsigned)std::min<int64_t>(nb, 148 * 16);
+  if (M->dtype == QT_F64)
+    k_unpack<double><<<g, 256, 0, st>>>(M->pool.as<double>(), M->key.as<uint64_t>(),
+                                        order.as<int32_t>(), nb, obr, obc, (double*)ov);
+  else
+    k_unpack<float><<<g, 256, 0, st>>>(M->pool.as<float>(), M->key.as<uint64_t>(),
+                                       order.as<int32_t>(), nb, obr, obc, (float*)ov);
+  QT_LAUNCH_CHECK(ctx);
+  if (brow && !dr) QT_CUDA(cudaMemcpyAsync(brow, obr, nb * 4, cudaMemcpyDeviceToHost, st));
+  if (bcol && !dc) QT_CUDA(cudaMemcpyAsync(bcol, obc, nb * 4, cudaMemcpyDeviceToHost, st));
+  if (vals && !dv) QT_CUDA(cudaMemcpyAsync(vals, ov, nb * 1024 * es, cudaMemcpyDeviceToHost, st));
+  QT_CUDA(cudaStreamSynchronize(st));
+}
+
+static qt_mat clone_params(qt_mat A) {
+  qt_mat M = new qt_mat_s();
+  M->ctx = A->ctx;
+  M->n = A->n;
+  M->leaf_dim = A->leaf_dim;
+  M->bs = A->bs;
+  M->dtype = A->dtype;
+  M->L = A->L;
+  M->leaf_level = A->leaf_level;
+  M->nbr = A->nbr;
+  M->row_lo = A->row_lo;
+  M->row_hi = A->row_hi;
+  M->bounds = A->bounds;
+  return M;
+}
+
+qt_mat select_blocks(qt_mat A, const uint8_t* d_keep) {
+  qt_ctx ctx = A->ctx;
+  cudaStream_t st = ctx->stream;
+  qt_mat M = clone_params(A);
+  try {
+    int64_t n = A->nb;
+    int64_t kept = 0;
+    DevBuf k32, incl;
+    if (n > 0) {
+      k32.alloc(n * 4, st);
+      incl.alloc(n * 4, st);
+      k_u8_to_i32<<<grid_for(n), kThreads, 0, st>>>(d_keep, n, k32.as<int32_t>());
+      QT_LAUNCH_CHECK(ctx);
+      cub_incl_sum(ctx, k32.as<int32_t>(), incl.as<int32_t>(), n);
+      kept = read_scalar(ctx, incl.as<int32_t>() + (n - 1));
+    }
+    M->nb = kept;
+    if (kept > 0) {
+      size_t es = elem_size(A->dtype);
+      M->key.alloc(kept * 8, st);
+      M->pool.alloc(kept * 1024 * es, st);
+      int64_t vpb = 1024 * es / 16;
+      unsigned g = (unsigned)std::min<int64_t>(n, 148 * 16);
+      k_compact_blocks<<<g, 256, 0, st>>>(d_keep, incl.as<int32_t>(), A->key.as<uint64_t>(),
+                                          A->pool.as<uint4>(), n, vpb, M->key.as<uint64_t>(),
+                                          M->pool.as<uint4>());
+      QT_LAUNCH_CHECK(ctx);
+    }
+    build_levels(M);
+  } catch (...) {
+    delete M;
+    throw;
+  }
+  return M;
+}
+
+qt_mat truncate(qt_mat A, double tau) {
+  qt_ctx ctx = A->ctx;
+  cudaStream_t st = ctx->stream;
+  int64_t n = A->nb;
+  DevBuf keep(std::max<int64_t>(n, 1), st);
+  if (n > 0) {
+    DevBuf nrm(n * 8, st), rm(n * 8, st), rm2(n * 8, st), iota(n * 4, st), ord1(n * 4, st),
+        bits(n * 8, st), bits2(n * 8, st), ord2(n * 4, st), g(n * 8, st), pre(n * 8, st);
+    int wpb = 8;
+    unsigned gr = (unsigned)std::min<int64_t>((n + wpb - 1) / wpb, 148 * 32);
+    if (A->dtype == QT_F64)
+      k_block_norm2<double><<<gr, 32 * wpb, 0, st>>>(A->pool.as<double>(), n, nrm.as<double>());
+    else
+      k_block_norm2<float><<<gr, 32 * wpb, 0, st>>>(A->pool.as<float>(), n, nrm.as<double>());
+    QT_LAUNCH_CHECK(ctx);
+    // ties broken by (brow, bcol): stable sort by row-major key, then by norm
+    k_rowmajor_keys<<<grid_for(n), kThreads, 0, st>>>(A->key.as<uint64_t>(), n, rm.as<uint64_t>(),
+                                                      iota.as<int32_t>());
+    QT_LAUNCH_CHECK(ctx);
+    cub_sort_pairs(ctx, rm.as<uint64_t>(), rm2.as<uint64_t>(), iota.as<int32_t>(),
+                   ord1.as<int32_t>(), n, 64);
+    k_gather_f64<<<grid_for(n), kThreads, 0, st>>>(nrm.as<double>(), ord1.as<int32_t>(), n, nullptr,
+                                                   bits.as<uint64_t>());
+    QT_LAUNCH_CHECK(ctx);
+    cub_sort_pairs(ctx, bits.as<uint64_t>(), bits2.as<uint64_t>(), ord1.as<int32_t>(),
+                   ord2.as<int32_t>(), n, 64);
+    k_gather_f64<<<grid_for(n), kThreads, 0, st>>>(nrm.as<double>(), ord2.as<int32_t>(), n,
+                                                   g.as<double>(), nullptr);
+    QT_LAUNCH_CHECK(ctx);
+    cub_incl_sum(ctx, g.as<double>(), pre.as<double>(), n);
+    k_mark_keep<<<grid_for(n), kThreads, 0, st>>>(pre.as<double>(), ord2.as<int32_t>(), n,
+                                                  tau * tau, keep.as<uint8_t>());
+    QT_LAUNCH_CHECK(ctx);
+  }
+  return select_blocks(A, keep.as<uint8_t>());
+}
+
+}  // namespace qt

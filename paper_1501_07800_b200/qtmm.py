@@ -1,0 +1,272 @@
+"""Python binding of libqtmm (include/qt.h): argument marshalling only.
+
+Every step of the multiply runs in the CUDA kernels of libqtmm.so; this module
+turns numpy arrays / torch tensors into pointers, calls the C ABI and wraps the
+handles.  There is no fallback: if libqtmm.so is missing or fails to load, the
+import raises.  PyTorch is used only for streams and torch.distributed (the
+NCCL unique id broadcast).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libqtmm.so")
+
+QT_F64, QT_F32 = 0, 1
+STATUS = {0: "QT_OK", 1: "QT_EINVAL", 2: "QT_ERANGE", 3: "QT_EDUP", 4: "QT_EDIM", 5: "QT_EBS",
+          6: "QT_EDTYPE", 7: "QT_ENOMEM", 8: "QT_ECUDA", 9: "QT_ENCCL", 10: "QT_ESTATE"}
+MAX_LEVELS = 40
+
+
+class QtError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("nlevels", ctypes.c_int32),
+        ("leaf_level", ctypes.c_int32),
+        ("level_tasks", ctypes.c_int64 * MAX_LEVELS),
+        ("level_c_nodes", ctypes.c_int64 * MAX_LEVELS),
+        ("block_products", ctypes.c_int64),
+        ("c_blocks", ctypes.c_int64),
+        ("bytes_recv_payload", ctypes.c_int64),
+        ("bytes_recv_meta", ctypes.c_int64),
+        ("bytes_sent_payload", ctypes.c_int64),
+        ("bytes_sent_meta", ctypes.c_int64),
+        ("blocks_recv", ctypes.c_int64),
+        ("ms_exchange", ctypes.c_float),
+        ("ms_symbolic", ctypes.c_float),
+        ("ms_numeric", ctypes.c_float),
+        ("ms_total", ctypes.c_float),
+    ]
+
+    def as_dict(self) -> dict:
+        n = self.nlevels
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f not in ("level_tasks", "level_c_nodes")}
+        d["level_tasks"] = list(self.level_tasks[:n])
+        d["level_c_nodes"] = list(self.level_c_nodes[:n])
+        return d
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_1501_07800_b200.build`")
+    lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    P, i32, i64, st = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int
+    sig = {
+        "qt_ctx_create": [ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P, P],
+        "qt_ctx_destroy": [P],
+        "qt_nccl_unique_id": [P],
+        "qt_create": [P, i64, i32, i32, ctypes.c_int, i64, P, P, P, P, P],
+        "qt_multiply": [P, P, P, P],
+        "qt_multiply_virtual": [P, P, i32, i32, P, P, P],
+        "qt_truncate": [P, ctypes.c_double, P],
+        "qt_info": [P, P, P, P, P, P, P, P, P],
+        "qt_level_nodes": [P, P, i32, P],
+        "qt_read_back": [P, P, P, P],
+        "qt_destroy": [P],
+        "qt_fp64_peak": [P, ctypes.c_int, ctypes.c_float, P],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = st
+    lib.qt_last_error.restype = ctypes.c_char_p
+    lib.qt_last_error.argtypes = []
+    lib.qt_kernel_launches.restype = i64
+    lib.qt_kernel_launches.argtypes = [P]
+    return lib
+
+
+_lib = _load()
+EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_nccl_unique_id", "qt_create", "qt_multiply",
+            "qt_multiply_virtual", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
+            "qt_destroy", "qt_last_error", "qt_kernel_launches", "qt_fp64_peak")
+
+
+def _check(status: int):
+    if status != 0:
+        raise QtError(status, _lib.qt_last_error().decode(errors="replace"))
+
+
+def _ptr(x):
+    """Pointer of a numpy array or torch tensor (must be contiguous)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return ctypes.c_void_p(x.ctypes.data)
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return ctypes.c_void_p(x.data_ptr())
+    raise TypeError(f"unsupported buffer {type(x)}")
+
+
+def _dtype_code(vals) -> int:
+    dt = str(vals.dtype)
+    if dt in ("float64", "torch.float64"):
+        return QT_F64
+    if dt in ("float32", "torch.float32"):
+        return QT_F32
+    raise TypeError(f"values must be float64 or float32, got {dt}")
+
+
+class Context:
+    """One per process (rank): device, stream and (world > 1) NCCL communicator."""
+
+    def __init__(self, device: int = 0, stream=None, process_group=None):
+        import torch
+        self.device = device
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        sptr = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+        rank, world = 0, 1
+        uid = None
+        if process_group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()):
+            import torch.distributed as dist
+            world = dist.get_world_size(process_group)
+            rank = dist.get_rank(process_group)
+            if world > 1:
+                buf = ctypes.create_string_buffer(128)
+                if rank == 0:
+                    _check(_lib.qt_nccl_unique_id(buf))
+                obj = [bytes(buf.raw)]
+                src = dist.get_global_rank(process_group, 0) if process_group is not None else 0
+                dist.broadcast_object_list(obj, src=src, group=process_group)
+                uid = ctypes.create_string_buffer(obj[0], 128)
+        self.rank, self.world = rank, world
+        h = ctypes.c_void_p()
+        _check(_lib.qt_ctx_create(device, sptr, rank, world, uid, ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(_lib.qt_kernel_launches(self._h))
+
+    def fp64_peak(self, kind: str = "dmma", ms: float = 50.0) -> float:
+        out = ctypes.c_double()
+        _check(_lib.qt_fp64_peak(self._h, 0 if kind == "dmma" else 1, ms, ctypes.byref(out)))
+        return out.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _check(_lib.qt_ctx_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Matrix:
+    """Immutable quadtree matrix handle (the rank-local part when world > 1)."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx = ctx
+        self._h = handle
+
+    @classmethod
+    def from_blocks(cls, ctx: Context, n: int, leaf_dim: int, bs: int, brow, bcol, vals,
+                    row_bounds=None) -> "Matrix":
+        nb = int(brow.shape[0])
+        if nb:
+            if isinstance(brow, np.ndarray):
+                brow = np.ascontiguousarray(brow, dtype=np.int32)
+                bcol = np.ascontiguousarray(bcol, dtype=np.int32)
+            if isinstance(vals, np.ndarray):
+                vals = np.ascontiguousarray(vals)
+            if tuple(vals.shape[-2:]) != (bs, bs) or int(vals.shape[0]) != nb:
+                raise ValueError("vals must have shape [nblocks, bs, bs]")
+        code = _dtype_code(vals) if nb or hasattr(vals, "dtype") else QT_F64
+        rb = None
+        if row_bounds is not None:
+            rb = np.ascontiguousarray(np.asarray(row_bounds, dtype=np.int32))
+        h = ctypes.c_void_p()
+        _check(_lib.qt_create(ctx.handle, n, leaf_dim, bs, code, nb, _ptr(brow) if nb else None,
+                              _ptr(bcol) if nb else None, _ptr(vals) if nb else None,
+                              _ptr(rb), ctypes.byref(h)))
+        return cls(ctx, h)
+
+    def multiply(self, other: "Matrix"):
+        st = Stats()
+        h = ctypes.c_void_p()
+        _check(_lib.qt_multiply(self._h, other._h, ctypes.byref(h), ctypes.byref(st)))
+        return Matrix(self.ctx, h), st
+
+    def __matmul__(self, other: "Matrix") -> "Matrix":
+        return self.multiply(other)[0]
+
+    def multiply_virtual(self, other: "Matrix", P: int, g: int, row_bounds):
+        st = Stats()
+        h = ctypes.c_void_p()
+        rb = np.ascontiguousarray(np.asarray(row_bounds, dtype=np.int32))
+        _check(_lib.qt_multiply_virtual(self._h, other._h, P, g, _ptr(rb), ctypes.byref(h),
+                                        ctypes.byref(st)))
+        return Matrix(self.ctx, h), st
+
+    def truncate(self, tau: float) -> "Matrix":
+        h = ctypes.c_void_p()
+        _check(_lib.qt_truncate(self._h, float(tau), ctypes.byref(h)))
+        return Matrix(self.ctx, h)
+
+    def info(self) -> dict:
+        n, nl, nglob = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        leaf, bs, lo, hi = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        dt = ctypes.c_int()
+        _check(_lib.qt_info(self._h, ctypes.byref(n), ctypes.byref(leaf), ctypes.byref(bs),
+                            ctypes.byref(dt), ctypes.byref(nl), ctypes.byref(nglob),
+                            ctypes.byref(lo), ctypes.byref(hi)))
+        return {"n": n.value, "leaf_dim": leaf.value, "bs": bs.value,
+                "dtype": "f64" if dt.value == QT_F64 else "f32", "local_nblocks": nl.value,
+                "global_nblocks": nglob.value, "row_lo": lo.value, "row_hi": hi.value}
+
+    @property
+    def nblocks(self) -> int:
+        return self.info()["local_nblocks"]
+
+    def level_nodes(self):
+        buf = (ctypes.c_int64 * MAX_LEVELS)()
+        nl = ctypes.c_int32()
+        _check(_lib.qt_level_nodes(self._h, buf, MAX_LEVELS, ctypes.byref(nl)))
+        return list(buf[: nl.value])
+
+    def to_blocks(self, out=None):
+        """(brow, bcol, vals) sorted by (brow, bcol).  Default: new numpy arrays.
+        ``out=(brow, bcol, vals)`` writes into caller buffers (numpy or torch,
+        host or device)."""
+        inf = self.info()
+        nb, bs = inf["local_nblocks"], inf["bs"]
+        if out is None:
+            dt = np.float64 if inf["dtype"] == "f64" else np.float32
+            out = (np.empty(nb, np.int32), np.empty(nb, np.int32), np.empty((nb, bs, bs), dt))
+        if nb:
+            _check(_lib.qt_read_back(self._h, _ptr(out[0]), _ptr(out[1]), _ptr(out[2])))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _check(_lib.qt_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

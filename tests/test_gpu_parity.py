@@ -1,0 +1,348 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle.  Needs a B200.
+
+Bars: block patterns and integer-valued results
+bit-exact; uniform[-1,1] FP64 results within relative Frobenius error 1e-12
+and inside the elementwise Higham bound 2*gamma_K*(|A||B|) (pin P-9).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import qtgen
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+REL_FRO_F64 = 1e-12
+
+
+@pytest.fixture(scope="module")
+def qt():
+    from paper_1501_07800_b200 import build
+    build.build()
+    from paper_1501_07800_b200 import qtmm
+    return qtmm
+
+
+@pytest.fixture(scope="module")
+def ctx(qt):
+    import torch
+    torch.cuda.init()
+    return qt.Context(0)
+
+
+def mk(qt, ctx, M: qtgen.BlockMatrix):
+    return qt.Matrix.from_blocks(ctx, M.n, M.leaf_dim, M.bs, M.brow, M.bcol, M.vals)
+
+
+def as_tuple(M: qtgen.BlockMatrix):
+    return (M.brow, M.bcol, M.vals)
+
+
+def assert_same_pattern(got, ref):
+    assert got[0].shape == ref[0].shape, (got[0].shape, ref[0].shape)
+    assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+
+
+def assert_close_f64(got, ref, A, B, nbr, bs, k_terms):
+    assert_same_pattern(got, ref)
+    d = got[2] - ref[2]
+    nr = np.linalg.norm(ref[2])
+    rel = np.linalg.norm(d) / (nr if nr > 0 else 1.0)
+    assert rel <= REL_FRO_F64, rel
+    _, _, bound = oracle.higham_bound(nbr, bs, A, B, k_terms)
+    assert np.all(np.abs(d) <= bound + 1e-300)
+
+
+def random_bm(rng, nbr, bs, p, kind, leaf):
+    mask = rng.random((nbr, nbr)) < p
+    br, bc = np.nonzero(mask)
+    if kind == "int":
+        v = rng.integers(-4, 5, size=(len(br), bs, bs)).astype(np.float64)
+    else:
+        v = rng.uniform(-1, 1, size=(len(br), bs, bs))
+    return qtgen.BlockMatrix(nbr * bs, leaf, bs, br.astype(np.int32), bc.astype(np.int32), v)
+
+
+# ----------------------------------------------------------------- small cases
+
+
+def test_hand_example_embedded(qt, ctx):
+    g = json.load(open(os.path.join(GOLD, "spec_hand_example.json")))
+    a = np.zeros((1, 32, 32))
+    b = np.zeros((1, 32, 32))
+    a[0, :2, :2] = g["A"]
+    b[0, :2, :2] = g["B"]
+    z = np.zeros(1, np.int32)
+    A = qt.Matrix.from_blocks(ctx, 32, 32, 32, z, z, a)
+    B = qt.Matrix.from_blocks(ctx, 32, 32, 32, z, z, b)
+    C, st = A.multiply(B)
+    r, c, v = C.to_blocks()
+    assert list(r) == [0] and list(c) == [0]
+    assert np.array_equal(v[0, :2, :2], np.array(g["C"], float))
+    assert np.all(v[0, 2:, :] == 0) and np.all(v[0, :, 2:] == 0)
+    assert st.block_products == 1
+
+
+def test_create_read_back_roundtrip(qt, ctx):
+    rng = np.random.default_rng(0)
+    M = random_bm(rng, 13, 32, 0.4, "uniform", 128)
+    perm = rng.permutation(M.nb)
+    A = qt.Matrix.from_blocks(ctx, M.n, M.leaf_dim, 32, M.brow[perm], M.bcol[perm], M.vals[perm])
+    r, c, v = A.to_blocks()
+    o = np.lexsort((M.bcol, M.brow))
+    assert np.array_equal(r, M.brow[o]) and np.array_equal(c, M.bcol[o])
+    assert np.array_equal(v, M.vals[o])
+
+
+@pytest.mark.parametrize("nbr,p,leaf", [(1, 1.0, 32), (2, 1.0, 32), (5, 0.5, 64), (16, 0.3, 128),
+                                        (37, 0.2, 256), (64, 0.05, 512), (100, 0.08, 1024)])
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_random_patterns(qt, ctx, nbr, p, leaf, kind):
+    rng = np.random.default_rng(nbr * 7 + (kind == "int"))
+    Am = random_bm(rng, nbr, 32, p, kind, leaf)
+    Bm = random_bm(rng, nbr, 32, p, kind, leaf)
+    C, st = mk(qt, ctx, Am).multiply(mk(qt, ctx, Bm))
+    got = C.to_blocks()
+    ref = oracle.spgemm(nbr, 32, as_tuple(Am), as_tuple(Bm))
+    if kind == "int":
+        assert_same_pattern(got, ref)
+        assert np.array_equal(got[2], ref[2])
+    else:
+        assert_close_f64(got, ref, as_tuple(Am), as_tuple(Bm), nbr, 32, nbr * 32)
+    L, _ = oracle.tree_levels(Am.n, 32, leaf)
+    assert st.nlevels == L + 1
+    assert list(st.level_tasks[: L + 1]) == oracle.level_task_counts(
+        L, (Am.brow, Am.bcol), (Bm.brow, Bm.bcol))
+    assert st.c_blocks == len(ref[0])
+    # C's quadtree = the tree spanned by its blocks
+    assert C.level_nodes() == oracle.level_node_counts(L, (ref[0], ref[1]))
+
+
+def test_identity_both_sides(qt, ctx):
+    rng = np.random.default_rng(3)
+    Am = random_bm(rng, 24, 32, 0.3, "uniform", 256)
+    eye = qtgen.BlockMatrix(Am.n, 256, 32, np.arange(24, dtype=np.int32), np.arange(24, dtype=np.int32),
+                            np.repeat(np.eye(32)[None], 24, axis=0))
+    A, I = mk(qt, ctx, Am), mk(qt, ctx, eye)
+    o = np.lexsort((Am.bcol, Am.brow))
+    for X, Y in [(A, I), (I, A)]:
+        r, c, v = (X @ Y).to_blocks()
+        assert np.array_equal(r, Am.brow[o]) and np.array_equal(c, Am.bcol[o])
+        assert np.array_equal(v, Am.vals[o])
+
+
+@pytest.mark.parametrize("n,d", [(2048, 128), (4096, 100)])
+def test_banded_all_ones_closed_form(qt, ctx, n, d):
+    bs = 32
+    nbr = n // bs
+    br, bc = qtgen.pattern_banded(nbr, qtgen.band_blocks(d, bs))
+    v = qtgen.block_values(br, bc, bs, 0, "ones", band_d=d)
+    A = qt.Matrix.from_blocks(ctx, n, 512, bs, br, bc, v)
+    r, c, w = (A @ A).to_blocks()
+    D = qtgen.band_blocks(d, bs)
+    assert np.all(np.abs(r - c) <= 2 * D)
+    i = r[:, None, None].astype(np.int64) * bs + np.arange(bs)[None, :, None]
+    j = c[:, None, None].astype(np.int64) * bs + np.arange(bs)[None, None, :]
+    lo = np.maximum(np.maximum(i, j) - d, 0)
+    hi = np.minimum(np.minimum(i, j) + d, n - 1)
+    ref = np.where(np.abs(i - j) <= 2 * d, np.maximum(hi - lo + 1, 0), 0)
+    assert np.array_equal(w, ref.astype(float))
+
+
+def test_empty_operands(qt, ctx):
+    z = np.zeros(0, np.int32)
+    E = qt.Matrix.from_blocks(ctx, 256, 64, 32, z, z, np.zeros((0, 32, 32)))
+    rng = np.random.default_rng(1)
+    Am = random_bm(rng, 8, 32, 0.5, "int", 64)
+    A = mk(qt, ctx, Am)
+    for X, Y in [(E, A), (A, E), (E, E)]:
+        C, st = X.multiply(Y)
+        assert C.nblocks == 0 and st.block_products == 0
+        r, c, v = C.to_blocks()
+        assert r.shape[0] == 0
+
+
+def test_disjoint_k_gives_empty(qt, ctx):
+    # A has only block column 0, B only block row 1: every product is NIL
+    A = qt.Matrix.from_blocks(ctx, 64, 32, 32, np.array([0, 1], np.int32), np.array([0, 0], np.int32),
+                              np.ones((2, 32, 32)))
+    B = qt.Matrix.from_blocks(ctx, 64, 32, 32, np.array([1], np.int32), np.array([1], np.int32),
+                              np.ones((1, 32, 32)))
+    C, st = A.multiply(B)
+    assert C.nblocks == 0 and st.block_products == 0
+    assert C.level_nodes() == [0, 0]
+
+
+def test_errors(qt, ctx):
+    one = np.ones((1, 32, 32))
+    with pytest.raises(qt.QtError) as e:
+        qt.Matrix.from_blocks(ctx, 64, 32, 32, np.array([2], np.int32), np.array([0], np.int32), one)
+    assert e.value.name == "QT_ERANGE" and "brow=2" in str(e.value)
+    with pytest.raises(qt.QtError) as e:
+        qt.Matrix.from_blocks(ctx, 64, 32, 32, np.array([1, 1], np.int32), np.array([0, 0], np.int32),
+                              np.ones((2, 32, 32)))
+    assert e.value.name == "QT_EDUP" and "brow=1, bcol=0" in str(e.value)
+    with pytest.raises(qt.QtError) as e:
+        qt.Matrix.from_blocks(ctx, 48, 32, 32, np.array([0], np.int32), np.array([0], np.int32), one)
+    assert e.value.name == "QT_EINVAL"
+    with pytest.raises(qt.QtError) as e:
+        qt.Matrix.from_blocks(ctx, 64, 96, 32, np.array([0], np.int32), np.array([0], np.int32), one)
+    assert e.value.name == "QT_EINVAL"
+    z = np.array([0], np.int32)
+    A = qt.Matrix.from_blocks(ctx, 64, 32, 32, z, z, one)
+    B = qt.Matrix.from_blocks(ctx, 128, 32, 32, z, z, one)
+    with pytest.raises(qt.QtError) as e:
+        A @ B
+    assert e.value.name == "QT_EDIM"
+    B = qt.Matrix.from_blocks(ctx, 64, 64, 32, z, z, one)
+    with pytest.raises(qt.QtError) as e:
+        A @ B
+    assert e.value.name == "QT_EBS"
+    B = qt.Matrix.from_blocks(ctx, 64, 32, 32, z, z, one.astype(np.float32))
+    with pytest.raises(qt.QtError) as e:
+        A @ B
+    assert e.value.name == "QT_EDTYPE"
+
+
+def test_run_to_run_bitwise(qt, ctx):
+    c = qtgen.config(2, small=True)
+    A = mk(qt, ctx, c["A"])
+    v0 = (A @ A).to_blocks()[2]
+    for _ in range(3):
+        assert np.array_equal((A @ A).to_blocks()[2], v0)
+
+
+def test_leaf_dim_invariance(qt, ctx):
+    c = qtgen.config(2, small=True)
+    M = c["A"]
+    outs = []
+    for leaf in (32, 256, 2048):
+        A = qt.Matrix.from_blocks(ctx, M.n, leaf, 32, M.brow, M.bcol, M.vals)
+        outs.append((A @ A).to_blocks())
+    for o in outs[1:]:
+        assert_same_pattern(o, outs[0])
+        assert np.array_equal(o[2], outs[0][2])
+
+
+# ----------------------------------------------------------------- configs
+
+
+def test_cfg1_dense_int_bitexact_and_uniform(qt, ctx):
+    for kind in ("int", "uniform"):
+        c = qtgen.config(1, kind)
+        A, B = mk(qt, ctx, c["A"]), mk(qt, ctx, c["B"])
+        C, st = A.multiply(B)
+        got = C.to_blocks()
+        ref = oracle.spgemm(16, 32, as_tuple(c["A"]), as_tuple(c["B"]))
+        assert st.block_products == 4096
+        assert list(st.level_tasks[:5]) == [1, 8, 64, 512, 4096]
+        if kind == "int":
+            assert_same_pattern(got, ref)
+            assert np.array_equal(got[2], ref[2])
+        else:
+            assert_close_f64(got, ref, as_tuple(c["A"]), as_tuple(c["B"]), 16, 32, 512)
+
+
+def _sampled_rows_check(qt, ctx, c, rows, kind):
+    Am, Bm = c["A"], c["B"]
+    A = mk(qt, ctx, Am)
+    B = A if c["same"] else mk(qt, ctx, Bm)
+    C, st = A.multiply(B)
+    nbr = Am.nbr
+    L, _ = oracle.tree_levels(Am.n, 32, Am.leaf_dim)
+    assert list(st.level_tasks[: L + 1]) == oracle.level_task_counts(
+        L, (Am.brow, Am.bcol), (Bm.brow, Bm.bcol))
+    got = C.to_blocks()
+    pr, pc = oracle.pattern_product(nbr, (Am.brow, Am.bcol), (Bm.brow, Bm.bcol))
+    assert_same_pattern(got, (pr, pc))
+    sel = np.zeros(len(got[0]), bool)
+    for lo, hi in rows:
+        sel |= (got[0] >= lo) & (got[0] < hi)
+        ref = oracle.spgemm(nbr, 32, as_tuple(Am), as_tuple(Bm), rows=(lo, hi))
+        m = (got[0] >= lo) & (got[0] < hi)
+        g = (got[0][m], got[1][m], got[2][m])
+        if kind == "int":
+            assert_same_pattern(g, ref)
+            assert np.array_equal(g[2], ref[2])
+        else:
+            assert_same_pattern(g, ref)
+            d = g[2] - ref[2]
+            assert np.linalg.norm(d) <= REL_FRO_F64 * np.linalg.norm(ref[2])
+            _, _, bound = oracle.higham_bound(nbr, 32, as_tuple(Am), as_tuple(Bm), nbr * 32,
+                                              rows=(lo, hi))
+            assert np.all(np.abs(d) <= bound + 1e-300)
+    return st
+
+
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_cfg2_banded_full_size_sampled(qt, ctx, kind):
+    c = qtgen.config(2, kind)
+    st = _sampled_rows_check(qt, ctx, c, [(0, 8), (250, 262), (504, 512)], kind)
+    assert st.block_products == 2048800 and st.c_blocks == 61888
+
+
+def test_cfg3_random_full_size_sampled(qt, ctx):
+    c = qtgen.config(3)
+    _sampled_rows_check(qt, ctx, c, [(0, 16), (1000, 1024)], "uniform")
+
+
+def test_cfg4_eslike_full_size_sampled(qt, ctx):
+    c = qtgen.config(4)
+    _sampled_rows_check(qt, ctx, c, [(0, 4), (1500, 1504), (3068, 3072)], "uniform")
+
+
+def test_cfg4_small_full_oracle(qt, ctx):
+    c = qtgen.config(4, small=True)
+    Am = c["A"]
+    A = mk(qt, ctx, Am)
+    got = (A @ A).to_blocks()
+    ref = oracle.spgemm(Am.nbr, 32, as_tuple(Am), as_tuple(Am))
+    assert_close_f64(got, ref, as_tuple(Am), as_tuple(Am), Am.nbr, 32, Am.nbr * 32)
+
+
+# ----------------------------------------------------------------- virtual ranks (multi-GPU path)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_virtual_ranks_bitwise_and_bytes(qt, ctx, P):
+    c = qtgen.config(5, P=P, small=True)
+    Am = c["A"]
+    A = mk(qt, ctx, Am)
+    full = (A @ A).to_blocks()
+    per = Am.nbr // P
+    bounds = [g * per for g in range(P + 1)]
+    plan = oracle.exchange_plan(bounds, (Am.brow, Am.bcol), (Am.brow, Am.bcol), 8192)
+    for g in range(P):
+        Cg, st = A.multiply_virtual(A, P, g, bounds)
+        r, cc, v = Cg.to_blocks()
+        m = (full[0] >= bounds[g]) & (full[0] < bounds[g + 1])
+        assert np.array_equal(r, full[0][m]) and np.array_equal(cc, full[1][m])
+        assert np.array_equal(v, full[2][m])                  # P-10: bitwise across P
+        assert st.bytes_recv_payload == plan[g]["payload_bytes"]
+        assert st.bytes_recv_meta == plan[g]["meta_bytes"]
+        assert st.blocks_recv == plan[g]["blocks_received"]
+
+
+def test_virtual_single_rank_moves_nothing(qt, ctx):
+    c = qtgen.config(2, small=True)
+    A = mk(qt, ctx, c["A"])
+    C, st = A.multiply_virtual(A, 1, 0, [0, c["A"].nbr])
+    assert st.bytes_recv_payload == 0 and st.bytes_recv_meta == 0
+
+
+# ----------------------------------------------------------------- truncate
+
+
+@pytest.mark.parametrize("tau", [0.0, 0.5, 3.0, 20.0])
+def test_truncate_matches_oracle(qt, ctx, tau):
+    rng = np.random.default_rng(17)
+    Mm = random_bm(rng, 20, 32, 0.4, "uniform", 128)
+    Mm.vals *= rng.uniform(0, 1, size=(Mm.nb, 1, 1)) ** 4
+    A = mk(qt, ctx, Mm)
+    r, c, v = A.truncate(tau).to_blocks()
+    rr, rc, rv = oracle.truncate(Mm.brow, Mm.bcol, Mm.vals, tau)
+    assert np.array_equal(r, rr) and np.array_equal(c, rc) and np.array_equal(v, rv)
