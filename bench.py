@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark: effective FP64 GFLOP/s of C = A*A (block-sparse quadtree multiply)
+at N GPUs, plus bytes received per GPU (BASELINE.json metric).
+
+Workload:
+  N = 1  : BASELINE config 2 — banded N=16384, a_ij != 0 iff |i-j| <= 1024,
+           uniform[-1,1], leaf 1024, block 32, C = A*A (FP64).
+  N > 1  : BASELINE config 5 — weak-scaling banded N = 16384*P, bandwidth 1024,
+           leaf 2048, block 32; rank g generates and owns block rows
+           [512g, 512(g+1)) (counter-based generator: no data moves to set up).
+A step = one qt_multiply (symbolic BFS + [exchange] + numeric kernel) on
+device-resident inputs.  value = total nonzero block products * 2*32^3 /
+max-over-ranks device time.  Inputs (A 264 MB + C 507 MB per GPU) exceed the
+126 MB L2, so no explicit flush is done between steps.
+
+`--impl reference` times the oracle (plain CPU block-CSR multiply, the
+reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import qtgen  # noqa: E402  (seeded inputs only)
+
+BS = 32
+FLOP_PER_PRODUCT = 2 * BS ** 3
+METRIC = "effective FP64 GFLOP/s (nonzero block products)"
+UNIT = "GFLOP/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="qtmm", choices=["qtmm", "reference"])
+    ap.add_argument("--dtype", default="f64", choices=["f64"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(P: int, rank: int):
+    """Inputs of this rank: (config dict, description)."""
+    if P == 1:
+        c = qtgen.config(2)
+        desc = "cfg2 banded C=A*A N=16384 d=1024 (bandwidth 2049) leaf 1024 bs 32 FP64"
+    else:
+        c = qtgen.config(5, P=P, rank=rank)
+        desc = f"cfg5 weak-scaling banded C=A*A N=16384*{P} d=1024 leaf 2048 bs 32 FP64, row strips"
+    return c, desc
+
+
+def aggregate(dist, vals, device, world: int):
+    """All-gather a small float64 vector from every rank -> [world, len] numpy
+    (CUDA tensor under NCCL, CPU tensor under gloo)."""
+    import torch
+    if world == 1:
+        return np.asarray([vals], dtype=np.float64)
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    gl = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(gl, t)
+    return torch.stack(gl).cpu().numpy()
+
+
+def row_bounds(nbr: int, P: int):
+    """Equal block-row strips (config 5: 512 block rows = 16384 rows per GPU)."""
+    per = nbr // P
+    return [g * per for g in range(P)] + [nbr]
+
+
+# ----------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax.append(float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- oracle legs
+
+
+def oracle_sample(c: dict, target_s: float = 12.0, max_rows: int | None = None):
+    """Time the oracle (as it stands) on block rows of the same workload.
+    Returns (GFLOP/s, threads, description, seconds)."""
+    import oracle
+    A = c["A"]
+    nbr = A.nbr
+    Bm = c["B"]
+    # products of block row I = sum over K in row I of A of |row K of B|
+    rowcnt = np.bincount(Bm.brow, minlength=nbr)
+    prod_row = np.bincount(A.brow, weights=rowcnt[A.bcol], minlength=nbr).astype(np.int64)
+    nt = oracle.default_threads()
+    a = (A.brow, A.bcol, A.vals)
+    b = (Bm.brow, Bm.bcol, Bm.vals)
+    lo = int(A.brow.min()) if A.nb else 0
+    mid = lo + (int(A.brow.max()) - lo) // 2 if A.nb else 0
+    rows = max(nt, 4)
+    t0 = time.perf_counter()
+    oracle.spgemm(nbr, BS, a, b, nthreads=nt, rows=(mid, mid + rows))
+    dt = time.perf_counter() - t0
+    rate = prod_row[mid:mid + rows].sum() / max(dt, 1e-9)
+    want = int(target_s * rate)
+    r1 = mid
+    acc = 0
+    while r1 < nbr and acc < want and (max_rows is None or r1 - mid < max_rows):
+        acc += prod_row[r1]
+        r1 += 1
+    r1 = max(r1, mid + 1)
+    t0 = time.perf_counter()
+    oracle.spgemm(nbr, BS, a, b, nthreads=nt, rows=(mid, r1))
+    dt = time.perf_counter() - t0
+    prods = int(prod_row[mid:r1].sum())
+    gf = prods * FLOP_PER_PRODUCT / dt / 1e9
+    return gf, nt, f"block rows [{mid},{r1}) of the workload's C ({prods} block products)", dt
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    P = args.gpus
+    if P == 1:
+        c, desc = workload(1, 0)
+    else:  # rank 0's strip plus its halo rows (the sample stays inside the strip)
+        c = qtgen.config(5, P=P, rows=(0, 512 + 32))
+        desc = f"cfg5 weak-scaling banded N=16384*{P} d=1024 leaf 2048 bs 32 FP64 (rank 0's rows)"
+    per_step_s = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    times, rates = [], []
+    nt = 1
+    sample = ""
+    for i in range(args.warmup + args.steps):
+        gf, nt, sample, dt = oracle_sample(c, target_s=per_step_s)
+        if i >= args.warmup:
+            rates.append(gf)
+            times.append(dt)
+    v = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT, "n_gpus": P,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(times), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (qtgen counter-based generator)",
+        "config": {"workload": desc, "sample": sample},
+        "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": nt, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- product leg
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    P = world
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    from paper_1501_07800_b200 import qtmm
+
+    stream = torch.cuda.Stream(dev)
+    ctx = qtmm.Context(dev, stream=stream)
+    c, desc = workload(P, rank)
+    Am = c["A"]
+    bounds = row_bounds(Am.nbr, P) if P > 1 else None
+    # device-resident inputs
+    A = qtmm.Matrix.from_blocks(ctx, Am.n, Am.leaf_dim, BS, Am.brow, Am.bcol, Am.vals, row_bounds=bounds)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step():
+        C, st = A.multiply(A)
+        C.close()
+        return st
+
+    for _ in range(max(3, args.warmup)):
+        st = step()
+    # FP64 peak for the roofline denominator (MEASURED_PEAKS.json has no FP64 entry)
+    peak_dmma = ctx.fp64_peak("dmma", 200.0)
+    barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(dev)
+    sampler.start()
+    l0 = ctx.kernel_launches
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    stats = []
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        stats.append(step())
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    launches = ctx.kernel_launches - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    products = stats[-1].block_products
+    ms_num = statistics.mean(s.ms_numeric for s in stats)
+    ms_sym = statistics.mean(s.ms_symbolic for s in stats)
+    ms_exch = statistics.mean(s.ms_exchange for s in stats)
+    recv = stats[-1].bytes_recv_payload
+    recv_meta = stats[-1].bytes_recv_meta
+    allv = aggregate(dist, [ms, float(products), float(recv), float(recv_meta), float(launches)],
+                     "cuda", world)
+    ms_max = float(allv[:, 0].max())
+    total_products = float(allv[:, 1].sum())
+    recv_all = allv[:, 2]
+    launches_total = int(allv[:, 4].sum())
+    value = total_products * FLOP_PER_PRODUCT / (ms_max * 1e-3) / 1e9
+    # dominant kernel: the numeric kernel, timed with events on its stream (qt_stats)
+    flops_launch = products * FLOP_PER_PRODUCT
+    achieved = flops_launch / (ms_num * 1e-3) / 1e12
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier)
+    cpu = None
+    if rank == 0 and P == 1 and not args.no_cpu_baseline:
+        gf, nt, sample, _ = oracle_sample(c, target_s=12.0)
+        cpu = {"value": round(gf, 3), "unit": UNIT, "cores": nt, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        m_nnz_row = 2 * 1024 + 1
+        k = 16384
+        spsumma = [2 * m_nnz_row * k * (p ** 0.5) * 8 for p in [P]]
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": P,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_max, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (qtgen counter-based generator, uniform[-1,1])",
+            "config": {"workload": desc, "n": Am.n, "leaf_dim": Am.leaf_dim, "block": BS,
+                       "global_block_products": int(total_products),
+                       "l2": "no flush: inputs larger than L2 (A 264 MB + C 507 MB per GPU > 126 MB)",
+                       "parallelism": f"row strips x{P}" if P > 1 else "single GPU"},
+            "roofline": {"bound": "tensor", "kernel": "k_numeric_f64 (DMMA m8n8k4 f64)",
+                         "achieved": round(achieved, 3), "peak": round(peak_dmma / 1e12, 3),
+                         "unit": "TFLOP/s", "frac": round(achieved / (peak_dmma / 1e12), 4),
+                         "traffic": traffic_from_profiles(P),
+                         "peak_source": "live DMMA microbenchmark in this run (qt_fp64_peak); "
+                                        "MEASURED_PEAKS.json has no FP64 entry; nominal 37.2 TF "
+                                        "= 148 SM x 64 FMA x 2 x 1.965 GHz",
+                         "ms_numeric": round(ms_num, 4), "ms_symbolic": round(ms_sym, 4),
+                         "ms_exchange": round(ms_exch, 4),
+                         "numeric_share": round(ms_num / ms_max, 4)},
+            "bytes_recv_per_gpu": {"max": int(recv_all.max()), "avg": float(recv_all.mean()),
+                                   "min": int(recv_all.min()), "unit": "bytes (FP64 payload)",
+                                   "spsumma_comparator": spsumma[0] if P > 1 else 0},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_total,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def traffic_from_profiles(P: int):
+    """DRAM bytes per launch of the numeric kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("cfg2" if P == 1 else "cfg5")
+    except Exception:
+        return None
+
+
+def measure_e2e(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier):
+    """Same metric through the public API with HOST buffers: every step copies
+    A (pinned host) to the device inside qt_create, multiplies, and reads C back
+    to pinned host memory."""
+    import torch
+    brow = torch.from_numpy(Am.brow).pin_memory()
+    bcol = torch.from_numpy(Am.bcol).pin_memory()
+    vals = torch.from_numpy(Am.vals).pin_memory()
+    out = None
+    steps = max(2, min(args.steps, 5))
+
+    def step():
+        nonlocal out
+        A = qtmm.Matrix.from_blocks(ctx, Am.n, Am.leaf_dim, BS, brow, bcol, vals, row_bounds=bounds)
+        C, st = A.multiply(A)
+        nb = C.nblocks
+        if out is None or out[0].shape[0] != nb:
+            out = (torch.empty(nb, dtype=torch.int32).pin_memory(),
+                   torch.empty(nb, dtype=torch.int32).pin_memory(),
+                   torch.empty((nb, BS, BS), dtype=torch.float64).pin_memory())
+        C.to_blocks(out)
+        A.close()
+        C.close()
+        return st, nb
+
+    for _ in range(2):
+        step()
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        st, nb = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    a = aggregate(dist, [ms, float(st.block_products)], "cuda", world)
+    ms, prods = float(a[:, 0].max()), float(a[:, 1].sum())
+    h2d = Am.brow.nbytes + Am.bcol.nbytes + Am.vals.nbytes
+    d2h = nb * (8 + BS * BS * 8)
+    return {"value": round(prods * FLOP_PER_PRODUCT / (ms * 1e-3) / 1e9, 2), "unit": UNIT,
+            "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "api": "qt_create(host pinned) + qt_multiply + qt_read_back(host pinned)"}
+
+
+if __name__ == "__main__":
+    main()

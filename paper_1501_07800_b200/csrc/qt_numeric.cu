@@ -26,9 +26,15 @@ namespace qt {
 
 namespace {
 
-constexpr int kStages = 6;
+// Two independent tile streams per CTA (each: 4 consumer warps + 1 producer
+// warp + its own 3-stage ring), so every SM sub-partition runs two consumer
+// warps: while one is in its tile prologue/epilogue or waits on shared
+// memory, the other keeps the DMMA pipe busy.
+constexpr int kStreams = 2;
+constexpr int kStagesPer = 3;
+constexpr int kStages = kStreams * kStagesPer;
 constexpr int kConsumerWarps = 4;
-constexpr int kNumThreads = (kConsumerWarps + 1) * 32;
+constexpr int kNumThreads = kStreams * (kConsumerWarps + 1) * 32;
 constexpr int kBlockElems = 1024;                // 32 x 32
 constexpr int kStageElems = 4 * kBlockElems;     // A0 A1 B0 B1
 constexpr int kStageBytes = kStageElems * 8;     // 32 KiB (FP64)
@@ -115,16 +121,22 @@ __device__ __forceinline__ void warp_block_mma(double (&acc)[4][4][2], const dou
 
 __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  double* data = reinterpret_cast<double*>(smem);
-  StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + (size_t)kStages * kStageBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(hdr + kStages);
-  uint64_t* empty = full + kStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warps [0, 4*kStreams): consumers, stream = warp / 4 ; then one producer per stream
+  const bool producer = warp >= kStreams * kConsumerWarps;
+  const int sid = producer ? warp - kStreams * kConsumerWarps : warp / kConsumerWarps;
+  double* data = reinterpret_cast<double*>(smem) + (size_t)sid * kStagesPer * kStageElems;
+  StageHdr* hdr_all = reinterpret_cast<StageHdr*>(smem + (size_t)kStages * kStageBytes);
+  uint64_t* full_all = reinterpret_cast<uint64_t*>(hdr_all + kStages);
+  uint64_t* empty_all = full_all + kStages;
+  StageHdr* hdr = hdr_all + sid * kStagesPer;
+  uint64_t* full = full_all + sid * kStagesPer;
+  uint64_t* empty = empty_all + sid * kStagesPer;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&full_all[s], 1);
+      mbar_init(&empty_all[s], kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -133,7 +145,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   int stage = 0;
   uint32_t phase = 0;
 
-  if (warp == kConsumerWarps) {
+  if (producer) {
     // ------------------------------------------------------------ producer
     const double* poolA = static_cast<const double*>(a.poolA);
     const double* poolB = static_cast<const double*>(a.poolB);
@@ -195,7 +207,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
               }
             }
             __syncwarp();
-            if (++stage == kStages) {
+            if (++stage == kStagesPer) {
               stage = 0;
               phase ^= 1;
             }
@@ -213,14 +225,15 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         mbar_arrive(&full[stage]);
       }
       __syncwarp();
-      if (++stage == kStages) {
+      if (++stage == kStagesPer) {
         stage = 0;
         phase ^= 1;
       }
     }
   } else {
     // ------------------------------------------------------------ consumers
-    const int wi = warp >> 1, wj = warp & 1;
+    const int q = warp % kConsumerWarps;
+    const int wi = q >> 1, wj = q & 1;
     double* poolC = static_cast<double*>(a.poolC);
     double acc[4][4][2];
 #pragma unroll
@@ -234,7 +247,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
       const int flags = h.flags;
       if (flags & F_DONE) break;
       if (flags & F_STORE) {
-        const int cb = h.c[warp];
+        const int cb = h.c[q];
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (cb >= 0) {
@@ -260,7 +273,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
       }
-      if (++stage == kStages) {
+      if (++stage == kStagesPer) {
         stage = 0;
         phase ^= 1;
       }
