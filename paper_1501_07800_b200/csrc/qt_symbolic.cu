@@ -19,6 +19,14 @@
 // P:286-294).  The last transition (to the block level) only counts: the
 // numeric kernel consumes the level L-1 queue directly, one 2x2-block C node
 // (a "tile") per work item.
+//
+// Host synchronisation: the task count of every level is known before the BFS
+// starts — C_l = sum_K colcount(A_l)[K] * rowcount(B_l)[K] from per-level
+// occupancy histograms kept with each matrix — so all frontier buffers are
+// sized exactly and the BFS runs without host round trips.  The top levels
+// (frontiers up to 64K tasks) run in ONE single-CTA kernel with block-wide
+// scans; the large levels use grid-wide kernels + device scans.  One host sync
+// remains, before the numeric kernel (to size C's block pool).
 #include <cub/cub.cuh>
 
 #include "qt_common.cuh"
@@ -29,99 +37,56 @@ namespace qt {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kSmallThreads = 1024;
+constexpr int64_t kSmallMaxF = 1 << 16;
+
 inline unsigned grid_for(int64_t n) {
   int64_t g = (n + kThreads - 1) / kThreads;
   return (unsigned)(g < 1 ? 1 : g);
 }
 
-// counts of child tasks per (parent task, C child q), written group-major:
-// position 4*start(s) + q*m(s) + local(p)
-__global__ void k_count(int32_t F, const int32_t* __restrict__ pa, const int32_t* __restrict__ pb,
-                        const int32_t* __restrict__ pc, const int32_t* __restrict__ cstart,
-                        const int4* __restrict__ childA, const int4* __restrict__ childB,
-                        int32_t* __restrict__ cnt) {
-  int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= F) return;
-  int32_t s = pc[p];
-  int32_t c0 = cstart[s], m = cstart[s + 1] - c0, loc = p - c0;
-  int4 a = childA[pa[p]];
-  int4 b = childB[pb[p]];
-  // A child (i,k) in slot 2i+k ; B child (k,j) in slot 2k+j
-  int64_t base = 4ll * c0 + loc;
-  cnt[base + 0ll * m] = (a.x >= 0 && b.x >= 0) + (a.y >= 0 && b.z >= 0);  // (0,0)
-  cnt[base + 1ll * m] = (a.x >= 0 && b.y >= 0) + (a.y >= 0 && b.w >= 0);  // (0,1)
-  cnt[base + 2ll * m] = (a.z >= 0 && b.x >= 0) + (a.w >= 0 && b.z >= 0);  // (1,0)
-  cnt[base + 3ll * m] = (a.z >= 0 && b.y >= 0) + (a.w >= 0 && b.w >= 0);  // (1,1)
+// C_l for every level: one CTA per level
+__global__ void k_level_tasks(const int32_t* __restrict__ histA, const int32_t* __restrict__ histB,
+                              int64_t H, int64_t* __restrict__ out) {
+  using BR = cub::BlockReduce<long long, kThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  const int l = blockIdx.x;
+  const int64_t base = (1ll << l) - 1, m = 1ll << l;
+  long long s = 0;
+  for (int64_t K = threadIdx.x; K < m; K += blockDim.x)
+    s += (long long)histA[H + base + K] * (long long)histB[base + K];  // cols(A_l) . rows(B_l)
+  s = BR(tmp).Sum(s);
+  if (threadIdx.x == 0) out[l] = s;
 }
 
-// per (s,q): start and size of the new group; flag = non-empty
-__global__ void k_segs(int32_t ns, const int32_t* __restrict__ cstart,
-                       const int32_t* __restrict__ incl, int32_t* __restrict__ flag,
-                       int32_t* __restrict__ gstart) {
-  int32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= 4 * ns) return;
-  int32_t s = x >> 2, q = x & 3;
-  int32_t c0 = cstart[s], m = cstart[s + 1] - c0;
-  int64_t lo = 4ll * c0 + (int64_t)q * m, hi = lo + m;
-  int32_t st = lo == 0 ? 0 : incl[lo - 1];
-  int32_t en = incl[hi - 1];
-  flag[x] = en > st;
-  gstart[x] = st;
+// A child (i,k) sits in slot 2i+k, B child (k,j) in slot 2k+j, C child (i,j) in 2i+j.
+__device__ __forceinline__ void child_counts(int4 a, int4 b, int (&c)[4]) {
+  c[0] = (a.x >= 0 && b.x >= 0) + (a.y >= 0 && b.z >= 0);  // (0,0)
+  c[1] = (a.x >= 0 && b.y >= 0) + (a.y >= 0 && b.w >= 0);  // (0,1)
+  c[2] = (a.z >= 0 && b.x >= 0) + (a.w >= 0 && b.z >= 0);  // (1,0)
+  c[3] = (a.z >= 0 && b.y >= 0) + (a.w >= 0 && b.w >= 0);  // (1,1)
 }
 
-// C nodes of level l+1 (the non-empty groups) and the group -> node map of
-// level l (C's child table at level l before pruning)
-__global__ void k_newc(int32_t ns, const int32_t* __restrict__ flag,
-                       const int32_t* __restrict__ nincl, const int32_t* __restrict__ gstart,
-                       const uint64_t* __restrict__ ckey, const int32_t* __restrict__ incl,
-                       int64_t n4, int32_t* __restrict__ cstart_next,
-                       uint64_t* __restrict__ ckey_next, int32_t* __restrict__ cchild,
-                       int32_t* __restrict__ sizes_out) {
-  int32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x == 0) {
-    int32_t nsn = nincl[4 * ns - 1];
-    int32_t Fnext = incl[n4 - 1];
-    cstart_next[nsn] = Fnext;
-    sizes_out[0] = Fnext;
-    sizes_out[1] = nsn;
-  }
-  if (x >= 4 * ns) return;
-  if (flag[x]) {
-    int32_t t = nincl[x] - 1;
-    cstart_next[t] = gstart[x];
-    ckey_next[t] = (ckey[x >> 2] << 2) | (uint64_t)(x & 3);
-    cchild[x] = t;
-  } else {
-    cchild[x] = -1;
-  }
-}
-
-__global__ void k_emit(int32_t F, const int32_t* __restrict__ pa, const int32_t* __restrict__ pb,
-                       const int32_t* __restrict__ pc, const int32_t* __restrict__ cstart,
-                       const int4* __restrict__ childA, const int4* __restrict__ childB,
-                       const int32_t* __restrict__ incl, const int32_t* __restrict__ nincl,
-                       int32_t* __restrict__ pa2, int32_t* __restrict__ pb2,
-                       int32_t* __restrict__ pc2) {
-  int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= F) return;
-  int32_t s = pc[p];
-  int32_t c0 = cstart[s], m = cstart[s + 1] - c0, loc = p - c0;
-  int4 a4 = childA[pa[p]];
-  int4 b4 = childB[pb[p]];
-  int a[4] = {a4.x, a4.y, a4.z, a4.w};
-  int b[4] = {b4.x, b4.y, b4.z, b4.w};
-  int64_t base = 4ll * c0 + loc;
+// Write the child tasks of task p (group s, local index loc) at the exclusive
+// offsets `off` of its (s,q) slots; gidx maps (s,q) to the new group index.
+__device__ __forceinline__ void emit_task(int4 a4, int4 b4, int64_t base, int32_t m, int32_t s,
+                                          const int32_t* __restrict__ off,
+                                          const int32_t* __restrict__ gidx, int32_t* __restrict__ pa2,
+                                          int32_t* __restrict__ pb2, int32_t* __restrict__ pc2) {
+  const int a[4] = {a4.x, a4.y, a4.z, a4.w};
+  const int b[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    int i = q >> 1, j = q & 1;
-    int64_t idx = base + (int64_t)q * m;
-    int32_t pos = idx == 0 ? 0 : incl[idx - 1];
-    int32_t newc = -1;
+    const int i = q >> 1, j = q & 1;
+    int32_t pos = -1, newc = -1;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      int ac = a[2 * i + k], bc = b[2 * k + j];
+      const int ac = a[2 * i + k], bc = b[2 * k + j];
       if (ac >= 0 && bc >= 0) {
-        if (newc < 0) newc = nincl[4 * s + q] - 1;
+        if (pos < 0) {
+          pos = off[base + (int64_t)q * m];
+          newc = gidx[4 * s + q];
+        }
         pa2[pos] = ac;
         pb2[pos] = bc;
         pc2[pos] = newc;
@@ -131,12 +96,193 @@ __global__ void k_emit(int32_t F, const int32_t* __restrict__ pa, const int32_t*
   }
 }
 
+// ------------------------------------------------------------ small levels (one CTA)
+
+struct SmallBfsArgs {
+  int l_end;  // run transitions l -> l+1 for l < l_end
+  const int4* childA[QT_MAX_LEVELS];
+  const int4* childB[QT_MAX_LEVELS];
+  int32_t* pa[2];
+  int32_t* pb[2];
+  int32_t* pc[2];
+  int32_t* cstart[2];
+  uint64_t* ckey[2];
+  int32_t* off;     // 4 * max F scratch (counts, then exclusive offsets in place)
+  int32_t* gidx;    // 4 * max ns scratch
+  int32_t* ns_out;  // C groups per level
+};
+
+__global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) {
+  using BS = cub::BlockScan<int, kSmallThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int s_F, s_ns;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    a.pa[0][0] = 0;
+    a.pb[0][0] = 0;
+    a.pc[0][0] = 0;
+    a.cstart[0][0] = 0;
+    a.cstart[0][1] = 1;
+    a.ckey[0][0] = 0;
+    a.ns_out[0] = 1;
+    s_F = 1;
+    s_ns = 1;
+  }
+  __syncthreads();
+  for (int l = 0; l < a.l_end; ++l) {
+    const int cur = l & 1, nxt = cur ^ 1;
+    const int F = s_F, ns = s_ns;
+    const int32_t* pa = a.pa[cur];
+    const int32_t* pb = a.pb[cur];
+    const int32_t* pc = a.pc[cur];
+    const int32_t* cs = a.cstart[cur];
+    const uint64_t* ck = a.ckey[cur];
+    const int4* cA = a.childA[l];
+    const int4* cB = a.childB[l];
+    // 1. child-task counts per (task, C child), group-major
+    for (int p = tid; p < F; p += kSmallThreads) {
+      const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
+      int c[4];
+      child_counts(cA[pa[p]], cB[pb[p]], c);
+      const int64_t base = 4ll * c0 + (p - c0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a.off[base + (int64_t)q * m] = c[q];
+    }
+    __syncthreads();
+    // 2. exclusive scan in place
+    int carry = 0;
+    for (int b0 = 0; b0 < 4 * F; b0 += kSmallThreads) {
+      const int i = b0 + tid;
+      const int v = i < 4 * F ? a.off[i] : 0;
+      int ex, agg;
+      BS(tmp).ExclusiveSum(v, ex, agg);
+      if (i < 4 * F) a.off[i] = carry + ex;
+      carry += agg;
+      __syncthreads();
+    }
+    const int Fn = carry;
+    // 3. new groups (non-empty (s,q)), their starts and keys
+    int ncarry = 0;
+    for (int b0 = 0; b0 < 4 * ns; b0 += kSmallThreads) {
+      const int x = b0 + tid;
+      int flag = 0, gst = 0;
+      if (x < 4 * ns) {
+        const int s = x >> 2, q = x & 3, c0 = cs[s], m = cs[s + 1] - c0;
+        const int lo = 4 * c0 + q * m, hi = lo + m;
+        gst = a.off[lo];
+        const int en = hi < 4 * F ? a.off[hi] : Fn;
+        flag = en > gst;
+      }
+      int ex, agg;
+      BS(tmp).ExclusiveSum(flag, ex, agg);
+      if (x < 4 * ns) {
+        const int t = flag ? ncarry + ex : -1;
+        a.gidx[x] = t;
+        if (flag) {
+          a.cstart[nxt][t] = gst;
+          a.ckey[nxt][t] = (ck[x >> 2] << 2) | (uint64_t)(x & 3);
+        }
+      }
+      ncarry += agg;
+      __syncthreads();
+    }
+    const int nsn = ncarry;
+    if (tid == 0) {
+      a.cstart[nxt][nsn] = Fn;
+      a.ns_out[l + 1] = nsn;
+    }
+    __syncthreads();
+    // 4. emit the child tasks
+    for (int p = tid; p < F; p += kSmallThreads) {
+      const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
+      emit_task(cA[pa[p]], cB[pb[p]], 4ll * c0 + (p - c0), m, s, a.off, a.gidx, a.pa[nxt], a.pb[nxt],
+                a.pc[nxt]);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_F = Fn;
+      s_ns = nsn;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ large levels (grid-wide)
+
+__global__ void k_count(int32_t F, const int32_t* __restrict__ pa, const int32_t* __restrict__ pb,
+                        const int32_t* __restrict__ pc, const int32_t* __restrict__ cstart,
+                        const int4* __restrict__ childA, const int4* __restrict__ childB,
+                        int32_t* __restrict__ cnt) {
+  const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= F) return;
+  const int32_t s = pc[p], c0 = cstart[s], m = cstart[s + 1] - c0;
+  int c[4];
+  child_counts(childA[pa[p]], childB[pb[p]], c);
+  const int64_t base = 4ll * c0 + (p - c0);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) cnt[base + (int64_t)q * m] = c[q];
+}
+
+// per (s,q) slot: start of the new group and non-empty flag (0 beyond the real ns)
+__global__ void k_segs(int32_t nsb, const int32_t* __restrict__ ns_dev, int32_t F, int32_t Fn,
+                       const int32_t* __restrict__ cstart, const int32_t* __restrict__ off,
+                       int32_t* __restrict__ flag, int32_t* __restrict__ gstart) {
+  const int32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= 4 * nsb) return;
+  const int32_t ns = *ns_dev;
+  int32_t f = 0, st = 0;
+  if (x < 4 * ns) {
+    const int32_t s = x >> 2, q = x & 3, c0 = cstart[s], m = cstart[s + 1] - c0;
+    const int64_t lo = 4ll * c0 + (int64_t)q * m, hi = lo + m;
+    st = off[lo];
+    const int32_t en = hi < 4ll * F ? off[hi] : Fn;
+    f = en > st;
+  }
+  flag[x] = f;
+  gstart[x] = st;
+}
+
+__global__ void k_newc(int32_t nsb, const int32_t* __restrict__ ns_dev, int32_t Fn,
+                       const int32_t* __restrict__ flag, const int32_t* __restrict__ nex,
+                       const int32_t* __restrict__ gstart, const uint64_t* __restrict__ ckey,
+                       int32_t* __restrict__ cstart_next, uint64_t* __restrict__ ckey_next,
+                       int32_t* __restrict__ gidx, int32_t* __restrict__ ns_next) {
+  const int32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t ns = *ns_dev;
+  if (x >= 4 * ns) return;
+  if (x == 4 * ns - 1) {
+    const int32_t nsn = nex[x] + flag[x];
+    cstart_next[nsn] = Fn;
+    *ns_next = nsn;
+  }
+  if (flag[x]) {
+    const int32_t t = nex[x];
+    cstart_next[t] = gstart[x];
+    ckey_next[t] = (ckey[x >> 2] << 2) | (uint64_t)(x & 3);
+    gidx[x] = t;
+  } else {
+    gidx[x] = -1;
+  }
+}
+
+__global__ void k_emit(int32_t F, const int32_t* __restrict__ pa, const int32_t* __restrict__ pb,
+                       const int32_t* __restrict__ pc, const int32_t* __restrict__ cstart,
+                       const int4* __restrict__ childA, const int4* __restrict__ childB,
+                       const int32_t* __restrict__ off, const int32_t* __restrict__ gidx,
+                       int32_t* __restrict__ pa2, int32_t* __restrict__ pb2,
+                       int32_t* __restrict__ pc2) {
+  const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= F) return;
+  const int32_t s = pc[p], c0 = cstart[s], m = cstart[s + 1] - c0;
+  emit_task(childA[pa[p]], childB[pb[p]], 4ll * c0 + (p - c0), m, s, off, gidx, pa2, pb2, pc2);
+}
+
 template <class T>
-void incl_sum(qt_ctx ctx, const T* in, T* out, int64_t n) {
+void excl_sum(qt_ctx ctx, const T* in, T* out, int64_t n) {
   size_t tb = 0;
-  QT_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out, (int)n, ctx->stream));
+  QT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, ctx->stream));
   void* tmp = scratch(ctx, tb);
-  QT_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, in, out, (int)n, ctx->stream));
+  QT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, (int)n, ctx->stream));
   ctx->launches += 2;
 }
 
@@ -168,102 +314,138 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
   S.leaf_level = A->leaf_level;
   try {
     QT_CUDA(cudaEventRecord(ctx->ev[2], st));
-    if (A->nb == 0 || B->nb == 0) {
+    std::vector<int64_t> F(L + 1, 0);
+    if (A->nb > 0 && B->nb > 0) {
+      // exact task counts per level (one sync)
+      const int64_t H = 2ll << L;
+      DevBuf dF(8 * (L + 1), st);
+      k_level_tasks<<<L + 1, kThreads, 0, st>>>(A->hist.as<int32_t>(), B->hist.as<int32_t>(), H,
+                                               dF.as<int64_t>());
+      QT_LAUNCH_CHECK(ctx);
+      QT_CUDA(cudaMemcpyAsync(F.data(), dF.p, 8 * (L + 1), cudaMemcpyDeviceToHost, st));
+      QT_CUDA(cudaStreamSynchronize(st));
+      for (int l = 0; l <= L; ++l)
+        if (F[l] >= (1ll << 31) / 4) fail(QT_EINVAL, "level %d has %lld tasks (> 2^29)", l, (long long)F[l]);
+    }
+    for (int l = 0; l <= L; ++l) S.level_tasks[l] = F[l];
+    S.block_products = F[L];
+    if (F[L] == 0) {
+      // no block product at all: C is the NIL matrix
+      C->nb = 0;
       QT_CUDA(cudaEventRecord(ctx->ev[3], st));
       QT_CUDA(cudaEventRecord(ctx->ev[4], st));
     } else {
-      int32_t* sizes = ctx->counters.as<int32_t>() + 8;  // [F', ns']
-      int32_t* hsz = (int32_t*)ctx->pinned;
-      // level 0: the single root task
-      int32_t F = 1, ns = 1;
-      DevBuf pa(4, st), pb(4, st), pc(4, st), cstart(8, st), ckey(8, st);
-      {
-        int32_t h0[4] = {0, 0, 0, 1};
-        uint64_t k0 = 0;
-        QT_CUDA(cudaMemsetAsync(pa.p, 0, 4, st));
-        QT_CUDA(cudaMemsetAsync(pb.p, 0, 4, st));
-        QT_CUDA(cudaMemsetAsync(pc.p, 0, 4, st));
-        QT_CUDA(cudaMemcpyAsync(cstart.p, h0 + 2, 8, cudaMemcpyHostToDevice, st));
-        QT_CUDA(cudaMemcpyAsync(ckey.p, &k0, 8, cudaMemcpyHostToDevice, st));
+      // upper bounds of the group counts: ns_{l+1} <= min(4 ns_l, F_{l+1})
+      std::vector<int64_t> nsb(L + 1, 1);
+      for (int l = 0; l < L; ++l) nsb[l + 1] = std::min<int64_t>(4 * nsb[l], F[l + 1]);
+      DevBuf ns_dev(4 * (L + 1), st);
+      int32_t* nsd = ns_dev.as<int32_t>();
+      // --- small levels in one CTA
+      int l_end = 0;
+      while (l_end < L - 1 && F[l_end + 1] <= kSmallMaxF) ++l_end;
+      int64_t maxF = 1, maxNS = 1, maxF4 = 1;
+      for (int l = 0; l <= l_end; ++l) {
+        maxF = std::max(maxF, F[l]);
+        maxNS = std::max(maxNS, nsb[l]);
+        if (l < l_end) maxF4 = std::max(maxF4, 4 * F[l]);
       }
-      S.level_tasks[0] = 1;
-      S.level_c_nodes[0] = 1;
-      int64_t products = 0;
-      for (int l = 0; l < L && F > 0; ++l) {
-        bool last = (l == L - 1);
-        int64_t n4 = 4ll * F;
-        DevBuf cnt(n4 * 4, st), incl(n4 * 4, st);
-        k_count<<<grid_for(F), kThreads, 0, st>>>(F, pa.as<int32_t>(), pb.as<int32_t>(),
-                                                  pc.as<int32_t>(), cstart.as<int32_t>(),
-                                                  A->child[l].as<int4>(), B->child[l].as<int4>(),
-                                                  cnt.as<int32_t>());
+      DevBuf sp[2], sb[2], sc[2], scs[2], sck[2];
+      SmallBfsArgs sa;
+      sa.l_end = l_end;
+      for (int l = 0; l < L; ++l) {
+        sa.childA[l] = A->child[l].as<int4>();
+        sa.childB[l] = B->child[l].as<int4>();
+      }
+      for (int b = 0; b < 2; ++b) {
+        sp[b].alloc(4 * maxF, st);
+        sb[b].alloc(4 * maxF, st);
+        sc[b].alloc(4 * maxF, st);
+        scs[b].alloc(4 * (maxNS + 1), st);
+        sck[b].alloc(8 * maxNS, st);
+        sa.pa[b] = sp[b].as<int32_t>();
+        sa.pb[b] = sb[b].as<int32_t>();
+        sa.pc[b] = sc[b].as<int32_t>();
+        sa.cstart[b] = scs[b].as<int32_t>();
+        sa.ckey[b] = sck[b].as<uint64_t>();
+      }
+      DevBuf soff(4 * maxF4, st), sg(16 * maxNS, st);
+      sa.off = soff.as<int32_t>();
+      sa.gidx = sg.as<int32_t>();
+      sa.ns_out = nsd;
+      k_bfs_small<<<1, kSmallThreads, 0, st>>>(sa);
+      QT_LAUNCH_CHECK(ctx);
+      const int cb = l_end & 1;
+      DevBuf pa = std::move(sp[cb]), pb = std::move(sb[cb]), pc = std::move(sc[cb]);
+      DevBuf cstart = std::move(scs[cb]), ckey = std::move(sck[cb]);
+      // --- large levels, grid-wide, no host sync
+      DevBuf cchild;
+      for (int l = l_end; l < L; ++l) {
+        const bool last = (l == L - 1);
+        const int32_t Fl = (int32_t)F[l], Fn = (int32_t)F[l + 1];
+        const int64_t n4 = 4ll * Fl, s4 = 4ll * nsb[l];
+        DevBuf cnt(4 * n4, st), off(4 * n4, st);
+        k_count<<<grid_for(Fl), kThreads, 0, st>>>(Fl, pa.as<int32_t>(), pb.as<int32_t>(),
+                                                   pc.as<int32_t>(), cstart.as<int32_t>(),
+                                                   A->child[l].as<int4>(), B->child[l].as<int4>(),
+                                                   cnt.as<int32_t>());
         QT_LAUNCH_CHECK(ctx);
-        incl_sum(ctx, cnt.as<int32_t>(), incl.as<int32_t>(), n4);
-        DevBuf flag(16ll * ns, st), gstart(16ll * ns, st), nincl(16ll * ns, st);
-        k_segs<<<grid_for(4ll * ns), kThreads, 0, st>>>(ns, cstart.as<int32_t>(), incl.as<int32_t>(),
-                                                        flag.as<int32_t>(), gstart.as<int32_t>());
+        excl_sum(ctx, cnt.as<int32_t>(), off.as<int32_t>(), n4);
+        DevBuf flag(4 * s4, st), gstart(4 * s4, st), nex(4 * s4, st), gidx(4 * s4, st);
+        k_segs<<<grid_for(s4), kThreads, 0, st>>>((int32_t)nsb[l], nsd + l, Fl, Fn,
+                                                  cstart.as<int32_t>(), off.as<int32_t>(),
+                                                  flag.as<int32_t>(), gstart.as<int32_t>());
         QT_LAUNCH_CHECK(ctx);
-        incl_sum(ctx, flag.as<int32_t>(), nincl.as<int32_t>(), 4ll * ns);
-        // next-level C nodes (upper bound 4*ns) and the group -> node map
-        DevBuf cstart2(4 * (4ll * ns + 1), st), ckey2(8 * 4ll * ns, st), cchild(16ll * ns, st);
-        k_newc<<<grid_for(4ll * ns), kThreads, 0, st>>>(ns, flag.as<int32_t>(), nincl.as<int32_t>(),
-                                                        gstart.as<int32_t>(), ckey.as<uint64_t>(),
-                                                        incl.as<int32_t>(), n4, cstart2.as<int32_t>(),
-                                                        ckey2.as<uint64_t>(), cchild.as<int32_t>(),
-                                                        sizes);
+        excl_sum(ctx, flag.as<int32_t>(), nex.as<int32_t>(), s4);
+        DevBuf cstart2(4 * (nsb[l + 1] + 1), st), ckey2(8 * std::max<int64_t>(nsb[l + 1], 1), st);
+        k_newc<<<grid_for(s4), kThreads, 0, st>>>((int32_t)nsb[l], nsd + l, Fn, flag.as<int32_t>(),
+                                                  nex.as<int32_t>(), gstart.as<int32_t>(),
+                                                  ckey.as<uint64_t>(), cstart2.as<int32_t>(),
+                                                  ckey2.as<uint64_t>(), gidx.as<int32_t>(), nsd + l + 1);
         QT_LAUNCH_CHECK(ctx);
-        QT_CUDA(cudaMemcpyAsync(hsz, sizes, 8, cudaMemcpyDeviceToHost, st));
-        QT_CUDA(cudaStreamSynchronize(st));
-        int32_t Fn = hsz[0], nsn = hsz[1];
-        S.level_tasks[l + 1] = Fn;
-        S.level_c_nodes[l + 1] = nsn;
         if (last) {
-          products = Fn;
-          // C blocks = level-L nodes; keys ascending (Morton order by construction)
-          C->nb = nsn;
           C->key = std::move(ckey2);
-          C->pool.alloc((size_t)nsn * 1024 * elem_size(C->dtype), st);
-          QT_CUDA(cudaEventRecord(ctx->ev[3], st));
-          NumericArgs na;
-          na.ntiles = ns;
-          na.tile_start = cstart.as<int32_t>();
-          na.pa = pa.as<int32_t>();
-          na.pb = pb.as<int32_t>();
-          na.childA = A->child[l].as<int4>();
-          na.childB = B->child[l].as<int4>();
-          na.childC = cchild.as<int4>();
-          na.poolA = A->pool_ptr();
-          na.poolB = B->pool_ptr();
-          na.poolB2 = B->pool2;
-          na.splitB = B->split;
-          na.poolC = C->pool.p;
-          na.counter = ctx->counters.as<int>() + 16;
-          if (nsn > 0) launch_numeric(ctx, C->dtype, na);
-          QT_CUDA(cudaEventRecord(ctx->ev[4], st));
+          cchild = std::move(gidx);
           break;
         }
-        if (Fn == 0) break;
         DevBuf pa2(4ll * Fn, st), pb2(4ll * Fn, st), pc2(4ll * Fn, st);
-        k_emit<<<grid_for(F), kThreads, 0, st>>>(F, pa.as<int32_t>(), pb.as<int32_t>(),
-                                                 pc.as<int32_t>(), cstart.as<int32_t>(),
-                                                 A->child[l].as<int4>(), B->child[l].as<int4>(),
-                                                 incl.as<int32_t>(), nincl.as<int32_t>(),
-                                                 pa2.as<int32_t>(), pb2.as<int32_t>(),
-                                                 pc2.as<int32_t>());
+        k_emit<<<grid_for(Fl), kThreads, 0, st>>>(Fl, pa.as<int32_t>(), pb.as<int32_t>(),
+                                                  pc.as<int32_t>(), cstart.as<int32_t>(),
+                                                  A->child[l].as<int4>(), B->child[l].as<int4>(),
+                                                  off.as<int32_t>(), gidx.as<int32_t>(),
+                                                  pa2.as<int32_t>(), pb2.as<int32_t>(),
+                                                  pc2.as<int32_t>());
         QT_LAUNCH_CHECK(ctx);
         pa = std::move(pa2);
         pb = std::move(pb2);
         pc = std::move(pc2);
         cstart = std::move(cstart2);
         ckey = std::move(ckey2);
-        F = Fn;
-        ns = nsn;
       }
-      S.block_products = products;
-      if (products == 0) {
-        QT_CUDA(cudaEventRecord(ctx->ev[3], st));
-        QT_CUDA(cudaEventRecord(ctx->ev[4], st));
-      }
+      // --- group counts of every level (the one remaining sync): C's block count
+      std::vector<int32_t> ns(L + 1, 0);
+      QT_CUDA(cudaMemcpyAsync(ns.data(), nsd, 4 * (L + 1), cudaMemcpyDeviceToHost, st));
+      QT_CUDA(cudaStreamSynchronize(st));
+      for (int l = 0; l <= L; ++l) S.level_c_nodes[l] = ns[l];
+      C->nb = ns[L];
+      C->pool.alloc((size_t)C->nb * 1024 * elem_size(C->dtype), st);
+      QT_CUDA(cudaEventRecord(ctx->ev[3], st));
+      NumericArgs na;
+      na.ntiles = ns[L - 1];
+      na.tile_start = cstart.as<int32_t>();
+      na.pa = pa.as<int32_t>();
+      na.pb = pb.as<int32_t>();
+      na.childA = A->child[L - 1].as<int4>();
+      na.childB = B->child[L - 1].as<int4>();
+      na.childC = cchild.as<int4>();
+      na.poolA = A->pool_ptr();
+      na.poolB = B->pool_ptr();
+      na.poolB2 = B->pool2;
+      na.splitB = B->split;
+      na.poolC = C->pool.p;
+      na.counter = ctx->counters.as<int>() + 16;
+      if (C->nb > 0) launch_numeric(ctx, C->dtype, na);
+      QT_CUDA(cudaEventRecord(ctx->ev[4], st));
+      QT_CUDA(cudaEventSynchronize(ctx->ev[4]));  // frontier buffers are released after this
     }
     QT_CUDA(cudaEventSynchronize(ctx->ev[4]));
     QT_CUDA(cudaEventElapsedTime(ms_sym, ctx->ev[2], ctx->ev[3]));

@@ -82,6 +82,19 @@ __global__ void k_link(const uint64_t* __restrict__ key, const int32_t* __restri
   }
 }
 
+// per-level occupancy histograms: rows at hist[(1<<l)-1 + r], columns at
+// hist[H + (1<<l)-1 + c], H = 2^(L+1)
+__global__ void k_level_hist(const uint64_t* __restrict__ key, int64_t n, int l, int64_t H,
+                             int32_t* __restrict__ hist) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = key[t];
+    int64_t base = (1ll << l) - 1;
+    atomicAdd(&hist[base + morton_row(k)], 1);
+    atomicAdd(&hist[H + base + morton_col(k)], 1);
+  }
+}
+
 __global__ void k_rowmajor_keys(const uint64_t* __restrict__ key, int64_t n,
                                 uint64_t* __restrict__ rm, int32_t* __restrict__ iota) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
@@ -225,9 +238,15 @@ void build_levels(qt_mat M, const int32_t* leaf_ids) {
   M->child.clear();
   M->child.resize(M->L);
   M->cnt[M->L] = M->nb;
+  const int64_t H = 2ll << M->L;
+  M->hist.alloc(8 * H, st);
+  QT_CUDA(cudaMemsetAsync(M->hist.p, 0, 8 * H, st));
   if (M->nb == 0) return;
   DevBuf cur_keys(M->nb * 8, st);
   QT_CUDA(cudaMemcpyAsync(cur_keys.p, M->key.p, M->nb * 8, cudaMemcpyDeviceToDevice, st));
+  k_level_hist<<<grid_for(M->nb), kThreads, 0, st>>>(cur_keys.as<uint64_t>(), M->nb, M->L, H,
+                                                     M->hist.as<int32_t>());
+  QT_LAUNCH_CHECK(ctx);
   for (int l = M->L - 1; l >= 0; --l) {
     int64_t n = M->cnt[l + 1];
     DevBuf flag(n * 4, st), incl(n * 4, st);
@@ -244,6 +263,9 @@ void build_levels(qt_mat M, const int32_t* leaf_ids) {
                                              M->child[l].as<int32_t>(), pkey.as<uint64_t>());
     QT_LAUNCH_CHECK(ctx);
     cur_keys = std::move(pkey);
+    k_level_hist<<<grid_for(np), kThreads, 0, st>>>(cur_keys.as<uint64_t>(), np, l, H,
+                                                    M->hist.as<int32_t>());
+    QT_LAUNCH_CHECK(ctx);
   }
 }
 
