@@ -24,7 +24,7 @@
 // starts — C_l = sum_K colcount(A_l)[K] * rowcount(B_l)[K] from per-level
 // occupancy histograms kept with each matrix — so all frontier buffers are
 // sized exactly and the BFS runs without host round trips.  The top levels
-// (frontiers up to 64K tasks) run in ONE single-CTA kernel with block-wide
+// (frontiers up to 8K tasks) run in ONE single-CTA kernel with block-wide
 // scans; the large levels use grid-wide kernels + device scans.  One host sync
 // remains, before the numeric kernel (to size C's block pool).
 #include <cub/cub.cuh>
@@ -38,7 +38,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kSmallThreads = 1024;
-constexpr int64_t kSmallMaxF = 1 << 16;
+constexpr int64_t kSmallMaxF = 1 << 13;
 
 inline unsigned grid_for(int64_t n) {
   int64_t g = (n + kThreads - 1) / kThreads;

@@ -1,0 +1,81 @@
+"""Per-config device timing of qt_multiply (all BASELINE configs that fit one
+GPU), with the numeric-kernel share.  Not part of the bench contract: a
+development tool whose output is summarised in profiles/."""
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import qtgen  # noqa: E402
+from paper_1501_07800_b200 import qtmm  # noqa: E402
+
+FLOP = 2 * 32 ** 3
+
+
+def run(ctx, stream, name, c, steps=20):
+    Am = c["A"]
+    A = qtmm.Matrix.from_blocks(ctx, Am.n, Am.leaf_dim, 32, Am.brow, Am.bcol, Am.vals)
+    if c["same"]:
+        B = A
+    else:
+        Bm = c["B"]
+        B = qtmm.Matrix.from_blocks(ctx, Bm.n, Bm.leaf_dim, 32, Bm.brow, Bm.bcol, Bm.vals)
+    for _ in range(3):
+        C, st = A.multiply(B)
+        C.close()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sts = []
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        C, st = A.multiply(B)
+        sts.append(st)
+        C.close()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    st = sts[-1]
+    num = statistics.mean(s.ms_numeric for s in sts)
+    sym = statistics.mean(s.ms_symbolic for s in sts)
+    out = {"config": name, "block_products": st.block_products, "c_blocks": st.c_blocks,
+           "A_blocks": Am.nb, "ms_step": round(ms, 4), "ms_numeric": round(num, 4),
+           "ms_symbolic": round(sym, 4), "gflops_effective": round(st.block_products * FLOP / ms / 1e6, 1),
+           "tflops_numeric": round(st.block_products * FLOP / num / 1e9, 2),
+           "level_tasks": st.as_dict()["level_tasks"]}
+    print(json.dumps(out), flush=True)
+    return out
+
+
+def main():
+    which = sys.argv[1:] or ["1", "2", "3", "4", "5"]
+    torch.cuda.set_device(0)
+    stream = torch.cuda.Stream()
+    ctx = qtmm.Context(0, stream=stream)
+    peak = ctx.fp64_peak("dmma", 200.0)
+    print(json.dumps({"dmma_peak_tflops": round(peak / 1e12, 3),
+                      "dfma_peak_tflops": round(ctx.fp64_peak("dfma", 200.0) / 1e12, 3)}), flush=True)
+    for w in which:
+        if w == "1":
+            run(ctx, stream, "cfg1 dense N=512", qtgen.config(1), steps=200)
+        elif w == "2":
+            run(ctx, stream, "cfg2 banded N=16384", qtgen.config(2))
+        elif w == "3":
+            run(ctx, stream, "cfg3 random N=32768 p=0.01", qtgen.config(3))
+        elif w == "4":
+            run(ctx, stream, "cfg4 ES-like N=98304", qtgen.config(4), steps=10)
+        elif w == "5":
+            run(ctx, stream, "cfg5 P=1 banded N=16384 leaf 2048", qtgen.config(5, P=1))
+        elif w == "dense4096":
+            br, bc = qtgen.pattern_dense(128)
+            v = qtgen.block_values(br, bc, 32, 1)
+            M = qtgen.BlockMatrix(4096, 1024, 32, br, bc, v)
+            run(ctx, stream, "dense N=4096 (supplementary)", {"A": M, "B": M, "same": True})
+
+
+if __name__ == "__main__":
+    main()
