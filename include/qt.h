@@ -183,6 +183,19 @@ const char* qt_last_error(void);
 qt_status qt_multiply_virtual(qt_mat A, qt_mat B, int32_t P, int32_t g,
                               const int32_t* row_bounds, qt_mat* C, qt_stats* st);
 
+/* Loopback transport for testing the multi-rank path on ONE device: `world`
+ * rank threads of one process each create a context with
+ * qt_ctx_create_loopback on the same hub (and their own stream) and call the
+ * collective functions concurrently.  Every NCCL send/recv of the exchange is
+ * replaced by a device-to-device cudaMemcpyAsync ordered by CUDA events (no
+ * kernel waits on another rank); allgathers go through host memory.  All other
+ * code — partition, request lists, packing, B_ext merge, multiply — is the
+ * multi-rank code of qt_multiply.  The hub must outlive its contexts. */
+qt_status qt_loopback_hub_create(int32_t world, void** hub);
+qt_status qt_loopback_hub_destroy(void* hub);
+qt_status qt_ctx_create_loopback(int device, void* cuda_stream, int rank, int world, void* hub,
+                                 qt_ctx* out);
+
 /* Number of CUDA kernels this context has launched so far (bench accounting). */
 int64_t qt_kernel_launches(qt_ctx ctx);
 

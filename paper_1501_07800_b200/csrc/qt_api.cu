@@ -62,14 +62,11 @@ extern "C" {
 
 const char* qt_last_error(void) { return g_last_error.c_str(); }
 
-qt_status qt_ctx_create(int device, void* cuda_stream, int rank, int world,
-                        const void* nccl_unique_id, qt_ctx* out) {
-  API_TRY
+static void ctx_create(int device, void* cuda_stream, int rank, int world, const void* uid,
+                       void* hub, qt_ctx* out) {
   if (!out) fail(QT_EINVAL, "out is NULL");
   *out = nullptr;
   if (world < 1 || rank < 0 || rank >= world) fail(QT_EINVAL, "bad rank %d / world %d", rank, world);
-  if ((world > 1) != (nccl_unique_id != nullptr))
-    fail(QT_EINVAL, "nccl_unique_id must be non-NULL iff world > 1");
   int ndev = 0;
   QT_CUDA(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) fail(QT_EINVAL, "device %d not in [0,%d)", device, ndev);
@@ -91,7 +88,10 @@ qt_status qt_ctx_create(int device, void* cuda_stream, int rank, int world,
     QT_CUDA(cudaMemsetAsync(c->counters.p, 0, 256, c->stream));
     c->pinned_bytes = 256;
     QT_CUDA(cudaMallocHost(&c->pinned, c->pinned_bytes));
-    if (world > 1) dist_init(c, nccl_unique_id);
+    if (world > 1) {
+      if (hub) dist_init_loopback(c, hub);
+      else dist_init(c, uid);
+    }
     QT_CUDA(cudaStreamSynchronize(c->stream));
   } catch (...) {
     if (c->pinned) cudaFreeHost(c->pinned);
@@ -99,6 +99,35 @@ qt_status qt_ctx_create(int device, void* cuda_stream, int rank, int world,
     throw;
   }
   *out = c;
+}
+
+qt_status qt_ctx_create(int device, void* cuda_stream, int rank, int world,
+                        const void* nccl_unique_id, qt_ctx* out) {
+  API_TRY
+  if ((world > 1) != (nccl_unique_id != nullptr))
+    fail(QT_EINVAL, "nccl_unique_id must be non-NULL iff world > 1");
+  ctx_create(device, cuda_stream, rank, world, nccl_unique_id, nullptr, out);
+  API_CATCH
+}
+
+qt_status qt_loopback_hub_create(int32_t world, void** hub) {
+  API_TRY
+  if (!hub || world < 1) fail(QT_EINVAL, "bad arguments");
+  *hub = loop_hub_create(world);
+  API_CATCH
+}
+
+qt_status qt_loopback_hub_destroy(void* hub) {
+  API_TRY
+  if (hub) loop_hub_destroy(hub);
+  API_CATCH
+}
+
+qt_status qt_ctx_create_loopback(int device, void* cuda_stream, int rank, int world, void* hub,
+                                 qt_ctx* out) {
+  API_TRY
+  if (!hub) fail(QT_EINVAL, "hub is NULL");
+  ctx_create(device, cuda_stream, rank, world, nullptr, hub, out);
   API_CATCH
 }
 

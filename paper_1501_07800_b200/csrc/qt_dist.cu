@@ -24,6 +24,12 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <condition_variable>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <tuple>
+
 #include <algorithm>
 #include <cub/cub.cuh>
 
@@ -91,41 +97,182 @@ static NcclApi& nccl() {
     if (r_ != ncclSuccess) fail(QT_ENCCL, "%s: %s", #x, nccl().GetErrorString(r_));        \
   } while (0)
 
-static ncclComm_t comm(qt_ctx ctx) { return (ncclComm_t)ctx->nccl_comm; }
+// ------------------------------------------------------------------ transport
+//
+// The exchange talks to a Transport: NCCL in production (one process per GPU,
+// NVLink / NVSwitch), or — for testing the same orchestration on a single GPU —
+// a loopback between rank threads of one process, where a device-to-device
+// cudaMemcpyAsync ordered by CUDA events stands in for each send/recv pair.
+// Kernels never wait on other ranks in either transport.
 
-void dist_init(qt_ctx ctx, const void* uid) {
-  NcclApi& N = nccl();
-  ncclUniqueId id;
-  memcpy(&id, uid, sizeof(id));
-  ncclComm_t c;
-  NCCL_CALL(N.CommInitRank(&c, ctx->world, id, ctx->rank));
-  ctx->nccl_comm = c;
+struct Transport {
+  virtual ~Transport() = default;
+  virtual void allgather_i64(const int64_t* send_host, int64_t* recv_host, int count) = 0;
+  virtual void group_start() = 0;
+  virtual void send(const void* buf, size_t bytes, int peer) = 0;
+  virtual void recv(void* buf, size_t bytes, int peer) = 0;
+  virtual void group_end() = 0;
+};
+
+struct NcclTransport : Transport {
+  qt_ctx ctx;
+  ncclComm_t comm = nullptr;
+  NcclTransport(qt_ctx c, const void* uid) : ctx(c) {
+    NcclApi& N = nccl();
+    ncclUniqueId id;
+    memcpy(&id, uid, sizeof(id));
+    NCCL_CALL(N.CommInitRank(&comm, ctx->world, id, ctx->rank));
+  }
+  ~NcclTransport() override {
+    if (comm) nccl().CommDestroy(comm);
+  }
+  void allgather_i64(const int64_t* send_host, int64_t* recv_host, int count) override {
+    NcclApi& N = nccl();
+    DevBuf s(8 * count, ctx->stream), r(8ll * count * ctx->world, ctx->stream);
+    QT_CUDA(cudaMemcpyAsync(s.p, send_host, 8 * count, cudaMemcpyHostToDevice, ctx->stream));
+    NCCL_CALL(N.AllGather(s.p, r.p, count, ncclInt64, comm, ctx->stream));
+    QT_CUDA(cudaMemcpyAsync(recv_host, r.p, 8ll * count * ctx->world, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    QT_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  void group_start() override { NCCL_CALL(nccl().GroupStart()); }
+  void send(const void* buf, size_t bytes, int peer) override {
+    NCCL_CALL(nccl().Send(buf, bytes, ncclInt8, peer, comm, ctx->stream));
+  }
+  void recv(void* buf, size_t bytes, int peer) override {
+    NCCL_CALL(nccl().Recv(buf, bytes, ncclInt8, peer, comm, ctx->stream));
+  }
+  void group_end() override { NCCL_CALL(nccl().GroupEnd()); }
+};
+
+// Shared state of the loopback ranks (one per process, created by the caller).
+struct LoopHub {
+  int P;
+  std::mutex mu;
+  std::condition_variable cv;
+  struct Msg {
+    const void* src;
+    size_t bytes;
+    cudaEvent_t ready;  // sender's data is complete
+    cudaEvent_t done;   // receiver's copy is complete
+    bool taken = false, copied = false;
+  };
+  std::vector<std::deque<std::shared_ptr<Msg>>> q;  // [src*P + dst]
+  // allgather
+  std::vector<int64_t> ag;
+  int ag_count = 0, ag_arrived = 0, ag_left = 0;
+  uint64_t ag_gen = 0;
+  explicit LoopHub(int p) : P(p), q((size_t)p * p) {}
+};
+
+struct LoopTransport : Transport {
+  qt_ctx ctx;
+  LoopHub* hub;
+  std::vector<std::shared_ptr<LoopHub::Msg>> posted;
+  std::vector<std::tuple<void*, size_t, int>> pending;
+  LoopTransport(qt_ctx c, LoopHub* h) : ctx(c), hub(h) {}
+  void allgather_i64(const int64_t* send_host, int64_t* recv_host, int count) override {
+    std::unique_lock<std::mutex> lk(hub->mu);
+    // wait until the previous allgather has been fully consumed
+    hub->cv.wait(lk, [&] { return hub->ag_left == 0; });
+    if (hub->ag_arrived == 0) {
+      hub->ag.assign((size_t)count * hub->P, 0);
+      hub->ag_count = count;
+    }
+    if (hub->ag_count != count) fail(QT_ESTATE, "loopback allgather size mismatch");
+    for (int i = 0; i < count; ++i) hub->ag[(size_t)ctx->rank * count + i] = send_host[i];
+    uint64_t gen = hub->ag_gen;
+    if (++hub->ag_arrived == hub->P) {
+      hub->ag_arrived = 0;
+      hub->ag_left = hub->P;
+      ++hub->ag_gen;
+      hub->cv.notify_all();
+    } else {
+      hub->cv.wait(lk, [&] { return hub->ag_gen != gen; });
+    }
+    for (size_t i = 0; i < hub->ag.size(); ++i) recv_host[i] = hub->ag[i];
+    if (--hub->ag_left == 0) hub->cv.notify_all();
+  }
+  void group_start() override {
+    posted.clear();
+    pending.clear();
+  }
+  void send(const void* buf, size_t bytes, int peer) override {
+    auto m = std::make_shared<LoopHub::Msg>();
+    m->src = buf;
+    m->bytes = bytes;
+    QT_CUDA(cudaEventCreateWithFlags(&m->ready, cudaEventDisableTiming));
+    QT_CUDA(cudaEventCreateWithFlags(&m->done, cudaEventDisableTiming));
+    QT_CUDA(cudaEventRecord(m->ready, ctx->stream));
+    {
+      std::lock_guard<std::mutex> lk(hub->mu);
+      hub->q[(size_t)ctx->rank * hub->P + peer].push_back(m);
+    }
+    hub->cv.notify_all();
+    posted.push_back(m);
+  }
+  void recv(void* buf, size_t bytes, int peer) override { pending.emplace_back(buf, bytes, peer); }
+  void group_end() override {
+    // receives in program order per peer
+    for (auto& [buf, bytes, peer] : pending) {
+      std::shared_ptr<LoopHub::Msg> m;
+      {
+        std::unique_lock<std::mutex> lk(hub->mu);
+        auto& dq = hub->q[(size_t)peer * hub->P + ctx->rank];
+        hub->cv.wait(lk, [&] { return !dq.empty(); });
+        m = dq.front();
+        dq.pop_front();
+      }
+      if (m->bytes != bytes)
+        fail(QT_ESTATE, "loopback size mismatch: rank %d expects %zu bytes from %d, got %zu",
+             ctx->rank, bytes, peer, m->bytes);
+      QT_CUDA(cudaStreamWaitEvent(ctx->stream, m->ready, 0));
+      QT_CUDA(cudaMemcpyAsync(buf, m->src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+      QT_CUDA(cudaEventRecord(m->done, ctx->stream));
+      {
+        std::lock_guard<std::mutex> lk(hub->mu);
+        m->copied = true;
+      }
+      hub->cv.notify_all();
+    }
+    pending.clear();
+    // a send buffer may be reused only after the receiver's copy
+    for (auto& m : posted) {
+      {
+        std::unique_lock<std::mutex> lk(hub->mu);
+        hub->cv.wait(lk, [&] { return m->copied; });
+      }
+      QT_CUDA(cudaStreamWaitEvent(ctx->stream, m->done, 0));
+    }
+    QT_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (auto& m : posted) {
+      cudaEventDestroy(m->ready);
+      cudaEventDestroy(m->done);
+    }
+    posted.clear();
+  }
+};
+
+static Transport* T(qt_ctx ctx) { return static_cast<Transport*>(ctx->transport); }
+
+void dist_init(qt_ctx ctx, const void* uid) { ctx->transport = new NcclTransport(ctx, uid); }
+
+void dist_init_loopback(qt_ctx ctx, void* hub) {
+  LoopHub* h = static_cast<LoopHub*>(hub);
+  if (h->P != ctx->world) fail(QT_EINVAL, "hub for %d ranks, world is %d", h->P, ctx->world);
+  ctx->transport = new LoopTransport(ctx, h);
 }
 
 void dist_finalize(qt_ctx ctx) {
-  if (ctx->nccl_comm) nccl().CommDestroy(comm(ctx));
-  ctx->nccl_comm = nullptr;
+  delete T(ctx);
+  ctx->transport = nullptr;
 }
+
+void* loop_hub_create(int P) { return new LoopHub(P); }
+void loop_hub_destroy(void* h) { delete static_cast<LoopHub*>(h); }
 
 void allgather_i64(qt_ctx ctx, const int64_t* send_host, int64_t* recv_host, int count) {
-  NcclApi& N = nccl();
-  DevBuf s(8 * count, ctx->stream), r(8ll * count * ctx->world, ctx->stream);
-  QT_CUDA(cudaMemcpyAsync(s.p, send_host, 8 * count, cudaMemcpyHostToDevice, ctx->stream));
-  NCCL_CALL(N.AllGather(s.p, r.p, count, ncclInt64, comm(ctx), ctx->stream));
-  QT_CUDA(cudaMemcpyAsync(recv_host, r.p, 8ll * count * ctx->world, cudaMemcpyDeviceToHost,
-                          ctx->stream));
-  QT_CUDA(cudaStreamSynchronize(ctx->stream));
-}
-
-double allreduce_sum_f64(qt_ctx ctx, double v) {
-  NcclApi& N = nccl();
-  DevBuf b(8, ctx->stream);
-  QT_CUDA(cudaMemcpyAsync(b.p, &v, 8, cudaMemcpyHostToDevice, ctx->stream));
-  NCCL_CALL(N.AllReduce(b.p, b.p, 1, ncclFloat64, ncclSum, comm(ctx), ctx->stream));
-  double r;
-  QT_CUDA(cudaMemcpyAsync(&r, b.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  QT_CUDA(cudaStreamSynchronize(ctx->stream));
-  return r;
+  T(ctx)->allgather_i64(send_host, recv_host, count);
 }
 
 // ------------------------------------------------------------------ kernels
@@ -440,7 +587,7 @@ qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S) {
   cudaStream_t st = ctx->stream;
   const int P = ctx->world, g = ctx->rank;
   if (A->bounds != B->bounds) fail(QT_EINVAL, "A and B must have the same block-row bounds");
-  NcclApi& N = nccl();
+  Transport* X = T(ctx);
   const size_t bb = 1024 * elem_size(A->dtype);
   QT_CUDA(cudaEventRecord(ctx->ev[5], st));
   const int32_t lo = A->row_lo, hi = A->row_hi;
@@ -463,16 +610,16 @@ qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S) {
   for (int r = 0; r < P; ++r) in_off[r + 1] = in_off[r] + (r == g ? 0 : M[(size_t)r * P + g]);
   int64_t n_in = in_off[P];
   DevBuf d_in_rows(4 * std::max<int64_t>(n_in, 1), st);
-  NCCL_CALL(N.GroupStart());
+  X->group_start();
   for (int q = 0; q < P; ++q) {
     if (q == g) continue;
     if (my_counts[q] > 0)
-      NCCL_CALL(N.Send(d_req.as<int32_t>() + seg_off[q], my_counts[q], ncclInt32, q, comm(ctx), st));
+      X->send(d_req.as<int32_t>() + seg_off[q], 4 * my_counts[q], q);
     int64_t cnt = M[(size_t)q * P + g];
     if (cnt > 0)
-      NCCL_CALL(N.Recv(d_in_rows.as<int32_t>() + in_off[q], cnt, ncclInt32, q, comm(ctx), st));
+      X->recv(d_in_rows.as<int32_t>() + in_off[q], 4 * cnt, q);
   }
-  NCCL_CALL(N.GroupEnd());
+  X->group_end();
   // 2. owner: block counts of the requested rows; requester: receive counts
   RowView v;
   build_row_view(B, v);
@@ -483,16 +630,16 @@ qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S) {
   rx.rows = std::move(d_req);
   rx.counts.alloc(4 * std::max<int64_t>(rx.nrows, 1), st);
   rx.offs.alloc(4 * (rx.nrows + 1), st);
-  NCCL_CALL(N.GroupStart());
+  X->group_start();
   for (int q = 0; q < P; ++q) {
     if (q == g) continue;
     int64_t cnt_out = M[(size_t)q * P + g];
     if (cnt_out > 0)
-      NCCL_CALL(N.Send(d_out_counts.as<int32_t>() + in_off[q], cnt_out, ncclInt32, q, comm(ctx), st));
+      X->send(d_out_counts.as<int32_t>() + in_off[q], 4 * cnt_out, q);
     if (my_counts[q] > 0)
-      NCCL_CALL(N.Recv(rx.counts.as<int32_t>() + seg_off[q], my_counts[q], ncclInt32, q, comm(ctx), st));
+      X->recv(rx.counts.as<int32_t>() + seg_off[q], 4 * my_counts[q], q);
   }
-  NCCL_CALL(N.GroupEnd());
+  X->group_end();
   // offsets on both sides (host copies decide the message sizes)
   std::vector<int32_t> h_out_counts(n_in), h_in_counts(rx.nrows);
   if (n_in > 0) {
@@ -516,24 +663,24 @@ qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S) {
   rx.cols.alloc(4 * std::max<int64_t>(rx.nblk, 1), st);
   rx.payload.alloc(bb * std::max<int64_t>(rx.nblk, 1), st);
   int64_t sent_payload = 0, sent_meta = 0;
-  NCCL_CALL(N.GroupStart());
+  X->group_start();
   for (int q = 0; q < P; ++q) {
     if (q == g) continue;
     int64_t r0 = in_off[q], r1 = in_off[q + 1];
     int64_t b0 = h_out_offs[r0], b1 = h_out_offs[r1];
     if (b1 > b0) {
-      NCCL_CALL(N.Send(d_out_cols.as<int32_t>() + b0, b1 - b0, ncclInt32, q, comm(ctx), st));
-      NCCL_CALL(N.Send((char*)d_out_pay.p + b0 * bb, (b1 - b0) * bb, ncclInt8, q, comm(ctx), st));
+      X->send(d_out_cols.as<int32_t>() + b0, 4 * (b1 - b0), q);
+      X->send((char*)d_out_pay.p + b0 * bb, (b1 - b0) * bb, q);
       sent_payload += (b1 - b0) * bb;
     }
     sent_meta += 4 * (r1 - r0) + 4 * (b1 - b0);
     int64_t i0 = h_in_offs[seg_off[q]], i1 = h_in_offs[seg_off[q] + my_counts[q]];
     if (i1 > i0) {
-      NCCL_CALL(N.Recv(rx.cols.as<int32_t>() + i0, i1 - i0, ncclInt32, q, comm(ctx), st));
-      NCCL_CALL(N.Recv((char*)rx.payload.p + i0 * bb, (i1 - i0) * bb, ncclInt8, q, comm(ctx), st));
+      X->recv(rx.cols.as<int32_t>() + i0, 4 * (i1 - i0), q);
+      X->recv((char*)rx.payload.p + i0 * bb, (i1 - i0) * bb, q);
     }
   }
-  NCCL_CALL(N.GroupEnd());
+  X->group_end();
   qt_mat Bx = make_b_ext(B, rx);
   QT_CUDA(cudaEventRecord(ctx->ev[6], st));
   fill_exchange_stats(S, rx, bb);

@@ -88,7 +88,7 @@ struct qt_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   int rank = 0, world = 1;
-  void* nccl_comm = nullptr;
+  void* transport = nullptr;  // qt::Transport (NCCL or loopback), world > 1
   int num_sms = 148;
   int64_t launches = 0;
   cudaEvent_t ev[8] = {};
@@ -175,6 +175,9 @@ void launch_fp64_peak(qt_ctx ctx, int kind, int iters, int grid);
 
 // ----- distributed (qt_dist.cu)
 void dist_init(qt_ctx ctx, const void* uid);
+void dist_init_loopback(qt_ctx ctx, void* hub);
+void* loop_hub_create(int P);
+void loop_hub_destroy(void* hub);
 void nccl_unique_id(void* out128);
 void dist_finalize(qt_ctx ctx);
 qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* st);
@@ -182,6 +185,5 @@ qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* st);
 // the NCCL transfers); A and B are whole matrices on this context.
 qt_mat multiply_virtual(qt_mat A, qt_mat B, const int32_t* bounds, int P, int g, qt_stats* st);
 void allgather_i64(qt_ctx ctx, const int64_t* send_host, int64_t* recv_host, int count);
-double allreduce_sum_f64(qt_ctx ctx, double v);
 
 }  // namespace qt

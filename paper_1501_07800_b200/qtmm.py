@@ -74,6 +74,9 @@ def _load():
         "qt_read_back": [P, P, P, P],
         "qt_destroy": [P],
         "qt_fp64_peak": [P, ctypes.c_int, ctypes.c_float, P],
+        "qt_loopback_hub_create": [i32, P],
+        "qt_loopback_hub_destroy": [P],
+        "qt_ctx_create_loopback": [ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -89,7 +92,8 @@ def _load():
 _lib = _load()
 EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_nccl_unique_id", "qt_create", "qt_multiply",
             "qt_multiply_virtual", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
-            "qt_destroy", "qt_last_error", "qt_kernel_launches", "qt_fp64_peak")
+            "qt_destroy", "qt_last_error", "qt_kernel_launches", "qt_fp64_peak",
+            "qt_loopback_hub_create", "qt_loopback_hub_destroy", "qt_ctx_create_loopback")
 
 
 def _check(status: int):
@@ -124,7 +128,9 @@ def _dtype_code(vals) -> int:
 class Context:
     """One per process (rank): device, stream and (world > 1) NCCL communicator."""
 
-    def __init__(self, device: int = 0, stream=None, process_group=None):
+    def __init__(self, device: int = 0, stream=None, process_group=None, loopback=None):
+        """``loopback=(hub, rank, world)``: a rank thread of the single-device
+        loopback transport (testing only, see LoopbackHub)."""
         import torch
         self.device = device
         if stream is None:
@@ -133,6 +139,12 @@ class Context:
         sptr = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
         rank, world = 0, 1
         uid = None
+        if loopback is not None:
+            hub, rank, world = loopback
+            h = ctypes.c_void_p()
+            _check(_lib.qt_ctx_create_loopback(device, sptr, rank, world, hub.handle, ctypes.byref(h)))
+            self.rank, self.world, self._h = rank, world, h
+            return
         if process_group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()):
             import torch.distributed as dist
             world = dist.get_world_size(process_group)
@@ -173,6 +185,22 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+class LoopbackHub:
+    """Shared state of the single-device loopback transport (testing the
+    multi-rank path with rank threads on one GPU)."""
+
+    def __init__(self, world: int):
+        h = ctypes.c_void_p()
+        _check(_lib.qt_loopback_hub_create(world, ctypes.byref(h)))
+        self.handle = h
+        self.world = world
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _check(_lib.qt_loopback_hub_destroy(self.handle))
+            self.handle = None
 
 
 class Matrix:

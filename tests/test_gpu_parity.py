@@ -346,3 +346,75 @@ def test_truncate_matches_oracle(qt, ctx, tau):
     r, c, v = A.truncate(tau).to_blocks()
     rr, rc, rv = oracle.truncate(Mm.brow, Mm.bcol, Mm.vals, tau)
     assert np.array_equal(r, rr) and np.array_equal(c, rc) and np.array_equal(v, rv)
+
+
+# ----------------------------------------------------------------- loopback ranks (the NCCL code path)
+
+
+def _loopback_run(qt, P, c, bounds):
+    import threading
+    import torch
+    Am = c["A"]
+    hub = qt.LoopbackHub(P)
+    out = [None] * P
+    errs = []
+
+    def rank_fn(g):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            ctx = qt.Context(0, stream=s, loopback=(hub, g, P))
+            m = (Am.brow >= bounds[g]) & (Am.brow < bounds[g + 1])
+            A = qt.Matrix.from_blocks(ctx, Am.n, Am.leaf_dim, 32, Am.brow[m], Am.bcol[m], Am.vals[m],
+                                      row_bounds=bounds)
+            C, st = A.multiply(A)
+            out[g] = (C.to_blocks(), st.as_dict(), A.info(), C.info())
+            C.close()
+            A.close()
+            ctx.close()
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=rank_fn, args=(g,)) for g in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    hub.close()
+    assert not errs, errs
+    return out
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_loopback_ranks_nccl_path(qt, ctx, P):
+    c = qtgen.config(5, P=P, small=True)
+    Am = c["A"]
+    full = (mk(qt, ctx, Am) @ mk(qt, ctx, Am)).to_blocks()
+    per = Am.nbr // P
+    bounds = [g * per for g in range(P)] + [Am.nbr]
+    plan = oracle.exchange_plan(bounds, (Am.brow, Am.bcol), (Am.brow, Am.bcol), 8192)
+    out = _loopback_run(qt, P, c, bounds)
+    for g in range(P):
+        (r, cc, v), st, ainfo, cinfo = out[g]
+        m = (full[0] >= bounds[g]) & (full[0] < bounds[g + 1])
+        assert np.array_equal(r, full[0][m]) and np.array_equal(cc, full[1][m])
+        assert np.array_equal(v, full[2][m])                  # bitwise across P
+        assert st["bytes_recv_payload"] == plan[g]["payload_bytes"]
+        assert st["bytes_recv_meta"] == plan[g]["meta_bytes"]
+        assert ainfo["global_nblocks"] == Am.nb
+        assert (cinfo["row_lo"], cinfo["row_hi"]) == (bounds[g], bounds[g + 1])
+    # what each rank sent = what the others received from it
+    sent = sum(o[1]["bytes_sent_payload"] for o in out)
+    assert sent == sum(p["payload_bytes"] for p in plan)
+
+
+def test_loopback_cfg4_small_two_ranks(qt, ctx):
+    c = qtgen.config(4, small=True)
+    Am = c["A"]
+    full = (mk(qt, ctx, Am) @ mk(qt, ctx, Am)).to_blocks()
+    bounds = [0, Am.nbr // 3, Am.nbr]   # uneven strips
+    out = _loopback_run(qt, 2, c, bounds)
+    for g in range(2):
+        (r, cc, v), st, _, _ = out[g]
+        m = (full[0] >= bounds[g]) & (full[0] < bounds[g + 1])
+        assert np.array_equal(r, full[0][m]) and np.array_equal(v, full[2][m])
