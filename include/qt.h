@@ -106,7 +106,7 @@ qt_status qt_nccl_unique_id(void* out128);
  * device pointers; order of blocks is arbitrary.  Zero submatrices are never
  * stored: only the listed blocks exist, a listed all-zero block is
  * kept (reading C-2).
- * The quadtree is uniform: 2^L x 2^L blocks with 2^L >= max(2, ceil(n/bs)),
+ * The quadtree is uniform: 2^L x 2^L blocks with 2^L >= max(4, ceil(n/bs)),
  * padded children are NIL (reading C-3); the leaf level is
  * L - log2(leaf_dim/bs) (leaves are block-sparse submatrices, §4.1).
  * Requirements: block_size == 32 (the built kernels), leaf_dim a power-of-two

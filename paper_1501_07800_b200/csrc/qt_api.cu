@@ -174,7 +174,7 @@ qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
     M->bs = block_size;
     M->dtype = dtype;
     M->nbr = (int32_t)nbr;
-    int L = 1;
+    int L = 2;  // at least 4x4 blocks (reading C-3): the FP32 kernel tiles 4x4 blocks
     while ((1ll << L) < nbr) ++L;
     M->L = L;
     M->leaf_level = std::max(0, L - ilog2(leaf_dim / block_size));

@@ -42,4 +42,14 @@ __host__ __device__ inline uint32_t morton_col(uint64_t k) { return compact_bits
 // minimum for 256 bytes), and the accumulator pairs stay 16-byte contiguous.
 __host__ __device__ inline int swz64(int r, int c) { return r * 32 + (c ^ ((r & 3) << 2)); }
 
+// Internal FP32 block layout (32x32): rows of 128 bytes, the eight 16-byte
+// chunks of row r XOR-permuted by (r & 7) — the canonical 128-byte swizzle of
+// the tcgen05 shared-memory descriptors.  A 4 KiB block copied unchanged to a
+// 1024-byte-aligned smem address is then, at once, a K-major SW128 tile of the
+// A operand (rows = M, 32 fp32 of K per row) and an MN-major SW128 tile of the
+// B operand (rows = K, 32 fp32 of N per row): one pool serves both operands.
+__host__ __device__ inline int swz32(int r, int c) {
+  return r * 32 + ((((c >> 2) ^ (r & 7)) << 2) | (c & 3));
+}
+
 }  // namespace qt

@@ -58,7 +58,7 @@ __global__ void k_fill_pool(const T* __restrict__ vals, const int32_t* __restric
       int r = e >> 5, c = e & 31;
       T v = src[e];
       if (sizeof(T) == 8) dst[swz64(r, c)] = v;
-      else dst[e] = v;
+      else dst[swz32(r, c)] = v;
     }
   }
 }
@@ -123,7 +123,7 @@ __global__ void k_unpack(const T* __restrict__ pool, const uint64_t* __restrict_
 #pragma unroll
     for (int e = threadIdx.x; e < 1024; e += 256) {
       int r = e >> 5, c = e & 31;
-      dst[e] = (sizeof(T) == 8) ? src[swz64(r, c)] : src[e];
+      dst[e] = (sizeof(T) == 8) ? src[swz64(r, c)] : src[swz32(r, c)];
     }
   }
 }

@@ -174,7 +174,7 @@ def test_disjoint_k_gives_empty(qt, ctx):
                               np.ones((1, 32, 32)))
     C, st = A.multiply(B)
     assert C.nblocks == 0 and st.block_products == 0
-    assert C.level_nodes() == [0, 0]
+    assert C.level_nodes() == [0, 0, 0]
 
 
 def test_errors(qt, ctx):

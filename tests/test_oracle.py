@@ -207,7 +207,8 @@ def test_tree_levels_configs():
     assert oracle.tree_levels(32768, 32, 2048) == (10, 4)    # cfg3
     assert oracle.tree_levels(98304, 32, 4096) == (12, 5)    # cfg4 (padded to 4096 blocks)
     assert oracle.tree_levels(4, 1, 2) == (2, 1)
-    assert oracle.tree_levels(32, 32, 32) == (1, 1)          # single block: L >= 1
+    assert oracle.tree_levels(32, 32, 32) == (2, 2)          # single block: padded to 4x4 (L >= 2)
+    assert oracle.tree_levels(128, 32, 64) == (2, 1)
 
 
 def test_dense_two_level_spec_s90():
@@ -218,7 +219,7 @@ def test_dense_two_level_spec_s90():
     assert counts[: leaf + 1] == g["dense_two_level"]["levels"]
 
 
-@pytest.mark.parametrize("L", [1, 3, 5])
+@pytest.mark.parametrize("L", [2, 3, 5])
 def test_dense_counts_are_8_pow_l(L):
     br, bc = qtgen.pattern_dense(1 << L)
     assert oracle.level_task_counts(L, (br, bc), (br, bc)) == [8 ** l for l in range(L + 1)]
