@@ -86,6 +86,8 @@ static void ctx_create(int device, void* cuda_stream, int rank, int world, const
     QT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     c->counters.alloc(256, c->stream);
     QT_CUDA(cudaMemsetAsync(c->counters.p, 0, 256, c->stream));
+    c->zeros.alloc(8192, c->stream);
+    QT_CUDA(cudaMemsetAsync(c->zeros.p, 0, 8192, c->stream));
     c->pinned_bytes = 256;
     QT_CUDA(cudaMallocHost(&c->pinned, c->pinned_bytes));
     if (world > 1) {
@@ -140,6 +142,7 @@ qt_status qt_ctx_destroy(qt_ctx ctx) {
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   ctx->scratch.release();
   ctx->counters.release();
+  ctx->zeros.release();
   cudaStreamSynchronize(ctx->stream);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;

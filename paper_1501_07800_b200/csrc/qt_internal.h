@@ -94,6 +94,7 @@ struct qt_ctx_s {
   cudaEvent_t ev[8] = {};
   qt::DevBuf scratch;  // cub temp storage, grown on demand
   qt::DevBuf counters; // small device counters (scheduler, errors)
+  qt::DevBuf zeros;    // one zero block (8 KiB) for absent tcgen05 operands
   void* pinned = nullptr;  // small pinned host staging area
   size_t pinned_bytes = 0;
 };
@@ -171,6 +172,28 @@ struct NumericArgs {
   int* counter;              // tile scheduler counter (zeroed before launch)
 };
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a);
+
+// FP32 (tcgen05 kind::tf32, 3xTF32): tiles are C nodes at level L-2 (4x4 blocks)
+struct NumericArgs32 {
+  int64_t ntiles;            // C nodes at level L-2
+  const int32_t* tile_start; // [ntiles+1] task ranges at level L-2
+  const int32_t* pa;         // A node (level L-2) per task
+  const int32_t* pb;         // B node (level L-2) per task
+  const int4* childA2;       // A child tables at levels L-2 and L-1
+  const int4* childA1;
+  const int4* childB2;
+  const int4* childB1;
+  const int4* childC2;       // C child tables: level L-2 -> quads, level L-1 -> blocks
+  const int4* childC1;
+  const void* poolA;
+  const void* poolB;
+  const void* poolB2;
+  int64_t splitB;
+  void* poolC;
+  const void* zeros;         // one zero block (absent operands)
+  int* counter;
+};
+void launch_numeric_f32(qt_ctx ctx, const NumericArgs32& a);
 void launch_fp64_peak(qt_ctx ctx, int kind, int iters, int grid);
 
 // ----- distributed (qt_dist.cu)

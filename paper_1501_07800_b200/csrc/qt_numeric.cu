@@ -315,7 +315,7 @@ __global__ void k_peak_dfma(double* out, int iters) {
 }  // namespace
 
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a) {
-  if (dt != QT_F64) fail(QT_EDTYPE, "the FP32 numeric kernel is not built yet");
+  if (dt != QT_F64) fail(QT_EDTYPE, "launch_numeric is the FP64 kernel");
   static bool attr_set = false;
   if (!attr_set) {
     QT_CUDA(cudaFuncSetAttribute(k_numeric_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,0 +1,505 @@
+// FP32 numeric block-sparse multiply on the 5th-generation tensor cores
+// (tcgen05.mma kind::tf32, accumulators in TMEM) with the 3xTF32 split.
+//
+// Paper: the leaf multiply of §4.1 in single precision (the paper
+// benchmarks both precisions).  Reading C-9: inputs are FP32, the
+// result must be within 1e-5 relative Frobenius of the double product of the
+// FP32 inputs; one TF32 product per term is ~2.5e-4 off, so each product is
+// a_hi*b_hi + a_hi*b_lo + a_lo*b_hi with x_hi = tf32(x), x_lo = tf32(x - x_hi)
+// (error ~2^-22 per term, FP32 accumulation in TMEM).
+//
+// Work item ("tile") = one C node at level L-2: 4x4 C blocks = a 128x128 FP32
+// accumulator in TMEM (128 lanes x 128 columns; two tiles double-buffered = 256
+// columns).  A step of the tile is one inner block index k: the A column
+// A(I0..I3, k) (a 128x32 K-major operand) and the B row B(k, J0..J3) (a 32x128
+// MN-major operand) — absent blocks are copied from a zero block — staged by
+// eight 4 KiB cp.async.bulk copies into a 1024-byte-aligned stage.  Because
+// the pool stores every FP32 block in the canonical 128-byte swizzle
+// (qt_common.cuh swz32), the same bytes are a valid SW128 descriptor target
+// for both operands.  Per step: 4 K-slices x 3 MMAs (M=128, N=128, K=8).
+//
+// Warp roles (320 threads, one CTA per SM, persistent over tiles):
+//   warps 0-3 epilogue  TMEM -> registers (tcgen05.ld 32x32b) -> C pool
+//   warps 4-7 split     fp32 -> (tf32 hi in place, tf32 lo copy) per stage
+//   warp 8    producer  task metadata + TMA bulk copies
+//   warp 9    MMA       one elected lane issues tcgen05.mma / commit
+// Each C block is written once by one thread row-set: no atomics; summation
+// order per element is fixed (ascending k, and within a k the fixed K-slice
+// and hi/lo order), so results are run-to-run deterministic.
+#include <cuda_runtime.h>
+
+#include "qt_common.cuh"
+#include "qt_internal.h"
+
+namespace qt {
+
+namespace {
+
+constexpr int kStages = 3;
+constexpr int kBlkBytes = 4096;                 // 32x32 fp32
+constexpr int kHiBytes = 8 * kBlkBytes;         // A_hi[4] | B_hi[4]
+constexpr int kStageBytes = 2 * kHiBytes;       // + A_lo[4] | B_lo[4]  = 64 KiB
+constexpr int kThreads = 320;
+// TMEM: two tile buffers (double-buffered epilogue) x two accumulators x 128
+// columns = 512 columns.  The hi*hi products go to one accumulator, the two
+// cross terms (2^-11 smaller) to the other; the epilogue adds them with a
+// round-to-nearest FADD.  The tensor core's own accumulation into D is not
+// round-to-nearest, so its error grows with the number of MMAs that add into
+// one large accumulator: measured on config 5 (65 k-steps), one accumulator
+// for all 12 MMAs per step gave 1.02e-5 relative Frobenius error, even/odd
+// k-step accumulators 5.1e-6; the hi*hi / cross split leaves 4 MMAs per step
+// on the large accumulator.
+constexpr int kTmemCols = 512;
+
+enum : int { F_FIRST = 1, F_END = 2, F_DONE = 4 };
+
+struct __align__(16) Hdr {
+  int tile;
+  int flags;
+  int pad[2];
+};
+
+struct Smem {
+  Hdr hdr[kStages];
+  int acc_tile[2];
+  uint32_t tmem_base;
+  uint32_t pad;
+  uint64_t full[kStages];   // TMA landed (1 arrival + tx)
+  uint64_t conv[kStages];   // hi/lo split done (4 warp arrivals)
+  uint64_t empty[kStages];  // MMAs that read the stage done (tcgen05.commit)
+  uint64_t tfull[2];        // accumulator ready (commit + MMA-lane arrive)
+  uint64_t tempty[2];       // epilogue drained the accumulator (4 warp arrivals)
+};
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + sizeof(Smem);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem], kind::tf32
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// Shared-memory matrix descriptor (tcgen05): start >> 4 in [0,14), leading
+// byte offset >> 4 in [16,30), stride byte offset >> 4 in [32,46), version 1
+// at [46,48), layout type at [61,64).  (Measured with tools/tc_probe.cu: an
+// MN-major tf32 operand in the plain SWIZZLE_128B layout reads as zeros; the
+// 32-byte-atom variant SWIZZLE_128B_BASE32B with 4-row K atoms is exact.)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                          uint64_t layout) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (layout << 61);
+}
+constexpr uint64_t kSW128 = 2;         // K-major A: 16-byte chunks ^ (row & 7)
+constexpr uint64_t kSW128_32B = 1;     // MN-major B (32-bit types): 32-byte chunks ^ (row & 3)
+
+// Instruction descriptor: D f32 (bits 4-5 = 1), A tf32 (7-9 = 2), B tf32
+// (10-12 = 2), A K-major (15 = 0), B MN-major (16 = 1), N>>3 at 17, M>>4 at 24.
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
+                            ((128u >> 3) << 17) | ((128u >> 4) << 24);
+
+__global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* data = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  Smem& S = *reinterpret_cast<Smem*>(data + (size_t)kStages * kStageBytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.conv[s], 4);
+      mbar_init(&S.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.tfull[b], 2);
+      mbar_init(&S.tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&S.tmem_base)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ producer
+    const float* poolA = static_cast<const float*>(a.poolA);
+    const float* poolB = static_cast<const float*>(a.poolB);
+    const float* poolB2 = static_cast<const float*>(a.poolB2);
+    const float* zeros = static_cast<const float*>(a.zeros);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (;;) {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(a.counter, 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= a.ntiles) {
+        mbar_wait(&S.empty[stage], phase ^ 1);
+        if (lane == 0) {
+          S.hdr[stage].tile = -1;
+          S.hdr[stage].flags = F_DONE;
+          mbar_arrive(&S.full[stage]);
+        }
+        break;
+      }
+      const int p0 = a.tile_start[t], p1 = a.tile_start[t + 1];
+      bool first = true;
+      for (int pb0 = p0; pb0 < p1; pb0 += 32) {
+        const int p = pb0 + lane;
+        // this lane's task: A blocks A(i, kk) and B blocks B(kk, j), i, kk, j in 0..3
+        int ab[4][4], bb[4][4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) ab[x][y] = bb[x][y] = -1;
+        if (p < p1) {
+          const int4 qa = a.childA2[a.pa[p]];  // A quads (i', k') in slot 2i'+k'
+          const int4 qb = a.childB2[a.pb[p]];  // B quads (k', j') in slot 2k'+j'
+          const int qa_[4] = {qa.x, qa.y, qa.z, qa.w};
+          const int qb_[4] = {qb.x, qb.y, qb.z, qb.w};
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const int hi = s >> 1, lo = s & 1;
+            if (qa_[s] >= 0) {
+              const int4 c = a.childA1[qa_[s]];  // (i'', k'') in slot 2i''+k''
+              ab[2 * hi + 0][2 * lo + 0] = c.x;
+              ab[2 * hi + 0][2 * lo + 1] = c.y;
+              ab[2 * hi + 1][2 * lo + 0] = c.z;
+              ab[2 * hi + 1][2 * lo + 1] = c.w;
+            }
+            if (qb_[s] >= 0) {
+              const int4 c = a.childB1[qb_[s]];  // (k'', j'') in slot 2k''+j''
+              bb[2 * hi + 0][2 * lo + 0] = c.x;
+              bb[2 * hi + 0][2 * lo + 1] = c.y;
+              bb[2 * hi + 1][2 * lo + 0] = c.z;
+              bb[2 * hi + 1][2 * lo + 1] = c.w;
+            }
+          }
+        }
+        const int nloc = min(32, p1 - pb0);
+        for (int u = 0; u < nloc; ++u) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            int ac[4], br[4];
+            bool anyA = false, anyB = false;
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              ac[x] = __shfl_sync(0xffffffffu, ab[x][kk], u);
+              br[x] = __shfl_sync(0xffffffffu, bb[kk][x], u);
+              anyA |= ac[x] >= 0;
+              anyB |= br[x] >= 0;
+            }
+            if (!(anyA && anyB)) continue;
+            mbar_wait(&S.empty[stage], phase ^ 1);
+            if (lane == 0) {
+              S.hdr[stage].tile = t;
+              S.hdr[stage].flags = first ? F_FIRST : 0;
+              mbar_arrive_expect_tx(&S.full[stage], 8u * kBlkBytes);
+              uint8_t* dst = data + (size_t)stage * kStageBytes;
+#pragma unroll
+              for (int x = 0; x < 4; ++x) {
+                const float* srcA = ac[x] >= 0 ? poolA + (size_t)ac[x] * 1024 : zeros;
+                bulk_g2s(dst + x * kBlkBytes, srcA, kBlkBytes, &S.full[stage]);
+                const int b = br[x];
+                const float* srcB = b < 0 ? zeros
+                                          : (b < a.splitB ? poolB + (size_t)b * 1024
+                                                          : poolB2 + (size_t)(b - a.splitB) * 1024);
+                bulk_g2s(dst + (4 + x) * kBlkBytes, srcB, kBlkBytes, &S.full[stage]);
+              }
+            }
+            __syncwarp();
+            first = false;
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+      // end-of-tile marker (no data)
+      mbar_wait(&S.empty[stage], phase ^ 1);
+      if (lane == 0) {
+        S.hdr[stage].tile = t;
+        S.hdr[stage].flags = F_END;
+        mbar_arrive(&S.full[stage]);
+      }
+      __syncwarp();
+      if (++stage == kStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------ hi/lo split
+    // Each warp owns whole 1 KiB swizzle atoms (8 rows x 128 B = 64 float4),
+    // two float4 per lane.  A atoms keep their layout (K-major SW128: hi in
+    // place, lo at the same offset of the lo area).  B atoms are re-laid out
+    // for the MN-major operand, which for 32-bit types is the 128-byte swizzle
+    // with 32-byte atoms (layout type SWIZZLE_128B_BASE32B): 16-byte chunk c of
+    // row r moves from c ^ (r&7) to ((c>>1 ^ (r&3))<<1 | (c&1)) — in place,
+    // after all lanes of the warp have read the atom.
+    const int cw = warp - 4;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (;;) {
+      mbar_wait(&S.full[stage], phase);
+      const int flags = S.hdr[stage].flags;
+      if (!(flags & (F_END | F_DONE))) {
+        float4* hi = reinterpret_cast<float4*>(data + (size_t)stage * kStageBytes);
+        float4* lo = reinterpret_cast<float4*>(data + (size_t)stage * kStageBytes + kHiBytes);
+#pragma unroll 1
+        for (int atom = cw; atom < 32; atom += 4) {  // atoms 0-15: A, 16-31: B
+          const bool isB = atom >= 16;
+          float4 x[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) x[h] = hi[atom * 64 + lane + 32 * h];
+          __syncwarp();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int f = lane + 32 * h;
+            int t = f;
+            if (isB) {
+              const int r = f >> 3, c16 = (f & 7) ^ r;
+              t = r * 8 + ((((c16 >> 1) ^ (r & 3)) << 1) | (c16 & 1));
+            }
+            float4 hv, lv;
+            hv.x = tf32_rna(x[h].x);
+            hv.y = tf32_rna(x[h].y);
+            hv.z = tf32_rna(x[h].z);
+            hv.w = tf32_rna(x[h].w);
+            lv.x = tf32_rna(x[h].x - hv.x);
+            lv.y = tf32_rna(x[h].y - hv.y);
+            lv.z = tf32_rna(x[h].z - hv.z);
+            lv.w = tf32_rna(x[h].w - hv.w);
+            hi[atom * 64 + t] = hv;
+            lo[atom * 64 + t] = lv;
+          }
+        }
+        fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.conv[stage]);
+      if (flags & F_DONE) break;
+      if (++stage == kStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    bool started = false;
+    const uint32_t sbase = smem_u32(data);
+    for (;;) {
+      mbar_wait(&S.conv[stage], phase);
+      const int flags = S.hdr[stage].flags;
+      const int tile = S.hdr[stage].tile;
+      if (flags & F_DONE) {
+        mbar_wait(&S.tempty[acc], acc_phase ^ 1);
+        if (lane == 0) {
+          S.acc_tile[acc] = -1;
+          mbar_arrive(&S.tfull[acc]);
+          mbar_arrive(&S.tfull[acc]);
+        }
+        break;
+      }
+      if (flags & F_END) {
+        // a tile whose tasks produce no block product has no data step: still
+        // wait for the buffer before publishing its (empty) result
+        if (!started) mbar_wait(&S.tempty[acc], acc_phase ^ 1);
+        started = false;
+        if (lane == 0) {
+          S.acc_tile[acc] = tile;
+          tc_commit(&S.tfull[acc]);      // fires when every MMA of the tile is done
+          mbar_arrive(&S.tfull[acc]);    // publishes acc_tile
+          mbar_arrive(&S.empty[stage]);  // the marker stage carried no data
+        }
+        __syncwarp();
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      } else {
+        if (flags & F_FIRST) {
+          mbar_wait(&S.tempty[acc], acc_phase ^ 1);
+          started = true;
+        }
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t st = sbase + (uint32_t)stage * kStageBytes;
+          const uint32_t d_main = tmem + (uint32_t)acc * 256;  // hi*hi
+          const uint32_t d_cross = d_main + 128;                // hi*lo + lo*hi
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            // A: 128 rows x 32 fp32 K-major, SW128 (LBO 16 B unused, SBO 1024 B); K-slice j at +32 B
+            const uint64_t a_hi = sdesc(st + 32u * j, 16, 1024, kSW128);
+            const uint64_t a_lo = sdesc(st + kHiBytes + 32u * j, 16, 1024, kSW128);
+            // B: 32 rows (K) x 128 fp32 (N) MN-major, SW128 with 32-byte atoms (LBO 4096 B
+            // between the four 32-wide N atoms = blocks, SBO 512 B between 4-row K atoms);
+            // K-slice j (rows 8j..8j+7) at +1024 B
+            const uint64_t b_hi = sdesc(st + 4u * kBlkBytes + 1024u * j, 4096, 512, kSW128_32B);
+            const uint64_t b_lo = sdesc(st + kHiBytes + 4u * kBlkBytes + 1024u * j, 4096, 512, kSW128_32B);
+            const uint32_t acc_in = ((flags & F_FIRST) && j == 0) ? 0u : 1u;
+            tc_mma(d_cross, a_lo, b_hi, kIdesc, acc_in);
+            tc_mma(d_cross, a_hi, b_lo, kIdesc, 1u);
+            tc_mma(d_main, a_hi, b_hi, kIdesc, acc_in);
+          }
+          tc_commit(&S.empty[stage]);
+        }
+        __syncwarp();
+      }
+      if (++stage == kStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 0-3)
+    float* poolC = static_cast<float*>(a.poolC);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (;;) {
+      mbar_wait(&S.tfull[acc], acc_phase);
+      const int tile = S.acc_tile[acc];
+      if (tile < 0) break;
+      tc_fence_after();
+      const int4 q4 = a.childC2[tile];
+      const int i1 = warp >> 1, i2 = warp & 1;  // C block row i = warp = 2*i1 + i2
+#pragma unroll 1
+      for (int j = 0; j < 4; ++j) {
+        const int j1 = j >> 1, j2 = j & 1;
+        const int qs = 2 * i1 + j1;
+        const int quad = qs == 0 ? q4.x : qs == 1 ? q4.y : qs == 2 ? q4.z : q4.w;
+        int cb = -1;
+        if (quad >= 0) {
+          const int4 c4 = a.childC1[quad];
+          const int s = 2 * i2 + j2;
+          cb = s == 0 ? c4.x : s == 1 ? c4.y : s == 2 ? c4.z : c4.w;
+        }
+        uint32_t v[32], w[32];
+        const uint32_t taddr =
+            tmem + (uint32_t)acc * 256 + ((uint32_t)(warp * 32) << 16) + 32u * j;
+        tmem_ld32(taddr, v);        // hi*hi
+        tmem_ld32(taddr + 128, w);  // cross terms
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = __float_as_uint(__uint_as_float(w[c]) + __uint_as_float(v[c]));
+        if (cb >= 0) {
+          float* Cb = poolC + (size_t)cb * 1024;
+          const int r = lane;  // row of the C block
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float4 w = make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
+                                   __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3]));
+            *reinterpret_cast<float4*>(Cb + r * 32 + ((c ^ (r & 7)) << 2)) = w;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
+}  // namespace
+
+void launch_numeric_f32(qt_ctx ctx, const NumericArgs32& a) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmemBytes));
+    attr_set = true;
+  }
+  QT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), ctx->stream));
+  int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
+  k_numeric_f32<<<grid, kThreads, kSmemBytes, ctx->stream>>>(a);
+  QT_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace qt

@@ -341,8 +341,10 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       DevBuf ns_dev(4 * (L + 1), st);
       int32_t* nsd = ns_dev.as<int32_t>();
       // --- small levels in one CTA
+      const bool f32 = C->dtype == QT_F32;
       int l_end = 0;
       while (l_end < L - 1 && F[l_end + 1] <= kSmallMaxF) ++l_end;
+      if (f32) l_end = std::min(l_end, L - 2);  // the FP32 tiles need the level L-2 queue
       int64_t maxF = 1, maxNS = 1, maxF4 = 1;
       for (int l = 0; l <= l_end; ++l) {
         maxF = std::max(maxF, F[l]);
@@ -378,7 +380,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       DevBuf pa = std::move(sp[cb]), pb = std::move(sb[cb]), pc = std::move(sc[cb]);
       DevBuf cstart = std::move(scs[cb]), ckey = std::move(sck[cb]);
       // --- large levels, grid-wide, no host sync
-      DevBuf cchild;
+      DevBuf cchild, t2_pa, t2_pb, t2_cstart, cchild2;
       for (int l = l_end; l < L; ++l) {
         const bool last = (l == L - 1);
         const int32_t Fl = (int32_t)F[l], Fn = (int32_t)F[l + 1];
@@ -415,6 +417,12 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
                                                   pa2.as<int32_t>(), pb2.as<int32_t>(),
                                                   pc2.as<int32_t>());
         QT_LAUNCH_CHECK(ctx);
+        if (f32 && l == L - 2) {  // keep the level L-2 queue: the FP32 work items
+          t2_pa = std::move(pa);
+          t2_pb = std::move(pb);
+          t2_cstart = std::move(cstart);
+          cchild2 = std::move(gidx);
+        }
         pa = std::move(pa2);
         pb = std::move(pb2);
         pc = std::move(pc2);
@@ -443,7 +451,28 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       na.splitB = B->split;
       na.poolC = C->pool.p;
       na.counter = ctx->counters.as<int>() + 16;
-      if (C->nb > 0) launch_numeric(ctx, C->dtype, na);
+      if (C->nb > 0 && !f32) launch_numeric(ctx, C->dtype, na);
+      if (C->nb > 0 && f32) {
+        NumericArgs32 nb;
+        nb.ntiles = ns[L - 2];
+        nb.tile_start = t2_cstart.as<int32_t>();
+        nb.pa = t2_pa.as<int32_t>();
+        nb.pb = t2_pb.as<int32_t>();
+        nb.childA2 = A->child[L - 2].as<int4>();
+        nb.childA1 = A->child[L - 1].as<int4>();
+        nb.childB2 = B->child[L - 2].as<int4>();
+        nb.childB1 = B->child[L - 1].as<int4>();
+        nb.childC2 = cchild2.as<int4>();
+        nb.childC1 = cchild.as<int4>();
+        nb.poolA = A->pool_ptr();
+        nb.poolB = B->pool_ptr();
+        nb.poolB2 = B->pool2;
+        nb.splitB = B->split;
+        nb.poolC = C->pool.p;
+        nb.zeros = ctx->zeros.p;
+        nb.counter = ctx->counters.as<int>() + 16;
+        launch_numeric_f32(ctx, nb);
+      }
       QT_CUDA(cudaEventRecord(ctx->ev[4], st));
       QT_CUDA(cudaEventSynchronize(ctx->ev[4]));  // frontier buffers are released after this
     }

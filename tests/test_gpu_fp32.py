@@ -1,0 +1,163 @@
+"""FP32 path (tcgen05 kind::tf32, 3xTF32) parity with the oracle.  Needs a B200.
+
+Reading C-9: inputs are the FP32-rounded values; the oracle computes the
+double product of those rounded inputs; the bar is relative Frobenius error
+<= 1e-5 (BASELINE north star), and bit-exact results on small-integer inputs
+(pin P-12: every partial sum is an integer < 2^24, exact in FP32 and in the
+3xTF32 split)."""
+import numpy as np
+import pytest
+
+import oracle
+import qtgen
+
+pytestmark = pytest.mark.gpu
+REL_FRO_F32 = 1e-5
+
+
+@pytest.fixture(scope="module")
+def qt():
+    from paper_1501_07800_b200 import build
+    build.build()
+    from paper_1501_07800_b200 import qtmm
+    return qtmm
+
+
+@pytest.fixture(scope="module")
+def ctx(qt):
+    import torch
+    torch.cuda.init()
+    return qt.Context(0)
+
+
+def f32(M: qtgen.BlockMatrix):
+    return qtgen.BlockMatrix(M.n, M.leaf_dim, M.bs, M.brow, M.bcol, M.vals.astype(np.float32))
+
+
+def mk(qt, ctx, M):
+    return qt.Matrix.from_blocks(ctx, M.n, M.leaf_dim, M.bs, M.brow, M.bcol, M.vals)
+
+
+def ref64(M):
+    return (M.brow, M.bcol, M.vals.astype(np.float64))
+
+
+def random_bm(rng, nbr, p, kind, leaf):
+    mask = rng.random((nbr, nbr)) < p
+    br, bc = np.nonzero(mask)
+    if kind == "int":
+        v = rng.integers(-4, 5, size=(len(br), 32, 32)).astype(np.float32)
+    else:
+        v = rng.uniform(-1, 1, size=(len(br), 32, 32)).astype(np.float32)
+    return qtgen.BlockMatrix(nbr * 32, leaf, 32, br.astype(np.int32), bc.astype(np.int32), v)
+
+
+def check(got, ref, kind):
+    assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+    assert got[2].dtype == np.float32
+    if kind == "int":
+        assert np.array_equal(got[2].astype(np.float64), ref[2])
+    else:
+        d = got[2].astype(np.float64) - ref[2]
+        rel = np.linalg.norm(d) / np.linalg.norm(ref[2])
+        assert rel <= REL_FRO_F32, rel
+
+
+def test_fp32_hand_example_embedded(qt, ctx):
+    a = np.zeros((1, 32, 32), np.float32)
+    b = np.zeros((1, 32, 32), np.float32)
+    a[0, :2, :2] = [[1, 2], [3, 4]]
+    b[0, :2, :2] = [[5, 6], [7, 8]]
+    z = np.zeros(1, np.int32)
+    A = qt.Matrix.from_blocks(ctx, 32, 32, 32, z, z, a)
+    B = qt.Matrix.from_blocks(ctx, 32, 32, 32, z, z, b)
+    r, c, v = (A @ B).to_blocks()
+    assert list(r) == [0] and list(c) == [0]
+    assert np.array_equal(v[0, :2, :2], np.array([[19, 22], [43, 50]], np.float32))
+    assert np.all(v[0, 2:, :] == 0) and np.all(v[0, :, 2:] == 0)
+
+
+def test_fp32_roundtrip_layout(qt, ctx):
+    rng = np.random.default_rng(2)
+    M = random_bm(rng, 9, 0.5, "uniform", 64)
+    r, c, v = mk(qt, ctx, M).to_blocks()
+    o = np.lexsort((M.bcol, M.brow))
+    assert np.array_equal(v, M.vals[o])
+
+
+@pytest.mark.parametrize("nbr,p,leaf", [(1, 1.0, 32), (4, 1.0, 32), (5, 0.6, 64), (16, 0.3, 128),
+                                        (37, 0.2, 256), (64, 0.05, 512)])
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_fp32_random_patterns(qt, ctx, nbr, p, leaf, kind):
+    rng = np.random.default_rng(nbr * 11 + (kind == "int"))
+    Am = random_bm(rng, nbr, p, kind, leaf)
+    Bm = random_bm(rng, nbr, p, kind, leaf)
+    C, st = mk(qt, ctx, Am).multiply(mk(qt, ctx, Bm))
+    got = C.to_blocks()
+    ref = oracle.spgemm(nbr, 32, ref64(Am), ref64(Bm))
+    check(got, ref, kind)
+    L, _ = oracle.tree_levels(Am.n, 32, leaf)
+    assert list(st.level_tasks[: L + 1]) == oracle.level_task_counts(
+        L, (Am.brow, Am.bcol), (Bm.brow, Bm.bcol))
+
+
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_fp32_cfg1(qt, ctx, kind):
+    c = qtgen.config(1, kind)
+    Am, Bm = f32(c["A"]), f32(c["B"])
+    got = (mk(qt, ctx, Am) @ mk(qt, ctx, Bm)).to_blocks()
+    check(got, oracle.spgemm(16, 32, ref64(Am), ref64(Bm)), kind)
+
+
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_fp32_cfg5_small_full_oracle(qt, ctx, kind):
+    c = qtgen.config(5, kind, P=2, small=True)
+    Am = f32(c["A"])
+    A = mk(qt, ctx, Am)
+    got = (A @ A).to_blocks()
+    check(got, oracle.spgemm(Am.nbr, 32, ref64(Am), ref64(Am)), kind)
+
+
+def test_fp32_cfg5_full_size_sampled(qt, ctx):
+    c = qtgen.config(5, P=1)
+    Am = f32(c["A"])
+    A = mk(qt, ctx, Am)
+    C, st = A.multiply(A)
+    got = C.to_blocks()
+    assert st.block_products == 2048800 and st.c_blocks == 61888
+    for lo, hi in [(0, 6), (300, 306), (506, 512)]:
+        ref = oracle.spgemm(Am.nbr, 32, ref64(Am), ref64(Am), rows=(lo, hi))
+        m = (got[0] >= lo) & (got[0] < hi)
+        check((got[0][m], got[1][m], got[2][m]), ref, "uniform")
+
+
+def test_fp32_cfg4_small(qt, ctx):
+    c = qtgen.config(4, small=True)
+    Am = f32(c["A"])
+    A = mk(qt, ctx, Am)
+    check((A @ A).to_blocks(), oracle.spgemm(Am.nbr, 32, ref64(Am), ref64(Am)), "uniform")
+
+
+def test_fp32_run_to_run_bitwise(qt, ctx):
+    c = qtgen.config(5, P=2, small=True)
+    A = mk(qt, ctx, f32(c["A"]))
+    v0 = (A @ A).to_blocks()[2]
+    for _ in range(2):
+        assert np.array_equal((A @ A).to_blocks()[2], v0)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_fp32_virtual_ranks_bitwise(qt, ctx, P):
+    c = qtgen.config(5, P=P, small=True)
+    Am = f32(c["A"])
+    A = mk(qt, ctx, Am)
+    full = (A @ A).to_blocks()
+    per = Am.nbr // P
+    bounds = [g * per for g in range(P + 1)]
+    plan = oracle.exchange_plan(bounds, (Am.brow, Am.bcol), (Am.brow, Am.bcol), 4096)
+    for g in range(P):
+        Cg, st = A.multiply_virtual(A, P, g, bounds)
+        r, cc, v = Cg.to_blocks()
+        m = (full[0] >= bounds[g]) & (full[0] < bounds[g + 1])
+        assert np.array_equal(r, full[0][m]) and np.array_equal(v, full[2][m])
+        assert st.bytes_recv_payload == plan[g]["payload_bytes"]   # FP32 halves the payload

@@ -9,6 +9,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import qtgen  # noqa: E402
@@ -70,6 +71,32 @@ def main():
             run(ctx, stream, "cfg4 ES-like N=98304", qtgen.config(4), steps=10)
         elif w == "5":
             run(ctx, stream, "cfg5 P=1 banded N=16384 leaf 2048", qtgen.config(5, P=1))
+        elif w == "5f32":
+            c = qtgen.config(5, P=1)
+            M = c["A"]
+            M32 = qtgen.BlockMatrix(M.n, M.leaf_dim, 32, M.brow, M.bcol, M.vals.astype(np.float32))
+            out = run(ctx, stream, "cfg5 P=1 banded N=16384 leaf 2048 FP32 (3xTF32 tcgen05)",
+                      {"A": M32, "B": M32, "same": True})
+            if len(sys.argv) > 1 and "--err" in sys.argv:
+                pass
+        elif w == "dense4096f32":
+            br, bc = qtgen.pattern_dense(128)
+            v = qtgen.block_values(br, bc, 32, 1).astype(np.float32)
+            M = qtgen.BlockMatrix(4096, 1024, 32, br, bc, v)
+            run(ctx, stream, "dense N=4096 FP32 (supplementary)", {"A": M, "B": M, "same": True})
+        elif w == "err5f32":
+            import oracle
+            c = qtgen.config(5, P=1)
+            M = c["A"]
+            v32 = M.vals.astype(np.float32)
+            A = qtmm.Matrix.from_blocks(ctx, M.n, M.leaf_dim, 32, M.brow, M.bcol, v32)
+            r, cc, v = (A @ A).to_blocks()
+            ref = oracle.spgemm(M.nbr, 32, (M.brow, M.bcol, v32.astype(np.float64)),
+                                (M.brow, M.bcol, v32.astype(np.float64)), rows=(200, 232))
+            m = (r >= 200) & (r < 232)
+            d = v[m].astype(np.float64) - ref[2]
+            print(json.dumps({"cfg5_fp32_rel_fro_err_rows_200_232": float(np.linalg.norm(d) / np.linalg.norm(ref[2])),
+                              "max_abs_err": float(np.abs(d).max())}), flush=True)
         elif w == "dense4096":
             br, bc = qtgen.pattern_dense(128)
             v = qtgen.block_values(br, bc, 32, 1)
