@@ -5,8 +5,8 @@
 // benchmarks both precisions).  Reading C-9: inputs are FP32, the
 // result must be within 1e-5 relative Frobenius of the double product of the
 // FP32 inputs; one TF32 product per term is ~2.5e-4 off, so each product is
-// a_hi*b_hi + a_hi*b_lo + a_lo*b_hi with x_hi = tf32(x), x_lo = tf32(x - x_hi)
-// (error ~2^-22 per term, FP32 accumulation in TMEM).
+// a_hi*b_hi + a_hi*b_lo + a_lo*b_hi with x_hi = x truncated to TF32 and
+// x_lo = x - x_hi (error ~2^-21 per term, FP32 accumulation in TMEM).
 //
 // Work item ("tile") = one C node at level L-2: 4x4 C blocks = a 128x128 FP32
 // accumulator in TMEM (128 lanes x 128 columns; two tiles double-buffered = 256
@@ -18,11 +18,11 @@
 // (qt_common.cuh swz32), the same bytes are a valid SW128 descriptor target
 // for both operands.  Per step: 4 K-slices x 3 MMAs (M=128, N=128, K=8).
 //
-// Warp roles (320 threads, one CTA per SM, persistent over tiles):
-//   warps 0-3 epilogue  TMEM -> registers (tcgen05.ld 32x32b) -> C pool
-//   warps 4-7 split     fp32 -> (tf32 hi in place, tf32 lo copy) per stage
-//   warp 8    producer  task metadata + TMA bulk copies
-//   warp 9    MMA       one elected lane issues tcgen05.mma / commit
+// Warp roles (448 threads, one CTA per SM, persistent over tiles):
+//   warps 0-3  epilogue  TMEM -> registers (tcgen05.ld 32x32b) -> C pool
+//   warps 4-11 split     fp32 -> (tf32 hi in place, lo copy) per stage
+//   warp 12    producer  task metadata + TMA bulk copies
+//   warp 13    MMA       one elected lane issues tcgen05.mma / commit
 // Each C block is written once by one thread row-set: no atomics; summation
 // order per element is fixed (ascending k, and within a k the fixed K-slice
 // and hi/lo order), so results are run-to-run deterministic.
@@ -39,7 +39,10 @@ constexpr int kStages = 3;
 constexpr int kBlkBytes = 4096;                 // 32x32 fp32
 constexpr int kHiBytes = 8 * kBlkBytes;         // A_hi[4] | B_hi[4]
 constexpr int kStageBytes = 2 * kHiBytes;       // + A_lo[4] | B_lo[4]  = 64 KiB
-constexpr int kThreads = 320;
+constexpr int kSplitWarps = 8;
+constexpr int kProducerWarp = 4 + kSplitWarps;
+constexpr int kMmaWarp = kProducerWarp + 1;
+constexpr int kThreads = (kMmaWarp + 1) * 32;
 // TMEM: two tile buffers (double-buffered epilogue) x two accumulators x 128
 // columns = 512 columns.  The hi*hi products go to one accumulator, the two
 // cross terms (2^-11 smaller) to the other; the epilogue adds them with a
@@ -65,7 +68,7 @@ struct Smem {
   uint32_t tmem_base;
   uint32_t pad;
   uint64_t full[kStages];   // TMA landed (1 arrival + tx)
-  uint64_t conv[kStages];   // hi/lo split done (4 warp arrivals)
+  uint64_t conv[kStages];   // hi/lo split done (one arrival per split warp)
   uint64_t empty[kStages];  // MMAs that read the stage done (tcgen05.commit)
   uint64_t tfull[2];        // accumulator ready (commit + MMA-lane arrive)
   uint64_t tempty[2];       // epilogue drained the accumulator (4 warp arrivals)
@@ -141,10 +144,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
 }
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+// x_hi: the top 19 bits of x (a TF32 value); x - x_hi is exact in FP32 and
+// has at most 13 significant bits, of which the tensor core reads 11, so
+// x_hi + tf32(x - x_hi) represents x to ~2^-22 relative.
+__device__ __forceinline__ float tf32_trunc(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
 }
 
 // Shared-memory matrix descriptor (tcgen05): start >> 4 in [0,14), leading
@@ -167,15 +171,16 @@ constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1
 
 __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* data = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-byte aligned start (kept as an offset from the shared array so the
+  // compiler still emits shared-space LDS/STS for the split warps)
+  uint8_t* data = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   Smem& S = *reinterpret_cast<Smem*>(data + (size_t)kStages * kStageBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.conv[s], 4);
+      mbar_init(&S.conv[s], kSplitWarps);
       mbar_init(&S.empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -196,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
 
-  if (warp == 8) {
+  if (warp == kProducerWarp) {
     // ------------------------------------------------------------ producer
     const float* poolA = static_cast<const float*>(a.poolA);
     const float* poolB = static_cast<const float*>(a.poolB);
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
         phase ^= 1;
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && warp < 4 + kSplitWarps) {
     // ------------------------------------------------------------ hi/lo split
     // Each warp owns whole 1 KiB swizzle atoms (8 rows x 128 B = 64 float4),
     // two float4 per lane.  A atoms keep their layout (K-major SW128: hi in
@@ -323,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
         float4* hi = reinterpret_cast<float4*>(data + (size_t)stage * kStageBytes);
         float4* lo = reinterpret_cast<float4*>(data + (size_t)stage * kStageBytes + kHiBytes);
 #pragma unroll 1
-        for (int atom = cw; atom < 32; atom += 4) {  // atoms 0-15: A, 16-31: B
+        for (int atom = cw; atom < 32; atom += kSplitWarps) {  // atoms 0-15: A, 16-31: B
           const bool isB = atom >= 16;
           float4 x[2];
 #pragma unroll
@@ -338,14 +343,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
               t = r * 8 + ((((c16 >> 1) ^ (r & 3)) << 1) | (c16 & 1));
             }
             float4 hv, lv;
-            hv.x = tf32_rna(x[h].x);
-            hv.y = tf32_rna(x[h].y);
-            hv.z = tf32_rna(x[h].z);
-            hv.w = tf32_rna(x[h].w);
-            lv.x = tf32_rna(x[h].x - hv.x);
-            lv.y = tf32_rna(x[h].y - hv.y);
-            lv.z = tf32_rna(x[h].z - hv.z);
-            lv.w = tf32_rna(x[h].w - hv.w);
+            hv.x = tf32_trunc(x[h].x);
+            hv.y = tf32_trunc(x[h].y);
+            hv.z = tf32_trunc(x[h].z);
+            hv.w = tf32_trunc(x[h].w);
+            lv.x = x[h].x - hv.x;  // exact: at most 13 significant bits
+            lv.y = x[h].y - hv.y;
+            lv.z = x[h].z - hv.z;
+            lv.w = x[h].w - hv.w;
             hi[atom * 64 + t] = hv;
             lo[atom * 64 + t] = lv;
           }
@@ -360,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
         phase ^= 1;
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     int stage = 0;
     uint32_t phase = 0;
