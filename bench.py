@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--dtype", default="f64", choices=["f64"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true")
     return ap.parse_args()
 
 
@@ -291,6 +292,10 @@ def main():
     flops_launch = products * FLOP_PER_PRODUCT
     achieved = flops_launch / (ms_num * 1e-3) / 1e12
 
+    fp32 = None
+    if not args.no_fp32:
+        fp32 = measure_fp32(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier)
+
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier)
@@ -326,6 +331,7 @@ def main():
                                    "min": int(recv_all.min()), "unit": "bytes (FP64 payload)",
                                    "spsumma_comparator": spsumma[0] if P > 1 else 0},
             "cpu_baseline": cpu,
+            "fp32_variant": fp32,
             "e2e": e2e,
             "gpu_launches": launches_total,
             "clocks": clocks,
@@ -334,6 +340,57 @@ def main():
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_fp32(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier):
+    """BASELINE config 5's FP32 variant: the same matrix rounded to FP32, same
+    step, the tcgen05 3xTF32 kernel (secondary dtype; reported beside the FP64
+    headline, not instead of it)."""
+    import torch
+    A32 = qtmm.Matrix.from_blocks(ctx, Am.n, Am.leaf_dim, BS, Am.brow, Am.bcol,
+                                  Am.vals.astype(np.float32), row_bounds=bounds)
+    for _ in range(3):
+        C, st = A32.multiply(A32)
+        C.close()
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    sts = []
+    e0.record(stream)
+    for _ in range(args.steps):
+        C, st = A32.multiply(A32)
+        sts.append(st)
+        C.close()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_num = statistics.mean(x.ms_numeric for x in sts)
+    prods = sts[-1].block_products
+    a = aggregate(dist, [ms, float(prods), float(sts[-1].bytes_recv_payload)], "cuda", world)
+    A32.close()
+    value = a[:, 1].sum() * FLOP_PER_PRODUCT / (a[:, 0].max() * 1e-3) / 1e9
+    achieved = prods * FLOP_PER_PRODUCT / (ms_num * 1e-3) / 1e12
+    peaks = measured_peaks()
+    bf16 = peaks.get("bf16_tflops")
+    # 3xTF32: three kind::tf32 MMAs per product; TF32 = bf16 x (1.1 / 2.25) (nominal dense ratio)
+    peak = bf16 * (1.1 / 2.25) / 3.0 if bf16 else None
+    return {"value": round(value, 1), "unit": UNIT + " (FP32, 3xTF32 on tcgen05)",
+            "ms_per_step": round(float(a[:, 0].max()), 4), "dtype": "f32",
+            "bytes_recv_per_gpu_max": int(a[:, 2].max()),
+            "roofline": {"bound": "tensor", "kernel": "k_numeric_f32 (tcgen05.mma kind::tf32, 3 MMAs/product)",
+                         "achieved": round(achieved, 2), "peak": round(peak, 1) if peak else None,
+                         "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak else None,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops x (1.1/2.25 nominal tf32/bf16) / 3",
+                         "ms_numeric": round(ms_num, 4)}}
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0, "_source": "fallback (B200_PROFILING.md)"}
 
 
 def traffic_from_profiles(P: int):
