@@ -5,13 +5,17 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <new>
+#include <unordered_map>
 
 #include "qt_internal.h"
 
 namespace qt {
 
 static thread_local std::string g_last_error;
+static std::mutex g_ctx_mu;
+static std::unordered_map<cudaStream_t, int> g_stream_refs;
 
 void fail(qt_status s, const char* fmt, ...) {
   char buf[1024];
@@ -38,6 +42,81 @@ static qt_status handle_exception() {
     g_last_error = "unknown error";
     return QT_EINVAL;
   }
+}
+
+// ---------------------------------------------------------------- allocator
+
+namespace {
+struct StreamCache {
+  std::unordered_map<size_t, std::vector<void*>> free;
+};
+std::mutex g_cache_mu;
+std::unordered_map<cudaStream_t, StreamCache> g_cache;
+
+size_t size_class(size_t b) {
+  if (b <= 512) return 512;
+  if (b < (1u << 20)) {
+    size_t c = 512;
+    while (c < b) c <<= 1;
+    return c;
+  }
+  const size_t g = 2u << 20;
+  return (b + g - 1) / g * g;
+}
+
+void flush_all_caches() {
+  // called on out-of-memory: make sure no stream still uses a cached block
+  cudaDeviceSynchronize();
+  for (auto& kv : g_cache)
+    for (auto& fv : kv.second.free)
+      for (void* q : fv.second) cudaFree(q);
+  g_cache.clear();
+}
+}  // namespace
+
+void* cache_alloc(size_t bytes, cudaStream_t s, size_t* granted) {
+  const size_t c = size_class(bytes);
+  *granted = c;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache.find(s);
+    if (it != g_cache.end()) {
+      auto f = it->second.free.find(c);
+      if (f != it->second.free.end() && !f->second.empty()) {
+        void* q = f->second.back();
+        f->second.pop_back();
+        return q;
+      }
+    }
+  }
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, c);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    flush_all_caches();
+    e = cudaMalloc(&q, c);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(QT_ENOMEM, "device allocation of %zu bytes failed: %s", c, cudaGetErrorString(e));
+  }
+  return q;
+}
+
+void cache_free(void* p, size_t granted, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache[s].free[granted].push_back(p);
+}
+
+void cache_release_stream(cudaStream_t s) {
+  cudaStreamSynchronize(s);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = g_cache.find(s);
+  if (it == g_cache.end()) return;
+  for (auto& fv : it->second.free)
+    for (void* q : fv.second) cudaFree(q);
+  g_cache.erase(it);
 }
 
 static int ilog2(int64_t x) {
@@ -79,11 +158,10 @@ static void ctx_create(int device, void* cuda_stream, int rank, int world, const
     c->world = world;
     QT_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     for (auto& e : c->ev) QT_CUDA(cudaEventCreate(&e));
-    // keep freed blocks of the stream-ordered allocator cached in the pool
-    cudaMemPool_t pool;
-    QT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-    uint64_t thr = UINT64_MAX;
-    QT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    {
+      std::lock_guard<std::mutex> lk(g_ctx_mu);
+      ++g_stream_refs[c->stream];
+    }
     c->counters.alloc(256, c->stream);
     QT_CUDA(cudaMemsetAsync(c->counters.p, 0, 256, c->stream));
     c->zeros.alloc(8192, c->stream);
@@ -144,6 +222,14 @@ qt_status qt_ctx_destroy(qt_ctx ctx) {
   ctx->counters.release();
   ctx->zeros.release();
   cudaStreamSynchronize(ctx->stream);
+  // cached blocks of this stream are freed only when no other context uses it
+  {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    if (--g_stream_refs[ctx->stream] == 0) {
+      g_stream_refs.erase(ctx->stream);
+      cache_release_stream(ctx->stream);
+    }
+  }
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
   API_CATCH

@@ -42,19 +42,41 @@ struct Error : std::runtime_error {
 
 // ----------------------------------------------------------------- memory
 
-// Stream-ordered device buffer (cudaMallocAsync from the device's default
-// pool, which keeps freed memory cached: no OS calls in steady state).
+// Device memory: a caching allocator per CUDA stream.  Every kernel of a
+// context runs on its one stream, so a block freed on that stream can be handed
+// to the next allocation on the same stream with no synchronisation (stream
+// order guarantees the previous user is done).  Sizes are rounded to classes
+// (powers of two below 1 MiB, multiples of 2 MiB above) and matched exactly;
+// misses call cudaMalloc, and on out-of-memory the caches are flushed and the
+// allocation retried.  In steady state (repeated multiplies) no CUDA allocator
+// call happens at all.
+void* cache_alloc(size_t bytes, cudaStream_t s, size_t* granted);
+void cache_free(void* p, size_t granted, cudaStream_t s);
+void cache_release_stream(cudaStream_t s);
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  size_t granted = 0;
   cudaStream_t s = nullptr;
   DevBuf() = default;
   DevBuf(size_t b, cudaStream_t st) { alloc(b, st); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s) { o.p = nullptr; o.bytes = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), granted(o.granted), s(o.s) {
+    o.p = nullptr;
+    o.bytes = o.granted = 0;
+  }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; bytes = o.bytes; s = o.s; o.p = nullptr; o.bytes = 0; }
+    if (this != &o) {
+      release();
+      p = o.p;
+      bytes = o.bytes;
+      granted = o.granted;
+      s = o.s;
+      o.p = nullptr;
+      o.bytes = o.granted = 0;
+    }
     return *this;
   }
   ~DevBuf() { release(); }
@@ -63,17 +85,12 @@ struct DevBuf {
     s = st;
     bytes = b;
     if (b == 0) return;
-    cudaError_t e = cudaMallocAsync(&p, b, st);
-    if (e != cudaSuccess) {
-      p = nullptr;
-      cudaGetLastError();
-      fail(QT_ENOMEM, "device allocation of %zu bytes failed: %s", b, cudaGetErrorString(e));
-    }
+    p = cache_alloc(b, st, &granted);
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) cache_free(p, granted, s);
     p = nullptr;
-    bytes = 0;
+    bytes = granted = 0;
   }
   template <class T> T* as() const { return static_cast<T*>(p); }
 };

@@ -27,6 +27,8 @@
 // (frontiers up to 8K tasks) run in ONE single-CTA kernel with block-wide
 // scans; the large levels use grid-wide kernels + device scans.  One host sync
 // remains, before the numeric kernel (to size C's block pool).
+#include <chrono>
+#include <cstdlib>
 #include <cub/cub.cuh>
 
 #include "qt_common.cuh"
@@ -288,7 +290,26 @@ void excl_sum(qt_ctx ctx, const T* in, T* out, int64_t n) {
 
 }  // namespace
 
+// Optional host-side phase trace (QT_TRACE=1): wall-clock marks to stderr.
+struct Trace {
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  std::string buf;
+  Trace() : on(getenv("QT_TRACE") != nullptr), t0(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    char b[128];
+    snprintf(b, sizeof b, " %s@%.0f", what, us);
+    buf += b;
+  }
+  ~Trace() {
+    if (on) fprintf(stderr, "[qt trace] multiply:%s\n", buf.c_str());
+  }
+};
+
 qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* ms_num) {
+  Trace tr;
   qt_ctx ctx = A->ctx;
   cudaStream_t st = ctx->stream;
   const int L = A->L;
@@ -324,6 +345,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       QT_LAUNCH_CHECK(ctx);
       QT_CUDA(cudaMemcpyAsync(F.data(), dF.p, 8 * (L + 1), cudaMemcpyDeviceToHost, st));
       QT_CUDA(cudaStreamSynchronize(st));
+      tr.mark("counts");
       for (int l = 0; l <= L; ++l)
         if (F[l] >= (1ll << 31) / 4) fail(QT_EINVAL, "level %d has %lld tasks (> 2^29)", l, (long long)F[l]);
     }
@@ -374,6 +396,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       sa.off = soff.as<int32_t>();
       sa.gidx = sg.as<int32_t>();
       sa.ns_out = nsd;
+      tr.mark("small_alloc");
       k_bfs_small<<<1, kSmallThreads, 0, st>>>(sa);
       QT_LAUNCH_CHECK(ctx);
       const int cb = l_end & 1;
@@ -381,6 +404,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       DevBuf cstart = std::move(scs[cb]), ckey = std::move(sck[cb]);
       // --- large levels, grid-wide, no host sync
       DevBuf cchild, t2_pa, t2_pb, t2_cstart, cchild2;
+      tr.mark("small_launch");
       for (int l = l_end; l < L; ++l) {
         const bool last = (l == L - 1);
         const int32_t Fl = (int32_t)F[l], Fn = (int32_t)F[l + 1];
@@ -430,12 +454,15 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         ckey = std::move(ckey2);
       }
       // --- group counts of every level (the one remaining sync): C's block count
+      tr.mark("levels_launched");
       std::vector<int32_t> ns(L + 1, 0);
       QT_CUDA(cudaMemcpyAsync(ns.data(), nsd, 4 * (L + 1), cudaMemcpyDeviceToHost, st));
       QT_CUDA(cudaStreamSynchronize(st));
+      tr.mark("levels_done");
       for (int l = 0; l <= L; ++l) S.level_c_nodes[l] = ns[l];
       C->nb = ns[L];
       C->pool.alloc((size_t)C->nb * 1024 * elem_size(C->dtype), st);
+      tr.mark("c_alloc");
       QT_CUDA(cudaEventRecord(ctx->ev[3], st));
       NumericArgs na;
       na.ntiles = ns[L - 1];
@@ -474,7 +501,9 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         launch_numeric_f32(ctx, nb);
       }
       QT_CUDA(cudaEventRecord(ctx->ev[4], st));
+      tr.mark("numeric_launched");
       QT_CUDA(cudaEventSynchronize(ctx->ev[4]));  // frontier buffers are released after this
+      tr.mark("numeric_done");
     }
     QT_CUDA(cudaEventSynchronize(ctx->ev[4]));
     QT_CUDA(cudaEventElapsedTime(ms_sym, ctx->ev[2], ctx->ev[3]));
