@@ -187,6 +187,7 @@ struct NumericArgs {
   int64_t splitB;
   void* poolC;
   int* counter;              // tile scheduler counter (zeroed before launch)
+  int group = 1;             // tiles per scheduler grab (1..31)
 };
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a);
 

@@ -119,6 +119,7 @@ __device__ __forceinline__ void warp_block_mma(double (&acc)[4][4][2], const dou
   }
 }
 
+template <bool kGrouped>
 __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -146,6 +147,116 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   uint32_t phase = 0;
 
   if (producer) {
+    if constexpr (kGrouped) {
+    // ------------------------------------------------------------ producer
+    // Work is taken in groups of a.group consecutive tiles (one atomic per
+    // group; the next group's atomic is issued before the current group is
+    // streamed, so its latency is hidden).  The tasks of a group are a
+    // contiguous range of the level L-1 queue; they are streamed 32 at a time
+    // with lane-parallel metadata loads, across tile boundaries, and a STORE
+    // marker is posted at every tile end.  Sparse patterns (few tasks per
+    // tile) get large groups, banded/dense ones group = 1 (fine-grained
+    // dynamic balance).
+    const double* poolA = static_cast<const double*>(a.poolA);
+    const double* poolB = static_cast<const double*>(a.poolB);
+    const double* poolB2 = static_cast<const double*>(a.poolB2);
+    const int G = a.group;
+    int t0 = 0;
+    if (lane == 0) t0 = atomicAdd(a.counter, G);
+    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    auto post = [&](int flags, int4 cc) {
+      mbar_wait(&empty[stage], phase ^ 1);
+      if (lane == 0) {
+        StageHdr& h = hdr[stage];
+        h.c[0] = cc.x;
+        h.c[1] = cc.y;
+        h.c[2] = cc.z;
+        h.c[3] = cc.w;
+        h.flags = flags;
+        mbar_arrive(&full[stage]);
+      }
+      __syncwarp();
+      if (++stage == kStagesPer) {
+        stage = 0;
+        phase ^= 1;
+      }
+    };
+    while (t0 < a.ntiles) {
+      const int t1 = min(t0 + G, (int)a.ntiles);
+      // next group: prefetched now when groups are large (sparse patterns), taken
+      // at the end otherwise (a reserved-but-idle tile would lengthen the tail)
+      int tn = 0;
+      if (G > 1 && lane == 0) tn = atomicAdd(a.counter, G);
+      // lane l holds tile t0+l's task start and C children; lane (t1-t0) the end
+      int ts = 0;
+      int4 cc = make_int4(-1, -1, -1, -1);
+      if (lane <= t1 - t0) ts = a.tile_start[t0 + lane];
+      if (lane < t1 - t0) cc = a.childC[t0 + lane];
+      const int p_begin = __shfl_sync(0xffffffffu, ts, 0);
+      const int p_end = __shfl_sync(0xffffffffu, ts, t1 - t0);
+      int cur = 0;  // tile index within the group
+      int boundary = __shfl_sync(0xffffffffu, ts, 1);
+      for (int pb0 = p_begin; pb0 < p_end; pb0 += 32) {
+        const int p = pb0 + lane;
+        int4 ca = make_int4(-1, -1, -1, -1), cb = ca;
+        if (p < p_end) {
+          ca = a.childA[a.pa[p]];
+          cb = a.childB[a.pb[p]];
+        }
+        const int nloc = min(32, p_end - pb0);
+        for (int u = 0; u < nloc; ++u) {
+          while (pb0 + u >= boundary) {  // tile `cur` is complete
+            post(F_STORE, shfl_int4(cc, cur));
+            ++cur;
+            boundary = __shfl_sync(0xffffffffu, ts, cur + 1);
+          }
+          const int4 A4 = shfl_int4(ca, u);
+          const int4 B4 = shfl_int4(cb, u);
+#pragma unroll
+          for (int kb = 0; kb < 2; ++kb) {
+            // A child (i,kb) in slot 2i+kb ; B child (kb,j) in slot 2kb+j
+            const int a0 = kb ? A4.y : A4.x, a1 = kb ? A4.w : A4.z;
+            const int b0 = kb ? B4.z : B4.x, b1 = kb ? B4.w : B4.y;
+            if (!((a0 >= 0 || a1 >= 0) && (b0 >= 0 || b1 >= 0))) continue;
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (lane == 0) {
+              StageHdr& h = hdr[stage];
+              h.a[0] = a0;
+              h.a[1] = a1;
+              h.b[0] = b0;
+              h.b[1] = b1;
+              h.flags = F_COMPUTE;
+              const uint32_t bytes = 8192u * ((a0 >= 0) + (a1 >= 0) + (b0 >= 0) + (b1 >= 0));
+              mbar_arrive_expect_tx(&full[stage], bytes);
+              double* dst = data + (size_t)stage * kStageElems;
+              if (a0 >= 0) bulk_g2s(dst, poolA + (size_t)a0 * kBlockElems, 8192u, &full[stage]);
+              if (a1 >= 0)
+                bulk_g2s(dst + kBlockElems, poolA + (size_t)a1 * kBlockElems, 8192u, &full[stage]);
+              if (b0 >= 0) {
+                const double* src = b0 < a.splitB ? poolB + (size_t)b0 * kBlockElems
+                                                  : poolB2 + (size_t)(b0 - a.splitB) * kBlockElems;
+                bulk_g2s(dst + 2 * kBlockElems, src, 8192u, &full[stage]);
+              }
+              if (b1 >= 0) {
+                const double* src = b1 < a.splitB ? poolB + (size_t)b1 * kBlockElems
+                                                  : poolB2 + (size_t)(b1 - a.splitB) * kBlockElems;
+                bulk_g2s(dst + 3 * kBlockElems, src, 8192u, &full[stage]);
+              }
+            }
+            __syncwarp();
+            if (++stage == kStagesPer) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+      for (; cur < t1 - t0; ++cur) post(F_STORE, shfl_int4(cc, cur));
+      if (G == 1 && lane == 0) tn = atomicAdd(a.counter, G);
+      t0 = __shfl_sync(0xffffffffu, tn, 0);
+    }
+    post(F_DONE, make_int4(-1, -1, -1, -1));
+    } else {
     // ------------------------------------------------------------ producer
     const double* poolA = static_cast<const double*>(a.poolA);
     const double* poolB = static_cast<const double*>(a.poolB);
@@ -229,6 +340,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         stage = 0;
         phase ^= 1;
       }
+    }
     }
   } else {
     // ------------------------------------------------------------ consumers
@@ -318,13 +430,20 @@ void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a) {
   if (dt != QT_F64) fail(QT_EDTYPE, "launch_numeric is the FP64 kernel");
   static bool attr_set = false;
   if (!attr_set) {
-    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmemBytes));
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kSmemBytes));
     attr_set = true;
   }
   QT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), ctx->stream));
   int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
-  k_numeric_f64<<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
+  // one tile per grab (dense/banded: finest dynamic balance) or grouped grabs
+  // (sparse patterns: amortise the scheduler and metadata latency)
+  if (a.group > 1)
+    k_numeric_f64<true><<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
+  else
+    k_numeric_f64<false><<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
   QT_LAUNCH_CHECK(ctx);
 }
 

@@ -478,6 +478,20 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       na.splitB = B->split;
       na.poolC = C->pool.p;
       na.counter = ctx->counters.as<int>() + 16;
+      // tiles per scheduler grab: ~32 tasks per grab, at most 16 tiles
+      {
+        const int64_t per_tile = std::max<int64_t>(1, F[L - 1] / std::max<int32_t>(1, ns[L - 1]));
+        // (tiles with >= 8 tasks stream well one at a time: grouping only costs balance)
+        int64_t g = per_tile >= 8 ? 1 : std::min<int64_t>(16, 32 / per_tile);
+        // keep >= 8 grabs per tile stream (2 per CTA, one CTA per SM)
+        g = std::min<int64_t>(g, ns[L - 1] / (16ll * ctx->num_sms));
+        na.group = (int)std::max<int64_t>(1, g);
+        if (tr.on) {
+          char b[64];
+          snprintf(b, sizeof b, "group=%d", na.group);
+          tr.mark(b);
+        }
+      }
       if (C->nb > 0 && !f32) launch_numeric(ctx, C->dtype, na);
       if (C->nb > 0 && f32) {
         NumericArgs32 nb;

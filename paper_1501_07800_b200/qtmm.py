@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libqtmm.so")
+LIB_PATH = os.environ.get("QTMM_LIB_DEV") or os.path.join(_HERE, "lib", "libqtmm.so")  # dev A/B override
 
 QT_F64, QT_F32 = 0, 1
 STATUS = {0: "QT_OK", 1: "QT_EINVAL", 2: "QT_ERANGE", 3: "QT_EDUP", 4: "QT_EDIM", 5: "QT_EBS",
