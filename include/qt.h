@@ -142,7 +142,9 @@ qt_status qt_multiply(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st);
  * prefix of blocks, sorted ascending by Frobenius norm with ties broken by
  * (brow, bcol), whose accumulated squared norm is < tau^2, so that
  * ||A - out||_F < tau (or nothing removed).  tau >= 0.  New handle; A
- * unchanged.  Multi-rank: collective (the prefix is global).
+ * unchanged.  Multi-rank: collective — the prefix is global: every rank sends
+ * its (norm^2, brow, bcol) terms (24 bytes per block) to all others and all
+ * ranks take the same decision; each keeps its surviving local blocks.
  * Errors: QT_EINVAL, QT_ENOMEM, QT_ECUDA, QT_ENCCL. */
 qt_status qt_truncate(qt_mat A, double tau, qt_mat* out);
 

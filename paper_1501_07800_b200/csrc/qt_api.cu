@@ -366,9 +366,13 @@ qt_status qt_truncate(qt_mat A, double tau, qt_mat* out) {
   *out = nullptr;
   if (!(tau >= 0)) fail(QT_EINVAL, "tau must be >= 0");
   QT_CUDA(cudaSetDevice(A->ctx->device));
-  if (A->ctx->world > 1) fail(QT_EINVAL, "multi-rank truncate is not built yet");
-  qt_mat R = truncate(A, tau);
-  R->global_nb = R->nb;
+  qt_mat R;
+  if (A->ctx->world > 1) {
+    R = truncate_dist(A, tau);
+  } else {
+    R = truncate(A, tau);
+    R->global_nb = R->nb;
+  }
   QT_CUDA(cudaStreamSynchronize(A->ctx->stream));
   *out = R;
   API_CATCH

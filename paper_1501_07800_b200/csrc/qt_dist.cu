@@ -698,6 +698,73 @@ qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S) {
   return C;
 }
 
+// ------------------------------------------------------------ truncation (multi-rank)
+
+namespace {
+__global__ void k_ids(int64_t* __restrict__ out, int64_t n, int64_t rank) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = (rank << 32) | t;
+}
+}  // namespace
+
+// Every rank sends its (norm^2, row-major key, id) terms to every other rank,
+// then all ranks take the same global decision (truncate_decide) and keep
+// their local survivors.  Moves 24 bytes per block to each peer (not on the
+// multiply's hot path).
+qt_mat truncate_dist(qt_mat A, double tau) {
+  qt_ctx ctx = A->ctx;
+  cudaStream_t st = ctx->stream;
+  const int P = ctx->world, me = ctx->rank;
+  Transport* X = T(ctx);
+  const int64_t n = A->nb;
+  std::vector<int64_t> counts(P);
+  X->allgather_i64(&n, counts.data(), 1);
+  std::vector<int64_t> off(P + 1, 0);
+  for (int q = 0; q < P; ++q) off[q + 1] = off[q] + counts[q];
+  const int64_t n_all = off[P];
+  DevBuf nrm, rm;
+  truncate_terms(A, nrm, rm);
+  DevBuf ids(8 * std::max<int64_t>(n, 1), st);
+  if (n > 0) {
+    k_ids<<<gfor(n), kT, 0, st>>>(ids.as<int64_t>(), n, me);
+    QT_LAUNCH_CHECK(ctx);
+  }
+  DevBuf nrm_all(8 * std::max<int64_t>(n_all, 1), st), rm_all(8 * std::max<int64_t>(n_all, 1), st),
+      id_all(8 * std::max<int64_t>(n_all, 1), st);
+  if (n > 0) {
+    QT_CUDA(cudaMemcpyAsync(nrm_all.as<double>() + off[me], nrm.p, 8 * n, cudaMemcpyDeviceToDevice, st));
+    QT_CUDA(cudaMemcpyAsync(rm_all.as<uint64_t>() + off[me], rm.p, 8 * n, cudaMemcpyDeviceToDevice, st));
+    QT_CUDA(cudaMemcpyAsync(id_all.as<int64_t>() + off[me], ids.p, 8 * n, cudaMemcpyDeviceToDevice, st));
+  }
+  X->group_start();
+  for (int q = 0; q < P; ++q) {
+    if (q == me) continue;
+    if (n > 0) {
+      X->send(nrm.p, 8 * n, q);
+      X->send(rm.p, 8 * n, q);
+      X->send(ids.p, 8 * n, q);
+    }
+    if (counts[q] > 0) {
+      X->recv(nrm_all.as<double>() + off[q], 8 * counts[q], q);
+      X->recv(rm_all.as<uint64_t>() + off[q], 8 * counts[q], q);
+      X->recv(id_all.as<int64_t>() + off[q], 8 * counts[q], q);
+    }
+  }
+  X->group_end();
+  DevBuf keep(std::max<int64_t>(n, 1), st);
+  if (n > 0) QT_CUDA(cudaMemsetAsync(keep.p, 1, n, st));
+  truncate_decide(ctx, nrm_all.as<double>(), rm_all.as<uint64_t>(), id_all.as<int64_t>(), n_all,
+                  tau * tau, me, keep.as<uint8_t>());
+  qt_mat R = select_blocks(A, keep.as<uint8_t>());
+  int64_t kept = R->nb, tot = 0;
+  std::vector<int64_t> all(P);
+  X->allgather_i64(&kept, all.data(), 1);
+  for (auto v : all) tot += v;
+  R->global_nb = tot;
+  return R;
+}
+
 // ------------------------------------------------------------ virtual ranks
 
 qt_mat multiply_virtual(qt_mat A, qt_mat B, const int32_t* bounds, int P, int g, qt_stats* S) {

@@ -165,8 +165,12 @@ inline void ensure_levels(qt_mat M) {
 }
 // row-major (brow, bcol) order and un-swizzle into caller buffers
 void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals);
-// truncate
+// truncate (reading C-16): local terms, global decision, single-rank driver
+void truncate_terms(qt_mat A, DevBuf& nrm, DevBuf& rm);
+void truncate_decide(qt_ctx ctx, const double* nrm_all, const uint64_t* rm_all, const int64_t* id_all,
+                     int64_t n_all, double tau2, int me, uint8_t* keep_local);
 qt_mat truncate(qt_mat A, double tau);
+qt_mat truncate_dist(qt_mat A, double tau);
 // copy `keep` flagged blocks (Morton order preserved) of A into a new matrix
 qt_mat select_blocks(qt_mat A, const uint8_t* d_keep);
 

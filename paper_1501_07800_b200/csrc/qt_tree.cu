@@ -145,23 +145,6 @@ __global__ void k_block_norm2(const T* __restrict__ pool, int64_t nb, double* __
   }
 }
 
-__global__ void k_gather_f64(const double* __restrict__ in, const int32_t* __restrict__ order,
-                             int64_t n, double* __restrict__ out, uint64_t* __restrict__ bits) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    double v = in[order[t]];
-    if (out) out[t] = v;
-    if (bits) bits[t] = (uint64_t)__double_as_longlong(v);  // v >= 0: bit order = value order
-  }
-}
-
-__global__ void k_mark_keep(const double* __restrict__ prefix, const int32_t* __restrict__ order,
-                            int64_t n, double tau2, uint8_t* __restrict__ keep) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x)
-    keep[order[t]] = prefix[t] < tau2 ? 0 : 1;
-}
-
 __global__ void k_compact_blocks(const uint8_t* __restrict__ keep, const int32_t* __restrict__ incl,
                                  const uint64_t* __restrict__ key, const uint4* __restrict__ pool,
                                  int64_t n, int64_t vec_per_block, uint64_t* __restrict__ okey,
@@ -402,39 +385,98 @@ qt_mat select_blocks(qt_mat A, const uint8_t* d_keep) {
   return M;
 }
 
+// Frobenius norms^2 and row-major keys of the local blocks (truncation terms)
+void truncate_terms(qt_mat A, DevBuf& nrm, DevBuf& rm) {
+  qt_ctx ctx = A->ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = A->nb;
+  nrm.alloc(8 * std::max<int64_t>(n, 1), st);
+  rm.alloc(8 * std::max<int64_t>(n, 1), st);
+  if (n == 0) return;
+  DevBuf iota(n * 4, st);
+  const int wpb = 8;
+  const unsigned gr = (unsigned)std::min<int64_t>((n + wpb - 1) / wpb, 148 * 32);
+  if (A->dtype == QT_F64)
+    k_block_norm2<double><<<gr, 32 * wpb, 0, st>>>(A->pool.as<double>(), n, nrm.as<double>());
+  else
+    k_block_norm2<float><<<gr, 32 * wpb, 0, st>>>(A->pool.as<float>(), n, nrm.as<double>());
+  QT_LAUNCH_CHECK(ctx);
+  k_rowmajor_keys<<<grid_for(n), kThreads, 0, st>>>(A->key.as<uint64_t>(), n, rm.as<uint64_t>(),
+                                                    iota.as<int32_t>());
+  QT_LAUNCH_CHECK(ctx);
+}
+
+namespace {
+__global__ void k_iota64(int64_t* __restrict__ out, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = t;
+}
+__global__ void k_gather_bits(const double* __restrict__ nrm, const int64_t* __restrict__ ord,
+                              int64_t n, uint64_t* __restrict__ bits) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    bits[t] = (uint64_t)__double_as_longlong(nrm[ord[t]]);  // norms >= 0: bit order = value order
+}
+__global__ void k_gather_val(const double* __restrict__ nrm, const int64_t* __restrict__ ord,
+                             int64_t n, double* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = nrm[ord[t]];
+}
+// the blocks of the dropped prefix that belong to rank `me` lose their keep flag
+__global__ void k_mark_drop(const double* __restrict__ prefix, const int64_t* __restrict__ ord,
+                            const int64_t* __restrict__ id, int64_t n, double tau2, int me,
+                            uint8_t* __restrict__ keep) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (!(prefix[t] < tau2)) continue;
+    const int64_t v = id[ord[t]];
+    if ((int)(v >> 32) == me) keep[v & 0xffffffffll] = 0;
+  }
+}
+}  // namespace
+
+// Global truncation decision (reading C-16) over all terms of all ranks: order
+// by (norm^2, brow, bcol) — a stable sort by the row-major key, then a stable
+// sort by the norm — prefix sums of norm^2 in that order, and every term
+// whose prefix is < tau^2 is dropped.  Every rank evaluates the same
+// deterministic sort and scan on the same data, so all agree.
+void truncate_decide(qt_ctx ctx, const double* nrm_all, const uint64_t* rm_all, const int64_t* id_all,
+                     int64_t n_all, double tau2, int me, uint8_t* keep_local) {
+  cudaStream_t st = ctx->stream;
+  if (n_all == 0) return;
+  DevBuf iota(8 * n_all, st), rm2(8 * n_all, st), ord1(8 * n_all, st), bits(8 * n_all, st),
+      bits2(8 * n_all, st), ord2(8 * n_all, st), g(8 * n_all, st), pre(8 * n_all, st);
+  k_iota64<<<grid_for(n_all), kThreads, 0, st>>>(iota.as<int64_t>(), n_all);
+  QT_LAUNCH_CHECK(ctx);
+  cub_sort_pairs(ctx, rm_all, rm2.as<uint64_t>(), iota.as<int64_t>(), ord1.as<int64_t>(), n_all, 64);
+  k_gather_bits<<<grid_for(n_all), kThreads, 0, st>>>(nrm_all, ord1.as<int64_t>(), n_all,
+                                                      bits.as<uint64_t>());
+  QT_LAUNCH_CHECK(ctx);
+  cub_sort_pairs(ctx, bits.as<uint64_t>(), bits2.as<uint64_t>(), ord1.as<int64_t>(),
+                 ord2.as<int64_t>(), n_all, 64);
+  k_gather_val<<<grid_for(n_all), kThreads, 0, st>>>(nrm_all, ord2.as<int64_t>(), n_all, g.as<double>());
+  QT_LAUNCH_CHECK(ctx);
+  cub_incl_sum(ctx, g.as<double>(), pre.as<double>(), n_all);
+  k_mark_drop<<<grid_for(n_all), kThreads, 0, st>>>(pre.as<double>(), ord2.as<int64_t>(), id_all,
+                                                    n_all, tau2, me, keep_local);
+  QT_LAUNCH_CHECK(ctx);
+}
+
 qt_mat truncate(qt_mat A, double tau) {
   qt_ctx ctx = A->ctx;
   cudaStream_t st = ctx->stream;
-  int64_t n = A->nb;
+  const int64_t n = A->nb;
   DevBuf keep(std::max<int64_t>(n, 1), st);
   if (n > 0) {
-    DevBuf nrm(n * 8, st), rm(n * 8, st), rm2(n * 8, st), iota(n * 4, st), ord1(n * 4, st),
-        bits(n * 8, st), bits2(n * 8, st), ord2(n * 4, st), g(n * 8, st), pre(n * 8, st);
-    int wpb = 8;
-    unsigned gr = (unsigned)std::min<int64_t>((n + wpb - 1) / wpb, 148 * 32);
-    if (A->dtype == QT_F64)
-      k_block_norm2<double><<<gr, 32 * wpb, 0, st>>>(A->pool.as<double>(), n, nrm.as<double>());
-    else
-      k_block_norm2<float><<<gr, 32 * wpb, 0, st>>>(A->pool.as<float>(), n, nrm.as<double>());
+    QT_CUDA(cudaMemsetAsync(keep.p, 1, n, st));
+    DevBuf nrm, rm, id(8 * n, st);
+    truncate_terms(A, nrm, rm);
+    k_iota64<<<grid_for(n), kThreads, 0, st>>>(id.as<int64_t>(), n);  // rank 0, local index
     QT_LAUNCH_CHECK(ctx);
-    // ties broken by (brow, bcol): stable sort by row-major key, then by norm
-    k_rowmajor_keys<<<grid_for(n), kThreads, 0, st>>>(A->key.as<uint64_t>(), n, rm.as<uint64_t>(),
-                                                      iota.as<int32_t>());
-    QT_LAUNCH_CHECK(ctx);
-    cub_sort_pairs(ctx, rm.as<uint64_t>(), rm2.as<uint64_t>(), iota.as<int32_t>(),
-                   ord1.as<int32_t>(), n, 64);
-    k_gather_f64<<<grid_for(n), kThreads, 0, st>>>(nrm.as<double>(), ord1.as<int32_t>(), n, nullptr,
-                                                   bits.as<uint64_t>());
-    QT_LAUNCH_CHECK(ctx);
-    cub_sort_pairs(ctx, bits.as<uint64_t>(), bits2.as<uint64_t>(), ord1.as<int32_t>(),
-                   ord2.as<int32_t>(), n, 64);
-    k_gather_f64<<<grid_for(n), kThreads, 0, st>>>(nrm.as<double>(), ord2.as<int32_t>(), n,
-                                                   g.as<double>(), nullptr);
-    QT_LAUNCH_CHECK(ctx);
-    cub_incl_sum(ctx, g.as<double>(), pre.as<double>(), n);
-    k_mark_keep<<<grid_for(n), kThreads, 0, st>>>(pre.as<double>(), ord2.as<int32_t>(), n,
-                                                  tau * tau, keep.as<uint8_t>());
-    QT_LAUNCH_CHECK(ctx);
+    truncate_decide(ctx, nrm.as<double>(), rm.as<uint64_t>(), id.as<int64_t>(), n, tau * tau, 0,
+                    keep.as<uint8_t>());
   }
   return select_blocks(A, keep.as<uint8_t>());
 }

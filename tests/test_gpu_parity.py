@@ -418,3 +418,45 @@ def test_loopback_cfg4_small_two_ranks(qt, ctx):
         (r, cc, v), st, _, _ = out[g]
         m = (full[0] >= bounds[g]) & (full[0] < bounds[g + 1])
         assert np.array_equal(r, full[0][m]) and np.array_equal(v, full[2][m])
+
+
+@pytest.mark.parametrize("P,tau", [(2, 5.0), (3, 40.0), (2, 0.0)])
+def test_loopback_truncate_matches_single_rank(qt, ctx, P, tau):
+    import threading
+    import torch
+    rng = np.random.default_rng(23)
+    Mm = random_bm(rng, 24, 32, 0.4, "uniform", 128)
+    Mm.vals *= rng.uniform(0, 1, size=(Mm.nb, 1, 1)) ** 4
+    ref = oracle.truncate(Mm.brow, Mm.bcol, Mm.vals, tau)
+    single = mk(qt, ctx, Mm).truncate(tau).to_blocks()
+    assert np.array_equal(single[0], ref[0]) and np.array_equal(single[2], ref[2])
+    bounds = [g * 24 // P for g in range(P)] + [24]
+    hub = qt.LoopbackHub(P)
+    out, errs = [None] * P, []
+
+    def rank_fn(g):
+        try:
+            torch.cuda.set_device(0)
+            c = qt.Context(0, stream=torch.cuda.Stream(), loopback=(hub, g, P))
+            m = (Mm.brow >= bounds[g]) & (Mm.brow < bounds[g + 1])
+            A = qt.Matrix.from_blocks(c, Mm.n, 128, 32, Mm.brow[m], Mm.bcol[m], Mm.vals[m], row_bounds=bounds)
+            T = A.truncate(tau)
+            out[g] = (T.to_blocks(), T.info())
+            T.close()
+            A.close()
+            c.close()
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=rank_fn, args=(g,)) for g in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    hub.close()
+    assert not errs, errs
+    r = np.concatenate([o[0][0] for o in out])
+    c_ = np.concatenate([o[0][1] for o in out])
+    v = np.concatenate([o[0][2] for o in out])
+    assert np.array_equal(r, ref[0]) and np.array_equal(c_, ref[1]) and np.array_equal(v, ref[2])
+    assert all(o[1]["global_nblocks"] == len(ref[0]) for o in out)
