@@ -460,3 +460,26 @@ def test_loopback_truncate_matches_single_rank(qt, ctx, P, tau):
     v = np.concatenate([o[0][2] for o in out])
     assert np.array_equal(r, ref[0]) and np.array_equal(c_, ref[1]) and np.array_equal(v, ref[2])
     assert all(o[1]["global_nblocks"] == len(ref[0]) for o in out)
+
+
+@pytest.mark.parametrize("P,g,expect", [(2, 0, 17039360), (4, 1, 34078720), (8, 5, 34078720)])
+def test_virtual_rank_bytes_cfg5_full_size(qt, ctx, P, g, expect):
+    """Config 5 at full size (N = 16384*P): the bytes rank g receives in the
+    weak-scaling run — the paper's central quantity — equal the
+    oracle's exchange plan (34.1 MB per interior GPU, flat in P; 17.0 MB at P=2).
+    Only rank g's strip and its halo rows are generated (nothing else is read)."""
+    nbr = 512 * P
+    lo, hi = 512 * g, 512 * (g + 1)
+    c = qtgen.config(5, P=P, rows=(max(0, lo - 32), min(nbr, hi + 32)))
+    Am = c["A"]
+    A = mk(qt, ctx, Am)
+    bounds = [512 * q for q in range(P + 1)]
+    Cg, st = A.multiply_virtual(A, P, g, bounds)
+    plan = oracle.exchange_plan(bounds, (Am.brow, Am.bcol), (Am.brow, Am.bcol), 8192)[g]
+    assert st.bytes_recv_payload == plan["payload_bytes"] == expect
+    assert st.bytes_recv_meta == plan["meta_bytes"]
+    # the strip's product is complete: interior rows have the full 2*64+1 C blocks
+    rows = Cg.to_blocks()[0]
+    assert rows.min() >= lo and rows.max() < hi
+    counts = np.bincount(rows - lo, minlength=hi - lo)
+    assert counts.max() == 129
