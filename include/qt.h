@@ -138,6 +138,15 @@ qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
  * QT_ECUDA, QT_ENCCL. */
 qt_status qt_multiply(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st);
 
+/* C = op(A) op(B) with op(X) = X (0) or X^T (1): the transposed multiply task
+ * types C = A^T B, A B^T, A^T B^T of §3.2.  A transposed operand
+ * is read through its own quadtree with the off-diagonal children swapped and
+ * each block transposed on the fly (no copy).  Same requirements, statistics
+ * and errors as qt_multiply; world > 1 supports only trans_a = trans_b = 0
+ * (QT_EINVAL otherwise). */
+qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, qt_mat* C,
+                         qt_stats* st);
+
 /* Frobenius-norm truncation (reading C-16): remove the longest
  * prefix of blocks, sorted ascending by Frobenius norm with ties broken by
  * (brow, bcol), whose accumulated squared norm is < tau^2, so that

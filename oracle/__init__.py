@@ -16,6 +16,8 @@ S:nnn = SPEC.md line; readings C-n are listed in DESIGN.md):
                   products; C-1 structural pattern, C-5 order).  C source in
                   ``qt_oracle.c``.
 * ``dense_mm``    textbook triple loop (pin P-2).
+* ``transpose`` / ``spgemm_t``  the transposed task types C = A^T B, A B^T,
+                  A^T B^T by explicit block transposition.
 * ``pattern_product``   boolean product of block patterns (pin P-6).
 * ``level_task_counts`` multiply tasks per quadtree level: the number of
                   (A-node, B-node) pairs with both non-NIL at level l
@@ -125,6 +127,21 @@ def spgemm(nbr: int, bs: int, A, B, nthreads: int | None = None, rows=None):
                        nbr, _p(c_ptr), _p(c_col), _p(c_val), lo, hi, nt)
     c_row = np.repeat(np.arange(nbr, dtype=np.int32), c_cnt)
     return c_row, c_col[:nc], c_val[:nc]
+
+
+def transpose(brow, bcol, vals):
+    """X^T as a block list: block (I,J) becomes block (J,I) with its values
+    transposed (the operand of the transposed task types C = A^T B, A B^T,
+    A^T B^T)."""
+    return (np.asarray(bcol, np.int32), np.asarray(brow, np.int32),
+            np.ascontiguousarray(np.swapaxes(np.asarray(vals), 1, 2)))
+
+
+def spgemm_t(nbr: int, bs: int, A, B, trans_a=False, trans_b=False, nthreads=None, rows=None):
+    """C = op(A) op(B) (op = transpose when flagged), by explicit transposition."""
+    a = transpose(*A) if trans_a else A
+    b = transpose(*B) if trans_b else B
+    return spgemm(nbr, bs, a, b, nthreads, rows)
 
 
 def dense_mm(A: np.ndarray, B: np.ndarray) -> np.ndarray:

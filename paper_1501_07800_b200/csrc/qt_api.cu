@@ -326,6 +326,11 @@ qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
 }
 
 qt_status qt_multiply(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st) {
+  return qt_multiply_ex(A, B, 0, 0, C, st);
+}
+
+qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, qt_mat* C,
+                         qt_stats* st) {
   API_TRY
   if (!A || !B || !C) fail(QT_EINVAL, "NULL argument");
   *C = nullptr;
@@ -337,6 +342,10 @@ qt_status qt_multiply(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st) {
   if (A->dtype != B->dtype) fail(QT_EDTYPE, "dtype mismatch");
   qt_ctx ctx = A->ctx;
   QT_CUDA(cudaSetDevice(ctx->device));
+  if ((trans_a | trans_b) & ~1) fail(QT_EINVAL, "trans_a / trans_b must be 0 or 1");
+  const int trans = (trans_a ? 1 : 0) | (trans_b ? 2 : 0);
+  if (trans && ctx->world > 1)
+    fail(QT_EINVAL, "transposed operands are single-rank only (row strips of A^T are column strips of A)");
   ensure_levels(A);
   ensure_levels(B);
   qt_stats local;
@@ -346,7 +355,7 @@ qt_status qt_multiply(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st) {
   qt_mat R;
   if (ctx->world == 1) {
     float ms_sym = 0, ms_num = 0;
-    R = multiply_local(A, B, &S, &ms_sym, &ms_num);
+    R = multiply_local(A, B, &S, &ms_sym, &ms_num, trans);
     S.ms_symbolic = ms_sym;
     S.ms_numeric = ms_num;
   } else {

@@ -175,7 +175,8 @@ qt_mat truncate_dist(qt_mat A, double tau);
 qt_mat select_blocks(qt_mat A, const uint8_t* d_keep);
 
 // ----- symbolic + numeric multiply (qt_symbolic.cu, qt_numeric.cu)
-qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* st, float* ms_sym, float* ms_num);
+// trans: bit 0 = op(A) = A^T, bit 1 = op(B) = B^T  (C = op(A) op(B))
+qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* st, float* ms_sym, float* ms_num, int trans = 0);
 
 struct NumericArgs {
   int64_t ntiles;            // C nodes at level L-1
@@ -192,6 +193,7 @@ struct NumericArgs {
   void* poolC;
   int* counter;              // tile scheduler counter (zeroed before launch)
   int group = 1;             // tiles per scheduler grab (1..31)
+  int trans = 0;             // bit 0: A transposed, bit 1: B transposed
 };
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a);
 
@@ -214,6 +216,7 @@ struct NumericArgs32 {
   void* poolC;
   const void* zeros;         // one zero block (absent operands)
   int* counter;
+  int trans = 0;             // bit 0: A transposed, bit 1: B transposed
 };
 void launch_numeric_f32(qt_ctx ctx, const NumericArgs32& a);
 void launch_fp64_peak(qt_ctx ctx, int kind, int iters, int grid);

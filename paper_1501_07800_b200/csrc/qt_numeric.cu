@@ -97,8 +97,11 @@ __device__ __forceinline__ int4 shfl_int4(int4 v, int src) {
   return v;
 }
 
-// One 32x32x32 block product on one warp: acc += A·B, A and B in the internal
-// swizzled layout (qt_common.cuh swz64) in shared memory.
+// One 32x32x32 block product on one warp: acc += op(A)·op(B), A and B in the
+// internal swizzled layout (qt_common.cuh swz64) in shared memory.  A
+// transposed operand is read with the other operand's fragment pattern
+// (op(A)(r,c) = A(c,r)), which the swizzle also serves conflict-free.
+template <bool kTA, bool kTB>
 __device__ __forceinline__ void warp_block_mma(double (&acc)[4][4][2], const double* __restrict__ As,
                                                const double* __restrict__ Bs, int lane) {
   const int g = lane >> 2, t4 = lane & 3;
@@ -107,11 +110,13 @@ __device__ __forceinline__ void warp_block_mma(double (&acc)[4][4][2], const dou
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
     double af[4], bf[4];
-    const int acol = ((ks ^ xa) << 2) | t4;
+    const int kcol = ((ks ^ xa) << 2) | t4;
 #pragma unroll
-    for (int m = 0; m < 4; ++m) af[m] = As[(m * 8 + g) * 32 + acol];
+    for (int m = 0; m < 4; ++m)
+      af[m] = kTA ? As[(ks * 4 + t4) * 32 + ((m * 8) ^ xb)] : As[(m * 8 + g) * 32 + kcol];
 #pragma unroll
-    for (int n = 0; n < 4; ++n) bf[n] = Bs[(ks * 4 + t4) * 32 + ((n * 8) ^ xb)];
+    for (int n = 0; n < 4; ++n)
+      bf[n] = kTB ? Bs[(n * 8 + g) * 32 + kcol] : Bs[(ks * 4 + t4) * 32 + ((n * 8) ^ xb)];
 #pragma unroll
     for (int m = 0; m < 4; ++m)
 #pragma unroll
@@ -119,7 +124,19 @@ __device__ __forceinline__ void warp_block_mma(double (&acc)[4][4][2], const dou
   }
 }
 
-template <bool kGrouped>
+// child slots of op(X): a transposed node swaps its off-diagonal children
+template <bool kT>
+__device__ __forceinline__ int4 ldchild(const int4* __restrict__ tab, int idx) {
+  int4 c = tab[idx];
+  if (kT) {
+    const int t = c.y;
+    c.y = c.z;
+    c.z = t;
+  }
+  return c;
+}
+
+template <bool kGrouped, bool kTA, bool kTB>
 __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -200,8 +217,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         const int p = pb0 + lane;
         int4 ca = make_int4(-1, -1, -1, -1), cb = ca;
         if (p < p_end) {
-          ca = a.childA[a.pa[p]];
-          cb = a.childB[a.pb[p]];
+          ca = ldchild<kTA>(a.childA, a.pa[p]);
+          cb = ldchild<kTB>(a.childB, a.pb[p]);
         }
         const int nloc = min(32, p_end - pb0);
         for (int u = 0; u < nloc; ++u) {
@@ -279,8 +296,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         const int p = pb0 + lane;
         int4 ca = make_int4(-1, -1, -1, -1), cb = ca;
         if (p < p1) {
-          ca = a.childA[a.pa[p]];
-          cb = a.childB[a.pb[p]];
+          ca = ldchild<kTA>(a.childA, a.pa[p]);
+          cb = ldchild<kTB>(a.childB, a.pb[p]);
         }
         const int nloc = min(32, p1 - pb0);
         for (int u = 0; u < nloc; ++u) {
@@ -380,7 +397,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         const bool go = h.a[wi] >= 0 && h.b[wj] >= 0;
         if (go) {
           const double* st = data + (size_t)stage * kStageElems;
-          warp_block_mma(acc, st + wi * kBlockElems, st + (2 + wj) * kBlockElems, lane);
+          warp_block_mma<kTA, kTB>(acc, st + wi * kBlockElems, st + (2 + wj) * kBlockElems, lane);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
@@ -426,24 +443,34 @@ __global__ void k_peak_dfma(double* out, int iters) {
 
 }  // namespace
 
-void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a) {
-  if (dt != QT_F64) fail(QT_EDTYPE, "launch_numeric is the FP64 kernel");
+template <bool G, bool TA, bool TB>
+static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
   static bool attr_set = false;
   if (!attr_set) {
-    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemBytes));
-    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<G, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kSmemBytes));
     attr_set = true;
   }
+  k_numeric_f64<G, TA, TB><<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
+}
+
+void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a) {
+  if (dt != QT_F64) fail(QT_EDTYPE, "launch_numeric is the FP64 kernel");
   QT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), ctx->stream));
-  int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
+  const int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
   // one tile per grab (dense/banded: finest dynamic balance) or grouped grabs
   // (sparse patterns: amortise the scheduler and metadata latency)
-  if (a.group > 1)
-    k_numeric_f64<true><<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
-  else
-    k_numeric_f64<false><<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
+  const bool G = a.group > 1;
+  switch ((G ? 4 : 0) | (a.trans & 3)) {
+    case 0: launch_numeric_t<false, false, false>(ctx, a, grid); break;
+    case 1: launch_numeric_t<false, true, false>(ctx, a, grid); break;
+    case 2: launch_numeric_t<false, false, true>(ctx, a, grid); break;
+    case 3: launch_numeric_t<false, true, true>(ctx, a, grid); break;
+    case 4: launch_numeric_t<true, false, false>(ctx, a, grid); break;
+    case 5: launch_numeric_t<true, true, false>(ctx, a, grid); break;
+    case 6: launch_numeric_t<true, false, true>(ctx, a, grid); break;
+    default: launch_numeric_t<true, true, true>(ctx, a, grid); break;
+  }
   QT_LAUNCH_CHECK(ctx);
 }
 

@@ -165,10 +165,26 @@ constexpr uint64_t kSW128 = 2;         // K-major A: 16-byte chunks ^ (row & 7)
 constexpr uint64_t kSW128_32B = 1;     // MN-major B (32-bit types): 32-byte chunks ^ (row & 3)
 
 // Instruction descriptor: D f32 (bits 4-5 = 1), A tf32 (7-9 = 2), B tf32
-// (10-12 = 2), A K-major (15 = 0), B MN-major (16 = 1), N>>3 at 17, M>>4 at 24.
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
-                            ((128u >> 3) << 17) | ((128u >> 4) << 24);
+// (10-12 = 2), A major (15: 0 = K), B major (16: 1 = MN), N>>3 at 17, M>>4 at 24.
+// A stored row-major block is K-major as an A operand and MN-major as a B
+// operand; a transposed operand (C = A^T B, A B^T) flips that.
+template <bool kTA, bool kTB>
+__host__ __device__ constexpr uint32_t idesc_tf32() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((kTA ? 1u : 0u) << 15) | ((kTB ? 0u : 1u) << 16) |
+         ((128u >> 3) << 17) | ((128u >> 4) << 24);
+}
+template <bool kT>
+__device__ __forceinline__ int4 ldchild(const int4* __restrict__ tab, int idx) {
+  int4 c = tab[idx];
+  if (kT) {
+    const int t = c.y;
+    c.y = c.z;
+    c.z = t;
+  }
+  return c;
+}
 
+template <bool kTA, bool kTB>
 __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned start (kept as an offset from the shared array so the
@@ -233,22 +249,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
 #pragma unroll
           for (int y = 0; y < 4; ++y) ab[x][y] = bb[x][y] = -1;
         if (p < p1) {
-          const int4 qa = a.childA2[a.pa[p]];  // A quads (i', k') in slot 2i'+k'
-          const int4 qb = a.childB2[a.pb[p]];  // B quads (k', j') in slot 2k'+j'
+          const int4 qa = ldchild<kTA>(a.childA2, a.pa[p]);  // op(A) quads (i', k') in slot 2i'+k'
+          const int4 qb = ldchild<kTB>(a.childB2, a.pb[p]);  // op(B) quads (k', j') in slot 2k'+j'
           const int qa_[4] = {qa.x, qa.y, qa.z, qa.w};
           const int qb_[4] = {qb.x, qb.y, qb.z, qb.w};
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
             const int hi = s >> 1, lo = s & 1;
             if (qa_[s] >= 0) {
-              const int4 c = a.childA1[qa_[s]];  // (i'', k'') in slot 2i''+k''
+              const int4 c = ldchild<kTA>(a.childA1, qa_[s]);  // (i'', k'') in slot 2i''+k''
               ab[2 * hi + 0][2 * lo + 0] = c.x;
               ab[2 * hi + 0][2 * lo + 1] = c.y;
               ab[2 * hi + 1][2 * lo + 0] = c.z;
               ab[2 * hi + 1][2 * lo + 1] = c.w;
             }
             if (qb_[s] >= 0) {
-              const int4 c = a.childB1[qb_[s]];  // (k'', j'') in slot 2k''+j''
+              const int4 c = ldchild<kTB>(a.childB1, qb_[s]);  // (k'', j'') in slot 2k''+j''
               bb[2 * hi + 0][2 * lo + 0] = c.x;
               bb[2 * hi + 0][2 * lo + 1] = c.y;
               bb[2 * hi + 1][2 * lo + 0] = c.z;
@@ -329,7 +345,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
         float4* lo = reinterpret_cast<float4*>(data + (size_t)stage * kStageBytes + kHiBytes);
 #pragma unroll 1
         for (int atom = cw; atom < 32; atom += kSplitWarps) {  // atoms 0-15: A, 16-31: B
-          const bool isB = atom >= 16;
+          // MN-major operands get the 32-byte-atom layout: B unless transposed, A if transposed
+          const bool relayout = atom >= 16 ? !kTB : kTA;
           float4 x[2];
 #pragma unroll
           for (int h = 0; h < 2; ++h) x[h] = hi[atom * 64 + lane + 32 * h];
@@ -338,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
           for (int h = 0; h < 2; ++h) {
             const int f = lane + 32 * h;
             int t = f;
-            if (isB) {
+            if (relayout) {
               const int r = f >> 3, c16 = (f & 7) ^ r;
               t = r * 8 + ((((c16 >> 1) ^ (r & 3)) << 1) | (c16 & 1));
             }
@@ -413,13 +430,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             // A: 128 rows x 32 fp32 K-major, SW128 (LBO 16 B unused, SBO 1024 B); K-slice j at +32 B
-            const uint64_t a_hi = sdesc(st + 32u * j, 16, 1024, kSW128);
-            const uint64_t a_lo = sdesc(st + kHiBytes + 32u * j, 16, 1024, kSW128);
-            // B: 32 rows (K) x 128 fp32 (N) MN-major, SW128 with 32-byte atoms (LBO 4096 B
-            // between the four 32-wide N atoms = blocks, SBO 512 B between 4-row K atoms);
-            // K-slice j (rows 8j..8j+7) at +1024 B
-            const uint64_t b_hi = sdesc(st + 4u * kBlkBytes + 1024u * j, 4096, 512, kSW128_32B);
-            const uint64_t b_lo = sdesc(st + kHiBytes + 4u * kBlkBytes + 1024u * j, 4096, 512, kSW128_32B);
+            // K-major operand (4 blocks stacked along M or N, 32 fp32 of K per
+            // 128-byte row): SW128, SBO 1024 B between 8-row groups, K-slice j
+            // at +32 B.  MN-major operand (4 blocks side by side along M or N,
+            // rows = K): 32-byte-atom SW128, LBO 4096 B between the 32-wide
+            // atoms (= blocks), SBO 512 B between 4-row K atoms, K-slice j
+            // (rows 8j..8j+7) at +1024 B.
+            const uint32_t stA = st, stB = st + 4u * kBlkBytes;
+            const uint64_t a_hi = kTA ? sdesc(stA + 1024u * j, 4096, 512, kSW128_32B)
+                                      : sdesc(stA + 32u * j, 16, 1024, kSW128);
+            const uint64_t a_lo = kTA ? sdesc(stA + kHiBytes + 1024u * j, 4096, 512, kSW128_32B)
+                                      : sdesc(stA + kHiBytes + 32u * j, 16, 1024, kSW128);
+            const uint64_t b_hi = kTB ? sdesc(stB + 32u * j, 16, 1024, kSW128)
+                                      : sdesc(stB + 1024u * j, 4096, 512, kSW128_32B);
+            const uint64_t b_lo = kTB ? sdesc(stB + kHiBytes + 32u * j, 16, 1024, kSW128)
+                                      : sdesc(stB + kHiBytes + 1024u * j, 4096, 512, kSW128_32B);
+            constexpr uint32_t kIdesc = idesc_tf32<kTA, kTB>();
             const uint32_t acc_in = ((flags & F_FIRST) && j == 0) ? 0u : 1u;
             tc_mma(d_cross, a_lo, b_hi, kIdesc, acc_in);
             tc_mma(d_cross, a_hi, b_lo, kIdesc, 1u);
@@ -494,16 +520,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
 
 }  // namespace
 
-void launch_numeric_f32(qt_ctx ctx, const NumericArgs32& a) {
+template <bool TA, bool TB>
+static void launch_f32_t(qt_ctx ctx, const NumericArgs32& a, int grid) {
   static bool attr_set = false;
   if (!attr_set) {
-    QT_CUDA(cudaFuncSetAttribute(k_numeric_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f32<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kSmemBytes));
     attr_set = true;
   }
+  k_numeric_f32<TA, TB><<<grid, kThreads, kSmemBytes, ctx->stream>>>(a);
+}
+
+void launch_numeric_f32(qt_ctx ctx, const NumericArgs32& a) {
   QT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), ctx->stream));
-  int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
-  k_numeric_f32<<<grid, kThreads, kSmemBytes, ctx->stream>>>(a);
+  const int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
+  switch (a.trans & 3) {
+    case 0: launch_f32_t<false, false>(ctx, a, grid); break;
+    case 1: launch_f32_t<true, false>(ctx, a, grid); break;
+    case 2: launch_f32_t<false, true>(ctx, a, grid); break;
+    default: launch_f32_t<true, true>(ctx, a, grid); break;
+  }
   QT_LAUNCH_CHECK(ctx);
 }
 

@@ -49,16 +49,31 @@ inline unsigned grid_for(int64_t n) {
 
 // C_l for every level: one CTA per level
 __global__ void k_level_tasks(const int32_t* __restrict__ histA, const int32_t* __restrict__ histB,
-                              int64_t H, int64_t* __restrict__ out) {
+                              int64_t H, int trans, int64_t* __restrict__ out) {
   using BR = cub::BlockReduce<long long, kThreads>;
   __shared__ typename BR::TempStorage tmp;
   const int l = blockIdx.x;
   const int64_t base = (1ll << l) - 1, m = 1ll << l;
   long long s = 0;
   for (int64_t K = threadIdx.x; K < m; K += blockDim.x)
-    s += (long long)histA[H + base + K] * (long long)histB[base + K];  // cols(A_l) . rows(B_l)
+    // cols(op(A)_l) . rows(op(B)_l); a transposed operand swaps its row/column histograms
+    s += (long long)histA[((trans & 1) ? 0 : H) + base + K] *
+         (long long)histB[((trans & 2) ? H : 0) + base + K];
   s = BR(tmp).Sum(s);
   if (threadIdx.x == 0) out[l] = s;
+}
+
+// Child slots of op(X): the transpose of a node has its off-diagonal children
+// swapped (slot 1 <-> 2) and each child transposed in turn — so for a globally
+// transposed operand (C = A^T B etc.) only the slot order changes.
+__device__ __forceinline__ int4 ldchild(const int4* __restrict__ tab, int idx, bool trans) {
+  int4 c = tab[idx];
+  if (trans) {
+    const int t = c.y;
+    c.y = c.z;
+    c.z = t;
+  }
+  return c;
 }
 
 // A child (i,k) sits in slot 2i+k, B child (k,j) in slot 2k+j, C child (i,j) in 2i+j.
@@ -102,6 +117,7 @@ __device__ __forceinline__ void emit_task(int4 a4, int4 b4, int64_t base, int32_
 
 struct SmallBfsArgs {
   int l_end;  // run transitions l -> l+1 for l < l_end
+  int trans;  // bit 0: A transposed, bit 1: B transposed
   const int4* childA[QT_MAX_LEVELS];
   const int4* childB[QT_MAX_LEVELS];
   int32_t* pa[2];
@@ -145,7 +161,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     for (int p = tid; p < F; p += kSmallThreads) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
       int c[4];
-      child_counts(cA[pa[p]], cB[pb[p]], c);
+      child_counts(ldchild(cA, pa[p], a.trans & 1), ldchild(cB, pb[p], a.trans & 2), c);
       const int64_t base = 4ll * c0 + (p - c0);
 #pragma unroll
       for (int q = 0; q < 4; ++q) a.off[base + (int64_t)q * m] = c[q];
@@ -197,7 +213,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     // 4. emit the child tasks
     for (int p = tid; p < F; p += kSmallThreads) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
-      emit_task(cA[pa[p]], cB[pb[p]], 4ll * c0 + (p - c0), m, s, a.off, a.gidx, a.pa[nxt], a.pb[nxt],
+      emit_task(ldchild(cA, pa[p], a.trans & 1), ldchild(cB, pb[p], a.trans & 2), 4ll * c0 + (p - c0),
+                m, s, a.off, a.gidx, a.pa[nxt], a.pb[nxt],
                 a.pc[nxt]);
     }
     __syncthreads();
@@ -213,13 +230,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
 
 __global__ void k_count(int32_t F, const int32_t* __restrict__ pa, const int32_t* __restrict__ pb,
                         const int32_t* __restrict__ pc, const int32_t* __restrict__ cstart,
-                        const int4* __restrict__ childA, const int4* __restrict__ childB,
+                        const int4* __restrict__ childA, const int4* __restrict__ childB, int trans,
                         int32_t* __restrict__ cnt) {
   const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= F) return;
   const int32_t s = pc[p], c0 = cstart[s], m = cstart[s + 1] - c0;
   int c[4];
-  child_counts(childA[pa[p]], childB[pb[p]], c);
+  child_counts(ldchild(childA, pa[p], trans & 1), ldchild(childB, pb[p], trans & 2), c);
   const int64_t base = 4ll * c0 + (p - c0);
 #pragma unroll
   for (int q = 0; q < 4; ++q) cnt[base + (int64_t)q * m] = c[q];
@@ -269,14 +286,15 @@ __global__ void k_newc(int32_t nsb, const int32_t* __restrict__ ns_dev, int32_t 
 
 __global__ void k_emit(int32_t F, const int32_t* __restrict__ pa, const int32_t* __restrict__ pb,
                        const int32_t* __restrict__ pc, const int32_t* __restrict__ cstart,
-                       const int4* __restrict__ childA, const int4* __restrict__ childB,
+                       const int4* __restrict__ childA, const int4* __restrict__ childB, int trans,
                        const int32_t* __restrict__ off, const int32_t* __restrict__ gidx,
                        int32_t* __restrict__ pa2, int32_t* __restrict__ pb2,
                        int32_t* __restrict__ pc2) {
   const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= F) return;
   const int32_t s = pc[p], c0 = cstart[s], m = cstart[s + 1] - c0;
-  emit_task(childA[pa[p]], childB[pb[p]], 4ll * c0 + (p - c0), m, s, off, gidx, pa2, pb2, pc2);
+  emit_task(ldchild(childA, pa[p], trans & 1), ldchild(childB, pb[p], trans & 2), 4ll * c0 + (p - c0),
+            m, s, off, gidx, pa2, pb2, pc2);
 }
 
 template <class T>
@@ -308,7 +326,7 @@ struct Trace {
   }
 };
 
-qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* ms_num) {
+qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* ms_num, int trans) {
   Trace tr;
   qt_ctx ctx = A->ctx;
   cudaStream_t st = ctx->stream;
@@ -341,7 +359,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       const int64_t H = 2ll << L;
       DevBuf dF(8 * (L + 1), st);
       k_level_tasks<<<L + 1, kThreads, 0, st>>>(A->hist.as<int32_t>(), B->hist.as<int32_t>(), H,
-                                               dF.as<int64_t>());
+                                               trans, dF.as<int64_t>());
       QT_LAUNCH_CHECK(ctx);
       QT_CUDA(cudaMemcpyAsync(F.data(), dF.p, 8 * (L + 1), cudaMemcpyDeviceToHost, st));
       QT_CUDA(cudaStreamSynchronize(st));
@@ -376,6 +394,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       DevBuf sp[2], sb[2], sc[2], scs[2], sck[2];
       SmallBfsArgs sa;
       sa.l_end = l_end;
+      sa.trans = trans;
       for (int l = 0; l < L; ++l) {
         sa.childA[l] = A->child[l].as<int4>();
         sa.childB[l] = B->child[l].as<int4>();
@@ -413,7 +432,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         k_count<<<grid_for(Fl), kThreads, 0, st>>>(Fl, pa.as<int32_t>(), pb.as<int32_t>(),
                                                    pc.as<int32_t>(), cstart.as<int32_t>(),
                                                    A->child[l].as<int4>(), B->child[l].as<int4>(),
-                                                   cnt.as<int32_t>());
+                                                   trans, cnt.as<int32_t>());
         QT_LAUNCH_CHECK(ctx);
         excl_sum(ctx, cnt.as<int32_t>(), off.as<int32_t>(), n4);
         DevBuf flag(4 * s4, st), gstart(4 * s4, st), nex(4 * s4, st), gidx(4 * s4, st);
@@ -437,7 +456,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         k_emit<<<grid_for(Fl), kThreads, 0, st>>>(Fl, pa.as<int32_t>(), pb.as<int32_t>(),
                                                   pc.as<int32_t>(), cstart.as<int32_t>(),
                                                   A->child[l].as<int4>(), B->child[l].as<int4>(),
-                                                  off.as<int32_t>(), gidx.as<int32_t>(),
+                                                  trans, off.as<int32_t>(), gidx.as<int32_t>(),
                                                   pa2.as<int32_t>(), pb2.as<int32_t>(),
                                                   pc2.as<int32_t>());
         QT_LAUNCH_CHECK(ctx);
@@ -478,6 +497,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       na.splitB = B->split;
       na.poolC = C->pool.p;
       na.counter = ctx->counters.as<int>() + 16;
+      na.trans = trans;
       // tiles per scheduler grab: ~32 tasks per grab, at most 16 tiles
       {
         const int64_t per_tile = std::max<int64_t>(1, F[L - 1] / std::max<int32_t>(1, ns[L - 1]));
@@ -512,6 +532,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         nb.poolC = C->pool.p;
         nb.zeros = ctx->zeros.p;
         nb.counter = ctx->counters.as<int>() + 16;
+        nb.trans = trans;
         launch_numeric_f32(ctx, nb);
       }
       QT_CUDA(cudaEventRecord(ctx->ev[4], st));

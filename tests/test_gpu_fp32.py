@@ -161,3 +161,16 @@ def test_fp32_virtual_ranks_bitwise(qt, ctx, P):
         m = (full[0] >= bounds[g]) & (full[0] < bounds[g + 1])
         assert np.array_equal(r, full[0][m]) and np.array_equal(v, full[2][m])
         assert st.bytes_recv_payload == plan[g]["payload_bytes"]   # FP32 halves the payload
+
+
+
+@pytest.mark.parametrize("ta,tb", [(True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_fp32_transposed_products(qt, ctx, ta, tb, kind):
+    rng = np.random.default_rng(91 + 3 * ta + 7 * tb + (kind == "int"))
+    nbr = 21
+    Am = random_bm(rng, nbr, 0.3, kind, 128)
+    Bm = random_bm(rng, nbr, 0.3, kind, 128)
+    got = mk(qt, ctx, Am).multiply_ex(mk(qt, ctx, Bm), ta, tb)[0].to_blocks()
+    ref = oracle.spgemm_t(nbr, 32, ref64(Am), ref64(Bm), ta, tb)
+    check(got, ref, kind)

@@ -483,3 +483,39 @@ def test_virtual_rank_bytes_cfg5_full_size(qt, ctx, P, g, expect):
     assert rows.min() >= lo and rows.max() < hi
     counts = np.bincount(rows - lo, minlength=hi - lo)
     assert counts.max() == 129
+
+
+
+# ----------------------------------------------------------------- transposed task types
+
+
+@pytest.mark.parametrize("ta,tb", [(True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+@pytest.mark.parametrize("nbr,p", [(5, 0.6), (37, 0.2)])
+def test_transposed_products(qt, ctx, ta, tb, kind, nbr, p):
+    rng = np.random.default_rng(nbr + 3 * ta + 7 * tb + (kind == "int"))
+    Am = random_bm(rng, nbr, 32, p, kind, 128)
+    Bm = random_bm(rng, nbr, 32, p, kind, 128)
+    C, st = mk(qt, ctx, Am).multiply_ex(mk(qt, ctx, Bm), ta, tb)
+    got = C.to_blocks()
+    ref = oracle.spgemm_t(nbr, 32, as_tuple(Am), as_tuple(Bm), ta, tb)
+    if kind == "int":
+        assert_same_pattern(got, ref)
+        assert np.array_equal(got[2], ref[2])
+    else:
+        a = oracle.transpose(*as_tuple(Am)) if ta else as_tuple(Am)
+        b = oracle.transpose(*as_tuple(Bm)) if tb else as_tuple(Bm)
+        assert_close_f64(got, ref, a, b, nbr, 32, nbr * 32)
+    L, _ = oracle.tree_levels(Am.n, 32, 128)
+    ar = (Am.bcol, Am.brow) if ta else (Am.brow, Am.bcol)
+    br = (Bm.bcol, Bm.brow) if tb else (Bm.brow, Bm.bcol)
+    assert list(st.level_tasks[: L + 1]) == oracle.level_task_counts(L, ar, br)
+
+
+def test_transposed_aat_banded(qt, ctx):
+    c = qtgen.config(2, "int", small=True)
+    A = mk(qt, ctx, c["A"])
+    got = A.multiply_ex(A, False, True)[0].to_blocks()   # A A^T
+    ref = oracle.spgemm_t(c["A"].nbr, 32, as_tuple(c["A"]), as_tuple(c["A"]), False, True)
+    assert_same_pattern(got, ref)
+    assert np.array_equal(got[2], ref[2])

@@ -389,3 +389,34 @@ def test_higham_bound_holds_against_extended_precision():
     assert np.all(err <= B + 1e-300)
     assert np.max(err) > 0 or np.array_equal(got, ex)
     assert oracle.gamma(2080, 2.0 ** -53) == pytest.approx(2080 * 2.0 ** -53, rel=1e-10)
+
+
+# --------------------------------------------------------------------- transposed task types
+
+
+@pytest.mark.parametrize("ta,tb", [(True, False), (False, True), (True, True)])
+def test_transposed_products_vs_dense_library(ta, tb):
+    rng = np.random.default_rng(31 + 2 * ta + tb)
+    nbr, bs = 7, 4
+    a = _random_block_matrix(rng, nbr, bs, 0.4)
+    b = _random_block_matrix(rng, nbr, bs, 0.4)
+    r, c, v = oracle.spgemm_t(nbr, bs, a, b, ta, tb)
+    Ad = _blocks_to_dense(nbr, bs, *a)
+    Bd = _blocks_to_dense(nbr, bs, *b)
+    ref = (Ad.T if ta else Ad) @ (Bd.T if tb else Bd)
+    assert np.array_equal(_blocks_to_dense(nbr, bs, r, c, v), ref)
+    pr, pc = oracle.pattern_product(nbr, (a[1], a[0]) if ta else a[:2], (b[1], b[0]) if tb else b[:2])
+    assert np.array_equal(r, pr) and np.array_equal(c, pc)
+
+
+def test_transpose_identity_ab_t():
+    # (A B)^T = B^T A^T, both sides from the oracle's own routine on exact integers
+    rng = np.random.default_rng(5)
+    nbr, bs = 6, 4
+    a = _random_block_matrix(rng, nbr, bs, 0.5)
+    b = _random_block_matrix(rng, nbr, bs, 0.5)
+    ab = oracle.spgemm(nbr, bs, a, b)
+    btat = oracle.spgemm_t(nbr, bs, b, a, True, True)
+    t = oracle.transpose(*ab)
+    o = np.lexsort((t[1], t[0]))
+    assert np.array_equal(t[0][o], btat[0]) and np.array_equal(t[2][o], btat[2])
