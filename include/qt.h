@@ -147,6 +147,19 @@ qt_status qt_multiply(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st);
 qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, qt_mat* C,
                          qt_stats* st);
 
+/* Symmetric matrix square C = A^2 (§3.3): A is symmetric and given
+ * by its upper block triangle (every block of A has brow <= bcol; a diagonal
+ * block is a full bs x bs block, used as stored); C is returned the same way
+ * — only its upper block triangle is computed (about half of the products of
+ * the full multiply).  The symbolic pass walks the quadtree of the
+ * full matrix through references into U (diagonal nodes expose their (0,1)
+ * child transposed as (1,0); transposed nodes swap and transpose their
+ * children) and prunes C nodes below the diagonal at every level; the numeric
+ * kernel transposes blocks on the fly.  FP64, world == 1 in this build.
+ * Errors: QT_EINVAL (a block below the diagonal, or world > 1), QT_EDTYPE
+ * (FP32), QT_ENOMEM, QT_ECUDA. */
+qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st);
+
 /* Frobenius-norm truncation (reading C-16): remove the longest
  * prefix of blocks, sorted ascending by Frobenius norm with ties broken by
  * (brow, bcol), whose accumulated squared norm is < tau^2, so that

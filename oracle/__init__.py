@@ -18,6 +18,9 @@ S:nnn = SPEC.md line; readings C-n are listed in DESIGN.md):
 * ``dense_mm``    textbook triple loop (pin P-2).
 * ``transpose`` / ``spgemm_t``  the transposed task types C = A^T B, A B^T,
                   A^T B^T by explicit block transposition.
+* ``symm_square`` upper block triangle of A^2 for symmetric A in upper
+                  triangular storage (§3.3 P:297-311), by explicit expansion;
+                  ``level_task_counts_sym`` its per-level tasks.
 * ``pattern_product``   boolean product of block patterns (pin P-6).
 * ``level_task_counts`` multiply tasks per quadtree level: the number of
                   (A-node, B-node) pairs with both non-NIL at level l
@@ -142,6 +145,47 @@ def spgemm_t(nbr: int, bs: int, A, B, trans_a=False, trans_b=False, nthreads=Non
     a = transpose(*A) if trans_a else A
     b = transpose(*B) if trans_b else B
     return spgemm(nbr, bs, a, b, nthreads, rows)
+
+
+def expand_symmetric(brow, bcol, vals):
+    """The full symmetric matrix from its upper block triangle (brow <= bcol):
+    every off-diagonal block (I,J) also stands for (J,I) = block^T; diagonal
+    blocks are used as stored (§3.3, upper triangular storage)."""
+    brow = np.asarray(brow, np.int32)
+    bcol = np.asarray(bcol, np.int32)
+    vals = np.asarray(vals)
+    off = brow != bcol
+    tr = transpose(brow[off], bcol[off], vals[off])
+    return (np.concatenate([brow, tr[0]]), np.concatenate([bcol, tr[1]]),
+            np.concatenate([vals, tr[2]]))
+
+
+def symm_square(nbr: int, bs: int, U, nthreads=None, rows=None):
+    """C = A^2 for the symmetric A given by its upper block triangle U; returns
+    the upper block triangle of C (the operation of §3.3)."""
+    full = expand_symmetric(*U)
+    r, c, v = spgemm(nbr, bs, full, full, nthreads, rows)
+    keep = r <= c
+    return r[keep], c[keep], v[keep]
+
+
+def level_task_counts_sym(L: int, u_rc):
+    """Multiply tasks per level of the symmetric square: (I,K,J) at level l
+    with A_l(I,K), A_l(K,J) non-NIL and I <= J (only C's upper triangle is
+    computed), A the full symmetric pattern."""
+    import scipy.sparse as sp
+    r = np.asarray(u_rc[0], np.int64)
+    c = np.asarray(u_rc[1], np.int64)
+    fr, fc = np.concatenate([r, c]), np.concatenate([c, r])
+    out = []
+    for l in range(L + 1):
+        s = L - l
+        m = 1 << l
+        ar, ac = _coarsen((fr, fc), s)
+        M = sp.csr_matrix((np.ones(len(ar), np.int64), (ar, ac)), shape=(m, m))
+        P = sp.triu(M @ M)
+        out.append(int(P.sum()))
+    return out
 
 
 def dense_mm(A: np.ndarray, B: np.ndarray) -> np.ndarray:

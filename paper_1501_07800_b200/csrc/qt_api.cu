@@ -369,6 +369,32 @@ qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, q
   API_CATCH
 }
 
+qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
+  API_TRY
+  if (!A || !C) fail(QT_EINVAL, "NULL argument");
+  *C = nullptr;
+  qt_ctx ctx = A->ctx;
+  QT_CUDA(cudaSetDevice(ctx->device));
+  if (ctx->world > 1) fail(QT_EINVAL, "the symmetric square is single-rank only in this build");
+  if (A->dtype != QT_F64) fail(QT_EDTYPE, "the symmetric square is FP64-only in this build");
+  check_upper(A);
+  ensure_levels(A);
+  qt_stats local;
+  qt_stats& S = st ? *st : local;
+  memset(&S, 0, sizeof(S));
+  QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  float ms_sym = 0, ms_num = 0;
+  qt_mat R = multiply_local(A, A, &S, &ms_sym, &ms_num, 4);
+  S.ms_symbolic = ms_sym;
+  S.ms_numeric = ms_num;
+  QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+  QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
+  QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
+  R->global_nb = R->nb;
+  *C = R;
+  API_CATCH
+}
+
 qt_status qt_truncate(qt_mat A, double tau, qt_mat* out) {
   API_TRY
   if (!A || !out) fail(QT_EINVAL, "NULL argument");

@@ -52,4 +52,36 @@ __host__ __device__ inline int swz32(int r, int c) {
   return r * 32 + ((((c >> 2) ^ (r & 7)) << 2) | (c & 3));
 }
 
+// Child slots of op(X): the transpose of a node has its off-diagonal children
+// swapped (slot 1 <-> 2) and each child transposed in turn — so for a globally
+// transposed operand (C = A^T B etc.) only the slot order changes.
+__device__ __forceinline__ int4 ldchild(const int4* __restrict__ tab, int idx, bool trans) {
+  int4 c = tab[idx];
+  if (trans) {
+    const int t = c.y;
+    c.y = c.z;
+    c.z = t;
+  }
+  return c;
+}
+
+// Symmetric square (§3.3): A = B = the symmetric matrix whose upper
+// block triangle U is stored.  A node of the full matrix is a reference
+// (U node index, diagonal?, transposed?) = idx*4 + diag*2 + t: the children of
+// a diagonal node D are (D00 diag, D01, D01^T, D11 diag) — its stored (1,0)
+// slot is NIL in upper storage — and the children of a transposed node are the
+// slot-swapped transposes of its children.  NIL = -1.
+__device__ __forceinline__ int sref(int idx, int diag, int t) {
+  return idx < 0 ? -1 : ((idx << 2) | (diag << 1) | t);
+}
+__device__ __forceinline__ int4 op_children(const int4* __restrict__ tab, int ref, bool trans,
+                                            bool sym) {
+  if (!sym) return ldchild(tab, ref, trans);
+  const int idx = ref >> 2, diag = (ref >> 1) & 1, t = ref & 1;
+  const int4 c = tab[idx];
+  if (diag) return make_int4(sref(c.x, 1, 0), sref(c.y, 0, 0), sref(c.y, 0, 1), sref(c.w, 1, 0));
+  if (t) return make_int4(sref(c.x, 0, 1), sref(c.z, 0, 1), sref(c.y, 0, 1), sref(c.w, 0, 1));
+  return make_int4(sref(c.x, 0, 0), sref(c.y, 0, 0), sref(c.z, 0, 0), sref(c.w, 0, 0));
+}
+
 }  // namespace qt

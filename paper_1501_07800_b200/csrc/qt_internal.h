@@ -163,6 +163,8 @@ void build_levels(qt_mat M, const int32_t* leaf_ids = nullptr);
 inline void ensure_levels(qt_mat M) {
   if (!M->levels_built) { build_levels(M); M->levels_built = true; }
 }
+// QT_EINVAL unless every block has brow <= bcol (upper block triangle)
+void check_upper(qt_mat M);
 // row-major (brow, bcol) order and un-swizzle into caller buffers
 void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals);
 // truncate (reading C-16): local terms, global decision, single-rank driver
@@ -193,7 +195,7 @@ struct NumericArgs {
   void* poolC;
   int* counter;              // tile scheduler counter (zeroed before launch)
   int group = 1;             // tiles per scheduler grab (1..31)
-  int trans = 0;             // bit 0: A transposed, bit 1: B transposed
+  int trans = 0;             // bit 0: A transposed, bit 1: B transposed, bit 2: symmetric square
 };
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a);
 

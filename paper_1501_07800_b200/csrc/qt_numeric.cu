@@ -46,8 +46,20 @@ struct __align__(16) StageHdr {
   int b[2];
   int c[4];
   int flags;
-  int pad[3];
+  int tbits;  // symmetric square: bit i = A(i,k) transposed, bit 2+j = B(k,j) transposed
+  int pad[2];
 };
+
+// a level L-1 child entry -> (block index, transposed) ; plain indices unless symmetric
+template <bool kSym>
+__device__ __forceinline__ int blk(int ref, int& t) {
+  if (!kSym) {
+    t = 0;
+    return ref;
+  }
+  t = ref >= 0 ? (ref & 1) : 0;
+  return ref >= 0 ? (ref >> 2) : -1;
+}
 
 constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + kStages * sizeof(StageHdr) +
                               2 * kStages * sizeof(uint64_t);
@@ -124,19 +136,8 @@ __device__ __forceinline__ void warp_block_mma(double (&acc)[4][4][2], const dou
   }
 }
 
-// child slots of op(X): a transposed node swaps its off-diagonal children
-template <bool kT>
-__device__ __forceinline__ int4 ldchild(const int4* __restrict__ tab, int idx) {
-  int4 c = tab[idx];
-  if (kT) {
-    const int t = c.y;
-    c.y = c.z;
-    c.z = t;
-  }
-  return c;
-}
 
-template <bool kGrouped, bool kTA, bool kTB>
+template <bool kGrouped, bool kTA, bool kTB, bool kSym>
 __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -217,8 +218,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         const int p = pb0 + lane;
         int4 ca = make_int4(-1, -1, -1, -1), cb = ca;
         if (p < p_end) {
-          ca = ldchild<kTA>(a.childA, a.pa[p]);
-          cb = ldchild<kTB>(a.childB, a.pb[p]);
+          ca = op_children(a.childA, a.pa[p], kTA, kSym);
+          cb = op_children(a.childB, a.pb[p], kTB, kSym);
         }
         const int nloc = min(32, p_end - pb0);
         for (int u = 0; u < nloc; ++u) {
@@ -232,8 +233,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
 #pragma unroll
           for (int kb = 0; kb < 2; ++kb) {
             // A child (i,kb) in slot 2i+kb ; B child (kb,j) in slot 2kb+j
-            const int a0 = kb ? A4.y : A4.x, a1 = kb ? A4.w : A4.z;
-            const int b0 = kb ? B4.z : B4.x, b1 = kb ? B4.w : B4.y;
+            int ta0, ta1, tb0, tb1;
+            const int a0 = blk<kSym>(kb ? A4.y : A4.x, ta0), a1 = blk<kSym>(kb ? A4.w : A4.z, ta1);
+            const int b0 = blk<kSym>(kb ? B4.z : B4.x, tb0), b1 = blk<kSym>(kb ? B4.w : B4.y, tb1);
             if (!((a0 >= 0 || a1 >= 0) && (b0 >= 0 || b1 >= 0))) continue;
             mbar_wait(&empty[stage], phase ^ 1);
             if (lane == 0) {
@@ -243,6 +245,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
               h.b[0] = b0;
               h.b[1] = b1;
               h.flags = F_COMPUTE;
+              h.tbits = ta0 | (ta1 << 1) | (tb0 << 2) | (tb1 << 3);
               const uint32_t bytes = 8192u * ((a0 >= 0) + (a1 >= 0) + (b0 >= 0) + (b1 >= 0));
               mbar_arrive_expect_tx(&full[stage], bytes);
               double* dst = data + (size_t)stage * kStageElems;
@@ -296,8 +299,8 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         const int p = pb0 + lane;
         int4 ca = make_int4(-1, -1, -1, -1), cb = ca;
         if (p < p1) {
-          ca = ldchild<kTA>(a.childA, a.pa[p]);
-          cb = ldchild<kTB>(a.childB, a.pb[p]);
+          ca = op_children(a.childA, a.pa[p], kTA, kSym);
+          cb = op_children(a.childB, a.pb[p], kTB, kSym);
         }
         const int nloc = min(32, p1 - pb0);
         for (int u = 0; u < nloc; ++u) {
@@ -306,8 +309,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
 #pragma unroll
           for (int kb = 0; kb < 2; ++kb) {
             // A child (i,kb) in slot 2i+kb ; B child (kb,j) in slot 2kb+j
-            const int a0 = kb ? A4.y : A4.x, a1 = kb ? A4.w : A4.z;
-            const int b0 = kb ? B4.z : B4.x, b1 = kb ? B4.w : B4.y;
+            int ta0, ta1, tb0, tb1;
+            const int a0 = blk<kSym>(kb ? A4.y : A4.x, ta0), a1 = blk<kSym>(kb ? A4.w : A4.z, ta1);
+            const int b0 = blk<kSym>(kb ? B4.z : B4.x, tb0), b1 = blk<kSym>(kb ? B4.w : B4.y, tb1);
             if (!((a0 >= 0 || a1 >= 0) && (b0 >= 0 || b1 >= 0))) continue;
             mbar_wait(&empty[stage], phase ^ 1);
             if (lane == 0) {
@@ -317,6 +321,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
               h.b[0] = b0;
               h.b[1] = b1;
               h.flags = F_COMPUTE;
+              h.tbits = ta0 | (ta1 << 1) | (tb0 << 2) | (tb1 << 3);
               const uint32_t bytes = 8192u * ((a0 >= 0) + (a1 >= 0) + (b0 >= 0) + (b1 >= 0));
               mbar_arrive_expect_tx(&full[stage], bytes);
               double* dst = data + (size_t)stage * kStageElems;
@@ -397,7 +402,20 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         const bool go = h.a[wi] >= 0 && h.b[wj] >= 0;
         if (go) {
           const double* st = data + (size_t)stage * kStageElems;
-          warp_block_mma<kTA, kTB>(acc, st + wi * kBlockElems, st + (2 + wj) * kBlockElems, lane);
+          const double* As = st + wi * kBlockElems;
+          const double* Bs = st + (2 + wj) * kBlockElems;
+          if (kSym) {
+            // per-block transposes of the symmetric expansion (warp-uniform)
+            const int tb = h.tbits;
+            switch (((tb >> wi) & 1) | (((tb >> (2 + wj)) & 1) << 1)) {
+              case 0: warp_block_mma<false, false>(acc, As, Bs, lane); break;
+              case 1: warp_block_mma<true, false>(acc, As, Bs, lane); break;
+              case 2: warp_block_mma<false, true>(acc, As, Bs, lane); break;
+              default: warp_block_mma<true, true>(acc, As, Bs, lane); break;
+            }
+          } else {
+            warp_block_mma<kTA, kTB>(acc, As, Bs, lane);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
@@ -443,15 +461,15 @@ __global__ void k_peak_dfma(double* out, int iters) {
 
 }  // namespace
 
-template <bool G, bool TA, bool TB>
+template <bool G, bool TA, bool TB, bool SYM = false>
 static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
   static bool attr_set = false;
   if (!attr_set) {
-    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<G, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemBytes));
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<G, TA, TB, SYM>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
     attr_set = true;
   }
-  k_numeric_f64<G, TA, TB><<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
+  k_numeric_f64<G, TA, TB, SYM><<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
 }
 
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a) {
@@ -461,6 +479,12 @@ void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a) {
   // one tile per grab (dense/banded: finest dynamic balance) or grouped grabs
   // (sparse patterns: amortise the scheduler and metadata latency)
   const bool G = a.group > 1;
+  if (a.trans & 4) {  // symmetric square
+    if (G) launch_numeric_t<true, false, false, true>(ctx, a, grid);
+    else launch_numeric_t<false, false, false, true>(ctx, a, grid);
+    QT_LAUNCH_CHECK(ctx);
+    return;
+  }
   switch ((G ? 4 : 0) | (a.trans & 3)) {
     case 0: launch_numeric_t<false, false, false>(ctx, a, grid); break;
     case 1: launch_numeric_t<false, true, false>(ctx, a, grid); break;

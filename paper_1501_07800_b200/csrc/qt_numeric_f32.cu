@@ -173,16 +173,6 @@ __host__ __device__ constexpr uint32_t idesc_tf32() {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((kTA ? 1u : 0u) << 15) | ((kTB ? 0u : 1u) << 16) |
          ((128u >> 3) << 17) | ((128u >> 4) << 24);
 }
-template <bool kT>
-__device__ __forceinline__ int4 ldchild(const int4* __restrict__ tab, int idx) {
-  int4 c = tab[idx];
-  if (kT) {
-    const int t = c.y;
-    c.y = c.z;
-    c.z = t;
-  }
-  return c;
-}
 
 template <bool kTA, bool kTB>
 __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
@@ -249,22 +239,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
 #pragma unroll
           for (int y = 0; y < 4; ++y) ab[x][y] = bb[x][y] = -1;
         if (p < p1) {
-          const int4 qa = ldchild<kTA>(a.childA2, a.pa[p]);  // op(A) quads (i', k') in slot 2i'+k'
-          const int4 qb = ldchild<kTB>(a.childB2, a.pb[p]);  // op(B) quads (k', j') in slot 2k'+j'
+          const int4 qa = ldchild(a.childA2, a.pa[p], kTA);  // op(A) quads (i', k') in slot 2i'+k'
+          const int4 qb = ldchild(a.childB2, a.pb[p], kTB);  // op(B) quads (k', j') in slot 2k'+j'
           const int qa_[4] = {qa.x, qa.y, qa.z, qa.w};
           const int qb_[4] = {qb.x, qb.y, qb.z, qb.w};
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
             const int hi = s >> 1, lo = s & 1;
             if (qa_[s] >= 0) {
-              const int4 c = ldchild<kTA>(a.childA1, qa_[s]);  // (i'', k'') in slot 2i''+k''
+              const int4 c = ldchild(a.childA1, qa_[s], kTA);  // (i'', k'') in slot 2i''+k''
               ab[2 * hi + 0][2 * lo + 0] = c.x;
               ab[2 * hi + 0][2 * lo + 1] = c.y;
               ab[2 * hi + 1][2 * lo + 0] = c.z;
               ab[2 * hi + 1][2 * lo + 1] = c.w;
             }
             if (qb_[s] >= 0) {
-              const int4 c = ldchild<kTB>(a.childB1, qb_[s]);  // (k'', j'') in slot 2k''+j''
+              const int4 c = ldchild(a.childB1, qb_[s], kTB);  // (k'', j'') in slot 2k''+j''
               bb[2 * hi + 0][2 * lo + 0] = c.x;
               bb[2 * hi + 0][2 * lo + 1] = c.y;
               bb[2 * hi + 1][2 * lo + 0] = c.z;

@@ -63,17 +63,10 @@ __global__ void k_level_tasks(const int32_t* __restrict__ histA, const int32_t* 
   if (threadIdx.x == 0) out[l] = s;
 }
 
-// Child slots of op(X): the transpose of a node has its off-diagonal children
-// swapped (slot 1 <-> 2) and each child transposed in turn — so for a globally
-// transposed operand (C = A^T B etc.) only the slot order changes.
-__device__ __forceinline__ int4 ldchild(const int4* __restrict__ tab, int idx, bool trans) {
-  int4 c = tab[idx];
-  if (trans) {
-    const int t = c.y;
-    c.y = c.z;
-    c.z = t;
-  }
-  return c;
+// C node on the block diagonal: in the symmetric square only its upper
+// children exist (the (1,0) child is the transpose of (0,1), not computed)
+__device__ __forceinline__ bool on_diagonal(uint64_t ckey) {
+  return morton_row(ckey) == morton_col(ckey);
 }
 
 // A child (i,k) sits in slot 2i+k, B child (k,j) in slot 2k+j, C child (i,j) in 2i+j.
@@ -87,13 +80,14 @@ __device__ __forceinline__ void child_counts(int4 a, int4 b, int (&c)[4]) {
 // Write the child tasks of task p (group s, local index loc) at the exclusive
 // offsets `off` of its (s,q) slots; gidx maps (s,q) to the new group index.
 __device__ __forceinline__ void emit_task(int4 a4, int4 b4, int64_t base, int32_t m, int32_t s,
-                                          const int32_t* __restrict__ off,
+                                          bool skip_lower, const int32_t* __restrict__ off,
                                           const int32_t* __restrict__ gidx, int32_t* __restrict__ pa2,
                                           int32_t* __restrict__ pb2, int32_t* __restrict__ pc2) {
   const int a[4] = {a4.x, a4.y, a4.z, a4.w};
   const int b[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
+    if (skip_lower && q == 2) continue;
     const int i = q >> 1, j = q & 1;
     int32_t pos = -1, newc = -1;
 #pragma unroll
@@ -117,7 +111,7 @@ __device__ __forceinline__ void emit_task(int4 a4, int4 b4, int64_t base, int32_
 
 struct SmallBfsArgs {
   int l_end;  // run transitions l -> l+1 for l < l_end
-  int trans;  // bit 0: A transposed, bit 1: B transposed
+  int trans;  // mode: bit 0 A transposed, bit 1 B transposed, bit 2 symmetric square
   const int4* childA[QT_MAX_LEVELS];
   const int4* childB[QT_MAX_LEVELS];
   int32_t* pa[2];
@@ -128,6 +122,7 @@ struct SmallBfsArgs {
   int32_t* off;     // 4 * max F scratch (counts, then exclusive offsets in place)
   int32_t* gidx;    // 4 * max ns scratch
   int32_t* ns_out;  // C groups per level
+  int32_t* f_out;   // tasks per level
 };
 
 __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) {
@@ -135,10 +130,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
   __shared__ typename BS::TempStorage tmp;
   __shared__ int s_F, s_ns;
   const int tid = threadIdx.x;
+  const bool sym = a.trans & 4;
   if (tid == 0) {
-    a.pa[0][0] = 0;
-    a.pb[0][0] = 0;
+    a.pa[0][0] = sym ? 2 : 0;  // the root (a diagonal node in the symmetric square)
+    a.pb[0][0] = sym ? 2 : 0;
     a.pc[0][0] = 0;
+    a.f_out[0] = 1;
     a.cstart[0][0] = 0;
     a.cstart[0][1] = 1;
     a.ckey[0][0] = 0;
@@ -161,7 +158,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     for (int p = tid; p < F; p += kSmallThreads) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
       int c[4];
-      child_counts(ldchild(cA, pa[p], a.trans & 1), ldchild(cB, pb[p], a.trans & 2), c);
+      child_counts(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym), c);
+      if (sym && on_diagonal(ck[s])) c[2] = 0;
       const int64_t base = 4ll * c0 + (p - c0);
 #pragma unroll
       for (int q = 0; q < 4; ++q) a.off[base + (int64_t)q * m] = c[q];
@@ -208,13 +206,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     if (tid == 0) {
       a.cstart[nxt][nsn] = Fn;
       a.ns_out[l + 1] = nsn;
+      a.f_out[l + 1] = Fn;
     }
     __syncthreads();
     // 4. emit the child tasks
     for (int p = tid; p < F; p += kSmallThreads) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
-      emit_task(ldchild(cA, pa[p], a.trans & 1), ldchild(cB, pb[p], a.trans & 2), 4ll * c0 + (p - c0),
-                m, s, a.off, a.gidx, a.pa[nxt], a.pb[nxt],
+      emit_task(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym),
+                4ll * c0 + (p - c0), m, s, sym && on_diagonal(ck[s]), a.off, a.gidx, a.pa[nxt], a.pb[nxt],
                 a.pc[nxt]);
     }
     __syncthreads();
@@ -228,24 +227,36 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
 
 // ------------------------------------------------------------ large levels (grid-wide)
 
-__global__ void k_count(int32_t F, const int32_t* __restrict__ pa, const int32_t* __restrict__ pb,
-                        const int32_t* __restrict__ pc, const int32_t* __restrict__ cstart,
-                        const int4* __restrict__ childA, const int4* __restrict__ childB, int trans,
+// Launch sizes come from host-side bounds (exact for regular products); the
+// actual task count of the level is read from f_dev.  Threads of "virtual"
+// tasks p in [F, Fb) zero the count positions [4p, 4p+4), so the scan over
+// 4*Fb positions is exact.
+__global__ void k_count(int32_t Fb, const int32_t* __restrict__ f_dev, const int32_t* __restrict__ pa,
+                        const int32_t* __restrict__ pb, const int32_t* __restrict__ pc,
+                        const int32_t* __restrict__ cstart, const uint64_t* __restrict__ ckey,
+                        const int4* __restrict__ childA, const int4* __restrict__ childB, int mode,
                         int32_t* __restrict__ cnt) {
   const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= F) return;
+  if (p >= Fb) return;
+  if (p >= *f_dev) {
+    *reinterpret_cast<int4*>(cnt + 4ll * p) = make_int4(0, 0, 0, 0);
+    return;
+  }
+  const bool sym = mode & 4;
   const int32_t s = pc[p], c0 = cstart[s], m = cstart[s + 1] - c0;
   int c[4];
-  child_counts(ldchild(childA, pa[p], trans & 1), ldchild(childB, pb[p], trans & 2), c);
+  child_counts(op_children(childA, pa[p], mode & 1, sym), op_children(childB, pb[p], mode & 2, sym), c);
+  if (sym && on_diagonal(ckey[s])) c[2] = 0;
   const int64_t base = 4ll * c0 + (p - c0);
 #pragma unroll
   for (int q = 0; q < 4; ++q) cnt[base + (int64_t)q * m] = c[q];
 }
 
 // per (s,q) slot: start of the new group and non-empty flag (0 beyond the real ns)
-__global__ void k_segs(int32_t nsb, const int32_t* __restrict__ ns_dev, int32_t F, int32_t Fn,
+__global__ void k_segs(int32_t nsb, const int32_t* __restrict__ ns_dev, int64_t n4,
                        const int32_t* __restrict__ cstart, const int32_t* __restrict__ off,
-                       int32_t* __restrict__ flag, int32_t* __restrict__ gstart) {
+                       const int32_t* __restrict__ cnt, int32_t* __restrict__ flag,
+                       int32_t* __restrict__ gstart) {
   const int32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= 4 * nsb) return;
   const int32_t ns = *ns_dev;
@@ -254,25 +265,29 @@ __global__ void k_segs(int32_t nsb, const int32_t* __restrict__ ns_dev, int32_t 
     const int32_t s = x >> 2, q = x & 3, c0 = cstart[s], m = cstart[s + 1] - c0;
     const int64_t lo = 4ll * c0 + (int64_t)q * m, hi = lo + m;
     st = off[lo];
-    const int32_t en = hi < 4ll * F ? off[hi] : Fn;
+    const int32_t en = hi < n4 ? off[hi] : off[n4 - 1] + cnt[n4 - 1];
     f = en > st;
   }
   flag[x] = f;
   gstart[x] = st;
 }
 
-__global__ void k_newc(int32_t nsb, const int32_t* __restrict__ ns_dev, int32_t Fn,
+__global__ void k_newc(int32_t nsb, const int32_t* __restrict__ ns_dev, int64_t n4,
+                       const int32_t* __restrict__ off, const int32_t* __restrict__ cnt,
                        const int32_t* __restrict__ flag, const int32_t* __restrict__ nex,
                        const int32_t* __restrict__ gstart, const uint64_t* __restrict__ ckey,
                        int32_t* __restrict__ cstart_next, uint64_t* __restrict__ ckey_next,
-                       int32_t* __restrict__ gidx, int32_t* __restrict__ ns_next) {
+                       int32_t* __restrict__ gidx, int32_t* __restrict__ ns_next,
+                       int32_t* __restrict__ f_next) {
   const int32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   const int32_t ns = *ns_dev;
   if (x >= 4 * ns) return;
   if (x == 4 * ns - 1) {
     const int32_t nsn = nex[x] + flag[x];
+    const int32_t Fn = off[n4 - 1] + cnt[n4 - 1];
     cstart_next[nsn] = Fn;
     *ns_next = nsn;
+    *f_next = Fn;
   }
   if (flag[x]) {
     const int32_t t = nex[x];
@@ -284,17 +299,36 @@ __global__ void k_newc(int32_t nsb, const int32_t* __restrict__ ns_dev, int32_t 
   }
 }
 
-__global__ void k_emit(int32_t F, const int32_t* __restrict__ pa, const int32_t* __restrict__ pb,
-                       const int32_t* __restrict__ pc, const int32_t* __restrict__ cstart,
-                       const int4* __restrict__ childA, const int4* __restrict__ childB, int trans,
+__global__ void k_emit(int32_t Fb, const int32_t* __restrict__ f_dev, const int32_t* __restrict__ pa,
+                       const int32_t* __restrict__ pb, const int32_t* __restrict__ pc,
+                       const int32_t* __restrict__ cstart, const uint64_t* __restrict__ ckey,
+                       const int4* __restrict__ childA, const int4* __restrict__ childB, int mode,
                        const int32_t* __restrict__ off, const int32_t* __restrict__ gidx,
                        int32_t* __restrict__ pa2, int32_t* __restrict__ pb2,
                        int32_t* __restrict__ pc2) {
   const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= F) return;
+  if (p >= Fb || p >= *f_dev) return;
+  const bool sym = mode & 4;
   const int32_t s = pc[p], c0 = cstart[s], m = cstart[s + 1] - c0;
-  emit_task(ldchild(childA, pa[p], trans & 1), ldchild(childB, pb[p], trans & 2), 4ll * c0 + (p - c0),
-            m, s, off, gidx, pa2, pb2, pc2);
+  emit_task(op_children(childA, pa[p], mode & 1, sym), op_children(childB, pb[p], mode & 2, sym),
+            4ll * c0 + (p - c0), m, s, sym && on_diagonal(ckey[s]), off, gidx, pa2, pb2, pc2);
+}
+
+// Upper bound of the symmetric square's tasks per level: with the full
+// matrix's column and row counts both bounded by rows(U) + cols(U).
+__global__ void k_level_tasks_sym(const int32_t* __restrict__ hist, int64_t H,
+                                  int64_t* __restrict__ out) {
+  using BR = cub::BlockReduce<long long, kThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  const int l = blockIdx.x;
+  const int64_t base = (1ll << l) - 1, m = 1ll << l;
+  long long s = 0;
+  for (int64_t K = threadIdx.x; K < m; K += blockDim.x) {
+    const long long c = (long long)hist[base + K] + hist[H + base + K];
+    s += c * c;
+  }
+  s = BR(tmp).Sum(s);
+  if (threadIdx.x == 0) out[l] = s;
 }
 
 template <class T>
@@ -327,6 +361,8 @@ struct Trace {
 };
 
 qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* ms_num, int trans) {
+  // trans: bit 0 A^T, bit 1 B^T, bit 2 symmetric square (A = B = U, C upper)
+  const bool sym = trans & 4;
   Trace tr;
   qt_ctx ctx = A->ctx;
   cudaStream_t st = ctx->stream;
@@ -355,11 +391,15 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
     QT_CUDA(cudaEventRecord(ctx->ev[2], st));
     std::vector<int64_t> F(L + 1, 0);
     if (A->nb > 0 && B->nb > 0) {
-      // exact task counts per level (one sync)
+      // task counts per level (one sync): exact for regular products, an upper
+      // bound for the symmetric square (its actual counts come from the BFS)
       const int64_t H = 2ll << L;
       DevBuf dF(8 * (L + 1), st);
-      k_level_tasks<<<L + 1, kThreads, 0, st>>>(A->hist.as<int32_t>(), B->hist.as<int32_t>(), H,
-                                               trans, dF.as<int64_t>());
+      if (sym)
+        k_level_tasks_sym<<<L + 1, kThreads, 0, st>>>(A->hist.as<int32_t>(), H, dF.as<int64_t>());
+      else
+        k_level_tasks<<<L + 1, kThreads, 0, st>>>(A->hist.as<int32_t>(), B->hist.as<int32_t>(), H,
+                                                 trans, dF.as<int64_t>());
       QT_LAUNCH_CHECK(ctx);
       QT_CUDA(cudaMemcpyAsync(F.data(), dF.p, 8 * (L + 1), cudaMemcpyDeviceToHost, st));
       QT_CUDA(cudaStreamSynchronize(st));
@@ -378,8 +418,9 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       // upper bounds of the group counts: ns_{l+1} <= min(4 ns_l, F_{l+1})
       std::vector<int64_t> nsb(L + 1, 1);
       for (int l = 0; l < L; ++l) nsb[l + 1] = std::min<int64_t>(4 * nsb[l], F[l + 1]);
-      DevBuf ns_dev(4 * (L + 1), st);
+      DevBuf ns_dev(4 * (L + 1), st), f_dev(4 * (L + 1), st);
       int32_t* nsd = ns_dev.as<int32_t>();
+      int32_t* fd = f_dev.as<int32_t>();
       // --- small levels in one CTA
       const bool f32 = C->dtype == QT_F32;
       int l_end = 0;
@@ -415,6 +456,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       sa.off = soff.as<int32_t>();
       sa.gidx = sg.as<int32_t>();
       sa.ns_out = nsd;
+      sa.f_out = fd;
       tr.mark("small_alloc");
       k_bfs_small<<<1, kSmallThreads, 0, st>>>(sa);
       QT_LAUNCH_CHECK(ctx);
@@ -426,39 +468,42 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       tr.mark("small_launch");
       for (int l = l_end; l < L; ++l) {
         const bool last = (l == L - 1);
-        const int32_t Fl = (int32_t)F[l], Fn = (int32_t)F[l + 1];
-        const int64_t n4 = 4ll * Fl, s4 = 4ll * nsb[l];
+        const int32_t Fb = (int32_t)F[l];  // launch bound (exact unless symmetric)
+        const int64_t n4 = 4ll * Fb, s4 = 4ll * nsb[l];
         DevBuf cnt(4 * n4, st), off(4 * n4, st);
-        k_count<<<grid_for(Fl), kThreads, 0, st>>>(Fl, pa.as<int32_t>(), pb.as<int32_t>(),
+        k_count<<<grid_for(Fb), kThreads, 0, st>>>(Fb, fd + l, pa.as<int32_t>(), pb.as<int32_t>(),
                                                    pc.as<int32_t>(), cstart.as<int32_t>(),
-                                                   A->child[l].as<int4>(), B->child[l].as<int4>(),
-                                                   trans, cnt.as<int32_t>());
+                                                   ckey.as<uint64_t>(), A->child[l].as<int4>(),
+                                                   B->child[l].as<int4>(), trans, cnt.as<int32_t>());
         QT_LAUNCH_CHECK(ctx);
         excl_sum(ctx, cnt.as<int32_t>(), off.as<int32_t>(), n4);
         DevBuf flag(4 * s4, st), gstart(4 * s4, st), nex(4 * s4, st), gidx(4 * s4, st);
-        k_segs<<<grid_for(s4), kThreads, 0, st>>>((int32_t)nsb[l], nsd + l, Fl, Fn,
-                                                  cstart.as<int32_t>(), off.as<int32_t>(),
+        k_segs<<<grid_for(s4), kThreads, 0, st>>>((int32_t)nsb[l], nsd + l, n4, cstart.as<int32_t>(),
+                                                  off.as<int32_t>(), cnt.as<int32_t>(),
                                                   flag.as<int32_t>(), gstart.as<int32_t>());
         QT_LAUNCH_CHECK(ctx);
         excl_sum(ctx, flag.as<int32_t>(), nex.as<int32_t>(), s4);
         DevBuf cstart2(4 * (nsb[l + 1] + 1), st), ckey2(8 * std::max<int64_t>(nsb[l + 1], 1), st);
-        k_newc<<<grid_for(s4), kThreads, 0, st>>>((int32_t)nsb[l], nsd + l, Fn, flag.as<int32_t>(),
+        k_newc<<<grid_for(s4), kThreads, 0, st>>>((int32_t)nsb[l], nsd + l, n4, off.as<int32_t>(),
+                                                  cnt.as<int32_t>(), flag.as<int32_t>(),
                                                   nex.as<int32_t>(), gstart.as<int32_t>(),
                                                   ckey.as<uint64_t>(), cstart2.as<int32_t>(),
-                                                  ckey2.as<uint64_t>(), gidx.as<int32_t>(), nsd + l + 1);
+                                                  ckey2.as<uint64_t>(), gidx.as<int32_t>(), nsd + l + 1,
+                                                  fd + l + 1);
         QT_LAUNCH_CHECK(ctx);
         if (last) {
           C->key = std::move(ckey2);
           cchild = std::move(gidx);
           break;
         }
-        DevBuf pa2(4ll * Fn, st), pb2(4ll * Fn, st), pc2(4ll * Fn, st);
-        k_emit<<<grid_for(Fl), kThreads, 0, st>>>(Fl, pa.as<int32_t>(), pb.as<int32_t>(),
+        const int64_t Fnb = F[l + 1];
+        DevBuf pa2(4 * Fnb, st), pb2(4 * Fnb, st), pc2(4 * Fnb, st);
+        k_emit<<<grid_for(Fb), kThreads, 0, st>>>(Fb, fd + l, pa.as<int32_t>(), pb.as<int32_t>(),
                                                   pc.as<int32_t>(), cstart.as<int32_t>(),
-                                                  A->child[l].as<int4>(), B->child[l].as<int4>(),
-                                                  trans, off.as<int32_t>(), gidx.as<int32_t>(),
-                                                  pa2.as<int32_t>(), pb2.as<int32_t>(),
-                                                  pc2.as<int32_t>());
+                                                  ckey.as<uint64_t>(), A->child[l].as<int4>(),
+                                                  B->child[l].as<int4>(), trans, off.as<int32_t>(),
+                                                  gidx.as<int32_t>(), pa2.as<int32_t>(),
+                                                  pb2.as<int32_t>(), pc2.as<int32_t>());
         QT_LAUNCH_CHECK(ctx);
         if (f32 && l == L - 2) {  // keep the level L-2 queue: the FP32 work items
           t2_pa = std::move(pa);
@@ -474,11 +519,17 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       }
       // --- group counts of every level (the one remaining sync): C's block count
       tr.mark("levels_launched");
-      std::vector<int32_t> ns(L + 1, 0);
+      std::vector<int32_t> ns(L + 1, 0), Fa(L + 1, 0);
       QT_CUDA(cudaMemcpyAsync(ns.data(), nsd, 4 * (L + 1), cudaMemcpyDeviceToHost, st));
+      QT_CUDA(cudaMemcpyAsync(Fa.data(), fd, 4 * (L + 1), cudaMemcpyDeviceToHost, st));
       QT_CUDA(cudaStreamSynchronize(st));
       tr.mark("levels_done");
-      for (int l = 0; l <= L; ++l) S.level_c_nodes[l] = ns[l];
+      for (int l = 0; l <= L; ++l) {
+        S.level_c_nodes[l] = ns[l];
+        S.level_tasks[l] = Fa[l];  // actual counts (== F for regular products)
+        F[l] = Fa[l];
+      }
+      S.block_products = Fa[L];
       C->nb = ns[L];
       C->pool.alloc((size_t)C->nb * 1024 * elem_size(C->dtype), st);
       tr.mark("c_alloc");
@@ -497,7 +548,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       na.splitB = B->split;
       na.poolC = C->pool.p;
       na.counter = ctx->counters.as<int>() + 16;
-      na.trans = trans;
+      na.trans = trans;  // bit 2: symmetric square (block refs carry transpose bits)
       // tiles per scheduler grab: ~32 tasks per grab, at most 16 tiles
       {
         const int64_t per_tile = std::max<int64_t>(1, F[L - 1] / std::max<int32_t>(1, ns[L - 1]));
@@ -513,6 +564,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         }
       }
       if (C->nb > 0 && !f32) launch_numeric(ctx, C->dtype, na);
+      if (C->nb > 0 && f32 && sym) fail(QT_EDTYPE, "the symmetric square is FP64-only in this build");
       if (C->nb > 0 && f32) {
         NumericArgs32 nb;
         nb.ntiles = ns[L - 2];

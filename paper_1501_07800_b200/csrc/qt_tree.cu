@@ -300,6 +300,32 @@ void build_from_blocks(qt_mat M, int64_t nb, const int32_t* d_brow, const int32_
   build_levels(M);
 }
 
+namespace {
+__global__ void k_lower_count(const uint64_t* __restrict__ key, int64_t n, unsigned long long* bad) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = key[t];
+    if (morton_row(k) > morton_col(k)) atomicMin(bad, (unsigned long long)t);
+  }
+}
+}  // namespace
+
+void check_upper(qt_mat M) {
+  qt_ctx ctx = M->ctx;
+  if (M->nb == 0) return;
+  unsigned long long* bad = ctx->counters.as<unsigned long long>();
+  QT_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
+  k_lower_count<<<grid_for(M->nb), kThreads, 0, ctx->stream>>>(M->key.as<uint64_t>(), M->nb, bad);
+  QT_LAUNCH_CHECK(ctx);
+  const unsigned long long b = read_scalar(ctx, bad);
+  if (b != ~0ull) {
+    uint64_t k;
+    QT_CUDA(cudaMemcpy(&k, M->key.as<uint64_t>() + b, 8, cudaMemcpyDeviceToHost));
+    fail(QT_EINVAL, "symmetric square needs upper-triangular block storage; block (brow=%u, bcol=%u) "
+         "is below the diagonal", morton_row(k), morton_col(k));
+  }
+}
+
 void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals) {
   qt_ctx ctx = M->ctx;
   cudaStream_t st = ctx->stream;

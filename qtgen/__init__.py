@@ -145,12 +145,15 @@ def pattern_random(nbr: int, p: float, seed_pat: int, rows=None):
 
 
 def block_values(brow, bcol, bs: int, seed: int, kind: str = "uniform",
-                 band_d: int | None = None, scale=None, chunk: int = 4096) -> np.ndarray:
+                 band_d: int | None = None, scale=None, chunk: int = 4096,
+                 symmetric: bool = False) -> np.ndarray:
     """Values of the listed blocks: element (i, j) = F(h(seed, i, j)).
 
     ``kind``: "uniform" (uniform[-1,1]), "int" (integers -4..4), "ones".
     ``band_d``: zero the entries with |i-j| > band_d (banded configs).
     ``scale``: optional per-block multiplier (ES-like config).
+    ``symmetric``: hash the unordered pair (min(i,j), max(i,j)), so that the
+    matrix is symmetric (inputs of the symmetric square).
     """
     nb = len(brow)
     out = np.empty((nb, bs, bs), dtype=np.float64)
@@ -162,7 +165,7 @@ def block_values(brow, bcol, bs: int, seed: int, kind: str = "uniform",
         if kind == "ones":
             v = np.ones((e - s, bs, bs))
         else:
-            h = hash3(seed, R, C)
+            h = hash3(seed, np.minimum(R, C), np.maximum(R, C)) if symmetric else hash3(seed, R, C)
             v = uniform_pm1(h) if kind == "uniform" else int_pm4(h)
         if band_d is not None:
             v = np.where(np.abs(R - C) <= band_d, v, 0.0)
@@ -222,8 +225,14 @@ def pattern_es(pos: np.ndarray, rc: float, rows=None):
 # the BASELINE configs
 
 
+def upper(M: "BlockMatrix") -> "BlockMatrix":
+    """The upper block triangle (brow <= bcol) of a block list."""
+    k = M.brow <= M.bcol
+    return BlockMatrix(M.n, M.leaf_dim, M.bs, M.brow[k], M.bcol[k], M.vals[k])
+
+
 def config(idx: int, kind: str = "uniform", P: int = 1, rank: int | None = None,
-           rows=None, small: bool = False) -> dict:
+           rows=None, small: bool = False, symmetric: bool = False) -> dict:
     """Inputs of BASELINE.json configs[idx-1] (idx in 1..5).
 
     Returns ``{"name", "A", "B", "same"}``; ``B is A`` when the config computes
@@ -258,7 +267,8 @@ def config(idx: int, kind: str = "uniform", P: int = 1, rank: int | None = None,
             per = nbr // P
             rows = (rank * per, (rank + 1) * per)
         ar, ac = pattern_banded(nbr, D, rows)
-        A = BlockMatrix(n, leaf, bs, ar, ac, block_values(ar, ac, bs, SEED_A_VAL, kind, band_d=d))
+        A = BlockMatrix(n, leaf, bs, ar, ac,
+                        block_values(ar, ac, bs, SEED_A_VAL, kind, band_d=d, symmetric=symmetric))
         name = f"cfg{idx}-banded-N{n}-d{d}"
         return {"name": name, "A": A, "B": A, "same": True, "d": d}
     if idx == 3:
@@ -278,7 +288,8 @@ def config(idx: int, kind: str = "uniform", P: int = 1, rank: int | None = None,
             leaf = 1024
         ar, ac, r = pattern_es(pos, 7.0, rows)
         scale = np.exp(-0.5 * r) if kind == "uniform" else None
-        A = BlockMatrix(n, leaf, bs, ar, ac, block_values(ar, ac, bs, SEED_A_VAL, kind, scale=scale))
+        A = BlockMatrix(n, leaf, bs, ar, ac,
+                        block_values(ar, ac, bs, SEED_A_VAL, kind, scale=scale, symmetric=symmetric))
         return {"name": f"cfg4-eslike-N{n}", "A": A, "B": A, "same": True}
     raise ValueError(f"unknown config {idx}")
 

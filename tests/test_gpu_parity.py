@@ -519,3 +519,66 @@ def test_transposed_aat_banded(qt, ctx):
     ref = oracle.spgemm_t(c["A"].nbr, 32, as_tuple(c["A"]), as_tuple(c["A"]), False, True)
     assert_same_pattern(got, ref)
     assert np.array_equal(got[2], ref[2])
+
+
+# ----------------------------------------------------------------- symmetric square (§3.3)
+
+
+def random_sym_upper(rng, nbr, p, kind, leaf):
+    mask = np.triu(rng.random((nbr, nbr)) < p)
+    np.fill_diagonal(mask, rng.random(nbr) < 0.7)
+    br, bc = np.nonzero(mask)
+    v = (rng.integers(-4, 5, size=(len(br), 32, 32)).astype(np.float64) if kind == "int"
+         else rng.uniform(-1, 1, size=(len(br), 32, 32)))
+    for t in range(len(br)):
+        if br[t] == bc[t]:
+            v[t] = np.triu(v[t]) + np.triu(v[t], 1).T
+    return qtgen.BlockMatrix(nbr * 32, leaf, 32, br.astype(np.int32), bc.astype(np.int32), v)
+
+
+@pytest.mark.parametrize("nbr,p,leaf", [(1, 1.0, 32), (4, 1.0, 64), (7, 0.5, 64), (24, 0.25, 256),
+                                        (61, 0.08, 512)])
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_symm_square(qt, ctx, nbr, p, leaf, kind):
+    rng = np.random.default_rng(100 + nbr + (kind == "int"))
+    Um = random_sym_upper(rng, nbr, p, kind, leaf)
+    C, st = mk(qt, ctx, Um).symm_square()
+    got = C.to_blocks()
+    ref = oracle.symm_square(nbr, 32, as_tuple(Um))
+    if kind == "int":
+        assert_same_pattern(got, ref)
+        assert np.array_equal(got[2], ref[2])
+    else:
+        full = oracle.expand_symmetric(*as_tuple(Um))
+        assert_same_pattern(got, ref)
+        d = got[2] - ref[2]
+        assert np.linalg.norm(d) <= REL_FRO_F64 * np.linalg.norm(ref[2])
+        br_, bc_, bound = oracle.higham_bound(nbr, 32, full, full, nbr * 32)
+        assert np.all(np.abs(d) <= bound[br_ <= bc_] + 1e-300)
+    L, _ = oracle.tree_levels(Um.n, 32, leaf)
+    assert list(st.level_tasks[: L + 1]) == oracle.level_task_counts_sym(L, (Um.brow, Um.bcol))
+    assert st.block_products == oracle.level_task_counts_sym(L, (Um.brow, Um.bcol))[-1]
+
+
+def test_symm_square_banded_cfg2_small_and_half_work(qt, ctx):
+    c = qtgen.config(2, "int", small=True, symmetric=True)
+    full = c["A"]
+    U = qtgen.upper(full)
+    A = mk(qt, ctx, full)
+    Cf, stf = A.multiply(A)
+    Cs, sts = mk(qt, ctx, U).symm_square()
+    got = Cs.to_blocks()
+    r, cc, v = Cf.to_blocks()
+    k = r <= cc
+    assert np.array_equal(got[0], r[k]) and np.array_equal(got[1], cc[k])
+    assert np.array_equal(got[2], v[k])              # integers: exact, same as the full multiply
+    # about half the work (ratio in [0.4, 0.6]; diagonal C blocks are computed whole)
+    assert 0.4 <= sts.block_products / stf.block_products <= 0.6
+
+
+def test_symm_square_rejects_lower_blocks(qt, ctx):
+    A = qt.Matrix.from_blocks(ctx, 64, 32, 32, np.array([1], np.int32), np.array([0], np.int32),
+                              np.ones((1, 32, 32)))
+    with pytest.raises(qt.QtError) as e:
+        A.symm_square()
+    assert e.value.name == "QT_EINVAL" and "brow=1, bcol=0" in str(e.value)

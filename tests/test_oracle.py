@@ -420,3 +420,72 @@ def test_transpose_identity_ab_t():
     t = oracle.transpose(*ab)
     o = np.lexsort((t[1], t[0]))
     assert np.array_equal(t[0][o], btat[0]) and np.array_equal(t[2][o], btat[2])
+
+
+# --------------------------------------------------------------------- symmetric square (§3.3)
+
+
+def test_symm_square_spec_example():
+    g = _gold("spec_symm_square_example.json")
+    u = g["upper_A"]
+    U = (np.array(u["brow"], np.int32), np.array(u["bcol"], np.int32),
+         np.array(u["vals"], float).reshape(-1, 1, 1))
+    r, c, v = oracle.symm_square(2, 1, U)
+    e = g["upper_C"]
+    assert r.tolist() == e["brow"] and c.tolist() == e["bcol"]
+    assert v.ravel().tolist() == e["vals"]
+
+
+def _random_symmetric_upper(rng, nbr, bs, p, kind="int"):
+    mask = np.triu(rng.random((nbr, nbr)) < p)
+    br, bc = np.nonzero(mask)
+    v = (rng.integers(-4, 5, size=(len(br), bs, bs)).astype(float) if kind == "int"
+         else rng.uniform(-1, 1, size=(len(br), bs, bs)))
+    for t in range(len(br)):
+        if br[t] == bc[t]:
+            v[t] = np.triu(v[t]) + np.triu(v[t], 1).T   # symmetric diagonal block
+    return br.astype(np.int32), bc.astype(np.int32), v
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_symm_square_vs_dense_library_and_half_work(seed):
+    rng = np.random.default_rng(seed)
+    nbr, bs = 16, 4                       # N = 64
+    U = _random_symmetric_upper(rng, nbr, bs, 0.3)
+    full = oracle.expand_symmetric(*U)
+    D = _blocks_to_dense(nbr, bs, *full)
+    assert np.array_equal(D, D.T)
+    ref = D @ D
+    r, c, v = oracle.symm_square(nbr, bs, U)
+    assert np.all(r <= c)
+    got = _blocks_to_dense(nbr, bs, r, c, v)
+    for t in range(len(r)):
+        I, J = r[t], c[t]
+        assert np.array_equal(got[I * bs:(I + 1) * bs, J * bs:(J + 1) * bs],
+                              ref[I * bs:(I + 1) * bs, J * bs:(J + 1) * bs])
+    # every nonzero upper block of the product is present (structural pattern)
+    pr, pc = oracle.pattern_product(nbr, full[:2], full[:2])
+    k = pr <= pc
+    assert np.array_equal(r, pr[k]) and np.array_equal(c, pc[k])
+    # work: about half of the full multiply's block products ([0.4, 0.6])
+    L, _ = oracle.tree_levels(nbr * bs, bs, bs)
+    half = oracle.level_task_counts_sym(L, U[:2])[-1]
+    whole = oracle.level_task_counts(L, full[:2], full[:2])[-1]
+    assert 0.4 <= half / whole <= 0.6
+
+
+def test_symm_square_identity():
+    nbr, bs = 8, 4
+    I = (np.arange(nbr, dtype=np.int32), np.arange(nbr, dtype=np.int32),
+         np.repeat(np.eye(bs)[None], nbr, axis=0))
+    r, c, v = oracle.symm_square(nbr, bs, I)
+    assert np.array_equal(r, I[0]) and np.array_equal(c, I[1]) and np.array_equal(v, I[2])
+
+
+def test_symm_level_counts_dense_closed_form():
+    # dense symmetric pattern: at level l, pairs I <= J: m(m+1)/2, times m values of K
+    L = 4
+    nbr = 1 << L
+    r, c = np.nonzero(np.triu(np.ones((nbr, nbr), bool)))
+    got = oracle.level_task_counts_sym(L, (r, c))
+    assert got == [(1 << l) * (1 << l) * ((1 << l) + 1) // 2 for l in range(L + 1)]
