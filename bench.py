@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
+    ap.add_argument("--no-symm", action="store_true")
     return ap.parse_args()
 
 
@@ -292,6 +293,10 @@ def main():
     flops_launch = products * FLOP_PER_PRODUCT
     achieved = flops_launch / (ms_num * 1e-3) / 1e12
 
+    symm = None
+    if P == 1 and not args.no_symm:
+        symm = measure_symm(qtmm, ctx, stream, args)
+
     fp32 = None
     if not args.no_fp32:
         fp32 = measure_fp32(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier)
@@ -332,6 +337,7 @@ def main():
                                    "spsumma_comparator": spsumma[0] if P > 1 else 0},
             "cpu_baseline": cpu,
             "fp32_variant": fp32,
+            "symm_square": symm,
             "e2e": e2e,
             "gpu_launches": launches_total,
             "clocks": clocks,
@@ -383,6 +389,41 @@ def measure_fp32(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier):
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak else None,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops x (1.1/2.25 nominal tf32/bf16) / 3",
                          "ms_numeric": round(ms_num, 4)}}
+
+
+def measure_symm(qtmm, ctx, stream, args):
+    """The symmetric square (§3.3) of the same banded workload with symmetric
+    values, upper block triangle stored: its own effective GFLOP/s (over the
+    block products it performs) and its speedup over the full multiply of the
+    expanded matrix (the paper reports ~2x)."""
+    import torch
+    full = qtgen.config(2, symmetric=True)["A"]
+    U = qtgen.upper(full)
+    A = qtmm.Matrix.from_blocks(ctx, full.n, full.leaf_dim, BS, full.brow, full.bcol, full.vals)
+    Au = qtmm.Matrix.from_blocks(ctx, U.n, U.leaf_dim, BS, U.brow, U.bcol, U.vals)
+    res = {}
+    for label, fn in (("full", lambda: A.multiply(A)), ("symm", lambda: Au.symm_square())):
+        for _ in range(3):
+            C, st = fn()
+            C.close()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            C, st = fn()
+            C.close()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        res[label] = (e0.elapsed_time(e1) / args.steps, st.block_products)
+    A.close()
+    Au.close()
+    ms, prods = res["symm"]
+    return {"value": round(prods * FLOP_PER_PRODUCT / (ms * 1e-3) / 1e9, 1), "unit": UNIT,
+            "ms_per_step": round(ms, 4), "block_products": int(prods),
+            "full_multiply_ms": round(res["full"][0], 4),
+            "speedup_vs_full": round(res["full"][0] / ms, 3),
+            "workload": "cfg2 matrix with symmetric values, upper block triangle stored"}
 
 
 def measured_peaks() -> dict:

@@ -18,6 +18,36 @@ from paper_1501_07800_b200 import qtmm  # noqa: E402
 FLOP = 2 * 32 ** 3
 
 
+def run_sym(ctx, stream, name, full, steps=20):
+    """Symmetric square of the upper triangle vs the full multiply of the same matrix."""
+    U = qtgen.upper(full)
+    A = qtmm.Matrix.from_blocks(ctx, full.n, full.leaf_dim, 32, full.brow, full.bcol, full.vals)
+    Au = qtmm.Matrix.from_blocks(ctx, U.n, U.leaf_dim, 32, U.brow, U.bcol, U.vals)
+    out = {}
+    for label, fn in (("full", lambda: A.multiply(A)), ("symm", lambda: Au.symm_square())):
+        for _ in range(3):
+            C, st = fn()
+            C.close()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sts = []
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(steps):
+            C, st = fn()
+            sts.append(st)
+            C.close()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        out[label] = {"ms_step": round(ms, 4), "block_products": sts[-1].block_products,
+                      "c_blocks": sts[-1].c_blocks,
+                      "ms_numeric": round(statistics.mean(s.ms_numeric for s in sts), 4),
+                      "tflops_numeric": round(sts[-1].block_products * FLOP /
+                                              statistics.mean(s.ms_numeric for s in sts) / 1e9, 2)}
+    out["speedup"] = round(out["full"]["ms_step"] / out["symm"]["ms_step"], 3)
+    print(json.dumps({"config": name, **out}), flush=True)
+
+
 def run(ctx, stream, name, c, steps=20):
     Am = c["A"]
     A = qtmm.Matrix.from_blocks(ctx, Am.n, Am.leaf_dim, 32, Am.brow, Am.bcol, Am.vals)
@@ -97,6 +127,11 @@ def main():
             d = v[m].astype(np.float64) - ref[2]
             print(json.dumps({"cfg5_fp32_rel_fro_err_rows_200_232": float(np.linalg.norm(d) / np.linalg.norm(ref[2])),
                               "max_abs_err": float(np.abs(d).max())}), flush=True)
+        elif w == "sym2":
+            run_sym(ctx, stream, "cfg2 banded symmetric: symm_square vs full", qtgen.config(2, symmetric=True)["A"])
+        elif w == "sym4":
+            run_sym(ctx, stream, "cfg4 ES-like symmetric (S^2): symm_square vs full",
+                    qtgen.config(4, symmetric=True)["A"], steps=5)
         elif w == "dense4096":
             br, bc = qtgen.pattern_dense(128)
             v = qtgen.block_values(br, bc, 32, 1)
