@@ -35,10 +35,15 @@ namespace qt {
 
 namespace {
 
-constexpr int kStages = 3;
+// smem: a 4-deep ring of landing stages (A_hi[4] | B_hi[4], 32 KiB) for the
+// TMA lookahead, and a 2-deep ring of lo buffers (A_lo[4] | B_lo[4]) that the
+// split warps fill just before the MMA warp consumes them: 6 x 32 KiB.
+constexpr int kStages = 4;
+constexpr int kLoSlots = 2;
 constexpr int kBlkBytes = 4096;                 // 32x32 fp32
 constexpr int kHiBytes = 8 * kBlkBytes;         // A_hi[4] | B_hi[4]
-constexpr int kStageBytes = 2 * kHiBytes;       // + A_lo[4] | B_lo[4]  = 64 KiB
+constexpr int kStageBytes = kHiBytes;           // landing stage (hi in place)
+constexpr int kLoBase = kStages * kStageBytes;   // lo ring after the landing ring
 constexpr int kSplitWarps = 8;
 constexpr int kProducerWarp = 4 + kSplitWarps;
 constexpr int kMmaWarp = kProducerWarp + 1;
@@ -70,10 +75,12 @@ struct Smem {
   uint64_t full[kStages];   // TMA landed (1 arrival + tx)
   uint64_t conv[kStages];   // hi/lo split done (one arrival per split warp)
   uint64_t empty[kStages];  // MMAs that read the stage done (tcgen05.commit)
+  uint64_t lo_empty[kLoSlots];  // MMAs that read the lo slot done (tcgen05.commit)
   uint64_t tfull[2];        // accumulator ready (commit + MMA-lane arrive)
   uint64_t tempty[2];       // epilogue drained the accumulator (4 warp arrivals)
 };
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + sizeof(Smem);
+constexpr size_t kSmemBytes =
+    1024 /*align slack*/ + (size_t)kStages * kStageBytes + (size_t)kLoSlots * kHiBytes + sizeof(Smem);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -180,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
   // 1024-byte aligned start (kept as an offset from the shared array so the
   // compiler still emits shared-space LDS/STS for the split warps)
   uint8_t* data = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  Smem& S = *reinterpret_cast<Smem*>(data + (size_t)kStages * kStageBytes);
+  Smem& S = *reinterpret_cast<Smem*>(data + (size_t)kLoBase + (size_t)kLoSlots * kHiBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -189,6 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
       mbar_init(&S.conv[s], kSplitWarps);
       mbar_init(&S.empty[s], 1);
     }
+    for (int b = 0; b < kLoSlots; ++b) mbar_init(&S.lo_empty[b], 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&S.tfull[b], 2);
       mbar_init(&S.tempty[b], 4);
@@ -327,12 +335,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
     const int cw = warp - 4;
     int stage = 0;
     uint32_t phase = 0;
+    int lo_slot = 0;
+    uint32_t lo_phase = 0;
     for (;;) {
       mbar_wait(&S.full[stage], phase);
       const int flags = S.hdr[stage].flags;
       if (!(flags & (F_END | F_DONE))) {
+        mbar_wait(&S.lo_empty[lo_slot], lo_phase ^ 1);
         float4* hi = reinterpret_cast<float4*>(data + (size_t)stage * kStageBytes);
-        float4* lo = reinterpret_cast<float4*>(data + (size_t)stage * kStageBytes + kHiBytes);
+        float4* lo = reinterpret_cast<float4*>(data + kLoBase + (size_t)lo_slot * kHiBytes);
 #pragma unroll 1
         for (int atom = cw; atom < 32; atom += kSplitWarps) {  // atoms 0-15: A, 16-31: B
           // MN-major operands get the 32-byte-atom layout: B unless transposed, A if transposed
@@ -363,6 +374,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
           }
         }
         fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
+        if (++lo_slot == kLoSlots) {
+          lo_slot = 0;
+          lo_phase ^= 1;
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.conv[stage]);
@@ -379,6 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
     int acc = 0;
     uint32_t acc_phase = 0;
     bool started = false;
+    int lo_slot = 0;
     const uint32_t sbase = smem_u32(data);
     for (;;) {
       mbar_wait(&S.conv[stage], phase);
@@ -415,6 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
         tc_fence_after();
         if (lane == 0) {
           const uint32_t st = sbase + (uint32_t)stage * kStageBytes;
+          const uint32_t lo = sbase + kLoBase + (uint32_t)lo_slot * kHiBytes;
           const uint32_t d_main = tmem + (uint32_t)acc * 256;  // hi*hi
           const uint32_t d_cross = d_main + 128;                // hi*lo + lo*hi
 #pragma unroll
@@ -427,14 +444,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
             // atoms (= blocks), SBO 512 B between 4-row K atoms, K-slice j
             // (rows 8j..8j+7) at +1024 B.
             const uint32_t stA = st, stB = st + 4u * kBlkBytes;
+            const uint32_t loA = lo, loB = lo + 4u * kBlkBytes;
             const uint64_t a_hi = kTA ? sdesc(stA + 1024u * j, 4096, 512, kSW128_32B)
                                       : sdesc(stA + 32u * j, 16, 1024, kSW128);
-            const uint64_t a_lo = kTA ? sdesc(stA + kHiBytes + 1024u * j, 4096, 512, kSW128_32B)
-                                      : sdesc(stA + kHiBytes + 32u * j, 16, 1024, kSW128);
+            const uint64_t a_lo = kTA ? sdesc(loA + 1024u * j, 4096, 512, kSW128_32B)
+                                      : sdesc(loA + 32u * j, 16, 1024, kSW128);
             const uint64_t b_hi = kTB ? sdesc(stB + 32u * j, 16, 1024, kSW128)
                                       : sdesc(stB + 1024u * j, 4096, 512, kSW128_32B);
-            const uint64_t b_lo = kTB ? sdesc(stB + kHiBytes + 32u * j, 16, 1024, kSW128)
-                                      : sdesc(stB + kHiBytes + 1024u * j, 4096, 512, kSW128_32B);
+            const uint64_t b_lo = kTB ? sdesc(loB + 32u * j, 16, 1024, kSW128)
+                                      : sdesc(loB + 1024u * j, 4096, 512, kSW128_32B);
             constexpr uint32_t kIdesc = idesc_tf32<kTA, kTB>();
             const uint32_t acc_in = ((flags & F_FIRST) && j == 0) ? 0u : 1u;
             tc_mma(d_cross, a_lo, b_hi, kIdesc, acc_in);
@@ -442,8 +460,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
             tc_mma(d_main, a_hi, b_hi, kIdesc, acc_in);
           }
           tc_commit(&S.empty[stage]);
+          tc_commit(&S.lo_empty[lo_slot]);
         }
         __syncwarp();
+        if (++lo_slot == kLoSlots) lo_slot = 0;
       }
       if (++stage == kStages) {
         stage = 0;
