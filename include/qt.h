@@ -109,9 +109,12 @@ qt_status qt_nccl_unique_id(void* out128);
  * The quadtree is uniform: 2^L x 2^L blocks with 2^L >= max(4, ceil(n/bs)),
  * padded children are NIL (reading C-3); the leaf level is
  * L - log2(leaf_dim/bs) (leaves are block-sparse submatrices, §4.1).
- * Requirements: block_size == 32 (the built kernels), leaf_dim a power-of-two
- * multiple of block_size, n % block_size == 0 (reading C-4), nblocks >= 0
- * (0 gives the NIL matrix).
+ * Requirements: block_size 32 or 64 (the leaf block size; "16-64").
+ * A 64x64 block is held internally as a 2x2 quad of 32x32 blocks — the
+ * kernels' block size — so the quadtree simply continues one level below the
+ * caller's blocks; statistics, read-back, truncation and info are reported in
+ * the caller's blocks.  leaf_dim a power-of-two multiple of block_size,
+ * n % block_size == 0 (reading C-4), nblocks >= 0 (0 gives the NIL matrix).
  * Multi-rank (world > 1): collective; each rank passes the blocks of its own
  * block-row range.  `row_bounds` (host, world+1 non-decreasing block-row
  * boundaries, first 0 and last ceil(n/bs)) gives the ranges; NULL means equal

@@ -119,6 +119,19 @@ void cache_release_stream(cudaStream_t s) {
   g_cache.erase(it);
 }
 
+// statistics at the caller's block size: for 64-blocks the 32-block level is
+// internal (a 64-block product = one task at level L-1, 8 products of 32-blocks)
+static void user_stats(qt_mat R, qt_stats& S) {
+  if (R->ubs != 64) return;
+  const int L = R->L;
+  S.nlevels = L;  // levels 0 .. L-1
+  S.block_products = S.level_tasks[L - 1];
+  S.c_blocks = user_nblocks(R);
+  S.level_tasks[L] = 0;
+  S.level_c_nodes[L] = 0;
+  if (S.leaf_level > L - 1) S.leaf_level = L - 1;
+}
+
 static int ilog2(int64_t x) {
   int r = 0;
   while ((1ll << (r + 1)) <= x) ++r;
@@ -243,7 +256,8 @@ qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
   *out = nullptr;
   QT_CUDA(cudaSetDevice(ctx->device));
   if (dtype != QT_F64 && dtype != QT_F32) fail(QT_EDTYPE, "unknown dtype %d", (int)dtype);
-  if (block_size != 32) fail(QT_EINVAL, "block_size %d: only 32 is built", block_size);
+  if (block_size != 32 && block_size != 64)
+    fail(QT_EINVAL, "block_size %d: 32 and 64 are built", block_size);
   if (n <= 0 || n % block_size != 0)
     fail(QT_EINVAL, "n=%lld must be a positive multiple of block_size=%d (reading C-4)",
          (long long)n, block_size);
@@ -253,33 +267,37 @@ qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
          block_size);
   if (nblocks < 0 || nblocks >= (1ll << 31)) fail(QT_EINVAL, "nblocks=%lld", (long long)nblocks);
   if (nblocks > 0 && (!brow || !bcol || !values)) fail(QT_EINVAL, "NULL block arrays");
-  int64_t nbr = n / block_size;
+  // 64-blocks are held as 2x2 quads of 32-blocks (the kernels' block size)
+  const int f = block_size / 32;
+  int64_t nbr = n / 32;
   if (nbr > (1 << 20)) fail(QT_EINVAL, "n too large (more than 2^20 block rows)");
   qt_mat M = new qt_mat_s();
   try {
     M->ctx = ctx;
     M->n = n;
     M->leaf_dim = leaf_dim;
-    M->bs = block_size;
+    M->bs = 32;
+    M->ubs = block_size;
     M->dtype = dtype;
     M->nbr = (int32_t)nbr;
-    int L = 2;  // at least 4x4 blocks (reading C-3): the FP32 kernel tiles 4x4 blocks
+    // at least 4x4 (caller) blocks (reading C-3): the FP32 kernel tiles 4x4 32-blocks
+    int L = f == 2 ? 3 : 2;
     while ((1ll << L) < nbr) ++L;
     M->L = L;
-    M->leaf_level = std::max(0, L - ilog2(leaf_dim / block_size));
+    M->leaf_level = std::max(0, L - ilog2(leaf_dim / 32));
     // block-row ownership
     M->bounds.assign(ctx->world + 1, 0);
     if (ctx->world == 1) {
       M->bounds[1] = (int32_t)nbr;
     } else if (row_bounds) {
-      for (int g = 0; g <= ctx->world; ++g) M->bounds[g] = row_bounds[g];
+      for (int g = 0; g <= ctx->world; ++g) M->bounds[g] = row_bounds[g] * f;
       if (M->bounds[0] != 0 || M->bounds[ctx->world] != nbr)
-        fail(QT_EINVAL, "row_bounds must start at 0 and end at %lld", (long long)nbr);
+        fail(QT_EINVAL, "row_bounds must start at 0 and end at %lld", (long long)(nbr / f));
       for (int g = 0; g < ctx->world; ++g)
         if (M->bounds[g + 1] < M->bounds[g]) fail(QT_EINVAL, "row_bounds not non-decreasing");
     } else {
-      int64_t per = (nbr + ctx->world - 1) / ctx->world;
-      for (int g = 0; g <= ctx->world; ++g) M->bounds[g] = (int32_t)std::min<int64_t>(nbr, per * g);
+      const int64_t nu = nbr / f, per = (nu + ctx->world - 1) / ctx->world;
+      for (int g = 0; g <= ctx->world; ++g) M->bounds[g] = (int32_t)(std::min<int64_t>(nu, per * g) * f);
     }
     M->row_lo = M->bounds[ctx->rank];
     M->row_hi = M->bounds[ctx->rank + 1];
@@ -301,17 +319,24 @@ qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
         QT_CUDA(cudaMemcpyAsync(dc.p, bcol, nblocks * 4, cudaMemcpyHostToDevice, st));
         pc = dc.as<int32_t>();
       }
+      const size_t vb = (size_t)nblocks * block_size * block_size * es;
       if (!is_device_ptr(values)) {
-        dv.alloc(nblocks * 1024 * es, st);
-        QT_CUDA(cudaMemcpyAsync(dv.p, values, nblocks * 1024 * es, cudaMemcpyHostToDevice, st));
+        dv.alloc(vb, st);
+        QT_CUDA(cudaMemcpyAsync(dv.p, values, vb, cudaMemcpyHostToDevice, st));
         pv = dv.p;
       }
     }
-    build_from_blocks(M, nblocks, pr, pc, pv, M->row_lo, M->row_hi);
-    M->global_nb = M->nb;
+    if (f == 2 && nblocks > 0) {
+      DevBuf sr, sc, sv;
+      split64(ctx, dtype, nblocks, pr, pc, pv, sr, sc, sv);
+      build_from_blocks(M, 4 * nblocks, sr.as<int32_t>(), sc.as<int32_t>(), sv.p, M->row_lo, M->row_hi);
+    } else {
+      build_from_blocks(M, nblocks, pr, pc, pv, M->row_lo, M->row_hi);
+    }
+    M->global_nb = user_nblocks(M);
     if (ctx->world > 1) {
       std::vector<int64_t> all(ctx->world);
-      int64_t mine = M->nb;
+      int64_t mine = user_nblocks(M);
       allgather_i64(ctx, &mine, all.data(), 1);
       M->global_nb = 0;
       for (auto v : all) M->global_nb += v;
@@ -336,9 +361,9 @@ qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, q
   *C = nullptr;
   if (A->ctx != B->ctx) fail(QT_ESTATE, "A and B belong to different contexts");
   if (A->n != B->n) fail(QT_EDIM, "dimension mismatch: %lld vs %lld", (long long)A->n, (long long)B->n);
-  if (A->leaf_dim != B->leaf_dim || A->bs != B->bs)
-    fail(QT_EBS, "leaf_dim/block_size mismatch: (%d,%d) vs (%d,%d)", A->leaf_dim, A->bs,
-         B->leaf_dim, B->bs);
+  if (A->leaf_dim != B->leaf_dim || A->ubs != B->ubs)
+    fail(QT_EBS, "leaf_dim/block_size mismatch: (%d,%d) vs (%d,%d)", A->leaf_dim, A->ubs,
+         B->leaf_dim, B->ubs);
   if (A->dtype != B->dtype) fail(QT_EDTYPE, "dtype mismatch");
   qt_ctx ctx = A->ctx;
   QT_CUDA(cudaSetDevice(ctx->device));
@@ -364,7 +389,8 @@ qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, q
   QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
   QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
-  R->global_nb = R->nb;
+  R->global_nb = user_nblocks(R);
+  user_stats(R, S);
   *C = R;
   API_CATCH
 }
@@ -384,13 +410,29 @@ qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
   memset(&S, 0, sizeof(S));
   QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   float ms_sym = 0, ms_num = 0;
-  qt_mat R = multiply_local(A, A, &S, &ms_sym, &ms_num, 4);
+  qt_mat R;
+  if (A->ubs == 64) {
+    // drop the (1,0) 32-sub-block of every diagonal 64-block (it is the
+    // transpose of (0,1)); diagonal C 64-blocks are then completed by not
+    // pruning at the last (32-block) level
+    qt_mat U = upper32_view(A);
+    try {
+      R = multiply_local(U, U, &S, &ms_sym, &ms_num, 4 | ((A->L - 1) << 8));
+    } catch (...) {
+      delete U;
+      throw;
+    }
+    delete U;
+  } else {
+    R = multiply_local(A, A, &S, &ms_sym, &ms_num, 4 | (A->L << 8));
+  }
   S.ms_symbolic = ms_sym;
   S.ms_numeric = ms_num;
   QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
   QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
-  R->global_nb = R->nb;
+  R->global_nb = user_nblocks(R);
+  user_stats(R, S);
   *C = R;
   API_CATCH
 }
@@ -406,7 +448,7 @@ qt_status qt_truncate(qt_mat A, double tau, qt_mat* out) {
     R = truncate_dist(A, tau);
   } else {
     R = truncate(A, tau);
-    R->global_nb = R->nb;
+    R->global_nb = user_nblocks(R);
   }
   QT_CUDA(cudaStreamSynchronize(A->ctx->stream));
   *out = R;
@@ -420,12 +462,12 @@ qt_status qt_info(qt_mat A, int64_t* n, int32_t* leaf_dim, int32_t* block_size, 
   if (!A) fail(QT_EINVAL, "NULL matrix");
   if (n) *n = A->n;
   if (leaf_dim) *leaf_dim = A->leaf_dim;
-  if (block_size) *block_size = A->bs;
+  if (block_size) *block_size = A->ubs;
   if (dtype) *dtype = A->dtype;
-  if (local_nblocks) *local_nblocks = A->nb;
+  if (local_nblocks) *local_nblocks = user_nblocks(A);
   if (global_nblocks) *global_nblocks = A->global_nb;
-  if (row_lo) *row_lo = A->row_lo;
-  if (row_hi) *row_hi = A->row_hi;
+  if (row_lo) *row_lo = A->row_lo / (A->ubs / 32);
+  if (row_hi) *row_hi = A->row_hi / (A->ubs / 32);
   API_CATCH
 }
 
@@ -434,8 +476,9 @@ qt_status qt_level_nodes(qt_mat A, int64_t* counts, int32_t cap, int32_t* nlevel
   if (!A) fail(QT_EINVAL, "NULL matrix");
   QT_CUDA(cudaSetDevice(A->ctx->device));
   ensure_levels(A);
-  if (nlevels) *nlevels = A->L + 1;
-  for (int l = 0; l <= A->L && l < cap; ++l) counts[l] = A->cnt[l];
+  const int top = A->ubs == 64 ? A->L - 1 : A->L;  // the caller's block level
+  if (nlevels) *nlevels = top + 1;
+  for (int l = 0; l <= top && l < cap; ++l) counts[l] = A->cnt[l];
   API_CATCH
 }
 
@@ -473,21 +516,26 @@ qt_status qt_multiply_virtual(qt_mat A, qt_mat B, int32_t P, int32_t g, const in
   if (A->leaf_dim != B->leaf_dim || A->bs != B->bs) fail(QT_EBS, "leaf_dim/block_size mismatch");
   if (A->dtype != B->dtype) fail(QT_EDTYPE, "dtype mismatch");
   if (P < 1 || g < 0 || g >= P) fail(QT_EINVAL, "bad P=%d / g=%d", P, g);
-  if (row_bounds[0] != 0 || row_bounds[P] != A->nbr) fail(QT_EINVAL, "row_bounds must span [0,%d]", A->nbr);
+  if (A->ubs != B->ubs) fail(QT_EBS, "block_size mismatch");
+  const int f = A->ubs / 32;
+  std::vector<int32_t> b32(P + 1);
+  for (int q = 0; q <= P; ++q) b32[q] = row_bounds[q] * f;  // caller's block rows -> 32-rows
+  if (b32[0] != 0 || b32[P] != A->nbr) fail(QT_EINVAL, "row_bounds must span [0,%d]", A->nbr / f);
   for (int q = 0; q < P; ++q)
-    if (row_bounds[q + 1] < row_bounds[q]) fail(QT_EINVAL, "row_bounds not non-decreasing");
+    if (b32[q + 1] < b32[q]) fail(QT_EINVAL, "row_bounds not non-decreasing");
   qt_ctx ctx = A->ctx;
   QT_CUDA(cudaSetDevice(ctx->device));
   qt_stats local;
   qt_stats& S = st ? *st : local;
   memset(&S, 0, sizeof(S));
   QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
-  qt_mat R = multiply_virtual(A, B, row_bounds, P, g, &S);
+  qt_mat R = multiply_virtual(A, B, b32.data(), P, g, &S);
   QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
   QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
-  R->global_nb = R->nb;
-  R->bounds.assign(row_bounds, row_bounds + P + 1);
+  R->global_nb = user_nblocks(R);
+  R->bounds = b32;
+  user_stats(R, S);
   *C = R;
   API_CATCH
 }

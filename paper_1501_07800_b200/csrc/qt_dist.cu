@@ -507,6 +507,7 @@ qt_mat clone_shape(qt_mat A) {
   M->row_lo = A->row_lo;
   M->row_hi = A->row_hi;
   M->bounds = A->bounds;
+  M->ubs = A->ubs;
   return M;
 }
 
@@ -717,7 +718,7 @@ qt_mat truncate_dist(qt_mat A, double tau) {
   cudaStream_t st = ctx->stream;
   const int P = ctx->world, me = ctx->rank;
   Transport* X = T(ctx);
-  const int64_t n = A->nb;
+  const int64_t n = user_nblocks(A);
   std::vector<int64_t> counts(P);
   X->allgather_i64(&n, counts.data(), 1);
   std::vector<int64_t> off(P + 1, 0);
@@ -756,8 +757,15 @@ qt_mat truncate_dist(qt_mat A, double tau) {
   if (n > 0) QT_CUDA(cudaMemsetAsync(keep.p, 1, n, st));
   truncate_decide(ctx, nrm_all.as<double>(), rm_all.as<uint64_t>(), id_all.as<int64_t>(), n_all,
                   tau * tau, me, keep.as<uint8_t>());
-  qt_mat R = select_blocks(A, keep.as<uint8_t>());
-  int64_t kept = R->nb, tot = 0;
+  qt_mat R;
+  if (A->ubs == 64) {
+    DevBuf k32;
+    expand_keep(A, keep.as<uint8_t>(), k32);
+    R = select_blocks(A, k32.as<uint8_t>());
+  } else {
+    R = select_blocks(A, keep.as<uint8_t>());
+  }
+  int64_t kept = user_nblocks(R), tot = 0;
   std::vector<int64_t> all(P);
   X->allgather_i64(&kept, all.data(), 1);
   for (auto v : all) tot += v;

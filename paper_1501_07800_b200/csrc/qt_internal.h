@@ -119,7 +119,8 @@ struct qt_ctx_s {
 struct qt_mat_s {
   qt_ctx ctx = nullptr;
   int64_t n = 0;
-  int32_t leaf_dim = 0, bs = 0;
+  int32_t leaf_dim = 0, bs = 0;  // bs: the internal block size (32)
+  int32_t ubs = 32;    // the caller's block size: 32, or 64 = stored as 2x2 quads of 32-blocks
   qt_dtype dtype = QT_F64;
   int L = 1;           // levels above the block level; level L = blocks
   int leaf_level = 0;
@@ -163,10 +164,18 @@ void build_levels(qt_mat M, const int32_t* leaf_ids = nullptr);
 inline void ensure_levels(qt_mat M) {
   if (!M->levels_built) { build_levels(M); M->levels_built = true; }
 }
-// QT_EINVAL unless every block has brow <= bcol (upper block triangle)
+// QT_EINVAL unless every (caller-size) block has brow <= bcol (upper block triangle)
 void check_upper(qt_mat M);
-// row-major (brow, bcol) order and un-swizzle into caller buffers
+// 64-block matrix without the (1,0) 32-sub-blocks of its diagonal 64-blocks
+qt_mat upper32_view(qt_mat M);
+// row-major (brow, bcol) order and un-swizzle into caller buffers (caller's block size)
 void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals);
+// 64-blocks (2x2 quads of 32-blocks): split inputs / user-level block count
+void split64(qt_ctx ctx, qt_dtype dt, int64_t nb, const int32_t* brow, const int32_t* bcol,
+             const void* vals, DevBuf& obrow, DevBuf& obcol, DevBuf& ovals);
+inline int64_t user_nblocks(qt_mat M) { return M->ubs == 64 ? M->nb / 4 : M->nb; }
+// keep flags per user block -> per internal block
+void expand_keep(qt_mat M, const uint8_t* keep_user, DevBuf& keep32);
 // truncate (reading C-16): local terms, global decision, single-rank driver
 void truncate_terms(qt_mat A, DevBuf& nrm, DevBuf& rm);
 void truncate_decide(qt_ctx ctx, const double* nrm_all, const uint64_t* rm_all, const int64_t* id_all,

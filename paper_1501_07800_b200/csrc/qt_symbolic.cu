@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
   __syncthreads();
   for (int l = 0; l < a.l_end; ++l) {
     const int cur = l & 1, nxt = cur ^ 1;
+    const bool prune = sym && l < (a.trans >> 8);  // C below the diagonal is not computed
     const int F = s_F, ns = s_ns;
     const int32_t* pa = a.pa[cur];
     const int32_t* pb = a.pb[cur];
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
       int c[4];
       child_counts(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym), c);
-      if (sym && on_diagonal(ck[s])) c[2] = 0;
+      if (prune && on_diagonal(ck[s])) c[2] = 0;
       const int64_t base = 4ll * c0 + (p - c0);
 #pragma unroll
       for (int q = 0; q < 4; ++q) a.off[base + (int64_t)q * m] = c[q];
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     for (int p = tid; p < F; p += kSmallThreads) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
       emit_task(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym),
-                4ll * c0 + (p - c0), m, s, sym && on_diagonal(ck[s]), a.off, a.gidx, a.pa[nxt], a.pb[nxt],
+                4ll * c0 + (p - c0), m, s, prune && on_diagonal(ck[s]), a.off, a.gidx, a.pa[nxt], a.pb[nxt],
                 a.pc[nxt]);
     }
     __syncthreads();
@@ -246,7 +247,7 @@ __global__ void k_count(int32_t Fb, const int32_t* __restrict__ f_dev, const int
   const int32_t s = pc[p], c0 = cstart[s], m = cstart[s + 1] - c0;
   int c[4];
   child_counts(op_children(childA, pa[p], mode & 1, sym), op_children(childB, pb[p], mode & 2, sym), c);
-  if (sym && on_diagonal(ckey[s])) c[2] = 0;
+  if ((mode & 8) && on_diagonal(ckey[s])) c[2] = 0;
   const int64_t base = 4ll * c0 + (p - c0);
 #pragma unroll
   for (int q = 0; q < 4; ++q) cnt[base + (int64_t)q * m] = c[q];
@@ -311,7 +312,7 @@ __global__ void k_emit(int32_t Fb, const int32_t* __restrict__ f_dev, const int3
   const bool sym = mode & 4;
   const int32_t s = pc[p], c0 = cstart[s], m = cstart[s + 1] - c0;
   emit_task(op_children(childA, pa[p], mode & 1, sym), op_children(childB, pb[p], mode & 2, sym),
-            4ll * c0 + (p - c0), m, s, sym && on_diagonal(ckey[s]), off, gidx, pa2, pb2, pc2);
+            4ll * c0 + (p - c0), m, s, (mode & 8) && on_diagonal(ckey[s]), off, gidx, pa2, pb2, pc2);
 }
 
 // Upper bound of the symmetric square's tasks per level: with the full
@@ -379,6 +380,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
   C->row_lo = A->row_lo;
   C->row_hi = A->row_hi;
   C->bounds = A->bounds;
+  C->ubs = A->ubs;
   // C's quadtree levels are (re)built from its block keys on first use
   // (ensure_levels): a task group whose child products are all NIL is a NIL
   // node of C (the recursion of §3.2 returns NIL for it), so the canonical
@@ -399,7 +401,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         k_level_tasks_sym<<<L + 1, kThreads, 0, st>>>(A->hist.as<int32_t>(), H, dF.as<int64_t>());
       else
         k_level_tasks<<<L + 1, kThreads, 0, st>>>(A->hist.as<int32_t>(), B->hist.as<int32_t>(), H,
-                                                 trans, dF.as<int64_t>());
+                                                 trans & 3, dF.as<int64_t>());
       QT_LAUNCH_CHECK(ctx);
       QT_CUDA(cudaMemcpyAsync(F.data(), dF.p, 8 * (L + 1), cudaMemcpyDeviceToHost, st));
       QT_CUDA(cudaStreamSynchronize(st));
@@ -469,12 +471,14 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       for (int l = l_end; l < L; ++l) {
         const bool last = (l == L - 1);
         const int32_t Fb = (int32_t)F[l];  // launch bound (exact unless symmetric)
+        // per-level mode: transposes, symmetric, bit 3 = prune C below the diagonal here
+        const int mode_l = (trans & 7) | ((sym && l < (trans >> 8)) ? 8 : 0);
         const int64_t n4 = 4ll * Fb, s4 = 4ll * nsb[l];
         DevBuf cnt(4 * n4, st), off(4 * n4, st);
         k_count<<<grid_for(Fb), kThreads, 0, st>>>(Fb, fd + l, pa.as<int32_t>(), pb.as<int32_t>(),
                                                    pc.as<int32_t>(), cstart.as<int32_t>(),
                                                    ckey.as<uint64_t>(), A->child[l].as<int4>(),
-                                                   B->child[l].as<int4>(), trans, cnt.as<int32_t>());
+                                                   B->child[l].as<int4>(), mode_l, cnt.as<int32_t>());
         QT_LAUNCH_CHECK(ctx);
         excl_sum(ctx, cnt.as<int32_t>(), off.as<int32_t>(), n4);
         DevBuf flag(4 * s4, st), gstart(4 * s4, st), nex(4 * s4, st), gidx(4 * s4, st);
@@ -501,7 +505,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         k_emit<<<grid_for(Fb), kThreads, 0, st>>>(Fb, fd + l, pa.as<int32_t>(), pb.as<int32_t>(),
                                                   pc.as<int32_t>(), cstart.as<int32_t>(),
                                                   ckey.as<uint64_t>(), A->child[l].as<int4>(),
-                                                  B->child[l].as<int4>(), trans, off.as<int32_t>(),
+                                                  B->child[l].as<int4>(), mode_l, off.as<int32_t>(),
                                                   gidx.as<int32_t>(), pa2.as<int32_t>(),
                                                   pb2.as<int32_t>(), pc2.as<int32_t>());
         QT_LAUNCH_CHECK(ctx);
@@ -548,7 +552,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       na.splitB = B->split;
       na.poolC = C->pool.p;
       na.counter = ctx->counters.as<int>() + 16;
-      na.trans = trans;  // bit 2: symmetric square (block refs carry transpose bits)
+      na.trans = trans & 7;  // bit 2: symmetric square (block refs carry transpose bits)
       // tiles per scheduler grab: ~32 tasks per grab, at most 16 tiles
       {
         const int64_t per_tile = std::max<int64_t>(1, F[L - 1] / std::max<int32_t>(1, ns[L - 1]));
@@ -584,7 +588,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         nb.poolC = C->pool.p;
         nb.zeros = ctx->zeros.p;
         nb.counter = ctx->counters.as<int>() + 16;
-        nb.trans = trans;
+        nb.trans = trans & 7;
         launch_numeric_f32(ctx, nb);
       }
       QT_CUDA(cudaEventRecord(ctx->ev[4], st));

@@ -279,13 +279,16 @@ void build_from_blocks(qt_mat M, int64_t nb, const int32_t* d_brow, const int32_
     int32_t r, c;
     QT_CUDA(cudaMemcpy(&r, d_brow + e[0], 4, cudaMemcpyDeviceToHost));
     QT_CUDA(cudaMemcpy(&c, d_bcol + e[0], 4, cudaMemcpyDeviceToHost));
+    const int f = M->ubs / 32;
     fail(QT_ERANGE, "block %llu at (brow=%d, bcol=%d) is outside the block grid [0,%d) or this "
-         "rank's block rows [%d,%d)", e[0], r, c, M->nbr, row_lo, row_hi);
+         "rank's block rows [%d,%d)", e[0] / (f * f), r < 0 ? r : r / f, c < 0 ? c : c / f,
+         M->nbr / f, row_lo / f, row_hi / f);
   }
   if (e[1] != ~0ull) {
     uint64_t k;
     QT_CUDA(cudaMemcpy(&k, M->key.as<uint64_t>() + e[1], 8, cudaMemcpyDeviceToHost));
-    fail(QT_EDUP, "block (brow=%u, bcol=%u) is listed twice", morton_row(k), morton_col(k));
+    const int f = M->ubs / 32;
+    fail(QT_EDUP, "block (brow=%u, bcol=%u) is listed twice", morton_row(k) / f, morton_col(k) / f);
   }
   size_t es = elem_size(M->dtype);
   M->pool.alloc(nb * 1024 * es, st);
@@ -301,11 +304,19 @@ void build_from_blocks(qt_mat M, int64_t nb, const int32_t* d_brow, const int32_
 }
 
 namespace {
-__global__ void k_lower_count(const uint64_t* __restrict__ key, int64_t n, unsigned long long* bad) {
+__global__ void k_lower_count(const uint64_t* __restrict__ key, int64_t n, int f,
+                              unsigned long long* bad) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t k = key[t];
-    if (morton_row(k) > morton_col(k)) atomicMin(bad, (unsigned long long)t);
+    if (morton_row(k) / f > morton_col(k) / f) atomicMin(bad, (unsigned long long)t);
+  }
+}
+__global__ void k_keep_upper32(const uint64_t* __restrict__ key, int64_t n, uint8_t* __restrict__ keep) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = key[t];
+    keep[t] = morton_row(k) <= morton_col(k);
   }
 }
 }  // namespace
@@ -315,18 +326,164 @@ void check_upper(qt_mat M) {
   if (M->nb == 0) return;
   unsigned long long* bad = ctx->counters.as<unsigned long long>();
   QT_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
-  k_lower_count<<<grid_for(M->nb), kThreads, 0, ctx->stream>>>(M->key.as<uint64_t>(), M->nb, bad);
+  const int f = M->ubs / 32;
+  k_lower_count<<<grid_for(M->nb), kThreads, 0, ctx->stream>>>(M->key.as<uint64_t>(), M->nb, f, bad);
   QT_LAUNCH_CHECK(ctx);
   const unsigned long long b = read_scalar(ctx, bad);
   if (b != ~0ull) {
     uint64_t k;
     QT_CUDA(cudaMemcpy(&k, M->key.as<uint64_t>() + b, 8, cudaMemcpyDeviceToHost));
     fail(QT_EINVAL, "symmetric square needs upper-triangular block storage; block (brow=%u, bcol=%u) "
-         "is below the diagonal", morton_row(k), morton_col(k));
+         "is below the diagonal", morton_row(k) / f, morton_col(k) / f);
   }
 }
 
+qt_mat upper32_view(qt_mat M) {
+  DevBuf keep(std::max<int64_t>(M->nb, 1), M->ctx->stream);
+  if (M->nb > 0) {
+    k_keep_upper32<<<grid_for(M->nb), kThreads, 0, M->ctx->stream>>>(M->key.as<uint64_t>(), M->nb,
+                                                                     keep.as<uint8_t>());
+    QT_LAUNCH_CHECK(M->ctx);
+  }
+  return select_blocks(M, keep.as<uint8_t>());
+}
+
+namespace {
+template <class T>
+__global__ void k_split64(const int32_t* __restrict__ brow, const int32_t* __restrict__ bcol,
+                          const T* __restrict__ vals, int64_t nb, int32_t* __restrict__ obrow,
+                          int32_t* __restrict__ obcol, T* __restrict__ ovals) {
+  for (int64_t u = blockIdx.x; u < 4 * nb; u += gridDim.x) {
+    const int64_t t = u >> 2;
+    const int i = (u >> 1) & 1, j = u & 1;
+    if (threadIdx.x == 0) {
+      obrow[u] = 2 * brow[t] + i;
+      obcol[u] = 2 * bcol[t] + j;
+    }
+    for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+      const int r = e >> 5, c = e & 31;
+      ovals[u * 1024 + e] = vals[t * 4096 + (32 * i + r) * 64 + 32 * j + c];
+    }
+  }
+}
+
+// quads (level L-1 nodes) of a 64-block matrix: row-major key and first child
+__global__ void k_quad_keys(const int4* __restrict__ child, const uint64_t* __restrict__ key,
+                            int64_t nq, uint64_t* __restrict__ rm, int32_t* __restrict__ iota) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nq;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int4 c = child[t];
+    const int any = c.x >= 0 ? c.x : c.y >= 0 ? c.y : c.z >= 0 ? c.z : c.w;
+    const uint64_t q = key[any] >> 2;
+    rm[t] = ((uint64_t)morton_row(q) << 32) | morton_col(q);
+    iota[t] = (int32_t)t;
+  }
+}
+
+template <class T>
+__global__ void k_unpack64(const T* __restrict__ pool, const int4* __restrict__ child,
+                           const uint64_t* __restrict__ rm_sorted, const int32_t* __restrict__ order,
+                           int64_t nq, int32_t* __restrict__ brow, int32_t* __restrict__ bcol,
+                           T* __restrict__ out) {
+  for (int64_t u = blockIdx.x; u < nq; u += gridDim.x) {
+    const int4 c4 = child[order[u]];
+    if (threadIdx.x == 0) {
+      if (brow) brow[u] = (int32_t)(rm_sorted[u] >> 32);
+      if (bcol) bcol[u] = (int32_t)(rm_sorted[u] & 0xffffffffu);
+    }
+    if (!out) continue;
+    for (int e = threadIdx.x; e < 4096; e += blockDim.x) {
+      const int R = e >> 6, Cc = e & 63, i = R >> 5, j = Cc >> 5, r = R & 31, c = Cc & 31;
+      const int s = 2 * i + j;
+      const int b = s == 0 ? c4.x : s == 1 ? c4.y : s == 2 ? c4.z : c4.w;
+      T v = 0;
+      if (b >= 0) v = pool[(int64_t)b * 1024 + (sizeof(T) == 8 ? swz64(r, c) : swz32(r, c))];
+      out[u * 4096 + e] = v;
+    }
+  }
+}
+
+__global__ void k_expand_keep(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = in[t >> 2];
+}
+
+__global__ void k_quad_terms(const double* __restrict__ nrm32, const uint64_t* __restrict__ key,
+                             int64_t nq, double* __restrict__ nrm, uint64_t* __restrict__ rm) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nq;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    // the four 32-blocks of a complete quad are consecutive in Morton order; the
+    // squared norms are summed in the fixed sub-block order (0,0),(0,1),(1,0),(1,1)
+    nrm[t] = ((nrm32[4 * t] + nrm32[4 * t + 1]) + nrm32[4 * t + 2]) + nrm32[4 * t + 3];
+    const uint64_t q = key[4 * t] >> 2;
+    rm[t] = ((uint64_t)morton_row(q) << 32) | morton_col(q);
+  }
+}
+}  // namespace
+
+void split64(qt_ctx ctx, qt_dtype dt, int64_t nb, const int32_t* brow, const int32_t* bcol,
+             const void* vals, DevBuf& obrow, DevBuf& obcol, DevBuf& ovals) {
+  cudaStream_t st = ctx->stream;
+  obrow.alloc(16 * nb, st);
+  obcol.alloc(16 * nb, st);
+  ovals.alloc(4 * nb * 1024 * elem_size(dt), st);
+  const unsigned g = (unsigned)std::min<int64_t>(4 * nb, 148 * 16);
+  if (dt == QT_F64)
+    k_split64<double><<<g, 256, 0, st>>>(brow, bcol, (const double*)vals, nb, obrow.as<int32_t>(),
+                                         obcol.as<int32_t>(), ovals.as<double>());
+  else
+    k_split64<float><<<g, 256, 0, st>>>(brow, bcol, (const float*)vals, nb, obrow.as<int32_t>(),
+                                        obcol.as<int32_t>(), ovals.as<float>());
+  QT_LAUNCH_CHECK(ctx);
+}
+
+void expand_keep(qt_mat M, const uint8_t* keep_user, DevBuf& keep32) {
+  keep32.alloc(std::max<int64_t>(M->nb, 1), M->ctx->stream);
+  if (M->nb == 0) return;
+  k_expand_keep<<<grid_for(M->nb), kThreads, 0, M->ctx->stream>>>(keep_user, M->nb, keep32.as<uint8_t>());
+  QT_LAUNCH_CHECK(M->ctx);
+}
+
+static void read_back64(qt_mat M, int32_t* brow, int32_t* bcol, void* vals) {
+  qt_ctx ctx = M->ctx;
+  cudaStream_t st = ctx->stream;
+  ensure_levels(M);
+  const int64_t nq = M->cnt[M->L - 1];
+  if (nq == 0 || M->nb == 0) return;
+  const size_t es = elem_size(M->dtype);
+  const int4* child = M->child[M->L - 1].as<int4>();
+  DevBuf rm(nq * 8, st), rm2(nq * 8, st), iota(nq * 4, st), order(nq * 4, st);
+  k_quad_keys<<<grid_for(nq), kThreads, 0, st>>>(child, M->key.as<uint64_t>(), nq, rm.as<uint64_t>(),
+                                                 iota.as<int32_t>());
+  QT_LAUNCH_CHECK(ctx);
+  cub_sort_pairs(ctx, rm.as<uint64_t>(), rm2.as<uint64_t>(), iota.as<int32_t>(), order.as<int32_t>(),
+                 nq, 64);
+  bool dr = brow && is_device_ptr(brow), dc = bcol && is_device_ptr(bcol),
+       dv = vals && is_device_ptr(vals);
+  DevBuf sr, sc, sv;
+  int32_t* obr = brow ? (dr ? brow : (sr.alloc(nq * 4, st), sr.as<int32_t>())) : nullptr;
+  int32_t* obc = bcol ? (dc ? bcol : (sc.alloc(nq * 4, st), sc.as<int32_t>())) : nullptr;
+  void* ov = vals ? (dv ? vals : (sv.alloc(nq * 4096 * es, st), sv.p)) : nullptr;
+  const unsigned g = (unsigned)std::min<int64_t>(nq, 148 * 16);
+  if (M->dtype == QT_F64)
+    k_unpack64<double><<<g, 256, 0, st>>>(M->pool.as<double>(), child, rm2.as<uint64_t>(),
+                                          order.as<int32_t>(), nq, obr, obc, (double*)ov);
+  else
+    k_unpack64<float><<<g, 256, 0, st>>>(M->pool.as<float>(), child, rm2.as<uint64_t>(),
+                                         order.as<int32_t>(), nq, obr, obc, (float*)ov);
+  QT_LAUNCH_CHECK(ctx);
+  if (brow && !dr) QT_CUDA(cudaMemcpyAsync(brow, obr, nq * 4, cudaMemcpyDeviceToHost, st));
+  if (bcol && !dc) QT_CUDA(cudaMemcpyAsync(bcol, obc, nq * 4, cudaMemcpyDeviceToHost, st));
+  if (vals && !dv) QT_CUDA(cudaMemcpyAsync(vals, ov, nq * 4096 * es, cudaMemcpyDeviceToHost, st));
+  QT_CUDA(cudaStreamSynchronize(st));
+}
+
 void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals) {
+  if (M->ubs == 64) {
+    read_back64(M, brow, bcol, vals);
+    return;
+  }
   qt_ctx ctx = M->ctx;
   cudaStream_t st = ctx->stream;
   int64_t nb = M->nb;
@@ -372,6 +529,7 @@ static qt_mat clone_params(qt_mat A) {
   M->row_lo = A->row_lo;
   M->row_hi = A->row_hi;
   M->bounds = A->bounds;
+  M->ubs = A->ubs;
   return M;
 }
 
@@ -430,6 +588,15 @@ void truncate_terms(qt_mat A, DevBuf& nrm, DevBuf& rm) {
   k_rowmajor_keys<<<grid_for(n), kThreads, 0, st>>>(A->key.as<uint64_t>(), n, rm.as<uint64_t>(),
                                                     iota.as<int32_t>());
   QT_LAUNCH_CHECK(ctx);
+  if (A->ubs == 64) {  // terms of the caller's 64-blocks (complete quads of 32-blocks)
+    const int64_t nq = n / 4;
+    DevBuf n64(8 * std::max<int64_t>(nq, 1), st), r64(8 * std::max<int64_t>(nq, 1), st);
+    k_quad_terms<<<grid_for(nq), kThreads, 0, st>>>(nrm.as<double>(), A->key.as<uint64_t>(), nq,
+                                                    n64.as<double>(), r64.as<uint64_t>());
+    QT_LAUNCH_CHECK(ctx);
+    nrm = std::move(n64);
+    rm = std::move(r64);
+  }
 }
 
 namespace {
@@ -493,7 +660,7 @@ void truncate_decide(qt_ctx ctx, const double* nrm_all, const uint64_t* rm_all, 
 qt_mat truncate(qt_mat A, double tau) {
   qt_ctx ctx = A->ctx;
   cudaStream_t st = ctx->stream;
-  const int64_t n = A->nb;
+  const int64_t n = user_nblocks(A);
   DevBuf keep(std::max<int64_t>(n, 1), st);
   if (n > 0) {
     QT_CUDA(cudaMemsetAsync(keep.p, 1, n, st));
@@ -503,6 +670,11 @@ qt_mat truncate(qt_mat A, double tau) {
     QT_LAUNCH_CHECK(ctx);
     truncate_decide(ctx, nrm.as<double>(), rm.as<uint64_t>(), id.as<int64_t>(), n, tau * tau, 0,
                     keep.as<uint8_t>());
+  }
+  if (A->ubs == 64) {
+    DevBuf k32;
+    expand_keep(A, keep.as<uint8_t>(), k32);
+    return select_blocks(A, k32.as<uint8_t>());
   }
   return select_blocks(A, keep.as<uint8_t>());
 }

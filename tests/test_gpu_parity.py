@@ -582,3 +582,101 @@ def test_symm_square_rejects_lower_blocks(qt, ctx):
     with pytest.raises(qt.QtError) as e:
         A.symm_square()
     assert e.value.name == "QT_EINVAL" and "brow=1, bcol=0" in str(e.value)
+
+
+# ----------------------------------------------------------------- block size 64
+
+
+def random_bm64(rng, nbr, p, kind, leaf, dtype=np.float64):
+    mask = rng.random((nbr, nbr)) < p
+    br, bc = np.nonzero(mask)
+    v = (rng.integers(-4, 5, size=(len(br), 64, 64)) if kind == "int"
+         else rng.uniform(-1, 1, size=(len(br), 64, 64))).astype(dtype)
+    return qtgen.BlockMatrix(nbr * 64, leaf, 64, br.astype(np.int32), bc.astype(np.int32), v)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_bs64_roundtrip(qt, ctx, dtype):
+    rng = np.random.default_rng(64)
+    M = random_bm64(rng, 9, 0.4, "uniform", 128, dtype)
+    perm = rng.permutation(M.nb)
+    A = qt.Matrix.from_blocks(ctx, M.n, 128, 64, M.brow[perm], M.bcol[perm], M.vals[perm])
+    assert A.info()["bs"] == 64 and A.nblocks == M.nb
+    r, c, v = A.to_blocks()
+    o = np.lexsort((M.bcol, M.brow))
+    assert np.array_equal(r, M.brow[o]) and np.array_equal(c, M.bcol[o]) and np.array_equal(v, M.vals[o])
+
+
+@pytest.mark.parametrize("nbr,p", [(1, 1.0), (3, 0.7), (19, 0.2)])
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_bs64_multiply(qt, ctx, nbr, p, kind):
+    rng = np.random.default_rng(640 + nbr + (kind == "int"))
+    Am = random_bm64(rng, nbr, p, kind, 256)
+    Bm = random_bm64(rng, nbr, p, kind, 256)
+    C, st = mk(qt, ctx, Am).multiply(mk(qt, ctx, Bm))
+    got = C.to_blocks()
+    ref = oracle.spgemm(nbr, 64, as_tuple(Am), as_tuple(Bm))
+    assert_same_pattern(got, ref)
+    if kind == "int":
+        assert np.array_equal(got[2], ref[2])
+    else:
+        assert np.linalg.norm(got[2] - ref[2]) <= REL_FRO_F64 * np.linalg.norm(ref[2])
+        _, _, bound = oracle.higham_bound(nbr, 64, as_tuple(Am), as_tuple(Bm), nbr * 64)
+        assert np.all(np.abs(got[2] - ref[2]) <= bound + 1e-300)
+    L, _ = oracle.tree_levels(Am.n, 64, 256)
+    assert st.nlevels == L + 1
+    assert list(st.level_tasks[: L + 1]) == oracle.level_task_counts(L, (Am.brow, Am.bcol), (Bm.brow, Bm.bcol))
+    assert st.block_products == oracle.level_task_counts(L, (Am.brow, Am.bcol), (Bm.brow, Bm.bcol))[-1]
+    assert C.level_nodes() == oracle.level_node_counts(L, (ref[0], ref[1]))
+
+
+def test_bs64_fp32_and_transposed(qt, ctx):
+    rng = np.random.default_rng(6464)
+    Am = random_bm64(rng, 11, 0.3, "int", 128, np.float32)
+    Bm = random_bm64(rng, 11, 0.3, "int", 128, np.float32)
+    for ta, tb in [(False, False), (True, False), (False, True)]:
+        got = mk(qt, ctx, Am).multiply_ex(mk(qt, ctx, Bm), ta, tb)[0].to_blocks()
+        ref = oracle.spgemm_t(11, 64, (Am.brow, Am.bcol, Am.vals.astype(np.float64)),
+                              (Bm.brow, Bm.bcol, Bm.vals.astype(np.float64)), ta, tb)
+        assert_same_pattern(got, ref)
+        assert np.array_equal(got[2].astype(np.float64), ref[2])
+
+
+def test_bs64_symm_square(qt, ctx):
+    rng = np.random.default_rng(77)
+    nbr = 12
+    mask = np.triu(rng.random((nbr, nbr)) < 0.35)
+    np.fill_diagonal(mask, True)
+    br, bc = np.nonzero(mask)
+    v = rng.integers(-4, 5, size=(len(br), 64, 64)).astype(np.float64)
+    for t in range(len(br)):
+        if br[t] == bc[t]:
+            v[t] = np.triu(v[t]) + np.triu(v[t], 1).T
+    U = (br.astype(np.int32), bc.astype(np.int32), v)
+    A = qt.Matrix.from_blocks(ctx, nbr * 64, 256, 64, *U)
+    C, st = A.symm_square()
+    got = C.to_blocks()
+    ref = oracle.symm_square(nbr, 64, U)
+    assert_same_pattern(got, ref)
+    assert np.array_equal(got[2], ref[2])
+    L, _ = oracle.tree_levels(nbr * 64, 64, 256)
+    assert st.block_products == oracle.level_task_counts_sym(L, U[:2])[-1]
+
+
+def test_bs64_truncate_and_virtual(qt, ctx):
+    rng = np.random.default_rng(90)
+    M = random_bm64(rng, 16, 0.4, "uniform", 128)
+    M.vals *= rng.uniform(0, 1, size=(M.nb, 1, 1)) ** 4
+    A = mk(qt, ctx, M)
+    r, c, v = A.truncate(10.0).to_blocks()
+    rr, rc, rv = oracle.truncate(M.brow, M.bcol, M.vals, 10.0)
+    assert np.array_equal(r, rr) and np.array_equal(c, rc) and np.array_equal(v, rv)
+    full = (A @ A).to_blocks()
+    bounds = [0, 5, 16]
+    for g in range(2):
+        Cg, st = A.multiply_virtual(A, 2, g, bounds)
+        rg, cg, vg = Cg.to_blocks()
+        m = (full[0] >= bounds[g]) & (full[0] < bounds[g + 1])
+        assert np.array_equal(rg, full[0][m]) and np.array_equal(vg, full[2][m])
+        plan = oracle.exchange_plan(bounds, (M.brow, M.bcol), (M.brow, M.bcol), 64 * 64 * 8)[g]
+        assert st.bytes_recv_payload == plan["payload_bytes"]
