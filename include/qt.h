@@ -150,6 +150,20 @@ qt_status qt_multiply(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st);
 qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, qt_mat* C,
                          qt_stats* st);
 
+/* Norm-screened product (the norm-annotated quadtree of P:1294-1299):
+ * C~ = sum over block products with ||A(I,K)||_F * ||B(K,J)||_F >= tau of
+ * A(I,K) B(K,J).  Every quadtree node carries its squared Frobenius norm (sum
+ * of its blocks', computed once per matrix); the symbolic pass drops a task
+ * (a, b) as soon as ||a||^2 ||b||^2 < tau^2 — exact with respect to the
+ * block-level test, since a node's norm bounds its blocks' — and the numeric
+ * kernel skips the same block products.  ||C - C~||_F <= sum of the skipped
+ * ||A(I,K)|| ||B(K,J)||.  tau = 0 gives qt_multiply's result.  Squared block
+ * norms are summed row-major with separate multiply/add roundings (the
+ * oracle's order, so both take identical decisions).  FP64, block_size 32,
+ * world == 1.  Errors: QT_EINVAL (tau < 0), QT_EDIM, QT_EBS, QT_EDTYPE,
+ * QT_ENOMEM, QT_ECUDA. */
+qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_stats* st);
+
 /* Symmetric matrix square C = A^2 (§3.3): A is symmetric and given
  * by its upper block triangle (every block of A has brow <= bcol; a diagonal
  * block is a full bs x bs block, used as stored); C is returned the same way

@@ -18,6 +18,9 @@ S:nnn = SPEC.md line; readings C-n are listed in DESIGN.md):
 * ``dense_mm``    textbook triple loop (pin P-2).
 * ``transpose`` / ``spgemm_t``  the transposed task types C = A^T B, A B^T,
                   A^T B^T by explicit block transposition.
+* ``spgemm(..., tau=)`` the norm-screened product C~ (products with
+                  ||A_IK|| ||B_KJ|| < tau skipped),
+                  ``block_norm2`` the squared block norms it tests.
 * ``symm_square`` upper block triangle of A^2 for symmetric A in upper
                   triangular storage (§3.3 P:297-311), by explicit expansion;
                   ``level_task_counts_sym`` its per-level tasks.
@@ -73,9 +76,12 @@ def _load():
         P = ctypes.c_void_p
         i32, i64 = ctypes.c_int32, ctypes.c_int64
         lib.oracle_symbolic.restype = i64
-        lib.oracle_symbolic.argtypes = [i32, P, P, i32, P, P, i32, P]
+        D = ctypes.c_double
+        lib.oracle_symbolic.argtypes = [i32, P, P, i32, P, P, i32, P, P, P, D]
         lib.oracle_numeric.restype = None
-        lib.oracle_numeric.argtypes = [i32, i32, P, P, P, P, P, P, i32, P, P, P, i32, i32, i32]
+        lib.oracle_numeric.argtypes = [i32, i32, P, P, P, P, P, P, i32, P, P, P, i32, i32, i32, P, P, D]
+        lib.oracle_block_norm2.restype = None
+        lib.oracle_block_norm2.argtypes = [i64, i32, P, P]
         lib.oracle_dense.restype = None
         lib.oracle_dense.argtypes = [i32, P, P, P]
         _lib = lib
@@ -107,15 +113,31 @@ def to_bcsr(nbr: int, brow, bcol, vals):
     return ptr, col, val
 
 
-def spgemm(nbr: int, bs: int, A, B, nthreads: int | None = None, rows=None):
+def block_norm2(vals) -> np.ndarray:
+    """Squared Frobenius norm of each block (row-major, plain C loop)."""
+    vals = np.ascontiguousarray(np.asarray(vals, np.float64))
+    out = np.zeros(vals.shape[0], np.float64)
+    if vals.shape[0]:
+        _load().oracle_block_norm2(vals.shape[0], vals.shape[1], _p(vals), _p(out))
+    return out
+
+
+def spgemm(nbr: int, bs: int, A, B, nthreads: int | None = None, rows=None, tau: float | None = None):
     """C = A*B.  ``A``/``B`` are (brow, bcol, vals[nb,bs,bs]) tuples over an
     nbr x nbr block grid.  Returns (brow, bcol, vals) of C sorted by
-    (brow, bcol); ``rows=(lo,hi)`` restricts the work to those block rows."""
+    (brow, bcol); ``rows=(lo,hi)`` restricts the work to those block rows.
+    ``tau``: the norm-screened product — only block products with
+    ||A_IK||_F ||B_KJ||_F >= tau (squared norms: na2*nb2 >= tau^2) are taken."""
     lib = _load()
     a_ptr, a_col, a_val = to_bcsr(nbr, *A)
     b_ptr, b_col, b_val = to_bcsr(nbr, *B)
+    na2 = nb2 = None
+    tau2 = 0.0
+    if tau is not None:
+        na2, nb2, tau2 = block_norm2(a_val), block_norm2(b_val), float(tau) * float(tau)
     c_cnt = np.zeros(nbr, np.int64)
-    lib.oracle_symbolic(nbr, _p(a_ptr), _p(a_col), nbr, _p(b_ptr), _p(b_col), nbr, _p(c_cnt))
+    lib.oracle_symbolic(nbr, _p(a_ptr), _p(a_col), nbr, _p(b_ptr), _p(b_col), nbr, _p(c_cnt),
+                        _p(na2) if na2 is not None else None, _p(nb2) if nb2 is not None else None, tau2)
     lo, hi = rows if rows is not None else (0, nbr)
     if rows is not None:
         c_cnt[:lo] = 0
@@ -127,7 +149,8 @@ def spgemm(nbr: int, bs: int, A, B, nthreads: int | None = None, rows=None):
     c_val = np.zeros((max(nc, 1), bs, bs), np.float64)
     nt = default_threads() if nthreads is None else nthreads
     lib.oracle_numeric(nbr, bs, _p(a_ptr), _p(a_col), _p(a_val), _p(b_ptr), _p(b_col), _p(b_val),
-                       nbr, _p(c_ptr), _p(c_col), _p(c_val), lo, hi, nt)
+                       nbr, _p(c_ptr), _p(c_col), _p(c_val), lo, hi, nt,
+                       _p(na2) if na2 is not None else None, _p(nb2) if nb2 is not None else None, tau2)
     c_row = np.repeat(np.arange(nbr, dtype=np.int32), c_cnt)
     return c_row, c_col[:nc], c_val[:nc]
 

@@ -35,9 +35,18 @@
 
 /* Count C blocks per block row: c_cnt[I] = |{J : exists K, A(I,K), B(K,J)}|.
  * marker: caller-free scratch.  Returns total number of C blocks. */
+/* Norm screening (the optional last three arguments of oracle_symbolic and
+ * oracle_numeric): the block product A(I,K) B(K,J) is taken iff
+ * na2[p] * nb2[q] >= tau2, with na2/nb2 the squared Frobenius norms of the
+ * blocks (oracle_block_norm2) — the definition of the screened product C~. */
+static int keep_product(const double* na2, const double* nb2, double tau2, int64_t p, int64_t q) {
+  return !na2 || na2[p] * nb2[q] >= tau2;
+}
+
 int64_t oracle_symbolic(int32_t nbr, const int64_t* a_ptr, const int32_t* a_col,
                         int32_t nbk, const int64_t* b_ptr, const int32_t* b_col,
-                        int32_t nbc, int64_t* c_cnt) {
+                        int32_t nbc, int64_t* c_cnt, const double* na2, const double* nb2,
+                        double tau2) {
   (void)nbk;
   int32_t* marker = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nbc > 0 ? nbc : 1));
   for (int32_t j = 0; j < nbc; ++j) marker[j] = -1;
@@ -47,6 +56,7 @@ int64_t oracle_symbolic(int32_t nbr, const int64_t* a_ptr, const int32_t* a_col,
     for (int64_t p = a_ptr[I]; p < a_ptr[I + 1]; ++p) {
       int32_t K = a_col[p];
       for (int64_t q = b_ptr[K]; q < b_ptr[K + 1]; ++q) {
+        if (!keep_product(na2, nb2, tau2, p, q)) continue;
         int32_t J = b_col[q];
         if (marker[J] != I) { marker[J] = I; ++cnt; }
       }
@@ -66,6 +76,8 @@ static int cmp_i32(const void* x, const void* y) {
 /* ----------------------------------------------------------------- numeric */
 
 typedef struct {
+  const double *na2, *nb2;
+  double tau2;
   int32_t nbr, nbc, bs;
   const int64_t *a_ptr, *b_ptr, *c_ptr;
   const int32_t *a_col, *b_col;
@@ -85,6 +97,7 @@ static void row_product(const job_t* jb, int32_t I, int32_t* pos_of) {
   for (int64_t p = jb->a_ptr[I]; p < jb->a_ptr[I + 1]; ++p) {
     int32_t K = jb->a_col[p];
     for (int64_t q = jb->b_ptr[K]; q < jb->b_ptr[K + 1]; ++q) {
+      if (!keep_product(jb->na2, jb->nb2, jb->tau2, p, q)) continue;
       int32_t J = jb->b_col[q];
       if (pos_of[J] != -2 - I) { pos_of[J] = -2 - I; ccol[nc++] = J; }
     }
@@ -98,6 +111,7 @@ static void row_product(const job_t* jb, int32_t I, int32_t* pos_of) {
     int32_t K = jb->a_col[p];
     const double* a = jb->a_val + p * bb;
     for (int64_t q = jb->b_ptr[K]; q < jb->b_ptr[K + 1]; ++q) {
+      if (!keep_product(jb->na2, jb->nb2, jb->tau2, p, q)) continue;
       int32_t J = jb->b_col[q];
       const double* b = jb->b_val + q * bb;
       double* c = cv + (int64_t)pos_of[J] * bb;
@@ -130,14 +144,15 @@ void oracle_numeric(int32_t nbr, int32_t bs,
                     const int64_t* a_ptr, const int32_t* a_col, const double* a_val,
                     const int64_t* b_ptr, const int32_t* b_col, const double* b_val,
                     int32_t nbc, const int64_t* c_ptr, int32_t* c_col, double* c_val,
-                    int32_t row_lo, int32_t row_hi, int32_t nthreads) {
+                    int32_t row_lo, int32_t row_hi, int32_t nthreads, const double* na2,
+                    const double* nb2, double tau2) {
   if (nthreads <= 0) nthreads = 1;
   if (row_lo < 0) row_lo = 0;
   if (row_hi > nbr) row_hi = nbr;
   job_t* jobs = (job_t*)malloc(sizeof(job_t) * (size_t)nthreads);
   pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
   for (int32_t t = 0; t < nthreads; ++t) {
-    job_t j = {nbr, nbc, bs, a_ptr, b_ptr, c_ptr, a_col, b_col, a_val, b_val,
+    job_t j = {na2, nb2, tau2, nbr, nbc, bs, a_ptr, b_ptr, c_ptr, a_col, b_col, a_val, b_val,
                c_col, c_val, row_lo, row_hi, nthreads, t};
     jobs[t] = j;
   }
@@ -149,6 +164,20 @@ void oracle_numeric(int32_t nbr, int32_t bs,
   }
   free(th);
   free(jobs);
+}
+
+/* Squared Frobenius norm of each bs x bs block: row-major, one rounding per
+ * multiply and per add (compiled with -ffp-contract=off). */
+void oracle_block_norm2(int64_t nb, int32_t bs, const double* vals, double* out) {
+  const int64_t bb = (int64_t)bs * bs;
+  for (int64_t t = 0; t < nb; ++t) {
+    double s = 0.0;
+    for (int64_t e = 0; e < bb; ++e) {
+      double v = vals[t * bb + e];
+      s += v * v;
+    }
+    out[t] = s;
+  }
 }
 
 /* -------------------------------------------------- dense brute force (i) */

@@ -395,6 +395,38 @@ qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, q
   API_CATCH
 }
 
+qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_stats* st) {
+  API_TRY
+  if (!A || !B || !C) fail(QT_EINVAL, "NULL argument");
+  *C = nullptr;
+  if (!(tau >= 0)) fail(QT_EINVAL, "tau must be >= 0");
+  if (A->ctx != B->ctx) fail(QT_ESTATE, "A and B belong to different contexts");
+  if (A->n != B->n) fail(QT_EDIM, "dimension mismatch");
+  if (A->leaf_dim != B->leaf_dim || A->ubs != B->ubs) fail(QT_EBS, "leaf_dim/block_size mismatch");
+  if (A->dtype != B->dtype) fail(QT_EDTYPE, "dtype mismatch");
+  if (A->dtype != QT_F64) fail(QT_EDTYPE, "norm screening is FP64-only (the FP32 tile MMA cannot skip single products)");
+  if (A->ubs != 32) fail(QT_EBS, "norm screening is built for block_size 32");
+  qt_ctx ctx = A->ctx;
+  if (ctx->world > 1) fail(QT_EINVAL, "norm screening is single-rank in this build");
+  QT_CUDA(cudaSetDevice(ctx->device));
+  ensure_levels(A);
+  ensure_levels(B);
+  qt_stats local;
+  qt_stats& S = st ? *st : local;
+  memset(&S, 0, sizeof(S));
+  QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  float ms_sym = 0, ms_num = 0;
+  qt_mat R = multiply_local(A, B, &S, &ms_sym, &ms_num, 0, tau);
+  S.ms_symbolic = ms_sym;
+  S.ms_numeric = ms_num;
+  QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+  QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
+  QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
+  R->global_nb = user_nblocks(R);
+  *C = R;
+  API_CATCH
+}
+
 qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
   API_TRY
   if (!A || !C) fail(QT_EINVAL, "NULL argument");

@@ -135,6 +135,7 @@ struct qt_mat_s {
   std::vector<qt::DevBuf> child; // child[l] : int32 [cnt[l]][4], l = 0..L-1 (-1 = NIL)
   bool levels_built = true;     // false for a fresh product: built on first use
   qt::DevBuf hist;     // int32 per-level node counts per row / per column (see build_levels)
+  std::vector<qt::DevBuf> norm2;  // squared Frobenius norms per node, levels 0..L (screening; lazy)
   // B_ext of a multi-rank multiply: pool1 overrides pool.p (a borrowed view of
   // the local pool); block ids >= split live in pool2 (the received blocks).
   const void* pool1 = nullptr;
@@ -186,8 +187,13 @@ qt_mat truncate_dist(qt_mat A, double tau);
 qt_mat select_blocks(qt_mat A, const uint8_t* d_keep);
 
 // ----- symbolic + numeric multiply (qt_symbolic.cu, qt_numeric.cu)
-// trans: bit 0 = op(A) = A^T, bit 1 = op(B) = B^T  (C = op(A) op(B))
-qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* st, float* ms_sym, float* ms_num, int trans = 0);
+// trans: bit 0 = op(A) = A^T, bit 1 = op(B) = B^T  (C = op(A) op(B)),
+// bit 2 = symmetric square, bits 8+ = its pruning depth.  tau >= 0: norm
+// screening (block products with ||A_ik||*||B_kj|| < tau are skipped).
+qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* st, float* ms_sym, float* ms_num, int trans = 0,
+                      double tau = -1.0);
+// squared Frobenius norms of every quadtree node (levels 0..L) into M->norm2
+void ensure_norms(qt_mat M);
 
 struct NumericArgs {
   int64_t ntiles;            // C nodes at level L-1
@@ -205,6 +211,9 @@ struct NumericArgs {
   int* counter;              // tile scheduler counter (zeroed before launch)
   int group = 1;             // tiles per scheduler grab (1..31)
   int trans = 0;             // bit 0: A transposed, bit 1: B transposed, bit 2: symmetric square
+  const double* normA = nullptr;  // block squared norms (screening) or null
+  const double* normB = nullptr;
+  double tau2 = 0.0;
 };
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a);
 

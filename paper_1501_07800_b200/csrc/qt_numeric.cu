@@ -47,8 +47,15 @@ struct __align__(16) StageHdr {
   int c[4];
   int flags;
   int tbits;  // symmetric square: bit i = A(i,k) transposed, bit 2+j = B(k,j) transposed
-  int pad[2];
+  int pmask;  // bit 2i+j: warp (i,j) computes A(i,k)*B(k,j) at this step
+  int pad;
 };
+
+// a block product survives: both present and (screening) norms^2 product >= tau^2
+__device__ __forceinline__ bool prod_ok(int a, int b, const NumericArgs& na) {
+  if (a < 0 || b < 0) return false;
+  return !na.normA || __dmul_rn(na.normA[a], na.normB[b]) >= na.tau2;
+}
 
 // a level L-1 child entry -> (block index, transposed) ; plain indices unless symmetric
 template <bool kSym>
@@ -236,30 +243,37 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
             int ta0, ta1, tb0, tb1;
             const int a0 = blk<kSym>(kb ? A4.y : A4.x, ta0), a1 = blk<kSym>(kb ? A4.w : A4.z, ta1);
             const int b0 = blk<kSym>(kb ? B4.z : B4.x, tb0), b1 = blk<kSym>(kb ? B4.w : B4.y, tb1);
-            if (!((a0 >= 0 || a1 >= 0) && (b0 >= 0 || b1 >= 0))) continue;
+            // products of this step: both blocks present and, when screening,
+            // ||A(i,k)||^2 * ||B(k,j)||^2 >= tau^2 (the symbolic pass's test)
+            const int pm = (prod_ok(a0, b0, a) ? 1 : 0) | (prod_ok(a0, b1, a) ? 2 : 0) |
+                           (prod_ok(a1, b0, a) ? 4 : 0) | (prod_ok(a1, b1, a) ? 8 : 0);
+            if (!pm) continue;
+            const int la0 = (pm & 3) ? a0 : -1, la1 = (pm & 12) ? a1 : -1;
+            const int lb0 = (pm & 5) ? b0 : -1, lb1 = (pm & 10) ? b1 : -1;
             mbar_wait(&empty[stage], phase ^ 1);
             if (lane == 0) {
               StageHdr& h = hdr[stage];
-              h.a[0] = a0;
-              h.a[1] = a1;
-              h.b[0] = b0;
-              h.b[1] = b1;
+              h.a[0] = la0;
+              h.a[1] = la1;
+              h.b[0] = lb0;
+              h.b[1] = lb1;
               h.flags = F_COMPUTE;
               h.tbits = ta0 | (ta1 << 1) | (tb0 << 2) | (tb1 << 3);
-              const uint32_t bytes = 8192u * ((a0 >= 0) + (a1 >= 0) + (b0 >= 0) + (b1 >= 0));
+              h.pmask = pm;
+              const uint32_t bytes = 8192u * ((la0 >= 0) + (la1 >= 0) + (lb0 >= 0) + (lb1 >= 0));
               mbar_arrive_expect_tx(&full[stage], bytes);
               double* dst = data + (size_t)stage * kStageElems;
-              if (a0 >= 0) bulk_g2s(dst, poolA + (size_t)a0 * kBlockElems, 8192u, &full[stage]);
-              if (a1 >= 0)
-                bulk_g2s(dst + kBlockElems, poolA + (size_t)a1 * kBlockElems, 8192u, &full[stage]);
-              if (b0 >= 0) {
-                const double* src = b0 < a.splitB ? poolB + (size_t)b0 * kBlockElems
-                                                  : poolB2 + (size_t)(b0 - a.splitB) * kBlockElems;
+              if (la0 >= 0) bulk_g2s(dst, poolA + (size_t)la0 * kBlockElems, 8192u, &full[stage]);
+              if (la1 >= 0)
+                bulk_g2s(dst + kBlockElems, poolA + (size_t)la1 * kBlockElems, 8192u, &full[stage]);
+              if (lb0 >= 0) {
+                const double* src = lb0 < a.splitB ? poolB + (size_t)lb0 * kBlockElems
+                                                   : poolB2 + (size_t)(lb0 - a.splitB) * kBlockElems;
                 bulk_g2s(dst + 2 * kBlockElems, src, 8192u, &full[stage]);
               }
-              if (b1 >= 0) {
-                const double* src = b1 < a.splitB ? poolB + (size_t)b1 * kBlockElems
-                                                  : poolB2 + (size_t)(b1 - a.splitB) * kBlockElems;
+              if (lb1 >= 0) {
+                const double* src = lb1 < a.splitB ? poolB + (size_t)lb1 * kBlockElems
+                                                   : poolB2 + (size_t)(lb1 - a.splitB) * kBlockElems;
                 bulk_g2s(dst + 3 * kBlockElems, src, 8192u, &full[stage]);
               }
             }
@@ -312,30 +326,37 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
             int ta0, ta1, tb0, tb1;
             const int a0 = blk<kSym>(kb ? A4.y : A4.x, ta0), a1 = blk<kSym>(kb ? A4.w : A4.z, ta1);
             const int b0 = blk<kSym>(kb ? B4.z : B4.x, tb0), b1 = blk<kSym>(kb ? B4.w : B4.y, tb1);
-            if (!((a0 >= 0 || a1 >= 0) && (b0 >= 0 || b1 >= 0))) continue;
+            // products of this step: both blocks present and, when screening,
+            // ||A(i,k)||^2 * ||B(k,j)||^2 >= tau^2 (the symbolic pass's test)
+            const int pm = (prod_ok(a0, b0, a) ? 1 : 0) | (prod_ok(a0, b1, a) ? 2 : 0) |
+                           (prod_ok(a1, b0, a) ? 4 : 0) | (prod_ok(a1, b1, a) ? 8 : 0);
+            if (!pm) continue;
+            const int la0 = (pm & 3) ? a0 : -1, la1 = (pm & 12) ? a1 : -1;
+            const int lb0 = (pm & 5) ? b0 : -1, lb1 = (pm & 10) ? b1 : -1;
             mbar_wait(&empty[stage], phase ^ 1);
             if (lane == 0) {
               StageHdr& h = hdr[stage];
-              h.a[0] = a0;
-              h.a[1] = a1;
-              h.b[0] = b0;
-              h.b[1] = b1;
+              h.a[0] = la0;
+              h.a[1] = la1;
+              h.b[0] = lb0;
+              h.b[1] = lb1;
               h.flags = F_COMPUTE;
               h.tbits = ta0 | (ta1 << 1) | (tb0 << 2) | (tb1 << 3);
-              const uint32_t bytes = 8192u * ((a0 >= 0) + (a1 >= 0) + (b0 >= 0) + (b1 >= 0));
+              h.pmask = pm;
+              const uint32_t bytes = 8192u * ((la0 >= 0) + (la1 >= 0) + (lb0 >= 0) + (lb1 >= 0));
               mbar_arrive_expect_tx(&full[stage], bytes);
               double* dst = data + (size_t)stage * kStageElems;
-              if (a0 >= 0) bulk_g2s(dst, poolA + (size_t)a0 * kBlockElems, 8192u, &full[stage]);
-              if (a1 >= 0)
-                bulk_g2s(dst + kBlockElems, poolA + (size_t)a1 * kBlockElems, 8192u, &full[stage]);
-              if (b0 >= 0) {
-                const double* src = b0 < a.splitB ? poolB + (size_t)b0 * kBlockElems
-                                                  : poolB2 + (size_t)(b0 - a.splitB) * kBlockElems;
+              if (la0 >= 0) bulk_g2s(dst, poolA + (size_t)la0 * kBlockElems, 8192u, &full[stage]);
+              if (la1 >= 0)
+                bulk_g2s(dst + kBlockElems, poolA + (size_t)la1 * kBlockElems, 8192u, &full[stage]);
+              if (lb0 >= 0) {
+                const double* src = lb0 < a.splitB ? poolB + (size_t)lb0 * kBlockElems
+                                                   : poolB2 + (size_t)(lb0 - a.splitB) * kBlockElems;
                 bulk_g2s(dst + 2 * kBlockElems, src, 8192u, &full[stage]);
               }
-              if (b1 >= 0) {
-                const double* src = b1 < a.splitB ? poolB + (size_t)b1 * kBlockElems
-                                                  : poolB2 + (size_t)(b1 - a.splitB) * kBlockElems;
+              if (lb1 >= 0) {
+                const double* src = lb1 < a.splitB ? poolB + (size_t)lb1 * kBlockElems
+                                                   : poolB2 + (size_t)(lb1 - a.splitB) * kBlockElems;
                 bulk_g2s(dst + 3 * kBlockElems, src, 8192u, &full[stage]);
               }
             }
@@ -367,6 +388,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   } else {
     // ------------------------------------------------------------ consumers
     const int q = warp % kConsumerWarps;
+    const int warp_q = q;
     const int wi = q >> 1, wj = q & 1;
     double* poolC = static_cast<double*>(a.poolC);
     double acc[4][4][2];
@@ -399,7 +421,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
 #pragma unroll
           for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
       } else {
-        const bool go = h.a[wi] >= 0 && h.b[wj] >= 0;
+        const bool go = (h.pmask >> warp_q) & 1;
         if (go) {
           const double* st = data + (size_t)stage * kStageElems;
           const double* As = st + wi * kBlockElems;

@@ -70,17 +70,34 @@ __device__ __forceinline__ bool on_diagonal(uint64_t ckey) {
 }
 
 // A child (i,k) sits in slot 2i+k, B child (k,j) in slot 2k+j, C child (i,j) in 2i+j.
-__device__ __forceinline__ void child_counts(int4 a, int4 b, int (&c)[4]) {
-  c[0] = (a.x >= 0 && b.x >= 0) + (a.y >= 0 && b.z >= 0);  // (0,0)
-  c[1] = (a.x >= 0 && b.y >= 0) + (a.y >= 0 && b.w >= 0);  // (0,1)
-  c[2] = (a.z >= 0 && b.x >= 0) + (a.w >= 0 && b.z >= 0);  // (1,0)
-  c[3] = (a.z >= 0 && b.y >= 0) + (a.w >= 0 && b.w >= 0);  // (1,1)
+// Norm screening (qt_multiply_screened): a child task (a, b) survives iff
+// ||a||^2 * ||b||^2 >= tau^2, squared Frobenius norms of quadtree nodes.  A
+// node's squared norm is the sum of its blocks', so a node pair below the
+// threshold contains only block pairs below it: pruning at any level is exact
+// with respect to the block-level test.  na == nullptr: no screening.
+struct Screen {
+  const double* na;
+  const double* nb;
+  double tau2;
+};
+__device__ __forceinline__ bool pair_ok(int ar, int br, const Screen& sc, bool sym) {
+  if (ar < 0 || br < 0) return false;
+  if (!sc.na) return true;
+  const int ai = sym ? (ar >> 2) : ar, bi = sym ? (br >> 2) : br;
+  return __dmul_rn(sc.na[ai], sc.nb[bi]) >= sc.tau2;
+}
+__device__ __forceinline__ void child_counts(int4 a, int4 b, int (&c)[4], const Screen& sc, bool sym) {
+  c[0] = pair_ok(a.x, b.x, sc, sym) + pair_ok(a.y, b.z, sc, sym);  // (0,0)
+  c[1] = pair_ok(a.x, b.y, sc, sym) + pair_ok(a.y, b.w, sc, sym);  // (0,1)
+  c[2] = pair_ok(a.z, b.x, sc, sym) + pair_ok(a.w, b.z, sc, sym);  // (1,0)
+  c[3] = pair_ok(a.z, b.y, sc, sym) + pair_ok(a.w, b.w, sc, sym);  // (1,1)
 }
 
 // Write the child tasks of task p (group s, local index loc) at the exclusive
 // offsets `off` of its (s,q) slots; gidx maps (s,q) to the new group index.
 __device__ __forceinline__ void emit_task(int4 a4, int4 b4, int64_t base, int32_t m, int32_t s,
-                                          bool skip_lower, const int32_t* __restrict__ off,
+                                          bool skip_lower, const Screen& sc, bool sym,
+                                          const int32_t* __restrict__ off,
                                           const int32_t* __restrict__ gidx, int32_t* __restrict__ pa2,
                                           int32_t* __restrict__ pb2, int32_t* __restrict__ pc2) {
   const int a[4] = {a4.x, a4.y, a4.z, a4.w};
@@ -93,7 +110,7 @@ __device__ __forceinline__ void emit_task(int4 a4, int4 b4, int64_t base, int32_
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int ac = a[2 * i + k], bc = b[2 * k + j];
-      if (ac >= 0 && bc >= 0) {
+      if (pair_ok(ac, bc, sc, sym)) {
         if (pos < 0) {
           pos = off[base + (int64_t)q * m];
           newc = gidx[4 * s + q];
@@ -123,6 +140,9 @@ struct SmallBfsArgs {
   int32_t* gidx;    // 4 * max ns scratch
   int32_t* ns_out;  // C groups per level
   int32_t* f_out;   // tasks per level
+  const double* normA[QT_MAX_LEVELS];  // squared node norms per level (screening), or null
+  const double* normB[QT_MAX_LEVELS];
+  double tau2;
 };
 
 __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) {
@@ -155,11 +175,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     const uint64_t* ck = a.ckey[cur];
     const int4* cA = a.childA[l];
     const int4* cB = a.childB[l];
+    const Screen sc{a.normA[l + 1], a.normB[l + 1], a.tau2};
     // 1. child-task counts per (task, C child), group-major
     for (int p = tid; p < F; p += kSmallThreads) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
       int c[4];
-      child_counts(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym), c);
+      child_counts(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym), c,
+                   sc, sym);
       if (prune && on_diagonal(ck[s])) c[2] = 0;
       const int64_t base = 4ll * c0 + (p - c0);
 #pragma unroll
@@ -214,7 +236,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     for (int p = tid; p < F; p += kSmallThreads) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
       emit_task(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym),
-                4ll * c0 + (p - c0), m, s, prune && on_diagonal(ck[s]), a.off, a.gidx, a.pa[nxt], a.pb[nxt],
+                4ll * c0 + (p - c0), m, s, prune && on_diagonal(ck[s]), sc, sym, a.off, a.gidx, a.pa[nxt],
+                a.pb[nxt],
                 a.pc[nxt]);
     }
     __syncthreads();
@@ -236,7 +259,7 @@ __global__ void k_count(int32_t Fb, const int32_t* __restrict__ f_dev, const int
                         const int32_t* __restrict__ pb, const int32_t* __restrict__ pc,
                         const int32_t* __restrict__ cstart, const uint64_t* __restrict__ ckey,
                         const int4* __restrict__ childA, const int4* __restrict__ childB, int mode,
-                        int32_t* __restrict__ cnt) {
+                        Screen sc, int32_t* __restrict__ cnt) {
   const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= Fb) return;
   if (p >= *f_dev) {
@@ -246,7 +269,8 @@ __global__ void k_count(int32_t Fb, const int32_t* __restrict__ f_dev, const int
   const bool sym = mode & 4;
   const int32_t s = pc[p], c0 = cstart[s], m = cstart[s + 1] - c0;
   int c[4];
-  child_counts(op_children(childA, pa[p], mode & 1, sym), op_children(childB, pb[p], mode & 2, sym), c);
+  child_counts(op_children(childA, pa[p], mode & 1, sym), op_children(childB, pb[p], mode & 2, sym), c,
+               sc, sym);
   if ((mode & 8) && on_diagonal(ckey[s])) c[2] = 0;
   const int64_t base = 4ll * c0 + (p - c0);
 #pragma unroll
@@ -304,7 +328,7 @@ __global__ void k_emit(int32_t Fb, const int32_t* __restrict__ f_dev, const int3
                        const int32_t* __restrict__ pb, const int32_t* __restrict__ pc,
                        const int32_t* __restrict__ cstart, const uint64_t* __restrict__ ckey,
                        const int4* __restrict__ childA, const int4* __restrict__ childB, int mode,
-                       const int32_t* __restrict__ off, const int32_t* __restrict__ gidx,
+                       Screen sc, const int32_t* __restrict__ off, const int32_t* __restrict__ gidx,
                        int32_t* __restrict__ pa2, int32_t* __restrict__ pb2,
                        int32_t* __restrict__ pc2) {
   const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -312,7 +336,8 @@ __global__ void k_emit(int32_t Fb, const int32_t* __restrict__ f_dev, const int3
   const bool sym = mode & 4;
   const int32_t s = pc[p], c0 = cstart[s], m = cstart[s + 1] - c0;
   emit_task(op_children(childA, pa[p], mode & 1, sym), op_children(childB, pb[p], mode & 2, sym),
-            4ll * c0 + (p - c0), m, s, (mode & 8) && on_diagonal(ckey[s]), off, gidx, pa2, pb2, pc2);
+            4ll * c0 + (p - c0), m, s, (mode & 8) && on_diagonal(ckey[s]), sc, sym, off, gidx, pa2, pb2,
+            pc2);
 }
 
 // Upper bound of the symmetric square's tasks per level: with the full
@@ -361,7 +386,18 @@ struct Trace {
   }
 };
 
-qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* ms_num, int trans) {
+qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* ms_num, int trans,
+                      double tau) {
+  const bool screen = tau >= 0.0;
+  const double tau2 = tau * tau;
+  if (screen) {
+    ensure_norms(A);
+    ensure_norms(B);
+  }
+  auto screen_at = [&](int level) {
+    return Screen{screen ? A->norm2[level].as<double>() : nullptr,
+                  screen ? B->norm2[level].as<double>() : nullptr, tau2};
+  };
   // trans: bit 0 A^T, bit 1 B^T, bit 2 symmetric square (A = B = U, C upper)
   const bool sym = trans & 4;
   Trace tr;
@@ -438,6 +474,11 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       SmallBfsArgs sa;
       sa.l_end = l_end;
       sa.trans = trans;
+      sa.tau2 = tau2;
+      for (int l = 0; l <= L && l < QT_MAX_LEVELS; ++l) {
+        sa.normA[l] = screen ? A->norm2[l].as<double>() : nullptr;
+        sa.normB[l] = screen ? B->norm2[l].as<double>() : nullptr;
+      }
       for (int l = 0; l < L; ++l) {
         sa.childA[l] = A->child[l].as<int4>();
         sa.childB[l] = B->child[l].as<int4>();
@@ -478,7 +519,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         k_count<<<grid_for(Fb), kThreads, 0, st>>>(Fb, fd + l, pa.as<int32_t>(), pb.as<int32_t>(),
                                                    pc.as<int32_t>(), cstart.as<int32_t>(),
                                                    ckey.as<uint64_t>(), A->child[l].as<int4>(),
-                                                   B->child[l].as<int4>(), mode_l, cnt.as<int32_t>());
+                                                   B->child[l].as<int4>(), mode_l, screen_at(l + 1),
+                                                   cnt.as<int32_t>());
         QT_LAUNCH_CHECK(ctx);
         excl_sum(ctx, cnt.as<int32_t>(), off.as<int32_t>(), n4);
         DevBuf flag(4 * s4, st), gstart(4 * s4, st), nex(4 * s4, st), gidx(4 * s4, st);
@@ -505,7 +547,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         k_emit<<<grid_for(Fb), kThreads, 0, st>>>(Fb, fd + l, pa.as<int32_t>(), pb.as<int32_t>(),
                                                   pc.as<int32_t>(), cstart.as<int32_t>(),
                                                   ckey.as<uint64_t>(), A->child[l].as<int4>(),
-                                                  B->child[l].as<int4>(), mode_l, off.as<int32_t>(),
+                                                  B->child[l].as<int4>(), mode_l, screen_at(l + 1),
+                                                  off.as<int32_t>(),
                                                   gidx.as<int32_t>(), pa2.as<int32_t>(),
                                                   pb2.as<int32_t>(), pc2.as<int32_t>());
         QT_LAUNCH_CHECK(ctx);
@@ -553,6 +596,9 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       na.poolC = C->pool.p;
       na.counter = ctx->counters.as<int>() + 16;
       na.trans = trans & 7;  // bit 2: symmetric square (block refs carry transpose bits)
+      na.normA = screen ? A->norm2[L].as<double>() : nullptr;
+      na.normB = screen ? B->norm2[L].as<double>() : nullptr;
+      na.tau2 = tau2;
       // tiles per scheduler grab: ~32 tasks per grab, at most 16 tiles
       {
         const int64_t per_tile = std::max<int64_t>(1, F[L - 1] / std::max<int32_t>(1, ns[L - 1]));

@@ -422,6 +422,67 @@ __global__ void k_quad_terms(const double* __restrict__ nrm32, const uint64_t* _
 }
 }  // namespace
 
+namespace {
+// squared Frobenius norm of each block: one thread, row-major order, separate
+// multiply and add roundings (the oracle's loop, so both take the same
+// screening decisions)
+template <class T>
+__global__ void k_block_norm2_seq(const T* __restrict__ pool, int64_t nb, double* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nb;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const T* b = pool + t * 1024;
+    double s = 0.0;
+    for (int r = 0; r < 32; ++r)
+      for (int c = 0; c < 32; ++c) {
+        const double v = (double)b[sizeof(T) == 8 ? swz64(r, c) : swz32(r, c)];
+        s = __dadd_rn(s, __dmul_rn(v, v));
+      }
+    out[t] = s;
+  }
+}
+// node norm^2 = sum of its children's in slot order
+__global__ void k_node_norm2(const int4* __restrict__ child, int64_t n, const double* __restrict__ below,
+                             double* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int4 c = child[t];
+    double s = 0.0;
+    if (c.x >= 0) s = __dadd_rn(s, below[c.x]);
+    if (c.y >= 0) s = __dadd_rn(s, below[c.y]);
+    if (c.z >= 0) s = __dadd_rn(s, below[c.z]);
+    if (c.w >= 0) s = __dadd_rn(s, below[c.w]);
+    out[t] = s;
+  }
+}
+}  // namespace
+
+void ensure_norms(qt_mat M) {
+  if (!M->norm2.empty()) return;
+  ensure_levels(M);
+  qt_ctx ctx = M->ctx;
+  cudaStream_t st = ctx->stream;
+  std::vector<DevBuf> nv(M->L + 1);
+  nv[M->L].alloc(8 * std::max<int64_t>(M->nb, 1), st);
+  if (M->nb > 0) {
+    if (M->dtype == QT_F64)
+      k_block_norm2_seq<double><<<grid_for(M->nb), kThreads, 0, st>>>(M->pool.as<double>(), M->nb,
+                                                                       nv[M->L].as<double>());
+    else
+      k_block_norm2_seq<float><<<grid_for(M->nb), kThreads, 0, st>>>(M->pool.as<float>(), M->nb,
+                                                                      nv[M->L].as<double>());
+    QT_LAUNCH_CHECK(ctx);
+  }
+  for (int l = M->L - 1; l >= 0; --l) {
+    nv[l].alloc(8 * std::max<int64_t>(M->cnt[l], 1), st);
+    if (M->cnt[l] > 0) {
+      k_node_norm2<<<grid_for(M->cnt[l]), kThreads, 0, st>>>(M->child[l].as<int4>(), M->cnt[l],
+                                                             nv[l + 1].as<double>(), nv[l].as<double>());
+      QT_LAUNCH_CHECK(ctx);
+    }
+  }
+  M->norm2 = std::move(nv);
+}
+
 void split64(qt_ctx ctx, qt_dtype dt, int64_t nb, const int32_t* brow, const int32_t* bcol,
              const void* vals, DevBuf& obrow, DevBuf& obcol, DevBuf& ovals) {
   cudaStream_t st = ctx->stream;

@@ -69,6 +69,7 @@ def _load():
         "qt_multiply": [P, P, P, P],
         "qt_multiply_ex": [P, P, i32, i32, P, P],
         "qt_symm_square": [P, P, P],
+        "qt_multiply_screened": [P, P, ctypes.c_double, P, P],
         "qt_multiply_virtual": [P, P, i32, i32, P, P, P],
         "qt_truncate": [P, ctypes.c_double, P],
         "qt_info": [P, P, P, P, P, P, P, P, P],
@@ -93,7 +94,7 @@ def _load():
 
 _lib = _load()
 EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_nccl_unique_id", "qt_create", "qt_multiply",
-            "qt_multiply_ex", "qt_symm_square",
+            "qt_multiply_ex", "qt_symm_square", "qt_multiply_screened",
             "qt_multiply_virtual", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
             "qt_destroy", "qt_last_error", "qt_kernel_launches", "qt_fp64_peak",
             "qt_loopback_hub_create", "qt_loopback_hub_destroy", "qt_ctx_create_loopback")
@@ -247,6 +248,13 @@ class Matrix:
         h = ctypes.c_void_p()
         _check(_lib.qt_multiply_ex(self._h, other._h, int(trans_a), int(trans_b), ctypes.byref(h),
                                    ctypes.byref(st)))
+        return Matrix(self.ctx, h), st
+
+    def multiply_screened(self, other: "Matrix", tau: float):
+        """C~ = sum of the block products with ||A_ik|| ||B_kj|| >= tau."""
+        st = Stats()
+        h = ctypes.c_void_p()
+        _check(_lib.qt_multiply_screened(self._h, other._h, float(tau), ctypes.byref(h), ctypes.byref(st)))
         return Matrix(self.ctx, h), st
 
     def symm_square(self):

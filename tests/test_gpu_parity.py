@@ -680,3 +680,48 @@ def test_bs64_truncate_and_virtual(qt, ctx):
         assert np.array_equal(rg, full[0][m]) and np.array_equal(vg, full[2][m])
         plan = oracle.exchange_plan(bounds, (M.brow, M.bcol), (M.brow, M.bcol), 64 * 64 * 8)[g]
         assert st.bytes_recv_payload == plan["payload_bytes"]
+
+
+# ----------------------------------------------------------------- norm-screened product
+
+
+def _taus(Am, Bm):
+    na = np.sqrt(oracle.block_norm2(Am.vals))
+    nb = np.sqrt(oracle.block_norm2(Bm.vals))
+    prods = np.unique(np.outer(na, nb).ravel())
+    mids = (prods[1:] + prods[:-1]) / 2
+    return [0.0] + [float(mids[int(len(mids) * f)]) for f in (0.1, 0.5, 0.9)]
+
+
+@pytest.mark.parametrize("nbr,p", [(9, 0.5), (40, 0.15)])
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_screened_multiply(qt, ctx, nbr, p, kind):
+    rng = np.random.default_rng(300 + nbr + (kind == "int"))
+    Am = random_bm(rng, nbr, 32, p, kind, 128)
+    Bm = random_bm(rng, nbr, 32, p, kind, 128)
+    Am.vals *= rng.integers(1, 9, size=(Am.nb, 1, 1))     # varied block norms
+    Bm.vals *= rng.integers(1, 9, size=(Bm.nb, 1, 1))
+    A, B = mk(qt, ctx, Am), mk(qt, ctx, Bm)
+    for tau in _taus(Am, Bm):
+        C, st = A.multiply_screened(B, tau)
+        got = C.to_blocks()
+        ref = oracle.spgemm(nbr, 32, as_tuple(Am), as_tuple(Bm), tau=tau)
+        assert_same_pattern(got, ref)
+        if kind == "int":
+            assert np.array_equal(got[2], ref[2])
+        elif len(ref[0]):
+            assert np.linalg.norm(got[2] - ref[2]) <= REL_FRO_F64 * np.linalg.norm(ref[2])
+        assert st.block_products <= oracle.level_task_counts(
+            oracle.tree_levels(Am.n, 32, 128)[0], (Am.brow, Am.bcol), (Bm.brow, Bm.bcol))[-1]
+
+
+def test_screened_eslike_small(qt, ctx):
+    c = qtgen.config(4, small=True)
+    Am = c["A"]
+    A = mk(qt, ctx, Am)
+    for tau in [1e-3, 1e-1]:
+        C, st = A.multiply_screened(A, tau)
+        got = C.to_blocks()
+        ref = oracle.spgemm(Am.nbr, 32, as_tuple(Am), as_tuple(Am), tau=tau)
+        assert_same_pattern(got, ref)
+        assert np.linalg.norm(got[2] - ref[2]) <= REL_FRO_F64 * np.linalg.norm(ref[2])

@@ -489,3 +489,67 @@ def test_symm_level_counts_dense_closed_form():
     r, c = np.nonzero(np.triu(np.ones((nbr, nbr), bool)))
     got = oracle.level_task_counts_sym(L, (r, c))
     assert got == [(1 << l) * (1 << l) * ((1 << l) + 1) // 2 for l in range(L + 1)]
+
+
+# --------------------------------------------------------------------- norm-screened product (f4)
+
+
+def _scaled_int_matrix(rng, nbr, bs, p):
+    br, bc, v = _random_block_matrix(rng, nbr, bs, p)
+    v = v * rng.integers(1, 9, size=(len(br), 1, 1))     # varied block norms, still integers
+    return br, bc, v
+
+
+def _separating_taus(a, b):
+    """thresholds half-way between distinct values of ||A_IK|| ||B_KJ||, so no
+    product sits on the boundary (decisions independent of rounding order)"""
+    na = np.sqrt((a[2] ** 2).sum(axis=(1, 2)))
+    nb = np.sqrt((b[2] ** 2).sum(axis=(1, 2)))
+    prods = np.unique(np.outer(na, nb).ravel())
+    mids = (prods[1:] + prods[:-1]) / 2
+    return [float(mids[len(mids) // 4]), float(mids[len(mids) // 2]), float(mids[3 * len(mids) // 4])]
+
+
+def test_screened_product_vs_bruteforce_enumeration():
+    rng = np.random.default_rng(41)
+    nbr, bs = 8, 4
+    a = _scaled_int_matrix(rng, nbr, bs, 0.5)
+    b = _scaled_int_matrix(rng, nbr, bs, 0.5)
+    na = np.sqrt((a[2] ** 2).sum(axis=(1, 2)))
+    nb = np.sqrt((b[2] ** 2).sum(axis=(1, 2)))
+    for tau in _separating_taus(a, b) + [0.0]:
+        ref = {}
+        for p in range(len(a[0])):
+            for q in range(len(b[0])):
+                if a[1][p] != b[0][q] or na[p] * nb[q] < tau:
+                    continue
+                key = (int(a[0][p]), int(b[1][q]))
+                ref[key] = ref.get(key, 0) + a[2][p] @ b[2][q]
+        r, c, v = oracle.spgemm(nbr, bs, a, b, tau=tau)
+        assert sorted(ref) == list(zip(r.tolist(), c.tolist()))
+        for t in range(len(r)):
+            assert np.array_equal(v[t], ref[(r[t], c[t])])
+
+
+def test_screened_zero_tau_is_exact_and_error_bound():
+    rng = np.random.default_rng(42)
+    nbr, bs = 10, 4
+    a = _random_block_matrix(rng, nbr, bs, 0.5, "uniform")
+    b = _random_block_matrix(rng, nbr, bs, 0.5, "uniform")
+    full = oracle.spgemm(nbr, bs, a, b)
+    zero = oracle.spgemm(nbr, bs, a, b, tau=0.0)
+    assert np.array_equal(full[0], zero[0]) and np.array_equal(full[2], zero[2])
+    na = np.sqrt(oracle.block_norm2(a[2]))
+    nb = np.sqrt(oracle.block_norm2(b[2]))
+    prev = None
+    for tau in _separating_taus(a, b):
+        r, c, v = oracle.spgemm(nbr, bs, a, b, tau=tau)
+        F = _blocks_to_dense(nbr, bs, *full)
+        S = _blocks_to_dense(nbr, bs, r, c, v)
+        skipped = sum(na[p] * nb[q] for p in range(len(a[0])) for q in range(len(b[0]))
+                      if a[1][p] == b[0][q] and na[p] * nb[q] < tau)
+        assert np.linalg.norm(F - S) <= skipped * (1 + 1e-12)
+        cur = set(zip(r.tolist(), c.tolist()))
+        if prev is not None:
+            assert cur <= prev          # a larger tau keeps a subset of the pattern
+        prev = cur
