@@ -132,6 +132,38 @@ def main():
         elif w == "sym4":
             run_sym(ctx, stream, "cfg4 ES-like symmetric (S^2): symm_square vs full",
                     qtgen.config(4, symmetric=True)["A"], steps=5)
+        elif w == "scr4":
+            import oracle  # noqa: F401  (not used: error measured against the unscreened product)
+            c = qtgen.config(4)
+            Am = c["A"]
+            A = qtmm.Matrix.from_blocks(ctx, Am.n, Am.leaf_dim, 32, Am.brow, Am.bcol, Am.vals)
+            C0, st0 = A.multiply(A)
+            r0, c0, v0 = C0.to_blocks()
+            for tau in (0.5, 2.0, 8.0):
+                for _ in range(2):
+                    C, st = A.multiply_screened(A, tau)
+                    C.close()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(5):
+                    C, st = A.multiply_screened(A, tau)
+                    if _ < 4:
+                        C.close()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                r, cc, v = C.to_blocks()
+                # error vs the full product (blocks missing from C count as zero)
+                idx = {(int(a), int(b)): t for t, (a, b) in enumerate(zip(r, cc))}
+                err2 = 0.0
+                for t in range(len(r0)):
+                    k = (int(r0[t]), int(c0[t]))
+                    d = v0[t] - (v[idx[k]] if k in idx else 0.0)
+                    err2 += float((d * d).sum())
+                print(json.dumps({"config": f"cfg4 screened tau={tau}", "ms_step": round(e0.elapsed_time(e1) / 5, 4),
+                                  "block_products": st.block_products, "full_products": st0.block_products,
+                                  "c_blocks": st.c_blocks, "rel_fro_err_vs_full": (err2 ** 0.5) / float(np.linalg.norm(v0))}),
+                      flush=True)
         elif w == "dense4096":
             br, bc = qtgen.pattern_dense(128)
             v = qtgen.block_values(br, bc, 32, 1)
