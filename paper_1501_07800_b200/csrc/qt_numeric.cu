@@ -116,33 +116,85 @@ __device__ __forceinline__ int4 shfl_int4(int4 v, int src) {
   return v;
 }
 
-// One 32x32x32 block product on one warp: acc += op(A)·op(B), A and B in the
-// internal swizzled layout (qt_common.cuh swz64) in shared memory.  A
-// transposed operand is read with the other operand's fragment pattern
-// (op(A)(r,c) = A(c,r)), which the swizzle also serves conflict-free.
-template <bool kTA, bool kTB>
-__device__ __forceinline__ void warp_block_mma(double (&acc)[4][4][2], const double* __restrict__ As,
-                                               const double* __restrict__ Bs, int lane) {
+// Fragment offsets in the internal swizzled layout (qt_common.cuh swz64) for
+// the mma.m8n8k4.f64 operand of row/column x = 16q + 8m + g at k-slice ks:
+//   "x-major" element (x, 4ks+t4)  — A as stored, or B read transposed;
+//   "k-major" element (4ks+t4, x)  — B as stored, or A read transposed.
+// Both patterns hit every 8-byte bank pair exactly twice (the minimum).
+__device__ __forceinline__ int off_x(int q, int m, int ks, int g, int t4) {
+  return (16 * q + 8 * m + g) * 32 + (((ks ^ (g & 3)) << 2) | t4);
+}
+__device__ __forceinline__ int off_k(int q, int m, int ks, int g, int t4) {
+  return (4 * ks + t4) * 32 + 16 * q + ((8 * m + g) ^ (t4 << 2));
+}
+
+// One step of a tile on one consumer warp: warp (qi, qj) accumulates the
+// (qi, qj) 16x16 quadrant of C(Ii,Jj) += op(A(Ii,k))·op(B(k,Jj)) for every
+// product p = 2i+j of the step (bit p of PM).  Every warp therefore does the
+// same number of DMMAs whatever the step's product mask is, so the four SM
+// sub-partitions stay balanced on sparse patterns (a step of a banded tile has
+// 4 products, an ES-like one 2.2 on average, a random one ~1).  A fragments
+// of A(Ii,k) are shared by the products of row i, B fragments of B(k,Jj) by
+// those of column j.  PM is a template parameter so that only the step's own
+// loads and DMMAs are issued (a predicated-off DMMA still occupies the pipe).
+// tA/tB: per-block transposes (bit 0: block 0, bit 1: block 1).
+template <int PM>
+__device__ __forceinline__ void warp_step_mma(double (&acc)[4][2][2][2], const double* __restrict__ st,
+                                              int tA, int tB, int qi, int qj, int lane) {
+  constexpr bool ua0 = PM & 3, ua1 = PM & 12, ub0 = PM & 5, ub1 = PM & 10;
   const int g = lane >> 2, t4 = lane & 3;
-  const int xa = g & 3;
-  const int xb = g ^ (t4 << 2);
+  const double* A0 = st;
+  const double* A1 = st + kBlockElems;
+  const double* B0 = st + 2 * kBlockElems;
+  const double* B1 = st + 3 * kBlockElems;
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
-    double af[4], bf[4];
-    const int kcol = ((ks ^ xa) << 2) | t4;
+    double af[2][2], bf[2][2];
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
-      af[m] = kTA ? As[(ks * 4 + t4) * 32 + ((m * 8) ^ xb)] : As[(m * 8 + g) * 32 + kcol];
+    for (int m = 0; m < 2; ++m) {
+      const int ox = off_x(qi, m, ks, g, t4), ok = off_k(qi, m, ks, g, t4);
+      if (ua0) af[0][m] = A0[(tA & 1) ? ok : ox];
+      if (ua1) af[1][m] = A1[(tA & 2) ? ok : ox];
+    }
 #pragma unroll
-    for (int n = 0; n < 4; ++n)
-      bf[n] = kTB ? Bs[(n * 8 + g) * 32 + kcol] : Bs[(ks * 4 + t4) * 32 + ((n * 8) ^ xb)];
+    for (int n = 0; n < 2; ++n) {
+      const int ox = off_x(qj, n, ks, g, t4), ok = off_k(qj, n, ks, g, t4);
+      if (ub0) bf[0][n] = B0[(tB & 1) ? ox : ok];
+      if (ub1) bf[1][n] = B1[(tB & 2) ? ox : ok];
+    }
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
+    for (int p = 0; p < 4; ++p) {
+      if (PM & (1 << p)) {
 #pragma unroll
-      for (int n = 0; n < 4; ++n) dmma(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+          for (int n = 0; n < 2; ++n)
+            dmma(acc[p][m][n][0], acc[p][m][n][1], af[p >> 1][m], bf[p & 1][n]);
+      }
+    }
   }
 }
 
+__device__ __forceinline__ void warp_step(double (&acc)[4][2][2][2], const double* __restrict__ st,
+                                          int pm, int tA, int tB, int qi, int qj, int lane) {
+  switch (pm) {
+    case 1: warp_step_mma<1>(acc, st, tA, tB, qi, qj, lane); break;
+    case 2: warp_step_mma<2>(acc, st, tA, tB, qi, qj, lane); break;
+    case 3: warp_step_mma<3>(acc, st, tA, tB, qi, qj, lane); break;
+    case 4: warp_step_mma<4>(acc, st, tA, tB, qi, qj, lane); break;
+    case 5: warp_step_mma<5>(acc, st, tA, tB, qi, qj, lane); break;
+    case 6: warp_step_mma<6>(acc, st, tA, tB, qi, qj, lane); break;
+    case 7: warp_step_mma<7>(acc, st, tA, tB, qi, qj, lane); break;
+    case 8: warp_step_mma<8>(acc, st, tA, tB, qi, qj, lane); break;
+    case 9: warp_step_mma<9>(acc, st, tA, tB, qi, qj, lane); break;
+    case 10: warp_step_mma<10>(acc, st, tA, tB, qi, qj, lane); break;
+    case 11: warp_step_mma<11>(acc, st, tA, tB, qi, qj, lane); break;
+    case 12: warp_step_mma<12>(acc, st, tA, tB, qi, qj, lane); break;
+    case 13: warp_step_mma<13>(acc, st, tA, tB, qi, qj, lane); break;
+    case 14: warp_step_mma<14>(acc, st, tA, tB, qi, qj, lane); break;
+    default: warp_step_mma<15>(acc, st, tA, tB, qi, qj, lane); break;
+  }
+}
 
 template <bool kGrouped, bool kTA, bool kTB, bool kSym>
 __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
@@ -388,14 +440,15 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   } else {
     // ------------------------------------------------------------ consumers
     const int q = warp % kConsumerWarps;
-    const int warp_q = q;
-    const int wi = q >> 1, wj = q & 1;
+    const int qi = q >> 1, qj = q & 1;  // this warp's quadrant of every C block
     double* poolC = static_cast<double*>(a.poolC);
-    double acc[4][4][2];
+    double acc[4][2][2][2];
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
+    for (int p = 0; p < 4; ++p)
 #pragma unroll
-      for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int n = 0; n < 2; ++n) acc[p][m][n][0] = acc[p][m][n][1] = 0.0;
     const int g = lane >> 2, t4 = lane & 3;
     for (;;) {
       mbar_wait(&full[stage], phase);
@@ -403,42 +456,41 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
       const int flags = h.flags;
       if (flags & F_DONE) break;
       if (flags & F_STORE) {
-        const int cb = h.c[q];
+        int cb[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) cb[p] = h.c[p];
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
-        if (cb >= 0) {
-          double* Cb = poolC + (size_t)cb * kBlockElems;
 #pragma unroll
-          for (int m = 0; m < 4; ++m)
+        for (int p = 0; p < 4; ++p) {
+          if (cb[p] >= 0) {
+            double* Cb = poolC + (size_t)cb[p] * kBlockElems;
 #pragma unroll
-            for (int n = 0; n < 4; ++n) {
-              const int r = m * 8 + g, c = n * 8 + 2 * t4;
-              *reinterpret_cast<double2*>(Cb + swz64(r, c)) = make_double2(acc[m][n][0], acc[m][n][1]);
-            }
-        }
+            for (int m = 0; m < 2; ++m)
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
-#pragma unroll
-          for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
-      } else {
-        const bool go = (h.pmask >> warp_q) & 1;
-        if (go) {
-          const double* st = data + (size_t)stage * kStageElems;
-          const double* As = st + wi * kBlockElems;
-          const double* Bs = st + (2 + wj) * kBlockElems;
-          if (kSym) {
-            // per-block transposes of the symmetric expansion (warp-uniform)
-            const int tb = h.tbits;
-            switch (((tb >> wi) & 1) | (((tb >> (2 + wj)) & 1) << 1)) {
-              case 0: warp_block_mma<false, false>(acc, As, Bs, lane); break;
-              case 1: warp_block_mma<true, false>(acc, As, Bs, lane); break;
-              case 2: warp_block_mma<false, true>(acc, As, Bs, lane); break;
-              default: warp_block_mma<true, true>(acc, As, Bs, lane); break;
-            }
-          } else {
-            warp_block_mma<kTA, kTB>(acc, As, Bs, lane);
+              for (int n = 0; n < 2; ++n) {
+                const int r = 16 * qi + 8 * m + g, c = 16 * qj + 8 * n + 2 * t4;
+                *reinterpret_cast<double2*>(Cb + swz64(r, c)) =
+                    make_double2(acc[p][m][n][0], acc[p][m][n][1]);
+              }
           }
+#pragma unroll
+          for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int n = 0; n < 2; ++n) acc[p][m][n][0] = acc[p][m][n][1] = 0.0;
         }
+      } else {
+        const double* st = data + (size_t)stage * kStageElems;
+        const int pm = h.pmask;
+        int tA, tB;
+        if (kSym) {
+          tA = h.tbits & 3;
+          tB = (h.tbits >> 2) & 3;
+        } else {
+          tA = kTA ? 3 : 0;
+          tB = kTB ? 3 : 0;
+        }
+        warp_step(acc, st, pm, tA, tB, qi, qj, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
       }
