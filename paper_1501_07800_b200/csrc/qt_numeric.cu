@@ -52,9 +52,10 @@ struct __align__(16) StageHdr {
 };
 
 // a block product survives: both present and (screening) norms^2 product >= tau^2
+template <bool kScreen>
 __device__ __forceinline__ bool prod_ok(int a, int b, const NumericArgs& na) {
   if (a < 0 || b < 0) return false;
-  return !na.normA || __dmul_rn(na.normA[a], na.normB[b]) >= na.tau2;
+  return !kScreen || __dmul_rn(na.normA[a], na.normB[b]) >= na.tau2;
 }
 
 // a level L-1 child entry -> (block index, transposed) ; plain indices unless symmetric
@@ -196,7 +197,34 @@ __device__ __forceinline__ void warp_step(double (&acc)[4][2][2][2], const doubl
   }
 }
 
-template <bool kGrouped, bool kTA, bool kTB, bool kSym>
+// The two steps (kb = 0, 1) of task p at level L-1: the staged blocks
+// A(I0,k) A(I1,k) B(k,J0) B(k,J1) (-1 = not staged) and meta = product mask |
+// transposes << 4, computed lane-parallel for 32 tasks at a time so that the
+// producer's serial per-step path is only shuffles, the ring wait and the
+// TMA issue.
+struct StepDesc {
+  int a0, a1, b0, b1, meta;
+};
+template <bool kTA, bool kTB, bool kSym, bool kScreen>
+__device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, const NumericArgs& a) {
+  // A child (i,kb) in slot 2i+kb ; B child (kb,j) in slot 2kb+j
+  int ta0, ta1, tb0, tb1;
+  const int a0 = blk<kSym>(kb ? A4.y : A4.x, ta0), a1 = blk<kSym>(kb ? A4.w : A4.z, ta1);
+  const int b0 = blk<kSym>(kb ? B4.z : B4.x, tb0), b1 = blk<kSym>(kb ? B4.w : B4.y, tb1);
+  // products of this step: both blocks present and, when screening,
+  // ||A(i,k)||^2 * ||B(k,j)||^2 >= tau^2 (the symbolic pass's test)
+  const int pm = (prod_ok<kScreen>(a0, b0, a) ? 1 : 0) | (prod_ok<kScreen>(a0, b1, a) ? 2 : 0) |
+                 (prod_ok<kScreen>(a1, b0, a) ? 4 : 0) | (prod_ok<kScreen>(a1, b1, a) ? 8 : 0);
+  StepDesc d;
+  d.a0 = (pm & 3) ? a0 : -1;
+  d.a1 = (pm & 12) ? a1 : -1;
+  d.b0 = (pm & 5) ? b0 : -1;
+  d.b1 = (pm & 10) ? b1 : -1;
+  d.meta = pm | ((ta0 | (ta1 << 1) | (tb0 << 2) | (tb1 << 3)) << 4);
+  return d;
+}
+
+template <bool kTA, bool kTB, bool kSym, bool kScreen>
 __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -224,16 +252,15 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   uint32_t phase = 0;
 
   if (producer) {
-    if constexpr (kGrouped) {
     // ------------------------------------------------------------ producer
     // Work is taken in groups of a.group consecutive tiles (one atomic per
-    // group; the next group's atomic is issued before the current group is
-    // streamed, so its latency is hidden).  The tasks of a group are a
-    // contiguous range of the level L-1 queue; they are streamed 32 at a time
-    // with lane-parallel metadata loads, across tile boundaries, and a STORE
-    // marker is posted at every tile end.  Sparse patterns (few tasks per
-    // tile) get large groups, banded/dense ones group = 1 (fine-grained
-    // dynamic balance).
+    // group; for groups > 1 the next group's atomic is issued before the
+    // current group is streamed, so its latency is hidden).  The tasks of a
+    // group are a contiguous range of the level L-1 queue; they are streamed 32
+    // at a time with lane-parallel metadata loads and step descriptors, across
+    // tile boundaries, and a STORE marker is posted at every tile end.  Sparse
+    // patterns (few tasks per tile) get large groups, banded/dense ones
+    // group = 1 (fine-grained dynamic balance).
     const double* poolA = static_cast<const double*>(a.poolA);
     const double* poolB = static_cast<const double*>(a.poolB);
     const double* poolB2 = static_cast<const double*>(a.poolB2);
@@ -258,6 +285,10 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         phase ^= 1;
       }
     };
+    auto bsrc = [&](int lb) {
+      return lb < a.splitB ? poolB + (size_t)lb * kBlockElems
+                           : poolB2 + (size_t)(lb - a.splitB) * kBlockElems;
+    };
     while (t0 < a.ntiles) {
       const int t1 = min(t0 + G, (int)a.ntiles);
       // next group: prefetched now when groups are large (sparse patterns), taken
@@ -275,10 +306,12 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
       int boundary = __shfl_sync(0xffffffffu, ts, 1);
       for (int pb0 = p_begin; pb0 < p_end; pb0 += 32) {
         const int p = pb0 + lane;
-        int4 ca = make_int4(-1, -1, -1, -1), cb = ca;
+        StepDesc d0{-1, -1, -1, -1, 0}, d1{-1, -1, -1, -1, 0};
         if (p < p_end) {
-          ca = op_children(a.childA, a.pa[p], kTA, kSym);
-          cb = op_children(a.childB, a.pb[p], kTB, kSym);
+          const int4 ca = op_children(a.childA, a.pa[p], kTA, kSym);
+          const int4 cb = op_children(a.childB, a.pb[p], kTB, kSym);
+          d0 = make_step<kTA, kTB, kSym, kScreen>(ca, cb, 0, a);
+          d1 = make_step<kTA, kTB, kSym, kScreen>(ca, cb, 1, a);
         }
         const int nloc = min(32, p_end - pb0);
         for (int u = 0; u < nloc; ++u) {
@@ -287,21 +320,15 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
             ++cur;
             boundary = __shfl_sync(0xffffffffu, ts, cur + 1);
           }
-          const int4 A4 = shfl_int4(ca, u);
-          const int4 B4 = shfl_int4(cb, u);
 #pragma unroll
           for (int kb = 0; kb < 2; ++kb) {
-            // A child (i,kb) in slot 2i+kb ; B child (kb,j) in slot 2kb+j
-            int ta0, ta1, tb0, tb1;
-            const int a0 = blk<kSym>(kb ? A4.y : A4.x, ta0), a1 = blk<kSym>(kb ? A4.w : A4.z, ta1);
-            const int b0 = blk<kSym>(kb ? B4.z : B4.x, tb0), b1 = blk<kSym>(kb ? B4.w : B4.y, tb1);
-            // products of this step: both blocks present and, when screening,
-            // ||A(i,k)||^2 * ||B(k,j)||^2 >= tau^2 (the symbolic pass's test)
-            const int pm = (prod_ok(a0, b0, a) ? 1 : 0) | (prod_ok(a0, b1, a) ? 2 : 0) |
-                           (prod_ok(a1, b0, a) ? 4 : 0) | (prod_ok(a1, b1, a) ? 8 : 0);
-            if (!pm) continue;
-            const int la0 = (pm & 3) ? a0 : -1, la1 = (pm & 12) ? a1 : -1;
-            const int lb0 = (pm & 5) ? b0 : -1, lb1 = (pm & 10) ? b1 : -1;
+            const StepDesc& d = kb ? d1 : d0;
+            const int meta = __shfl_sync(0xffffffffu, d.meta, u);
+            if (!(meta & 15)) continue;
+            const int la0 = __shfl_sync(0xffffffffu, d.a0, u);
+            const int la1 = __shfl_sync(0xffffffffu, d.a1, u);
+            const int lb0 = __shfl_sync(0xffffffffu, d.b0, u);
+            const int lb1 = __shfl_sync(0xffffffffu, d.b1, u);
             mbar_wait(&empty[stage], phase ^ 1);
             if (lane == 0) {
               StageHdr& h = hdr[stage];
@@ -310,24 +337,15 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
               h.b[0] = lb0;
               h.b[1] = lb1;
               h.flags = F_COMPUTE;
-              h.tbits = ta0 | (ta1 << 1) | (tb0 << 2) | (tb1 << 3);
-              h.pmask = pm;
+              h.tbits = meta >> 4;
+              h.pmask = meta & 15;
               const uint32_t bytes = 8192u * ((la0 >= 0) + (la1 >= 0) + (lb0 >= 0) + (lb1 >= 0));
               mbar_arrive_expect_tx(&full[stage], bytes);
               double* dst = data + (size_t)stage * kStageElems;
               if (la0 >= 0) bulk_g2s(dst, poolA + (size_t)la0 * kBlockElems, 8192u, &full[stage]);
-              if (la1 >= 0)
-                bulk_g2s(dst + kBlockElems, poolA + (size_t)la1 * kBlockElems, 8192u, &full[stage]);
-              if (lb0 >= 0) {
-                const double* src = lb0 < a.splitB ? poolB + (size_t)lb0 * kBlockElems
-                                                   : poolB2 + (size_t)(lb0 - a.splitB) * kBlockElems;
-                bulk_g2s(dst + 2 * kBlockElems, src, 8192u, &full[stage]);
-              }
-              if (lb1 >= 0) {
-                const double* src = lb1 < a.splitB ? poolB + (size_t)lb1 * kBlockElems
-                                                   : poolB2 + (size_t)(lb1 - a.splitB) * kBlockElems;
-                bulk_g2s(dst + 3 * kBlockElems, src, 8192u, &full[stage]);
-              }
+              if (la1 >= 0) bulk_g2s(dst + kBlockElems, poolA + (size_t)la1 * kBlockElems, 8192u, &full[stage]);
+              if (lb0 >= 0) bulk_g2s(dst + 2 * kBlockElems, bsrc(lb0), 8192u, &full[stage]);
+              if (lb1 >= 0) bulk_g2s(dst + 3 * kBlockElems, bsrc(lb1), 8192u, &full[stage]);
             }
             __syncwarp();
             if (++stage == kStagesPer) {
@@ -342,101 +360,6 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
       t0 = __shfl_sync(0xffffffffu, tn, 0);
     }
     post(F_DONE, make_int4(-1, -1, -1, -1));
-    } else {
-    // ------------------------------------------------------------ producer
-    const double* poolA = static_cast<const double*>(a.poolA);
-    const double* poolB = static_cast<const double*>(a.poolB);
-    const double* poolB2 = static_cast<const double*>(a.poolB2);
-    for (;;) {
-      int t = 0;
-      if (lane == 0) t = atomicAdd(a.counter, 1);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      if (t >= a.ntiles) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (lane == 0) {
-          hdr[stage].flags = F_DONE;
-          mbar_arrive(&full[stage]);
-        }
-        break;
-      }
-      const int p0 = a.tile_start[t], p1 = a.tile_start[t + 1];
-      const int4 cc = a.childC[t];
-      for (int pb0 = p0; pb0 < p1; pb0 += 32) {
-        const int p = pb0 + lane;
-        int4 ca = make_int4(-1, -1, -1, -1), cb = ca;
-        if (p < p1) {
-          ca = op_children(a.childA, a.pa[p], kTA, kSym);
-          cb = op_children(a.childB, a.pb[p], kTB, kSym);
-        }
-        const int nloc = min(32, p1 - pb0);
-        for (int u = 0; u < nloc; ++u) {
-          const int4 A4 = shfl_int4(ca, u);
-          const int4 B4 = shfl_int4(cb, u);
-#pragma unroll
-          for (int kb = 0; kb < 2; ++kb) {
-            // A child (i,kb) in slot 2i+kb ; B child (kb,j) in slot 2kb+j
-            int ta0, ta1, tb0, tb1;
-            const int a0 = blk<kSym>(kb ? A4.y : A4.x, ta0), a1 = blk<kSym>(kb ? A4.w : A4.z, ta1);
-            const int b0 = blk<kSym>(kb ? B4.z : B4.x, tb0), b1 = blk<kSym>(kb ? B4.w : B4.y, tb1);
-            // products of this step: both blocks present and, when screening,
-            // ||A(i,k)||^2 * ||B(k,j)||^2 >= tau^2 (the symbolic pass's test)
-            const int pm = (prod_ok(a0, b0, a) ? 1 : 0) | (prod_ok(a0, b1, a) ? 2 : 0) |
-                           (prod_ok(a1, b0, a) ? 4 : 0) | (prod_ok(a1, b1, a) ? 8 : 0);
-            if (!pm) continue;
-            const int la0 = (pm & 3) ? a0 : -1, la1 = (pm & 12) ? a1 : -1;
-            const int lb0 = (pm & 5) ? b0 : -1, lb1 = (pm & 10) ? b1 : -1;
-            mbar_wait(&empty[stage], phase ^ 1);
-            if (lane == 0) {
-              StageHdr& h = hdr[stage];
-              h.a[0] = la0;
-              h.a[1] = la1;
-              h.b[0] = lb0;
-              h.b[1] = lb1;
-              h.flags = F_COMPUTE;
-              h.tbits = ta0 | (ta1 << 1) | (tb0 << 2) | (tb1 << 3);
-              h.pmask = pm;
-              const uint32_t bytes = 8192u * ((la0 >= 0) + (la1 >= 0) + (lb0 >= 0) + (lb1 >= 0));
-              mbar_arrive_expect_tx(&full[stage], bytes);
-              double* dst = data + (size_t)stage * kStageElems;
-              if (la0 >= 0) bulk_g2s(dst, poolA + (size_t)la0 * kBlockElems, 8192u, &full[stage]);
-              if (la1 >= 0)
-                bulk_g2s(dst + kBlockElems, poolA + (size_t)la1 * kBlockElems, 8192u, &full[stage]);
-              if (lb0 >= 0) {
-                const double* src = lb0 < a.splitB ? poolB + (size_t)lb0 * kBlockElems
-                                                   : poolB2 + (size_t)(lb0 - a.splitB) * kBlockElems;
-                bulk_g2s(dst + 2 * kBlockElems, src, 8192u, &full[stage]);
-              }
-              if (lb1 >= 0) {
-                const double* src = lb1 < a.splitB ? poolB + (size_t)lb1 * kBlockElems
-                                                   : poolB2 + (size_t)(lb1 - a.splitB) * kBlockElems;
-                bulk_g2s(dst + 3 * kBlockElems, src, 8192u, &full[stage]);
-              }
-            }
-            __syncwarp();
-            if (++stage == kStagesPer) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-        }
-      }
-      mbar_wait(&empty[stage], phase ^ 1);
-      if (lane == 0) {
-        StageHdr& h = hdr[stage];
-        h.c[0] = cc.x;
-        h.c[1] = cc.y;
-        h.c[2] = cc.z;
-        h.c[3] = cc.w;
-        h.flags = F_STORE;
-        mbar_arrive(&full[stage]);
-      }
-      __syncwarp();
-      if (++stage == kStagesPer) {
-        stage = 0;
-        phase ^= 1;
-      }
-    }
-    }
   } else {
     // ------------------------------------------------------------ consumers
     const int q = warp % kConsumerWarps;
@@ -535,39 +458,39 @@ __global__ void k_peak_dfma(double* out, int iters) {
 
 }  // namespace
 
-template <bool G, bool TA, bool TB, bool SYM = false>
+template <bool TA, bool TB, bool SYM = false, bool SCR = false>
 static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
   static bool attr_set = false;
   if (!attr_set) {
-    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<G, TA, TB, SYM>,
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<TA, TB, SYM, SCR>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
     attr_set = true;
   }
-  k_numeric_f64<G, TA, TB, SYM><<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
+  k_numeric_f64<TA, TB, SYM, SCR><<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
 }
 
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a) {
   if (dt != QT_F64) fail(QT_EDTYPE, "launch_numeric is the FP64 kernel");
   QT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), ctx->stream));
   const int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
-  // one tile per grab (dense/banded: finest dynamic balance) or grouped grabs
-  // (sparse patterns: amortise the scheduler and metadata latency)
-  const bool G = a.group > 1;
+  // a.group: one tile per grab (dense/banded: finest dynamic balance) or
+  // grouped grabs (sparse patterns: amortise the scheduler and metadata latency)
   if (a.trans & 4) {  // symmetric square
-    if (G) launch_numeric_t<true, false, false, true>(ctx, a, grid);
-    else launch_numeric_t<false, false, false, true>(ctx, a, grid);
-    QT_LAUNCH_CHECK(ctx);
-    return;
-  }
-  switch ((G ? 4 : 0) | (a.trans & 3)) {
-    case 0: launch_numeric_t<false, false, false>(ctx, a, grid); break;
-    case 1: launch_numeric_t<false, true, false>(ctx, a, grid); break;
-    case 2: launch_numeric_t<false, false, true>(ctx, a, grid); break;
-    case 3: launch_numeric_t<false, true, true>(ctx, a, grid); break;
-    case 4: launch_numeric_t<true, false, false>(ctx, a, grid); break;
-    case 5: launch_numeric_t<true, true, false>(ctx, a, grid); break;
-    case 6: launch_numeric_t<true, false, true>(ctx, a, grid); break;
-    default: launch_numeric_t<true, true, true>(ctx, a, grid); break;
+    launch_numeric_t<false, false, true>(ctx, a, grid);
+  } else if (a.normA) {  // norm-screened product
+    switch (a.trans & 3) {
+      case 0: launch_numeric_t<false, false, false, true>(ctx, a, grid); break;
+      case 1: launch_numeric_t<true, false, false, true>(ctx, a, grid); break;
+      case 2: launch_numeric_t<false, true, false, true>(ctx, a, grid); break;
+      default: launch_numeric_t<true, true, false, true>(ctx, a, grid); break;
+    }
+  } else {
+    switch (a.trans & 3) {
+      case 0: launch_numeric_t<false, false>(ctx, a, grid); break;
+      case 1: launch_numeric_t<true, false>(ctx, a, grid); break;
+      case 2: launch_numeric_t<false, true>(ctx, a, grid); break;
+      default: launch_numeric_t<true, true>(ctx, a, grid); break;
+    }
   }
   QT_LAUNCH_CHECK(ctx);
 }
