@@ -74,14 +74,26 @@ __device__ __forceinline__ int4 ldchild(const int4* __restrict__ tab, int idx, b
 __device__ __forceinline__ int sref(int idx, int diag, int t) {
   return idx < 0 ? -1 : ((idx << 2) | (diag << 1) | t);
 }
-__device__ __forceinline__ int4 op_children(const int4* __restrict__ tab, int ref, bool trans,
-                                            bool sym) {
-  if (!sym) return ldchild(tab, ref, trans);
-  const int idx = ref >> 2, diag = (ref >> 1) & 1, t = ref & 1;
-  const int4 c = tab[idx];
+// op_children split into the table load (row tab[ref >> 2] when symmetric,
+// tab[ref] otherwise) and the transform of the loaded row, so a caller can
+// issue the load early and transform later.
+__device__ __forceinline__ int4 op_xform(int4 c, int ref, bool trans, bool sym) {
+  if (!sym) {
+    if (trans) {
+      const int t = c.y;
+      c.y = c.z;
+      c.z = t;
+    }
+    return c;
+  }
+  const int diag = (ref >> 1) & 1, t = ref & 1;
   if (diag) return make_int4(sref(c.x, 1, 0), sref(c.y, 0, 0), sref(c.y, 0, 1), sref(c.w, 1, 0));
   if (t) return make_int4(sref(c.x, 0, 1), sref(c.z, 0, 1), sref(c.y, 0, 1), sref(c.w, 0, 1));
   return make_int4(sref(c.x, 0, 0), sref(c.y, 0, 0), sref(c.z, 0, 0), sref(c.w, 0, 0));
+}
+__device__ __forceinline__ int4 op_children(const int4* __restrict__ tab, int ref, bool trans,
+                                            bool sym) {
+  return op_xform(tab[sym ? (ref >> 2) : ref], ref, trans, sym);
 }
 
 }  // namespace qt

@@ -6,17 +6,18 @@
 // fig:block-sparse-mmul).  Here the same block products are instead grouped by
 // OUTPUT: a work item ("tile") is a C node at level L-1, i.e. a 2x2 group of
 // 32x32 C blocks, together with its ascending-k task list from the symbolic
-// pass.  Each step of a tile stages A(I0,k), A(I1,k), B(k,J0), B(k,J1) in
-// shared memory with 1-D TMA bulk copies (cp.async.bulk, mbarrier
-// complete_tx); four consumer warps each own one C block and accumulate
-// A(Ii,k)·B(k,Jj) in registers with FP64 tensor-core DMMA
-// (mma.sync.m8n8k4.f64) — every staged block feeds two products.  Each C block
-// is written exactly once, by one warp: no atomics, no batch barriers, and a
-// deterministic summation order (ascending k, reading C-5).
+// pass.  Each step of a tile stages the blocks among A(I0,k), A(I1,k),
+// B(k,J0), B(k,J1) that take part in a product, in shared memory with 1-D TMA
+// bulk copies (cp.async.bulk, mbarrier complete_tx); four consumer warps each
+// own one 16x16 quadrant of all four C blocks and accumulate A(Ii,k)·B(k,Jj)
+// in registers with FP64 tensor-core DMMA (mma.sync.m8n8k4.f64) — a staged
+// block feeds up to two products.  Each C element is written exactly once: no
+// atomics, no batch barriers, and a deterministic summation order (ascending
+// k, reading C-5).
 //
-// CTA = 4 consumer warps + 1 producer warp, persistent (one CTA per SM), tiles
-// handed out by an atomic counter in Morton order (L2 locality), 6-stage
-// smem ring (6 x 32 KiB).
+// CTA = 3 streams x (4 consumer warps + 1 producer warp), persistent (one CTA
+// per SM), tiles handed out by an atomic counter in Morton order (L2
+// locality); each stream stages through its own ring of 8 KiB block slots.
 #include <cuda_runtime.h>
 
 #include "qt_common.cuh"
@@ -26,29 +27,43 @@ namespace qt {
 
 namespace {
 
-// Two independent tile streams per CTA (each: 4 consumer warps + 1 producer
-// warp + its own 3-stage ring), so every SM sub-partition runs two consumer
-// warps: while one is in its tile prologue/epilogue or waits on shared
-// memory, the other keeps the DMMA pipe busy.
-constexpr int kStreams = 2;
-constexpr int kStagesPer = 3;
-constexpr int kStages = kStreams * kStagesPer;
+// Independent tile streams per CTA (each: 4 consumer warps + 1 producer
+// warp), so every SM sub-partition runs several consumer warps: while one is
+// in its tile prologue/epilogue or waits on shared memory, the others keep the
+// DMMA pipe busy.
+//
+// Each stream stages blocks through a ring of kSlotsPer 8 KiB block slots and
+// describes its steps in a ring of kHdrPer step headers.  A step takes only
+// the slots of the blocks it uses (1-4), so sparse steps (ES-like: 2.9 blocks
+// per step on average, random: ~2) keep more steps in flight than fixed
+// 4-block stages would.
+//
+// Streams per CTA and block slots per stream: three streams (three consumer
+// warps per SM sub-partition: one stream's step boundary — header wait,
+// dispatch, tile epilogue — is covered by the other two) with 9 slots each;
+// the symmetric square's consumers (per-block transposes chosen at run time)
+// need more registers than 3 x 5 warps leave, so it runs 2 streams x 13 slots.
+template <bool kSym> struct Cfg {
+  static constexpr int kStreams = kSym ? 2 : 3;
+  static constexpr int kSlotsPer = kSym ? 13 : 9;
+};
+constexpr int kHdrPer = 16;
 constexpr int kConsumerWarps = 4;
-constexpr int kNumThreads = kStreams * (kConsumerWarps + 1) * 32;
+template <bool kSym>
+constexpr int num_threads() { return Cfg<kSym>::kStreams * (kConsumerWarps + 1) * 32; }
 constexpr int kBlockElems = 1024;                // 32 x 32
-constexpr int kStageElems = 4 * kBlockElems;     // A0 A1 B0 B1
-constexpr int kStageBytes = kStageElems * 8;     // 32 KiB (FP64)
+constexpr int kBlockBytes = kBlockElems * 8;     // 8 KiB (FP64)
 
 enum : int { F_COMPUTE = 1, F_STORE = 2, F_DONE = 4 };
 
 struct __align__(16) StageHdr {
-  int a[2];
-  int b[2];
-  int c[4];
+  int a[2];      // slot of A(I0,k), A(I1,k) in the stream's ring (-1: not staged)
+  int b[2];      // slot of B(k,J0), B(k,J1)
+  int c[4];      // F_STORE: C block indices of the tile (slot 2i+j; -1 = none)
   int flags;
-  int tbits;  // symmetric square: bit i = A(i,k) transposed, bit 2+j = B(k,j) transposed
-  int pmask;  // bit 2i+j: warp (i,j) computes A(i,k)*B(k,j) at this step
-  int pad;
+  int tbits;     // symmetric square: bit i = A(i,k) transposed, bit 2+j = B(k,j) transposed
+  int pmask;     // bit 2i+j: product A(i,k)*B(k,j) at this step
+  int slot_end;  // producer bookkeeping: slots allocated up to and including this step
 };
 
 // a block product survives: both present and (screening) norms^2 product >= tau^2
@@ -69,8 +84,12 @@ __device__ __forceinline__ int blk(int ref, int& t) {
   return ref >= 0 ? (ref >> 2) : -1;
 }
 
-constexpr size_t kSmemBytes = (size_t)kStages * kStageBytes + kStages * sizeof(StageHdr) +
-                              2 * kStages * sizeof(uint64_t);
+template <bool kSym>
+constexpr size_t smem_bytes() {
+  return (size_t)Cfg<kSym>::kStreams * Cfg<kSym>::kSlotsPer * kBlockBytes +
+         Cfg<kSym>::kStreams * kHdrPer * sizeof(StageHdr) +
+         2 * Cfg<kSym>::kStreams * kHdrPer * sizeof(uint64_t);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -140,14 +159,12 @@ __device__ __forceinline__ int off_k(int q, int m, int ks, int g, int t4) {
 // loads and DMMAs are issued (a predicated-off DMMA still occupies the pipe).
 // tA/tB: per-block transposes (bit 0: block 0, bit 1: block 1).
 template <int PM>
-__device__ __forceinline__ void warp_step_mma(double (&acc)[4][2][2][2], const double* __restrict__ st,
-                                              int tA, int tB, int qi, int qj, int lane) {
+__device__ __forceinline__ void warp_step_mma(double (&acc)[4][2][2][2], const double* __restrict__ A0,
+                                              const double* __restrict__ A1, const double* __restrict__ B0,
+                                              const double* __restrict__ B1, int tA, int tB, int qi,
+                                              int qj, int lane) {
   constexpr bool ua0 = PM & 3, ua1 = PM & 12, ub0 = PM & 5, ub1 = PM & 10;
   const int g = lane >> 2, t4 = lane & 3;
-  const double* A0 = st;
-  const double* A1 = st + kBlockElems;
-  const double* B0 = st + 2 * kBlockElems;
-  const double* B1 = st + 3 * kBlockElems;
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
     double af[2][2], bf[2][2];
@@ -176,24 +193,25 @@ __device__ __forceinline__ void warp_step_mma(double (&acc)[4][2][2][2], const d
   }
 }
 
-__device__ __forceinline__ void warp_step(double (&acc)[4][2][2][2], const double* __restrict__ st,
-                                          int pm, int tA, int tB, int qi, int qj, int lane) {
+__device__ __forceinline__ void warp_step(double (&acc)[4][2][2][2], const double* A0, const double* A1,
+                                          const double* B0, const double* B1, int pm, int tA, int tB,
+                                          int qi, int qj, int lane) {
   switch (pm) {
-    case 1: warp_step_mma<1>(acc, st, tA, tB, qi, qj, lane); break;
-    case 2: warp_step_mma<2>(acc, st, tA, tB, qi, qj, lane); break;
-    case 3: warp_step_mma<3>(acc, st, tA, tB, qi, qj, lane); break;
-    case 4: warp_step_mma<4>(acc, st, tA, tB, qi, qj, lane); break;
-    case 5: warp_step_mma<5>(acc, st, tA, tB, qi, qj, lane); break;
-    case 6: warp_step_mma<6>(acc, st, tA, tB, qi, qj, lane); break;
-    case 7: warp_step_mma<7>(acc, st, tA, tB, qi, qj, lane); break;
-    case 8: warp_step_mma<8>(acc, st, tA, tB, qi, qj, lane); break;
-    case 9: warp_step_mma<9>(acc, st, tA, tB, qi, qj, lane); break;
-    case 10: warp_step_mma<10>(acc, st, tA, tB, qi, qj, lane); break;
-    case 11: warp_step_mma<11>(acc, st, tA, tB, qi, qj, lane); break;
-    case 12: warp_step_mma<12>(acc, st, tA, tB, qi, qj, lane); break;
-    case 13: warp_step_mma<13>(acc, st, tA, tB, qi, qj, lane); break;
-    case 14: warp_step_mma<14>(acc, st, tA, tB, qi, qj, lane); break;
-    default: warp_step_mma<15>(acc, st, tA, tB, qi, qj, lane); break;
+    case 1: warp_step_mma<1>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 2: warp_step_mma<2>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 3: warp_step_mma<3>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 4: warp_step_mma<4>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 5: warp_step_mma<5>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 6: warp_step_mma<6>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 7: warp_step_mma<7>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 8: warp_step_mma<8>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 9: warp_step_mma<9>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 10: warp_step_mma<10>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 11: warp_step_mma<11>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 12: warp_step_mma<12>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 13: warp_step_mma<13>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 14: warp_step_mma<14>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    default: warp_step_mma<15>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
   }
 }
 
@@ -225,31 +243,30 @@ __device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, const Nu
 }
 
 template <bool kTA, bool kTB, bool kSym, bool kScreen>
-__global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
+__global__ void __launch_bounds__(num_threads<kSym>(), 1) k_numeric_f64(NumericArgs a) {
+  constexpr int kStreams = Cfg<kSym>::kStreams;
+  constexpr int kSlotsPer = Cfg<kSym>::kSlotsPer;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // warps [0, 4*kStreams): consumers, stream = warp / 4 ; then one producer per stream
   const bool producer = warp >= kStreams * kConsumerWarps;
   const int sid = producer ? warp - kStreams * kConsumerWarps : warp / kConsumerWarps;
-  double* data = reinterpret_cast<double*>(smem) + (size_t)sid * kStagesPer * kStageElems;
-  StageHdr* hdr_all = reinterpret_cast<StageHdr*>(smem + (size_t)kStages * kStageBytes);
-  uint64_t* full_all = reinterpret_cast<uint64_t*>(hdr_all + kStages);
-  uint64_t* empty_all = full_all + kStages;
-  StageHdr* hdr = hdr_all + sid * kStagesPer;
-  uint64_t* full = full_all + sid * kStagesPer;
-  uint64_t* empty = empty_all + sid * kStagesPer;
+  double* data = reinterpret_cast<double*>(smem) + (size_t)sid * kSlotsPer * kBlockElems;
+  StageHdr* hdr_all = reinterpret_cast<StageHdr*>(smem + (size_t)kStreams * kSlotsPer * kBlockBytes);
+  uint64_t* full_all = reinterpret_cast<uint64_t*>(hdr_all + kStreams * kHdrPer);
+  uint64_t* empty_all = full_all + kStreams * kHdrPer;
+  StageHdr* hdr = hdr_all + sid * kHdrPer;
+  uint64_t* full = full_all + sid * kHdrPer;
+  uint64_t* empty = empty_all + sid * kHdrPer;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kStreams * kHdrPer; ++s) {
       mbar_init(&full_all[s], 1);
       mbar_init(&empty_all[s], kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-
-  int stage = 0;
-  uint32_t phase = 0;
 
   if (producer) {
     // ------------------------------------------------------------ producer
@@ -264,100 +281,198 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
     const double* poolA = static_cast<const double*>(a.poolA);
     const double* poolB = static_cast<const double*>(a.poolB);
     const double* poolB2 = static_cast<const double*>(a.poolB2);
+    // The metadata of the NEXT batch of 32 tasks (for a new group: the
+    // scheduler atomic, the group's tile starts and C children, then the
+    // tasks' node ids and child tables) is fetched by a small state machine
+    // advanced once per posted step, so its four dependent round trips overlap
+    // the ring waits instead of stalling the ring at every group start.  The
+    // next group is grabbed when <= kGrabAhead tasks of the current one remain
+    // (late enough to keep the dynamic balance of the tail).
+    constexpr int kGrabAhead = 8;
     const int G = a.group;
-    int t0 = 0;
-    if (lane == 0) t0 = atomicAdd(a.counter, G);
-    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    const int ntiles = (int)a.ntiles;
+    // current group: tiles [g_t0, g_t0+g_n), lane l: task start of tile g_t0+l (lane g_n: end), C children
+    int g_n = 0, g_ts = 0, g_pend = 0;
+    int4 g_cc = make_int4(-1, -1, -1, -1);
+    // next batch
+    int n_state = 0, n_tl = 0, n_t0 = 0, n_n = 0, n_ts = 0, n_pb0 = 0, n_pend = 0, n_pa = -1, n_pb = -1;
+    bool n_newgroup = true, n_valid = false;
+    int4 n_cc = make_int4(-1, -1, -1, -1), n_ra = n_cc, n_rb = n_cc;
+    StepDesc n_d0{-1, -1, -1, -1, 0}, n_d1{-1, -1, -1, -1, 0};
+    auto issue_tasks = [&]() {  // node ids of the next batch
+      const int p = n_pb0 + lane;
+      n_pa = p < n_pend ? a.pa[p] : -1;
+      n_pb = p < n_pend ? a.pb[p] : -1;
+    };
+    auto adv = [&]() {
+      switch (n_state) {
+        case 1: {  // scheduler atomic -> group metadata loads
+          n_t0 = __shfl_sync(0xffffffffu, n_tl, 0);
+          if (n_t0 >= ntiles) {
+            n_valid = false;
+            n_state = 5;
+            break;
+          }
+          n_valid = true;
+          n_n = min(G, ntiles - n_t0);
+          n_ts = lane <= n_n ? a.tile_start[n_t0 + lane] : 0;
+          n_cc = lane < n_n ? a.childC[n_t0 + lane] : make_int4(-1, -1, -1, -1);
+          n_state = 2;
+          break;
+        }
+        case 2: {  // group metadata -> first batch's node ids
+          n_pb0 = __shfl_sync(0xffffffffu, n_ts, 0);
+          n_pend = __shfl_sync(0xffffffffu, n_ts, n_n);
+          issue_tasks();
+          n_state = 3;
+          break;
+        }
+        case 3: {  // node ids -> child tables
+          const int4 nil = make_int4(-1, -1, -1, -1);
+          n_ra = n_pa >= 0 ? a.childA[kSym ? (n_pa >> 2) : n_pa] : nil;
+          n_rb = n_pb >= 0 ? a.childB[kSym ? (n_pb >> 2) : n_pb] : nil;
+          n_state = 4;
+          break;
+        }
+        case 4: {  // child tables -> step descriptors
+          if (n_pa >= 0) {
+            const int4 ca = op_xform(n_ra, n_pa, kTA, kSym);
+            const int4 cb = op_xform(n_rb, n_pb, kTB, kSym);
+            n_d0 = make_step<kTA, kTB, kSym, kScreen>(ca, cb, 0, a);
+            n_d1 = make_step<kTA, kTB, kSym, kScreen>(ca, cb, 1, a);
+          } else {
+            n_d0 = StepDesc{-1, -1, -1, -1, 0};
+            n_d1 = n_d0;
+          }
+          n_state = 5;
+          break;
+        }
+        default: break;
+      }
+    };
+    auto grab = [&]() {  // start fetching the next group
+      n_newgroup = true;
+      if (lane == 0) n_tl = atomicAdd(a.counter, G);
+      n_state = 1;
+    };
+    int posted = 0, released = 0;  // steps posted / known released by the consumers
+    int head = 0, freed = 0;       // slots allocated / released (monotonic)
+    int slot_pos = 0;              // head % kSlotsPer
+    int hpos = 0;                  // posted % kHdrPer
+    // wait until a header and n slots are free (consumers release steps in order)
+    auto reserve = [&](int n) {
+      while (posted - released >= kHdrPer || head + n - freed > kSlotsPer) {
+        const int ri = released % kHdrPer;
+        mbar_wait(&empty[ri], (released / kHdrPer) & 1);
+        freed = *reinterpret_cast<volatile int*>(&hdr[ri].slot_end);
+        ++released;
+      }
+    };
     auto post = [&](int flags, int4 cc) {
-      mbar_wait(&empty[stage], phase ^ 1);
+      adv();
+      reserve(0);
       if (lane == 0) {
-        StageHdr& h = hdr[stage];
+        StageHdr& h = hdr[hpos];
         h.c[0] = cc.x;
         h.c[1] = cc.y;
         h.c[2] = cc.z;
         h.c[3] = cc.w;
         h.flags = flags;
-        mbar_arrive(&full[stage]);
+        h.slot_end = head;
+        mbar_arrive(&full[hpos]);
       }
       __syncwarp();
-      if (++stage == kStagesPer) {
-        stage = 0;
-        phase ^= 1;
-      }
+      ++posted;
+      if (++hpos == kHdrPer) hpos = 0;
     };
     auto bsrc = [&](int lb) {
       return lb < a.splitB ? poolB + (size_t)lb * kBlockElems
                            : poolB2 + (size_t)(lb - a.splitB) * kBlockElems;
     };
-    while (t0 < a.ntiles) {
-      const int t1 = min(t0 + G, (int)a.ntiles);
-      // next group: prefetched now when groups are large (sparse patterns), taken
-      // at the end otherwise (a reserved-but-idle tile would lengthen the tail)
-      int tn = 0;
-      if (G > 1 && lane == 0) tn = atomicAdd(a.counter, G);
-      // lane l holds tile t0+l's task start and C children; lane (t1-t0) the end
-      int ts = 0;
-      int4 cc = make_int4(-1, -1, -1, -1);
-      if (lane <= t1 - t0) ts = a.tile_start[t0 + lane];
-      if (lane < t1 - t0) cc = a.childC[t0 + lane];
-      const int p_begin = __shfl_sync(0xffffffffu, ts, 0);
-      const int p_end = __shfl_sync(0xffffffffu, ts, t1 - t0);
-      int cur = 0;  // tile index within the group
-      int boundary = __shfl_sync(0xffffffffu, ts, 1);
-      for (int pb0 = p_begin; pb0 < p_end; pb0 += 32) {
-        const int p = pb0 + lane;
-        StepDesc d0{-1, -1, -1, -1, 0}, d1{-1, -1, -1, -1, 0};
-        if (p < p_end) {
-          const int4 ca = op_children(a.childA, a.pa[p], kTA, kSym);
-          const int4 cb = op_children(a.childB, a.pb[p], kTB, kSym);
-          d0 = make_step<kTA, kTB, kSym, kScreen>(ca, cb, 0, a);
-          d1 = make_step<kTA, kTB, kSym, kScreen>(ca, cb, 1, a);
+    grab();
+    while (n_state < 5) adv();
+    int cur = 0, boundary = 0;
+    while (n_valid) {
+      // promote the prefetched batch
+      if (n_newgroup) {
+        g_n = n_n;
+        g_ts = n_ts;
+        g_cc = n_cc;
+        g_pend = n_pend;
+        cur = 0;
+        boundary = __shfl_sync(0xffffffffu, g_ts, 1);
+      }
+      const int c_pb0 = n_pb0;
+      const StepDesc c_d0 = n_d0, c_d1 = n_d1;
+      const int c_nloc = max(0, min(32, g_pend - c_pb0));
+      const bool last = c_pb0 + 32 >= g_pend;
+      n_state = 0;
+      if (!last) {  // next batch of the same group
+        n_newgroup = false;
+        n_pb0 = c_pb0 + 32;
+        n_pend = g_pend;
+        issue_tasks();
+        n_state = 3;
+      } else if (g_pend - c_pb0 <= kGrabAhead) {
+        grab();
+      }
+      for (int u = 0; u < c_nloc; ++u) {
+        if (last && n_state == 0 && g_pend - (c_pb0 + u) <= kGrabAhead) grab();
+        while (c_pb0 + u >= boundary) {  // tile `cur` is complete
+          post(F_STORE, shfl_int4(g_cc, cur));
+          ++cur;
+          boundary = __shfl_sync(0xffffffffu, g_ts, cur + 1);
         }
-        const int nloc = min(32, p_end - pb0);
-        for (int u = 0; u < nloc; ++u) {
-          while (pb0 + u >= boundary) {  // tile `cur` is complete
-            post(F_STORE, shfl_int4(cc, cur));
-            ++cur;
-            boundary = __shfl_sync(0xffffffffu, ts, cur + 1);
-          }
 #pragma unroll
-          for (int kb = 0; kb < 2; ++kb) {
-            const StepDesc& d = kb ? d1 : d0;
-            const int meta = __shfl_sync(0xffffffffu, d.meta, u);
-            if (!(meta & 15)) continue;
-            const int la0 = __shfl_sync(0xffffffffu, d.a0, u);
-            const int la1 = __shfl_sync(0xffffffffu, d.a1, u);
-            const int lb0 = __shfl_sync(0xffffffffu, d.b0, u);
-            const int lb1 = __shfl_sync(0xffffffffu, d.b1, u);
-            mbar_wait(&empty[stage], phase ^ 1);
-            if (lane == 0) {
-              StageHdr& h = hdr[stage];
-              h.a[0] = la0;
-              h.a[1] = la1;
-              h.b[0] = lb0;
-              h.b[1] = lb1;
-              h.flags = F_COMPUTE;
-              h.tbits = meta >> 4;
-              h.pmask = meta & 15;
-              const uint32_t bytes = 8192u * ((la0 >= 0) + (la1 >= 0) + (lb0 >= 0) + (lb1 >= 0));
-              mbar_arrive_expect_tx(&full[stage], bytes);
-              double* dst = data + (size_t)stage * kStageElems;
-              if (la0 >= 0) bulk_g2s(dst, poolA + (size_t)la0 * kBlockElems, 8192u, &full[stage]);
-              if (la1 >= 0) bulk_g2s(dst + kBlockElems, poolA + (size_t)la1 * kBlockElems, 8192u, &full[stage]);
-              if (lb0 >= 0) bulk_g2s(dst + 2 * kBlockElems, bsrc(lb0), 8192u, &full[stage]);
-              if (lb1 >= 0) bulk_g2s(dst + 3 * kBlockElems, bsrc(lb1), 8192u, &full[stage]);
-            }
-            __syncwarp();
-            if (++stage == kStagesPer) {
-              stage = 0;
-              phase ^= 1;
-            }
+        for (int kb = 0; kb < 2; ++kb) {
+          const StepDesc& d = kb ? c_d1 : c_d0;
+          const int meta = __shfl_sync(0xffffffffu, d.meta, u);
+          if (!(meta & 15)) continue;
+          const int la0 = __shfl_sync(0xffffffffu, d.a0, u);
+          const int la1 = __shfl_sync(0xffffffffu, d.a1, u);
+          const int lb0 = __shfl_sync(0xffffffffu, d.b0, u);
+          const int lb1 = __shfl_sync(0xffffffffu, d.b1, u);
+          adv();
+          const int n = (la0 >= 0) + (la1 >= 0) + (lb0 >= 0) + (lb1 >= 0);
+          reserve(n);
+          if (lane == 0) {
+            StageHdr& h = hdr[hpos];
+            int sp = slot_pos;
+            auto take = [&](int blkidx) {
+              if (blkidx < 0) return -1;
+              const int sl = sp;
+              sp = sp + 1 == kSlotsPer ? 0 : sp + 1;
+              return sl;
+            };
+            const int s0 = take(la0), s1 = take(la1), s2 = take(lb0), s3 = take(lb1);
+            h.a[0] = s0;
+            h.a[1] = s1;
+            h.b[0] = s2;
+            h.b[1] = s3;
+            h.flags = F_COMPUTE;
+            h.tbits = meta >> 4;
+            h.pmask = meta & 15;
+            h.slot_end = head + n;
+            uint64_t* fb = &full[hpos];
+            mbar_arrive_expect_tx(fb, (uint32_t)kBlockBytes * n);
+            if (s0 >= 0) bulk_g2s(data + s0 * kBlockElems, poolA + (size_t)la0 * kBlockElems, kBlockBytes, fb);
+            if (s1 >= 0) bulk_g2s(data + s1 * kBlockElems, poolA + (size_t)la1 * kBlockElems, kBlockBytes, fb);
+            if (s2 >= 0) bulk_g2s(data + s2 * kBlockElems, bsrc(lb0), kBlockBytes, fb);
+            if (s3 >= 0) bulk_g2s(data + s3 * kBlockElems, bsrc(lb1), kBlockBytes, fb);
           }
+          __syncwarp();
+          head += n;
+          slot_pos += n;
+          if (slot_pos >= kSlotsPer) slot_pos -= kSlotsPer;
+          ++posted;
+          if (++hpos == kHdrPer) hpos = 0;
         }
       }
-      for (; cur < t1 - t0; ++cur) post(F_STORE, shfl_int4(cc, cur));
-      if (G == 1 && lane == 0) tn = atomicAdd(a.counter, G);
-      t0 = __shfl_sync(0xffffffffu, tn, 0);
+      if (last) {
+        for (; cur < g_n; ++cur) post(F_STORE, shfl_int4(g_cc, cur));
+        if (n_state == 0) grab();
+      }
+      while (n_state < 5) adv();
     }
     post(F_DONE, make_int4(-1, -1, -1, -1));
   } else {
@@ -373,9 +488,11 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
 #pragma unroll
         for (int n = 0; n < 2; ++n) acc[p][m][n][0] = acc[p][m][n][1] = 0.0;
     const int g = lane >> 2, t4 = lane & 3;
+    int hi = 0;
+    uint32_t phase = 0;
     for (;;) {
-      mbar_wait(&full[stage], phase);
-      const StageHdr& h = hdr[stage];
+      mbar_wait(&full[hi], phase);
+      const StageHdr& h = hdr[hi];
       const int flags = h.flags;
       if (flags & F_DONE) break;
       if (flags & F_STORE) {
@@ -383,7 +500,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
 #pragma unroll
         for (int p = 0; p < 4; ++p) cb[p] = h.c[p];
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (lane == 0) mbar_arrive(&empty[hi]);
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
           if (cb[p] >= 0) {
@@ -403,8 +520,11 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
             for (int n = 0; n < 2; ++n) acc[p][m][n][0] = acc[p][m][n][1] = 0.0;
         }
       } else {
-        const double* st = data + (size_t)stage * kStageElems;
         const int pm = h.pmask;
+        const double* A0 = data + h.a[0] * kBlockElems;
+        const double* A1 = data + h.a[1] * kBlockElems;
+        const double* B0 = data + h.b[0] * kBlockElems;
+        const double* B1 = data + h.b[1] * kBlockElems;
         int tA, tB;
         if (kSym) {
           tA = h.tbits & 3;
@@ -413,12 +533,12 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
           tA = kTA ? 3 : 0;
           tB = kTB ? 3 : 0;
         }
-        warp_step(acc, st, pm, tA, tB, qi, qj, lane);
+        warp_step(acc, A0, A1, B0, B1, pm, tA, tB, qi, qj, lane);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (lane == 0) mbar_arrive(&empty[hi]);
       }
-      if (++stage == kStagesPer) {
-        stage = 0;
+      if (++hi == kHdrPer) {
+        hi = 0;
         phase ^= 1;
       }
     }
@@ -463,10 +583,10 @@ static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
   static bool attr_set = false;
   if (!attr_set) {
     QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<TA, TB, SYM, SCR>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<SYM>()));
     attr_set = true;
   }
-  k_numeric_f64<TA, TB, SYM, SCR><<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
+  k_numeric_f64<TA, TB, SYM, SCR><<<grid, num_threads<SYM>(), smem_bytes<SYM>(), ctx->stream>>>(a);
 }
 
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a) {
