@@ -211,11 +211,13 @@ struct NumericArgs {
   int* counter;              // tile scheduler counter (zeroed before launch)
   int group = 1;             // tiles per scheduler grab (1..31)
   int trans = 0;             // bit 0: A transposed, bit 1: B transposed, bit 2: symmetric square
+  const void* poolT = nullptr;    // symmetric square: transposed copy of poolA (= poolB)
   const double* normA = nullptr;  // block squared norms (screening) or null
   const double* normB = nullptr;
   double tau2 = 0.0;
 };
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a);
+void launch_transpose_blocks(qt_ctx ctx, const void* in, void* out, int64_t nb);
 
 // FP32 (tcgen05 kind::tf32, 3xTF32): tiles are C nodes at level L-2 (4x4 blocks)
 struct NumericArgs32 {

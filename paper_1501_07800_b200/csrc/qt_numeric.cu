@@ -38,19 +38,15 @@ namespace {
 // per step on average, random: ~2) keep more steps in flight than fixed
 // 4-block stages would.
 //
-// Streams per CTA and block slots per stream: three streams (three consumer
-// warps per SM sub-partition: one stream's step boundary — header wait,
-// dispatch, tile epilogue — is covered by the other two) with 9 slots each;
-// the symmetric square's consumers (per-block transposes chosen at run time)
-// need more registers than 3 x 5 warps leave, so it runs 2 streams x 13 slots.
-template <bool kSym> struct Cfg {
-  static constexpr int kStreams = kSym ? 2 : 3;
-  static constexpr int kSlotsPer = kSym ? 13 : 9;
-};
+// Three streams (three consumer warps per SM sub-partition: one stream's step
+// boundary — header wait, dispatch, tile epilogue — is covered by the other
+// two) with 9 slots each: 216 KiB of the 227 KiB of shared memory.  The
+// consumers need <= 128 registers for 15 warps to fit one SM.
+constexpr int kStreams = 3;
+constexpr int kSlotsPer = 9;
 constexpr int kHdrPer = 16;
 constexpr int kConsumerWarps = 4;
-template <bool kSym>
-constexpr int num_threads() { return Cfg<kSym>::kStreams * (kConsumerWarps + 1) * 32; }
+constexpr int kNumThreads = kStreams * (kConsumerWarps + 1) * 32;
 constexpr int kBlockElems = 1024;                // 32 x 32
 constexpr int kBlockBytes = kBlockElems * 8;     // 8 KiB (FP64)
 
@@ -61,7 +57,7 @@ struct __align__(16) StageHdr {
   int b[2];      // slot of B(k,J0), B(k,J1)
   int c[4];      // F_STORE: C block indices of the tile (slot 2i+j; -1 = none)
   int flags;
-  int tbits;     // symmetric square: bit i = A(i,k) transposed, bit 2+j = B(k,j) transposed
+  int pad0;
   int pmask;     // bit 2i+j: product A(i,k)*B(k,j) at this step
   int slot_end;  // producer bookkeeping: slots allocated up to and including this step
 };
@@ -84,12 +80,9 @@ __device__ __forceinline__ int blk(int ref, int& t) {
   return ref >= 0 ? (ref >> 2) : -1;
 }
 
-template <bool kSym>
-constexpr size_t smem_bytes() {
-  return (size_t)Cfg<kSym>::kStreams * Cfg<kSym>::kSlotsPer * kBlockBytes +
-         Cfg<kSym>::kStreams * kHdrPer * sizeof(StageHdr) +
-         2 * Cfg<kSym>::kStreams * kHdrPer * sizeof(uint64_t);
-}
+constexpr size_t kSmemBytes = (size_t)kStreams * kSlotsPer * kBlockBytes +
+                              kStreams * kHdrPer * sizeof(StageHdr) +
+                              2 * kStreams * kHdrPer * sizeof(uint64_t);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -243,9 +236,7 @@ __device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, const Nu
 }
 
 template <bool kTA, bool kTB, bool kSym, bool kScreen>
-__global__ void __launch_bounds__(num_threads<kSym>(), 1) k_numeric_f64(NumericArgs a) {
-  constexpr int kStreams = Cfg<kSym>::kStreams;
-  constexpr int kSlotsPer = Cfg<kSym>::kSlotsPer;
+__global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // warps [0, 4*kStreams): consumers, stream = warp / 4 ; then one producer per stream
@@ -385,6 +376,10 @@ __global__ void __launch_bounds__(num_threads<kSym>(), 1) k_numeric_f64(NumericA
       ++posted;
       if (++hpos == kHdrPer) hpos = 0;
     };
+    const double* poolT = static_cast<const double*>(a.poolT);
+    auto asrc = [&](int la, int t) {
+      return (kSym && t ? poolT : poolA) + (size_t)la * kBlockElems;
+    };
     auto bsrc = [&](int lb) {
       return lb < a.splitB ? poolB + (size_t)lb * kBlockElems
                            : poolB2 + (size_t)(lb - a.splitB) * kBlockElems;
@@ -450,15 +445,18 @@ __global__ void __launch_bounds__(num_threads<kSym>(), 1) k_numeric_f64(NumericA
             h.b[0] = s2;
             h.b[1] = s3;
             h.flags = F_COMPUTE;
-            h.tbits = meta >> 4;
             h.pmask = meta & 15;
             h.slot_end = head + n;
             uint64_t* fb = &full[hpos];
             mbar_arrive_expect_tx(fb, (uint32_t)kBlockBytes * n);
-            if (s0 >= 0) bulk_g2s(data + s0 * kBlockElems, poolA + (size_t)la0 * kBlockElems, kBlockBytes, fb);
-            if (s1 >= 0) bulk_g2s(data + s1 * kBlockElems, poolA + (size_t)la1 * kBlockElems, kBlockBytes, fb);
-            if (s2 >= 0) bulk_g2s(data + s2 * kBlockElems, bsrc(lb0), kBlockBytes, fb);
-            if (s3 >= 0) bulk_g2s(data + s3 * kBlockElems, bsrc(lb1), kBlockBytes, fb);
+            // symmetric square: a block of U read transposed comes from the
+            // transposed copy of the pool (meta bits 4..7), so the consumers
+            // always read blocks as stored
+            const int tb = meta >> 4;
+            if (s0 >= 0) bulk_g2s(data + s0 * kBlockElems, asrc(la0, tb & 1), kBlockBytes, fb);
+            if (s1 >= 0) bulk_g2s(data + s1 * kBlockElems, asrc(la1, tb & 2), kBlockBytes, fb);
+            if (s2 >= 0) bulk_g2s(data + s2 * kBlockElems, kSym ? asrc(lb0, tb & 4) : bsrc(lb0), kBlockBytes, fb);
+            if (s3 >= 0) bulk_g2s(data + s3 * kBlockElems, kSym ? asrc(lb1, tb & 8) : bsrc(lb1), kBlockBytes, fb);
           }
           __syncwarp();
           head += n;
@@ -525,14 +523,7 @@ __global__ void __launch_bounds__(num_threads<kSym>(), 1) k_numeric_f64(NumericA
         const double* A1 = data + h.a[1] * kBlockElems;
         const double* B0 = data + h.b[0] * kBlockElems;
         const double* B1 = data + h.b[1] * kBlockElems;
-        int tA, tB;
-        if (kSym) {
-          tA = h.tbits & 3;
-          tB = (h.tbits >> 2) & 3;
-        } else {
-          tA = kTA ? 3 : 0;
-          tB = kTB ? 3 : 0;
-        }
+        const int tA = kTA ? 3 : 0, tB = kTB ? 3 : 0;
         warp_step(acc, A0, A1, B0, B1, pm, tA, tB, qi, qj, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[hi]);
@@ -542,6 +533,30 @@ __global__ void __launch_bounds__(num_threads<kSym>(), 1) k_numeric_f64(NumericA
         phase ^= 1;
       }
     }
+  }
+}
+
+// Transposed copy of a pool of FP64 blocks (symmetric square: U(i,j)^T is
+// read wherever the full matrix has its (j,i) block): out(r,c) = in(c,r), both
+// in the internal swizzled layout.  One 32x32 block per 256-thread CTA
+// iteration, staged through a padded shared tile.
+__global__ void k_transpose_blocks(const double* __restrict__ in, double* __restrict__ out, int64_t nb) {
+  __shared__ double tile[32][33];
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const double* src = in + b * kBlockElems;
+    double* dst = out + b * kBlockElems;
+#pragma unroll
+    for (int i = threadIdx.x; i < kBlockElems; i += blockDim.x) {
+      const int r = i >> 5, c = (i & 31) ^ ((r & 3) << 2);  // i = swz64(r, c)
+      tile[r][c] = src[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int o = threadIdx.x; o < kBlockElems; o += blockDim.x) {
+      const int r = o >> 5, c = (o & 31) ^ ((r & 3) << 2);  // o = swz64(r, c)
+      dst[o] = tile[c][r];
+    }
+    __syncthreads();
   }
 }
 
@@ -583,10 +598,10 @@ static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
   static bool attr_set = false;
   if (!attr_set) {
     QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<TA, TB, SYM, SCR>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<SYM>()));
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
     attr_set = true;
   }
-  k_numeric_f64<TA, TB, SYM, SCR><<<grid, num_threads<SYM>(), smem_bytes<SYM>(), ctx->stream>>>(a);
+  k_numeric_f64<TA, TB, SYM, SCR><<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
 }
 
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a) {
@@ -612,6 +627,14 @@ void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a) {
       default: launch_numeric_t<true, true>(ctx, a, grid); break;
     }
   }
+  QT_LAUNCH_CHECK(ctx);
+}
+
+void launch_transpose_blocks(qt_ctx ctx, const void* in, void* out, int64_t nb) {
+  if (nb <= 0) return;
+  const int grid = (int)std::min<int64_t>(nb, 8ll * ctx->num_sms);
+  k_transpose_blocks<<<grid, 256, 0, ctx->stream>>>(static_cast<const double*>(in),
+                                                     static_cast<double*>(out), nb);
   QT_LAUNCH_CHECK(ctx);
 }
 

@@ -613,6 +613,12 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
           tr.mark(b);
         }
       }
+      DevBuf poolT;  // symmetric square: blocks of U read transposed come from U^T's copy
+      if (C->nb > 0 && !f32 && sym) {
+        poolT.alloc((size_t)A->nb * 1024 * 8, st);
+        launch_transpose_blocks(ctx, A->pool_ptr(), poolT.p, A->nb);
+        na.poolT = poolT.p;
+      }
       if (C->nb > 0 && !f32) launch_numeric(ctx, C->dtype, na);
       if (C->nb > 0 && f32 && sym) fail(QT_EDTYPE, "the symmetric square is FP64-only in this build");
       if (C->nb > 0 && f32) {
