@@ -135,6 +135,7 @@ struct qt_mat_s {
   std::vector<qt::DevBuf> child; // child[l] : int32 [cnt[l]][4], l = 0..L-1 (-1 = NIL)
   bool levels_built = true;     // false for a fresh product: built on first use
   qt::DevBuf hist;     // int32 per-level node counts per row / per column (see build_levels)
+  std::vector<int32_t> hist_host;  // host copy of hist (per-level task counts without a sync)
   std::vector<qt::DevBuf> norm2;  // squared Frobenius norms per node, levels 0..L (screening; lazy)
   // B_ext of a multi-rank multiply: pool1 overrides pool.p (a borrowed view of
   // the local pool); block ids >= split live in pool2 (the received blocks).

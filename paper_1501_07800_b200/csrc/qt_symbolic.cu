@@ -25,8 +25,9 @@
 // occupancy histograms kept with each matrix — so all frontier buffers are
 // sized exactly and the BFS runs without host round trips.  The top levels
 // (frontiers up to 8K tasks) run in ONE single-CTA kernel with block-wide
-// scans; the large levels use grid-wide kernels + device scans.  One host sync
-// remains, before the numeric kernel (to size C's block pool).
+// scans; the large levels in ONE persistent cooperative kernel whose phases
+// are separated by grid-wide barriers.  One host sync remains, before the
+// numeric kernel (to size C's block pool).
 #include <chrono>
 #include <cstdlib>
 #include <cub/cub.cuh>
@@ -42,26 +43,7 @@ constexpr int kThreads = 256;
 constexpr int kSmallThreads = 1024;
 constexpr int64_t kSmallMaxF = 1 << 13;
 
-inline unsigned grid_for(int64_t n) {
-  int64_t g = (n + kThreads - 1) / kThreads;
-  return (unsigned)(g < 1 ? 1 : g);
-}
 
-// C_l for every level: one CTA per level
-__global__ void k_level_tasks(const int32_t* __restrict__ histA, const int32_t* __restrict__ histB,
-                              int64_t H, int trans, int64_t* __restrict__ out) {
-  using BR = cub::BlockReduce<long long, kThreads>;
-  __shared__ typename BR::TempStorage tmp;
-  const int l = blockIdx.x;
-  const int64_t base = (1ll << l) - 1, m = 1ll << l;
-  long long s = 0;
-  for (int64_t K = threadIdx.x; K < m; K += blockDim.x)
-    // cols(op(A)_l) . rows(op(B)_l); a transposed operand swaps its row/column histograms
-    s += (long long)histA[((trans & 1) ? 0 : H) + base + K] *
-         (long long)histB[((trans & 2) ? H : 0) + base + K];
-  s = BR(tmp).Sum(s);
-  if (threadIdx.x == 0) out[l] = s;
-}
 
 // C node on the block diagonal: in the symmetric square only its upper
 // children exist (the (1,0) child is the transpose of (0,1), not computed)
@@ -249,122 +231,321 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
   }
 }
 
-// ------------------------------------------------------------ large levels (grid-wide)
+// ------------------------------------------------------------ large levels (one persistent kernel)
+//
+// All transitions l -> l+1 for l in [l_begin, L) run in ONE cooperative launch
+// (one 1024-thread CTA per SM, all resident), three phases per level separated
+// by grid-wide barriers.  Work is split by groups (C nodes of level l): CTA b
+// owns the groups whose first task lies in its 1/G share of the level's tasks,
+// a warp walks one group's tasks at a time.
+//   A count  per group and C child q: the number of child tasks T[4s+q]
+//            (warp reduction over the group's tasks); CTA sums of T and of
+//            the non-empty slots
+//   B groups exclusive scans over the 4·ns slots (CTA prefix from the CTA
+//            sums + block scans): new group index, its first task, its key;
+//            the task and group counts of level l+1
+//   C emit   the child tasks, slot by slot in (parent task, k) order (warp
+//            scans place them), written at their group's start
+// So the scans run over the 4·ns group slots, not the 4·F task slots, and a
+// level costs three barriers.  The launch replaces ~8 kernel launches + 2
+// device scans per level (the large levels were host-launch bound).
+constexpr int kLargeThreads = 1024;
+constexpr int kLargeWarps = kLargeThreads / 32;
 
-// Launch sizes come from host-side bounds (exact for regular products); the
-// actual task count of the level is read from f_dev.  Threads of "virtual"
-// tasks p in [F, Fb) zero the count positions [4p, 4p+4), so the scan over
-// 4*Fb positions is exact.
-__global__ void k_count(int32_t Fb, const int32_t* __restrict__ f_dev, const int32_t* __restrict__ pa,
-                        const int32_t* __restrict__ pb, const int32_t* __restrict__ pc,
-                        const int32_t* __restrict__ cstart, const uint64_t* __restrict__ ckey,
-                        const int4* __restrict__ childA, const int4* __restrict__ childB, int mode,
-                        Screen sc, int32_t* __restrict__ cnt) {
-  const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= Fb) return;
-  if (p >= *f_dev) {
-    *reinterpret_cast<int4*>(cnt + 4ll * p) = make_int4(0, 0, 0, 0);
-    return;
+struct LargeBfsArgs {
+  int l_begin, L;
+  int trans;  // bits 0-2: mode (A^T, B^T, symmetric); trans >> 8: symmetric prune levels
+  double tau2;
+  const int4* childA[QT_MAX_LEVELS];
+  const int4* childB[QT_MAX_LEVELS];
+  const double* normA[QT_MAX_LEVELS];  // squared node norms per level (screening), or null
+  const double* normB[QT_MAX_LEVELS];
+  int32_t* pa[QT_MAX_LEVELS];  // tasks of level l
+  int32_t* pb[QT_MAX_LEVELS];
+  int32_t* pc[QT_MAX_LEVELS];
+  int32_t* cstart[QT_MAX_LEVELS];  // groups (C nodes) of level l: task starts (+ end)
+  uint64_t* ckey[QT_MAX_LEVELS];
+  int32_t* gidx[QT_MAX_LEVELS];  // transition l: (s,q) -> group of level l+1, or -1
+  int32_t* slot_cnt;             // 4 * max ns: child tasks per (s,q)
+  int32_t* slot_off;             // 4 * max ns: first child task of (s,q)
+  int32_t* part;                 // 2 * gridDim
+  int32_t* ns_out;               // groups per level
+  int32_t* f_out;                // tasks per level
+  unsigned* bar;                 // grid barrier: arrival count (self-resetting), generation
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Sense-reversing grid barrier (all CTAs are co-resident: cooperative launch).
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = gen;
+    unsigned prev;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(bar) : "memory");
+    if (prev == gridDim.x - 1) {
+      bar[0] = 0;
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(g + 1) : "memory");
+    } else {
+      while (ld_acquire(bar + 1) == g) {
+      }
+    }
+    gen = g + 1;
   }
-  const bool sym = mode & 4;
-  const int32_t s = pc[p], c0 = cstart[s], m = cstart[s + 1] - c0;
-  int c[4];
-  child_counts(op_children(childA, pa[p], mode & 1, sym), op_children(childB, pb[p], mode & 2, sym), c,
-               sc, sym);
-  if ((mode & 8) && on_diagonal(ckey[s])) c[2] = 0;
-  const int64_t base = 4ll * c0 + (p - c0);
+  __syncthreads();
+}
+
+// CTA-wide lower bound: the first index in [0, n] with v[i] >= x (v ascending),
+// by rounds of 1024 parallel samples (__syncthreads_count) instead of a
+// serial binary search — two rounds of loads for up to 1M groups.
+__device__ __forceinline__ int32_t cta_lower_bound(const int32_t* v, int32_t n, int64_t x) {
+  int32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int32_t span = hi - lo;
+    const int32_t step = (span + kLargeThreads - 1) / kLargeThreads;
+    const int32_t k = (span + step - 1) / step;  // samples lo, lo+step, ... < hi
+    const int32_t pos = lo + (int32_t)threadIdx.x * step;
+    const bool below = (int32_t)threadIdx.x < k && v[pos] < x;
+    const int32_t c = __syncthreads_count(below);
+    const int32_t nlo = c == 0 ? lo : lo + (c - 1) * step + 1;
+    const int32_t nhi = c == k ? hi : lo + c * step;
+    lo = nlo;
+    hi = nhi;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) {
+  using BS = cub::BlockScan<int, kLargeThreads>;
+  using BR = cub::BlockReduce<int, kLargeThreads>;
+  __shared__ union {
+    typename BS::TempStorage scan;
+    typename BR::TempStorage red;
+  } tmp;
+  __shared__ int s_val[4];
+  __shared__ int s_wsum[kLargeWarps][2];
+  unsigned gen = 0;
+  if (threadIdx.x == 0) gen = ld_acquire(&a.bar[1]);
+  const bool sym = a.trans & 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  for (int l = a.l_begin; l < a.L; ++l) {
+    const bool last = l == a.L - 1;
+    const int mode = (a.trans & 7) | ((sym && l < (a.trans >> 8)) ? 8 : 0);
+    const Screen sc{a.normA[l + 1], a.normB[l + 1], a.tau2};
+    const int32_t F = a.f_out[l], ns = a.ns_out[l];
+    const int32_t* pa = a.pa[l];
+    const int32_t* pb = a.pb[l];
+    const int32_t* cs = a.cstart[l];
+    const uint64_t* ck = a.ckey[l];
+    const int4* cA = a.childA[l];
+    const int4* cB = a.childB[l];
+    // this CTA's groups: first task in [b F / G, (b+1) F / G)
+    const int32_t g_lo = cta_lower_bound(cs, ns, (int64_t)F * blockIdx.x / gridDim.x);
+    const int32_t g_hi = cta_lower_bound(cs, ns, (int64_t)F * (blockIdx.x + 1) / gridDim.x);
+    // child counts of task p per C child q (0 for the pruned lower child of a diagonal node)
+    auto counts = [&](int32_t p, int32_t sgrp, int (&c)[4]) {
+      child_counts(op_children(cA, pa[p], mode & 1, sym), op_children(cB, pb[p], mode & 2, sym), c, sc,
+                   sym);
+      if ((mode & 8) && on_diagonal(ck[sgrp])) c[2] = 0;
+    };
+    // A. child tasks per (s,q).  A group is walked by W lanes (a power of two
+    // near half the level's mean group size): random patterns have ~1-task
+    // groups at the lower levels, banded ones ~17.
+    int W = 1;
+    {
+      const int32_t half_mean = (F / max(ns, 1) + 1) / 2;
+      while (W < 32 && W < half_mean) W <<= 1;
+    }
+    const int gpw = 32 / W;                 // groups per warp pass
+    const int sub = lane / W, li = lane % W;
+    {
+      int vsum = 0, vflag = 0;  // this lane's sums over the groups it leads
+      for (int32_t sg0 = g_lo + warp * gpw; sg0 < g_hi; sg0 += kLargeWarps * gpw) {
+        const int32_t sg = sg0 + sub;
+        int t[4] = {0, 0, 0, 0};
+        if (sg < g_hi) {
+          const int32_t c0 = cs[sg], c1 = cs[sg + 1];
+          for (int32_t p = c0 + li; p < c1; p += W) {
+            int c[4];
+            counts(p, sg, c);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) cnt[base + (int64_t)q * m] = c[q];
-}
-
-// per (s,q) slot: start of the new group and non-empty flag (0 beyond the real ns)
-__global__ void k_segs(int32_t nsb, const int32_t* __restrict__ ns_dev, int64_t n4,
-                       const int32_t* __restrict__ cstart, const int32_t* __restrict__ off,
-                       const int32_t* __restrict__ cnt, int32_t* __restrict__ flag,
-                       int32_t* __restrict__ gstart) {
-  const int32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= 4 * nsb) return;
-  const int32_t ns = *ns_dev;
-  int32_t f = 0, st = 0;
-  if (x < 4 * ns) {
-    const int32_t s = x >> 2, q = x & 3, c0 = cstart[s], m = cstart[s + 1] - c0;
-    const int64_t lo = 4ll * c0 + (int64_t)q * m, hi = lo + m;
-    st = off[lo];
-    const int32_t en = hi < n4 ? off[hi] : off[n4 - 1] + cnt[n4 - 1];
-    f = en > st;
+            for (int q = 0; q < 4; ++q) t[q] += c[q];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          for (int d = W >> 1; d > 0; d >>= 1) t[q] += __shfl_xor_sync(FULL, t[q], d);
+        }
+        if (sg < g_hi && li == 0) {
+          *reinterpret_cast<int4*>(a.slot_cnt + 4ll * sg) = make_int4(t[0], t[1], t[2], t[3]);
+          vsum += t[0] + t[1] + t[2] + t[3];
+          vflag += (t[0] > 0) + (t[1] > 0) + (t[2] > 0) + (t[3] > 0);
+        }
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        vsum += __shfl_xor_sync(FULL, vsum, d);
+        vflag += __shfl_xor_sync(FULL, vflag, d);
+      }
+      if (lane == 0) {
+        s_wsum[warp][0] = vsum;
+        s_wsum[warp][1] = vflag;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int x0 = 0, x1 = 0;
+        for (int w = 0; w < kLargeWarps; ++w) {
+          x0 += s_wsum[w][0];
+          x1 += s_wsum[w][1];
+        }
+        a.part[blockIdx.x] = x0;
+        a.part[gridDim.x + blockIdx.x] = x1;
+      }
+    }
+    grid_sync(a.bar, gen);
+    // B. new groups: starts, keys, (s,q) -> group map
+    int tpre, Fn, gpre, nsn;
+    {
+      int v[4] = {0, 0, 0, 0};
+      for (int i = threadIdx.x; i < (int)gridDim.x; i += kLargeThreads) {
+        const int x = a.part[i], y = a.part[gridDim.x + i];
+        v[1] += x;
+        v[3] += y;
+        if (i < (int)blockIdx.x) {
+          v[0] += x;
+          v[2] += y;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = BR(tmp.red).Sum(v[k]);
+        if (threadIdx.x == 0) s_val[k] = r;
+        __syncthreads();
+      }
+      tpre = s_val[0];
+      Fn = s_val[1];
+      gpre = s_val[2];
+      nsn = s_val[3];
+      __syncthreads();
+    }
+    int32_t* csn = a.cstart[l + 1];
+    uint64_t* ckn = a.ckey[l + 1];
+    int32_t* gx = a.gidx[l];
+    for (int64_t b0 = 4ll * g_lo; b0 < 4ll * g_hi; b0 += kLargeThreads) {
+      const int64_t x = b0 + threadIdx.x;
+      const bool in = x < 4ll * g_hi;
+      const int c = in ? a.slot_cnt[x] : 0;
+      const int f = c > 0;
+      int ex_t, agg_t, ex_f, agg_f;
+      BS(tmp.scan).ExclusiveSum(c, ex_t, agg_t);
+      __syncthreads();
+      BS(tmp.scan).ExclusiveSum(f, ex_f, agg_f);
+      if (in) {
+        const int32_t start = tpre + ex_t;
+        a.slot_off[x] = start;
+        const int t = f ? gpre + ex_f : -1;
+        gx[x] = t;
+        if (f) {
+          csn[t] = start;
+          ckn[t] = (ck[x >> 2] << 2) | (uint64_t)(x & 3);
+        }
+      }
+      tpre += agg_t;
+      gpre += agg_f;
+      __syncthreads();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      csn[nsn] = Fn;
+      a.ns_out[l + 1] = nsn;
+      a.f_out[l + 1] = Fn;
+    }
+    if (last) break;
+    grid_sync(a.bar, gen);
+    // C. emit the child tasks of level l+1: slot (s,q) lists, for every parent
+    // task in order, k = 0 then k = 1 (ascending global k inside the group)
+    {
+      int32_t* pa2 = a.pa[l + 1];
+      int32_t* pb2 = a.pb[l + 1];
+      int32_t* pc2 = a.pc[l + 1];
+      for (int32_t sg0 = g_lo + warp * gpw; sg0 < g_hi; sg0 += kLargeWarps * gpw) {
+        const int32_t sg = sg0 + sub;
+        const bool live = sg < g_hi;
+        int32_t c0 = 0, c1 = 0;
+        bool skip_lower = false;
+        int pos[4] = {0, 0, 0, 0}, gq[4] = {-1, -1, -1, -1};
+        if (live) {
+          c0 = cs[sg];
+          c1 = cs[sg + 1];
+          skip_lower = (mode & 8) && on_diagonal(ck[sg]);
+          const int4 o4 = *reinterpret_cast<const int4*>(a.slot_off + 4ll * sg);
+          const int4 g4 = *reinterpret_cast<const int4*>(gx + 4ll * sg);
+          pos[0] = o4.x; pos[1] = o4.y; pos[2] = o4.z; pos[3] = o4.w;
+          gq[0] = g4.x; gq[1] = g4.y; gq[2] = g4.z; gq[3] = g4.w;
+        }
+        // uniform trip count across the warp (the scans below shuffle)
+        int iters = (c1 - c0 + W - 1) / W;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) iters = max(iters, __shfl_xor_sync(FULL, iters, d));
+        for (int it = 0; it < iters; ++it) {
+          const int32_t p = c0 + it * W + li;
+          int4 A4 = make_int4(-1, -1, -1, -1), B4 = A4;
+          if (p < c1) {
+            A4 = op_children(cA, pa[p], mode & 1, sym);
+            B4 = op_children(cB, pb[p], mode & 2, sym);
+          }
+          const int av[4] = {A4.x, A4.y, A4.z, A4.w};
+          const int bv[4] = {B4.x, B4.y, B4.z, B4.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = q >> 1, j = q & 1;
+            const bool on = !(q == 2 && skip_lower);
+            const bool k0 = on && pair_ok(av[2 * i], bv[j], sc, sym);
+            const bool k1 = on && pair_ok(av[2 * i + 1], bv[2 + j], sc, sym);
+            const int n = (int)k0 + (int)k1;
+            int ex = n;
+            for (int d = 1; d < W; d <<= 1) {
+              const int y = __shfl_up_sync(FULL, ex, d, W);
+              if (li >= d) ex += y;
+            }
+            const int tot = __shfl_sync(FULL, ex, W - 1, W);
+            ex -= n;
+            int w = pos[q] + ex;
+            if (k0) {
+              pa2[w] = av[2 * i];
+              pb2[w] = bv[j];
+              pc2[w] = gq[q];
+              ++w;
+            }
+            if (k1) {
+              pa2[w] = av[2 * i + 1];
+              pb2[w] = bv[2 + j];
+              pc2[w] = gq[q];
+            }
+            pos[q] += tot;
+          }
+        }
+      }
+    }
+    grid_sync(a.bar, gen);
   }
-  flag[x] = f;
-  gstart[x] = st;
 }
 
-__global__ void k_newc(int32_t nsb, const int32_t* __restrict__ ns_dev, int64_t n4,
-                       const int32_t* __restrict__ off, const int32_t* __restrict__ cnt,
-                       const int32_t* __restrict__ flag, const int32_t* __restrict__ nex,
-                       const int32_t* __restrict__ gstart, const uint64_t* __restrict__ ckey,
-                       int32_t* __restrict__ cstart_next, uint64_t* __restrict__ ckey_next,
-                       int32_t* __restrict__ gidx, int32_t* __restrict__ ns_next,
-                       int32_t* __restrict__ f_next) {
-  const int32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int32_t ns = *ns_dev;
-  if (x >= 4 * ns) return;
-  if (x == 4 * ns - 1) {
-    const int32_t nsn = nex[x] + flag[x];
-    const int32_t Fn = off[n4 - 1] + cnt[n4 - 1];
-    cstart_next[nsn] = Fn;
-    *ns_next = nsn;
-    *f_next = Fn;
+// CTAs of the cooperative BFS launch: every CTA resident (occupancy x SMs)
+int large_bfs_grid(qt_ctx ctx) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    int n = 0;
+    QT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_bfs_large, kLargeThreads, 0));
+    if (n < 1) fail(QT_ECUDA, "k_bfs_large cannot be resident");
+    per_sm = 1;
   }
-  if (flag[x]) {
-    const int32_t t = nex[x];
-    cstart_next[t] = gstart[x];
-    ckey_next[t] = (ckey[x >> 2] << 2) | (uint64_t)(x & 3);
-    gidx[x] = t;
-  } else {
-    gidx[x] = -1;
-  }
+  return per_sm * ctx->num_sms;
 }
 
-__global__ void k_emit(int32_t Fb, const int32_t* __restrict__ f_dev, const int32_t* __restrict__ pa,
-                       const int32_t* __restrict__ pb, const int32_t* __restrict__ pc,
-                       const int32_t* __restrict__ cstart, const uint64_t* __restrict__ ckey,
-                       const int4* __restrict__ childA, const int4* __restrict__ childB, int mode,
-                       Screen sc, const int32_t* __restrict__ off, const int32_t* __restrict__ gidx,
-                       int32_t* __restrict__ pa2, int32_t* __restrict__ pb2,
-                       int32_t* __restrict__ pc2) {
-  const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= Fb || p >= *f_dev) return;
-  const bool sym = mode & 4;
-  const int32_t s = pc[p], c0 = cstart[s], m = cstart[s + 1] - c0;
-  emit_task(op_children(childA, pa[p], mode & 1, sym), op_children(childB, pb[p], mode & 2, sym),
-            4ll * c0 + (p - c0), m, s, (mode & 8) && on_diagonal(ckey[s]), sc, sym, off, gidx, pa2, pb2,
-            pc2);
-}
-
-// Upper bound of the symmetric square's tasks per level: with the full
-// matrix's column and row counts both bounded by rows(U) + cols(U).
-__global__ void k_level_tasks_sym(const int32_t* __restrict__ hist, int64_t H,
-                                  int64_t* __restrict__ out) {
-  using BR = cub::BlockReduce<long long, kThreads>;
-  __shared__ typename BR::TempStorage tmp;
-  const int l = blockIdx.x;
-  const int64_t base = (1ll << l) - 1, m = 1ll << l;
-  long long s = 0;
-  for (int64_t K = threadIdx.x; K < m; K += blockDim.x) {
-    const long long c = (long long)hist[base + K] + hist[H + base + K];
-    s += c * c;
-  }
-  s = BR(tmp).Sum(s);
-  if (threadIdx.x == 0) out[l] = s;
-}
-
-template <class T>
-void excl_sum(qt_ctx ctx, const T* in, T* out, int64_t n) {
-  size_t tb = 0;
-  QT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, ctx->stream));
-  void* tmp = scratch(ctx, tb);
-  QT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, (int)n, ctx->stream));
-  ctx->launches += 2;
-}
 
 }  // namespace
 
@@ -394,10 +575,6 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
     ensure_norms(A);
     ensure_norms(B);
   }
-  auto screen_at = [&](int level) {
-    return Screen{screen ? A->norm2[level].as<double>() : nullptr,
-                  screen ? B->norm2[level].as<double>() : nullptr, tau2};
-  };
   // trans: bit 0 A^T, bit 1 B^T, bit 2 symmetric square (A = B = U, C upper)
   const bool sym = trans & 4;
   Trace tr;
@@ -429,18 +606,26 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
     QT_CUDA(cudaEventRecord(ctx->ev[2], st));
     std::vector<int64_t> F(L + 1, 0);
     if (A->nb > 0 && B->nb > 0) {
-      // task counts per level (one sync): exact for regular products, an upper
-      // bound for the symmetric square (its actual counts come from the BFS)
+      // task counts per level from the host copies of the occupancy
+      // histograms (no device work, no sync): exact for regular products, an
+      // upper bound for the symmetric square (its actual counts come from the BFS)
       const int64_t H = 2ll << L;
-      DevBuf dF(8 * (L + 1), st);
-      if (sym)
-        k_level_tasks_sym<<<L + 1, kThreads, 0, st>>>(A->hist.as<int32_t>(), H, dF.as<int64_t>());
-      else
-        k_level_tasks<<<L + 1, kThreads, 0, st>>>(A->hist.as<int32_t>(), B->hist.as<int32_t>(), H,
-                                                 trans & 3, dF.as<int64_t>());
-      QT_LAUNCH_CHECK(ctx);
-      QT_CUDA(cudaMemcpyAsync(F.data(), dF.p, 8 * (L + 1), cudaMemcpyDeviceToHost, st));
-      QT_CUDA(cudaStreamSynchronize(st));
+      const int32_t* hA = A->hist_host.data();
+      const int32_t* hB = B->hist_host.data();
+      for (int l = 0; l <= L; ++l) {
+        const int64_t base = (1ll << l) - 1, m = 1ll << l;
+        int64_t f = 0;
+        for (int64_t K = 0; K < m; ++K) {
+          if (sym) {
+            const int64_t c = (int64_t)hA[base + K] + hA[H + base + K];
+            f += c * c;
+          } else {
+            // cols(op(A)_l) . rows(op(B)_l); a transposed operand swaps its row/column histograms
+            f += (int64_t)hA[((trans & 1) ? 0 : H) + base + K] * (int64_t)hB[((trans & 2) ? H : 0) + base + K];
+          }
+        }
+        F[l] = f;
+      }
       tr.mark("counts");
       for (int l = 0; l <= L; ++l)
         if (F[l] >= (1ll << 31) / 4) fail(QT_EINVAL, "level %d has %lld tasks (> 2^29)", l, (long long)F[l]);
@@ -506,63 +691,96 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       const int cb = l_end & 1;
       DevBuf pa = std::move(sp[cb]), pb = std::move(sb[cb]), pc = std::move(sc[cb]);
       DevBuf cstart = std::move(scs[cb]), ckey = std::move(sck[cb]);
-      // --- large levels, grid-wide, no host sync
+      // --- large levels: one persistent cooperative kernel, no host sync
       DevBuf cchild, t2_pa, t2_pb, t2_cstart, cchild2;
       tr.mark("small_launch");
-      for (int l = l_end; l < L; ++l) {
-        const bool last = (l == L - 1);
-        const int32_t Fb = (int32_t)F[l];  // launch bound (exact unless symmetric)
-        // per-level mode: transposes, symmetric, bit 3 = prune C below the diagonal here
-        const int mode_l = (trans & 7) | ((sym && l < (trans >> 8)) ? 8 : 0);
-        const int64_t n4 = 4ll * Fb, s4 = 4ll * nsb[l];
-        DevBuf cnt(4 * n4, st), off(4 * n4, st);
-        k_count<<<grid_for(Fb), kThreads, 0, st>>>(Fb, fd + l, pa.as<int32_t>(), pb.as<int32_t>(),
-                                                   pc.as<int32_t>(), cstart.as<int32_t>(),
-                                                   ckey.as<uint64_t>(), A->child[l].as<int4>(),
-                                                   B->child[l].as<int4>(), mode_l, screen_at(l + 1),
-                                                   cnt.as<int32_t>());
-        QT_LAUNCH_CHECK(ctx);
-        excl_sum(ctx, cnt.as<int32_t>(), off.as<int32_t>(), n4);
-        DevBuf flag(4 * s4, st), gstart(4 * s4, st), nex(4 * s4, st), gidx(4 * s4, st);
-        k_segs<<<grid_for(s4), kThreads, 0, st>>>((int32_t)nsb[l], nsd + l, n4, cstart.as<int32_t>(),
-                                                  off.as<int32_t>(), cnt.as<int32_t>(),
-                                                  flag.as<int32_t>(), gstart.as<int32_t>());
-        QT_LAUNCH_CHECK(ctx);
-        excl_sum(ctx, flag.as<int32_t>(), nex.as<int32_t>(), s4);
-        DevBuf cstart2(4 * (nsb[l + 1] + 1), st), ckey2(8 * std::max<int64_t>(nsb[l + 1], 1), st);
-        k_newc<<<grid_for(s4), kThreads, 0, st>>>((int32_t)nsb[l], nsd + l, n4, off.as<int32_t>(),
-                                                  cnt.as<int32_t>(), flag.as<int32_t>(),
-                                                  nex.as<int32_t>(), gstart.as<int32_t>(),
-                                                  ckey.as<uint64_t>(), cstart2.as<int32_t>(),
-                                                  ckey2.as<uint64_t>(), gidx.as<int32_t>(), nsd + l + 1,
-                                                  fd + l + 1);
-        QT_LAUNCH_CHECK(ctx);
-        if (last) {
-          C->key = std::move(ckey2);
-          cchild = std::move(gidx);
-          break;
+      {
+        // level l_end lives in the small kernel's buffers; levels l_end+1..L
+        // alternate between two buffer sets (level L: groups only)
+        int64_t mF = 1, mNS = 1, mNSg = 1;
+        for (int l = l_end + 1; l < L; ++l) mF = std::max(mF, F[l]);
+        for (int l = l_end + 1; l < L; ++l) mNS = std::max(mNS, nsb[l]);
+        for (int l = l_end; l < L; ++l) mNSg = std::max(mNSg, 4 * nsb[l]);
+        DevBuf qa[2], qb[2], qc[2], qcs[2], qck[2], qgx[2];
+        for (int b = 0; b < 2; ++b) {
+          if (l_end + 1 < L) {
+            qa[b].alloc(4 * mF, st);
+            qb[b].alloc(4 * mF, st);
+            qc[b].alloc(4 * mF, st);
+          }
+          qcs[b].alloc(4 * (mNS + 1), st);
+          qck[b].alloc(8 * mNS, st);
+          qgx[b].alloc(4 * mNSg, st);
         }
-        const int64_t Fnb = F[l + 1];
-        DevBuf pa2(4 * Fnb, st), pb2(4 * Fnb, st), pc2(4 * Fnb, st);
-        k_emit<<<grid_for(Fb), kThreads, 0, st>>>(Fb, fd + l, pa.as<int32_t>(), pb.as<int32_t>(),
-                                                  pc.as<int32_t>(), cstart.as<int32_t>(),
-                                                  ckey.as<uint64_t>(), A->child[l].as<int4>(),
-                                                  B->child[l].as<int4>(), mode_l, screen_at(l + 1),
-                                                  off.as<int32_t>(),
-                                                  gidx.as<int32_t>(), pa2.as<int32_t>(),
-                                                  pb2.as<int32_t>(), pc2.as<int32_t>());
-        QT_LAUNCH_CHECK(ctx);
-        if (f32 && l == L - 2) {  // keep the level L-2 queue: the FP32 work items
-          t2_pa = std::move(pa);
-          t2_pb = std::move(pb);
-          t2_cstart = std::move(cstart);
-          cchild2 = std::move(gidx);
+        // level L (C's blocks): its own buffers — the ping-pong set of level L
+        // is level L-2's, whose queue the FP32 kernel still needs
+        DevBuf ckeyL(8 * std::max<int64_t>(nsb[L], 1), st), csL(4 * (nsb[L] + 1), st);
+        DevBuf slot_cnt(4 * mNSg, st), slot_off(4 * mNSg, st);
+        const int G = large_bfs_grid(ctx);
+        DevBuf part(4 * 2 * G, st);
+        LargeBfsArgs la;
+        la.l_begin = l_end;
+        la.L = L;
+        la.trans = trans;
+        la.tau2 = tau2;
+        for (int l = 0; l < L && l < QT_MAX_LEVELS; ++l) {
+          la.childA[l] = A->child[l].as<int4>();
+          la.childB[l] = B->child[l].as<int4>();
         }
-        pa = std::move(pa2);
-        pb = std::move(pb2);
-        pc = std::move(pc2);
-        cstart = std::move(cstart2);
-        ckey = std::move(ckey2);
+        for (int l = 0; l <= L && l < QT_MAX_LEVELS; ++l) {
+          la.normA[l] = screen ? A->norm2[l].as<double>() : nullptr;
+          la.normB[l] = screen ? B->norm2[l].as<double>() : nullptr;
+        }
+        auto set = [&](int l) { return (l - l_end) & 1; };
+        for (int l = l_end; l <= L; ++l) {
+          if (l == l_end) {
+            la.pa[l] = pa.as<int32_t>();
+            la.pb[l] = pb.as<int32_t>();
+            la.pc[l] = pc.as<int32_t>();
+            la.cstart[l] = cstart.as<int32_t>();
+            la.ckey[l] = ckey.as<uint64_t>();
+          } else {
+            if (l < L) {
+              la.pa[l] = qa[set(l)].as<int32_t>();
+              la.pb[l] = qb[set(l)].as<int32_t>();
+              la.pc[l] = qc[set(l)].as<int32_t>();
+            }
+            la.cstart[l] = l == L ? csL.as<int32_t>() : qcs[set(l)].as<int32_t>();
+            la.ckey[l] = l == L ? ckeyL.as<uint64_t>() : qck[set(l)].as<uint64_t>();
+          }
+          if (l < L) la.gidx[l] = qgx[set(l)].as<int32_t>();
+        }
+        la.slot_cnt = slot_cnt.as<int32_t>();
+        la.slot_off = slot_off.as<int32_t>();
+        la.part = part.as<int32_t>();
+        la.ns_out = nsd;
+        la.f_out = fd;
+        la.bar = reinterpret_cast<unsigned*>(ctx->counters.as<int>() + 40);
+        void* kargs[] = {&la};
+        QT_CUDA(cudaLaunchCooperativeKernel((const void*)k_bfs_large, dim3(G), dim3(kLargeThreads), kargs, 0,
+                                            st));
+        ctx->launches += 1;
+        QT_LAUNCH_CHECK(ctx);
+        // hand the queues the numeric kernels consume over
+        C->key = std::move(ckeyL);
+        cchild = std::move(qgx[set(L - 1)]);
+        if (f32) {  // the level L-2 queue: the FP32 work items (l_end <= L-2)
+          cchild2 = std::move(qgx[set(L - 2)]);
+          if (L - 2 > l_end) {
+            t2_pa = std::move(qa[set(L - 2)]);
+            t2_pb = std::move(qb[set(L - 2)]);
+            t2_cstart = std::move(qcs[set(L - 2)]);
+          } else {  // level l_end: the small kernel's buffers
+            t2_pa = std::move(pa);
+            t2_pb = std::move(pb);
+            t2_cstart = std::move(cstart);
+          }
+        }
+        if (L - 1 > l_end) {
+          pa = std::move(qa[set(L - 1)]);
+          pb = std::move(qb[set(L - 1)]);
+          cstart = std::move(qcs[set(L - 1)]);
+        }
       }
       // --- group counts of every level (the one remaining sync): C's block count
       tr.mark("levels_launched");

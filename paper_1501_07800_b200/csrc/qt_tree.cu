@@ -224,6 +224,7 @@ void build_levels(qt_mat M, const int32_t* leaf_ids) {
   const int64_t H = 2ll << M->L;
   M->hist.alloc(8 * H, st);
   QT_CUDA(cudaMemsetAsync(M->hist.p, 0, 8 * H, st));
+  M->hist_host.assign(2 * H, 0);
   if (M->nb == 0) return;
   DevBuf cur_keys(M->nb * 8, st);
   QT_CUDA(cudaMemcpyAsync(cur_keys.p, M->key.p, M->nb * 8, cudaMemcpyDeviceToDevice, st));
@@ -250,6 +251,9 @@ void build_levels(qt_mat M, const int32_t* leaf_ids) {
                                                     M->hist.as<int32_t>());
     QT_LAUNCH_CHECK(ctx);
   }
+  // host copy: qt_multiply derives its per-level task counts from it
+  QT_CUDA(cudaMemcpyAsync(M->hist_host.data(), M->hist.p, 8 * H, cudaMemcpyDeviceToHost, st));
+  QT_CUDA(cudaStreamSynchronize(st));
 }
 
 void build_from_blocks(qt_mat M, int64_t nb, const int32_t* d_brow, const int32_t* d_bcol,
