@@ -9,18 +9,28 @@
 // x_lo = x - x_hi (error ~2^-21 per term, FP32 accumulation in TMEM).
 //
 // Work item ("tile") = one C node at level L-2: 4x4 C blocks = a 128x128 FP32
-// accumulator in TMEM (128 lanes x 128 columns; two tiles double-buffered = 256
-// columns).  A step of the tile is one inner block index k: the A column
-// A(I0..I3, k) (a 128x32 K-major operand) and the B row B(k, J0..J3) (a 32x128
-// MN-major operand) — absent blocks are copied from a zero block — staged by
-// eight 4 KiB cp.async.bulk copies into a 1024-byte-aligned stage.  Because
-// the pool stores every FP32 block in the canonical 128-byte swizzle
-// (qt_common.cuh swz32), the same bytes are a valid SW128 descriptor target
-// for both operands.  Per step: 4 K-slices x 3 MMAs (M=128, N=128, K=8).
+// accumulator in TMEM (128 lanes x 128 columns).  A step of the tile is one
+// inner block index k: the A column A(I0..I3, k) (128x32) and the B row
+// B(k, J0..J3) (32x128) — absent blocks are copied from a zero block — staged
+// by eight 4 KiB cp.async.bulk copies into a stage.  The pool stores every
+// FP32 block in the canonical 128-byte swizzle (qt_common.cuh swz32).  Per
+// step: 4 K-slices x 3 MMAs (M=128, N=128, K=8).
+//
+// Data path (measured with tools/tc_rate and tools/tc_ts_probe): the tensor
+// core's shared-memory operand reads and LDS share the SM's 128 B/clk
+// shared-memory read bandwidth, tensor core first — back-to-back M=128 N=128
+// tf32 MMAs with both operands in shared memory read exactly 128 B/clk and
+// leave an LDS stream 6 B/clk, so an in-SM hi/lo split that reads the landed
+// stage starves.  Here the A operand lives in TENSOR MEMORY ("TS" MMAs): the
+// split warps of A read the landed A column once (LDS), split each row into
+// hi/lo in registers and write them to TMEM with tcgen05.st (lane = row, one
+// 32-bit column per K element); the MMAs then read only B from shared memory
+// (64 B/clk), which leaves room for the split warps' LDS.
 //
 // Warp roles (448 threads, one CTA per SM, persistent over tiles):
 //   warps 0-3  epilogue  TMEM -> registers (tcgen05.ld 32x32b) -> C pool
-//   warps 4-11 split     fp32 -> (tf32 hi in place, lo copy) per stage
+//   warps 4-7  split A   block q: rows -> (hi, lo) -> tcgen05.st into TMEM
+//   warps 8-11 split B   block q: fp32 -> (tf32 hi in place, lo copy) in smem
 //   warp 12    producer  task metadata + TMA bulk copies
 //   warp 13    MMA       one elected lane issues tcgen05.mma / commit
 // Each C block is written once by one thread row-set: no atomics; summation
@@ -35,29 +45,32 @@ namespace qt {
 
 namespace {
 
-// smem: a 4-deep ring of landing stages (A_hi[4] | B_hi[4], 32 KiB) for the
-// TMA lookahead, and a 2-deep ring of lo buffers (A_lo[4] | B_lo[4]) that the
-// split warps fill just before the MMA warp consumes them: 6 x 32 KiB.
+// smem: a 4-deep ring of stages, each A raw[4] (16 KiB, read once by the A
+// split warps) | B[4] (landed, then hi in place) | B lo[4] = 48 KiB.
 constexpr int kStages = 4;
-constexpr int kLoSlots = 2;
 constexpr int kBlkBytes = 4096;                 // 32x32 fp32
-constexpr int kHiBytes = 8 * kBlkBytes;         // A_hi[4] | B_hi[4]
-constexpr int kStageBytes = kHiBytes;           // landing stage (hi in place)
-constexpr int kLoBase = kStages * kStageBytes;   // lo ring after the landing ring
+constexpr int kLandBytes = 8 * kBlkBytes;       // A[4] | B[4] as landed
+constexpr int kBloOff = kLandBytes;             // B lo after the landing area
+constexpr int kStageBytes = kLandBytes + 4 * kBlkBytes;
 constexpr int kSplitWarps = 8;
 constexpr int kProducerWarp = 4 + kSplitWarps;
 constexpr int kMmaWarp = kProducerWarp + 1;
 constexpr int kThreads = (kMmaWarp + 1) * 32;
-// TMEM: two tile buffers (double-buffered epilogue) x two accumulators x 128
-// columns = 512 columns.  The hi*hi products go to one accumulator, the two
-// cross terms (2^-11 smaller) to the other; the epilogue adds them with a
-// round-to-nearest FADD.  The tensor core's own accumulation into D is not
-// round-to-nearest, so its error grows with the number of MMAs that add into
-// one large accumulator: measured on config 5 (65 k-steps), one accumulator
-// for all 12 MMAs per step gave 1.02e-5 relative Frobenius error, even/odd
-// k-step accumulators 5.1e-6; the hi*hi / cross split leaves 4 MMAs per step
-// on the large accumulator.
+// TMEM (512 columns): two hi*hi accumulators (double-buffered tiles, columns
+// 0 and 128), one cross-term accumulator (256), and two A slots of 64 columns
+// (hi 32 + lo 32, K along columns) at 384 and 448.  The hi*hi products go to
+// one accumulator, the two cross terms (2^-11 smaller) to the other; the
+// epilogue adds them with a round-to-nearest FADD.  The tensor core's own
+// accumulation into D is not round-to-nearest, so its error grows with the
+// number of MMAs that add into one large accumulator: measured on config 5
+// (65 k-steps), one accumulator for all 12 MMAs per step gave 1.02e-5
+// relative Frobenius error, even/odd k-step accumulators 5.1e-6; the hi*hi /
+// cross split leaves 4 MMAs per step on the large accumulator.  The cross
+// accumulator is single-buffered: a tile's first MMAs wait until the
+// epilogue has drained the previous tile.
 constexpr int kTmemCols = 512;
+constexpr uint32_t kColCross = 256;
+constexpr uint32_t kColA = 384;
 
 enum : int { F_FIRST = 1, F_END = 2, F_DONE = 4 };
 
@@ -73,14 +86,14 @@ struct Smem {
   uint32_t tmem_base;
   uint32_t pad;
   uint64_t full[kStages];   // TMA landed (1 arrival + tx)
-  uint64_t conv[kStages];   // hi/lo split done (one arrival per split warp)
+  uint64_t conv[kStages];   // A in TMEM and B hi/lo in smem (one arrival per split warp)
   uint64_t empty[kStages];  // MMAs that read the stage done (tcgen05.commit)
-  uint64_t lo_empty[kLoSlots];  // MMAs that read the lo slot done (tcgen05.commit)
+  uint64_t afree[2];        // MMAs that read the A slot done (tcgen05.commit)
   uint64_t tfull[2];        // accumulator ready (commit + MMA-lane arrive)
-  uint64_t tempty[2];       // epilogue drained the accumulator (4 warp arrivals)
+  uint64_t tempty[2];       // epilogue drained the hi*hi accumulator (4 warp arrivals)
+  uint64_t cfree;           // epilogue drained the cross accumulator (4 warp arrivals)
 };
-constexpr size_t kSmemBytes =
-    1024 /*align slack*/ + (size_t)kStages * kStageBytes + (size_t)kLoSlots * kHiBytes + sizeof(Smem);
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + sizeof(Smem);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -128,16 +141,27 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
-// D[tmem] (+)= A[smem] * B[smem], kind::tf32
-__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                       uint32_t idesc, uint32_t accumulate) {
+// D[tmem] (+)= A[tmem] * B[smem], kind::tf32 (A: lane = row, column = K element)
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 consecutive 32-bit TMEM columns of this warp's 32 lanes
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+      "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
@@ -175,9 +199,11 @@ constexpr uint64_t kSW128_32B = 1;     // MN-major B (32-bit types): 32-byte chu
 // (10-12 = 2), A major (15: 0 = K), B major (16: 1 = MN), N>>3 at 17, M>>4 at 24.
 // A stored row-major block is K-major as an A operand and MN-major as a B
 // operand; a transposed operand (C = A^T B, A B^T) flips that.
-template <bool kTA, bool kTB>
-__host__ __device__ constexpr uint32_t idesc_tf32() {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((kTA ? 1u : 0u) << 15) | ((kTB ? 0u : 1u) << 16) |
+
+// TS form: A comes from TMEM in the M-lanes x K-columns layout (K-major)
+template <bool kTB>
+__host__ __device__ constexpr uint32_t idesc_tf32_ts() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | ((kTB ? 0u : 1u) << 16) |
          ((128u >> 3) << 17) | ((128u >> 4) << 24);
 }
 
@@ -187,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
   // 1024-byte aligned start (kept as an offset from the shared array so the
   // compiler still emits shared-space LDS/STS for the split warps)
   uint8_t* data = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  Smem& S = *reinterpret_cast<Smem*>(data + (size_t)kLoBase + (size_t)kLoSlots * kHiBytes);
+  Smem& S = *reinterpret_cast<Smem*>(data + (size_t)kStages * kStageBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -196,11 +222,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
       mbar_init(&S.conv[s], kSplitWarps);
       mbar_init(&S.empty[s], 1);
     }
-    for (int b = 0; b < kLoSlots; ++b) mbar_init(&S.lo_empty[b], 1);
     for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.afree[b], 1);
       mbar_init(&S.tfull[b], 2);
       mbar_init(&S.tempty[b], 4);
     }
+    mbar_init(&S.cfree, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -323,31 +350,85 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
         phase ^= 1;
       }
     }
-  } else if (warp >= 4 && warp < 4 + kSplitWarps) {
-    // ------------------------------------------------------------ hi/lo split
-    // Each warp owns whole 1 KiB swizzle atoms (8 rows x 128 B = 64 float4),
-    // two float4 per lane.  A atoms keep their layout (K-major SW128: hi in
-    // place, lo at the same offset of the lo area).  B atoms are re-laid out
-    // for the MN-major operand, which for 32-bit types is the 128-byte swizzle
-    // with 32-byte atoms (layout type SWIZZLE_128B_BASE32B): 16-byte chunk c of
-    // row r moves from c ^ (r&7) to ((c>>1 ^ (r&3))<<1 | (c&1)) — in place,
-    // after all lanes of the warp have read the atom.
-    const int cw = warp - 4;
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------ split A -> TMEM
+    // Warp 4+q owns A block q = rows 32q..32q+31 of the 128-row A column,
+    // i.e. exactly its own TMEM lane quarter; lane r holds row r.  The row's
+    // 32 fp32 (K) are read once from the landed stage, split into hi (TF32
+    // truncation) and lo (exact remainder) and written to the A slot's hi and
+    // lo columns.  A transposed A (C = A^T B) is read by columns instead.
+    const int q = warp - 4;
     int stage = 0;
     uint32_t phase = 0;
-    int lo_slot = 0;
-    uint32_t lo_phase = 0;
+    int as = 0;
+    uint32_t aph = 0;
     for (;;) {
       mbar_wait(&S.full[stage], phase);
       const int flags = S.hdr[stage].flags;
       if (!(flags & (F_END | F_DONE))) {
-        mbar_wait(&S.lo_empty[lo_slot], lo_phase ^ 1);
-        float4* hi = reinterpret_cast<float4*>(data + (size_t)stage * kStageBytes);
-        float4* lo = reinterpret_cast<float4*>(data + kLoBase + (size_t)lo_slot * kHiBytes);
+        mbar_wait(&S.afree[as], aph ^ 1);
+        const float* blk = reinterpret_cast<const float*>(data + (size_t)stage * kStageBytes + q * kBlkBytes);
+        uint32_t hv[32], lv[32];
+        const int r = lane;
+        if (!kTA) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {  // 16-byte chunk c of row r (SW128: chunk c ^ (r & 7))
+            const float4 x = *reinterpret_cast<const float4*>(blk + r * 32 + ((c ^ (r & 7)) << 2));
+            const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float h = tf32_trunc(xs[e]);
+              hv[4 * c + e] = __float_as_uint(h);
+              lv[4 * c + e] = __float_as_uint(xs[e] - h);  // exact: at most 13 significant bits
+            }
+          }
+        } else {
+          // op(A)(r, k) = stored(k, r): column r of the stored block
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float x = blk[k * 32 + ((((r >> 2) ^ (k & 7)) << 2) | (r & 3))];
+            const float h = tf32_trunc(x);
+            hv[k] = __float_as_uint(h);
+            lv[k] = __float_as_uint(x - h);
+          }
+        }
+        const uint32_t ta = tmem + kColA + 64u * (uint32_t)as + ((uint32_t)(32 * q) << 16);
+        tmem_st32(ta, hv);
+        tmem_st32(ta + 32, lv);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        if (++as == 2) {
+          as = 0;
+          aph ^= 1;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.conv[stage]);
+      if (flags & F_DONE) break;
+      if (++stage == kStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else if (warp >= 8 && warp < 4 + kSplitWarps) {
+    // ------------------------------------------------------------ split B (smem)
+    // Warp 8+q owns B block q (four 1 KiB swizzle atoms of 8 rows x 128 B, two
+    // float4 per lane).  hi replaces the landed value in place, lo goes to the
+    // stage's lo area.  The MN-major operand (B unless transposed) is re-laid
+    // out for the 128-byte swizzle with 32-byte atoms (SWIZZLE_128B_BASE32B):
+    // 16-byte chunk c of row r moves from c ^ (r&7) to ((c>>1 ^ (r&3))<<1 | (c&1))
+    // — in place, after all lanes of the warp have read the atom.
+    const int q = warp - 8;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (;;) {
+      mbar_wait(&S.full[stage], phase);
+      const int flags = S.hdr[stage].flags;
+      if (!(flags & (F_END | F_DONE))) {
+        float4* hi = reinterpret_cast<float4*>(data + (size_t)stage * kStageBytes + (4 + q) * kBlkBytes);
+        float4* lo = reinterpret_cast<float4*>(data + (size_t)stage * kStageBytes + kBloOff + q * kBlkBytes);
 #pragma unroll 1
-        for (int atom = cw; atom < 32; atom += kSplitWarps) {  // atoms 0-15: A, 16-31: B
-          // MN-major operands get the 32-byte-atom layout: B unless transposed, A if transposed
-          const bool relayout = atom >= 16 ? !kTB : kTA;
+        for (int atom = 0; atom < 4; ++atom) {
           float4 x[2];
 #pragma unroll
           for (int h = 0; h < 2; ++h) x[h] = hi[atom * 64 + lane + 32 * h];
@@ -356,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
           for (int h = 0; h < 2; ++h) {
             const int f = lane + 32 * h;
             int t = f;
-            if (relayout) {
+            if (!kTB) {
               const int r = f >> 3, c16 = (f & 7) ^ r;
               t = r * 8 + ((((c16 >> 1) ^ (r & 3)) << 1) | (c16 & 1));
             }
@@ -374,10 +455,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
           }
         }
         fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
-        if (++lo_slot == kLoSlots) {
-          lo_slot = 0;
-          lo_phase ^= 1;
-        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.conv[stage]);
@@ -393,8 +470,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int as = 0;
+    int ntiles_done = 0;  // tiles published to the epilogue (cross-accumulator uses)
     bool started = false;
-    int lo_slot = 0;
     const uint32_t sbase = smem_u32(data);
     for (;;) {
       mbar_wait(&S.conv[stage], phase);
@@ -421,49 +499,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
           mbar_arrive(&S.empty[stage]);  // the marker stage carried no data
         }
         __syncwarp();
+        ++ntiles_done;
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       } else {
         if (flags & F_FIRST) {
           mbar_wait(&S.tempty[acc], acc_phase ^ 1);
+          // the cross accumulator is shared: the previous tile's epilogue must be done
+          if (ntiles_done > 0) mbar_wait(&S.cfree, (uint32_t)((ntiles_done - 1) & 1));
           started = true;
         }
         tc_fence_after();
         if (lane == 0) {
           const uint32_t st = sbase + (uint32_t)stage * kStageBytes;
-          const uint32_t lo = sbase + kLoBase + (uint32_t)lo_slot * kHiBytes;
-          const uint32_t d_main = tmem + (uint32_t)acc * 256;  // hi*hi
-          const uint32_t d_cross = d_main + 128;                // hi*lo + lo*hi
+          const uint32_t d_main = tmem + (uint32_t)acc * 128;  // hi*hi
+          const uint32_t d_cross = tmem + kColCross;           // hi*lo + lo*hi
+          const uint32_t a_slot = tmem + kColA + 64u * (uint32_t)as;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            // A: 128 rows x 32 fp32 K-major, SW128 (LBO 16 B unused, SBO 1024 B); K-slice j at +32 B
-            // K-major operand (4 blocks stacked along M or N, 32 fp32 of K per
-            // 128-byte row): SW128, SBO 1024 B between 8-row groups, K-slice j
-            // at +32 B.  MN-major operand (4 blocks side by side along M or N,
-            // rows = K): 32-byte-atom SW128, LBO 4096 B between the 32-wide
-            // atoms (= blocks), SBO 512 B between 4-row K atoms, K-slice j
-            // (rows 8j..8j+7) at +1024 B.
-            const uint32_t stA = st, stB = st + 4u * kBlkBytes;
-            const uint32_t loA = lo, loB = lo + 4u * kBlkBytes;
-            const uint64_t a_hi = kTA ? sdesc(stA + 1024u * j, 4096, 512, kSW128_32B)
-                                      : sdesc(stA + 32u * j, 16, 1024, kSW128);
-            const uint64_t a_lo = kTA ? sdesc(loA + 1024u * j, 4096, 512, kSW128_32B)
-                                      : sdesc(loA + 32u * j, 16, 1024, kSW128);
+            // A: TMEM, K-slice j = columns 8j..8j+7 of the slot's hi (+0) and lo (+32) halves.
+            // B MN-major (4 blocks side by side along N, rows = K): 32-byte-atom
+            // SW128, LBO 4096 B between the 32-wide atoms (= blocks), SBO 512 B
+            // between 4-row K atoms, K-slice j (rows 8j..8j+7) at +1024 B;
+            // K-major (transposed B): SW128, SBO 1024 B, K-slice j at +32 B.
+            const uint32_t stB = st + 4u * kBlkBytes, loB = st + kBloOff;
             const uint64_t b_hi = kTB ? sdesc(stB + 32u * j, 16, 1024, kSW128)
                                       : sdesc(stB + 1024u * j, 4096, 512, kSW128_32B);
             const uint64_t b_lo = kTB ? sdesc(loB + 32u * j, 16, 1024, kSW128)
                                       : sdesc(loB + 1024u * j, 4096, 512, kSW128_32B);
-            constexpr uint32_t kIdesc = idesc_tf32<kTA, kTB>();
+            constexpr uint32_t kIdesc = idesc_tf32_ts<kTB>();
             const uint32_t acc_in = ((flags & F_FIRST) && j == 0) ? 0u : 1u;
-            tc_mma(d_cross, a_lo, b_hi, kIdesc, acc_in);
-            tc_mma(d_cross, a_hi, b_lo, kIdesc, 1u);
-            tc_mma(d_main, a_hi, b_hi, kIdesc, acc_in);
+            const uint32_t a_hi = a_slot + 8u * j, a_lo = a_hi + 32u;
+            tc_mma_ts(d_cross, a_lo, b_hi, kIdesc, acc_in);
+            tc_mma_ts(d_cross, a_hi, b_lo, kIdesc, 1u);
+            tc_mma_ts(d_main, a_hi, b_hi, kIdesc, acc_in);
           }
           tc_commit(&S.empty[stage]);
-          tc_commit(&S.lo_empty[lo_slot]);
+          tc_commit(&S.afree[as]);
         }
         __syncwarp();
-        if (++lo_slot == kLoSlots) lo_slot = 0;
+        as ^= 1;
       }
       if (++stage == kStages) {
         stage = 0;
@@ -494,10 +569,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
           cb = s == 0 ? c4.x : s == 1 ? c4.y : s == 2 ? c4.z : c4.w;
         }
         uint32_t v[32], w[32];
-        const uint32_t taddr =
-            tmem + (uint32_t)acc * 256 + ((uint32_t)(warp * 32) << 16) + 32u * j;
-        tmem_ld32(taddr, v);        // hi*hi
-        tmem_ld32(taddr + 128, w);  // cross terms
+        const uint32_t lanes = (uint32_t)(warp * 32) << 16;
+        tmem_ld32(tmem + (uint32_t)acc * 128 + lanes + 32u * j, v);  // hi*hi
+        tmem_ld32(tmem + kColCross + lanes + 32u * j, w);            // cross terms
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int c = 0; c < 32; ++c) v[c] = __float_as_uint(__uint_as_float(w[c]) + __uint_as_float(v[c]));
@@ -514,7 +588,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.tempty[acc]);
+      if (lane == 0) {
+        mbar_arrive(&S.tempty[acc]);
+        mbar_arrive(&S.cfree);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
