@@ -725,3 +725,74 @@ def test_screened_eslike_small(qt, ctx):
         ref = oracle.spgemm(Am.nbr, 32, as_tuple(Am), as_tuple(Am), tau=tau)
         assert_same_pattern(got, ref)
         assert np.linalg.norm(got[2] - ref[2]) <= REL_FRO_F64 * np.linalg.norm(ref[2])
+
+
+# ---------------------------------------------- persistent BFS (large levels)
+
+def _arrow_bm(rng, nbr, bs, kind, leaf):
+    """Dense first block row and column plus the diagonal: level groups of very
+    different sizes (one C node with ~nbr tasks, the rest with 1-2)."""
+    mask = np.eye(nbr, dtype=bool)
+    mask[0, :] = True
+    mask[:, 0] = True
+    mask |= rng.random((nbr, nbr)) < 0.01
+    br, bc = np.nonzero(mask)
+    if kind == "int":
+        v = rng.integers(-4, 5, size=(len(br), bs, bs)).astype(np.float64)
+    else:
+        v = rng.uniform(-1, 1, size=(len(br), bs, bs))
+    return qtgen.BlockMatrix(nbr * bs, leaf, bs, br.astype(np.int32), bc.astype(np.int32), v)
+
+
+@pytest.mark.parametrize("nbr", [200, 700])
+def test_bfs_skewed_group_sizes(qt, ctx, nbr):
+    """The large-level kernel splits work by task counts and walks groups with
+    W-lane sub-warps chosen from the mean group size: an arrow pattern puts a
+    huge group next to thousands of tiny ones."""
+    rng = np.random.default_rng(900 + nbr)
+    Am = _arrow_bm(rng, nbr, 32, "int", 256)
+    Bm = _arrow_bm(rng, nbr, 32, "int", 256)
+    A, B = mk(qt, ctx, Am), mk(qt, ctx, Bm)
+    C, st = A.multiply(B)
+    got = C.to_blocks()
+    ref = oracle.spgemm(nbr, 32, as_tuple(Am), as_tuple(Bm))
+    assert_same_pattern(got, ref)
+    assert np.array_equal(got[2], ref[2])
+    L = oracle.tree_levels(Am.n, 32, 256)[0]
+    want = oracle.level_task_counts(L, (Am.brow, Am.bcol), (Bm.brow, Bm.bcol))
+    assert list(st.level_tasks[:len(want)]) == list(want)
+
+
+def test_bfs_deep_sparse_levels(qt, ctx):
+    """Random p = 0.002 on a 2048 x 2048 block grid (12 levels): almost every
+    group at the lower levels has one task (W = 1 sub-warps) and several
+    levels run in the persistent kernel."""
+    rng = np.random.default_rng(77)
+    nbr = 2048
+    Am = random_bm(rng, nbr, 32, 0.002, "int", 2048)
+    Bm = random_bm(rng, nbr, 32, 0.002, "int", 2048)
+    A, B = mk(qt, ctx, Am), mk(qt, ctx, Bm)
+    C, st = A.multiply(B)
+    r, c, v = C.to_blocks()
+    pat = oracle.pattern_product(nbr, (Am.brow, Am.bcol), (Bm.brow, Bm.bcol))
+    assert np.array_equal(r, pat[0]) and np.array_equal(c, pat[1])
+    L = oracle.tree_levels(Am.n, 32, 2048)[0]
+    want = oracle.level_task_counts(L, (Am.brow, Am.bcol), (Bm.brow, Bm.bcol))
+    assert list(st.level_tasks[:len(want)]) == list(want)
+    # values on a sample of block rows
+    lo, hi = 1000, 1040
+    ref = oracle.spgemm(nbr, 32, as_tuple(Am), as_tuple(Bm), rows=(lo, hi))
+    m = (r >= lo) & (r < hi)
+    assert np.array_equal(r[m], ref[0]) and np.array_equal(c[m], ref[1])
+    assert np.array_equal(v[m], ref[2])
+
+
+def test_screened_everything_pruned(qt, ctx):
+    """tau above every block-product norm: the BFS prunes at an upper level
+    and the large levels see empty frontiers; C is the empty matrix."""
+    rng = np.random.default_rng(31)
+    Am = random_bm(rng, 300, 32, 0.05, "uniform", 256)
+    A = mk(qt, ctx, Am)
+    C, st = A.multiply_screened(A, 1e6)
+    r, c, v = C.to_blocks()
+    assert len(r) == 0 and st.block_products == 0
