@@ -12,12 +12,13 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (lt << 61);
 }
 
-__global__ void __launch_bounds__(288, 1) rate(int iters, int mode, unsigned long long* out, float* sink) {
+__global__ void __launch_bounds__(288, 1) rate(int iters, int mode, unsigned long long* out, float* sink,
+                                               int commit_every, int ncommit, int altd) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
   uint8_t* sB = base;            // 16 KiB B (K-major SW128, N=128 rows)
   uint8_t* sH = base + 16384;    // 64 KiB hammer region
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, cbar[2];
   __shared__ uint32_t tbase;
   __shared__ volatile int stop;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -27,6 +28,8 @@ __global__ void __launch_bounds__(288, 1) rate(int iters, int mode, unsigned lon
   if (tid == 0) {
     stop = 0;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "r"(1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&cbar[0])), "r"(1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&cbar[1])), "r"(1));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -46,9 +49,18 @@ __global__ void __launch_bounds__(288, 1) rate(int iters, int mode, unsigned lon
       for (int it = 0; it < iters; ++it)
         for (int j = 0; j < 4; ++j) {
           const uint32_t acc = (it | j) > 0;
-          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tm),
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tm + (altd ? 256u * (j & 1) : 0u)),
                        "r"(tm + 128 + 8 * j), "l"(sdesc(b0 + 32 * j, 16, 1024, 2)), "r"(idesc), "r"(acc)
                        : "memory");
+          if (commit_every && ((it * 4 + j + 1) % commit_every) == 0) {
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(&cbar[0]))
+                         : "memory");
+            if (ncommit > 1)
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                               smem_u32(&cbar[1]))
+                           : "memory");
+          }
         }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar))
                    : "memory");
@@ -123,6 +135,69 @@ __global__ void __launch_bounds__(288, 1) rate(int iters, int mode, unsigned lon
   }
 }
 
+template <int COMMITS, int ROT>  // commits after every group of 4 MMAs; ROT: rotate A slot / B stage per group
+__global__ void __launch_bounds__(128, 1) rate_commit(int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar, cbar[2];
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 4 * 16384 / 16; i += blockDim.x) reinterpret_cast<float4*>(base)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "r"(1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&cbar[0])), "r"(1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&cbar[1])), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)), "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  if (warp == 0) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+    const uint32_t b0 = smem_u32(base);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      if (tid == 0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t acc = (it | j) > 0;
+          const uint32_t rot = ROT ? (uint32_t)(it & 3) : 0u;
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tm),
+                       "r"(tm + 256 + 64 * rot + 8 * j), "l"(sdesc(b0 + 16384 * rot + 32 * j, 16, 1024, 2)), "r"(idesc), "r"(acc)
+                       : "memory");
+        }
+#pragma unroll
+        for (int c = 0; c < COMMITS; ++c)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&cbar[c & 1]))
+                       : "memory");
+      }
+      __syncwarp();
+    }
+    if (tid == 0) {
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar))
+                   : "memory");
+      asm volatile("{\n.reg .pred p;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W;\n}\n" ::"r"(
+                       smem_u32(&bar))
+                   : "memory");
+      out[0] = clock64() - t0;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(512) : "memory");
+  }
+}
+
 int main() {
   unsigned long long* out;
   float* sink;
@@ -131,9 +206,40 @@ int main() {
   const int smem = 1024 + 16384 + 65536;
   cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* names[] = {"none", "LDS.128", "STS.128", "tcgen05.st", "tcgen05.ld", "LDS+STS"};
+  cudaFuncSetAttribute(rate_commit<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+  cudaFuncSetAttribute(rate_commit<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+  cudaFuncSetAttribute(rate_commit<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+  cudaFuncSetAttribute(rate_commit<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+  cudaFuncSetAttribute(rate_commit<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+  cudaFuncSetAttribute(rate_commit<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+  for (int c = 0; c < 6; ++c) {
+    cudaMemset(out, 0, 16);
+    if (c == 0) rate_commit<0, 0><<<148, 128, 70000>>>(2000, out);
+    if (c == 1) rate_commit<1, 0><<<148, 128, 70000>>>(2000, out);
+    if (c == 2) rate_commit<2, 0><<<148, 128, 70000>>>(2000, out);
+    if (c == 3) rate_commit<0, 1><<<148, 128, 70000>>>(2000, out);
+    if (c == 4) rate_commit<1, 1><<<148, 128, 70000>>>(2000, out);
+    if (c == 5) rate_commit<2, 1><<<148, 128, 70000>>>(2000, out);
+    cudaError_t e = cudaDeviceSynchronize();
+    unsigned long long o[2];
+    cudaMemcpy(o, out, 16, cudaMemcpyDeviceToHost);
+    printf("template loop, %d commit(s) per 4 MMAs, %s: %.1f cycles/MMA [%s]\n", c % 3,
+           c >= 3 ? "A slot / B stage rotating" : "same A / B", (double)o[0] / 8000.0, cudaGetErrorString(e));
+  }
+  for (int altd = 0; altd < 2; ++altd)
+    for (int nc = 1; nc <= 2; ++nc)
+      for (int ce : {4, 12, 48}) {
+        cudaMemset(out, 0, 16);
+        rate<<<148, 288, smem>>>(2000, 0, out, sink, ce, nc, altd);
+        cudaDeviceSynchronize();
+        unsigned long long o[2];
+        cudaMemcpy(o, out, 16, cudaMemcpyDeviceToHost);
+        printf("TS tf32 M=128 N=128, %d commit(s) every %2d MMAs, %s D: %.1f cycles/MMA\n", nc, ce,
+               altd ? "alternating" : "one", (double)o[0] / 8000.0);
+      }
   for (int mode = 0; mode < 6; ++mode) {
     cudaMemset(out, 0, 16);
-    rate<<<148, 288, smem>>>(2000, mode, out, sink);
+    rate<<<148, 288, smem>>>(2000, mode, out, sink, 0, 0, 0);
     cudaError_t e = cudaDeviceSynchronize();
     unsigned long long o[2];
     cudaMemcpy(o, out, 16, cudaMemcpyDeviceToHost);
