@@ -198,6 +198,82 @@ __global__ void __launch_bounds__(128, 1) rate_commit(int iters, unsigned long l
   }
 }
 
+// The FP32 kernel's exact per-step MMA sequence: 4 K-slices x (cross += a_lo.b_hi,
+// cross += a_hi.b_lo, main += a_hi.b_hi), B hi/lo MN-major (32-byte-atom SW128),
+// A hi/lo in a rotating TMEM slot, B in a rotating smem stage, COMMITS commits per step.
+template <int COMMITS>
+__global__ void __launch_bounds__(128, 1) rate_step(int steps, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar, cbar[2];
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 4 * 32768 / 16; i += blockDim.x) reinterpret_cast<float4*>(base)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "r"(1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&cbar[0])), "r"(1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&cbar[1])), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)), "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  if (warp == 0) {
+    // idesc: D f32, A/B tf32, A K-major (TMEM), B MN-major
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+    const uint32_t b0 = smem_u32(base);
+    long long t0 = clock64();
+    for (int s = 0; s < steps; ++s) {
+      if (tid == 0) {
+        const uint32_t st = b0 + 32768u * (uint32_t)(s & 3);
+        const uint32_t stB = st, loB = st + 16384u;
+        const uint32_t d_main = tm, d_cross = tm + 256;
+        const uint32_t a_slot = tm + 384 + 64u * (uint32_t)(s & 1);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t b_hi = sdesc(stB + 1024u * j, 4096, 512, 1);
+          const uint64_t b_lo = sdesc(loB + 1024u * j, 4096, 512, 1);
+          const uint32_t a_hi = a_slot + 8u * j, a_lo = a_hi + 32u;
+          const uint32_t acc = (s | j) > 0;
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_cross),
+                       "r"(a_lo), "l"(b_hi), "r"(idesc), "r"(acc) : "memory");
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_cross),
+                       "r"(a_hi), "l"(b_lo), "r"(idesc), "r"(1u) : "memory");
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_main),
+                       "r"(a_hi), "l"(b_hi), "r"(idesc), "r"(acc) : "memory");
+        }
+#pragma unroll
+        for (int c = 0; c < COMMITS; ++c)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&cbar[c & 1]))
+                       : "memory");
+      }
+      __syncwarp();
+    }
+    if (tid == 0) {
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar))
+                   : "memory");
+      asm volatile("{\n.reg .pred p;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W;\n}\n" ::"r"(
+                       smem_u32(&bar))
+                   : "memory");
+      out[0] = clock64() - t0;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(512) : "memory");
+  }
+}
+
 int main() {
   unsigned long long* out;
   float* sink;
@@ -206,6 +282,17 @@ int main() {
   const int smem = 1024 + 16384 + 65536;
   cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* names[] = {"none", "LDS.128", "STS.128", "tcgen05.st", "tcgen05.ld", "LDS+STS"};
+  for (int c = 0; c < 3; ++c) {
+    auto k = c == 0 ? rate_step<0> : c == 1 ? rate_step<1> : rate_step<2>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 140000);
+    cudaMemset(out, 0, 16);
+    k<<<148, 128, 140000>>>(1000, out);
+    cudaError_t e = cudaDeviceSynchronize();
+    unsigned long long o[2];
+    cudaMemcpy(o, out, 16, cudaMemcpyDeviceToHost);
+    printf("FP32 kernel step sequence (12 MMAs), %d commit(s) per step: %.1f cycles/step (floor 768) [%s]\n", c,
+           (double)o[0] / 1000.0, cudaGetErrorString(e));
+  }
   cudaFuncSetAttribute(rate_commit<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
   cudaFuncSetAttribute(rate_commit<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
   cudaFuncSetAttribute(rate_commit<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
