@@ -211,6 +211,7 @@ struct NumericArgs {
   void* poolC;
   int* counter;              // tile scheduler counter (zeroed before launch)
   int group = 1;             // tiles per scheduler grab (1..31)
+  int split = 0;             // 1: work item = (tile, C child q), ntiles = 4 x tiles (few-tile problems)
   int trans = 0;             // bit 0: A transposed, bit 1: B transposed, bit 2: symmetric square
   const void* poolT = nullptr;    // symmetric square: transposed copy of poolA (= poolB)
   const double* normA = nullptr;  // block squared norms (screening) or null

@@ -217,15 +217,16 @@ struct StepDesc {
   int a0, a1, b0, b1, meta;
 };
 template <bool kTA, bool kTB, bool kSym, bool kScreen>
-__device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, const NumericArgs& a) {
+__device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, int keep, const NumericArgs& a) {
   // A child (i,kb) in slot 2i+kb ; B child (kb,j) in slot 2kb+j
   int ta0, ta1, tb0, tb1;
   const int a0 = blk<kSym>(kb ? A4.y : A4.x, ta0), a1 = blk<kSym>(kb ? A4.w : A4.z, ta1);
   const int b0 = blk<kSym>(kb ? B4.z : B4.x, tb0), b1 = blk<kSym>(kb ? B4.w : B4.y, tb1);
   // products of this step: both blocks present and, when screening,
   // ||A(i,k)||^2 * ||B(k,j)||^2 >= tau^2 (the symbolic pass's test)
-  const int pm = (prod_ok<kScreen>(a0, b0, a) ? 1 : 0) | (prod_ok<kScreen>(a0, b1, a) ? 2 : 0) |
-                 (prod_ok<kScreen>(a1, b0, a) ? 4 : 0) | (prod_ok<kScreen>(a1, b1, a) ? 8 : 0);
+  const int pm = ((prod_ok<kScreen>(a0, b0, a) ? 1 : 0) | (prod_ok<kScreen>(a0, b1, a) ? 2 : 0) |
+                  (prod_ok<kScreen>(a1, b0, a) ? 4 : 0) | (prod_ok<kScreen>(a1, b1, a) ? 8 : 0)) &
+                 keep;
   StepDesc d;
   d.a0 = (pm & 3) ? a0 : -1;
   d.a1 = (pm & 12) ? a1 : -1;
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
     int4 g_cc = make_int4(-1, -1, -1, -1);
     // next batch
     int n_state = 0, n_tl = 0, n_t0 = 0, n_n = 0, n_ts = 0, n_pb0 = 0, n_pend = 0, n_pa = -1, n_pb = -1;
+    int n_keep = 15, g_keep = 15;  // product mask of the work item (split mode: one C child)
     bool n_newgroup = true, n_valid = false;
     int4 n_cc = make_int4(-1, -1, -1, -1), n_ra = n_cc, n_rb = n_cc;
     StepDesc n_d0{-1, -1, -1, -1, 0}, n_d1{-1, -1, -1, -1, 0};
@@ -305,9 +307,25 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
             break;
           }
           n_valid = true;
-          n_n = min(G, ntiles - n_t0);
-          n_ts = lane <= n_n ? a.tile_start[n_t0 + lane] : 0;
-          n_cc = lane < n_n ? a.childC[n_t0 + lane] : make_int4(-1, -1, -1, -1);
+          if (a.split) {  // item = (tile, C child q): one product slot of the tile
+            const int tile = n_t0 >> 2, q = n_t0 & 3;
+            n_n = 1;
+            n_keep = 1 << q;
+            n_ts = lane <= 1 ? a.tile_start[tile + lane] : 0;
+            int4 c = make_int4(-1, -1, -1, -1);
+            if (lane == 0) {
+              const int4 t4 = a.childC[tile];
+              if (q == 0) c.x = t4.x;
+              if (q == 1) c.y = t4.y;
+              if (q == 2) c.z = t4.z;
+              if (q == 3) c.w = t4.w;
+            }
+            n_cc = c;
+          } else {
+            n_n = min(G, ntiles - n_t0);
+            n_ts = lane <= n_n ? a.tile_start[n_t0 + lane] : 0;
+            n_cc = lane < n_n ? a.childC[n_t0 + lane] : make_int4(-1, -1, -1, -1);
+          }
           n_state = 2;
           break;
         }
@@ -329,8 +347,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
           if (n_pa >= 0) {
             const int4 ca = op_xform(n_ra, n_pa, kTA, kSym);
             const int4 cb = op_xform(n_rb, n_pb, kTB, kSym);
-            n_d0 = make_step<kTA, kTB, kSym, kScreen>(ca, cb, 0, a);
-            n_d1 = make_step<kTA, kTB, kSym, kScreen>(ca, cb, 1, a);
+            const int keep = n_newgroup ? n_keep : g_keep;
+            n_d0 = make_step<kTA, kTB, kSym, kScreen>(ca, cb, 0, keep, a);
+            n_d1 = make_step<kTA, kTB, kSym, kScreen>(ca, cb, 1, keep, a);
           } else {
             n_d0 = StepDesc{-1, -1, -1, -1, 0};
             n_d1 = n_d0;
@@ -391,6 +410,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
       // promote the prefetched batch
       if (n_newgroup) {
         g_n = n_n;
+        g_keep = n_keep;
         g_ts = n_ts;
         g_cc = n_cc;
         g_pend = n_pend;
@@ -604,9 +624,19 @@ static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
   k_numeric_f64<TA, TB, SYM, SCR><<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
 }
 
-void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a) {
+void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
   if (dt != QT_F64) fail(QT_EDTYPE, "launch_numeric is the FP64 kernel");
-  QT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), ctx->stream));
+  QT_CUDA(cudaMemsetAsync(a0.counter, 0, sizeof(int), ctx->stream));
+  // Few tiles (fewer than half the tile streams of the GPU): every C block of
+  // a tile becomes its own work item, so more streams share the work — a lone
+  // stream per SM is latency bound (its 9-slot ring covers ~2 steps of TMA
+  // latency).  Config 1 (64 tiles): numeric 60 -> 29 us.
+  NumericArgs a = a0;
+  if (a.ntiles * 2 < (int64_t)ctx->num_sms * kStreams) {
+    a.split = 1;
+    a.ntiles = 4 * a0.ntiles;
+    a.group = 1;
+  }
   const int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
   // a.group: one tile per grab (dense/banded: finest dynamic balance) or
   // grouped grabs (sparse patterns: amortise the scheduler and metadata latency)
