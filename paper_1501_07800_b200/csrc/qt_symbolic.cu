@@ -110,6 +110,7 @@ __device__ __forceinline__ void emit_task(int4 a4, int4 b4, int64_t base, int32_
 
 struct SmallBfsArgs {
   int l_end;  // run transitions l -> l+1 for l < l_end
+  int L;      // the block level: the transition L-1 -> L only counts (no emit)
   int trans;  // mode: bit 0 A transposed, bit 1 B transposed, bit 2 symmetric square
   const int4* childA[QT_MAX_LEVELS];
   const int4* childB[QT_MAX_LEVELS];
@@ -214,8 +215,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
       a.f_out[l + 1] = Fn;
     }
     __syncthreads();
-    // 4. emit the child tasks
-    for (int p = tid; p < F; p += kSmallThreads) {
+    // 4. emit the child tasks (none below the block level)
+    for (int p = tid; p < F && l + 1 < a.L; p += kSmallThreads) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
       emit_task(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym),
                 4ll * c0 + (p - c0), m, s, prune && on_diagonal(ck[s]), sc, sym, a.off, a.gidx, a.pa[nxt],
@@ -648,6 +649,9 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       const bool f32 = C->dtype == QT_F32;
       int l_end = 0;
       while (l_end < L - 1 && F[l_end + 1] <= kSmallMaxF) ++l_end;
+      // every level small (FP64): the single-CTA kernel also runs the last
+      // transition and no cooperative launch is needed
+      if (!f32 && l_end == L - 1 && F[L - 1] <= kSmallMaxF) l_end = L;
       if (f32) l_end = std::min(l_end, L - 2);  // the FP32 tiles need the level L-2 queue
       int64_t maxF = 1, maxNS = 1, maxF4 = 1;
       for (int l = 0; l <= l_end; ++l) {
@@ -658,6 +662,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       DevBuf sp[2], sb[2], sc[2], scs[2], sck[2];
       SmallBfsArgs sa;
       sa.l_end = l_end;
+      sa.L = L;
       sa.trans = trans;
       sa.tau2 = tau2;
       for (int l = 0; l <= L && l < QT_MAX_LEVELS; ++l) {
@@ -688,13 +693,18 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       tr.mark("small_alloc");
       k_bfs_small<<<1, kSmallThreads, 0, st>>>(sa);
       QT_LAUNCH_CHECK(ctx);
-      const int cb = l_end & 1;
+      const bool all_small = l_end == L;
+      const int cb = (all_small ? L - 1 : l_end) & 1;
       DevBuf pa = std::move(sp[cb]), pb = std::move(sb[cb]), pc = std::move(sc[cb]);
       DevBuf cstart = std::move(scs[cb]), ckey = std::move(sck[cb]);
       // --- large levels: one persistent cooperative kernel, no host sync
       DevBuf cchild, t2_pa, t2_pb, t2_cstart, cchild2;
       tr.mark("small_launch");
-      {
+      if (all_small) {
+        // level L-1's queue and C's blocks (level L groups) came from the small kernel
+        C->key = std::move(sck[L & 1]);
+        cchild = std::move(sg);
+      } else {
         // level l_end lives in the small kernel's buffers; levels l_end+1..L
         // alternate between two buffer sets (level L: groups only)
         int64_t mF = 1, mNS = 1, mNSg = 1;
