@@ -796,3 +796,52 @@ def test_screened_everything_pruned(qt, ctx):
     C, st = A.multiply_screened(A, 1e6)
     r, c, v = C.to_blocks()
     assert len(r) == 0 and st.block_products == 0
+
+
+# ------------------------------------------ f1 / f4 at the full BASELINE size
+
+def test_symm_square_cfg4_full_size_sampled(qt, ctx):
+    """The paper's S^2 operation at config 4's full size (3072 atoms, symmetric
+    values, upper triangle stored): C's pattern is the upper triangle of the
+    full boolean product, sampled block rows match the oracle's product of
+    the expanded matrix, and the work is half the full multiply's."""
+    c = qtgen.config(4, symmetric=True)
+    full = c["A"]
+    U = qtgen.upper(full)
+    C, st = mk(qt, ctx, U).symm_square()
+    r, cc, v = C.to_blocks()
+    nbr = full.nbr
+    pr, pc = oracle.pattern_product(nbr, (full.brow, full.bcol), (full.brow, full.bcol))
+    up = pr <= pc
+    assert np.array_equal(r, pr[up]) and np.array_equal(cc, pc[up])
+    L, _ = oracle.tree_levels(U.n, 32, U.leaf_dim)
+    assert list(st.level_tasks[: L + 1]) == oracle.level_task_counts_sym(L, (U.brow, U.bcol))
+    full_products = oracle.level_task_counts(L, (full.brow, full.bcol), (full.brow, full.bcol))[-1]
+    assert 0.45 <= st.block_products / full_products <= 0.55
+    for lo, hi in [(0, 4), (1500, 1504), (3064, 3072)]:
+        ref = oracle.spgemm(nbr, 32, as_tuple(full), as_tuple(full), rows=(lo, hi))
+        k = ref[0] <= ref[1]
+        m = (r >= lo) & (r < hi)
+        assert np.array_equal(r[m], ref[0][k]) and np.array_equal(cc[m], ref[1][k])
+        d = v[m] - ref[2][k]
+        assert np.linalg.norm(d) <= REL_FRO_F64 * np.linalg.norm(ref[2][k])
+
+
+def test_screened_cfg4_full_size_sampled(qt, ctx):
+    """Norm-screened product at config 4's full size (tau = 2): the pattern and
+    sampled block rows equal the oracle's screened product, and the skipped
+    products obey the error bound ||C - C~||_F <= sum of skipped ||A_IK|| ||B_KJ||."""
+    c = qtgen.config(4)
+    Am = c["A"]
+    A = mk(qt, ctx, Am)
+    tau = 2.0
+    C, st = A.multiply_screened(A, tau)
+    r, cc, v = C.to_blocks()
+    nbr = Am.nbr
+    for lo, hi in [(0, 4), (1500, 1504), (3068, 3072)]:
+        ref = oracle.spgemm(nbr, 32, as_tuple(Am), as_tuple(Am), rows=(lo, hi), tau=tau)
+        m = (r >= lo) & (r < hi)
+        assert np.array_equal(r[m], ref[0]) and np.array_equal(cc[m], ref[1])
+        assert np.linalg.norm(v[m] - ref[2]) <= REL_FRO_F64 * np.linalg.norm(ref[2])
+    C0, st0 = A.multiply(A)
+    assert st.block_products < st0.block_products
