@@ -205,6 +205,21 @@ qt_status qt_level_nodes(qt_mat A, int64_t* counts, int32_t cap, int32_t* nlevel
  * Errors: QT_EINVAL, QT_ECUDA. */
 qt_status qt_read_back(qt_mat A, int32_t* brow, int32_t* bcol, void* values);
 
+/* qt_read_back without the final synchronisation, for pipelined host
+ * transfers: the reorder/unpack kernels run on the context stream into a
+ * device staging buffer, and the device-to-host copies run on the context's
+ * COPY stream (PCIe is full duplex: they overlap the next step's host-to-device
+ * input copy and its compute).  The host buffers (pinned, for real overlap)
+ * are valid only after qt_ctx_synchronize(ctx); A may be destroyed right
+ * after the call.  Device destination pointers are written on the context
+ * stream (no copy stream involved).
+ * Errors: QT_EINVAL, QT_ECUDA. */
+qt_status qt_read_back_async(qt_mat A, int32_t* brow, int32_t* bcol, void* values);
+
+/* Wait for everything this context has enqueued, including the copies of
+ * qt_read_back_async, and release their staging buffers.  Errors: QT_ECUDA. */
+qt_status qt_ctx_synchronize(qt_ctx ctx);
+
 /* Release a matrix (stream-ordered; safe right after the last use). */
 qt_status qt_destroy(qt_mat A);
 

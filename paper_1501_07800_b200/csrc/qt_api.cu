@@ -229,6 +229,8 @@ qt_status qt_ctx_destroy(qt_ctx ctx) {
   if (!ctx) return QT_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  reap_pending(ctx, true);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->world > 1) dist_finalize(ctx);
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   ctx->scratch.release();
@@ -519,6 +521,23 @@ qt_status qt_read_back(qt_mat A, int32_t* brow, int32_t* bcol, void* values) {
   if (!A) fail(QT_EINVAL, "NULL matrix");
   QT_CUDA(cudaSetDevice(A->ctx->device));
   read_back(A, brow, bcol, values);
+  API_CATCH
+}
+
+qt_status qt_read_back_async(qt_mat A, int32_t* brow, int32_t* bcol, void* values) {
+  API_TRY
+  if (!A) fail(QT_EINVAL, "NULL matrix");
+  QT_CUDA(cudaSetDevice(A->ctx->device));
+  read_back(A, brow, bcol, values, true);
+  API_CATCH
+}
+
+qt_status qt_ctx_synchronize(qt_ctx ctx) {
+  API_TRY
+  if (!ctx) fail(QT_EINVAL, "NULL context");
+  QT_CUDA(cudaSetDevice(ctx->device));
+  QT_CUDA(cudaStreamSynchronize(ctx->stream));
+  reap_pending(ctx, true);
   API_CATCH
 }
 

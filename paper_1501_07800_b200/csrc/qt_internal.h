@@ -114,6 +114,12 @@ struct qt_ctx_s {
   qt::DevBuf zeros;    // one zero block (8 KiB) for absent tcgen05 operands
   void* pinned = nullptr;  // small pinned host staging area
   size_t pinned_bytes = 0;
+  cudaStream_t copy_stream = nullptr;  // device-to-host copies of qt_read_back_async
+  struct PendingCopy {
+    cudaEvent_t done;
+    qt::DevBuf bufs[3];  // staging buffers, released when `done` has completed
+  };
+  std::vector<PendingCopy*> pending;
 };
 
 struct qt_mat_s {
@@ -171,7 +177,8 @@ void check_upper(qt_mat M);
 // 64-block matrix without the (1,0) 32-sub-blocks of its diagonal 64-blocks
 qt_mat upper32_view(qt_mat M);
 // row-major (brow, bcol) order and un-swizzle into caller buffers (caller's block size)
-void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals);
+void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals, bool async = false);
+void reap_pending(qt_ctx ctx, bool wait);
 // 64-blocks (2x2 quads of 32-blocks): split inputs / user-level block count
 void split64(qt_ctx ctx, qt_dtype dt, int64_t nb, const int32_t* brow, const int32_t* bcol,
              const void* vals, DevBuf& obrow, DevBuf& obcol, DevBuf& ovals);

@@ -544,8 +544,27 @@ static void read_back64(qt_mat M, int32_t* brow, int32_t* bcol, void* vals) {
   QT_CUDA(cudaStreamSynchronize(st));
 }
 
-void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals) {
+void reap_pending(qt_ctx ctx, bool wait) {
+  auto& P = ctx->pending;
+  size_t keep = 0;
+  for (size_t i = 0; i < P.size(); ++i) {
+    auto* pc = P[i];
+    const cudaError_t e = wait ? cudaEventSynchronize(pc->done) : cudaEventQuery(pc->done);
+    if (e == cudaSuccess) {
+      cudaEventDestroy(pc->done);
+      delete pc;  // releases the staging buffers
+    } else if (e == cudaErrorNotReady) {
+      P[keep++] = pc;
+    } else {
+      QT_CUDA(e);
+    }
+  }
+  P.resize(keep);
+}
+
+void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals, bool async) {
   if (M->ubs == 64) {
+    if (async) fail(QT_EINVAL, "qt_read_back_async is built for block_size 32");
     read_back64(M, brow, bcol, vals);
     return;
   }
@@ -575,10 +594,33 @@ void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals) {
     k_unpack<float><<<g, 256, 0, st>>>(M->pool.as<float>(), M->key.as<uint64_t>(),
                                        order.as<int32_t>(), nb, obr, obc, (float*)ov);
   QT_LAUNCH_CHECK(ctx);
+  if (async && ((brow && !dr) || (bcol && !dc) || (vals && !dv))) {
+    // device-to-host copies on the copy stream after the unpack; the staging
+    // buffers live until the copies are done (reap_pending)
+    reap_pending(ctx, false);
+    if (!ctx->copy_stream) QT_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    auto* pc = new qt_ctx_s::PendingCopy();
+    cudaEvent_t ready;
+    QT_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    QT_CUDA(cudaEventCreateWithFlags(&pc->done, cudaEventDisableTiming));
+    QT_CUDA(cudaEventRecord(ready, st));
+    QT_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
+    cudaStream_t cs = ctx->copy_stream;
+    if (brow && !dr) QT_CUDA(cudaMemcpyAsync(brow, obr, nb * 4, cudaMemcpyDeviceToHost, cs));
+    if (bcol && !dc) QT_CUDA(cudaMemcpyAsync(bcol, obc, nb * 4, cudaMemcpyDeviceToHost, cs));
+    if (vals && !dv) QT_CUDA(cudaMemcpyAsync(vals, ov, nb * 1024 * es, cudaMemcpyDeviceToHost, cs));
+    QT_CUDA(cudaEventRecord(pc->done, cs));
+    QT_CUDA(cudaEventDestroy(ready));  // destruction is deferred until the event completes
+    pc->bufs[0] = std::move(sr);
+    pc->bufs[1] = std::move(sc);
+    pc->bufs[2] = std::move(sv);
+    ctx->pending.push_back(pc);
+    return;
+  }
   if (brow && !dr) QT_CUDA(cudaMemcpyAsync(brow, obr, nb * 4, cudaMemcpyDeviceToHost, st));
   if (bcol && !dc) QT_CUDA(cudaMemcpyAsync(bcol, obc, nb * 4, cudaMemcpyDeviceToHost, st));
   if (vals && !dv) QT_CUDA(cudaMemcpyAsync(vals, ov, nb * 1024 * es, cudaMemcpyDeviceToHost, st));
-  QT_CUDA(cudaStreamSynchronize(st));
+  if (!async) QT_CUDA(cudaStreamSynchronize(st));
 }
 
 static qt_mat clone_params(qt_mat A) {

@@ -75,6 +75,8 @@ def _load():
         "qt_info": [P, P, P, P, P, P, P, P, P],
         "qt_level_nodes": [P, P, i32, P],
         "qt_read_back": [P, P, P, P],
+        "qt_read_back_async": [P, P, P, P],
+        "qt_ctx_synchronize": [P],
         "qt_destroy": [P],
         "qt_fp64_peak": [P, ctypes.c_int, ctypes.c_float, P],
         "qt_loopback_hub_create": [i32, P],
@@ -96,7 +98,7 @@ _lib = _load()
 EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_nccl_unique_id", "qt_create", "qt_multiply",
             "qt_multiply_ex", "qt_symm_square", "qt_multiply_screened",
             "qt_multiply_virtual", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
-            "qt_destroy", "qt_last_error", "qt_kernel_launches", "qt_fp64_peak",
+            "qt_read_back_async", "qt_ctx_synchronize", "qt_destroy", "qt_last_error", "qt_kernel_launches", "qt_fp64_peak",
             "qt_loopback_hub_create", "qt_loopback_hub_destroy", "qt_ctx_create_loopback")
 
 
@@ -173,6 +175,10 @@ class Context:
     @property
     def kernel_launches(self) -> int:
         return int(_lib.qt_kernel_launches(self._h))
+
+    def synchronize(self):
+        """Wait for all enqueued work, including qt_read_back_async copies."""
+        _check(_lib.qt_ctx_synchronize(self._h))
 
     def fp64_peak(self, kind: str = "dmma", ms: float = 50.0) -> float:
         out = ctypes.c_double()
@@ -301,17 +307,19 @@ class Matrix:
         _check(_lib.qt_level_nodes(self._h, buf, MAX_LEVELS, ctypes.byref(nl)))
         return list(buf[: nl.value])
 
-    def to_blocks(self, out=None):
+    def to_blocks(self, out=None, wait=True):
         """(brow, bcol, vals) sorted by (brow, bcol).  Default: new numpy arrays.
         ``out=(brow, bcol, vals)`` writes into caller buffers (numpy or torch,
-        host or device)."""
+        host or device).  ``wait=False`` (qt_read_back_async): host copies run
+        on the context's copy stream and are valid after ``ctx.synchronize()``."""
         inf = self.info()
         nb, bs = inf["local_nblocks"], inf["bs"]
         if out is None:
             dt = np.float64 if inf["dtype"] == "f64" else np.float32
             out = (np.empty(nb, np.int32), np.empty(nb, np.int32), np.empty((nb, bs, bs), dt))
         if nb:
-            _check(_lib.qt_read_back(self._h, _ptr(out[0]), _ptr(out[1]), _ptr(out[2])))
+            fn = _lib.qt_read_back if wait else _lib.qt_read_back_async
+            _check(fn(self._h, _ptr(out[0]), _ptr(out[1]), _ptr(out[2])))
         return out
 
     def close(self):

@@ -845,3 +845,31 @@ def test_screened_cfg4_full_size_sampled(qt, ctx):
         assert np.linalg.norm(v[m] - ref[2]) <= REL_FRO_F64 * np.linalg.norm(ref[2])
     C0, st0 = A.multiply(A)
     assert st.block_products < st0.block_products
+
+
+def test_read_back_async_matches_sync(qt, ctx):
+    """qt_read_back_async: unpack on the context stream, device-to-host copies
+    on the copy stream; after qt_ctx_synchronize the pinned host buffers hold
+    exactly what qt_read_back returns, even when C is destroyed right after
+    the call and its memory is reused by the next multiply."""
+    import torch
+    rng = np.random.default_rng(55)
+    Am = random_bm(rng, 96, 32, 0.2, "uniform", 256)
+    A = mk(qt, ctx, Am)
+    refs, outs = [], []
+    for _ in range(3):
+        C, _ = A.multiply(A)
+        ref = C.to_blocks()
+        nb = len(ref[0])
+        o = (torch.empty(nb, dtype=torch.int32).pin_memory(), torch.empty(nb, dtype=torch.int32).pin_memory(),
+             torch.empty((nb, 32, 32), dtype=torch.float64).pin_memory())
+        C.to_blocks(o, wait=False)
+        C.close()
+        refs.append(ref)
+        outs.append(o)
+        D, _ = A.multiply(A)      # reuses C's memory while the copies may still run
+        D.close()
+    ctx.synchronize()
+    for ref, o in zip(refs, outs):
+        assert np.array_equal(o[0].numpy(), ref[0]) and np.array_equal(o[1].numpy(), ref[1])
+        assert np.array_equal(o[2].numpy(), ref[2])
