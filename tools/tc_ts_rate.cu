@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(128, 1) rate_commit(int iters, unsigned long l
 // The FP32 kernel's exact per-step MMA sequence: 4 K-slices x (cross += a_lo.b_hi,
 // cross += a_hi.b_lo, main += a_hi.b_hi), B hi/lo MN-major (32-byte-atom SW128),
 // A hi/lo in a rotating TMEM slot, B in a rotating smem stage, COMMITS commits per step.
-template <int COMMITS>
+template <int COMMITS, int FENCE = 0>
 __global__ void __launch_bounds__(128, 1) rate_step(int steps, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
@@ -231,6 +231,12 @@ __global__ void __launch_bounds__(128, 1) rate_step(int steps, unsigned long lon
     const uint32_t b0 = smem_u32(base);
     long long t0 = clock64();
     for (int s = 0; s < steps; ++s) {
+      if (FENCE == 1) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (FENCE == 2) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
       if (tid == 0) {
         const uint32_t st = b0 + 32768u * (uint32_t)(s & 3);
         const uint32_t stB = st, loB = st + 16384u;
@@ -282,15 +288,16 @@ int main() {
   const int smem = 1024 + 16384 + 65536;
   cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* names[] = {"none", "LDS.128", "STS.128", "tcgen05.st", "tcgen05.ld", "LDS+STS"};
-  for (int c = 0; c < 3; ++c) {
-    auto k = c == 0 ? rate_step<0> : c == 1 ? rate_step<1> : rate_step<2>;
+  for (int c = 0; c < 5; ++c) {
+    auto k = c == 0 ? rate_step<0> : c == 1 ? rate_step<1> : c == 2 ? rate_step<2> : c == 3 ? rate_step<2, 1> : rate_step<2, 2>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 140000);
     cudaMemset(out, 0, 16);
     k<<<148, 128, 140000>>>(1000, out);
     cudaError_t e = cudaDeviceSynchronize();
     unsigned long long o[2];
     cudaMemcpy(o, out, 16, cudaMemcpyDeviceToHost);
-    printf("FP32 kernel step sequence (12 MMAs), %d commit(s) per step: %.1f cycles/step (floor 768) [%s]\n", c,
+    printf("FP32 kernel step sequence (12 MMAs), %d commit(s) per step%s: %.1f cycles/step (floor 768) [%s]\n",
+           c < 3 ? c : 2, c == 3 ? " + fence::after_thread_sync" : c == 4 ? " + before/syncwarp/after fences" : "",
            (double)o[0] / 1000.0, cudaGetErrorString(e));
   }
   cudaFuncSetAttribute(rate_commit<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
