@@ -201,14 +201,22 @@ __global__ void __launch_bounds__(128, 1) rate_commit(int iters, unsigned long l
 // The FP32 kernel's exact per-step MMA sequence: 4 K-slices x (cross += a_lo.b_hi,
 // cross += a_hi.b_lo, main += a_hi.b_hi), B hi/lo MN-major (32-byte-atom SW128),
 // A hi/lo in a rotating TMEM slot, B in a rotating smem stage, COMMITS commits per step.
-template <int COMMITS, int FENCE = 0>
+template <int COMMITS, int FENCE = 0, int RANDOM = 0>
 __global__ void __launch_bounds__(128, 1) rate_step(int steps, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t bar, cbar[2];
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < 4 * 32768 / 16; i += blockDim.x) reinterpret_cast<float4*>(base)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = tid; i < 4 * 32768 / 4; i += blockDim.x) {
+    float x = 0.f;
+    if (RANDOM) {
+      unsigned h = (unsigned)i * 2654435761u + 12345u;
+      h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+      x = (float)(h & 0xffffff) * (1.0f / 16777216.0f) - 0.5f;
+    }
+    reinterpret_cast<float*>(base)[i] = x;
+  }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "r"(1));
@@ -225,6 +233,27 @@ __global__ void __launch_bounds__(128, 1) rate_step(int steps, unsigned long lon
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tm = tbase;
+  if (RANDOM) {
+    uint32_t v[32];
+    for (int c = 0; c < 32; ++c) {
+      unsigned h = (unsigned)(tid * 131 + c) * 2654435761u;
+      h ^= h >> 15;
+      v[c] = __float_as_uint((float)(h & 0xffff) * (1.0f / 65536.0f) - 0.5f);
+    }
+    for (int col = 384; col < 512; col += 32)
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+          "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(tm + col + ((uint32_t)(warp * 32) << 16)),
+          "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+          "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+          "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+          "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+          : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
   if (warp == 0) {
     // idesc: D f32, A/B tf32, A K-major (TMEM), B MN-major
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
@@ -288,8 +317,8 @@ int main() {
   const int smem = 1024 + 16384 + 65536;
   cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* names[] = {"none", "LDS.128", "STS.128", "tcgen05.st", "tcgen05.ld", "LDS+STS"};
-  for (int c = 0; c < 5; ++c) {
-    auto k = c == 0 ? rate_step<0> : c == 1 ? rate_step<1> : c == 2 ? rate_step<2> : c == 3 ? rate_step<2, 1> : rate_step<2, 2>;
+  for (int c = 0; c < 6; ++c) {
+    auto k = c == 0 ? rate_step<0> : c == 1 ? rate_step<1> : c == 2 ? rate_step<2> : c == 3 ? rate_step<2, 1> : c == 4 ? rate_step<2, 2> : rate_step<2, 0, 1>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 140000);
     cudaMemset(out, 0, 16);
     k<<<148, 128, 140000>>>(1000, out);
@@ -297,7 +326,7 @@ int main() {
     unsigned long long o[2];
     cudaMemcpy(o, out, 16, cudaMemcpyDeviceToHost);
     printf("FP32 kernel step sequence (12 MMAs), %d commit(s) per step%s: %.1f cycles/step (floor 768) [%s]\n",
-           c < 3 ? c : 2, c == 3 ? " + fence::after_thread_sync" : c == 4 ? " + before/syncwarp/after fences" : "",
+           c < 3 ? c : 2, c == 3 ? " + fence::after_thread_sync" : c == 4 ? " + before/syncwarp/after fences" : c == 5 ? ", RANDOM operands" : "",
            (double)o[0] / 1000.0, cudaGetErrorString(e));
   }
   cudaFuncSetAttribute(rate_commit<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
