@@ -447,11 +447,13 @@ def traffic_from_profiles(P: int):
 
 def measure_e2e(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier):
     """Same metric through the public API with HOST buffers: every step copies
-    A (pinned host) to the device inside qt_create, multiplies, and reads C back
-    to pinned host memory with qt_read_back_async — its device-to-host copies
-    run on the context's copy stream, overlapping the next step's host-to-device
-    copy (PCIe is full duplex) and compute; the timed region ends after
-    qt_ctx_synchronize, i.e. after the last step's C is in host memory."""
+    A (pinned host) to the device inside qt_create (on the context's H2D
+    stream), multiplies with qt_multiply_async (returns once the numeric kernel
+    is enqueued) and reads C back to pinned host memory with
+    qt_read_back_async (device-to-host copies on the copy stream): step i+1's
+    H2D overlaps step i's numeric kernel and D2H (PCIe is full duplex); the
+    timed region ends after qt_ctx_synchronize, i.e. after the last step's C
+    is in host memory."""
     import torch
     brow = torch.from_numpy(Am.brow).pin_memory()
     bcol = torch.from_numpy(Am.bcol).pin_memory()
@@ -461,7 +463,7 @@ def measure_e2e(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier):
 
     def step(i):
         A = qtmm.Matrix.from_blocks(ctx, Am.n, Am.leaf_dim, BS, brow, bcol, vals, row_bounds=bounds)
-        C, st = A.multiply(A)
+        C, st = A.multiply(A, wait=False)
         nb = C.nblocks
         o = outs[i % 2]
         if o is None or o[0].shape[0] != nb:
@@ -494,8 +496,8 @@ def measure_e2e(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier):
     d2h = nb * (8 + BS * BS * 8)
     return {"value": round(prods * FLOP_PER_PRODUCT / (ms * 1e-3) / 1e9, 2), "unit": UNIT,
             "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "api": "qt_create(host pinned) + qt_multiply + qt_read_back_async(host pinned), "
-                   "D2H of step i overlapping step i+1 (copy stream), qt_ctx_synchronize at the end"}
+            "api": "qt_create(host pinned, H2D stream) + qt_multiply_async + qt_read_back_async(host pinned, "
+                   "copy stream), steps pipelined, qt_ctx_synchronize at the end"}
 
 
 if __name__ == "__main__":

@@ -205,6 +205,16 @@ qt_status qt_level_nodes(qt_mat A, int64_t* counts, int32_t cap, int32_t* nlevel
  * Errors: QT_EINVAL, QT_ECUDA. */
 qt_status qt_read_back(qt_mat A, int32_t* brow, int32_t* bcol, void* values);
 
+/* qt_multiply without the final synchronisation on the numeric kernel
+ * (single rank; a multi-rank context behaves as qt_multiply): C is returned
+ * as soon as its blocks are allocated and the numeric kernel is enqueued on
+ * the context stream, so the caller can already enqueue the next step (e.g.
+ * qt_create from host, whose value copy runs on the context's H2D stream).
+ * The st->ms_* timings are 0; everything else in st is filled.  A and B may
+ * be destroyed right after the call (stream-ordered reuse).
+ * Errors: as qt_multiply. */
+qt_status qt_multiply_async(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st);
+
 /* qt_read_back without the final synchronisation, for pipelined host
  * transfers: the reorder/unpack kernels run on the context stream into a
  * device staging buffer, and the device-to-host copies run on the context's

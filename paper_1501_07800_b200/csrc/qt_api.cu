@@ -231,6 +231,12 @@ qt_status qt_ctx_destroy(qt_ctx ctx) {
   cudaStreamSynchronize(ctx->stream);
   reap_pending(ctx, true);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->h2d_stream) {
+    cudaStreamSynchronize(ctx->h2d_stream);
+    cache_release_stream(ctx->h2d_stream);
+    cudaStreamDestroy(ctx->h2d_stream);
+    cudaEventDestroy(ctx->h2d_done);
+  }
   if (ctx->world > 1) dist_finalize(ctx);
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   ctx->scratch.release();
@@ -323,8 +329,18 @@ qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
       }
       const size_t vb = (size_t)nblocks * block_size * block_size * es;
       if (!is_device_ptr(values)) {
-        dv.alloc(vb, st);
-        QT_CUDA(cudaMemcpyAsync(dv.p, values, vb, cudaMemcpyHostToDevice, st));
+        // the values (the bulk) come in on the context's H2D stream, into a
+        // staging buffer of that stream's cache: the copy can start while the
+        // context stream still runs earlier work (e.g. the previous
+        // qt_multiply_async); the build waits for it through an event
+        if (!ctx->h2d_stream) {
+          QT_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+          QT_CUDA(cudaEventCreateWithFlags(&ctx->h2d_done, cudaEventDisableTiming));
+        }
+        dv.alloc(vb, ctx->h2d_stream);
+        QT_CUDA(cudaMemcpyAsync(dv.p, values, vb, cudaMemcpyHostToDevice, ctx->h2d_stream));
+        QT_CUDA(cudaEventRecord(ctx->h2d_done, ctx->h2d_stream));
+        QT_CUDA(cudaStreamWaitEvent(st, ctx->h2d_done, 0));
         pv = dv.p;
       }
     }
@@ -389,12 +405,25 @@ qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, q
     R = multiply_dist(A, B, &S);
   }
   QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
-  QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
-  QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
+  if (!ctx->async_multiply) {
+    QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
+    QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
+  }
   R->global_nb = user_nblocks(R);
   user_stats(R, S);
   *C = R;
   API_CATCH
+}
+
+qt_status qt_multiply_async(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st) {
+  if (!A) return qt_multiply(A, B, C, st);
+  qt_ctx ctx = A->ctx;
+  // single rank only (the multi-rank exchange synchronises anyway)
+  const bool was = ctx->async_multiply;
+  ctx->async_multiply = ctx->world == 1;
+  const qt_status r = qt_multiply(A, B, C, st);
+  ctx->async_multiply = was;
+  return r;
 }
 
 qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_stats* st) {

@@ -115,6 +115,9 @@ struct qt_ctx_s {
   void* pinned = nullptr;  // small pinned host staging area
   size_t pinned_bytes = 0;
   cudaStream_t copy_stream = nullptr;  // device-to-host copies of qt_read_back_async
+  cudaStream_t h2d_stream = nullptr;   // host-to-device value copies of qt_create
+  cudaEvent_t h2d_done = nullptr;
+  bool async_multiply = false;         // qt_multiply_async: no final synchronisation
   struct PendingCopy {
     cudaEvent_t done;
     qt::DevBuf bufs[3];  // staging buffers, released when `done` has completed

@@ -873,12 +873,15 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       }
       QT_CUDA(cudaEventRecord(ctx->ev[4], st));
       tr.mark("numeric_launched");
-      QT_CUDA(cudaEventSynchronize(ctx->ev[4]));  // frontier buffers are released after this
+      // (the frontier buffers go back to this stream's cache: stream-ordered reuse)
+      if (!ctx->async_multiply) QT_CUDA(cudaEventSynchronize(ctx->ev[4]));
       tr.mark("numeric_done");
     }
-    QT_CUDA(cudaEventSynchronize(ctx->ev[4]));
-    QT_CUDA(cudaEventElapsedTime(ms_sym, ctx->ev[2], ctx->ev[3]));
-    QT_CUDA(cudaEventElapsedTime(ms_num, ctx->ev[3], ctx->ev[4]));
+    if (!ctx->async_multiply) {
+      QT_CUDA(cudaEventSynchronize(ctx->ev[4]));
+      QT_CUDA(cudaEventElapsedTime(ms_sym, ctx->ev[2], ctx->ev[3]));
+      QT_CUDA(cudaEventElapsedTime(ms_num, ctx->ev[3], ctx->ev[4]));
+    }
     S.c_blocks = C->nb;
   } catch (...) {
     delete C;

@@ -67,6 +67,7 @@ def _load():
         "qt_nccl_unique_id": [P],
         "qt_create": [P, i64, i32, i32, ctypes.c_int, i64, P, P, P, P, P],
         "qt_multiply": [P, P, P, P],
+        "qt_multiply_async": [P, P, P, P],
         "qt_multiply_ex": [P, P, i32, i32, P, P],
         "qt_symm_square": [P, P, P],
         "qt_multiply_screened": [P, P, ctypes.c_double, P, P],
@@ -96,6 +97,7 @@ def _load():
 
 _lib = _load()
 EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_nccl_unique_id", "qt_create", "qt_multiply",
+            "qt_multiply_async",
             "qt_multiply_ex", "qt_symm_square", "qt_multiply_screened",
             "qt_multiply_virtual", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
             "qt_read_back_async", "qt_ctx_synchronize", "qt_destroy", "qt_last_error", "qt_kernel_launches", "qt_fp64_peak",
@@ -242,10 +244,13 @@ class Matrix:
                               _ptr(rb), ctypes.byref(h)))
         return cls(ctx, h)
 
-    def multiply(self, other: "Matrix"):
+    def multiply(self, other: "Matrix", wait: bool = True):
+        """C = self * other.  ``wait=False`` (qt_multiply_async): returns once
+        the numeric kernel is enqueued (stats without timings)."""
         st = Stats()
         h = ctypes.c_void_p()
-        _check(_lib.qt_multiply(self._h, other._h, ctypes.byref(h), ctypes.byref(st)))
+        fn = _lib.qt_multiply if wait else _lib.qt_multiply_async
+        _check(fn(self._h, other._h, ctypes.byref(h), ctypes.byref(st)))
         return Matrix(self.ctx, h), st
 
     def multiply_ex(self, other: "Matrix", trans_a: bool = False, trans_b: bool = False):

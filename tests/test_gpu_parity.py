@@ -873,3 +873,38 @@ def test_read_back_async_matches_sync(qt, ctx):
     for ref, o in zip(refs, outs):
         assert np.array_equal(o[0].numpy(), ref[0]) and np.array_equal(o[1].numpy(), ref[1])
         assert np.array_equal(o[2].numpy(), ref[2])
+
+
+def test_multiply_async_pipeline(qt, ctx):
+    """qt_create from pinned host memory (H2D stream) + qt_multiply_async +
+    qt_read_back_async, three steps issued back to back with A and C destroyed
+    right after use: after qt_ctx_synchronize every step's host result equals
+    the synchronous multiply's, and the stats other than timings are filled."""
+    import torch
+    rng = np.random.default_rng(56)
+    mats = [random_bm(rng, 80, 32, 0.25, "uniform", 256) for _ in range(3)]
+    refs = []
+    for Am in mats:
+        A = mk(qt, ctx, Am)
+        C, st_ref = A.multiply(A)
+        refs.append((C.to_blocks(), st_ref.block_products))
+    outs, stats = [], []
+    for Am, (ref, _) in zip(mats, refs):
+        br = torch.from_numpy(Am.brow).pin_memory()
+        bc = torch.from_numpy(Am.bcol).pin_memory()
+        v = torch.from_numpy(Am.vals).pin_memory()
+        A = qt.Matrix.from_blocks(ctx, Am.n, Am.leaf_dim, 32, br, bc, v)
+        C, st = A.multiply(A, wait=False)
+        A.close()
+        nb = len(ref[0])
+        o = (torch.empty(nb, dtype=torch.int32).pin_memory(), torch.empty(nb, dtype=torch.int32).pin_memory(),
+             torch.empty((nb, 32, 32), dtype=torch.float64).pin_memory())
+        C.to_blocks(o, wait=False)
+        C.close()
+        outs.append(o)
+        stats.append(st)
+    ctx.synchronize()
+    for (ref, prods), o, st in zip(refs, outs, stats):
+        assert st.block_products == prods
+        assert np.array_equal(o[0].numpy(), ref[0]) and np.array_equal(o[1].numpy(), ref[1])
+        assert np.array_equal(o[2].numpy(), ref[2])

@@ -12,7 +12,7 @@ def step(i, wait):
     t0 = time.perf_counter()
     A = qtmm.Matrix.from_blocks(ctx, Am.n, Am.leaf_dim, 32, brow, bcol, vals)
     t1 = time.perf_counter()
-    C, st = A.multiply(A)
+    C, st = A.multiply(A, wait=wait)
     t2 = time.perf_counter()
     nb = C.nblocks
     o = outs[i % 2]
