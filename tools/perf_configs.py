@@ -82,6 +82,46 @@ def run(ctx, stream, name, c, steps=20):
     return out
 
 
+def leaf_sweep(ctx, stream):
+    """The paper's leaf benchmark shape (Figs. leafmat_bench_double /
+    _single): C = A*B at N = 4096 as ONE leaf, blocks of size bs placed
+    uniformly at random with a given fill factor (A and B independent),
+    FP64 and FP32; device time of qt_multiply, effective GFLOP/s over nonzero
+    block products (2 bs^3 each).  Block size 16 is not built (reading C-4)."""
+    n = 4096
+    for dtype in (np.float64, np.float32):
+        for bs in (32, 64):
+            nb = n // bs
+            for fill in (0.01, 0.02, 0.05, 0.1, 0.2, 0.5, 1.0):
+                rng = np.random.default_rng(int(1000 * fill) + bs)
+                mats = []
+                for _ in range(2):
+                    m = rng.random((nb, nb)) < fill
+                    br, bc = np.nonzero(m)
+                    v = rng.uniform(-1, 1, size=(len(br), bs, bs)).astype(dtype)
+                    mats.append(qtmm.Matrix.from_blocks(ctx, n, n, bs, br.astype(np.int32), bc.astype(np.int32), v))
+                A, B = mats
+                for _ in range(3):
+                    C, st = A.multiply(B)
+                    C.close()
+                steps = 10
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record(stream)
+                for _ in range(steps):
+                    C, st = A.multiply(B)
+                    C.close()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / steps
+                flop = st.block_products * 2.0 * bs ** 3
+                print(json.dumps({"config": "leaf sweep N=4096 (one leaf)", "dtype": "f64" if dtype == np.float64 else "f32",
+                                  "bs": bs, "fill": fill, "block_products": st.block_products,
+                                  "ms_step": round(ms, 4), "gflops_effective": round(flop / ms / 1e6, 1)}), flush=True)
+                A.close()
+                B.close()
+
+
 def main():
     which = sys.argv[1:] or ["1", "2", "3", "4", "5"]
     torch.cuda.set_device(0)
@@ -91,7 +131,9 @@ def main():
     print(json.dumps({"dmma_peak_tflops": round(peak / 1e12, 3),
                       "dfma_peak_tflops": round(ctx.fp64_peak("dfma", 200.0) / 1e12, 3)}), flush=True)
     for w in which:
-        if w == "1":
+        if w == "leafsweep":
+            leaf_sweep(ctx, stream)
+        elif w == "1":
             run(ctx, stream, "cfg1 dense N=512", qtgen.config(1), steps=200)
         elif w == "2":
             run(ctx, stream, "cfg2 banded N=16384", qtgen.config(2))
