@@ -171,10 +171,11 @@ qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_sta
  * the full multiply).  The symbolic pass walks the quadtree of the
  * full matrix through references into U (diagonal nodes expose their (0,1)
  * child transposed as (1,0); transposed nodes swap and transpose their
- * children) and prunes C nodes below the diagonal at every level; the numeric
- * kernel transposes blocks on the fly.  FP64, world == 1 in this build.
- * Errors: QT_EINVAL (a block below the diagonal, or world > 1), QT_EDTYPE
- * (FP32), QT_ENOMEM, QT_ECUDA. */
+ * children) and prunes C nodes below the diagonal at every level; blocks
+ * read transposed come from a transposed copy of U's block pool made once
+ * per call.  FP64 or FP32 (A's dtype), world == 1 in this build.
+ * Errors: QT_EINVAL (a block below the diagonal, or world > 1), QT_ENOMEM,
+ * QT_ECUDA. */
 qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st);
 
 /* Frobenius-norm truncation (reading C-16): remove the longest

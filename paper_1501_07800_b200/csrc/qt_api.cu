@@ -465,7 +465,6 @@ qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
   qt_ctx ctx = A->ctx;
   QT_CUDA(cudaSetDevice(ctx->device));
   if (ctx->world > 1) fail(QT_EINVAL, "the symmetric square is single-rank only in this build");
-  if (A->dtype != QT_F64) fail(QT_EDTYPE, "the symmetric square is FP64-only in this build");
   check_upper(A);
   ensure_levels(A);
   qt_stats local;

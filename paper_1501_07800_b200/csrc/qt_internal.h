@@ -230,6 +230,7 @@ struct NumericArgs {
 };
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a);
 void launch_transpose_blocks(qt_ctx ctx, const void* in, void* out, int64_t nb);
+void launch_transpose_blocks_f32(qt_ctx ctx, const void* in, void* out, int64_t nb);
 
 // FP32 (tcgen05 kind::tf32, 3xTF32): tiles are C nodes at level L-2 (4x4 blocks)
 struct NumericArgs32 {
@@ -250,7 +251,8 @@ struct NumericArgs32 {
   void* poolC;
   const void* zeros;         // one zero block (absent operands)
   int* counter;
-  int trans = 0;             // bit 0: A transposed, bit 1: B transposed
+  int trans = 0;             // bit 0: A transposed, bit 1: B transposed, bit 2: symmetric square
+  const void* poolT = nullptr;  // symmetric square: transposed copy of poolA (= poolB)
 };
 void launch_numeric_f32(qt_ctx ctx, const NumericArgs32& a);
 void launch_fp64_peak(qt_ctx ctx, int kind, int iters, int grid);

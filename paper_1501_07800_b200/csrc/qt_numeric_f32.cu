@@ -207,7 +207,7 @@ __host__ __device__ constexpr uint32_t idesc_tf32_ts() {
          ((128u >> 3) << 17) | ((128u >> 4) << 24);
 }
 
-template <bool kTA, bool kTB>
+template <bool kTA, bool kTB, bool kSym>
 __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned start (kept as an offset from the shared array so the
@@ -274,22 +274,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
 #pragma unroll
           for (int y = 0; y < 4; ++y) ab[x][y] = bb[x][y] = -1;
         if (p < p1) {
-          const int4 qa = ldchild(a.childA2, a.pa[p], kTA);  // op(A) quads (i', k') in slot 2i'+k'
-          const int4 qb = ldchild(a.childB2, a.pb[p], kTB);  // op(B) quads (k', j') in slot 2k'+j'
+          // op(A) quads (i', k') in slot 2i'+k' and op(B) quads (k', j') in slot
+          // 2k'+j'; symmetric square: references into U (index, diagonal,
+          // transposed bits), block references idx*4 + diag*2 + t
+          const int4 qa = op_children(a.childA2, a.pa[p], kTA, kSym);
+          const int4 qb = op_children(a.childB2, a.pb[p], kTB, kSym);
           const int qa_[4] = {qa.x, qa.y, qa.z, qa.w};
           const int qb_[4] = {qb.x, qb.y, qb.z, qb.w};
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
             const int hi = s >> 1, lo = s & 1;
             if (qa_[s] >= 0) {
-              const int4 c = ldchild(a.childA1, qa_[s], kTA);  // (i'', k'') in slot 2i''+k''
+              const int4 c = op_children(a.childA1, qa_[s], kTA, kSym);  // (i'', k'') in slot 2i''+k''
               ab[2 * hi + 0][2 * lo + 0] = c.x;
               ab[2 * hi + 0][2 * lo + 1] = c.y;
               ab[2 * hi + 1][2 * lo + 0] = c.z;
               ab[2 * hi + 1][2 * lo + 1] = c.w;
             }
             if (qb_[s] >= 0) {
-              const int4 c = ldchild(a.childB1, qb_[s], kTB);  // (k'', j'') in slot 2k''+j''
+              const int4 c = op_children(a.childB1, qb_[s], kTB, kSym);  // (k'', j'') in slot 2k''+j''
               bb[2 * hi + 0][2 * lo + 0] = c.x;
               bb[2 * hi + 0][2 * lo + 1] = c.y;
               bb[2 * hi + 1][2 * lo + 0] = c.z;
@@ -319,12 +322,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
               uint8_t* dst = data + (size_t)stage * kStageBytes;
 #pragma unroll
               for (int x = 0; x < 4; ++x) {
-                const float* srcA = ac[x] >= 0 ? poolA + (size_t)ac[x] * 1024 : zeros;
+                // symmetric square: a block of U read transposed comes from the
+                // transposed copy of the pool, so the split warps read blocks as stored
+                const float* srcA;
+                const float* srcB;
+                if (kSym) {
+                  const float* poolT = static_cast<const float*>(a.poolT);
+                  srcA = ac[x] < 0 ? zeros : ((ac[x] & 1) ? poolT : poolA) + (size_t)(ac[x] >> 2) * 1024;
+                  srcB = br[x] < 0 ? zeros : ((br[x] & 1) ? poolT : poolA) + (size_t)(br[x] >> 2) * 1024;
+                } else {
+                  srcA = ac[x] >= 0 ? poolA + (size_t)ac[x] * 1024 : zeros;
+                  const int b = br[x];
+                  srcB = b < 0 ? zeros
+                               : (b < a.splitB ? poolB + (size_t)b * 1024 : poolB2 + (size_t)(b - a.splitB) * 1024);
+                }
                 bulk_g2s(dst + x * kBlkBytes, srcA, kBlkBytes, &S.full[stage]);
-                const int b = br[x];
-                const float* srcB = b < 0 ? zeros
-                                          : (b < a.splitB ? poolB + (size_t)b * 1024
-                                                          : poolB2 + (size_t)(b - a.splitB) * 1024);
                 bulk_g2s(dst + (4 + x) * kBlkBytes, srcB, kBlkBytes, &S.full[stage]);
               }
             }
@@ -605,22 +617,55 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
   }
 }
 
+// Transposed copy of a pool of FP32 blocks (symmetric square): out(r,c) =
+// in(c,r), both in the internal 128-byte swizzle (swz32).
+__global__ void k_transpose_blocks_f32(const float* __restrict__ in, float* __restrict__ out, int64_t nb) {
+  __shared__ float tile[32][33];
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const float* src = in + b * 1024;
+    float* dst = out + b * 1024;
+    for (int r = threadIdx.x >> 5; r < 32; r += blockDim.x >> 5) {
+      const int c = threadIdx.x & 31;
+      tile[r][c] = src[swz32(r, c)];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x >> 5; r < 32; r += blockDim.x >> 5) {
+      const int c = threadIdx.x & 31;
+      dst[swz32(r, c)] = tile[c][r];
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
-template <bool TA, bool TB>
+void launch_transpose_blocks_f32(qt_ctx ctx, const void* in, void* out, int64_t nb) {
+  if (nb <= 0) return;
+  const int grid = (int)std::min<int64_t>(nb, 8ll * ctx->num_sms);
+  k_transpose_blocks_f32<<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(in), static_cast<float*>(out),
+                                                         nb);
+  QT_LAUNCH_CHECK(ctx);
+}
+
+template <bool TA, bool TB, bool SYM = false>
 static void launch_f32_t(qt_ctx ctx, const NumericArgs32& a, int grid) {
   static bool attr_set = false;
   if (!attr_set) {
-    QT_CUDA(cudaFuncSetAttribute(k_numeric_f32<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f32<TA, TB, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kSmemBytes));
     attr_set = true;
   }
-  k_numeric_f32<TA, TB><<<grid, kThreads, kSmemBytes, ctx->stream>>>(a);
+  k_numeric_f32<TA, TB, SYM><<<grid, kThreads, kSmemBytes, ctx->stream>>>(a);
 }
 
 void launch_numeric_f32(qt_ctx ctx, const NumericArgs32& a) {
   QT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), ctx->stream));
   const int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
+  if (a.trans & 4) {  // symmetric square
+    launch_f32_t<false, false, true>(ctx, a, grid);
+    QT_LAUNCH_CHECK(ctx);
+    return;
+  }
   switch (a.trans & 3) {
     case 0: launch_f32_t<false, false>(ctx, a, grid); break;
     case 1: launch_f32_t<true, false>(ctx, a, grid); break;

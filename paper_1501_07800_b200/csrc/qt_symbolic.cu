@@ -842,13 +842,15 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         }
       }
       DevBuf poolT;  // symmetric square: blocks of U read transposed come from U^T's copy
-      if (C->nb > 0 && !f32 && sym) {
-        poolT.alloc((size_t)A->nb * 1024 * 8, st);
-        launch_transpose_blocks(ctx, A->pool_ptr(), poolT.p, A->nb);
+      if (C->nb > 0 && sym) {
+        poolT.alloc((size_t)A->nb * 1024 * elem_size(C->dtype), st);
+        if (f32)
+          launch_transpose_blocks_f32(ctx, A->pool_ptr(), poolT.p, A->nb);
+        else
+          launch_transpose_blocks(ctx, A->pool_ptr(), poolT.p, A->nb);
         na.poolT = poolT.p;
       }
       if (C->nb > 0 && !f32) launch_numeric(ctx, C->dtype, na);
-      if (C->nb > 0 && f32 && sym) fail(QT_EDTYPE, "the symmetric square is FP64-only in this build");
       if (C->nb > 0 && f32) {
         NumericArgs32 nb;
         nb.ntiles = ns[L - 2];
@@ -869,6 +871,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         nb.zeros = ctx->zeros.p;
         nb.counter = ctx->counters.as<int>() + 16;
         nb.trans = trans & 7;
+        nb.poolT = poolT.p;
         launch_numeric_f32(ctx, nb);
       }
       QT_CUDA(cudaEventRecord(ctx->ev[4], st));

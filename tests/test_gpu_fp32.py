@@ -174,3 +174,43 @@ def test_fp32_transposed_products(qt, ctx, ta, tb, kind):
     got = mk(qt, ctx, Am).multiply_ex(mk(qt, ctx, Bm), ta, tb)[0].to_blocks()
     ref = oracle.spgemm_t(nbr, 32, ref64(Am), ref64(Bm), ta, tb)
     check(got, ref, kind)
+
+
+def _sym_upper_f32(rng, nbr, p, kind, leaf):
+    mask = np.triu(rng.random((nbr, nbr)) < p)
+    np.fill_diagonal(mask, rng.random(nbr) < 0.7)
+    br, bc = np.nonzero(mask)
+    v = (rng.integers(-4, 5, size=(len(br), 32, 32)) if kind == "int"
+         else rng.uniform(-1, 1, size=(len(br), 32, 32))).astype(np.float32)
+    for t in range(len(br)):
+        if br[t] == bc[t]:
+            v[t] = np.triu(v[t]) + np.triu(v[t], 1).T
+    return qtgen.BlockMatrix(nbr * 32, leaf, 32, br.astype(np.int32), bc.astype(np.int32), v)
+
+
+@pytest.mark.parametrize("nbr,p,leaf", [(4, 1.0, 64), (13, 0.4, 128), (40, 0.12, 256)])
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_fp32_symm_square(qt, ctx, nbr, p, leaf, kind):
+    """FP32 symmetric square (upper block triangle stored) on the
+    tcgen05 kernel: blocks of U read transposed are staged from a transposed
+    copy of the pool; C's upper triangle equals the oracle's (double product
+    of the FP32 inputs, expanded symmetric matrix) bit-exactly on integers and
+    within 1e-5 relative Frobenius on uniform values."""
+    rng = np.random.default_rng(700 + nbr + (kind == "int"))
+    Um = _sym_upper_f32(rng, nbr, p, kind, leaf)
+    C, st = mk(qt, ctx, Um).symm_square()
+    got = C.to_blocks()
+    ref = oracle.symm_square(nbr, 32, ref64(Um))
+    check(got, ref, kind)
+    L, _ = oracle.tree_levels(Um.n, 32, leaf)
+    assert st.block_products == oracle.level_task_counts_sym(L, (Um.brow, Um.bcol))[-1]
+
+
+def test_fp32_symm_square_cfg5_small(qt, ctx):
+    c = qtgen.config(5, P=1, small=True, symmetric=True)
+    full = f32(c["A"])
+    U = qtgen.upper(full)
+    C, _ = mk(qt, ctx, U).symm_square()
+    got = C.to_blocks()
+    ref = oracle.symm_square(full.nbr, 32, ref64(U))
+    check(got, ref, "uniform")

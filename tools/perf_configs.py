@@ -171,6 +171,10 @@ def main():
                               "max_abs_err": float(np.abs(d).max())}), flush=True)
         elif w == "sym2":
             run_sym(ctx, stream, "cfg2 banded symmetric: symm_square vs full", qtgen.config(2, symmetric=True)["A"])
+        elif w == "sym5f32":
+            M = qtgen.config(5, P=1, symmetric=True)["A"]
+            run_sym(ctx, stream, "cfg5 banded symmetric FP32: symm_square vs full",
+                    qtgen.BlockMatrix(M.n, M.leaf_dim, 32, M.brow, M.bcol, M.vals.astype(np.float32)))
         elif w == "sym4":
             run_sym(ctx, stream, "cfg4 ES-like symmetric (S^2): symm_square vs full",
                     qtgen.config(4, symmetric=True)["A"], steps=5)
