@@ -331,6 +331,8 @@ def main():
                                         "= 148 SM x 64 FMA x 2 x 1.965 GHz",
                          "ms_numeric": round(ms_num, 4), "ms_symbolic": round(ms_sym, 4),
                          "ms_exchange": round(ms_exch, 4),
+                         "ms_payload_overlapped": round(statistics.mean(s.ms_payload for s in stats), 4),
+                         "tiles_overlapped_after": [int(stats[-1].tiles_overlapped), int(stats[-1].tiles_after)],
                          "numeric_share": round(ms_num / ms_max, 4)},
             "bytes_recv_per_gpu": {"max": int(recv_all.max()), "avg": float(recv_all.mean()),
                                    "min": int(recv_all.min()), "unit": "bytes (FP64 payload)",

@@ -78,6 +78,12 @@ typedef struct {
   float ms_symbolic;         /* device time of the symbolic BFS (a5-a7) */
   float ms_numeric;          /* device time of the numeric kernel (a8) */
   float ms_total;            /* device time of the whole call */
+  /* multi-rank overlap (world > 1, on unless QT_OVERLAP=0): the payload is
+   * exchanged on a second stream while the symbolic pass and the C tiles
+   * that read only local B blocks run; the other tiles follow it */
+  int64_t tiles_overlapped;  /* numeric tiles run while the payload was in flight */
+  int64_t tiles_after;       /* numeric tiles launched behind the payload */
+  float ms_payload;          /* device time of the payload transfer (comm stream) */
 } qt_stats;
 
 /* ------------------------------------------------------------------ context */

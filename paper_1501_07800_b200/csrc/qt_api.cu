@@ -237,6 +237,11 @@ qt_status qt_ctx_destroy(qt_ctx ctx) {
     cudaStreamDestroy(ctx->h2d_stream);
     cudaEventDestroy(ctx->h2d_done);
   }
+  if (ctx->comm_stream) {
+    cudaStreamSynchronize(ctx->comm_stream);
+    cudaStreamDestroy(ctx->comm_stream);
+    for (auto& e : ctx->ov_ev) cudaEventDestroy(e);
+  }
   if (ctx->world > 1) dist_finalize(ctx);
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   ctx->scratch.release();

@@ -112,6 +112,12 @@ struct Transport {
   virtual void send(const void* buf, size_t bytes, int peer) = 0;
   virtual void recv(void* buf, size_t bytes, int peer) = 0;
   virtual void group_end() = 0;
+  // stream the following send/recv groups are ordered on (null: the ctx stream)
+  void set_stream(cudaStream_t s) { cur_ = s; }
+  cudaStream_t cur(qt_ctx ctx) const { return cur_ ? cur_ : ctx->stream; }
+
+ protected:
+  cudaStream_t cur_ = nullptr;
 };
 
 struct NcclTransport : Transport {
@@ -137,10 +143,10 @@ struct NcclTransport : Transport {
   }
   void group_start() override { NCCL_CALL(nccl().GroupStart()); }
   void send(const void* buf, size_t bytes, int peer) override {
-    NCCL_CALL(nccl().Send(buf, bytes, ncclInt8, peer, comm, ctx->stream));
+    NCCL_CALL(nccl().Send(buf, bytes, ncclInt8, peer, comm, cur(ctx)));
   }
   void recv(void* buf, size_t bytes, int peer) override {
-    NCCL_CALL(nccl().Recv(buf, bytes, ncclInt8, peer, comm, ctx->stream));
+    NCCL_CALL(nccl().Recv(buf, bytes, ncclInt8, peer, comm, cur(ctx)));
   }
   void group_end() override { NCCL_CALL(nccl().GroupEnd()); }
 };
@@ -203,7 +209,7 @@ struct LoopTransport : Transport {
     m->bytes = bytes;
     QT_CUDA(cudaEventCreateWithFlags(&m->ready, cudaEventDisableTiming));
     QT_CUDA(cudaEventCreateWithFlags(&m->done, cudaEventDisableTiming));
-    QT_CUDA(cudaEventRecord(m->ready, ctx->stream));
+    QT_CUDA(cudaEventRecord(m->ready, cur(ctx)));
     {
       std::lock_guard<std::mutex> lk(hub->mu);
       hub->q[(size_t)ctx->rank * hub->P + peer].push_back(m);
@@ -226,9 +232,9 @@ struct LoopTransport : Transport {
       if (m->bytes != bytes)
         fail(QT_ESTATE, "loopback size mismatch: rank %d expects %zu bytes from %d, got %zu",
              ctx->rank, bytes, peer, m->bytes);
-      QT_CUDA(cudaStreamWaitEvent(ctx->stream, m->ready, 0));
-      QT_CUDA(cudaMemcpyAsync(buf, m->src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
-      QT_CUDA(cudaEventRecord(m->done, ctx->stream));
+      QT_CUDA(cudaStreamWaitEvent(cur(ctx), m->ready, 0));
+      QT_CUDA(cudaMemcpyAsync(buf, m->src, bytes, cudaMemcpyDeviceToDevice, cur(ctx)));
+      QT_CUDA(cudaEventRecord(m->done, cur(ctx)));
       {
         std::lock_guard<std::mutex> lk(hub->mu);
         m->copied = true;
@@ -242,9 +248,9 @@ struct LoopTransport : Transport {
         std::unique_lock<std::mutex> lk(hub->mu);
         hub->cv.wait(lk, [&] { return m->copied; });
       }
-      QT_CUDA(cudaStreamWaitEvent(ctx->stream, m->done, 0));
+      QT_CUDA(cudaStreamWaitEvent(cur(ctx), m->done, 0));
     }
-    QT_CUDA(cudaStreamSynchronize(ctx->stream));
+    QT_CUDA(cudaStreamSynchronize(cur(ctx)));
     for (auto& m : posted) {
       cudaEventDestroy(m->ready);
       cudaEventDestroy(m->done);
@@ -372,6 +378,34 @@ __global__ void k_iota(int32_t* __restrict__ out, int64_t n) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x)
     out[t] = (int32_t)t;
+}
+
+// one warp per tile: local[t] = 0 if a task of tile t reads a received B
+// block (block id >= split), through the B node's children (and, for tiles
+// at level L-2, its children's children), else 1; ids[t] = t
+__global__ void k_tile_local(const int32_t* __restrict__ ts, const int32_t* __restrict__ pb, int64_t ntiles,
+                             const int4* __restrict__ cbt, const int4* __restrict__ cb1, int64_t split,
+                             uint8_t* __restrict__ local, int32_t* __restrict__ ids) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  if (t >= ntiles) return;
+  auto far = [&](int4 c) { return c.x >= split || c.y >= split || c.z >= split || c.w >= split; };
+  bool rem = false;
+  for (int32_t p = ts[t] + lane; p < ts[t + 1] && !rem; p += 32) {
+    const int4 c = cbt[pb[p]];
+    if (!cb1) {
+      rem = far(c);
+    } else {
+      const int n[4] = {c.x, c.y, c.z, c.w};
+      for (int i = 0; i < 4; ++i)
+        if (n[i] >= 0 && far(cb1[n[i]])) rem = true;
+    }
+  }
+  rem = __any_sync(0xffffffffu, rem);
+  if (lane == 0) {
+    local[t] = rem ? 0 : 1;
+    ids[t] = (int32_t)t;
+  }
 }
 
 template <class T>
@@ -571,14 +605,56 @@ void fill_exchange_stats(qt_stats* S, const Received& rx, size_t block_bytes) {
   S->bytes_sent_meta = 4ll * rx.nrows;
 }
 
-qt_mat finish_multiply(qt_mat A_local, qt_mat Bx, qt_stats* S) {
+}  // namespace
+
+void split_tiles(qt_ctx ctx, int64_t ntiles, const int32_t* ts, const int32_t* pb, const int4* childB_t,
+                 const int4* childB_1, int64_t splitB, int32_t* map, int32_t* nsel) {
+  cudaStream_t st = ctx->stream;
+  if (ntiles <= 0) return;
+  DevBuf local(ntiles, st), ids(4 * ntiles, st);
+  const unsigned gw = (unsigned)((ntiles + 7) / 8);  // 8 warps per 256-thread CTA
+  k_tile_local<<<gw, 256, 0, st>>>(ts, pb, ntiles, childB_t, childB_1, splitB, local.as<uint8_t>(),
+                                   ids.as<int32_t>());
+  QT_LAUNCH_CHECK(ctx);
+  // selected (local) tiles first in order, the rest after them (reversed)
+  size_t tb = 0;
+  QT_CUDA(cub::DevicePartition::Flagged(nullptr, tb, ids.as<int32_t>(), local.as<uint8_t>(), map, nsel,
+                                        (int)ntiles, st));
+  void* tmp = scratch(ctx, tb);
+  QT_CUDA(cub::DevicePartition::Flagged(tmp, tb, ids.as<int32_t>(), local.as<uint8_t>(), map, nsel,
+                                        (int)ntiles, st));
+  ctx->launches += 2;
+}
+
+namespace {
+qt_mat finish_multiply(qt_mat A_local, qt_mat Bx, qt_stats* S, Overlap* ov) {
   float ms_sym = 0, ms_num = 0;
-  qt_mat C = multiply_local(A_local, Bx, S, &ms_sym, &ms_num);
+  qt_mat C = multiply_local(A_local, Bx, S, &ms_sym, &ms_num, 0, -1.0, ov);
   S->ms_symbolic = ms_sym;
   S->ms_numeric = ms_num;
+  if (ov) {
+    S->tiles_overlapped = ov->tiles_local;
+    S->tiles_after = ov->tiles_remote;
+  }
   return C;
 }
 
+// the overlap is on unless QT_OVERLAP=0
+bool overlap_enabled() {
+  const char* e = getenv("QT_OVERLAP");
+  return !(e && e[0] == '0');
+}
+
+cudaStream_t comm_stream(qt_ctx ctx) {
+  if (!ctx->comm_stream) {
+    QT_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    QT_CUDA(cudaEventCreateWithFlags(&ctx->ov_ev[0], cudaEventDisableTiming));
+    QT_CUDA(cudaEventCreateWithFlags(&ctx->ov_ev[1], cudaEventDisableTiming));
+    QT_CUDA(cudaEventCreate(&ctx->ov_ev[2]));
+    QT_CUDA(cudaEventCreate(&ctx->ov_ev[3]));
+  }
+  return ctx->comm_stream;
+}
 }  // namespace
 
 // ------------------------------------------------------------------ NCCL path
@@ -664,35 +740,67 @@ qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S) {
   rx.cols.alloc(4 * std::max<int64_t>(rx.nblk, 1), st);
   rx.payload.alloc(bb * std::max<int64_t>(rx.nblk, 1), st);
   int64_t sent_payload = 0, sent_meta = 0;
+  // 3a. block columns (ctx stream): B_ext's quadtree and the whole symbolic
+  // multiply need only them
   X->group_start();
   for (int q = 0; q < P; ++q) {
     if (q == g) continue;
     int64_t r0 = in_off[q], r1 = in_off[q + 1];
     int64_t b0 = h_out_offs[r0], b1 = h_out_offs[r1];
+    if (b1 > b0) X->send(d_out_cols.as<int32_t>() + b0, 4 * (b1 - b0), q);
+    sent_meta += 4 * (r1 - r0) + 4 * (b1 - b0);
+    int64_t i0 = h_in_offs[seg_off[q]], i1 = h_in_offs[seg_off[q] + my_counts[q]];
+    if (i1 > i0) X->recv(rx.cols.as<int32_t>() + i0, 4 * (i1 - i0), q);
+  }
+  X->group_end();
+  // 3b. values: on the comm stream (behind the packing) when overlapped, so
+  // the symbolic pass and the local-only tiles run while they are in flight
+  const bool ovl = overlap_enabled();
+  cudaStream_t s2 = ovl ? comm_stream(ctx) : st;
+  if (ovl) {
+    QT_CUDA(cudaEventRecord(ctx->ov_ev[0], st));
+    QT_CUDA(cudaStreamWaitEvent(s2, ctx->ov_ev[0], 0));
+    QT_CUDA(cudaEventRecord(ctx->ov_ev[2], s2));
+    X->set_stream(s2);
+  }
+  X->group_start();
+  for (int q = 0; q < P; ++q) {
+    if (q == g) continue;
+    int64_t b0 = h_out_offs[in_off[q]], b1 = h_out_offs[in_off[q + 1]];
     if (b1 > b0) {
-      X->send(d_out_cols.as<int32_t>() + b0, 4 * (b1 - b0), q);
       X->send((char*)d_out_pay.p + b0 * bb, (b1 - b0) * bb, q);
       sent_payload += (b1 - b0) * bb;
     }
-    sent_meta += 4 * (r1 - r0) + 4 * (b1 - b0);
     int64_t i0 = h_in_offs[seg_off[q]], i1 = h_in_offs[seg_off[q] + my_counts[q]];
-    if (i1 > i0) {
-      X->recv(rx.cols.as<int32_t>() + i0, 4 * (i1 - i0), q);
-      X->recv((char*)rx.payload.p + i0 * bb, (i1 - i0) * bb, q);
-    }
+    if (i1 > i0) X->recv((char*)rx.payload.p + i0 * bb, (i1 - i0) * bb, q);
   }
   X->group_end();
+  if (ovl) {
+    X->set_stream(nullptr);
+    QT_CUDA(cudaEventRecord(ctx->ov_ev[3], s2));
+  }
   qt_mat Bx = make_b_ext(B, rx);
   QT_CUDA(cudaEventRecord(ctx->ev[6], st));
   fill_exchange_stats(S, rx, bb);
   S->bytes_sent_payload = sent_payload;
   S->bytes_sent_meta += sent_meta;
   qt_mat C;
+  Overlap ov;
+  ov.s2 = s2;
   try {
-    C = finish_multiply(A, Bx, S);
+    C = finish_multiply(A, Bx, S, ovl ? &ov : nullptr);
   } catch (...) {
+    if (ovl) cudaStreamSynchronize(s2);
     delete Bx;
     throw;
+  }
+  if (ovl) {
+    // the send/receive buffers go back to the ctx stream's cache: join s2 first
+    QT_CUDA(cudaStreamWaitEvent(st, ctx->ov_ev[3], 0));
+    if (!ctx->async_multiply) {
+      QT_CUDA(cudaEventSynchronize(ctx->ov_ev[3]));
+      QT_CUDA(cudaEventElapsedTime(&S->ms_payload, ctx->ov_ev[2], ctx->ov_ev[3]));
+    }
   }
   delete Bx;
   QT_CUDA(cudaEventElapsedTime(&S->ms_exchange, ctx->ev[5], ctx->ev[6]));
@@ -810,7 +918,11 @@ qt_mat multiply_virtual(qt_mat A, qt_mat B, const int32_t* bounds, int P, int g,
     Bx = make_b_ext(Bl, rx);
     QT_CUDA(cudaEventRecord(ctx->ev[6], st));
     fill_exchange_stats(S, rx, bb);
-    C = finish_multiply(Al, Bx, S);
+    // the two-phase numeric launch of the NCCL path (here the payload is
+    // already in place: the phases' split and stream ordering are what runs)
+    Overlap ov;
+    if (overlap_enabled()) ov.s2 = comm_stream(ctx);
+    C = finish_multiply(Al, Bx, S, ov.s2 ? &ov : nullptr);
     QT_CUDA(cudaEventElapsedTime(&S->ms_exchange, ctx->ev[5], ctx->ev[6]));
     C->row_lo = lo;
     C->row_hi = hi;

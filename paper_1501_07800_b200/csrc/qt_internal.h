@@ -117,6 +117,8 @@ struct qt_ctx_s {
   cudaStream_t copy_stream = nullptr;  // device-to-host copies of qt_read_back_async
   cudaStream_t h2d_stream = nullptr;   // host-to-device value copies of qt_create
   cudaEvent_t h2d_done = nullptr;
+  cudaStream_t comm_stream = nullptr;  // multi-rank: payload exchange + the remote tiles' numeric launch
+  cudaEvent_t ov_ev[4] = {};           // overlap ordering (0, 1) and payload timing (2, 3)
   bool async_multiply = false;         // qt_multiply_async: no final synchronisation
   struct PendingCopy {
     cudaEvent_t done;
@@ -201,8 +203,25 @@ qt_mat select_blocks(qt_mat A, const uint8_t* d_keep);
 // trans: bit 0 = op(A) = A^T, bit 1 = op(B) = B^T  (C = op(A) op(B)),
 // bit 2 = symmetric square, bits 8+ = its pruning depth.  tau >= 0: norm
 // screening (block products with ||A_ik||*||B_kj|| < tau are skipped).
+// Multi-rank overlap of the payload exchange with the numeric kernel
+// (SURVEY §8(a) a4, §8(e)): when B is a B_ext with received blocks (ids >=
+// B->split), the C tiles whose products read only local B blocks run on the
+// ctx stream while the payload is still in flight; the other tiles are
+// launched on `s2` behind the exchange (whatever was enqueued on s2 before the
+// call) and the ctx stream joins s2 at the end.
+struct Overlap {
+  cudaStream_t s2 = nullptr;
+  int64_t tiles_local = 0, tiles_remote = 0;  // out: C tiles per phase
+};
 qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* st, float* ms_sym, float* ms_num, int trans = 0,
-                      double tau = -1.0);
+                      double tau = -1.0, Overlap* ov = nullptr);
+// Tiles (C nodes of one level with CSR task ranges `ts` over the task array
+// pb) partitioned on the device: map[0, *nsel) = the tiles whose B nodes hold
+// only block ids < splitB (Morton order), map[*nsel, ntiles) = the rest.
+// childB_t: B's child table at the tiles' level; childB_1: B's level L-1 table
+// when the tiles sit at level L-2 (FP32), else null.  No host sync.
+void split_tiles(qt_ctx ctx, int64_t ntiles, const int32_t* ts, const int32_t* pb, const int4* childB_t,
+                 const int4* childB_1, int64_t splitB, int32_t* map, int32_t* nsel);
 // squared Frobenius norms of every quadtree node (levels 0..L) into M->norm2
 void ensure_norms(qt_mat M);
 
@@ -227,6 +246,12 @@ struct NumericArgs {
   const double* normA = nullptr;  // block squared norms (screening) or null
   const double* normB = nullptr;
   double tau2 = 0.0;
+  cudaStream_t stream = nullptr;  // launch stream (null: the ctx stream)
+  // overlap phases (split_tiles): phase 1 = tiles map[0, *nsel), phase 2 =
+  // map[*nsel, ntiles); 0 = all tiles in order (tile_map unused).  group == 1.
+  int phase = 0;
+  const int32_t* tile_map = nullptr;
+  const int32_t* nsel = nullptr;
 };
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a);
 void launch_transpose_blocks(qt_ctx ctx, const void* in, void* out, int64_t nb);
@@ -253,6 +278,10 @@ struct NumericArgs32 {
   int* counter;
   int trans = 0;             // bit 0: A transposed, bit 1: B transposed, bit 2: symmetric square
   const void* poolT = nullptr;  // symmetric square: transposed copy of poolA (= poolB)
+  cudaStream_t stream = nullptr;  // launch stream (null: the ctx stream)
+  int phase = 0;                   // overlap phases, as in NumericArgs
+  const int32_t* tile_map = nullptr;
+  const int32_t* nsel = nullptr;
 };
 void launch_numeric_f32(qt_ctx ctx, const NumericArgs32& a);
 void launch_fp64_peak(qt_ctx ctx, int kind, int iters, int grid);

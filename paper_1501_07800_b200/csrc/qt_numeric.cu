@@ -282,7 +282,15 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
     // (late enough to keep the dynamic balance of the tail).
     constexpr int kGrabAhead = 8;
     const int G = a.group;
-    const int ntiles = (int)a.ntiles;
+    // phase launches of the multi-rank overlap: work items map[t_off + i]
+    int ntiles = (int)a.ntiles, t_off = 0;
+    if (a.phase) {
+      const int ns = *a.nsel;
+      const int nt = a.split ? (int)a.ntiles / 4 : (int)a.ntiles;
+      t_off = a.phase == 1 ? 0 : ns;
+      ntiles = (a.phase == 1 ? ns : nt - ns) * (a.split ? 4 : 1);
+    }
+    auto tile_of = [&](int i) { return a.tile_map ? a.tile_map[t_off + i] : i; };
     // current group: tiles [g_t0, g_t0+g_n), lane l: task start of tile g_t0+l (lane g_n: end), C children
     int g_n = 0, g_ts = 0, g_pend = 0;
     int4 g_cc = make_int4(-1, -1, -1, -1);
@@ -308,7 +316,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
           }
           n_valid = true;
           if (a.split) {  // item = (tile, C child q): one product slot of the tile
-            const int tile = n_t0 >> 2, q = n_t0 & 3;
+            const int tile = tile_of(n_t0 >> 2), q = n_t0 & 3;
             n_n = 1;
             n_keep = 1 << q;
             n_ts = lane <= 1 ? a.tile_start[tile + lane] : 0;
@@ -322,9 +330,10 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
             }
             n_cc = c;
           } else {
-            n_n = min(G, ntiles - n_t0);
-            n_ts = lane <= n_n ? a.tile_start[n_t0 + lane] : 0;
-            n_cc = lane < n_n ? a.childC[n_t0 + lane] : make_int4(-1, -1, -1, -1);
+            n_n = min(G, ntiles - n_t0);  // (G == 1 with a tile map)
+            const int t0 = tile_of(n_t0);
+            n_ts = lane <= n_n ? a.tile_start[t0 + lane] : 0;
+            n_cc = lane < n_n ? a.childC[t0 + lane] : make_int4(-1, -1, -1, -1);
           }
           n_state = 2;
           break;
@@ -621,12 +630,12 @@ static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
     attr_set = true;
   }
-  k_numeric_f64<TA, TB, SYM, SCR><<<grid, kNumThreads, kSmemBytes, ctx->stream>>>(a);
+  k_numeric_f64<TA, TB, SYM, SCR><<<grid, kNumThreads, kSmemBytes, a.stream ? a.stream : ctx->stream>>>(a);
 }
 
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
   if (dt != QT_F64) fail(QT_EDTYPE, "launch_numeric is the FP64 kernel");
-  QT_CUDA(cudaMemsetAsync(a0.counter, 0, sizeof(int), ctx->stream));
+  QT_CUDA(cudaMemsetAsync(a0.counter, 0, sizeof(int), a0.stream ? a0.stream : ctx->stream));
   // Few tiles (fewer than half the tile streams of the GPU): every C block of
   // a tile becomes its own work item, so more streams share the work — a lone
   // stream per SM is latency bound (its 9-slot ring covers ~2 steps of TMA

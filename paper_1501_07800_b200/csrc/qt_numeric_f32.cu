@@ -250,11 +250,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
     const float* zeros = static_cast<const float*>(a.zeros);
     int stage = 0;
     uint32_t phase = 0;
+    // phase launches of the multi-rank overlap: tiles map[t_off + i]
+    int ntiles = (int)a.ntiles, t_off = 0;
+    if (a.phase) {
+      const int ns = *a.nsel;
+      t_off = a.phase == 1 ? 0 : ns;
+      ntiles = a.phase == 1 ? ns : (int)a.ntiles - ns;
+    }
     for (;;) {
       int t = 0;
       if (lane == 0) t = atomicAdd(a.counter, 1);
       t = __shfl_sync(0xffffffffu, t, 0);
-      if (t >= a.ntiles) {
+      if (t >= ntiles) {
         mbar_wait(&S.empty[stage], phase ^ 1);
         if (lane == 0) {
           S.hdr[stage].tile = -1;
@@ -263,6 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
         }
         break;
       }
+      if (a.tile_map) t = a.tile_map[t_off + t];
       const int p0 = a.tile_start[t], p1 = a.tile_start[t + 1];
       bool first = true;
       for (int pb0 = p0; pb0 < p1; pb0 += 32) {
@@ -655,11 +663,11 @@ static void launch_f32_t(qt_ctx ctx, const NumericArgs32& a, int grid) {
                                  (int)kSmemBytes));
     attr_set = true;
   }
-  k_numeric_f32<TA, TB, SYM><<<grid, kThreads, kSmemBytes, ctx->stream>>>(a);
+  k_numeric_f32<TA, TB, SYM><<<grid, kThreads, kSmemBytes, a.stream ? a.stream : ctx->stream>>>(a);
 }
 
 void launch_numeric_f32(qt_ctx ctx, const NumericArgs32& a) {
-  QT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), ctx->stream));
+  QT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), a.stream ? a.stream : ctx->stream));
   const int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
   if (a.trans & 4) {  // symmetric square
     launch_f32_t<false, false, true>(ctx, a, grid);

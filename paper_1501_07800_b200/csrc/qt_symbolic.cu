@@ -569,7 +569,7 @@ struct Trace {
 };
 
 qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* ms_num, int trans,
-                      double tau) {
+                      double tau, Overlap* ov) {
   const bool screen = tau >= 0.0;
   const double tau2 = tau * tau;
   if (screen) {
@@ -808,6 +808,40 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       C->nb = ns[L];
       C->pool.alloc((size_t)C->nb * 1024 * elem_size(C->dtype), st);
       tr.mark("c_alloc");
+      // tiles per scheduler grab (FP64): ~32 tasks per grab, at most 16 tiles
+      int group = 1;
+      {
+        const int64_t per_tile = std::max<int64_t>(1, F[L - 1] / std::max<int32_t>(1, ns[L - 1]));
+        // (tiles with >= 8 tasks stream well one at a time: grouping only costs balance)
+        int64_t g = per_tile >= 8 ? 1 : std::min<int64_t>(16, 32 / per_tile);
+        // keep >= 8 grabs per tile stream (2 per CTA, one CTA per SM)
+        g = std::min<int64_t>(g, ns[L - 1] / (16ll * ctx->num_sms));
+        group = (int)std::max<int64_t>(1, g);
+        if (tr.on) {
+          char b[64];
+          snprintf(b, sizeof b, "group=%d", group);
+          tr.mark(b);
+        }
+      }
+      // multi-rank overlap: the tiles that read only local B blocks run while
+      // the payload is in flight, the rest behind it on ov->s2.  Partitioned
+      // on the device (no host sync); FP64 only with one tile per grab (the
+      // grouped grabs of sparse patterns need contiguous task ranges).
+      const bool two_phase = ov && ov->s2 && B->pool2 && B->split < B->nb && C->nb > 0 && (f32 || group == 1);
+      DevBuf tmap, tnsel;
+      int64_t n_all = 0;
+      if (two_phase) {
+        n_all = f32 ? ns[L - 2] : ns[L - 1];
+        tmap.alloc(4 * n_all, st);
+        tnsel.alloc(4, st);
+        if (f32)
+          split_tiles(ctx, n_all, t2_cstart.as<int32_t>(), t2_pb.as<int32_t>(), B->child[L - 2].as<int4>(),
+                      B->child[L - 1].as<int4>(), B->split, tmap.as<int32_t>(), tnsel.as<int32_t>());
+        else
+          split_tiles(ctx, n_all, cstart.as<int32_t>(), pb.as<int32_t>(), B->child[L - 1].as<int4>(), nullptr,
+                      B->split, tmap.as<int32_t>(), tnsel.as<int32_t>());
+        tr.mark("tile_split");
+      }
       QT_CUDA(cudaEventRecord(ctx->ev[3], st));
       NumericArgs na;
       na.ntiles = ns[L - 1];
@@ -827,20 +861,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       na.normA = screen ? A->norm2[L].as<double>() : nullptr;
       na.normB = screen ? B->norm2[L].as<double>() : nullptr;
       na.tau2 = tau2;
-      // tiles per scheduler grab: ~32 tasks per grab, at most 16 tiles
-      {
-        const int64_t per_tile = std::max<int64_t>(1, F[L - 1] / std::max<int32_t>(1, ns[L - 1]));
-        // (tiles with >= 8 tasks stream well one at a time: grouping only costs balance)
-        int64_t g = per_tile >= 8 ? 1 : std::min<int64_t>(16, 32 / per_tile);
-        // keep >= 8 grabs per tile stream (2 per CTA, one CTA per SM)
-        g = std::min<int64_t>(g, ns[L - 1] / (16ll * ctx->num_sms));
-        na.group = (int)std::max<int64_t>(1, g);
-        if (tr.on) {
-          char b[64];
-          snprintf(b, sizeof b, "group=%d", na.group);
-          tr.mark(b);
-        }
-      }
+      na.group = group;
       DevBuf poolT;  // symmetric square: blocks of U read transposed come from U^T's copy
       if (C->nb > 0 && sym) {
         poolT.alloc((size_t)A->nb * 1024 * elem_size(C->dtype), st);
@@ -850,7 +871,31 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
           launch_transpose_blocks(ctx, A->pool_ptr(), poolT.p, A->nb);
         na.poolT = poolT.p;
       }
-      if (C->nb > 0 && !f32) launch_numeric(ctx, C->dtype, na);
+      // phase launches: the local-only tiles on the ctx stream now, the rest
+      // on ov->s2 behind the payload; the ctx stream joins s2 afterwards.
+      // Phase 2's CTAs take over the SMs as phase 1's finish.
+      auto phases = [&](auto args, auto launch) {
+        args.tile_map = tmap.as<int32_t>();
+        args.nsel = tnsel.as<int32_t>();
+        QT_CUDA(cudaEventRecord(ctx->ov_ev[0], st));
+        auto a1 = args;
+        a1.phase = 1;
+        launch(a1);
+        QT_CUDA(cudaStreamWaitEvent(ov->s2, ctx->ov_ev[0], 0));
+        auto a2 = args;
+        a2.phase = 2;
+        a2.counter = ctx->counters.as<int>() + 17;
+        a2.stream = ov->s2;
+        launch(a2);
+        QT_CUDA(cudaEventRecord(ctx->ov_ev[1], ov->s2));
+        QT_CUDA(cudaStreamWaitEvent(st, ctx->ov_ev[1], 0));
+      };
+      if (C->nb > 0 && !f32) {
+        if (two_phase)
+          phases(na, [&](const NumericArgs& x) { launch_numeric(ctx, C->dtype, x); });
+        else
+          launch_numeric(ctx, C->dtype, na);
+      }
       if (C->nb > 0 && f32) {
         NumericArgs32 nb;
         nb.ntiles = ns[L - 2];
@@ -872,13 +917,23 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         nb.counter = ctx->counters.as<int>() + 16;
         nb.trans = trans & 7;
         nb.poolT = poolT.p;
-        launch_numeric_f32(ctx, nb);
+        if (two_phase)
+          phases(nb, [&](const NumericArgs32& x) { launch_numeric_f32(ctx, x); });
+        else
+          launch_numeric_f32(ctx, nb);
       }
       QT_CUDA(cudaEventRecord(ctx->ev[4], st));
       tr.mark("numeric_launched");
       // (the frontier buffers go back to this stream's cache: stream-ordered reuse)
       if (!ctx->async_multiply) QT_CUDA(cudaEventSynchronize(ctx->ev[4]));
       tr.mark("numeric_done");
+      if (two_phase && !ctx->async_multiply) {
+        int32_t h = 0;
+        QT_CUDA(cudaMemcpyAsync(&h, tnsel.p, 4, cudaMemcpyDeviceToHost, st));
+        QT_CUDA(cudaStreamSynchronize(st));
+        ov->tiles_local = h;
+        ov->tiles_remote = n_all - h;
+      }
     }
     if (!ctx->async_multiply) {
       QT_CUDA(cudaEventSynchronize(ctx->ev[4]));

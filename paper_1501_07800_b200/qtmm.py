@@ -46,6 +46,9 @@ class Stats(ctypes.Structure):
         ("ms_symbolic", ctypes.c_float),
         ("ms_numeric", ctypes.c_float),
         ("ms_total", ctypes.c_float),
+        ("tiles_overlapped", ctypes.c_int64),
+        ("tiles_after", ctypes.c_int64),
+        ("ms_payload", ctypes.c_float),
     ]
 
     def as_dict(self) -> dict:

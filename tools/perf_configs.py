@@ -82,6 +82,36 @@ def run(ctx, stream, name, c, steps=20):
     return out
 
 
+def run_virtual(ctx, stream, name, M, P, ranks, steps=10):
+    """Rank g of a P-rank multiply on one GPU (virtual ranks): numeric time with
+    the exchange overlap on (two launches: local-only tiles, then the tiles
+    behind the payload) and off (one launch).  The difference is what the
+    split costs; the payload time it can hide is only measurable with P GPUs."""
+    A = qtmm.Matrix.from_blocks(ctx, M.n, M.leaf_dim, 32, M.brow, M.bcol, M.vals)
+    bounds = [g * (M.nbr // P) for g in range(P)] + [M.nbr]
+    for g in ranks:
+        out = {"config": name, "P": P, "rank": g}
+        for ov in ("0", "1"):
+            os.environ["QT_OVERLAP"] = ov
+            for _ in range(2):
+                C, st = A.multiply_virtual(A, P, g, bounds)
+                C.close()
+            sts = []
+            for _ in range(steps):
+                C, st = A.multiply_virtual(A, P, g, bounds)
+                sts.append(st)
+                C.close()
+            num = statistics.median(s.ms_numeric for s in sts)
+            out["overlap_" + ov] = {"ms_numeric": round(num, 4),
+                                    "ms_symbolic": round(statistics.median(s.ms_symbolic for s in sts), 4),
+                                    "tflops_numeric": round(st.block_products * FLOP / num / 1e9, 2),
+                                    "tiles_overlapped": st.tiles_overlapped, "tiles_after": st.tiles_after}
+        out["block_products"] = st.block_products
+        out["bytes_recv_payload"] = st.bytes_recv_payload
+        print(json.dumps(out), flush=True)
+    os.environ.pop("QT_OVERLAP", None)
+
+
 def leaf_sweep(ctx, stream):
     """The paper's leaf benchmark shape (Figs. leafmat_bench_double /
     _single): C = A*B at N = 4096 as ONE leaf, blocks of size bs placed
@@ -210,6 +240,14 @@ def main():
                                   "block_products": st.block_products, "full_products": st0.block_products,
                                   "c_blocks": st.c_blocks, "rel_fro_err_vs_full": (err2 ** 0.5) / float(np.linalg.norm(v0))}),
                       flush=True)
+        elif w == "virt8":
+            run_virtual(ctx, stream, "cfg5 P=8 banded (virtual ranks)", qtgen.config(5, P=8)["A"], 8, [0, 3])
+        elif w == "virt8f32":
+            M = qtgen.config(5, P=8)["A"]
+            run_virtual(ctx, stream, "cfg5 P=8 banded FP32 (virtual ranks)",
+                        qtgen.BlockMatrix(M.n, M.leaf_dim, 32, M.brow, M.bcol, M.vals.astype(np.float32)), 8, [3])
+        elif w == "virt4cfg4":
+            run_virtual(ctx, stream, "cfg4 ES-like P=4 (virtual ranks)", qtgen.config(4)["A"], 4, [1], steps=5)
         elif w == "dense4096":
             br, bc = qtgen.pattern_dense(128)
             v = qtgen.block_values(br, bc, 32, 1)
