@@ -179,9 +179,17 @@ qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_sta
  * child transposed as (1,0); transposed nodes swap and transpose their
  * children) and prunes C nodes below the diagonal at every level; blocks
  * read transposed come from a transposed copy of U's block pool made once
- * per call.  FP64 or FP32 (A's dtype), world == 1 in this build.
- * Errors: QT_EINVAL (a block below the diagonal, or world > 1), QT_ENOMEM,
- * QT_ECUDA. */
+ * per call.  FP64 or FP32 (A's dtype).
+ * Multi-rank (world > 1, block_size 32; collective): each rank passes its
+ * block rows of U (the bounds given at create time) and gets its block rows
+ * of C, upper triangle.  Rank g receives from the others every block of U
+ * that a product of its C rows reads, and no other — the rows and columns its
+ * strip references above it, and the parts (columns >= its first row) of the
+ * rows below it that reach into it (DESIGN reading C-26; bytes in `st`,
+ * oracle.exchange_plan_symm) — and runs the
+ * symmetric-square BFS on its blocks + the received ones, pruned to its rows.
+ * Errors: QT_EINVAL (a block below the diagonal), QT_EBS (world > 1 with
+ * block_size 64), QT_ENOMEM, QT_ECUDA, QT_ENCCL. */
 qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st);
 
 /* Frobenius-norm truncation (reading C-16): remove the longest
@@ -253,6 +261,16 @@ const char* qt_last_error(void);
  * local multiply.  Only the NCCL transfers are replaced by device copies.
  * C holds rank g's block rows of A*B; `st` reports what rank g would receive.
  * Used to test the distributed path on one GPU. */
+/* The multi-rank symmetric square of rank g out of P virtual ranks on this
+ * single (world == 1) context: A is the whole upper-triangular U; rank g's
+ * block rows are [row_bounds[g], row_bounds[g+1]); the blocks it would receive
+ * are selected from U by the rule of qt_symm_square and the same pruned BFS
+ * runs.  C holds rank g's rows of A^2 (upper triangle); `st` reports what
+ * rank g would receive.  block_size 32.  Errors: as qt_multiply_virtual,
+ * QT_EINVAL (a block below the diagonal), QT_EBS (block_size 64). */
+qt_status qt_symm_square_virtual(qt_mat A, int32_t P, int32_t g, const int32_t* row_bounds, qt_mat* C,
+                                 qt_stats* st);
+
 qt_status qt_multiply_virtual(qt_mat A, qt_mat B, int32_t P, int32_t g,
                               const int32_t* row_bounds, qt_mat* C, qt_stats* st);
 

@@ -319,6 +319,49 @@ def exchange_plan(bounds, a_rc, b_rc, block_bytes: int):
     return out
 
 
+def exchange_plan_symm(bounds, u_rc, block_bytes: int):
+    """Per-rank received bytes of the multi-rank symmetric square (DESIGN.md
+    reading C-26; §3.3 P:297-311 for the operation, P:1179-1183 for the
+    paper's measured communication of S^2).  Rank g owns rows [lo, hi) of the
+    upper-triangular storage U and computes C rows [lo, hi), upper triangle.
+    With R_g = the block columns >= hi of g's blocks, g receives every block
+    (r, c) of U outside its strip with
+        r >= hi and (r in R_g or c in R_g), or
+        r <  lo, c >= lo and row r of U has a block in columns [lo, hi).
+    This is exactly the set of other ranks' blocks read by some product
+    A(I,K)·A(K,J), I in [lo, hi), J >= I (A(I,K) = U(I,K) or U(K,I)^T).
+    Metadata received: one int64 key per block, one int32 count per peer, and
+    the int32 lists R_q of the lower ranks q < g (sent to every higher rank)."""
+    bounds = np.asarray(bounds, np.int64)
+    P = len(bounds) - 1
+    nbr = int(bounds[-1])
+    ur = np.asarray(u_rc[0], np.int64)
+    uc = np.asarray(u_rc[1], np.int64)
+    R = []
+    for g in range(P):
+        lo, hi = bounds[g], bounds[g + 1]
+        r = np.unique(uc[(ur >= lo) & (ur < hi)])
+        R.append(r[r >= hi])
+    out = []
+    for g in range(P):
+        lo, hi = bounds[g], bounds[g + 1]
+        strip = (ur >= lo) & (ur < hi)
+        in_r = np.zeros(nbr, bool)
+        in_r[R[g]] = True
+        hit = np.zeros(nbr, bool)
+        hit[ur[(uc >= lo) & (uc < hi)]] = True
+        sel = ~strip & (((ur >= hi) & (in_r[ur] | in_r[uc])) | ((ur < lo) & (uc >= lo) & hit[ur]))
+        n = int(sel.sum())
+        lists_in = int(sum(len(R[q]) for q in range(g)))
+        out.append({
+            "blocks_received": n,
+            "payload_bytes": n * block_bytes,
+            "meta_bytes": 8 * n + 4 * (P - 1) + 4 * lists_in,
+            "selected": np.nonzero(sel)[0],
+        })
+    return out
+
+
 def spsumma_volume(m: float, N: float, p: float) -> float:
     """Elements each process fetches under random permutation + Sparse SUMMA:
     2 m N / sqrt(p) (Eq. eq:sqrtp_equation)."""

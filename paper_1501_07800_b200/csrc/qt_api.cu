@@ -469,7 +469,7 @@ qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
   *C = nullptr;
   qt_ctx ctx = A->ctx;
   QT_CUDA(cudaSetDevice(ctx->device));
-  if (ctx->world > 1) fail(QT_EINVAL, "the symmetric square is single-rank only in this build");
+  if (ctx->world > 1 && A->ubs != 32) fail(QT_EBS, "the multi-rank symmetric square needs block_size 32");
   check_upper(A);
   ensure_levels(A);
   qt_stats local;
@@ -478,7 +478,11 @@ qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
   QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   float ms_sym = 0, ms_num = 0;
   qt_mat R;
-  if (A->ubs == 64) {
+  if (ctx->world > 1) {
+    R = symm_square_dist(A, &S);
+    ms_sym = S.ms_symbolic;
+    ms_num = S.ms_numeric;
+  } else if (A->ubs == 64) {
     // drop the (1,0) 32-sub-block of every diagonal 64-block (it is the
     // transpose of (0,1)); diagonal C 64-blocks are then completed by not
     // pruning at the last (32-block) level
@@ -586,6 +590,36 @@ qt_status qt_nccl_unique_id(void* out128) {
   API_TRY
   if (!out128) fail(QT_EINVAL, "out128 is NULL");
   nccl_unique_id(out128);
+  API_CATCH
+}
+
+qt_status qt_symm_square_virtual(qt_mat A, int32_t P, int32_t g, const int32_t* row_bounds, qt_mat* C,
+                                 qt_stats* st) {
+  API_TRY
+  if (!A || !C || !row_bounds) fail(QT_EINVAL, "NULL argument");
+  *C = nullptr;
+  if (A->ctx->world != 1) fail(QT_ESTATE, "virtual ranks need a single-rank context");
+  if (A->ubs != 32) fail(QT_EBS, "the multi-rank symmetric square needs block_size 32");
+  if (P < 1 || g < 0 || g >= P) fail(QT_EINVAL, "bad P=%d / g=%d", P, g);
+  std::vector<int32_t> b(row_bounds, row_bounds + P + 1);
+  if (b[0] != 0 || b[P] != A->nbr) fail(QT_EINVAL, "row_bounds must span [0,%d]", A->nbr);
+  for (int q = 0; q < P; ++q)
+    if (b[q + 1] < b[q]) fail(QT_EINVAL, "row_bounds not non-decreasing");
+  qt_ctx ctx = A->ctx;
+  QT_CUDA(cudaSetDevice(ctx->device));
+  check_upper(A);
+  qt_stats local;
+  qt_stats& S = st ? *st : local;
+  memset(&S, 0, sizeof(S));
+  QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  qt_mat R = symm_square_virtual(A, b.data(), P, g, &S);
+  QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+  QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
+  QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
+  R->global_nb = user_nblocks(R);
+  R->bounds = b;
+  user_stats(R, S);
+  *C = R;
   API_CATCH
 }
 

@@ -938,6 +938,295 @@ qt_mat multiply_virtual(qt_mat A, qt_mat B, const int32_t* bounds, int P, int g,
   return C;
 }
 
+// ------------------------------------------------------------ symmetric square (multi-rank)
+//
+// Rank g owns block rows [lo, hi) of the upper-triangular storage U and
+// computes C = A^2 for its rows, upper triangle only (reading C-26).
+// A(I,K) for I in the strip is U(I,K) (K >= I, local) or U(K,I)^T (K < I),
+// and A(K,J) for J >= lo is U(K,J) (J >= K) or U(J,K)^T (lo <= J < K).  With
+// R_g = the block columns >= hi of g's blocks, g receives every block (r,c) of
+// another rank with
+//   r >= hi and (r in R_g or c in R_g)       -- rows and columns above the strip
+//   r <  lo, c >= lo and row r has a block in [lo,hi) -- rows reaching into it
+// which is exactly the set of other ranks' blocks that some product of C's
+// strip rows reads (oracle.exchange_plan_symm, pinned in tests/test_oracle.py
+// against a brute-force enumeration of the products).  The symmetric-square BFS
+// then runs on U_ext = local + received blocks, pruned to C rows [lo, hi).
+
+namespace {
+// flag[r] = 1 for every block row r with a block in columns [lo, hi)
+__global__ void k_mark_rowhit(const uint64_t* __restrict__ key, int64_t nb, int32_t lo, int32_t hi,
+                              int32_t* __restrict__ flag) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nb;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = (int32_t)morton_col(key[t]);
+    if (c >= lo && c < hi) flag[morton_row(key[t])] = 1;
+  }
+}
+
+__global__ void k_scatter_list(const int32_t* __restrict__ list, int64_t n, int32_t* __restrict__ flag) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    flag[list[t]] = 1;
+}
+
+// the selection rule above for the strip [lo, hi); blocks inside the strip: keep_strip
+__global__ void k_sym_keep(const uint64_t* __restrict__ key, int64_t nb, int32_t lo, int32_t hi,
+                           const int32_t* __restrict__ inR, const int32_t* __restrict__ rowhit,
+                           uint8_t keep_strip, uint8_t* __restrict__ keep) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nb;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = (int32_t)morton_row(key[t]), c = (int32_t)morton_col(key[t]);
+    uint8_t k;
+    if (r < lo)
+      k = rowhit && rowhit[r] && c >= lo;
+    else if (r >= hi)
+      k = inR && (inR[r] || inR[c]);
+    else
+      k = keep_strip;
+    keep[t] = k;
+  }
+}
+
+// one warp per listed block: its key and values into the packed buffers
+__global__ void k_pack_sel(const int32_t* __restrict__ ids, int64_t n, const uint64_t* __restrict__ key,
+                           const uint4* __restrict__ pool, int vpb, uint64_t* __restrict__ okey,
+                           uint4* __restrict__ opay) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  if (w >= n) return;
+  const int32_t id = ids[w];
+  if (lane == 0) okey[w] = key[id];
+  const uint4* sp = pool + (int64_t)id * vpb;
+  uint4* dp = opay + w * vpb;
+  for (int e = lane; e < vpb; e += 32) dp[e] = sp[e];
+}
+
+// U_ext = U's local blocks + nr received blocks (keys, values): one pool
+qt_mat make_u_ext(qt_mat U, int64_t nr, const uint64_t* rkeys, const void* rpay) {
+  qt_ctx ctx = U->ctx;
+  cudaStream_t st = ctx->stream;
+  const size_t bb = 1024 * elem_size(U->dtype);
+  qt_mat X = clone_shape(U);
+  try {
+    const int64_t nl = U->nb, nt = nl + nr;
+    X->nb = nt;
+    if (nt == 0) {
+      build_levels(X);
+      return X;
+    }
+    DevBuf keys(8 * nt, st), ids(4 * nt, st), sids(4 * nt, st);
+    if (nl > 0) QT_CUDA(cudaMemcpyAsync(keys.p, U->key.p, 8 * nl, cudaMemcpyDeviceToDevice, st));
+    if (nr > 0) QT_CUDA(cudaMemcpyAsync(keys.as<uint64_t>() + nl, rkeys, 8 * nr, cudaMemcpyDeviceToDevice, st));
+    k_iota<<<gfor(nt), kT, 0, st>>>(ids.as<int32_t>(), nt);
+    QT_LAUNCH_CHECK(ctx);
+    X->key.alloc(8 * nt, st);
+    sort_pairs(ctx, keys.as<uint64_t>(), X->key.as<uint64_t>(), ids.as<int32_t>(), sids.as<int32_t>(), nt,
+               2 * X->L);
+    X->pool.alloc(bb * nt, st);
+    if (nl > 0) QT_CUDA(cudaMemcpyAsync(X->pool.p, U->pool_ptr(), bb * nl, cudaMemcpyDeviceToDevice, st));
+    if (nr > 0)
+      QT_CUDA(cudaMemcpyAsync((char*)X->pool.p + bb * nl, rpay, bb * nr, cudaMemcpyDeviceToDevice, st));
+    build_levels(X, sids.as<int32_t>());
+  } catch (...) {
+    delete X;
+    throw;
+  }
+  return X;
+}
+
+qt_mat symm_finish(qt_mat X, int32_t lo, int32_t hi, qt_stats* S) {
+  float ms_sym = 0, ms_num = 0;
+  qt_mat C = multiply_local(X, X, S, &ms_sym, &ms_num, 4 | (X->L << 8), -1.0, nullptr, lo, hi);
+  S->ms_symbolic = ms_sym;
+  S->ms_numeric = ms_num;
+  C->row_lo = lo;
+  C->row_hi = hi;
+  return C;
+}
+
+// |R_q|: distinct block columns >= hi of the blocks in rows [lo, hi)
+int64_t count_requests(qt_mat U, int32_t lo, int32_t hi) {
+  qt_mat Uq = rows_of(U, lo, hi);
+  DevBuf d;
+  int64_t n = 0;
+  try {
+    n = (int64_t)needed_rows(Uq, lo, hi, d).size();
+  } catch (...) {
+    delete Uq;
+    throw;
+  }
+  delete Uq;
+  return n;
+}
+}  // namespace
+
+qt_mat symm_square_dist(qt_mat U, qt_stats* S) {
+  qt_ctx ctx = U->ctx;
+  cudaStream_t st = ctx->stream;
+  const int P = ctx->world, g = ctx->rank;
+  Transport* X = T(ctx);
+  const size_t bb = 1024 * elem_size(U->dtype);
+  const int vpb = (int)(bb / 16);
+  const int32_t lo = U->row_lo, hi = U->row_hi, nbr = U->nbr;
+  const std::vector<int32_t>& b = U->bounds;
+  const int64_t nb = U->nb;
+  QT_CUDA(cudaEventRecord(ctx->ev[5], st));
+  // 0. R_g (every local block has row in the strip) and the list sizes
+  DevBuf d_req;
+  const int64_t nreq = (int64_t)needed_rows(U, lo, hi, d_req).size();
+  std::vector<int64_t> nr_all(P);
+  X->allgather_i64(&nreq, nr_all.data(), 1);
+  // 1. request lists go to the higher ranks (owners of rows >= hi)
+  std::vector<DevBuf> rlist(P);
+  for (int q = 0; q < g; ++q) rlist[q].alloc(4 * std::max<int64_t>(nr_all[q], 1), st);
+  X->group_start();
+  for (int q = 0; q < P; ++q) {
+    if (q > g && nreq > 0) X->send(d_req.p, 4 * nreq, q);
+    if (q < g && nr_all[q] > 0) X->recv(rlist[q].p, 4 * nr_all[q], q);
+  }
+  X->group_end();
+  // 2. owner side: the blocks each other rank needs
+  DevBuf iota(4 * std::max<int64_t>(nb, 1), st), keep(std::max<int64_t>(nb, 1), st),
+      flag(4ll * nbr, st), cnt(4ll * P, st), rcnt(4ll * P, st);
+  QT_CUDA(cudaMemsetAsync(cnt.p, 0, 4ll * P, st));
+  QT_CUDA(cudaMemsetAsync(rcnt.p, 0, 4ll * P, st));
+  if (nb > 0) {
+    k_iota<<<gfor(nb), kT, 0, st>>>(iota.as<int32_t>(), nb);
+    QT_LAUNCH_CHECK(ctx);
+  }
+  std::vector<DevBuf> sel(P);
+  for (int q = 0; q < P && nb > 0; ++q) {
+    if (q == g) continue;
+    QT_CUDA(cudaMemsetAsync(flag.p, 0, 4ll * nbr, st));
+    if (q > g) {  // my rows are below q's strip
+      k_mark_rowhit<<<gfor(nb), kT, 0, st>>>(U->key.as<uint64_t>(), nb, b[q], b[q + 1], flag.as<int32_t>());
+    } else if (nr_all[q] > 0) {  // my rows are above q's strip
+      k_scatter_list<<<gfor(nr_all[q]), kT, 0, st>>>(rlist[q].as<int32_t>(), nr_all[q], flag.as<int32_t>());
+    }
+    QT_LAUNCH_CHECK(ctx);
+    k_sym_keep<<<gfor(nb), kT, 0, st>>>(U->key.as<uint64_t>(), nb, b[q], b[q + 1],
+                                        q < g ? flag.as<int32_t>() : nullptr,
+                                        q > g ? flag.as<int32_t>() : nullptr, 0, keep.as<uint8_t>());
+    QT_LAUNCH_CHECK(ctx);
+    sel[q].alloc(4 * nb, st);
+    size_t tb = 0;
+    QT_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.as<int32_t>(), keep.as<uint8_t>(), sel[q].as<int32_t>(),
+                                       cnt.as<int32_t>() + q, (int)nb, st));
+    void* tmp = scratch(ctx, tb);
+    QT_CUDA(cub::DeviceSelect::Flagged(tmp, tb, iota.as<int32_t>(), keep.as<uint8_t>(), sel[q].as<int32_t>(),
+                                       cnt.as<int32_t>() + q, (int)nb, st));
+    ctx->launches += 2;
+  }
+  // 3. counts
+  X->group_start();
+  for (int q = 0; q < P; ++q) {
+    if (q == g) continue;
+    X->send(cnt.as<int32_t>() + q, 4, q);
+    X->recv(rcnt.as<int32_t>() + q, 4, q);
+  }
+  X->group_end();
+  std::vector<int32_t> out_cnt(P), in_cnt(P);
+  QT_CUDA(cudaMemcpyAsync(out_cnt.data(), cnt.p, 4ll * P, cudaMemcpyDeviceToHost, st));
+  QT_CUDA(cudaMemcpyAsync(in_cnt.data(), rcnt.p, 4ll * P, cudaMemcpyDeviceToHost, st));
+  QT_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> out_off(P + 1, 0), in_off(P + 1, 0);
+  for (int q = 0; q < P; ++q) {
+    out_off[q + 1] = out_off[q] + (q == g ? 0 : out_cnt[q]);
+    in_off[q + 1] = in_off[q] + (q == g ? 0 : in_cnt[q]);
+  }
+  // 4. keys + values
+  const int64_t n_out = out_off[P], n_in = in_off[P];
+  DevBuf okey(8 * std::max<int64_t>(n_out, 1), st), opay(bb * std::max<int64_t>(n_out, 1), st);
+  DevBuf ikey(8 * std::max<int64_t>(n_in, 1), st), ipay(bb * std::max<int64_t>(n_in, 1), st);
+  for (int q = 0; q < P; ++q) {
+    if (q == g || out_cnt[q] == 0) continue;
+    k_pack_sel<<<(unsigned)((out_cnt[q] + 7) / 8), 256, 0, st>>>(
+        sel[q].as<int32_t>(), out_cnt[q], U->key.as<uint64_t>(), static_cast<const uint4*>(U->pool_ptr()), vpb,
+        okey.as<uint64_t>() + out_off[q], opay.as<uint4>() + out_off[q] * vpb);
+    QT_LAUNCH_CHECK(ctx);
+  }
+  X->group_start();
+  for (int q = 0; q < P; ++q) {
+    if (q == g) continue;
+    if (out_cnt[q] > 0) {
+      X->send(okey.as<uint64_t>() + out_off[q], 8ll * out_cnt[q], q);
+      X->send((char*)opay.p + bb * out_off[q], bb * out_cnt[q], q);
+    }
+    if (in_cnt[q] > 0) {
+      X->recv(ikey.as<uint64_t>() + in_off[q], 8ll * in_cnt[q], q);
+      X->recv((char*)ipay.p + bb * in_off[q], bb * in_cnt[q], q);
+    }
+  }
+  X->group_end();
+  qt_mat Ux = make_u_ext(U, n_in, ikey.as<uint64_t>(), ipay.p);
+  QT_CUDA(cudaEventRecord(ctx->ev[6], st));
+  int64_t lists_in = 0;
+  for (int q = 0; q < g; ++q) lists_in += nr_all[q];
+  S->blocks_recv = n_in;
+  S->bytes_recv_payload = n_in * (int64_t)bb;
+  S->bytes_recv_meta = 8 * n_in + 4ll * (P - 1) + 4 * lists_in;
+  S->bytes_sent_payload = n_out * (int64_t)bb;
+  S->bytes_sent_meta = 8 * n_out + 4ll * (P - 1) + 4 * nreq * (P - 1 - g);
+  qt_mat C;
+  try {
+    C = symm_finish(Ux, lo, hi, S);
+  } catch (...) {
+    delete Ux;
+    throw;
+  }
+  delete Ux;
+  QT_CUDA(cudaEventElapsedTime(&S->ms_exchange, ctx->ev[5], ctx->ev[6]));
+  return C;
+}
+
+qt_mat symm_square_virtual(qt_mat U, const int32_t* bounds, int P, int g, qt_stats* S) {
+  qt_ctx ctx = U->ctx;
+  cudaStream_t st = ctx->stream;
+  const size_t bb = 1024 * elem_size(U->dtype);
+  const int32_t lo = bounds[g], hi = bounds[g + 1], nbr = U->nbr;
+  const int64_t nb = U->nb;
+  qt_mat Ul = rows_of(U, lo, hi), Ux = nullptr, C = nullptr;
+  try {
+    QT_CUDA(cudaEventRecord(ctx->ev[5], st));
+    DevBuf d_req;
+    const int64_t nreq = (int64_t)needed_rows(Ul, lo, hi, d_req).size();
+    DevBuf inR(4ll * nbr, st), rowhit(4ll * nbr, st), keep(std::max<int64_t>(nb, 1), st);
+    QT_CUDA(cudaMemsetAsync(inR.p, 0, 4ll * nbr, st));
+    QT_CUDA(cudaMemsetAsync(rowhit.p, 0, 4ll * nbr, st));
+    if (nreq > 0) {
+      k_scatter_list<<<gfor(nreq), kT, 0, st>>>(d_req.as<int32_t>(), nreq, inR.as<int32_t>());
+      QT_LAUNCH_CHECK(ctx);
+    }
+    if (nb > 0) {
+      k_mark_rowhit<<<gfor(nb), kT, 0, st>>>(U->key.as<uint64_t>(), nb, lo, hi, rowhit.as<int32_t>());
+      QT_LAUNCH_CHECK(ctx);
+      k_sym_keep<<<gfor(nb), kT, 0, st>>>(U->key.as<uint64_t>(), nb, lo, hi, inR.as<int32_t>(),
+                                          rowhit.as<int32_t>(), 1, keep.as<uint8_t>());
+      QT_LAUNCH_CHECK(ctx);
+    }
+    Ux = select_blocks(U, keep.as<uint8_t>());
+    ensure_levels(Ux);
+    QT_CUDA(cudaEventRecord(ctx->ev[6], st));
+    int64_t lists_in = 0;
+    for (int q = 0; q < g; ++q) lists_in += count_requests(U, bounds[q], bounds[q + 1]);
+    const int64_t n_in = Ux->nb - Ul->nb;
+    S->blocks_recv = n_in;
+    S->bytes_recv_payload = n_in * (int64_t)bb;
+    S->bytes_recv_meta = 8 * n_in + 4ll * (P - 1) + 4 * lists_in;
+    S->bytes_sent_meta = 4 * nreq * (P - 1 - g);
+    C = symm_finish(Ux, lo, hi, S);
+    QT_CUDA(cudaEventElapsedTime(&S->ms_exchange, ctx->ev[5], ctx->ev[6]));
+  } catch (...) {
+    delete Ul;
+    delete Ux;
+    throw;
+  }
+  delete Ux;
+  delete Ul;
+  return C;
+}
+
 }  // namespace qt
 
 namespace qt {

@@ -213,8 +213,11 @@ struct Overlap {
   cudaStream_t s2 = nullptr;
   int64_t tiles_local = 0, tiles_remote = 0;  // out: C tiles per phase
 };
+// [row_lo, row_hi): only C blocks in these block rows are computed (the BFS
+// prunes C nodes outside the window at every level).
 qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* st, float* ms_sym, float* ms_num, int trans = 0,
-                      double tau = -1.0, Overlap* ov = nullptr);
+                      double tau = -1.0, Overlap* ov = nullptr, int32_t row_lo = 0,
+                      int32_t row_hi = INT32_MAX);
 // Tiles (C nodes of one level with CSR task ranges `ts` over the task array
 // pb) partitioned on the device: map[0, *nsel) = the tiles whose B nodes hold
 // only block ids < splitB (Morton order), map[*nsel, ntiles) = the rest.
@@ -298,5 +301,10 @@ qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* st);
 // the NCCL transfers); A and B are whole matrices on this context.
 qt_mat multiply_virtual(qt_mat A, qt_mat B, const int32_t* bounds, int P, int g, qt_stats* st);
 void allgather_i64(qt_ctx ctx, const int64_t* send_host, int64_t* recv_host, int count);
+// multi-rank symmetric square (32-blocks): U's rows [row_lo, row_hi) on this
+// rank; C = its rows of A^2, upper triangle.  The virtual form runs rank g of P
+// on one device from the whole U.
+qt_mat symm_square_dist(qt_mat U, qt_stats* st);
+qt_mat symm_square_virtual(qt_mat U, const int32_t* bounds, int P, int g, qt_stats* st);
 
 }  // namespace qt

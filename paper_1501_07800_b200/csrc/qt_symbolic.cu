@@ -51,6 +51,24 @@ __device__ __forceinline__ bool on_diagonal(uint64_t ckey) {
   return morton_row(ckey) == morton_col(ckey);
 }
 
+// C children (bit q = child (i,j), q = 2i+j) of C node `ck` at level l that
+// are computed: not the (1,0) child of a diagonal node in the symmetric
+// square's pruned levels, and only children whose block rows meet the row
+// window [rlo, rhi) (a rank's strip in the multi-rank symmetric square)
+__device__ __forceinline__ int cmask(uint64_t ck, int l, int L, bool prune, int32_t rlo, int32_t rhi) {
+  int m = (prune && on_diagonal(ck)) ? 0xB : 0xF;
+  if (rlo > 0 || rhi < INT32_MAX) {
+    const int64_t r = morton_row(ck);
+    const int sh = L - l - 1;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int64_t a0 = (2 * r + i) << sh, a1 = (2 * r + i + 1) << sh;
+      if (a1 <= rlo || a0 >= rhi) m &= i ? ~0xC : ~0x3;
+    }
+  }
+  return m;
+}
+
 // A child (i,k) sits in slot 2i+k, B child (k,j) in slot 2k+j, C child (i,j) in 2i+j.
 // Norm screening (qt_multiply_screened): a child task (a, b) survives iff
 // ||a||^2 * ||b||^2 >= tau^2, squared Frobenius norms of quadtree nodes.  A
@@ -78,7 +96,7 @@ __device__ __forceinline__ void child_counts(int4 a, int4 b, int (&c)[4], const 
 // Write the child tasks of task p (group s, local index loc) at the exclusive
 // offsets `off` of its (s,q) slots; gidx maps (s,q) to the new group index.
 __device__ __forceinline__ void emit_task(int4 a4, int4 b4, int64_t base, int32_t m, int32_t s,
-                                          bool skip_lower, const Screen& sc, bool sym,
+                                          int cm, const Screen& sc, bool sym,
                                           const int32_t* __restrict__ off,
                                           const int32_t* __restrict__ gidx, int32_t* __restrict__ pa2,
                                           int32_t* __restrict__ pb2, int32_t* __restrict__ pc2) {
@@ -86,7 +104,7 @@ __device__ __forceinline__ void emit_task(int4 a4, int4 b4, int64_t base, int32_
   const int b[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    if (skip_lower && q == 2) continue;
+    if (!((cm >> q) & 1)) continue;
     const int i = q >> 1, j = q & 1;
     int32_t pos = -1, newc = -1;
 #pragma unroll
@@ -126,6 +144,7 @@ struct SmallBfsArgs {
   const double* normA[QT_MAX_LEVELS];  // squared node norms per level (screening), or null
   const double* normB[QT_MAX_LEVELS];
   double tau2;
+  int32_t row_lo, row_hi;  // C row window (block rows)
 };
 
 __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) {
@@ -165,7 +184,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
       int c[4];
       child_counts(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym), c,
                    sc, sym);
-      if (prune && on_diagonal(ck[s])) c[2] = 0;
+      const int cm = cmask(ck[s], l, a.L, prune, a.row_lo, a.row_hi);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!((cm >> q) & 1)) c[q] = 0;
       const int64_t base = 4ll * c0 + (p - c0);
 #pragma unroll
       for (int q = 0; q < 4; ++q) a.off[base + (int64_t)q * m] = c[q];
@@ -219,7 +241,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     for (int p = tid; p < F && l + 1 < a.L; p += kSmallThreads) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
       emit_task(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym),
-                4ll * c0 + (p - c0), m, s, prune && on_diagonal(ck[s]), sc, sym, a.off, a.gidx, a.pa[nxt],
+                4ll * c0 + (p - c0), m, s, cmask(ck[s], l, a.L, prune, a.row_lo, a.row_hi), sc, sym, a.off,
+                a.gidx, a.pa[nxt],
                 a.pb[nxt],
                 a.pc[nxt]);
     }
@@ -273,6 +296,7 @@ struct LargeBfsArgs {
   int32_t* ns_out;               // groups per level
   int32_t* f_out;                // tasks per level
   unsigned* bar;                 // grid barrier: arrival count (self-resetting), generation
+  int32_t row_lo, row_hi;        // C row window (block rows)
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -351,7 +375,10 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
     auto counts = [&](int32_t p, int32_t sgrp, int (&c)[4]) {
       child_counts(op_children(cA, pa[p], mode & 1, sym), op_children(cB, pb[p], mode & 2, sym), c, sc,
                    sym);
-      if ((mode & 8) && on_diagonal(ck[sgrp])) c[2] = 0;
+      const int cm = cmask(ck[sgrp], l, a.L, mode & 8, a.row_lo, a.row_hi);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!((cm >> q) & 1)) c[q] = 0;
     };
     // A. child tasks per (s,q).  A group is walked by W lanes (a power of two
     // near half the level's mean group size): random patterns have ~1-task
@@ -476,12 +503,12 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
         const int32_t sg = sg0 + sub;
         const bool live = sg < g_hi;
         int32_t c0 = 0, c1 = 0;
-        bool skip_lower = false;
+        int cm = 0xF;
         int pos[4] = {0, 0, 0, 0}, gq[4] = {-1, -1, -1, -1};
         if (live) {
           c0 = cs[sg];
           c1 = cs[sg + 1];
-          skip_lower = (mode & 8) && on_diagonal(ck[sg]);
+          cm = cmask(ck[sg], l, a.L, mode & 8, a.row_lo, a.row_hi);
           const int4 o4 = *reinterpret_cast<const int4*>(a.slot_off + 4ll * sg);
           const int4 g4 = *reinterpret_cast<const int4*>(gx + 4ll * sg);
           pos[0] = o4.x; pos[1] = o4.y; pos[2] = o4.z; pos[3] = o4.w;
@@ -503,7 +530,7 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int i = q >> 1, j = q & 1;
-            const bool on = !(q == 2 && skip_lower);
+            const bool on = (cm >> q) & 1;
             const bool k0 = on && pair_ok(av[2 * i], bv[j], sc, sym);
             const bool k1 = on && pair_ok(av[2 * i + 1], bv[2 + j], sc, sym);
             const int n = (int)k0 + (int)k1;
@@ -569,7 +596,7 @@ struct Trace {
 };
 
 qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* ms_num, int trans,
-                      double tau, Overlap* ov) {
+                      double tau, Overlap* ov, int32_t row_lo, int32_t row_hi) {
   const bool screen = tau >= 0.0;
   const double tau2 = tau * tau;
   if (screen) {
@@ -665,6 +692,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       sa.L = L;
       sa.trans = trans;
       sa.tau2 = tau2;
+      sa.row_lo = row_lo;
+      sa.row_hi = row_hi;
       for (int l = 0; l <= L && l < QT_MAX_LEVELS; ++l) {
         sa.normA[l] = screen ? A->norm2[l].as<double>() : nullptr;
         sa.normB[l] = screen ? B->norm2[l].as<double>() : nullptr;
@@ -733,6 +762,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         la.L = L;
         la.trans = trans;
         la.tau2 = tau2;
+        la.row_lo = row_lo;
+        la.row_hi = row_hi;
         for (int l = 0; l < L && l < QT_MAX_LEVELS; ++l) {
           la.childA[l] = A->child[l].as<int4>();
           la.childB[l] = B->child[l].as<int4>();

@@ -75,6 +75,7 @@ def _load():
         "qt_symm_square": [P, P, P],
         "qt_multiply_screened": [P, P, ctypes.c_double, P, P],
         "qt_multiply_virtual": [P, P, i32, i32, P, P, P],
+        "qt_symm_square_virtual": [P, i32, i32, P, P, P],
         "qt_truncate": [P, ctypes.c_double, P],
         "qt_info": [P, P, P, P, P, P, P, P, P],
         "qt_level_nodes": [P, P, i32, P],
@@ -102,7 +103,7 @@ _lib = _load()
 EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_nccl_unique_id", "qt_create", "qt_multiply",
             "qt_multiply_async",
             "qt_multiply_ex", "qt_symm_square", "qt_multiply_screened",
-            "qt_multiply_virtual", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
+            "qt_multiply_virtual", "qt_symm_square_virtual", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
             "qt_read_back_async", "qt_ctx_synchronize", "qt_destroy", "qt_last_error", "qt_kernel_launches", "qt_fp64_peak",
             "qt_loopback_hub_create", "qt_loopback_hub_destroy", "qt_ctx_create_loopback")
 
@@ -287,6 +288,14 @@ class Matrix:
         rb = np.ascontiguousarray(np.asarray(row_bounds, dtype=np.int32))
         _check(_lib.qt_multiply_virtual(self._h, other._h, P, g, _ptr(rb), ctypes.byref(h),
                                         ctypes.byref(st)))
+        return Matrix(self.ctx, h), st
+
+    def symm_square_virtual(self, P: int, g: int, row_bounds):
+        """Rank g of the P-rank symmetric square, on one device (self = the whole U)."""
+        st = Stats()
+        h = ctypes.c_void_p()
+        rb = np.ascontiguousarray(np.asarray(row_bounds, dtype=np.int32))
+        _check(_lib.qt_symm_square_virtual(self._h, P, g, _ptr(rb), ctypes.byref(h), ctypes.byref(st)))
         return Matrix(self.ctx, h), st
 
     def truncate(self, tau: float) -> "Matrix":

@@ -553,3 +553,61 @@ def test_screened_zero_tau_is_exact_and_error_bound():
         if prev is not None:
             assert cur <= prev          # a larger tau keeps a subset of the pattern
         prev = cur
+
+
+# ------------------------------------------------- multi-rank symmetric square (reading C-26)
+
+
+def _symm_needed(ur, uc, lo, hi):
+    """Brute force: indices of U blocks read by some product A(I,K)·A(K,J),
+    I in [lo, hi), J >= I, where A(r,c) = U(r,c) and A(c,r) = U(r,c)^T."""
+    src = {}
+    for t, (r, c) in enumerate(zip(ur.tolist(), uc.tolist())):
+        src[(r, c)] = t
+        src[(c, r)] = t
+    rows = {}
+    for (r, c), t in src.items():
+        rows.setdefault(r, []).append((c, t))
+    need = set()
+    for I in range(lo, hi):
+        for K, t1 in rows.get(I, []):
+            for J, t2 in rows.get(K, []):
+                if J >= I:
+                    need.add(t1)
+                    need.add(t2)
+    return need
+
+
+@pytest.mark.parametrize("seed,nbr,p,P", [(1, 24, 0.15, 3), (2, 30, 0.3, 4), (3, 17, 0.5, 2), (4, 40, 0.08, 5)])
+def test_exchange_plan_symm_is_exactly_the_needed_blocks(seed, nbr, p, P):
+    rng = np.random.default_rng(seed)
+    m = np.triu(rng.random((nbr, nbr)) < p)
+    ur, uc = np.nonzero(m)
+    cuts = np.sort(rng.choice(np.arange(1, nbr), size=P - 1, replace=False))
+    bounds = [0] + cuts.tolist() + [nbr]
+    plan = oracle.exchange_plan_symm(bounds, (ur, uc), 8192)
+    for g in range(P):
+        lo, hi = bounds[g], bounds[g + 1]
+        local = set(np.nonzero((ur >= lo) & (ur < hi))[0].tolist())
+        remote_needed = _symm_needed(ur, uc, lo, hi) - local
+        assert set(plan[g]["selected"].tolist()) == remote_needed
+        assert plan[g]["payload_bytes"] == len(remote_needed) * 8192
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_exchange_plan_symm_banded_closed_form(P):
+    # config 5's upper band: block band D = 32, 512 block rows per rank.  An
+    # interior rank receives the D full U rows above its strip (D+1 blocks
+    # each) and the parts c >= lo of the D rows below it (1..D blocks):
+    # D(D+1) + D(D+1)/2 blocks, vs D(2D+1) per neighbour for the full multiply.
+    nbr, D, per = 512 * P, 32, 512
+    br, bc = qtgen.pattern_banded(nbr, D)
+    up = br <= bc
+    bounds = [g * per for g in range(P + 1)]
+    plan = oracle.exchange_plan_symm(bounds, (br[up], bc[up]), 8192)
+    for g in range(P):
+        n = (D * (D + 1) if g < P - 1 else 0) + (D * (D + 1) // 2 if g > 0 else 0)
+        assert plan[g]["blocks_received"] == n
+    full = oracle.exchange_plan(bounds, (br, bc), (br, bc), 8192)
+    mx, mx_full = max(q["payload_bytes"] for q in plan), max(q["payload_bytes"] for q in full)
+    assert mx == (1584 if P > 2 else 1056) * 8192 and mx_full == (34078720 if P > 2 else 17039360)

@@ -112,6 +112,33 @@ def run_virtual(ctx, stream, name, M, P, ranks, steps=10):
     os.environ.pop("QT_OVERLAP", None)
 
 
+def run_virtual_sym(ctx, stream, name, full, P, ranks, steps=5):
+    """Rank g of the P-rank symmetric square (virtual ranks) vs rank g of the
+    full multiply of the expanded matrix: received bytes, products, times."""
+    U = qtgen.upper(full)
+    A = qtmm.Matrix.from_blocks(ctx, full.n, full.leaf_dim, 32, full.brow, full.bcol, full.vals)
+    Au = qtmm.Matrix.from_blocks(ctx, U.n, U.leaf_dim, 32, U.brow, U.bcol, U.vals)
+    bounds = [g * (full.nbr // P) for g in range(P)] + [full.nbr]
+    for g in ranks:
+        out = {"config": name, "P": P, "rank": g}
+        for label, fn in (("full", lambda: A.multiply_virtual(A, P, g, bounds)),
+                          ("symm", lambda: Au.symm_square_virtual(P, g, bounds))):
+            for _ in range(2):
+                C, st = fn()
+                C.close()
+            sts = []
+            for _ in range(steps):
+                C, st = fn()
+                sts.append(st)
+                C.close()
+            out[label] = {"block_products": st.block_products, "bytes_recv_payload": st.bytes_recv_payload,
+                          "bytes_recv_meta": st.bytes_recv_meta,
+                          "ms_symbolic": round(statistics.median(s.ms_symbolic for s in sts), 4),
+                          "ms_numeric": round(statistics.median(s.ms_numeric for s in sts), 4)}
+        out["payload_ratio"] = round(out["symm"]["bytes_recv_payload"] / max(1, out["full"]["bytes_recv_payload"]), 4)
+        print(json.dumps(out), flush=True)
+
+
 def leaf_sweep(ctx, stream):
     """The paper's leaf benchmark shape (Figs. leafmat_bench_double /
     _single): C = A*B at N = 4096 as ONE leaf, blocks of size bs placed
@@ -248,6 +275,12 @@ def main():
                         qtgen.BlockMatrix(M.n, M.leaf_dim, 32, M.brow, M.bcol, M.vals.astype(np.float32)), 8, [3])
         elif w == "virt4cfg4":
             run_virtual(ctx, stream, "cfg4 ES-like P=4 (virtual ranks)", qtgen.config(4)["A"], 4, [1], steps=5)
+        elif w == "virtsym8":
+            run_virtual_sym(ctx, stream, "cfg5 P=8 banded symmetric (virtual ranks)",
+                            qtgen.config(5, P=8, symmetric=True)["A"], 8, [0, 3])
+        elif w == "virtsym4cfg4":
+            run_virtual_sym(ctx, stream, "cfg4 ES-like symmetric P=4 (virtual ranks)",
+                            qtgen.config(4, symmetric=True)["A"], 4, [0, 1])
         elif w == "dense4096":
             br, bc = qtgen.pattern_dense(128)
             v = qtgen.block_values(br, bc, 32, 1)
