@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "lib", "libqtmm.so")
 SOURCES = ["qt_api.cu", "qt_tree.cu", "qt_symbolic.cu", "qt_numeric.cu", "qt_numeric_f32.cu",
-           "qt_dist.cu"]
+           "qt_dist.cu", "qt_bs16.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

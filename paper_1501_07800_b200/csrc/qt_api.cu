@@ -122,6 +122,10 @@ void cache_release_stream(cudaStream_t s) {
 // statistics at the caller's block size: for 64-blocks the 32-block level is
 // internal (a 64-block product = one task at level L-1, 8 products of 32-blocks)
 static void user_stats(qt_mat R, qt_stats& S) {
+  if (R->ubs == 16) {  // levels and products at 16-block granularity were set by the multiply
+    S.c_blocks = R->nb16;
+    return;
+  }
   if (R->ubs != 64) return;
   const int L = R->L;
   S.nlevels = L;  // levels 0 .. L-1
@@ -269,14 +273,15 @@ qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
   *out = nullptr;
   QT_CUDA(cudaSetDevice(ctx->device));
   if (dtype != QT_F64 && dtype != QT_F32) fail(QT_EDTYPE, "unknown dtype %d", (int)dtype);
-  if (block_size != 32 && block_size != 64)
-    fail(QT_EINVAL, "block_size %d: 32 and 64 are built", block_size);
-  if (n <= 0 || n % block_size != 0)
-    fail(QT_EINVAL, "n=%lld must be a positive multiple of block_size=%d (reading C-4)",
-         (long long)n, block_size);
-  if (leaf_dim < block_size || leaf_dim % block_size != 0 ||
-      ((leaf_dim / block_size) & (leaf_dim / block_size - 1)) != 0)
-    fail(QT_EINVAL, "leaf_dim=%d must be a power-of-two multiple of block_size=%d", leaf_dim,
+  if (block_size != 16 && block_size != 32 && block_size != 64)
+    fail(QT_EINVAL, "block_size %d: 16, 32 and 64 are built", block_size);
+  // (16-blocks are held in 32-blocks: n and leaf_dim multiples of 32, reading C-27)
+  const int gran = std::max(block_size, 32);
+  if (n <= 0 || n % gran != 0)
+    fail(QT_EINVAL, "n=%lld must be a positive multiple of %d (block_size=%d, readings C-4, C-27)",
+         (long long)n, gran, block_size);
+  if (leaf_dim < gran || leaf_dim % gran != 0 || ((leaf_dim / gran) & (leaf_dim / gran - 1)) != 0)
+    fail(QT_EINVAL, "leaf_dim=%d must be a power-of-two multiple of %d (block_size=%d)", leaf_dim, gran,
          block_size);
   if (nblocks < 0 || nblocks >= (1ll << 31)) fail(QT_EINVAL, "nblocks=%lld", (long long)nblocks);
   if (nblocks > 0 && (!brow || !bcol || !values)) fail(QT_EINVAL, "NULL block arrays");
@@ -303,14 +308,20 @@ qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
     if (ctx->world == 1) {
       M->bounds[1] = (int32_t)nbr;
     } else if (row_bounds) {
-      for (int g = 0; g <= ctx->world; ++g) M->bounds[g] = row_bounds[g] * f;
+      for (int g = 0; g <= ctx->world; ++g) {
+        if (block_size == 16 && (row_bounds[g] & 1)) fail(QT_EINVAL, "block_size 16: row_bounds must be even");
+        M->bounds[g] = rows_to_internal(row_bounds[g], block_size);
+      }
       if (M->bounds[0] != 0 || M->bounds[ctx->world] != nbr)
-        fail(QT_EINVAL, "row_bounds must start at 0 and end at %lld", (long long)(nbr / f));
+        fail(QT_EINVAL, "row_bounds must start at 0 and end at %lld",
+             (long long)rows_to_user((int32_t)nbr, block_size));
       for (int g = 0; g < ctx->world; ++g)
         if (M->bounds[g + 1] < M->bounds[g]) fail(QT_EINVAL, "row_bounds not non-decreasing");
     } else {
-      const int64_t nu = nbr / f, per = (nu + ctx->world - 1) / ctx->world;
-      for (int g = 0; g <= ctx->world; ++g) M->bounds[g] = (int32_t)(std::min<int64_t>(nu, per * g) * f);
+      const int64_t nu = std::max<int64_t>(1, nbr / std::max(f, 1)),
+                    per = (nu + ctx->world - 1) / ctx->world;
+      for (int g = 0; g <= ctx->world; ++g)
+        M->bounds[g] = (int32_t)(std::min<int64_t>(nu, per * g) * std::max(f, 1));
     }
     M->row_lo = M->bounds[ctx->rank];
     M->row_hi = M->bounds[ctx->rank + 1];
@@ -349,7 +360,9 @@ qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
         pv = dv.p;
       }
     }
-    if (f == 2 && nblocks > 0) {
+    if (block_size == 16) {
+      build_from_blocks16(M, nblocks, pr, pc, pv, 2 * M->row_lo, 2 * M->row_hi);
+    } else if (f == 2 && nblocks > 0) {
       DevBuf sr, sc, sv;
       split64(ctx, dtype, nblocks, pr, pc, pv, sr, sc, sv);
       build_from_blocks(M, 4 * nblocks, sr.as<int32_t>(), sc.as<int32_t>(), sv.p, M->row_lo, M->row_hi);
@@ -469,6 +482,7 @@ qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
   *C = nullptr;
   qt_ctx ctx = A->ctx;
   QT_CUDA(cudaSetDevice(ctx->device));
+  if (A->ubs == 16) fail(QT_EBS, "the symmetric square is built for block sizes 32 and 64");
   if (ctx->world > 1 && A->ubs != 32) fail(QT_EBS, "the multi-rank symmetric square needs block_size 32");
   check_upper(A);
   ensure_levels(A);
@@ -537,8 +551,8 @@ qt_status qt_info(qt_mat A, int64_t* n, int32_t* leaf_dim, int32_t* block_size, 
   if (dtype) *dtype = A->dtype;
   if (local_nblocks) *local_nblocks = user_nblocks(A);
   if (global_nblocks) *global_nblocks = A->global_nb;
-  if (row_lo) *row_lo = A->row_lo / (A->ubs / 32);
-  if (row_hi) *row_hi = A->row_hi / (A->ubs / 32);
+  if (row_lo) *row_lo = rows_to_user(A->row_lo, A->ubs);
+  if (row_hi) *row_hi = rows_to_user(A->row_hi, A->ubs);
   API_CATCH
 }
 
@@ -547,9 +561,9 @@ qt_status qt_level_nodes(qt_mat A, int64_t* counts, int32_t cap, int32_t* nlevel
   if (!A) fail(QT_EINVAL, "NULL matrix");
   QT_CUDA(cudaSetDevice(A->ctx->device));
   ensure_levels(A);
-  const int top = A->ubs == 64 ? A->L - 1 : A->L;  // the caller's block level
+  const int top = A->ubs == 64 ? A->L - 1 : A->ubs == 16 ? A->L + 1 : A->L;  // the caller's block level
   if (nlevels) *nlevels = top + 1;
-  for (int l = 0; l <= top && l < cap; ++l) counts[l] = A->cnt[l];
+  for (int l = 0; l <= top && l < cap; ++l) counts[l] = l <= A->L ? A->cnt[l] : A->nb16;
   API_CATCH
 }
 
@@ -635,10 +649,13 @@ qt_status qt_multiply_virtual(qt_mat A, qt_mat B, int32_t P, int32_t g, const in
   if (A->dtype != B->dtype) fail(QT_EDTYPE, "dtype mismatch");
   if (P < 1 || g < 0 || g >= P) fail(QT_EINVAL, "bad P=%d / g=%d", P, g);
   if (A->ubs != B->ubs) fail(QT_EBS, "block_size mismatch");
-  const int f = A->ubs / 32;
   std::vector<int32_t> b32(P + 1);
-  for (int q = 0; q <= P; ++q) b32[q] = row_bounds[q] * f;  // caller's block rows -> 32-rows
-  if (b32[0] != 0 || b32[P] != A->nbr) fail(QT_EINVAL, "row_bounds must span [0,%d]", A->nbr / f);
+  for (int q = 0; q <= P; ++q) {  // caller's block rows -> 32-rows
+    if (A->ubs == 16 && (row_bounds[q] & 1)) fail(QT_EINVAL, "block_size 16: row_bounds must be even");
+    b32[q] = rows_to_internal(row_bounds[q], A->ubs);
+  }
+  if (b32[0] != 0 || b32[P] != A->nbr)
+    fail(QT_EINVAL, "row_bounds must span [0,%d]", rows_to_user(A->nbr, A->ubs));
   for (int q = 0; q < P; ++q)
     if (b32[q + 1] < b32[q]) fail(QT_EINVAL, "row_bounds not non-decreasing");
   qt_ctx ctx = A->ctx;

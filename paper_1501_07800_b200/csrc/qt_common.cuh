@@ -96,4 +96,12 @@ __device__ __forceinline__ int4 op_children(const int4* __restrict__ tab, int re
   return op_xform(tab[sym ? (ref >> 2) : ref], ref, trans, sym);
 }
 
+// Block size 16 (qt_bs16.cu): quadrant masks of 32-blocks, bit 2i+j = 16-block (i,j).
+// mask of the transposed 32-block: quadrant (i,j) -> (j,i)
+__host__ __device__ __forceinline__ int mask_t(int m) { return (m & 9) | ((m & 2) << 1) | ((m & 4) >> 1); }
+// some 16-block product x(r,s)·y(s,c) exists (column s of x meets row s of y)
+__host__ __device__ __forceinline__ bool mask_meet(int x, int y) {
+  return ((x & 5) && (y & 3)) || ((x & 10) && (y & 12));
+}
+
 }  // namespace qt

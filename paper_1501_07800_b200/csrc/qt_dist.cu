@@ -344,7 +344,8 @@ __global__ void k_req_counts(const int32_t* __restrict__ rows, int32_t n,
 __global__ void k_pack(const int32_t* __restrict__ rows, int32_t n, const int32_t* __restrict__ offs,
                        const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ order,
                        const uint64_t* __restrict__ rm_sorted, const uint4* __restrict__ pool,
-                       int vec_per_block, int32_t* __restrict__ cols, uint4* __restrict__ payload) {
+                       int vec_per_block, int32_t* __restrict__ cols, uint4* __restrict__ payload,
+                       const uint8_t* __restrict__ sub_in, uint8_t* __restrict__ sub_out) {
   int lane = threadIdx.x & 31;
   int64_t w = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
   if (w >= n) return;
@@ -354,6 +355,7 @@ __global__ void k_pack(const int32_t* __restrict__ rows, int32_t n, const int32_
   for (int32_t s = s0; s < s1; ++s) {
     int32_t src = order[s];
     if (lane == 0) cols[o + (s - s0)] = (int32_t)(rm_sorted[s] & 0xffffffffu);
+    if (lane == 0 && sub_in) sub_out[o + (s - s0)] = sub_in[src];
     const uint4* sp = pool + (int64_t)src * vec_per_block;
     uint4* dp = payload + (int64_t)(o + (s - s0)) * vec_per_block;
     for (int e = lane; e < vec_per_block; e += 32) dp[e] = sp[e];
@@ -510,14 +512,15 @@ void pack_counts(qt_mat B, const RowView& v, const int32_t* d_rows, int32_t n, i
 // Owner side, step 3: columns and values of the requested rows, packed at the
 // exclusive-scan offsets of the counts.
 void pack_blocks(qt_mat B, const RowView& v, const int32_t* d_rows, int32_t n, const int32_t* d_offs,
-                 int32_t* d_cols, void* d_payload) {
+                 int32_t* d_cols, void* d_payload, uint8_t* d_sub = nullptr) {
   qt_ctx ctx = B->ctx;
   if (n == 0) return;
   int vpb = (int)(1024 * elem_size(B->dtype) / 16);
   unsigned g = (unsigned)((n + 7) / 8);
   k_pack<<<g, 256, 0, ctx->stream>>>(d_rows, n, d_offs, v.row_ptr.as<int32_t>(), v.order.as<int32_t>(),
                                      v.rm_sorted.as<uint64_t>(), static_cast<const uint4*>(B->pool_ptr()),
-                                     vpb, d_cols, static_cast<uint4*>(d_payload));
+                                     vpb, d_cols, static_cast<uint4*>(d_payload),
+                                     B->ubs == 16 ? B->sub.as<uint8_t>() : nullptr, d_sub);
   QT_LAUNCH_CHECK(ctx);
 }
 
@@ -526,6 +529,7 @@ struct Received {
   int32_t nrows = 0;
   int64_t nblk = 0;
   DevBuf rows, counts, offs, cols, payload;
+  DevBuf sub;  // block size 16: the received blocks' quadrant masks
 };
 
 qt_mat clone_shape(qt_mat A) {
@@ -556,6 +560,11 @@ qt_mat make_b_ext(qt_mat B, Received& rx) {
     X->pool1 = B->pool_ptr();
     X->pool2 = rx.payload.p;
     X->split = nl;
+    if (B->ubs == 16) {  // masks indexed like the pool ids: local, then received
+      X->sub.alloc(std::max<int64_t>(nt, 1), st);
+      if (nl > 0) QT_CUDA(cudaMemcpyAsync(X->sub.p, B->sub.p, nl, cudaMemcpyDeviceToDevice, st));
+      if (nr > 0) QT_CUDA(cudaMemcpyAsync(X->sub.as<uint8_t>() + nl, rx.sub.p, nr, cudaMemcpyDeviceToDevice, st));
+    }
     if (nt == 0) {
       build_levels(X);
       return X;
@@ -598,10 +607,10 @@ qt_mat rows_of(qt_mat A, int32_t lo, int32_t hi) {
   return M;
 }
 
-void fill_exchange_stats(qt_stats* S, const Received& rx, size_t block_bytes) {
+void fill_exchange_stats(qt_stats* S, const Received& rx, size_t block_bytes, bool masks) {
   S->blocks_recv = rx.nblk;
   S->bytes_recv_payload = rx.nblk * (int64_t)block_bytes;
-  S->bytes_recv_meta = 4ll * rx.nrows + 4ll * rx.nblk;
+  S->bytes_recv_meta = 4ll * rx.nrows + 4ll * rx.nblk + (masks ? rx.nblk : 0);
   S->bytes_sent_meta = 4ll * rx.nrows;
 }
 
@@ -734,9 +743,12 @@ qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S) {
   int64_t nblk_out = h_out_offs[n_in];
   rx.nblk = h_in_offs[rx.nrows];
   // 3. owner packs columns + values; exchange
-  DevBuf d_out_cols(4 * std::max<int64_t>(nblk_out, 1), st), d_out_pay(bb * std::max<int64_t>(nblk_out, 1), st);
+  const bool m16 = B->ubs == 16;
+  DevBuf d_out_cols(4 * std::max<int64_t>(nblk_out, 1), st), d_out_pay(bb * std::max<int64_t>(nblk_out, 1), st),
+      d_out_sub(m16 ? std::max<int64_t>(nblk_out, 1) : 0, st);
   pack_blocks(B, v, d_in_rows.as<int32_t>(), (int32_t)n_in, d_out_offs.as<int32_t>(),
-              d_out_cols.as<int32_t>(), d_out_pay.p);
+              d_out_cols.as<int32_t>(), d_out_pay.p, m16 ? d_out_sub.as<uint8_t>() : nullptr);
+  if (m16) rx.sub.alloc(std::max<int64_t>(rx.nblk, 1), st);
   rx.cols.alloc(4 * std::max<int64_t>(rx.nblk, 1), st);
   rx.payload.alloc(bb * std::max<int64_t>(rx.nblk, 1), st);
   int64_t sent_payload = 0, sent_meta = 0;
@@ -748,9 +760,11 @@ qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S) {
     int64_t r0 = in_off[q], r1 = in_off[q + 1];
     int64_t b0 = h_out_offs[r0], b1 = h_out_offs[r1];
     if (b1 > b0) X->send(d_out_cols.as<int32_t>() + b0, 4 * (b1 - b0), q);
-    sent_meta += 4 * (r1 - r0) + 4 * (b1 - b0);
+    if (b1 > b0 && m16) X->send(d_out_sub.as<uint8_t>() + b0, b1 - b0, q);
+    sent_meta += 4 * (r1 - r0) + (m16 ? 5 : 4) * (b1 - b0);
     int64_t i0 = h_in_offs[seg_off[q]], i1 = h_in_offs[seg_off[q] + my_counts[q]];
     if (i1 > i0) X->recv(rx.cols.as<int32_t>() + i0, 4 * (i1 - i0), q);
+    if (i1 > i0 && m16) X->recv(rx.sub.as<uint8_t>() + i0, i1 - i0, q);
   }
   X->group_end();
   // 3b. values: on the comm stream (behind the packing) when overlapped, so
@@ -781,7 +795,7 @@ qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S) {
   }
   qt_mat Bx = make_b_ext(B, rx);
   QT_CUDA(cudaEventRecord(ctx->ev[6], st));
-  fill_exchange_stats(S, rx, bb);
+  fill_exchange_stats(S, rx, bb, m16);
   S->bytes_sent_payload = sent_payload;
   S->bytes_sent_meta += sent_meta;
   qt_mat C;
@@ -870,6 +884,8 @@ qt_mat truncate_dist(qt_mat A, double tau) {
     DevBuf k32;
     expand_keep(A, keep.as<uint8_t>(), k32);
     R = select_blocks(A, k32.as<uint8_t>());
+  } else if (A->ubs == 16) {
+    R = apply_keep16(A, keep.as<uint8_t>());
   } else {
     R = select_blocks(A, keep.as<uint8_t>());
   }
@@ -913,11 +929,12 @@ qt_mat multiply_virtual(qt_mat A, qt_mat B, const int32_t* bounds, int P, int g,
     rx.nblk = ho[rx.nrows];
     rx.cols.alloc(4 * std::max<int64_t>(rx.nblk, 1), st);
     rx.payload.alloc(bb * std::max<int64_t>(rx.nblk, 1), st);
+    if (B->ubs == 16) rx.sub.alloc(std::max<int64_t>(rx.nblk, 1), st);
     pack_blocks(B, v, rx.rows.as<int32_t>(), rx.nrows, rx.offs.as<int32_t>(), rx.cols.as<int32_t>(),
-                rx.payload.p);
+                rx.payload.p, B->ubs == 16 ? rx.sub.as<uint8_t>() : nullptr);
     Bx = make_b_ext(Bl, rx);
     QT_CUDA(cudaEventRecord(ctx->ev[6], st));
-    fill_exchange_stats(S, rx, bb);
+    fill_exchange_stats(S, rx, bb, B->ubs == 16);
     // the two-phase numeric launch of the NCCL path (here the payload is
     // already in place: the phases' split and stream ordering are what runs)
     Overlap ov;

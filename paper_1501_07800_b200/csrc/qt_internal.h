@@ -131,7 +131,8 @@ struct qt_mat_s {
   qt_ctx ctx = nullptr;
   int64_t n = 0;
   int32_t leaf_dim = 0, bs = 0;  // bs: the internal block size (32)
-  int32_t ubs = 32;    // the caller's block size: 32, or 64 = stored as 2x2 quads of 32-blocks
+  int32_t ubs = 32;    // the caller's block size: 32; 64 = stored as 2x2 quads of 32-blocks;
+                       // 16 = held as the quadrants of 32-blocks (qt_bs16.cu)
   qt_dtype dtype = QT_F64;
   int L = 1;           // levels above the block level; level L = blocks
   int leaf_level = 0;
@@ -148,6 +149,8 @@ struct qt_mat_s {
   qt::DevBuf hist;     // int32 per-level node counts per row / per column (see build_levels)
   std::vector<int32_t> hist_host;  // host copy of hist (per-level task counts without a sync)
   std::vector<qt::DevBuf> norm2;  // squared Frobenius norms per node, levels 0..L (screening; lazy)
+  qt::DevBuf sub;      // ubs == 16: uint8 [nb] quadrant occupancy (bit 2i+j), indexed like the pool
+  int64_t nb16 = 0;    // ubs == 16: the caller's blocks (set quadrants)
   // B_ext of a multi-rank multiply: pool1 overrides pool.p (a borrowed view of
   // the local pool); block ids >= split live in pool2 (the received blocks).
   const void* pool1 = nullptr;
@@ -187,7 +190,24 @@ void reap_pending(qt_ctx ctx, bool wait);
 // 64-blocks (2x2 quads of 32-blocks): split inputs / user-level block count
 void split64(qt_ctx ctx, qt_dtype dt, int64_t nb, const int32_t* brow, const int32_t* bcol,
              const void* vals, DevBuf& obrow, DevBuf& obcol, DevBuf& ovals);
-inline int64_t user_nblocks(qt_mat M) { return M->ubs == 64 ? M->nb / 4 : M->nb; }
+inline int64_t user_nblocks(qt_mat M) { return M->ubs == 64 ? M->nb / 4 : M->ubs == 16 ? M->nb16 : M->nb; }
+// the caller's block rows -> internal 32-block rows (16: must be even)
+inline int32_t rows_to_internal(int32_t r, int ubs) { return ubs == 64 ? 2 * r : ubs == 16 ? r / 2 : r; }
+inline int32_t rows_to_user(int32_t r, int ubs) { return ubs == 64 ? r / 2 : ubs == 16 ? 2 * r : r; }
+// block size 16 (qt_bs16.cu)
+void build_from_blocks16(qt_mat M, int64_t n, const int32_t* brow, const int32_t* bcol, const void* vals,
+                         int32_t lo16, int32_t hi16);
+void read_back16(qt_mat M, int32_t* brow, int32_t* bcol, void* vals);
+void truncate_terms16(qt_mat A, DevBuf& nrm, DevBuf& rm);
+qt_mat apply_keep16(qt_mat A, const uint8_t* keep_user);
+int64_t compact_sub16(qt_ctx ctx, const uint8_t* keep, const int32_t* incl, const uint8_t* in, int64_t n,
+                      int64_t kept, DevBuf& out);
+// C's quadrant masks from the level L-1 task list; out = {16-block products, C 16-blocks, empty
+// containers, non-NIL container pairs (the level-L task count)}
+void cmask16(qt_ctx ctx, int64_t ntiles, const int32_t* ts, const int32_t* pa, const int32_t* pb, const int4* cA,
+             const int4* cB, const int4* cC, const uint8_t* subA, const uint8_t* subB, int trans, uint8_t* subC,
+             int64_t nc, int64_t out[4]);
+qt_mat drop_empty16(qt_mat C);
 // keep flags per user block -> per internal block
 void expand_keep(qt_mat M, const uint8_t* keep_user, DevBuf& keep32);
 // truncate (reading C-16): local terms, global decision, single-rank driver
@@ -249,6 +269,8 @@ struct NumericArgs {
   const double* normA = nullptr;  // block squared norms (screening) or null
   const double* normB = nullptr;
   double tau2 = 0.0;
+  const uint8_t* subA = nullptr;  // block size 16: quadrant masks (products whose quadrants never meet are skipped)
+  const uint8_t* subB = nullptr;
   cudaStream_t stream = nullptr;  // launch stream (null: the ctx stream)
   // overlap phases (split_tiles): phase 1 = tiles map[0, *nsel), phase 2 =
   // map[*nsel, ntiles); 0 = all tiles in order (tile_map unused).  group == 1.

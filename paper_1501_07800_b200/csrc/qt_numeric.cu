@@ -63,10 +63,19 @@ struct __align__(16) StageHdr {
 };
 
 // a block product survives: both present and (screening) norms^2 product >= tau^2
-template <bool kScreen>
+// (block size 16: "screening" by the quadrant masks — a product whose
+// quadrants never meet adds only zeros and is skipped, as in the BFS)
+template <bool kTA, bool kTB, bool kScreen>
 __device__ __forceinline__ bool prod_ok(int a, int b, const NumericArgs& na) {
   if (a < 0 || b < 0) return false;
-  return !kScreen || __dmul_rn(na.normA[a], na.normB[b]) >= na.tau2;
+  if (!kScreen) return true;
+  if (na.subA) {
+    int x = na.subA[a], y = na.subB[b];
+    if (kTA) x = mask_t(x);
+    if (kTB) y = mask_t(y);
+    return mask_meet(x, y);
+  }
+  return __dmul_rn(na.normA[a], na.normB[b]) >= na.tau2;
 }
 
 // a level L-1 child entry -> (block index, transposed) ; plain indices unless symmetric
@@ -224,8 +233,8 @@ __device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, int keep
   const int b0 = blk<kSym>(kb ? B4.z : B4.x, tb0), b1 = blk<kSym>(kb ? B4.w : B4.y, tb1);
   // products of this step: both blocks present and, when screening,
   // ||A(i,k)||^2 * ||B(k,j)||^2 >= tau^2 (the symbolic pass's test)
-  const int pm = ((prod_ok<kScreen>(a0, b0, a) ? 1 : 0) | (prod_ok<kScreen>(a0, b1, a) ? 2 : 0) |
-                  (prod_ok<kScreen>(a1, b0, a) ? 4 : 0) | (prod_ok<kScreen>(a1, b1, a) ? 8 : 0)) &
+  const int pm = ((prod_ok<kTA, kTB, kScreen>(a0, b0, a) ? 1 : 0) | (prod_ok<kTA, kTB, kScreen>(a0, b1, a) ? 2 : 0) |
+                  (prod_ok<kTA, kTB, kScreen>(a1, b0, a) ? 4 : 0) | (prod_ok<kTA, kTB, kScreen>(a1, b1, a) ? 8 : 0)) &
                  keep;
   StepDesc d;
   d.a0 = (pm & 3) ? a0 : -1;
@@ -651,7 +660,7 @@ void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
   // grouped grabs (sparse patterns: amortise the scheduler and metadata latency)
   if (a.trans & 4) {  // symmetric square
     launch_numeric_t<false, false, true>(ctx, a, grid);
-  } else if (a.normA) {  // norm-screened product
+  } else if (a.normA || a.subA) {  // norm-screened product, or block size 16 (quadrant masks)
     switch (a.trans & 3) {
       case 0: launch_numeric_t<false, false, false, true>(ctx, a, grid); break;
       case 1: launch_numeric_t<true, false, false, true>(ctx, a, grid); break;

@@ -75,13 +75,25 @@ __device__ __forceinline__ int cmask(uint64_t ck, int l, int L, bool prune, int3
 // node's squared norm is the sum of its blocks', so a node pair below the
 // threshold contains only block pairs below it: pruning at any level is exact
 // with respect to the block-level test.  na == nullptr: no screening.
+// Block size 16 (qt_bs16.cu): at the block level a pair whose quadrant masks
+// never meet has no 16-block product and is skipped (ma/mb: the operands'
+// masks, tr: transposed operands), so C gets no container without one.
 struct Screen {
   const double* na;
   const double* nb;
   double tau2;
+  const uint8_t* ma = nullptr;
+  const uint8_t* mb = nullptr;
+  int tr = 0;
 };
 __device__ __forceinline__ bool pair_ok(int ar, int br, const Screen& sc, bool sym) {
   if (ar < 0 || br < 0) return false;
+  if (sc.ma) {
+    int x = sc.ma[ar], y = sc.mb[br];
+    if (sc.tr & 1) x = mask_t(x);
+    if (sc.tr & 2) y = mask_t(y);
+    return mask_meet(x, y);
+  }
   if (!sc.na) return true;
   const int ai = sym ? (ar >> 2) : ar, bi = sym ? (br >> 2) : br;
   return __dmul_rn(sc.na[ai], sc.nb[bi]) >= sc.tau2;
@@ -145,6 +157,8 @@ struct SmallBfsArgs {
   const double* normB[QT_MAX_LEVELS];
   double tau2;
   int32_t row_lo, row_hi;  // C row window (block rows)
+  const uint8_t* subA;     // block size 16: quadrant masks (pair test at the block level)
+  const uint8_t* subB;
 };
 
 __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) {
@@ -177,7 +191,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     const uint64_t* ck = a.ckey[cur];
     const int4* cA = a.childA[l];
     const int4* cB = a.childB[l];
-    const Screen sc{a.normA[l + 1], a.normB[l + 1], a.tau2};
+    const bool lastl = l + 1 == a.L && a.subA;
+    const Screen sc{a.normA[l + 1], a.normB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
+                    a.trans & 3};
     // 1. child-task counts per (task, C child), group-major
     for (int p = tid; p < F; p += kSmallThreads) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
@@ -297,6 +313,8 @@ struct LargeBfsArgs {
   int32_t* f_out;                // tasks per level
   unsigned* bar;                 // grid barrier: arrival count (self-resetting), generation
   int32_t row_lo, row_hi;        // C row window (block rows)
+  const uint8_t* subA;           // block size 16: quadrant masks (pair test at the block level)
+  const uint8_t* subB;
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -360,7 +378,9 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
   for (int l = a.l_begin; l < a.L; ++l) {
     const bool last = l == a.L - 1;
     const int mode = (a.trans & 7) | ((sym && l < (a.trans >> 8)) ? 8 : 0);
-    const Screen sc{a.normA[l + 1], a.normB[l + 1], a.tau2};
+    const bool lastl = l + 1 == a.L && a.subA;
+    const Screen sc{a.normA[l + 1], a.normB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
+                    a.trans & 3};
     const int32_t F = a.f_out[l], ns = a.ns_out[l];
     const int32_t* pa = a.pa[l];
     const int32_t* pb = a.pb[l];
@@ -694,6 +714,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       sa.tau2 = tau2;
       sa.row_lo = row_lo;
       sa.row_hi = row_hi;
+      sa.subA = A->ubs == 16 ? A->sub.as<uint8_t>() : nullptr;
+      sa.subB = A->ubs == 16 ? B->sub.as<uint8_t>() : nullptr;
       for (int l = 0; l <= L && l < QT_MAX_LEVELS; ++l) {
         sa.normA[l] = screen ? A->norm2[l].as<double>() : nullptr;
         sa.normB[l] = screen ? B->norm2[l].as<double>() : nullptr;
@@ -764,6 +786,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         la.tau2 = tau2;
         la.row_lo = row_lo;
         la.row_hi = row_hi;
+        la.subA = sa.subA;
+        la.subB = sa.subB;
         for (int l = 0; l < L && l < QT_MAX_LEVELS; ++l) {
           la.childA[l] = A->child[l].as<int4>();
           la.childB[l] = B->child[l].as<int4>();
@@ -892,6 +916,10 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       na.normA = screen ? A->norm2[L].as<double>() : nullptr;
       na.normB = screen ? B->norm2[L].as<double>() : nullptr;
       na.tau2 = tau2;
+      if (A->ubs == 16) {
+        na.subA = A->sub.as<uint8_t>();
+        na.subB = B->sub.as<uint8_t>();
+      }
       na.group = group;
       DevBuf poolT;  // symmetric square: blocks of U read transposed come from U^T's copy
       if (C->nb > 0 && sym) {
@@ -965,6 +993,23 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         ov->tiles_local = h;
         ov->tiles_remote = n_all - h;
       }
+      if (A->ubs == 16) {  // the 16-block pattern of C and the 16-block products (qt_bs16.cu)
+        C->sub.alloc(std::max<int64_t>(C->nb, 1), st);
+        int64_t r16[4];
+        cmask16(ctx, ns[L - 1], cstart.as<int32_t>(), pa.as<int32_t>(), pb.as<int32_t>(), A->child[L - 1].as<int4>(),
+                B->child[L - 1].as<int4>(), cchild.as<int4>(), A->sub.as<uint8_t>(), B->sub.as<uint8_t>(), trans & 3,
+                C->sub.as<uint8_t>(), C->nb, r16);
+        C->nb16 = r16[1];
+        S.level_tasks[L] = r16[3];  // all non-NIL container pairs (the BFS kept those with a 16-block product)
+        S.level_tasks[L + 1] = r16[0];
+        S.level_c_nodes[L + 1] = r16[1];
+        S.block_products = r16[0];
+        if (r16[2] > 0) {  // containers none of whose quadrants is a product: NIL at 16-granularity
+          qt_mat D = drop_empty16(C);
+          delete C;
+          C = D;
+        }
+      }
     }
     if (!ctx->async_multiply) {
       QT_CUDA(cudaEventSynchronize(ctx->ev[4]));
@@ -972,6 +1017,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       QT_CUDA(cudaEventElapsedTime(ms_num, ctx->ev[3], ctx->ev[4]));
     }
     S.c_blocks = C->nb;
+    if (A->ubs == 16) S.nlevels = L + 2;  // + the 16-block level below the containers
   } catch (...) {
     delete C;
     throw;

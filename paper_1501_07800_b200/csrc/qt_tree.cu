@@ -563,6 +563,10 @@ void reap_pending(qt_ctx ctx, bool wait) {
 }
 
 void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals, bool async) {
+  if (M->ubs == 16) {  // (async: completes before returning)
+    read_back16(M, brow, bcol, vals);
+    return;
+  }
   if (M->ubs == 64) {
     if (async) fail(QT_EINVAL, "qt_read_back_async is built for block_size 32");
     read_back64(M, brow, bcol, vals);
@@ -657,6 +661,7 @@ qt_mat select_blocks(qt_mat A, const uint8_t* d_keep) {
       kept = read_scalar(ctx, incl.as<int32_t>() + (n - 1));
     }
     M->nb = kept;
+    if (A->ubs == 16) M->nb16 = n > 0 ? compact_sub16(ctx, d_keep, incl.as<int32_t>(), A->sub.as<uint8_t>(), n, kept, M->sub) : 0;
     if (kept > 0) {
       size_t es = elem_size(A->dtype);
       M->key.alloc(kept * 8, st);
@@ -678,6 +683,10 @@ qt_mat select_blocks(qt_mat A, const uint8_t* d_keep) {
 
 // Frobenius norms^2 and row-major keys of the local blocks (truncation terms)
 void truncate_terms(qt_mat A, DevBuf& nrm, DevBuf& rm) {
+  if (A->ubs == 16) {
+    truncate_terms16(A, nrm, rm);
+    return;
+  }
   qt_ctx ctx = A->ctx;
   cudaStream_t st = ctx->stream;
   const int64_t n = A->nb;
@@ -783,6 +792,7 @@ qt_mat truncate(qt_mat A, double tau) {
     expand_keep(A, keep.as<uint8_t>(), k32);
     return select_blocks(A, k32.as<uint8_t>());
   }
+  if (A->ubs == 16) return apply_keep16(A, keep.as<uint8_t>());
   return select_blocks(A, keep.as<uint8_t>());
 }
 

@@ -1,0 +1,233 @@
+"""Block size 16 ("a block size around 16-64", the
+paper's S^2 runs use block size 16; reading C-27).  Needs a B200.
+
+16x16 blocks are held as the quadrants of the kernels' 32x32 blocks with an
+occupancy mask; C's 16-block pattern is the symbolic product one level below
+the 32-blocks.  Every result is compared with the oracle run at bs = 16 (its
+own plain block-CSR multiply at that block size): pattern identical,
+integer-valued inputs bit-exact, uniform inputs within the FP64 gate and the
+Higham bound; per-level task counts (16-block level included) equal the
+oracle's coarsening counts."""
+import numpy as np
+import pytest
+
+import oracle
+import qtgen
+
+pytestmark = pytest.mark.gpu
+REL_FRO_F64 = 1e-12
+
+
+@pytest.fixture(scope="module")
+def qt():
+    from paper_1501_07800_b200 import build
+    build.build()
+    from paper_1501_07800_b200 import qtmm
+    return qtmm
+
+
+@pytest.fixture(scope="module")
+def ctx(qt):
+    import torch
+    torch.cuda.init()
+    return qt.Context(0)
+
+
+def random_bm16(rng, nbr, p, kind, leaf, dtype=np.float64, mask=None):
+    m = rng.random((nbr, nbr)) < p if mask is None else mask
+    br, bc = np.nonzero(m)
+    v = (rng.integers(-4, 5, size=(len(br), 16, 16)) if kind == "int"
+         else rng.uniform(-1, 1, size=(len(br), 16, 16))).astype(dtype)
+    return qtgen.BlockMatrix(nbr * 16, leaf, 16, br.astype(np.int32), bc.astype(np.int32), v)
+
+
+def mk(qt, ctx, M):
+    return qt.Matrix.from_blocks(ctx, M.n, M.leaf_dim, 16, M.brow, M.bcol, M.vals)
+
+
+def tup(M):
+    return (M.brow, M.bcol, M.vals.astype(np.float64))
+
+
+def check(got, ref, A, B, nbr, kind):
+    assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+    if kind == "int":
+        assert np.array_equal(got[2].astype(np.float64), ref[2])
+    elif len(ref[0]):
+        d = got[2] - ref[2]
+        assert np.linalg.norm(d) <= REL_FRO_F64 * np.linalg.norm(ref[2])
+        _, _, bound = oracle.higham_bound(nbr, 16, A, B, nbr * 16)
+        assert np.all(np.abs(d) <= bound + 1e-300)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_bs16_roundtrip(qt, ctx, dtype):
+    rng = np.random.default_rng(16)
+    M = random_bm16(rng, 14, 0.35, "uniform", 64, dtype)
+    perm = rng.permutation(M.nb)
+    A = qt.Matrix.from_blocks(ctx, M.n, 64, 16, M.brow[perm], M.bcol[perm], M.vals[perm])
+    info = A.info()
+    assert info["bs"] == 16 and A.nblocks == M.nb and info["global_nblocks"] == M.nb
+    r, c, v = A.to_blocks()
+    o = np.lexsort((M.bcol, M.brow))
+    assert np.array_equal(r, M.brow[o]) and np.array_equal(c, M.bcol[o]) and np.array_equal(v, M.vals[o])
+
+
+def test_bs16_errors(qt, ctx):
+    v = np.ones((2, 16, 16))
+    with pytest.raises(qt.QtError) as e:
+        qt.Matrix.from_blocks(ctx, 128, 64, 16, np.array([3, 3], np.int32), np.array([5, 5], np.int32), v)
+    assert e.value.name == "QT_EDUP" and "brow=3, bcol=5" in str(e.value)
+    with pytest.raises(qt.QtError) as e:
+        qt.Matrix.from_blocks(ctx, 128, 64, 16, np.array([0, 8], np.int32), np.array([0, 1], np.int32), v)
+    assert e.value.name == "QT_ERANGE" and "brow=8" in str(e.value)
+    with pytest.raises(qt.QtError) as e:      # n must be a multiple of 32 (reading C-27)
+        qt.Matrix.from_blocks(ctx, 48, 32, 16, np.array([0], np.int32), np.array([0], np.int32), v[:1])
+    assert e.value.name == "QT_EINVAL"
+    U = qt.Matrix.from_blocks(ctx, 128, 64, 16, np.array([0], np.int32), np.array([1], np.int32), v[:1])
+    with pytest.raises(qt.QtError) as e:
+        U.symm_square()
+    assert e.value.name == "QT_EBS"
+
+
+@pytest.mark.parametrize("nbr,p,leaf", [(2, 1.0, 32), (8, 1.0, 64), (14, 0.5, 64), (38, 0.15, 128),
+                                        (64, 0.04, 256)])
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_bs16_multiply(qt, ctx, nbr, p, leaf, kind):
+    rng = np.random.default_rng(1600 + nbr + (kind == "int"))
+    Am = random_bm16(rng, nbr, p, kind, leaf)
+    Bm = random_bm16(rng, nbr, p, kind, leaf)
+    C, st = mk(qt, ctx, Am).multiply(mk(qt, ctx, Bm))
+    got = C.to_blocks()
+    ref = oracle.spgemm(nbr, 16, tup(Am), tup(Bm))
+    check(got, ref, tup(Am), tup(Bm), nbr, kind)
+    assert C.nblocks == len(ref[0]) and st.c_blocks == len(ref[0])
+    L, _ = oracle.tree_levels(Am.n, 16, leaf)
+    counts = oracle.level_task_counts(L, (Am.brow, Am.bcol), (Bm.brow, Bm.bcol))
+    if nbr >= 8:      # (smaller grids: the containers' quadtree has one level more than the oracle's)
+        assert st.nlevels == L + 1
+        assert list(st.level_tasks[: L + 1]) == counts
+        assert C.level_nodes() == oracle.level_node_counts(L, (ref[0], ref[1]))
+    assert st.block_products == counts[-1]
+
+
+def test_bs16_quadrants_that_never_meet(qt, ctx):
+    # A holds only (even, even) 16-blocks, B only (odd, odd): every 32-level
+    # container pair exists but no 16-block product does -> C is empty
+    nbr = 16
+    ev = np.zeros((nbr, nbr), bool)
+    ev[0::2, 0::2] = True
+    od = np.zeros((nbr, nbr), bool)
+    od[1::2, 1::2] = True
+    rng = np.random.default_rng(5)
+    Am = random_bm16(rng, nbr, 0, "int", 64, mask=ev)
+    Bm = random_bm16(rng, nbr, 0, "int", 64, mask=od)
+    C, st = mk(qt, ctx, Am).multiply(mk(qt, ctx, Bm))
+    assert C.nblocks == 0 and st.block_products == 0 and st.c_blocks == 0
+    assert len(C.to_blocks()[0]) == 0
+    # mixed: half the containers' products vanish at 16-granularity
+    Bm2 = random_bm16(rng, nbr, 0, "int", 64, mask=ev | od)
+    C2, st2 = mk(qt, ctx, Am).multiply(mk(qt, ctx, Bm2))
+    ref = oracle.spgemm(nbr, 16, tup(Am), tup(Bm2))
+    check(C2.to_blocks(), ref, tup(Am), tup(Bm2), nbr, "int")
+
+
+def test_bs16_chain_and_transposes_fp32(qt, ctx):
+    rng = np.random.default_rng(161)
+    nbr = 22
+    Am = random_bm16(rng, nbr, 0.2, "int", 64, np.float32)
+    Bm = random_bm16(rng, nbr, 0.2, "int", 64, np.float32)
+    A, B = mk(qt, ctx, Am), mk(qt, ctx, Bm)
+    for ta, tb in [(False, False), (True, False), (False, True), (True, True)]:
+        got = A.multiply_ex(B, ta, tb)[0].to_blocks()
+        ref = oracle.spgemm_t(nbr, 16, tup(Am), tup(Bm), ta, tb)
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+        assert np.array_equal(got[2].astype(np.float64), ref[2])
+    # a product used as an operand again: its masks drive the next product
+    C = A @ B
+    got = (C @ A).to_blocks()
+    c_ref = oracle.spgemm(nbr, 16, tup(Am), tup(Bm))
+    ref = oracle.spgemm(nbr, 16, c_ref, tup(Am))
+    assert np.array_equal(got[0], ref[0]) and np.array_equal(got[2].astype(np.float64), ref[2])
+
+
+@pytest.mark.parametrize("tau", [0.0, 2.0, 9.0])
+def test_bs16_truncate(qt, ctx, tau):
+    rng = np.random.default_rng(162)
+    M = random_bm16(rng, 20, 0.4, "uniform", 64)
+    M.vals *= rng.uniform(0, 1, size=(M.nb, 1, 1)) ** 4
+    A = mk(qt, ctx, M)
+    T = A.truncate(tau)
+    r, c, v = T.to_blocks()
+    rr, rc, rv = oracle.truncate(M.brow, M.bcol, M.vals, tau)
+    assert np.array_equal(r, rr) and np.array_equal(c, rc) and np.array_equal(v, rv)
+    assert T.nblocks == len(rr)
+    # the truncated matrix multiplies as its listed blocks
+    got = (T @ T).to_blocks()
+    ref = oracle.spgemm(20, 16, (rr, rc, rv), (rr, rc, rv))
+    check(got, ref, (rr, rc, rv), (rr, rc, rv), 20, "uniform")
+
+
+@pytest.mark.parametrize("P,bounds", [(2, [0, 16, 40]), (3, [0, 6, 22, 40])])
+def test_bs16_virtual_ranks(qt, ctx, P, bounds):
+    rng = np.random.default_rng(163 + P)
+    M = random_bm16(rng, 40, 0.12, "uniform", 128)
+    A = mk(qt, ctx, M)
+    full = (A @ A).to_blocks()
+    # the exchange moves 32-blocks (containers): the plan on the container pattern
+    cont = np.unique((M.brow // 2).astype(np.int64) * 1000 + M.bcol // 2)
+    cr, cc = cont // 1000, cont % 1000
+    plan = oracle.exchange_plan([b // 2 for b in bounds], (cr, cc), (cr, cc), 8192)
+    for g in range(P):
+        Cg, st = A.multiply_virtual(A, P, g, bounds)
+        r, c, v = Cg.to_blocks()
+        m = (full[0] >= bounds[g]) & (full[0] < bounds[g + 1])
+        assert np.array_equal(r, full[0][m]) and np.array_equal(c, full[1][m]) and np.array_equal(v, full[2][m])
+        assert st.bytes_recv_payload == plan[g]["payload_bytes"]
+        assert st.bytes_recv_meta == plan[g]["meta_bytes"] + plan[g]["blocks_received"]   # + 1 mask byte per block
+    with pytest.raises(qt.QtError) as e:
+        A.multiply_virtual(A, 2, 0, [0, 15, 40])
+    assert e.value.name == "QT_EINVAL"
+
+
+def test_bs16_loopback_two_ranks(qt, ctx):
+    import threading
+    import torch
+    rng = np.random.default_rng(164)
+    M = random_bm16(rng, 48, 0.1, "int", 128)
+    full = (mk(qt, ctx, M) @ mk(qt, ctx, M)).to_blocks()
+    bounds = [0, 20, 48]
+    hub = qt.LoopbackHub(2)
+    out, errs = [None] * 2, []
+
+    def rank_fn(g):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            c = qt.Context(0, stream=s, loopback=(hub, g, 2))
+            m = (M.brow >= bounds[g]) & (M.brow < bounds[g + 1])
+            A = qt.Matrix.from_blocks(c, M.n, M.leaf_dim, 16, M.brow[m], M.bcol[m], M.vals[m], row_bounds=bounds)
+            C, st = A.multiply(A)
+            T = C.truncate(50.0)
+            out[g] = (C.to_blocks(), C.info(), T.to_blocks())
+            for x in (T, C, A):
+                x.close()
+            c.close()
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=rank_fn, args=(g,)) for g in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    hub.close()
+    assert not errs, errs
+    tr = oracle.truncate(*full, 50.0)
+    for g in range(2):
+        (r, c, v), info, (tr_r, tr_c, tr_v) = out[g]
+        m = (full[0] >= bounds[g]) & (full[0] < bounds[g + 1])
+        assert np.array_equal(r, full[0][m]) and np.array_equal(v, full[2][m])
+        assert (info["row_lo"], info["row_hi"]) == (bounds[g], bounds[g + 1])
+        mt = (tr[0] >= bounds[g]) & (tr[0] < bounds[g + 1])
+        assert np.array_equal(tr_r, tr[0][mt]) and np.array_equal(tr_c, tr[1][mt])

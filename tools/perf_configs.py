@@ -144,10 +144,11 @@ def leaf_sweep(ctx, stream):
     _single): C = A*B at N = 4096 as ONE leaf, blocks of size bs placed
     uniformly at random with a given fill factor (A and B independent),
     FP64 and FP32; device time of qt_multiply, effective GFLOP/s over nonzero
-    block products (2 bs^3 each).  Block size 16 is not built (reading C-4)."""
+    block products (2 bs^3 each).  Block size 16 runs as quadrants of the
+    32-blocks (reading C-27): only its 16-block products are counted."""
     n = 4096
     for dtype in (np.float64, np.float32):
-        for bs in (32, 64):
+        for bs in (16, 32, 64):
             nb = n // bs
             for fill in (0.01, 0.02, 0.05, 0.1, 0.2, 0.5, 1.0):
                 rng = np.random.default_rng(int(1000 * fill) + bs)
