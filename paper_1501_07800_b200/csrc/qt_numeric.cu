@@ -245,7 +245,7 @@ __device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, int keep
   return d;
 }
 
-template <bool kTA, bool kTB, bool kSym, bool kScreen>
+template <bool kTA, bool kTB, bool kSym, bool kScreen, bool kPhase>
 __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -291,15 +291,17 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
     // (late enough to keep the dynamic balance of the tail).
     constexpr int kGrabAhead = 8;
     const int G = a.group;
-    // phase launches of the multi-rank overlap: work items map[t_off + i]
+    // phase launches of the multi-rank overlap (kPhase): work items map[t_off + i]
+    // (a separate instantiation: the runtime checks cost the plain kernel 2-5 %
+    // on sparse patterns)
     int ntiles = (int)a.ntiles, t_off = 0;
-    if (a.phase) {
+    if (kPhase) {
       const int ns = *a.nsel;
       const int nt = a.split ? (int)a.ntiles / 4 : (int)a.ntiles;
       t_off = a.phase == 1 ? 0 : ns;
       ntiles = (a.phase == 1 ? ns : nt - ns) * (a.split ? 4 : 1);
     }
-    auto tile_of = [&](int i) { return a.tile_map ? a.tile_map[t_off + i] : i; };
+    auto tile_of = [&](int i) { return kPhase ? a.tile_map[t_off + i] : i; };
     // current group: tiles [g_t0, g_t0+g_n), lane l: task start of tile g_t0+l (lane g_n: end), C children
     int g_n = 0, g_ts = 0, g_pend = 0;
     int4 g_cc = make_int4(-1, -1, -1, -1);
@@ -631,15 +633,15 @@ __global__ void k_peak_dfma(double* out, int iters) {
 
 }  // namespace
 
-template <bool TA, bool TB, bool SYM = false, bool SCR = false>
+template <bool TA, bool TB, bool SYM = false, bool SCR = false, bool PH = false>
 static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
   static bool attr_set = false;
   if (!attr_set) {
-    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<TA, TB, SYM, SCR>,
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<TA, TB, SYM, SCR, PH>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
     attr_set = true;
   }
-  k_numeric_f64<TA, TB, SYM, SCR><<<grid, kNumThreads, kSmemBytes, a.stream ? a.stream : ctx->stream>>>(a);
+  k_numeric_f64<TA, TB, SYM, SCR, PH><<<grid, kNumThreads, kSmemBytes, a.stream ? a.stream : ctx->stream>>>(a);
 }
 
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
@@ -658,7 +660,13 @@ void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
   const int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
   // a.group: one tile per grab (dense/banded: finest dynamic balance) or
   // grouped grabs (sparse patterns: amortise the scheduler and metadata latency)
-  if (a.trans & 4) {  // symmetric square
+  if (a.phase) {  // multi-rank overlap phases: plain (or bs-16 masked) products only
+    if (a.trans & 7) fail(QT_EINVAL, "overlap phases are built for the plain product");
+    if (a.subA)
+      launch_numeric_t<false, false, false, true, true>(ctx, a, grid);
+    else
+      launch_numeric_t<false, false, false, false, true>(ctx, a, grid);
+  } else if (a.trans & 4) {  // symmetric square
     launch_numeric_t<false, false, true>(ctx, a, grid);
   } else if (a.normA || a.subA) {  // norm-screened product, or block size 16 (quadrant masks)
     switch (a.trans & 3) {

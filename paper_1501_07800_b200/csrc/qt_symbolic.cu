@@ -55,9 +55,14 @@ __device__ __forceinline__ bool on_diagonal(uint64_t ckey) {
 // are computed: not the (1,0) child of a diagonal node in the symmetric
 // square's pruned levels, and only children whose block rows meet the row
 // window [rlo, rhi) (a rank's strip in the multi-rank symmetric square)
-__device__ __forceinline__ int cmask(uint64_t ck, int l, int L, bool prune, int32_t rlo, int32_t rhi) {
+// (the node key is loaded only when a rule needs it)
+__device__ __forceinline__ int cmask(const uint64_t* __restrict__ ckp, int l, int L, bool prune, int32_t rlo,
+                                     int32_t rhi) {
+  const bool window = rlo > 0 || rhi < INT32_MAX;
+  if (!prune && !window) return 0xF;
+  const uint64_t ck = *ckp;
   int m = (prune && on_diagonal(ck)) ? 0xB : 0xF;
-  if (rlo > 0 || rhi < INT32_MAX) {
+  if (window) {
     const int64_t r = morton_row(ck);
     const int sh = L - l - 1;
 #pragma unroll
@@ -161,6 +166,10 @@ struct SmallBfsArgs {
   const uint8_t* subB;
 };
 
+// kExt: the block-size-16 pair test and the C row window (multi-rank
+// symmetric square) are compiled in only for the launches that use them — the
+// runtime checks cost the plain BFS ~10 % (cfg4)
+template <bool kExt>
 __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) {
   using BS = cub::BlockScan<int, kSmallThreads>;
   __shared__ typename BS::TempStorage tmp;
@@ -191,16 +200,17 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     const uint64_t* ck = a.ckey[cur];
     const int4* cA = a.childA[l];
     const int4* cB = a.childB[l];
-    const bool lastl = l + 1 == a.L && a.subA;
+    const bool lastl = kExt && l + 1 == a.L && a.subA;
     const Screen sc{a.normA[l + 1], a.normB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
                     a.trans & 3};
+    const int32_t rlo = kExt ? a.row_lo : 0, rhi = kExt ? a.row_hi : INT32_MAX;
     // 1. child-task counts per (task, C child), group-major
     for (int p = tid; p < F; p += kSmallThreads) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
       int c[4];
       child_counts(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym), c,
                    sc, sym);
-      const int cm = cmask(ck[s], l, a.L, prune, a.row_lo, a.row_hi);
+      const int cm = cmask(ck + s, l, a.L, prune, rlo, rhi);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         if (!((cm >> q) & 1)) c[q] = 0;
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     for (int p = tid; p < F && l + 1 < a.L; p += kSmallThreads) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
       emit_task(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym),
-                4ll * c0 + (p - c0), m, s, cmask(ck[s], l, a.L, prune, a.row_lo, a.row_hi), sc, sym, a.off,
+                4ll * c0 + (p - c0), m, s, cmask(ck + s, l, a.L, prune, rlo, rhi), sc, sym, a.off,
                 a.gidx, a.pa[nxt],
                 a.pb[nxt],
                 a.pc[nxt]);
@@ -361,6 +371,7 @@ __device__ __forceinline__ int32_t cta_lower_bound(const int32_t* v, int32_t n, 
   return lo;
 }
 
+template <bool kExt>
 __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) {
   using BS = cub::BlockScan<int, kLargeThreads>;
   using BR = cub::BlockReduce<int, kLargeThreads>;
@@ -378,9 +389,10 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
   for (int l = a.l_begin; l < a.L; ++l) {
     const bool last = l == a.L - 1;
     const int mode = (a.trans & 7) | ((sym && l < (a.trans >> 8)) ? 8 : 0);
-    const bool lastl = l + 1 == a.L && a.subA;
+    const bool lastl = kExt && l + 1 == a.L && a.subA;
     const Screen sc{a.normA[l + 1], a.normB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
                     a.trans & 3};
+    const int32_t rlo = kExt ? a.row_lo : 0, rhi = kExt ? a.row_hi : INT32_MAX;
     const int32_t F = a.f_out[l], ns = a.ns_out[l];
     const int32_t* pa = a.pa[l];
     const int32_t* pb = a.pb[l];
@@ -395,7 +407,7 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
     auto counts = [&](int32_t p, int32_t sgrp, int (&c)[4]) {
       child_counts(op_children(cA, pa[p], mode & 1, sym), op_children(cB, pb[p], mode & 2, sym), c, sc,
                    sym);
-      const int cm = cmask(ck[sgrp], l, a.L, mode & 8, a.row_lo, a.row_hi);
+      const int cm = cmask(ck + sgrp, l, a.L, mode & 8, rlo, rhi);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         if (!((cm >> q) & 1)) c[q] = 0;
@@ -528,7 +540,7 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
         if (live) {
           c0 = cs[sg];
           c1 = cs[sg + 1];
-          cm = cmask(ck[sg], l, a.L, mode & 8, a.row_lo, a.row_hi);
+          cm = cmask(ck + sg, l, a.L, mode & 8, rlo, rhi);
           const int4 o4 = *reinterpret_cast<const int4*>(a.slot_off + 4ll * sg);
           const int4 g4 = *reinterpret_cast<const int4*>(gx + 4ll * sg);
           pos[0] = o4.x; pos[1] = o4.y; pos[2] = o4.z; pos[3] = o4.w;
@@ -587,7 +599,10 @@ int large_bfs_grid(qt_ctx ctx) {
   static int per_sm = -1;
   if (per_sm < 0) {
     int n = 0;
-    QT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_bfs_large, kLargeThreads, 0));
+    int n1 = 0;
+    QT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_bfs_large<false>, kLargeThreads, 0));
+    QT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, k_bfs_large<true>, kLargeThreads, 0));
+    n = std::min(n, n1);
     if (n < 1) fail(QT_ECUDA, "k_bfs_large cannot be resident");
     per_sm = 1;
   }
@@ -742,7 +757,11 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       sa.ns_out = nsd;
       sa.f_out = fd;
       tr.mark("small_alloc");
-      k_bfs_small<<<1, kSmallThreads, 0, st>>>(sa);
+      const bool ext = sa.subA || row_lo > 0 || row_hi < INT32_MAX;
+      if (ext)
+        k_bfs_small<true><<<1, kSmallThreads, 0, st>>>(sa);
+      else
+        k_bfs_small<false><<<1, kSmallThreads, 0, st>>>(sa);
       QT_LAUNCH_CHECK(ctx);
       const bool all_small = l_end == L;
       const int cb = (all_small ? L - 1 : l_end) & 1;
@@ -822,7 +841,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         la.f_out = fd;
         la.bar = reinterpret_cast<unsigned*>(ctx->counters.as<int>() + 40);
         void* kargs[] = {&la};
-        QT_CUDA(cudaLaunchCooperativeKernel((const void*)k_bfs_large, dim3(G), dim3(kLargeThreads), kargs, 0,
+        QT_CUDA(cudaLaunchCooperativeKernel(ext ? (const void*)k_bfs_large<true> : (const void*)k_bfs_large<false>,
+                                            dim3(G), dim3(kLargeThreads), kargs, 0,
                                             st));
         ctx->launches += 1;
         QT_LAUNCH_CHECK(ctx);
