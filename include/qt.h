@@ -261,6 +261,24 @@ const char* qt_last_error(void);
  * local multiply.  Only the NCCL transfers are replaced by device copies.
  * C holds rank g's block rows of A*B; `st` reports what rank g would receive.
  * Used to test the distributed path on one GPU. */
+/* Row-strip plan (the locality-aware partition of P:82-97,
+ * §5.2): `parts` contiguous block-row strips of C = A·B, boundaries
+ * at multiples of `align_rows` block rows (a quadtree node row: leaf_dim /
+ * block_size for leaf-aligned strips), balanced by block products — row I of
+ * C costs sum over A(I,K) of nnz(B(K,:)) products — so that the largest strip
+ * is as small as any contiguous aligned partition allows.  Host-only, O(nnz).
+ * ctx: NULL or a single-rank context = the arrays are the whole A (block rows
+ * and columns) and B (block rows); a multi-rank context = each rank passes its
+ * own blocks and the counts are summed over ranks (collective; every rank gets
+ * the same bounds).  Out: bounds[parts+1] (caller block rows, bounds[0] = 0,
+ * bounds[parts] = n / block_size; trailing strips may be empty) and, if not
+ * NULL, strip_products[parts].  Use the bounds as qt_create's row_bounds.
+ * Errors: QT_EINVAL (sizes, NULL arrays), QT_ERANGE (a block outside the
+ * grid), QT_ENCCL (multi-rank). */
+qt_status qt_plan_strips(qt_ctx ctx, int64_t n, int32_t block_size, int32_t align_rows, int64_t nb_a,
+                         const int32_t* a_brow, const int32_t* a_bcol, int64_t nb_b, const int32_t* b_brow,
+                         int32_t parts, int32_t* bounds, int64_t* strip_products);
+
 /* The multi-rank symmetric square of rank g out of P virtual ranks on this
  * single (world == 1) context: A is the whole upper-triangular U; rank g's
  * block rows are [row_bounds[g], row_bounds[g+1]); the blocks it would receive

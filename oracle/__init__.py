@@ -362,6 +362,40 @@ def exchange_plan_symm(bounds, u_rc, block_bytes: int):
     return out
 
 
+def row_products(nbr: int, a_rc, b_rc):
+    """Block products of each row of C = A·B (the work of a
+    row strip), by enumeration: for every A block (I, K), the blocks of B's row K."""
+    ar = np.asarray(a_rc[0], np.int64)
+    ac = np.asarray(a_rc[1], np.int64)
+    nnz_b = np.bincount(np.asarray(b_rc[0], np.int64), minlength=nbr)
+    out = np.zeros(nbr, np.int64)
+    for i, k in zip(ar.tolist(), ac.tolist()):
+        out[i] += nnz_b[k]
+    return out
+
+
+def strips_min_max(weights, parts: int, align: int):
+    """Smallest possible largest strip load over all partitions of the rows
+    into `parts` contiguous strips with boundaries at multiples of `align`
+    (brute-force dynamic program over the aligned chunks)."""
+    w = np.asarray(weights, np.int64)
+    nch = -(-len(w) // align)
+    cw = [int(w[c * align:(c + 1) * align].sum()) for c in range(nch)]
+    pre = [0]
+    for x in cw:
+        pre.append(pre[-1] + x)
+    INF = float("inf")
+    best = [[INF] * (nch + 1) for _ in range(parts + 1)]
+    best[0][0] = 0
+    for g in range(1, parts + 1):
+        for j in range(nch + 1):
+            for i in range(j + 1):
+                v = max(best[g - 1][i], pre[j] - pre[i])
+                if v < best[g][j]:
+                    best[g][j] = v
+    return int(min(best[g][nch] for g in range(1, parts + 1)))
+
+
 def spsumma_volume(m: float, N: float, p: float) -> float:
     """Elements each process fetches under random permutation + Sparse SUMMA:
     2 m N / sqrt(p) (Eq. eq:sqrtp_equation)."""

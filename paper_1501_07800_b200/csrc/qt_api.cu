@@ -607,6 +607,106 @@ qt_status qt_nccl_unique_id(void* out128) {
   API_CATCH
 }
 
+// ------------------------------------------------------------ row-strip plan (a3)
+
+qt_status qt_plan_strips(qt_ctx ctx, int64_t n, int32_t block_size, int32_t align_rows, int64_t nb_a,
+                         const int32_t* a_brow, const int32_t* a_bcol, int64_t nb_b, const int32_t* b_brow,
+                         int32_t parts, int32_t* bounds, int64_t* strip_products) {
+  API_TRY
+  if (!bounds) fail(QT_EINVAL, "bounds is NULL");
+  if (block_size != 16 && block_size != 32 && block_size != 64) fail(QT_EINVAL, "block_size %d", block_size);
+  if (n <= 0 || n % block_size != 0) fail(QT_EINVAL, "n=%lld must be a positive multiple of block_size",
+                                          (long long)n);
+  if (parts < 1) fail(QT_EINVAL, "parts=%d", parts);
+  if (align_rows < 1) fail(QT_EINVAL, "align_rows=%d", align_rows);
+  if ((nb_a > 0 && (!a_brow || !a_bcol)) || (nb_b > 0 && !b_brow) || nb_a < 0 || nb_b < 0)
+    fail(QT_EINVAL, "NULL or negative block arrays");
+  const int64_t nbr = n / block_size;
+  if (nbr > (1ll << 22)) fail(QT_EINVAL, "too many block rows");
+  // B's blocks per row, then products per C row: prod(I) = sum over A(I,K) of nnz(B(K,:))
+  std::vector<int64_t> rowB(nbr, 0), prod(nbr, 0);
+  for (int64_t t = 0; t < nb_b; ++t) {
+    const int32_t r = b_brow[t];
+    if (r < 0 || r >= nbr) fail(QT_ERANGE, "B block %lld: brow=%d outside [0,%lld)", (long long)t, r, (long long)nbr);
+    ++rowB[r];
+  }
+  const bool multi = ctx && ctx->world > 1;
+  if (multi) {  // every rank passed its own blocks: sum the row counts over ranks
+    std::vector<int64_t> all((size_t)nbr * ctx->world);
+    allgather_i64(ctx, rowB.data(), all.data(), (int)nbr);
+    for (int64_t r = 0; r < nbr; ++r) {
+      int64_t v = 0;
+      for (int q = 0; q < ctx->world; ++q) v += all[(size_t)q * nbr + r];
+      rowB[r] = v;
+    }
+  }
+  for (int64_t t = 0; t < nb_a; ++t) {
+    const int32_t r = a_brow[t], c = a_bcol[t];
+    if (r < 0 || r >= nbr || c < 0 || c >= nbr)
+      fail(QT_ERANGE, "A block %lld at (brow=%d, bcol=%d) outside [0,%lld)", (long long)t, r, c, (long long)nbr);
+    prod[r] += rowB[c];
+  }
+  if (multi) {
+    std::vector<int64_t> all((size_t)nbr * ctx->world);
+    allgather_i64(ctx, prod.data(), all.data(), (int)nbr);
+    for (int64_t r = 0; r < nbr; ++r) {
+      int64_t v = 0;
+      for (int q = 0; q < ctx->world; ++q) v += all[(size_t)q * nbr + r];
+      prod[r] = v;
+    }
+  }
+  // chunks of align_rows rows; contiguous partition into `parts` strips
+  // minimising the largest strip (binary search on the bound, greedy packing
+  // from the top; every rank computes the same boundaries)
+  const int64_t nch = (nbr + align_rows - 1) / align_rows;
+  std::vector<int64_t> w(nch, 0);
+  for (int64_t r = 0; r < nbr; ++r) w[r / align_rows] += prod[r];
+  int64_t lo = 0, hi = 0;
+  for (int64_t c = 0; c < nch; ++c) {
+    lo = std::max(lo, w[c]);
+    hi += w[c];
+  }
+  auto strips_for = [&](int64_t cap) {
+    int64_t cnt = 1, cur = 0;
+    for (int64_t c = 0; c < nch; ++c) {
+      if (cur + w[c] > cap) {
+        ++cnt;
+        cur = 0;
+      }
+      cur += w[c];
+    }
+    return cnt;
+  };
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (strips_for(mid) <= parts) hi = mid;
+    else lo = mid + 1;
+  }
+  // boundaries of the greedy packing at the optimal bound; unused strips are empty at the end
+  std::vector<int32_t> b(parts + 1, (int32_t)nbr);
+  b[0] = 0;
+  {
+    int g = 1;
+    int64_t cur = 0;
+    for (int64_t c = 0; c < nch; ++c) {
+      if (cur + w[c] > lo && g < parts) {
+        b[g++] = (int32_t)std::min<int64_t>(c * align_rows, nbr);
+        cur = 0;
+      }
+      cur += w[c];
+    }
+  }
+  for (int g = 0; g <= parts; ++g) bounds[g] = b[g];
+  if (strip_products) {
+    for (int g = 0; g < parts; ++g) {
+      int64_t v = 0;
+      for (int64_t r = b[g]; r < b[g + 1]; ++r) v += prod[r];
+      strip_products[g] = v;
+    }
+  }
+  API_CATCH
+}
+
 qt_status qt_symm_square_virtual(qt_mat A, int32_t P, int32_t g, const int32_t* row_bounds, qt_mat* C,
                                  qt_stats* st) {
   API_TRY

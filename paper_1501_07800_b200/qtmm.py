@@ -76,6 +76,7 @@ def _load():
         "qt_multiply_screened": [P, P, ctypes.c_double, P, P],
         "qt_multiply_virtual": [P, P, i32, i32, P, P, P],
         "qt_symm_square_virtual": [P, i32, i32, P, P, P],
+        "qt_plan_strips": [P, i64, i32, i32, i64, P, P, i64, P, i32, P, P],
         "qt_truncate": [P, ctypes.c_double, P],
         "qt_info": [P, P, P, P, P, P, P, P, P],
         "qt_level_nodes": [P, P, i32, P],
@@ -103,7 +104,7 @@ _lib = _load()
 EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_nccl_unique_id", "qt_create", "qt_multiply",
             "qt_multiply_async",
             "qt_multiply_ex", "qt_symm_square", "qt_multiply_screened",
-            "qt_multiply_virtual", "qt_symm_square_virtual", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
+            "qt_multiply_virtual", "qt_symm_square_virtual", "qt_plan_strips", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
             "qt_read_back_async", "qt_ctx_synchronize", "qt_destroy", "qt_last_error", "qt_kernel_launches", "qt_fp64_peak",
             "qt_loopback_hub_create", "qt_loopback_hub_destroy", "qt_ctx_create_loopback")
 
@@ -201,6 +202,22 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def plan_strips(n: int, block_size: int, parts: int, a_rc, b_rows, align_rows: int = 1, ctx=None):
+    """Product-balanced block-row strips of C = A·B (qt_plan_strips).
+    ``a_rc`` = (brow, bcol) of A's blocks, ``b_rows`` = B's block rows; with a
+    multi-rank ``ctx`` each rank passes its own blocks (collective).  Returns
+    (bounds[parts+1], products per strip)."""
+    ar = np.ascontiguousarray(np.asarray(a_rc[0], dtype=np.int32))
+    ac = np.ascontiguousarray(np.asarray(a_rc[1], dtype=np.int32))
+    br = np.ascontiguousarray(np.asarray(b_rows, dtype=np.int32))
+    bounds = np.zeros(parts + 1, np.int32)
+    prods = np.zeros(parts, np.int64)
+    _check(_lib.qt_plan_strips(ctx.handle if ctx is not None else None, int(n), int(block_size), int(align_rows),
+                               ar.shape[0], _ptr(ar) if ar.size else None, _ptr(ac) if ac.size else None,
+                               br.shape[0], _ptr(br) if br.size else None, int(parts), _ptr(bounds), _ptr(prods)))
+    return bounds, prods
 
 
 class LoopbackHub:
