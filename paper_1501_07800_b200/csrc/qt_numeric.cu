@@ -65,11 +65,12 @@ struct __align__(16) StageHdr {
 // a block product survives: both present and (screening) norms^2 product >= tau^2
 // (block size 16: "screening" by the quadrant masks — a product whose
 // quadrants never meet adds only zeros and is skipped, as in the BFS)
-template <bool kTA, bool kTB, bool kScreen>
+// kScreen: 0 none, 1 norms, 2 block-size-16 quadrant masks
+template <bool kTA, bool kTB, int kScreen>
 __device__ __forceinline__ bool prod_ok(int a, int b, const NumericArgs& na) {
   if (a < 0 || b < 0) return false;
-  if (!kScreen) return true;
-  if (na.subA) {
+  if (kScreen == 0) return true;
+  if (kScreen == 2) {
     int x = na.subA[a], y = na.subB[b];
     if (kTA) x = mask_t(x);
     if (kTB) y = mask_t(y);
@@ -225,7 +226,7 @@ __device__ __forceinline__ void warp_step(double (&acc)[4][2][2][2], const doubl
 struct StepDesc {
   int a0, a1, b0, b1, meta;
 };
-template <bool kTA, bool kTB, bool kSym, bool kScreen>
+template <bool kTA, bool kTB, bool kSym, int kScreen>
 __device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, int keep, const NumericArgs& a) {
   // A child (i,kb) in slot 2i+kb ; B child (kb,j) in slot 2kb+j
   int ta0, ta1, tb0, tb1;
@@ -245,7 +246,7 @@ __device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, int keep
   return d;
 }
 
-template <bool kTA, bool kTB, bool kSym, bool kScreen, bool kPhase>
+template <bool kTA, bool kTB, bool kSym, int kScreen, bool kPhase>
 __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -633,7 +634,7 @@ __global__ void k_peak_dfma(double* out, int iters) {
 
 }  // namespace
 
-template <bool TA, bool TB, bool SYM = false, bool SCR = false, bool PH = false>
+template <bool TA, bool TB, bool SYM = false, int SCR = 0, bool PH = false>
 static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
   static bool attr_set = false;
   if (!attr_set) {
@@ -663,17 +664,24 @@ void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
   if (a.phase) {  // multi-rank overlap phases: plain (or bs-16 masked) products only
     if (a.trans & 7) fail(QT_EINVAL, "overlap phases are built for the plain product");
     if (a.subA)
-      launch_numeric_t<false, false, false, true, true>(ctx, a, grid);
+      launch_numeric_t<false, false, false, 2, true>(ctx, a, grid);
     else
-      launch_numeric_t<false, false, false, false, true>(ctx, a, grid);
+      launch_numeric_t<false, false, false, 0, true>(ctx, a, grid);
   } else if (a.trans & 4) {  // symmetric square
     launch_numeric_t<false, false, true>(ctx, a, grid);
-  } else if (a.normA || a.subA) {  // norm-screened product, or block size 16 (quadrant masks)
+  } else if (a.normA) {  // norm-screened product
     switch (a.trans & 3) {
-      case 0: launch_numeric_t<false, false, false, true>(ctx, a, grid); break;
-      case 1: launch_numeric_t<true, false, false, true>(ctx, a, grid); break;
-      case 2: launch_numeric_t<false, true, false, true>(ctx, a, grid); break;
-      default: launch_numeric_t<true, true, false, true>(ctx, a, grid); break;
+      case 0: launch_numeric_t<false, false, false, 1>(ctx, a, grid); break;
+      case 1: launch_numeric_t<true, false, false, 1>(ctx, a, grid); break;
+      case 2: launch_numeric_t<false, true, false, 1>(ctx, a, grid); break;
+      default: launch_numeric_t<true, true, false, 1>(ctx, a, grid); break;
+    }
+  } else if (a.subA) {  // block size 16: products whose quadrant masks never meet are skipped
+    switch (a.trans & 3) {
+      case 0: launch_numeric_t<false, false, false, 2>(ctx, a, grid); break;
+      case 1: launch_numeric_t<true, false, false, 2>(ctx, a, grid); break;
+      case 2: launch_numeric_t<false, true, false, 2>(ctx, a, grid); break;
+      default: launch_numeric_t<true, true, false, 2>(ctx, a, grid); break;
     }
   } else {
     switch (a.trans & 3) {
