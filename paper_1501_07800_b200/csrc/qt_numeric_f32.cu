@@ -327,26 +327,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
               S.hdr[stage].tile = t;
               S.hdr[stage].flags = first ? F_FIRST : 0;
               mbar_arrive_expect_tx(&S.full[stage], 8u * kBlkBytes);
-              uint8_t* dst = data + (size_t)stage * kStageBytes;
+            }
+            __syncwarp();
+            // eight lanes issue the eight 4 KiB copies at once (lane x < 4: A
+            // block x, lane 4 + x: B block x)
+            if (lane < 8) {
+              const int x = lane & 3;
+              int ref = -1;
 #pragma unroll
-              for (int x = 0; x < 4; ++x) {
+              for (int y = 0; y < 4; ++y)
+                if (y == x) ref = lane < 4 ? ac[y] : br[y];
+              const float* src;
+              if (kSym) {
                 // symmetric square: a block of U read transposed comes from the
                 // transposed copy of the pool, so the split warps read blocks as stored
-                const float* srcA;
-                const float* srcB;
-                if (kSym) {
-                  const float* poolT = static_cast<const float*>(a.poolT);
-                  srcA = ac[x] < 0 ? zeros : ((ac[x] & 1) ? poolT : poolA) + (size_t)(ac[x] >> 2) * 1024;
-                  srcB = br[x] < 0 ? zeros : ((br[x] & 1) ? poolT : poolA) + (size_t)(br[x] >> 2) * 1024;
-                } else {
-                  srcA = ac[x] >= 0 ? poolA + (size_t)ac[x] * 1024 : zeros;
-                  const int b = br[x];
-                  srcB = b < 0 ? zeros
-                               : (b < a.splitB ? poolB + (size_t)b * 1024 : poolB2 + (size_t)(b - a.splitB) * 1024);
-                }
-                bulk_g2s(dst + x * kBlkBytes, srcA, kBlkBytes, &S.full[stage]);
-                bulk_g2s(dst + (4 + x) * kBlkBytes, srcB, kBlkBytes, &S.full[stage]);
+                const float* poolT = static_cast<const float*>(a.poolT);
+                src = ref < 0 ? zeros : ((ref & 1) ? poolT : poolA) + (size_t)(ref >> 2) * 1024;
+              } else if (lane < 4) {
+                src = ref >= 0 ? poolA + (size_t)ref * 1024 : zeros;
+              } else {
+                src = ref < 0 ? zeros
+                              : (ref < a.splitB ? poolB + (size_t)ref * 1024 : poolB2 + (size_t)(ref - a.splitB) * 1024);
               }
+              bulk_g2s(data + (size_t)stage * kStageBytes + lane * kBlkBytes, src, kBlkBytes, &S.full[stage]);
             }
             __syncwarp();
             first = false;
