@@ -92,6 +92,10 @@ struct Smem {
   uint64_t tfull[2];        // accumulator ready (commit + MMA-lane arrive)
   uint64_t tempty[2];       // epilogue drained the hi*hi accumulator (4 warp arrivals)
   uint64_t cfree;           // epilogue drained the cross accumulator (4 warp arrivals)
+  // producer: the current batch's block references, row = task lane: A(x, kk)
+  // at 4x+kk, B(kk, x) at 16+4kk+x, and at 32 the mask of k-steps with an A
+  // and a B block
+  int refs[32][33];
 };
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + sizeof(Smem);
 
@@ -308,20 +312,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
             }
           }
         }
-        const int nloc = min(32, p1 - pb0);
-        for (int u = 0; u < nloc; ++u) {
+        __syncwarp();  // (every lane is done with the previous batch's table)
+        {
+          int vm = 0;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            int ac[4], br[4];
             bool anyA = false, anyB = false;
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
-              ac[x] = __shfl_sync(0xffffffffu, ab[x][kk], u);
-              br[x] = __shfl_sync(0xffffffffu, bb[kk][x], u);
-              anyA |= ac[x] >= 0;
-              anyB |= br[x] >= 0;
+              S.refs[lane][4 * x + kk] = ab[x][kk];
+              S.refs[lane][16 + 4 * kk + x] = bb[kk][x];
+              anyA |= ab[x][kk] >= 0;
+              anyB |= bb[kk][x] >= 0;
             }
-            if (!(anyA && anyB)) continue;
+            vm |= (anyA && anyB ? 1 : 0) << kk;
+          }
+          S.refs[lane][32] = vm;
+        }
+        __syncwarp();
+        const int nloc = min(32, p1 - pb0);
+        for (int u = 0; u < nloc; ++u) {
+          const int vm = S.refs[u][32];
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            if (!((vm >> kk) & 1)) continue;
             mbar_wait(&S.empty[stage], phase ^ 1);
             if (lane == 0) {
               S.hdr[stage].tile = t;
@@ -332,11 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
             // eight lanes issue the eight 4 KiB copies at once (lane x < 4: A
             // block x, lane 4 + x: B block x)
             if (lane < 8) {
-              const int x = lane & 3;
-              int ref = -1;
-#pragma unroll
-              for (int y = 0; y < 4; ++y)
-                if (y == x) ref = lane < 4 ? ac[y] : br[y];
+              const int ref = S.refs[u][lane < 4 ? 4 * lane + kk : 16 + 4 * kk + (lane - 4)];
               const float* src;
               if (kSym) {
                 // symmetric square: a block of U read transposed comes from the
