@@ -125,3 +125,33 @@ def test_plan_multi_rank_loopback_then_multiply(qt):
         m = (full[0] >= bounds[g]) & (full[0] < bounds[g + 1])
         assert np.array_equal(r, full[0][m]) and np.array_equal(v, full[2][m])
         assert prods == rp[bounds[g]:bounds[g + 1]].sum()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_oracle_strips_min_max_vs_enumeration(seed):
+    """Pin the oracle's DP: exhaustive enumeration of every aligned boundary set."""
+    import itertools
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(3, 10))
+    w = rng.integers(0, 20, n)
+    parts = int(rng.integers(1, 5))
+    align = int(rng.integers(1, 3))
+    cuts = list(range(align, n, align))
+    best = None
+    for k in range(0, min(parts - 1, len(cuts)) + 1):
+        for cs in itertools.combinations(cuts, k):
+            b = [0, *cs, n]
+            m = max(int(w[b[i]:b[i + 1]].sum()) for i in range(len(b) - 1))
+            best = m if best is None else min(best, m)
+    assert oracle.strips_min_max(w, parts, align) == best
+
+
+def test_oracle_row_products_small_closed_form():
+    """Dense nbr x nbr A and B: every row of C has nbr^2 block products."""
+    nbr = 5
+    r, c = np.nonzero(np.ones((nbr, nbr), bool))
+    assert np.all(oracle.row_products(nbr, (r, c), (r, c)) == nbr * nbr)
+    # identity A: row I of C costs nnz(B row I)
+    br, bc = np.nonzero(np.tril(np.ones((nbr, nbr), bool)))
+    ii = np.arange(nbr)
+    assert np.array_equal(oracle.row_products(nbr, (ii, ii), (br, bc)), np.arange(1, nbr + 1))
