@@ -1,0 +1,116 @@
+"""Seeded randomized sweep over the entry points (needs a B200): random grid
+sizes (ragged against the 2x2 / 4x4 tiles and the leaves), densities from
+empty to full, leaf sizes, block sizes 16/32/64, FP64/FP32, transposed
+operands, the symmetric square, the screened product and virtual ranks —
+every result against the oracle on the same inputs (integer values: exact)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import qtgen
+
+pytestmark = pytest.mark.gpu
+N_MUL = int(os.environ.get("QT_FUZZ_MUL", 24))   # (larger sweeps: QT_FUZZ_MUL=300 QT_FUZZ_MISC=100)
+N_MISC = int(os.environ.get("QT_FUZZ_MISC", 10))
+
+
+@pytest.fixture(scope="module")
+def qt():
+    from paper_1501_07800_b200 import build
+    build.build()
+    from paper_1501_07800_b200 import qtmm
+    return qtmm
+
+
+@pytest.fixture(scope="module")
+def ctx(qt):
+    import torch
+    torch.cuda.init()
+    return qt.Context(0)
+
+
+def rand_int_bm(rng, nbr, p, bs, leaf, dtype, upper=False):
+    m = rng.random((nbr, nbr)) < p
+    if upper:
+        m = np.triu(m)
+    br, bc = np.nonzero(m)
+    v = rng.integers(-4, 5, size=(len(br), bs, bs)).astype(dtype)
+    if upper:
+        for t in range(len(br)):
+            if br[t] == bc[t]:
+                v[t] = np.triu(v[t]) + np.triu(v[t], 1).T
+    return qtgen.BlockMatrix(nbr * bs, leaf, bs, br.astype(np.int32), bc.astype(np.int32), v)
+
+
+def mk(qt, ctx, M):
+    return qt.Matrix.from_blocks(ctx, M.n, M.leaf_dim, M.bs, M.brow, M.bcol, M.vals)
+
+
+def t64(M):
+    return (M.brow, M.bcol, M.vals.astype(np.float64))
+
+
+def same(got, ref):
+    assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+    assert np.array_equal(got[2].astype(np.float64), ref[2])
+
+
+@pytest.mark.parametrize("seed", range(N_MUL))
+def test_fuzz_multiply(qt, ctx, seed):
+    rng = np.random.default_rng(7000 + seed)
+    bs = int(rng.choice([16, 32, 32, 64]))
+    dtype = np.float64 if rng.random() < 0.6 else np.float32
+    nbr = int(rng.integers(1, 40)) if bs != 16 else 2 * int(rng.integers(1, 20))
+    p = float(rng.choice([0.0, 0.03, 0.1, 0.3, 0.7, 1.0]))
+    gran = max(bs, 32)
+    leaf = gran * int(2 ** rng.integers(0, 4))
+    Am = rand_int_bm(rng, nbr, p, bs, leaf, dtype)
+    Bm = rand_int_bm(rng, nbr, p, bs, leaf, dtype)
+    ta, tb = bool(rng.random() < 0.3), bool(rng.random() < 0.3)
+    A, B = mk(qt, ctx, Am), mk(qt, ctx, Bm)
+    C, st = A.multiply_ex(B, ta, tb)
+    ref = oracle.spgemm_t(nbr, bs, t64(Am), t64(Bm), ta, tb)
+    same(C.to_blocks(), ref)
+    assert C.nblocks == len(ref[0])
+    # the product again as an operand
+    got2 = (C @ A).to_blocks()
+    ref2 = oracle.spgemm(nbr, bs, ref, t64(Am))
+    same(got2, ref2)
+
+
+@pytest.mark.parametrize("seed", range(N_MISC))
+def test_fuzz_symm_screen_truncate_virtual(qt, ctx, seed):
+    rng = np.random.default_rng(8000 + seed)
+    dtype = np.float64 if seed % 3 else np.float32
+    nbr = int(rng.integers(2, 36))
+    p = float(rng.choice([0.05, 0.2, 0.5]))
+    leaf = 32 * int(2 ** rng.integers(0, 3))
+    U = rand_int_bm(rng, nbr, p, 32, leaf, dtype, upper=True)
+    Au = mk(qt, ctx, U)
+    same(Au.symm_square()[0].to_blocks(), oracle.symm_square(nbr, 32, t64(U)))
+    M = rand_int_bm(rng, nbr, p, 32, leaf, dtype)
+    A = mk(qt, ctx, M)
+    full = (A @ A).to_blocks()
+    same(full, oracle.spgemm(nbr, 32, t64(M), t64(M)))
+    if dtype == np.float64:
+        tau = float(rng.choice([0.0, 50.0, 400.0]))
+        same(A.multiply_screened(A, tau)[0].to_blocks(), oracle.spgemm(nbr, 32, t64(M), t64(M), tau=tau))
+        tt = float(rng.choice([0.0, 100.0, 1000.0]))
+        r, c, v = A.truncate(tt).to_blocks()
+        rr, rc, rv = oracle.truncate(M.brow, M.bcol, M.vals, tt)
+        assert np.array_equal(r, rr) and np.array_equal(c, rc) and np.array_equal(v, rv)
+    P = int(rng.integers(2, 5))
+    cuts = np.sort(rng.choice(np.arange(0, nbr + 1), size=P - 1))
+    bounds = [0, *cuts.tolist(), nbr]
+    for g in range(P):
+        Cg, _ = A.multiply_virtual(A, P, g, bounds)
+        r, c, v = Cg.to_blocks()
+        m = (full[0] >= bounds[g]) & (full[0] < bounds[g + 1])
+        assert np.array_equal(r, full[0][m]) and np.array_equal(v, full[2][m])
+        Sg, _ = Au.symm_square_virtual(P, g, bounds)
+        sref = Au.symm_square()[0].to_blocks()
+        ms = (sref[0] >= bounds[g]) & (sref[0] < bounds[g + 1])
+        r, c, v = Sg.to_blocks()
+        assert np.array_equal(r, sref[0][ms]) and np.array_equal(v, sref[2][ms])
