@@ -45,13 +45,20 @@ namespace qt {
 
 namespace {
 
-// smem: a 4-deep ring of stages, each A raw[4] (16 KiB, read once by the A
-// split warps) | B[4] (landed, then hi in place) | B lo[4] = 48 KiB.
-constexpr int kStages = 4;
+// smem: two rings advanced once per step.  The B ring (5 stages): B[4]
+// (landed, then hi in place) | B lo[4] = 32 KiB, released by the MMAs'
+// commit.  The A ring (3 stages): A raw[4] = 16 KiB, read once by the A split
+// warps and released by them as soon as A is in TMEM — so an A landing slot
+// turns over in TMA latency + split time, without waiting for the MMAs, and
+// the B ring gets five stages in the same shared memory (the kernel's
+// throughput is bounded by ring depth / stage round-trip time).
+constexpr int kStages = 5;
+constexpr int kAStages = 3;
 constexpr int kBlkBytes = 4096;                 // 32x32 fp32
-constexpr int kLandBytes = 8 * kBlkBytes;       // A[4] | B[4] as landed
-constexpr int kBloOff = kLandBytes;             // B lo after the landing area
-constexpr int kStageBytes = kLandBytes + 4 * kBlkBytes;
+constexpr int kBloOff = 4 * kBlkBytes;          // B lo after B
+constexpr int kStageBytes = 8 * kBlkBytes;
+constexpr int kAStageBytes = 4 * kBlkBytes;
+constexpr int kARingOff = kStages * kStageBytes;
 constexpr int kSplitWarps = 8;
 constexpr int kProducerWarp = 4 + kSplitWarps;
 constexpr int kMmaWarp = kProducerWarp + 1;
@@ -82,12 +89,15 @@ struct __align__(16) Hdr {
 
 struct Smem {
   Hdr hdr[kStages];
+  Hdr ahdr[kAStages];       // flags of the A ring's steps
   int acc_tile[2];
   uint32_t tmem_base;
   uint32_t pad;
   uint64_t full[kStages];   // TMA landed (1 arrival + tx)
   uint64_t conv[kStages];   // A in TMEM and B hi/lo in smem (one arrival per split warp)
   uint64_t empty[kStages];  // MMAs that read the stage done (tcgen05.commit)
+  uint64_t afull[kAStages];   // A landed (1 arrival + tx)
+  uint64_t aempty[kAStages];  // A split into TMEM (one arrival per A split warp)
   uint64_t afree[2];        // MMAs that read the A slot done (tcgen05.commit)
   uint64_t tfull[2];        // accumulator ready (commit + MMA-lane arrive)
   uint64_t tempty[2];       // epilogue drained the hi*hi accumulator (4 warp arrivals)
@@ -97,7 +107,8 @@ struct Smem {
   // and a B block
   int refs[32][33];
 };
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + sizeof(Smem);
+constexpr size_t kSmemBytes =
+    1024 /*align slack*/ + (size_t)kStages * kStageBytes + (size_t)kAStages * kAStageBytes + sizeof(Smem);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -217,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
   // 1024-byte aligned start (kept as an offset from the shared array so the
   // compiler still emits shared-space LDS/STS for the split warps)
   uint8_t* data = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  Smem& S = *reinterpret_cast<Smem*>(data + (size_t)kStages * kStageBytes);
+  Smem& S = *reinterpret_cast<Smem*>(data + (size_t)kARingOff + (size_t)kAStages * kAStageBytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -225,6 +236,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
       mbar_init(&S.full[s], 1);
       mbar_init(&S.conv[s], kSplitWarps);
       mbar_init(&S.empty[s], 1);
+    }
+    for (int s = 0; s < kAStages; ++s) {
+      mbar_init(&S.afull[s], 1);
+      mbar_init(&S.aempty[s], 4);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&S.afree[b], 1);
@@ -252,8 +267,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
     const float* poolB = static_cast<const float*>(a.poolB);
     const float* poolB2 = static_cast<const float*>(a.poolB2);
     const float* zeros = static_cast<const float*>(a.zeros);
-    int stage = 0;
-    uint32_t phase = 0;
+    int stage = 0, ast = 0;
+    uint32_t phase = 0, aphase = 0;
+    auto next_stage = [&]() {
+      if (++stage == kStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+      if (++ast == kAStages) {
+        ast = 0;
+        aphase ^= 1;
+      }
+    };
+    // a step without data (end-of-tile / done marker) on both rings
+    auto post_marker = [&](int tile, int flags) {
+      mbar_wait(&S.empty[stage], phase ^ 1);
+      mbar_wait(&S.aempty[ast], aphase ^ 1);
+      if (lane == 0) {
+        S.hdr[stage].tile = tile;
+        S.hdr[stage].flags = flags;
+        S.ahdr[ast].flags = flags;
+        mbar_arrive(&S.full[stage]);
+        mbar_arrive(&S.afull[ast]);
+      }
+      __syncwarp();
+      next_stage();
+    };
     // phase launches of the multi-rank overlap: tiles map[t_off + i]
     int ntiles = (int)a.ntiles, t_off = 0;
     if (a.phase) {
@@ -266,12 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
       if (lane == 0) t = atomicAdd(a.counter, 1);
       t = __shfl_sync(0xffffffffu, t, 0);
       if (t >= ntiles) {
-        mbar_wait(&S.empty[stage], phase ^ 1);
-        if (lane == 0) {
-          S.hdr[stage].tile = -1;
-          S.hdr[stage].flags = F_DONE;
-          mbar_arrive(&S.full[stage]);
-        }
+        post_marker(-1, F_DONE);
         break;
       }
       if (a.tile_map) t = a.tile_map[t_off + t];
@@ -337,10 +371,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
           for (int kk = 0; kk < 4; ++kk) {
             if (!((vm >> kk) & 1)) continue;
             mbar_wait(&S.empty[stage], phase ^ 1);
+            mbar_wait(&S.aempty[ast], aphase ^ 1);
             if (lane == 0) {
               S.hdr[stage].tile = t;
               S.hdr[stage].flags = first ? F_FIRST : 0;
-              mbar_arrive_expect_tx(&S.full[stage], 8u * kBlkBytes);
+              S.ahdr[ast].flags = first ? F_FIRST : 0;
+              mbar_arrive_expect_tx(&S.full[stage], 4u * kBlkBytes);
+              mbar_arrive_expect_tx(&S.afull[ast], 4u * kBlkBytes);
             }
             __syncwarp();
             // eight lanes issue the eight 4 KiB copies at once (lane x < 4: A
@@ -359,29 +396,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
                 src = ref < 0 ? zeros
                               : (ref < a.splitB ? poolB + (size_t)ref * 1024 : poolB2 + (size_t)(ref - a.splitB) * 1024);
               }
-              bulk_g2s(data + (size_t)stage * kStageBytes + lane * kBlkBytes, src, kBlkBytes, &S.full[stage]);
+              if (lane < 4)
+                bulk_g2s(data + kARingOff + (size_t)ast * kAStageBytes + lane * kBlkBytes, src, kBlkBytes, &S.afull[ast]);
+              else
+                bulk_g2s(data + (size_t)stage * kStageBytes + (lane - 4) * kBlkBytes, src, kBlkBytes, &S.full[stage]);
             }
             __syncwarp();
             first = false;
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
-            }
+            next_stage();
           }
         }
       }
-      // end-of-tile marker (no data)
-      mbar_wait(&S.empty[stage], phase ^ 1);
-      if (lane == 0) {
-        S.hdr[stage].tile = t;
-        S.hdr[stage].flags = F_END;
-        mbar_arrive(&S.full[stage]);
-      }
-      __syncwarp();
-      if (++stage == kStages) {
-        stage = 0;
-        phase ^= 1;
-      }
+      post_marker(t, F_END);  // end-of-tile marker (no data)
     }
   } else if (warp >= 4 && warp < 8) {
     // ------------------------------------------------------------ split A -> TMEM
@@ -391,16 +417,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
     // truncation) and lo (exact remainder) and written to the A slot's hi and
     // lo columns.  A transposed A (C = A^T B) is read by columns instead.
     const int q = warp - 4;
-    int stage = 0;
-    uint32_t phase = 0;
+    int stage = 0, ast = 0;
+    uint32_t phase = 0, aphase = 0;
     int as = 0;
     uint32_t aph = 0;
     for (;;) {
-      mbar_wait(&S.full[stage], phase);
-      const int flags = S.hdr[stage].flags;
+      mbar_wait(&S.afull[ast], aphase);
+      const int flags = S.ahdr[ast].flags;
       if (!(flags & (F_END | F_DONE))) {
         mbar_wait(&S.afree[as], aph ^ 1);
-        const float* blk = reinterpret_cast<const float*>(data + (size_t)stage * kStageBytes + q * kBlkBytes);
+        const float* blk =
+            reinterpret_cast<const float*>(data + kARingOff + (size_t)ast * kAStageBytes + q * kBlkBytes);
         uint32_t hv[32], lv[32];
         const int r = lane;
         if (!kTA) {
@@ -436,11 +463,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.conv[stage]);
+      if (lane == 0) {
+        mbar_arrive(&S.aempty[ast]);
+        mbar_arrive(&S.conv[stage]);
+      }
       if (flags & F_DONE) break;
       if (++stage == kStages) {
         stage = 0;
         phase ^= 1;
+      }
+      if (++ast == kAStages) {
+        ast = 0;
+        aphase ^= 1;
       }
     }
   } else if (warp >= 8 && warp < 4 + kSplitWarps) {
@@ -458,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
       mbar_wait(&S.full[stage], phase);
       const int flags = S.hdr[stage].flags;
       if (!(flags & (F_END | F_DONE))) {
-        float4* hi = reinterpret_cast<float4*>(data + (size_t)stage * kStageBytes + (4 + q) * kBlkBytes);
+        float4* hi = reinterpret_cast<float4*>(data + (size_t)stage * kStageBytes + q * kBlkBytes);
         float4* lo = reinterpret_cast<float4*>(data + (size_t)stage * kStageBytes + kBloOff + q * kBlkBytes);
 #pragma unroll 1
         for (int atom = 0; atom < 4; ++atom) {
@@ -555,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
             // SW128, LBO 4096 B between the 32-wide atoms (= blocks), SBO 512 B
             // between 4-row K atoms, K-slice j (rows 8j..8j+7) at +1024 B;
             // K-major (transposed B): SW128, SBO 1024 B, K-slice j at +32 B.
-            const uint32_t stB = st + 4u * kBlkBytes, loB = st + kBloOff;
+            const uint32_t stB = st, loB = st + kBloOff;
             const uint64_t b_hi = kTB ? sdesc(stB + 32u * j, 16, 1024, kSW128)
                                       : sdesc(stB + 1024u * j, 4096, 512, kSW128_32B);
             const uint64_t b_lo = kTB ? sdesc(loB + 32u * j, 16, 1024, kSW128)
