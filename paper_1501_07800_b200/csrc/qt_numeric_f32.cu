@@ -533,6 +533,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
+    // One thread runs the whole role (waits, MMAs, commits): no warp
+    // synchronisation on the issue path; the other lanes go straight to the
+    // final barrier.
+    if (lane == 0) {
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -541,17 +545,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
     int ntiles_done = 0;  // tiles published to the epilogue (cross-accumulator uses)
     bool started = false;
     const uint32_t sbase = smem_u32(data);
+    // B descriptors of stage 0, K-slice 0; a stage / K-slice only moves the
+    // start-address field (address >> 4, < 2^14 for any shared address)
+    const uint64_t bd_hi0 = kTB ? sdesc(sbase, 16, 1024, kSW128) : sdesc(sbase, 4096, 512, kSW128_32B);
+    const uint64_t bd_lo0 = kTB ? sdesc(sbase + kBloOff, 16, 1024, kSW128) : sdesc(sbase + kBloOff, 4096, 512, kSW128_32B);
     for (;;) {
       mbar_wait(&S.conv[stage], phase);
       const int flags = S.hdr[stage].flags;
       const int tile = S.hdr[stage].tile;
       if (flags & F_DONE) {
         mbar_wait(&S.tempty[acc], acc_phase ^ 1);
-        if (lane == 0) {
-          S.acc_tile[acc] = -1;
-          mbar_arrive(&S.tfull[acc]);
-          mbar_arrive(&S.tfull[acc]);
-        }
+        S.acc_tile[acc] = -1;
+        mbar_arrive(&S.tfull[acc]);
+        mbar_arrive(&S.tfull[acc]);
         break;
       }
       if (flags & F_END) {
@@ -559,13 +565,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
         // wait for the buffer before publishing its (empty) result
         if (!started) mbar_wait(&S.tempty[acc], acc_phase ^ 1);
         started = false;
-        if (lane == 0) {
-          S.acc_tile[acc] = tile;
-          tc_commit(&S.tfull[acc]);      // fires when every MMA of the tile is done
-          mbar_arrive(&S.tfull[acc]);    // publishes acc_tile
-          mbar_arrive(&S.empty[stage]);  // the marker stage carried no data
-        }
-        __syncwarp();
+        S.acc_tile[acc] = tile;
+        tc_commit(&S.tfull[acc]);      // fires when every MMA of the tile is done
+        mbar_arrive(&S.tfull[acc]);    // publishes acc_tile
+        mbar_arrive(&S.empty[stage]);  // the marker stage carried no data
         ++ntiles_done;
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
@@ -577,8 +580,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
           started = true;
         }
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t st = sbase + (uint32_t)stage * kStageBytes;
+        {
+          const uint64_t so = (uint64_t)(((uint32_t)stage * kStageBytes) >> 4);
           const uint32_t d_main = tmem + (uint32_t)acc * 128;  // hi*hi
           const uint32_t d_cross = tmem + kColCross;           // hi*lo + lo*hi
           const uint32_t a_slot = tmem + kColA + 64u * (uint32_t)as;
@@ -589,11 +592,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
             // SW128, LBO 4096 B between the 32-wide atoms (= blocks), SBO 512 B
             // between 4-row K atoms, K-slice j (rows 8j..8j+7) at +1024 B;
             // K-major (transposed B): SW128, SBO 1024 B, K-slice j at +32 B.
-            const uint32_t stB = st, loB = st + kBloOff;
-            const uint64_t b_hi = kTB ? sdesc(stB + 32u * j, 16, 1024, kSW128)
-                                      : sdesc(stB + 1024u * j, 4096, 512, kSW128_32B);
-            const uint64_t b_lo = kTB ? sdesc(loB + 32u * j, 16, 1024, kSW128)
-                                      : sdesc(loB + 1024u * j, 4096, 512, kSW128_32B);
+            const uint64_t jo = (uint64_t)((kTB ? 32u * j : 1024u * j) >> 4);
+            const uint64_t b_hi = bd_hi0 + so + jo;
+            const uint64_t b_lo = bd_lo0 + so + jo;
             constexpr uint32_t kIdesc = idesc_tf32_ts<kTB>();
             const uint32_t acc_in = ((flags & F_FIRST) && j == 0) ? 0u : 1u;
             const uint32_t a_hi = a_slot + 8u * j, a_lo = a_hi + 32u;
@@ -604,7 +605,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
           tc_commit(&S.empty[stage]);
           tc_commit(&S.afree[as]);
         }
-        __syncwarp();
         as ^= 1;
       }
       if (++stage == kStages) {
@@ -612,6 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
         phase ^= 1;
       }
     }
+    }  // lane 0
   } else {
     // ------------------------------------------------------------ epilogue (warps 0-3)
     float* poolC = static_cast<float*>(a.poolC);
