@@ -12,7 +12,8 @@
 // accumulator in TMEM (128 lanes x 128 columns).  A step of the tile is one
 // inner block index k: the A column A(I0..I3, k) (128x32) and the B row
 // B(k, J0..J3) (32x128) — absent blocks are copied from a zero block — staged
-// by eight 4 KiB cp.async.bulk copies into a stage.  The pool stores every
+// by eight 4 KiB cp.async.bulk copies (A into the A ring, B into the B ring,
+// see below).  The pool stores every
 // FP32 block in the canonical 128-byte swizzle (qt_common.cuh swz32).  Per
 // step: 4 K-slices x 3 MMAs (M=128, N=128, K=8).
 //
@@ -31,8 +32,8 @@
 //   warps 0-3  epilogue  TMEM -> registers (tcgen05.ld 32x32b) -> C pool
 //   warps 4-7  split A   block q: rows -> (hi, lo) -> tcgen05.st into TMEM
 //   warps 8-11 split B   block q: fp32 -> (tf32 hi in place, lo copy) in smem
-//   warp 12    producer  task metadata + TMA bulk copies
-//   warp 13    MMA       one elected lane issues tcgen05.mma / commit
+//   warp 12    producer  task metadata + TMA bulk copies (eight lanes issue a step's copies)
+//   warp 13    MMA       lane 0 alone waits, issues tcgen05.mma / commit
 // Each C block is written once by one thread row-set: no atomics; summation
 // order per element is fixed (ascending k, and within a k the fixed K-slice
 // and hi/lo order), so results are run-to-run deterministic.
