@@ -552,8 +552,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
     const uint64_t bd_lo0 = kTB ? sdesc(sbase + kBloOff, 16, 1024, kSW128) : sdesc(sbase + kBloOff, 4096, 512, kSW128_32B);
     for (;;) {
       mbar_wait(&S.conv[stage], phase);
-      const int flags = S.hdr[stage].flags;
-      const int tile = S.hdr[stage].tile;
+      const int2 th = *reinterpret_cast<const int2*>(&S.hdr[stage]);  // (tile, flags) in one load
+      const int tile = th.x, flags = th.y;
       if (flags & F_DONE) {
         mbar_wait(&S.tempty[acc], acc_phase ^ 1);
         S.acc_tile[acc] = -1;
