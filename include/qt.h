@@ -237,7 +237,8 @@ qt_status qt_multiply_async(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st);
  * input copy and its compute).  The host buffers (pinned, for real overlap)
  * are valid only after qt_ctx_synchronize(ctx); A may be destroyed right
  * after the call.  Device destination pointers are written on the context
- * stream (no copy stream involved).
+ * stream (no copy stream involved).  Block sizes 16 and 64 complete the
+ * read-back before returning (as qt_read_back).
  * Errors: QT_EINVAL, QT_ECUDA. */
 qt_status qt_read_back_async(qt_mat A, int32_t* brow, int32_t* bcol, void* values);
 

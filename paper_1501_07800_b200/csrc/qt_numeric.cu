@@ -18,6 +18,8 @@
 // CTA = 3 streams x (4 consumer warps + 1 producer warp), persistent (one CTA
 // per SM), tiles handed out by an atomic counter in Morton order (L2
 // locality); each stream stages through its own ring of 8 KiB block slots.
+#include <atomic>
+
 #include <cuda_runtime.h>
 
 #include "qt_common.cuh"
@@ -636,11 +638,14 @@ __global__ void k_peak_dfma(double* out, int iters) {
 
 template <bool TA, bool TB, bool SYM = false, int SCR = 0, bool PH = false>
 static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<TA, TB, SYM, SCR, PH>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
-    attr_set = true;
+  // the dynamic shared memory limit is a per-device function attribute: set
+  // it once per device (bit d of `attr_set`; concurrent first calls only
+  // repeat an idempotent call)
+  static std::atomic<unsigned long long> attr_set{0};
+  const unsigned long long bit = 1ull << (ctx->device & 63);
+  if (!(attr_set.load(std::memory_order_acquire) & bit)) {
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<TA, TB, SYM, SCR, PH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+    attr_set.fetch_or(bit, std::memory_order_release);
   }
   k_numeric_f64<TA, TB, SYM, SCR, PH><<<grid, kNumThreads, kSmemBytes, a.stream ? a.stream : ctx->stream>>>(a);
 }

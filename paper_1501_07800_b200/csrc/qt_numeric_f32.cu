@@ -37,6 +37,8 @@
 // Each C block is written once by one thread row-set: no atomics; summation
 // order per element is fixed (ascending k, and within a k the fixed K-slice
 // and hi/lo order), so results are run-to-run deterministic.
+#include <atomic>
+
 #include <cuda_runtime.h>
 
 #include "qt_common.cuh"
@@ -706,11 +708,14 @@ void launch_transpose_blocks_f32(qt_ctx ctx, const void* in, void* out, int64_t 
 
 template <bool TA, bool TB, bool SYM = false>
 static void launch_f32_t(qt_ctx ctx, const NumericArgs32& a, int grid) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    QT_CUDA(cudaFuncSetAttribute(k_numeric_f32<TA, TB, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemBytes));
-    attr_set = true;
+  // the dynamic shared memory limit is a per-device function attribute: set
+  // it once per device (bit d of `attr_set`; concurrent first calls only
+  // repeat an idempotent call)
+  static std::atomic<unsigned long long> attr_set{0};
+  const unsigned long long bit = 1ull << (ctx->device & 63);
+  if (!(attr_set.load(std::memory_order_acquire) & bit)) {
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f32<TA, TB, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+    attr_set.fetch_or(bit, std::memory_order_release);
   }
   k_numeric_f32<TA, TB, SYM><<<grid, kThreads, kSmemBytes, a.stream ? a.stream : ctx->stream>>>(a);
 }

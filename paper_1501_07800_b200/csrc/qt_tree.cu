@@ -567,8 +567,7 @@ void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals, bool async) {
     read_back16(M, brow, bcol, vals);
     return;
   }
-  if (M->ubs == 64) {
-    if (async) fail(QT_EINVAL, "qt_read_back_async is built for block_size 32");
+  if (M->ubs == 64) {  // (async: completes before returning)
     read_back64(M, brow, bcol, vals);
     return;
   }
