@@ -182,6 +182,19 @@ def oracle_sample(c: dict, target_s: float = 12.0, max_rows: int | None = None):
     return gf, nt, f"block rows [{mid},{r1}) of the workload's C ({prods} block products)", dt
 
 
+def cpu_info():
+    """The host the oracle ran on (print the CPU model and the compile flags)."""
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "oracle_flags": "gcc -O2 -ffp-contract=off, pthreads"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -209,7 +222,7 @@ def run_reference(args):
         "data": "synthetic (qtgen counter-based generator)",
         "config": {"workload": desc, "sample": sample},
         "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": nt, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, **cpu_info()},
         "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -307,7 +320,7 @@ def main():
     cpu = None
     if rank == 0 and P == 1 and not args.no_cpu_baseline:
         gf, nt, sample, _ = oracle_sample(c, target_s=12.0)
-        cpu = {"value": round(gf, 3), "unit": UNIT, "cores": nt, "kind": "oracle", "sample": sample}
+        cpu = {"value": round(gf, 3), "unit": UNIT, "cores": nt, "kind": "oracle", "sample": sample, **cpu_info()}
 
     if rank == 0:
         m_nnz_row = 2 * 1024 + 1
@@ -330,6 +343,8 @@ def main():
                                         "MEASURED_PEAKS.json has no FP64 entry; nominal 37.2 TF "
                                         "= 148 SM x 64 FMA x 2 x 1.965 GHz",
                          "ms_numeric": round(ms_num, 4), "ms_symbolic": round(ms_sym, 4),
+                         "ms_call_median": round(statistics.median(s.ms_total for s in stats), 4),
+                         "ms_call_min": round(min(s.ms_total for s in stats), 4),
                          "ms_exchange": round(ms_exch, 4),
                          "ms_payload_overlapped": round(statistics.mean(s.ms_payload for s in stats), 4),
                          "tiles_overlapped_after": [int(stats[-1].tiles_overlapped), int(stats[-1].tiles_after)],
