@@ -242,6 +242,30 @@ qt_status qt_multiply_async(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st);
  * Errors: QT_EINVAL, QT_ECUDA. */
 qt_status qt_read_back_async(qt_mat A, int32_t* brow, int32_t* bcol, void* values);
 
+/* Plans: a multiply whose numeric pass can be re-run.  qt_multiply_plan is
+ * qt_multiply_ex (single rank; no overlap phases) that also keeps the numeric
+ * launch and the symbolic pass's buffers it reads; C is returned as usual.
+ * qt_plan_execute recomputes C's values from the CURRENT values of A and B
+ * (the patterns are fixed: change values with qt_update_values) — the same
+ * kernel and summation order, so the result is bitwise that of a fresh
+ * qt_multiply.  It only enqueues work on the context stream (no host
+ * synchronisation, no allocation), so it can be captured into a CUDA graph.
+ * A, B and C must outlive the plan.  For the symmetric square use
+ * qt_symm_square (no plan).  Errors: as qt_multiply_ex; QT_EINVAL
+ * (world > 1). */
+typedef struct qt_plan_s* qt_plan;
+qt_status qt_multiply_plan(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, qt_plan* plan,
+                           qt_mat* C, qt_stats* st);
+qt_status qt_plan_execute(qt_plan plan);
+qt_status qt_plan_destroy(qt_plan plan);
+
+/* New values for A's blocks (same pattern): `values` holds nblocks blocks of
+ * bs x bs row-major values in qt_read_back order (ascending brow, then bcol),
+ * host or device memory; A's cached screening norms are dropped.  Stream
+ * ordered on the context stream (a host source is copied before return).
+ * block_size 32.  Errors: QT_EINVAL, QT_EBS, QT_ECUDA. */
+qt_status qt_update_values(qt_mat A, const void* values);
+
 /* Wait for everything this context has enqueued, including the copies of
  * qt_read_back_async, and release their staging buffers.  Errors: QT_ECUDA. */
 qt_status qt_ctx_synchronize(qt_ctx ctx);

@@ -146,7 +146,11 @@ static int ilog2(int64_t x) {
 
 using namespace qt;
 
-#define API_TRY try {
+// (a stale, non-sticky CUDA error left by an earlier call — already reported
+// through that call's status — must not be attributed to this call's launches)
+#define API_TRY \
+  try {         \
+    (void)cudaGetLastError();
 #define API_CATCH              \
   }                            \
   catch (...) {                \
@@ -430,6 +434,97 @@ qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, q
   R->global_nb = user_nblocks(R);
   user_stats(R, S);
   *C = R;
+  API_CATCH
+}
+
+// ------------------------------------------------------------ plan / execute
+
+struct qt_plan_s {
+  qt_ctx ctx = nullptr;
+  qt_mat C = nullptr;  // the product the plan writes (owned by the caller)
+  NumericPlan np;
+};
+
+qt_status qt_multiply_plan(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, qt_plan* plan, qt_mat* C,
+                           qt_stats* st) {
+  API_TRY
+  if (!A || !B || !C || !plan) fail(QT_EINVAL, "NULL argument");
+  *C = nullptr;
+  *plan = nullptr;
+  if (A->ctx != B->ctx) fail(QT_ESTATE, "A and B belong to different contexts");
+  if (A->ctx->world != 1) fail(QT_EINVAL, "plans are single-rank");
+  if (A->ctx->async_multiply) fail(QT_ESTATE, "plan inside qt_multiply_async");
+  if (A->n != B->n) fail(QT_EDIM, "dimension mismatch");
+  if (A->leaf_dim != B->leaf_dim || A->ubs != B->ubs) fail(QT_EBS, "leaf_dim/block_size mismatch");
+  if (A->dtype != B->dtype) fail(QT_EDTYPE, "dtype mismatch");
+  if ((trans_a | trans_b) & ~1) fail(QT_EINVAL, "trans_a / trans_b must be 0 or 1");
+  qt_ctx ctx = A->ctx;
+  QT_CUDA(cudaSetDevice(ctx->device));
+  ensure_levels(A);
+  ensure_levels(B);
+  qt_stats local;
+  qt_stats& S = st ? *st : local;
+  memset(&S, 0, sizeof(S));
+  auto* P = new qt_plan_s();
+  try {
+    P->ctx = ctx;
+    QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+    float ms_sym = 0, ms_num = 0;
+    qt_mat R = multiply_local(A, B, &S, &ms_sym, &ms_num, (trans_a ? 1 : 0) | (trans_b ? 2 : 0), -1.0, nullptr, 0,
+                              INT32_MAX, &P->np);
+    S.ms_symbolic = ms_sym;
+    S.ms_numeric = ms_num;
+    QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+    QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
+    QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
+    R->global_nb = user_nblocks(R);
+    user_stats(R, S);
+    P->C = R;
+    *C = R;
+  } catch (...) {
+    delete P;
+    throw;
+  }
+  *plan = P;
+  API_CATCH
+}
+
+qt_status qt_plan_execute(qt_plan plan) {
+  API_TRY
+  if (!plan) fail(QT_EINVAL, "NULL plan");
+  qt_ctx ctx = plan->ctx;
+  QT_CUDA(cudaSetDevice(ctx->device));
+  NumericPlan& np = plan->np;
+  if (!np.valid) return QT_OK;  // an empty product: nothing to recompute
+  if (np.tnb > 0) {             // symmetric square: U's transposed copy from its current values
+    if (np.f32)
+      launch_transpose_blocks_f32(ctx, np.tsrc, np.poolT.p, np.tnb);
+    else
+      launch_transpose_blocks(ctx, np.tsrc, np.poolT.p, np.tnb);
+  }
+  if (np.f32)
+    launch_numeric_f32(ctx, np.nb);
+  else
+    launch_numeric(ctx, QT_F64, np.na);
+  API_CATCH
+}
+
+qt_status qt_plan_destroy(qt_plan plan) {
+  API_TRY
+  if (!plan) return QT_OK;
+  QT_CUDA(cudaSetDevice(plan->ctx->device));
+  QT_CUDA(cudaStreamSynchronize(plan->ctx->stream));
+  delete plan;
+  API_CATCH
+}
+
+qt_status qt_update_values(qt_mat A, const void* values) {
+  API_TRY
+  if (!A) fail(QT_EINVAL, "NULL matrix");
+  if (A->ubs != 32) fail(QT_EBS, "qt_update_values is built for block_size 32");
+  if (A->nb > 0 && !values) fail(QT_EINVAL, "NULL values");
+  QT_CUDA(cudaSetDevice(A->ctx->device));
+  update_values(A, values);
   API_CATCH
 }
 

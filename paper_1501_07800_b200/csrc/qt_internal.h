@@ -149,6 +149,7 @@ struct qt_mat_s {
   qt::DevBuf hist;     // int32 per-level node counts per row / per column (see build_levels)
   std::vector<int32_t> hist_host;  // host copy of hist (per-level task counts without a sync)
   std::vector<qt::DevBuf> norm2;  // squared Frobenius norms per node, levels 0..L (screening; lazy)
+  qt::DevBuf rm_inv;   // pool index -> position in row-major (brow, bcol) order (qt_update_values; lazy)
   qt::DevBuf sub;      // ubs == 16: uint8 [nb] quadrant occupancy (bit 2i+j), indexed like the pool
   int64_t nb16 = 0;    // ubs == 16: the caller's blocks (set quadrants)
   // B_ext of a multi-rank multiply: pool1 overrides pool.p (a borrowed view of
@@ -187,6 +188,8 @@ qt_mat upper32_view(qt_mat M);
 // row-major (brow, bcol) order and un-swizzle into caller buffers (caller's block size)
 void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals, bool async = false);
 void reap_pending(qt_ctx ctx, bool wait);
+// new values for M's blocks, given in read-back (row-major brow, bcol) order, host or device
+void update_values(qt_mat M, const void* values);
 // 64-blocks (2x2 quads of 32-blocks): split inputs / user-level block count
 void split64(qt_ctx ctx, qt_dtype dt, int64_t nb, const int32_t* brow, const int32_t* bcol,
              const void* vals, DevBuf& obrow, DevBuf& obcol, DevBuf& ovals);
@@ -235,9 +238,10 @@ struct Overlap {
 };
 // [row_lo, row_hi): only C blocks in these block rows are computed (the BFS
 // prunes C nodes outside the window at every level).
+struct NumericPlan;
 qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* st, float* ms_sym, float* ms_num, int trans = 0,
                       double tau = -1.0, Overlap* ov = nullptr, int32_t row_lo = 0,
-                      int32_t row_hi = INT32_MAX);
+                      int32_t row_hi = INT32_MAX, NumericPlan* plan = nullptr);
 // Tiles (C nodes of one level with CSR task ranges `ts` over the task array
 // pb) partitioned on the device: map[0, *nsel) = the tiles whose B nodes hold
 // only block ids < splitB (Morton order), map[*nsel, ntiles) = the rest.
@@ -309,6 +313,18 @@ struct NumericArgs32 {
   const int32_t* nsel = nullptr;
 };
 void launch_numeric_f32(qt_ctx ctx, const NumericArgs32& a);
+
+// The numeric launch of a multiply kept for re-execution (qt_multiply_plan):
+// its arguments and the symbolic pass's buffers the kernel reads.
+struct NumericPlan {
+  bool valid = false, f32 = false;
+  NumericArgs na;
+  NumericArgs32 nb;
+  DevBuf keep[6];
+  DevBuf poolT;                   // symmetric square: U^T's pool, refreshed on execute
+  const void* tsrc = nullptr;
+  int64_t tnb = 0;
+};
 void launch_fp64_peak(qt_ctx ctx, int kind, int iters, int grid);
 
 // ----- distributed (qt_dist.cu)

@@ -631,7 +631,7 @@ struct Trace {
 };
 
 qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* ms_num, int trans,
-                      double tau, Overlap* ov, int32_t row_lo, int32_t row_hi) {
+                      double tau, Overlap* ov, int32_t row_lo, int32_t row_hi, NumericPlan* plan) {
   const bool screen = tau >= 0.0;
   const double tau2 = tau * tau;
   if (screen) {
@@ -1013,6 +1013,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         ov->tiles_local = h;
         ov->tiles_remote = n_all - h;
       }
+      void* const plan_pool_c = C->pool.p;  // (a bs-16 drop of empty containers would move C: no plan then)
       if (A->ubs == 16) {  // the 16-block pattern of C and the 16-block products (qt_bs16.cu)
         C->sub.alloc(std::max<int64_t>(C->nb, 1), st);
         int64_t r16[4];
@@ -1028,6 +1029,49 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
           qt_mat D = drop_empty16(C);
           delete C;
           C = D;
+        }
+      }
+      if (plan && C->nb > 0 && !two_phase && C->pool.p == plan_pool_c) {  // keep the launch for qt_plan_execute
+        plan->valid = true;
+        plan->f32 = f32;
+        if (f32) {
+          NumericArgs32 nb;  // rebuilt as launched above
+          nb.ntiles = ns[L - 2];
+          nb.tile_start = t2_cstart.as<int32_t>();
+          nb.pa = t2_pa.as<int32_t>();
+          nb.pb = t2_pb.as<int32_t>();
+          nb.childA2 = A->child[L - 2].as<int4>();
+          nb.childA1 = A->child[L - 1].as<int4>();
+          nb.childB2 = B->child[L - 2].as<int4>();
+          nb.childB1 = B->child[L - 1].as<int4>();
+          nb.childC2 = cchild2.as<int4>();
+          nb.childC1 = cchild.as<int4>();
+          nb.poolA = A->pool_ptr();
+          nb.poolB = B->pool_ptr();
+          nb.poolB2 = B->pool2;
+          nb.splitB = B->split;
+          nb.poolC = C->pool.p;
+          nb.zeros = ctx->zeros.p;
+          nb.counter = ctx->counters.as<int>() + 16;
+          nb.trans = trans & 7;
+          nb.poolT = poolT.p;
+          plan->nb = nb;
+          plan->keep[0] = std::move(t2_cstart);
+          plan->keep[1] = std::move(t2_pa);
+          plan->keep[2] = std::move(t2_pb);
+          plan->keep[3] = std::move(cchild2);
+          plan->keep[4] = std::move(cchild);
+        } else {
+          plan->na = na;
+          plan->keep[0] = std::move(cstart);
+          plan->keep[1] = std::move(pa);
+          plan->keep[2] = std::move(pb);
+          plan->keep[3] = std::move(cchild);
+        }
+        if (sym) {
+          plan->poolT = std::move(poolT);
+          plan->tsrc = A->pool_ptr();
+          plan->tnb = A->nb;
         }
       }
     }

@@ -626,6 +626,46 @@ void read_back(qt_mat M, int32_t* brow, int32_t* bcol, void* vals, bool async) {
   if (!async) QT_CUDA(cudaStreamSynchronize(st));
 }
 
+namespace {
+__global__ void k_scatter_inv(const int32_t* __restrict__ order, int64_t n, int32_t* __restrict__ inv) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    inv[order[t]] = (int32_t)t;
+}
+}  // namespace
+
+void update_values(qt_mat M, const void* values) {
+  qt_ctx ctx = M->ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t nb = M->nb;
+  if (nb == 0) return;
+  const size_t es = elem_size(M->dtype);
+  if (!M->rm_inv.p) {  // pool index -> row-major position, once per matrix
+    DevBuf rm(nb * 8, st), rm2(nb * 8, st), iota(nb * 4, st), order(nb * 4, st);
+    k_rowmajor_keys<<<grid_for(nb), kThreads, 0, st>>>(M->key.as<uint64_t>(), nb, rm.as<uint64_t>(),
+                                                       iota.as<int32_t>());
+    QT_LAUNCH_CHECK(ctx);
+    cub_sort_pairs(ctx, rm.as<uint64_t>(), rm2.as<uint64_t>(), iota.as<int32_t>(), order.as<int32_t>(), nb, 64);
+    M->rm_inv.alloc(nb * 4, st);
+    k_scatter_inv<<<grid_for(nb), kThreads, 0, st>>>(order.as<int32_t>(), nb, M->rm_inv.as<int32_t>());
+    QT_LAUNCH_CHECK(ctx);
+  }
+  DevBuf dv;
+  const void* src = values;
+  if (!is_device_ptr(values)) {
+    dv.alloc(nb * 1024 * es, st);
+    QT_CUDA(cudaMemcpyAsync(dv.p, values, nb * 1024 * es, cudaMemcpyHostToDevice, st));
+    src = dv.p;
+  }
+  const unsigned g = (unsigned)std::min<int64_t>(nb, 148 * 16);
+  if (M->dtype == QT_F64)
+    k_fill_pool<double><<<g, 256, 0, st>>>((const double*)src, M->rm_inv.as<int32_t>(), nb, M->pool.as<double>());
+  else
+    k_fill_pool<float><<<g, 256, 0, st>>>((const float*)src, M->rm_inv.as<int32_t>(), nb, M->pool.as<float>());
+  QT_LAUNCH_CHECK(ctx);
+  M->norm2.clear();  // (screening norms follow the values)
+  if (!is_device_ptr(values)) QT_CUDA(cudaStreamSynchronize(st));  // the host buffer may be reused on return
+}
+
 static qt_mat clone_params(qt_mat A) {
   qt_mat M = new qt_mat_s();
   M->ctx = A->ctx;

@@ -77,6 +77,10 @@ def _load():
         "qt_multiply_virtual": [P, P, i32, i32, P, P, P],
         "qt_symm_square_virtual": [P, i32, i32, P, P, P],
         "qt_plan_strips": [P, i64, i32, i32, i64, P, P, i64, P, i32, P, P],
+        "qt_multiply_plan": [P, P, i32, i32, P, P, P],
+        "qt_plan_execute": [P],
+        "qt_plan_destroy": [P],
+        "qt_update_values": [P, P],
         "qt_truncate": [P, ctypes.c_double, P],
         "qt_info": [P, P, P, P, P, P, P, P, P],
         "qt_level_nodes": [P, P, i32, P],
@@ -104,7 +108,8 @@ _lib = _load()
 EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_nccl_unique_id", "qt_create", "qt_multiply",
             "qt_multiply_async",
             "qt_multiply_ex", "qt_symm_square", "qt_multiply_screened",
-            "qt_multiply_virtual", "qt_symm_square_virtual", "qt_plan_strips", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
+            "qt_multiply_virtual", "qt_symm_square_virtual", "qt_plan_strips", "qt_multiply_plan",
+            "qt_plan_execute", "qt_plan_destroy", "qt_update_values", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
             "qt_read_back_async", "qt_ctx_synchronize", "qt_destroy", "qt_last_error", "qt_kernel_launches", "qt_fp64_peak",
             "qt_loopback_hub_create", "qt_loopback_hub_destroy", "qt_ctx_create_loopback")
 
@@ -220,6 +225,28 @@ def plan_strips(n: int, block_size: int, parts: int, a_rc, b_rows, align_rows: i
     return bounds, prods
 
 
+class Plan:
+    """A multiply whose numeric pass can be re-run (qt_multiply_plan)."""
+
+    def __init__(self, ctx, handle):
+        self.ctx, self._h = ctx, handle
+
+    def execute(self):
+        """Recompute C from the current values of A and B (enqueue only; CUDA-graph capturable)."""
+        _check(_lib.qt_plan_execute(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _check(_lib.qt_plan_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class LoopbackHub:
     """Shared state of the single-device loopback transport (testing the
     multi-rank path with rank threads on one GPU)."""
@@ -314,6 +341,20 @@ class Matrix:
         rb = np.ascontiguousarray(np.asarray(row_bounds, dtype=np.int32))
         _check(_lib.qt_symm_square_virtual(self._h, P, g, _ptr(rb), ctypes.byref(h), ctypes.byref(st)))
         return Matrix(self.ctx, h), st
+
+    def multiply_plan(self, other: "Matrix", trans_a: bool = False, trans_b: bool = False):
+        """C = op(A) op(B) plus a Plan that recomputes C after qt_update_values."""
+        st = Stats()
+        h, p = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(_lib.qt_multiply_plan(self._h, other._h, int(trans_a), int(trans_b), ctypes.byref(p),
+                                     ctypes.byref(h), ctypes.byref(st)))
+        return Plan(self.ctx, p), Matrix(self.ctx, h), st
+
+    def update_values(self, vals):
+        """New values (same pattern) in to_blocks order: [nblocks, bs, bs]."""
+        if isinstance(vals, np.ndarray):
+            vals = np.ascontiguousarray(vals)
+        _check(_lib.qt_update_values(self._h, _ptr(vals)))
 
     def truncate(self, tau: float) -> "Matrix":
         h = ctypes.c_void_p()

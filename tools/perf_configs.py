@@ -139,6 +139,41 @@ def run_virtual_sym(ctx, stream, name, full, P, ranks, steps=5):
         print(json.dumps(out), flush=True)
 
 
+def run_graph(ctx, stream, name, c, reps=1000, per_graph=10):
+    """Numeric pass only, re-run through a plan captured into a CUDA graph
+    (config 1 is launch-latency bound; its kernel time is taken
+    from graph-replayed iterations).  per_graph executes per captured graph."""
+    Am = c["A"]
+    A = qtmm.Matrix.from_blocks(ctx, Am.n, Am.leaf_dim, 32, Am.brow, Am.bcol, Am.vals)
+    B = A if c["same"] else qtmm.Matrix.from_blocks(ctx, c["B"].n, c["B"].leaf_dim, 32, c["B"].brow, c["B"].bcol,
+                                                    c["B"].vals)
+    plan, C, st = A.multiply_plan(B)
+    for _ in range(3):
+        plan.execute()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(per_graph):
+            plan.execute()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    n = max(1, reps // per_graph)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(n):
+            g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / (n * per_graph)
+    print(json.dumps({"config": name + " (numeric pass via plan, CUDA-graph replay)", "block_products": st.block_products,
+                      "us_per_execute": round(us, 2),
+                      "tflops_numeric": round(st.block_products * FLOP / (us * 1e-6) / 1e12, 2),
+                      "executes": n * per_graph, "per_call_ms_numeric": round(st.ms_numeric, 4)}), flush=True)
+    plan.close()
+
+
 def leaf_sweep(ctx, stream):
     """The paper's leaf benchmark shape (Figs. leafmat_bench_double /
     _single): C = A*B at N = 4096 as ONE leaf, blocks of size bs placed
@@ -282,6 +317,10 @@ def main():
         elif w == "virtsym4cfg4":
             run_virtual_sym(ctx, stream, "cfg4 ES-like symmetric P=4 (virtual ranks)",
                             qtgen.config(4, symmetric=True)["A"], 4, [0, 1])
+        elif w == "graph1":
+            run_graph(ctx, stream, "cfg1 dense N=512", qtgen.config(1))
+        elif w == "graph2":
+            run_graph(ctx, stream, "cfg2 banded N=16384", qtgen.config(2), reps=50, per_graph=5)
         elif w == "dense4096":
             br, bc = qtgen.pattern_dense(128)
             v = qtgen.block_values(br, bc, 32, 1)
