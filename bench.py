@@ -380,6 +380,8 @@ def measure_fp32(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     sts = []
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
     e0.record(stream)
     for _ in range(args.steps):
         C, st = A32.multiply(A32)
@@ -387,6 +389,7 @@ def measure_fp32(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier):
         C.close()
     e1.record(stream)
     torch.cuda.synchronize()
+    clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / args.steps
     ms_num = statistics.mean(x.ms_numeric for x in sts)
     prods = sts[-1].block_products
@@ -405,7 +408,9 @@ def measure_fp32(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier):
                          "achieved": round(achieved, 2), "peak": round(peak, 1) if peak else None,
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak else None,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops x (1.1/2.25 nominal tf32/bf16) / 3",
-                         "ms_numeric": round(ms_num, 4)}}
+                         "ms_numeric": round(ms_num, 4)},
+            # the 3xTF32 kernel draws ~990 W: the board's power cap lowers the SM clock (sw_power_cap)
+            "clocks": clocks}
 
 
 def measure_symm(qtmm, ctx, stream, args):
