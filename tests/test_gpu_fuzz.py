@@ -114,3 +114,27 @@ def test_fuzz_symm_screen_truncate_virtual(qt, ctx, seed):
         ms = (sref[0] >= bounds[g]) & (sref[0] < bounds[g + 1])
         r, c, v = Sg.to_blocks()
         assert np.array_equal(r, sref[0][ms]) and np.array_equal(v, sref[2][ms])
+
+
+@pytest.mark.parametrize("seed", range(N_MISC))
+def test_fuzz_plans(qt, ctx, seed):
+    rng = np.random.default_rng(9000 + seed)
+    dtype = np.float64 if seed % 2 else np.float32
+    nbr = int(rng.integers(1, 30))
+    p = float(rng.choice([0.0, 0.1, 0.4, 1.0]))
+    leaf = 32 * int(2 ** rng.integers(0, 3))
+    Am = rand_int_bm(rng, nbr, p, 32, leaf, dtype)
+    Bm = rand_int_bm(rng, nbr, p, 32, leaf, dtype)
+    ta, tb = bool(rng.random() < 0.3), bool(rng.random() < 0.3)
+    A, B = mk(qt, ctx, Am), mk(qt, ctx, Bm)
+    plan, C, _ = A.multiply_plan(B, ta, tb)
+    oa, ob = np.lexsort((Am.bcol, Am.brow)), np.lexsort((Bm.bcol, Bm.brow))
+    va = rng.integers(-4, 5, size=Am.vals.shape).astype(dtype)[oa]
+    vb = rng.integers(-4, 5, size=Bm.vals.shape).astype(dtype)[ob]
+    A.update_values(np.ascontiguousarray(va))
+    B.update_values(np.ascontiguousarray(vb))
+    plan.execute()
+    ref = oracle.spgemm_t(nbr, 32, (Am.brow[oa], Am.bcol[oa], va.astype(np.float64)),
+                          (Bm.brow[ob], Bm.bcol[ob], vb.astype(np.float64)), ta, tb)
+    same(C.to_blocks(), ref)
+    plan.close()
