@@ -230,6 +230,16 @@ qt_status qt_read_back(qt_mat A, int32_t* brow, int32_t* bcol, void* values);
  * Errors: as qt_multiply. */
 qt_status qt_multiply_async(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st);
 
+/* Distributed read-back: collective over the context's ranks.
+ * `root` receives every rank's blocks in (brow, bcol) order — the ranks own
+ * contiguous block-row strips, so this is the order of the whole matrix —
+ * into brow/bcol/values (caller block size, host or device; the other ranks'
+ * pointers are ignored).  *total (all ranks, may be NULL) = the number of
+ * blocks of the whole matrix.  Call once with NULL buffers on the root to
+ * learn the size, then with buffers.  world == 1: qt_read_back.
+ * Errors: QT_EINVAL (root), QT_ECUDA, QT_ENCCL. */
+qt_status qt_gather(qt_mat A, int32_t root, int32_t* brow, int32_t* bcol, void* values, int64_t* total);
+
 /* qt_read_back without the final synchronisation, for pipelined host
  * transfers: the reorder/unpack kernels run on the context stream into a
  * device staging buffer, and the device-to-host copies run on the context's

@@ -670,6 +670,24 @@ qt_status qt_read_back(qt_mat A, int32_t* brow, int32_t* bcol, void* values) {
   API_CATCH
 }
 
+qt_status qt_gather(qt_mat A, int32_t root, int32_t* brow, int32_t* bcol, void* values, int64_t* total) {
+  API_TRY
+  if (!A) fail(QT_EINVAL, "NULL matrix");
+  qt_ctx ctx = A->ctx;
+  if (root < 0 || root >= ctx->world) fail(QT_EINVAL, "root %d outside [0,%d)", root, ctx->world);
+  QT_CUDA(cudaSetDevice(ctx->device));
+  int64_t N;
+  if (ctx->world == 1) {
+    N = user_nblocks(A);
+    if (brow || bcol || values) read_back(A, brow, bcol, values);
+  } else {
+    N = gather_dist(A, root, ctx->rank == root ? brow : nullptr, ctx->rank == root ? bcol : nullptr,
+                    ctx->rank == root ? values : nullptr);
+  }
+  if (total) *total = N;
+  API_CATCH
+}
+
 qt_status qt_read_back_async(qt_mat A, int32_t* brow, int32_t* bcol, void* values) {
   API_TRY
   if (!A) fail(QT_EINVAL, "NULL matrix");

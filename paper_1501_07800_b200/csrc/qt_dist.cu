@@ -1244,6 +1244,66 @@ qt_mat symm_square_virtual(qt_mat U, const int32_t* bounds, int P, int g, qt_sta
   return C;
 }
 
+// ------------------------------------------------------------ gather (X4)
+
+// Every rank's blocks to `root`, in (brow, bcol) order: the ranks own
+// contiguous block-row strips in rank order, so the root concatenates the
+// ranks' own sorted lists.  Collective; returns the total block count.
+int64_t gather_dist(qt_mat A, int root, int32_t* brow, int32_t* bcol, void* vals) {
+  qt_ctx ctx = A->ctx;
+  cudaStream_t st = ctx->stream;
+  const int P = ctx->world, g = ctx->rank;
+  Transport* X = T(ctx);
+  const int64_t n = user_nblocks(A);
+  std::vector<int64_t> cnt(P);
+  X->allgather_i64(&n, cnt.data(), 1);
+  std::vector<int64_t> off(P + 1, 0);
+  for (int q = 0; q < P; ++q) off[q + 1] = off[q] + cnt[q];
+  const int64_t N = off[P];
+  const bool want = brow || bcol || vals;
+  int any = want ? 1 : 0;
+  {  // every rank must take the same branch: the root decides (it owns the buffers)
+    int64_t w = any;
+    std::vector<int64_t> aw(P);
+    X->allgather_i64(&w, aw.data(), 1);
+    any = (int)aw[root];
+  }
+  if (!any || N == 0) return N;
+  const size_t vb = (size_t)A->ubs * A->ubs * elem_size(A->dtype);
+  DevBuf lr(4 * std::max<int64_t>(n, 1), st), lc(4 * std::max<int64_t>(n, 1), st),
+      lv(vb * std::max<int64_t>(n, 1), st);
+  if (n > 0) read_back(A, lr.as<int32_t>(), lc.as<int32_t>(), lv.p);
+  if (g != root) {
+    X->group_start();
+    if (n > 0) {
+      X->send(lr.p, 4 * n, root);
+      X->send(lc.p, 4 * n, root);
+      X->send(lv.p, vb * n, root);
+    }
+    X->group_end();
+    return N;
+  }
+  DevBuf R(4 * N, st), Cc(4 * N, st), V(vb * N, st);
+  if (n > 0) {
+    QT_CUDA(cudaMemcpyAsync(R.as<int32_t>() + off[g], lr.p, 4 * n, cudaMemcpyDeviceToDevice, st));
+    QT_CUDA(cudaMemcpyAsync(Cc.as<int32_t>() + off[g], lc.p, 4 * n, cudaMemcpyDeviceToDevice, st));
+    QT_CUDA(cudaMemcpyAsync((char*)V.p + vb * off[g], lv.p, vb * n, cudaMemcpyDeviceToDevice, st));
+  }
+  X->group_start();
+  for (int q = 0; q < P; ++q) {
+    if (q == g || cnt[q] == 0) continue;
+    X->recv(R.as<int32_t>() + off[q], 4 * cnt[q], q);
+    X->recv(Cc.as<int32_t>() + off[q], 4 * cnt[q], q);
+    X->recv((char*)V.p + vb * off[q], vb * cnt[q], q);
+  }
+  X->group_end();
+  if (brow) QT_CUDA(cudaMemcpyAsync(brow, R.p, 4 * N, cudaMemcpyDefault, st));
+  if (bcol) QT_CUDA(cudaMemcpyAsync(bcol, Cc.p, 4 * N, cudaMemcpyDefault, st));
+  if (vals) QT_CUDA(cudaMemcpyAsync(vals, V.p, vb * N, cudaMemcpyDefault, st));
+  QT_CUDA(cudaStreamSynchronize(st));
+  return N;
+}
+
 }  // namespace qt
 
 namespace qt {

@@ -343,6 +343,8 @@ void allgather_i64(qt_ctx ctx, const int64_t* send_host, int64_t* recv_host, int
 // rank; C = its rows of A^2, upper triangle.  The virtual form runs rank g of P
 // on one device from the whole U.
 qt_mat symm_square_dist(qt_mat U, qt_stats* st);
+// every rank's blocks to `root` in (brow, bcol) order (collective); returns the total count
+int64_t gather_dist(qt_mat A, int root, int32_t* brow, int32_t* bcol, void* vals);
 qt_mat symm_square_virtual(qt_mat U, const int32_t* bounds, int P, int g, qt_stats* st);
 
 }  // namespace qt

@@ -81,6 +81,7 @@ def _load():
         "qt_plan_execute": [P],
         "qt_plan_destroy": [P],
         "qt_update_values": [P, P],
+        "qt_gather": [P, i32, P, P, P, P],
         "qt_truncate": [P, ctypes.c_double, P],
         "qt_info": [P, P, P, P, P, P, P, P, P],
         "qt_level_nodes": [P, P, i32, P],
@@ -109,7 +110,7 @@ EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_nccl_unique_id", "qt_create",
             "qt_multiply_async",
             "qt_multiply_ex", "qt_symm_square", "qt_multiply_screened",
             "qt_multiply_virtual", "qt_symm_square_virtual", "qt_plan_strips", "qt_multiply_plan",
-            "qt_plan_execute", "qt_plan_destroy", "qt_update_values", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
+            "qt_plan_execute", "qt_plan_destroy", "qt_update_values", "qt_gather", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
             "qt_read_back_async", "qt_ctx_synchronize", "qt_destroy", "qt_last_error", "qt_kernel_launches", "qt_fp64_peak",
             "qt_loopback_hub_create", "qt_loopback_hub_destroy", "qt_ctx_create_loopback")
 
@@ -349,6 +350,23 @@ class Matrix:
         _check(_lib.qt_multiply_plan(self._h, other._h, int(trans_a), int(trans_b), ctypes.byref(p),
                                      ctypes.byref(h), ctypes.byref(st)))
         return Plan(self.ctx, p), Matrix(self.ctx, h), st
+
+    def gather(self, root: int = 0):
+        """Collective: every rank's blocks on `root` in (brow, bcol) order
+        (qt_gather); returns (brow, bcol, vals) on the root, None elsewhere."""
+        total = ctypes.c_int64()
+        _check(_lib.qt_gather(self._h, root, None, None, None, ctypes.byref(total)))
+        n = total.value
+        if self.ctx.world > 1 and self.ctx.rank != root:
+            _check(_lib.qt_gather(self._h, root, None, None, None, None))
+            return None
+        inf = self.info()
+        bs = inf["bs"]
+        dt = np.float64 if inf["dtype"] == "f64" else np.float32
+        out = (np.empty(n, np.int32), np.empty(n, np.int32), np.empty((n, bs, bs), dt))
+        _check(_lib.qt_gather(self._h, root, _ptr(out[0]) if n else None, _ptr(out[1]) if n else None,
+                              _ptr(out[2]) if n else None, None))
+        return out
 
     def update_values(self, vals):
         """New values (same pattern) in to_blocks order: [nblocks, bs, bs]."""
