@@ -14,6 +14,7 @@ import qtgen
 pytestmark = pytest.mark.gpu
 N_MUL = int(os.environ.get("QT_FUZZ_MUL", 24))   # (larger sweeps: QT_FUZZ_MUL=300 QT_FUZZ_MISC=100)
 N_MISC = int(os.environ.get("QT_FUZZ_MISC", 10))
+NBR_MAX = int(os.environ.get("QT_FUZZ_NBR", 40))    # (larger grids: QT_FUZZ_NBR=160)
 
 
 @pytest.fixture(scope="module")
@@ -62,7 +63,7 @@ def test_fuzz_multiply(qt, ctx, seed):
     rng = np.random.default_rng(7000 + seed)
     bs = int(rng.choice([16, 32, 32, 64]))
     dtype = np.float64 if rng.random() < 0.6 else np.float32
-    nbr = int(rng.integers(1, 40)) if bs != 16 else 2 * int(rng.integers(1, 20))
+    nbr = int(rng.integers(1, NBR_MAX)) if bs != 16 else 2 * int(rng.integers(1, NBR_MAX // 2))
     p = float(rng.choice([0.0, 0.03, 0.1, 0.3, 0.7, 1.0]))
     gran = max(bs, 32)
     leaf = gran * int(2 ** rng.integers(0, 4))
