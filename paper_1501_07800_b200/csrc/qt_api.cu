@@ -551,7 +551,6 @@ qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_sta
   if (A->dtype != QT_F64) fail(QT_EDTYPE, "norm screening is FP64-only (the FP32 tile MMA cannot skip single products)");
   if (A->ubs != 32) fail(QT_EBS, "norm screening is built for block_size 32");
   qt_ctx ctx = A->ctx;
-  if (ctx->world > 1) fail(QT_EINVAL, "norm screening is single-rank in this build");
   QT_CUDA(cudaSetDevice(ctx->device));
   ensure_levels(A);
   ensure_levels(B);
@@ -559,10 +558,15 @@ qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_sta
   qt_stats& S = st ? *st : local;
   memset(&S, 0, sizeof(S));
   QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
-  float ms_sym = 0, ms_num = 0;
-  qt_mat R = multiply_local(A, B, &S, &ms_sym, &ms_num, 0, tau);
-  S.ms_symbolic = ms_sym;
-  S.ms_numeric = ms_num;
+  qt_mat R;
+  if (ctx->world > 1) {  // the exchange of the full product, then the screened multiply on B_ext
+    R = multiply_dist(A, B, &S, tau);
+  } else {
+    float ms_sym = 0, ms_num = 0;
+    R = multiply_local(A, B, &S, &ms_sym, &ms_num, 0, tau);
+    S.ms_symbolic = ms_sym;
+    S.ms_numeric = ms_num;
+  }
   QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
   QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));

@@ -636,9 +636,9 @@ void split_tiles(qt_ctx ctx, int64_t ntiles, const int32_t* ts, const int32_t* p
 }
 
 namespace {
-qt_mat finish_multiply(qt_mat A_local, qt_mat Bx, qt_stats* S, Overlap* ov) {
+qt_mat finish_multiply(qt_mat A_local, qt_mat Bx, qt_stats* S, Overlap* ov, double tau = -1.0) {
   float ms_sym = 0, ms_num = 0;
-  qt_mat C = multiply_local(A_local, Bx, S, &ms_sym, &ms_num, 0, -1.0, ov);
+  qt_mat C = multiply_local(A_local, Bx, S, &ms_sym, &ms_num, 0, tau, ov);
   S->ms_symbolic = ms_sym;
   S->ms_numeric = ms_num;
   if (ov) {
@@ -668,7 +668,7 @@ cudaStream_t comm_stream(qt_ctx ctx) {
 
 // ------------------------------------------------------------------ NCCL path
 
-qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S) {
+qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S, double tau) {
   qt_ctx ctx = A->ctx;
   cudaStream_t st = ctx->stream;
   const int P = ctx->world, g = ctx->rank;
@@ -802,7 +802,7 @@ qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S) {
   Overlap ov;
   ov.s2 = s2;
   try {
-    C = finish_multiply(A, Bx, S, ovl ? &ov : nullptr);
+    C = finish_multiply(A, Bx, S, ovl ? &ov : nullptr, tau);
   } catch (...) {
     if (ovl) cudaStreamSynchronize(s2);
     delete Bx;

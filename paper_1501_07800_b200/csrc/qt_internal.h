@@ -334,7 +334,8 @@ void* loop_hub_create(int P);
 void loop_hub_destroy(void* hub);
 void nccl_unique_id(void* out128);
 void dist_finalize(qt_ctx ctx);
-qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* st);
+// tau >= 0: the norm-screened product (B_ext's norms from both of its pools)
+qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* st, double tau = -1.0);
 // the same path for virtual rank g of P on one device (D2D copies stand in for
 // the NCCL transfers); A and B are whole matrices on this context.
 qt_mat multiply_virtual(qt_mat A, qt_mat B, const int32_t* bounds, int P, int g, qt_stats* st);

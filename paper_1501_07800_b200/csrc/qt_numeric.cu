@@ -670,6 +670,8 @@ void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
     if (a.trans & 7) fail(QT_EINVAL, "overlap phases are built for the plain product");
     if (a.subA)
       launch_numeric_t<false, false, false, 2, true>(ctx, a, grid);
+    else if (a.normA)
+      launch_numeric_t<false, false, false, 1, true>(ctx, a, grid);
     else
       launch_numeric_t<false, false, false, 0, true>(ctx, a, grid);
   } else if (a.trans & 4) {  // symmetric square

@@ -467,13 +467,19 @@ void ensure_norms(qt_mat M) {
   cudaStream_t st = ctx->stream;
   std::vector<DevBuf> nv(M->L + 1);
   nv[M->L].alloc(8 * std::max<int64_t>(M->nb, 1), st);
-  if (M->nb > 0) {
+  // block norms indexed like the pool ids (a multi-rank B_ext: ids < split in
+  // the local pool, the rest in the received payload)
+  const int64_t n1 = std::min<int64_t>(M->nb, M->split), n2 = M->nb - n1;
+  const void* p1 = M->pool_ptr();
+  for (int part = 0; part < 2; ++part) {
+    const int64_t n = part ? n2 : n1;
+    if (n <= 0) continue;
+    const void* src = part ? M->pool2 : p1;
+    double* out = nv[M->L].as<double>() + (part ? n1 : 0);
     if (M->dtype == QT_F64)
-      k_block_norm2_seq<double><<<grid_for(M->nb), kThreads, 0, st>>>(M->pool.as<double>(), M->nb,
-                                                                       nv[M->L].as<double>());
+      k_block_norm2_seq<double><<<grid_for(n), kThreads, 0, st>>>(static_cast<const double*>(src), n, out);
     else
-      k_block_norm2_seq<float><<<grid_for(M->nb), kThreads, 0, st>>>(M->pool.as<float>(), M->nb,
-                                                                      nv[M->L].as<double>());
+      k_block_norm2_seq<float><<<grid_for(n), kThreads, 0, st>>>(static_cast<const float*>(src), n, out);
     QT_LAUNCH_CHECK(ctx);
   }
   for (int l = M->L - 1; l >= 0; --l) {

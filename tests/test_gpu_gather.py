@@ -69,3 +69,53 @@ def test_gather_equals_single_rank_product(qt, bs, dtype, P, root):
             assert out[g] is None
     r, c, v = out[root]
     assert np.array_equal(r, full[0]) and np.array_equal(c, full[1]) and np.array_equal(v, full[2])
+
+
+@pytest.mark.parametrize("P,frac", [(2, 0.0), (2, 0.5), (3, 1.0)])
+def test_screened_multi_rank_loopback(qt, P, frac):
+    """The norm-screened product on P loopback ranks (B_ext's norms come from
+    its local and received pools) equals the single-rank screened product."""
+    import threading
+    import torch
+    rng = np.random.default_rng(60 + P)
+    nbr = 30
+    M = _rand(rng, nbr, 0.25, 32, np.float64)
+    M.vals *= rng.integers(1, 9, size=(M.nb, 1, 1))
+    nrm = np.sqrt((M.vals.astype(np.float64) ** 2).sum(axis=(1, 2)))
+    tau = frac * float(np.median(nrm)) ** 2      # (frac 1: about half of the block products are screened)
+    ctx0 = qt.Context(0)
+    A0 = qt.Matrix.from_blocks(ctx0, M.n, M.leaf_dim, 32, M.brow, M.bcol, M.vals)
+    ref, st_ref = A0.multiply_screened(A0, tau)
+    full = A0.multiply(A0)[1]
+    if frac > 0:
+        assert st_ref.block_products < full.block_products
+    ref = ref.to_blocks()
+    bounds = [g * (nbr // P) for g in range(P)] + [nbr]
+    hub = qt.LoopbackHub(P)
+    out, errs = [None] * P, []
+
+    def rank_fn(g):
+        try:
+            torch.cuda.set_device(0)
+            c = qt.Context(0, stream=torch.cuda.Stream(), loopback=(hub, g, P))
+            m = (M.brow >= bounds[g]) & (M.brow < bounds[g + 1])
+            A = qt.Matrix.from_blocks(c, M.n, M.leaf_dim, 32, M.brow[m], M.bcol[m], M.vals[m], row_bounds=bounds)
+            C, _ = A.multiply_screened(A, tau)
+            out[g] = C.to_blocks()
+            C.close()
+            A.close()
+            c.close()
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=rank_fn, args=(g,)) for g in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    hub.close()
+    assert not errs, errs
+    for g in range(P):
+        r, c, v = out[g]
+        m = (ref[0] >= bounds[g]) & (ref[0] < bounds[g + 1])
+        assert np.array_equal(r, ref[0][m]) and np.array_equal(c, ref[1][m]) and np.array_equal(v, ref[2][m])
