@@ -262,12 +262,16 @@ qt_status qt_read_back_async(qt_mat A, int32_t* brow, int32_t* bcol, void* value
  * kernel and summation order, so the result is bitwise that of a fresh
  * qt_multiply.  It only enqueues work on the context stream (no host
  * synchronisation, no allocation), so it can be captured into a CUDA graph.
- * A, B and C must outlive the plan.  For the symmetric square use
- * qt_symm_square (no plan).  Errors: as qt_multiply_ex; QT_EINVAL
+ * A, B and C must outlive the plan.  Errors: as qt_multiply_ex; QT_EINVAL
  * (world > 1). */
 typedef struct qt_plan_s* qt_plan;
 qt_status qt_multiply_plan(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, qt_plan* plan,
                            qt_mat* C, qt_stats* st);
+/* The symmetric square's plan (qt_symm_square, single rank, block_size 32):
+ * executing it refreshes U's transposed copy from U's current values and
+ * recomputes C — the S^2 of density-matrix purification steps whose pattern
+ * is fixed.  Errors: as qt_symm_square; QT_EBS (block_size != 32). */
+qt_status qt_symm_square_plan(qt_mat A, qt_plan* plan, qt_mat* C, qt_stats* st);
 qt_status qt_plan_execute(qt_plan plan);
 qt_status qt_plan_destroy(qt_plan plan);
 

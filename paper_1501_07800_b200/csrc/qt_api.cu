@@ -489,6 +489,43 @@ qt_status qt_multiply_plan(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b,
   API_CATCH
 }
 
+qt_status qt_symm_square_plan(qt_mat A, qt_plan* plan, qt_mat* C, qt_stats* st) {
+  API_TRY
+  if (!A || !C || !plan) fail(QT_EINVAL, "NULL argument");
+  *C = nullptr;
+  *plan = nullptr;
+  qt_ctx ctx = A->ctx;
+  if (ctx->world != 1) fail(QT_EINVAL, "plans are single-rank");
+  if (ctx->async_multiply) fail(QT_ESTATE, "plan inside qt_multiply_async");
+  if (A->ubs != 32) fail(QT_EBS, "symmetric-square plans are built for block_size 32");
+  QT_CUDA(cudaSetDevice(ctx->device));
+  check_upper(A);
+  ensure_levels(A);
+  qt_stats local;
+  qt_stats& S = st ? *st : local;
+  memset(&S, 0, sizeof(S));
+  auto* P = new qt_plan_s();
+  try {
+    P->ctx = ctx;
+    QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+    float ms_sym = 0, ms_num = 0;
+    qt_mat R = multiply_local(A, A, &S, &ms_sym, &ms_num, 4 | (A->L << 8), -1.0, nullptr, 0, INT32_MAX, &P->np);
+    S.ms_symbolic = ms_sym;
+    S.ms_numeric = ms_num;
+    QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+    QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
+    QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
+    R->global_nb = user_nblocks(R);
+    P->C = R;
+    *C = R;
+  } catch (...) {
+    delete P;
+    throw;
+  }
+  *plan = P;
+  API_CATCH
+}
+
 qt_status qt_plan_execute(qt_plan plan) {
   API_TRY
   if (!plan) fail(QT_EINVAL, "NULL plan");

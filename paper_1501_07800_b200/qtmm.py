@@ -79,6 +79,7 @@ def _load():
         "qt_plan_strips": [P, i64, i32, i32, i64, P, P, i64, P, i32, P, P],
         "qt_multiply_plan": [P, P, i32, i32, P, P, P],
         "qt_plan_execute": [P],
+        "qt_symm_square_plan": [P, P, P, P],
         "qt_plan_destroy": [P],
         "qt_update_values": [P, P],
         "qt_gather": [P, i32, P, P, P, P],
@@ -110,7 +111,7 @@ EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_nccl_unique_id", "qt_create",
             "qt_multiply_async",
             "qt_multiply_ex", "qt_symm_square", "qt_multiply_screened",
             "qt_multiply_virtual", "qt_symm_square_virtual", "qt_plan_strips", "qt_multiply_plan",
-            "qt_plan_execute", "qt_plan_destroy", "qt_update_values", "qt_gather", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
+            "qt_symm_square_plan", "qt_plan_execute", "qt_plan_destroy", "qt_update_values", "qt_gather", "qt_truncate", "qt_info", "qt_level_nodes", "qt_read_back",
             "qt_read_back_async", "qt_ctx_synchronize", "qt_destroy", "qt_last_error", "qt_kernel_launches", "qt_fp64_peak",
             "qt_loopback_hub_create", "qt_loopback_hub_destroy", "qt_ctx_create_loopback")
 
@@ -367,6 +368,13 @@ class Matrix:
         _check(_lib.qt_gather(self._h, root, _ptr(out[0]) if n else None, _ptr(out[1]) if n else None,
                               _ptr(out[2]) if n else None, None))
         return out
+
+    def symm_square_plan(self):
+        """C = A^2 (upper-triangular storage) plus a Plan that recomputes C after qt_update_values."""
+        st = Stats()
+        h, p = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(_lib.qt_symm_square_plan(self._h, ctypes.byref(p), ctypes.byref(h), ctypes.byref(st)))
+        return Plan(self.ctx, p), Matrix(self.ctx, h), st
 
     def update_values(self, vals):
         """New values (same pattern) in to_blocks order: [nblocks, bs, bs]."""

@@ -119,3 +119,34 @@ def test_plan_block_size_64_and_16_execute(qt, ctx):
             M.update_values(Mm.vals)
         assert e.value.name == "QT_EBS"
         plan.close()
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_symm_square_plan(qt, ctx, dtype):
+    """Purification-style S^2 with a fixed pattern: update U's values, execute
+    the plan, compare with a fresh symmetric square and the oracle (exact)."""
+    rng = np.random.default_rng(900 + (dtype == np.float32))
+    nbr = 20
+    m = np.triu(rng.random((nbr, nbr)) < 0.3)
+    np.fill_diagonal(m, True)
+    br, bc = np.nonzero(m)
+
+    def vals():
+        v = rng.integers(-4, 5, size=(len(br), 32, 32)).astype(dtype)
+        for t in range(len(br)):
+            if br[t] == bc[t]:
+                v[t] = np.triu(v[t]) + np.triu(v[t], 1).T
+        return v
+
+    U = qt.Matrix.from_blocks(ctx, nbr * 32, 128, 32, br.astype(np.int32), bc.astype(np.int32), vals())
+    plan, C, _ = U.symm_square_plan()
+    for _ in range(2):
+        v = vals()                      # (br, bc) from np.nonzero: already in (brow, bcol) order
+        U.update_values(v)
+        plan.execute()
+        got = C.to_blocks()
+        fresh = U.symm_square()[0].to_blocks()
+        assert all(np.array_equal(x, y) for x, y in zip(got, fresh))
+        ref = oracle.symm_square(nbr, 32, (br.astype(np.int32), bc.astype(np.int32), v.astype(np.float64)))
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[2].astype(np.float64), ref[2])
+    plan.close()
