@@ -319,6 +319,31 @@ def exchange_plan(bounds, a_rc, b_rc, block_bytes: int):
     return out
 
 
+def exchange_plan_leaf_granular(bounds, a_rc, b_rc, block_bytes: int, leaf_blocks: int):
+    """The paper's fetch granularity as a counterfactual: a
+    rank fetches whole leaf matrices ("chunks") — every B leaf
+    (leaf row, leaf column) holding a block it needs — instead of exactly the
+    needed blocks.  Returns the bytes received per rank."""
+    bounds = np.asarray(bounds, np.int64)
+    P = len(bounds) - 1
+    ar = np.asarray(a_rc[0], np.int64)
+    ac = np.asarray(a_rc[1], np.int64)
+    br = np.asarray(b_rc[0], np.int64)
+    bc = np.asarray(b_rc[1], np.int64)
+    out = []
+    for g in range(P):
+        lo, hi = bounds[g], bounds[g + 1]
+        need_rows = np.unique(ac[(ar >= lo) & (ar < hi)])
+        need_rows = need_rows[(need_rows < lo) | (need_rows >= hi)]
+        needed = np.isin(br, need_rows)
+        leaves = set(zip((br[needed] // leaf_blocks).tolist(), (bc[needed] // leaf_blocks).tolist()))
+        remote = (br < lo) | (br >= hi)
+        in_leaf = np.array([(r // leaf_blocks, c // leaf_blocks) in leaves for r, c in zip(br.tolist(), bc.tolist())],
+                           bool) if len(br) else np.zeros(0, bool)
+        out.append(int((in_leaf & remote).sum()) * block_bytes)
+    return out
+
+
 def exchange_plan_symm(bounds, u_rc, block_bytes: int):
     """Per-rank received bytes of the multi-rank symmetric square (DESIGN.md
     reading C-26; §3.3 P:297-311 for the operation, P:1179-1183 for the

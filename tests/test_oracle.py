@@ -611,3 +611,23 @@ def test_exchange_plan_symm_banded_closed_form(P):
     full = oracle.exchange_plan(bounds, (br, bc), (br, bc), 8192)
     mx, mx_full = max(q["payload_bytes"] for q in plan), max(q["payload_bytes"] for q in full)
     assert mx == (1584 if P > 2 else 1056) * 8192 and mx_full == (34078720 if P > 2 else 17039360)
+
+
+def test_exchange_plan_leaf_granular_banded():
+    """fetching whole leaves (the paper's chunks) instead of exact
+    blocks.  Config 5 at P = 4, leaf = 64 block rows: an interior rank needs
+    the 32 block rows of each neighbouring leaf row next to its strip; the
+    needed blocks touch two leaves per side, which hold the full band of the
+    32 needed rows (32·65 blocks) plus, for the other 32 rows of the leaf row,
+    the part of their band inside those two leaf columns (Σ_{k=33}^{64} k):
+    3632 blocks per side = 1.75x the exact fetch (SURVEY: "roughly doubles")."""
+    P, D, per, leaf = 4, 32, 512, 64
+    br, bc = qtgen.pattern_banded(512 * P, D)
+    bounds = [g * per for g in range(P + 1)]
+    exact = oracle.exchange_plan(bounds, (br, bc), (br, bc), 8192)
+    chunks = oracle.exchange_plan_leaf_granular(bounds, (br, bc), (br, bc), 8192, leaf)
+    side = D * (2 * D + 1) + sum(range(D + 1, 2 * D + 1))                           # 3632
+    for g in (1, 2):
+        assert exact[g]["payload_bytes"] == 2 * D * (2 * D + 1) * 8192              # 34.1 MB
+        assert chunks[g] == 2 * side * 8192                                         # 59.5 MB
+    assert chunks[0] == side * 8192 and exact[0]["payload_bytes"] == D * (2 * D + 1) * 8192
