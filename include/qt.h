@@ -205,8 +205,10 @@ qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st);
 qt_status qt_truncate(qt_mat A, double tau, qt_mat* out);
 
 /* Describe a matrix.  Any output pointer may be NULL.  local_nblocks: blocks
- * held by this rank; global_nblocks: over all ranks; row_lo/row_hi: this
- * rank's block-row range. */
+ * held by this rank; global_nblocks: over all ranks for created and truncated
+ * matrices — for the product of a multi-rank multiply it is the local count
+ * (summing would cost the multiply a collective; qt_gather's `total` gives
+ * the global count); row_lo/row_hi: this rank's block-row range. */
 qt_status qt_info(qt_mat A, int64_t* n, int32_t* leaf_dim, int32_t* block_size,
                   qt_dtype* dtype, int64_t* local_nblocks, int64_t* global_nblocks,
                   int32_t* row_lo, int32_t* row_hi);
