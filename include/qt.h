@@ -181,7 +181,12 @@ qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_sta
  * child transposed as (1,0); transposed nodes swap and transpose their
  * children) and prunes C nodes below the diagonal at every level; blocks
  * read transposed come from a transposed copy of U's block pool made once
- * per call.  FP64 or FP32 (A's dtype).
+ * per call.  FP64 or FP32 (A's dtype).  Block size 16 (the paper's S^2 runs,
+ * P:926-935): the 32-containers of U are the upper triangle at container
+ * granularity; a diagonal container's (1,0) 16-block is below the diagonal
+ * (QT_EINVAL) and is filled in as (0,1)^T on a copy of U, C's diagonal
+ * containers are computed whole and their (1,0) 16-blocks dropped
+ * (DESIGN reading C-28); block_products counts 16-block products.
  * Multi-rank (world > 1, block_size 32; collective): each rank passes its
  * block rows of U (the bounds given at create time) and gets its block rows
  * of C, upper triangle.  Rank g receives from the others every block of U
@@ -191,7 +196,7 @@ qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_sta
  * oracle.exchange_plan_symm) — and runs the
  * symmetric-square BFS on its blocks + the received ones, pruned to its rows.
  * Errors: QT_EINVAL (a block below the diagonal), QT_EBS (world > 1 with
- * block_size 64), QT_ENOMEM, QT_ECUDA, QT_ENCCL. */
+ * block_size 16 or 64), QT_ENOMEM, QT_ECUDA, QT_ENCCL. */
 qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st);
 
 /* Frobenius-norm truncation (reading C-16): remove the longest

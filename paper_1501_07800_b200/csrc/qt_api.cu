@@ -618,9 +618,11 @@ qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
   *C = nullptr;
   qt_ctx ctx = A->ctx;
   QT_CUDA(cudaSetDevice(ctx->device));
-  if (A->ubs == 16) fail(QT_EBS, "the symmetric square is built for block sizes 32 and 64");
   if (ctx->world > 1 && A->ubs != 32) fail(QT_EBS, "the multi-rank symmetric square needs block_size 32");
-  check_upper(A);
+  if (A->ubs == 16)
+    check_upper16(A);
+  else
+    check_upper(A);
   ensure_levels(A);
   qt_stats local;
   qt_stats& S = st ? *st : local;
@@ -644,6 +646,13 @@ qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
       throw;
     }
     delete U;
+  } else if (A->ubs == 16) {
+    // diagonal 32-containers completed with (1,0) = (0,1)^T: the symmetric
+    // square of the 32-container matrix, the (1,0) 16-blocks of C's diagonal
+    // containers left out (k_cmask16) and zeroed (symm_finish16); the
+    // completed copy is kept with A for the next call
+    if (!A->sym16) A->sym16.reset(symm_prepare16(A));
+    R = multiply_local(A->sym16.get(), A->sym16.get(), &S, &ms_sym, &ms_num, 4 | (A->L << 8));
   } else {
     R = multiply_local(A, A, &S, &ms_sym, &ms_num, 4 | (A->L << 8));
   }

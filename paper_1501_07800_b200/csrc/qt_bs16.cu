@@ -60,12 +60,13 @@ __device__ __forceinline__ int swz(int r, int c) {
 }
 
 // boolean 2x2 product of quadrant masks, and the number of quadrant products
-__device__ __forceinline__ int mask_mul(int a, int b, int& nprod) {
+__device__ __forceinline__ int mask_mul(int a, int b, int& nprod, int keep = 15) {
   int out = 0;
 #pragma unroll
   for (int r = 0; r < 2; ++r)
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
+      if (!((keep >> (2 * r + c)) & 1)) continue;
       const int n = (((a >> (2 * r)) & 1) & ((b >> c) & 1)) + (((a >> (2 * r + 1)) & 1) & ((b >> (2 + c)) & 1));
       nprod += n;
       if (n) out |= 1 << (2 * r + c);
@@ -213,14 +214,27 @@ __global__ void k_zero_absent16(T* __restrict__ pool, const uint8_t* __restrict_
 __global__ void k_cmask16(const int32_t* __restrict__ ts, const int32_t* __restrict__ pa, const int32_t* __restrict__ pb,
                           int64_t ntiles, const int4* __restrict__ cA, const int4* __restrict__ cB,
                           const int4* __restrict__ cC, const uint8_t* __restrict__ subA,
-                          const uint8_t* __restrict__ subB, int trans, uint8_t* __restrict__ subC,
-                          unsigned long long* __restrict__ counts) {
+                          const uint8_t* __restrict__ subB, int trans, const uint64_t* __restrict__ keyC,
+                          uint8_t* __restrict__ subC, unsigned long long* __restrict__ counts) {
+  // symmetric square (trans bit 2): node and block entries are references
+  // into U (index << 2 | diagonal << 1 | transposed), see op_children; the
+  // (1,0) quadrant of a diagonal C container, and every container below the
+  // diagonal, are not part of C: none of their products counted
+  const bool sym = trans & 4;
   const int lane = threadIdx.x & 31;
   const int64_t t = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
   if (t >= ntiles) return;
+  int keep[4] = {15, 15, 15, 15};
+  if (sym) {
+    const int4 c4 = cC[t];
+    const int c[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)  // (a container below the diagonal of a diagonal tile is NIL in C)
+      keep[q] = c[q] < 0 ? 0 : morton_row(keyC[c[q]]) == morton_col(keyC[c[q]]) ? 11 : 15;
+  }
   int m[4] = {0, 0, 0, 0}, np = 0, npairs = 0;
   for (int32_t p = ts[t] + lane; p < ts[t + 1]; p += 32) {
-    const int4 A4 = op_children(cA, pa[p], trans & 1, false), B4 = op_children(cB, pb[p], trans & 2, false);
+    const int4 A4 = op_children(cA, pa[p], trans & 1, sym), B4 = op_children(cB, pb[p], trans & 2, sym);
     const int a[4] = {A4.x, A4.y, A4.z, A4.w}, b[4] = {B4.x, B4.y, B4.z, B4.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -230,10 +244,19 @@ __global__ void k_cmask16(const int32_t* __restrict__ ts, const int32_t* __restr
         const int x = a[2 * i + k], y = b[2 * k + j];
         if (x < 0 || y < 0) continue;
         ++npairs;
-        int ma = subA[x], mb = subB[y];
-        if (trans & 1) ma = mask_t(ma);
-        if (trans & 2) mb = mask_t(mb);
-        m[q] |= mask_mul(ma, mb, np);
+        int ma, mb;
+        if (sym) {
+          ma = subA[x >> 2];
+          mb = subB[y >> 2];
+          if (x & 1) ma = mask_t(ma);
+          if (y & 1) mb = mask_t(mb);
+        } else {
+          ma = subA[x];
+          mb = subB[y];
+          if (trans & 1) ma = mask_t(ma);
+          if (trans & 2) mb = mask_t(mb);
+        }
+        m[q] |= mask_mul(ma, mb, np, keep[q]);
       }
     }
   }
@@ -259,6 +282,44 @@ __global__ void k_cmask16(const int32_t* __restrict__ ts, const int32_t* __restr
     atomicAdd(&counts[1], (unsigned long long)n16);
     atomicAdd(&counts[2], (unsigned long long)empty);
     atomicAdd(&counts[3], (unsigned long long)npairs);
+  }
+}
+
+// the first container holding a 16-block below the diagonal (R > C, or the
+// (1,0) quadrant of a diagonal container)
+__global__ void k_lower16(const uint64_t* __restrict__ key, const uint8_t* __restrict__ sub, int64_t n,
+                          unsigned long long* __restrict__ bad) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t R = morton_row(key[t]), C = morton_col(key[t]);
+    if (R > C || (R == C && (sub[t] & 4))) atomicMin(bad, (unsigned long long)t);
+  }
+}
+
+// symmetric square at bs 16: a diagonal container of U gets its (1,0)
+// quadrant = (0,1)^T, so it is the full symmetric 32-block the 32-level
+// symmetric square uses as stored (reading C-23 one level down)
+template <class T>
+__global__ void k_complete_diag16(const uint64_t* __restrict__ key, uint8_t* __restrict__ sub, int64_t n,
+                                  T* __restrict__ pool) {
+  for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+    if (morton_row(key[t]) != morton_col(key[t]) || !(sub[t] & 2)) continue;
+    T* b = pool + t * 1024;
+    const int e = threadIdx.x, r = e >> 4, c = e & 15;  // (1,0)[r][c] = (0,1)[c][r]
+    b[swz<T>(16 + r, c)] = b[swz<T>(c, 16 + r)];
+    if (threadIdx.x == 0) sub[t] |= 4;
+  }
+}
+
+// C of the bs-16 symmetric square: the (1,0) quadrant of a diagonal
+// container is below the diagonal — not part of C (k_cmask16 left its mask
+// bit clear); the numeric kernel computed it with the full 32-block: zero it
+template <class T>
+__global__ void k_drop_lower16(const uint64_t* __restrict__ key, int64_t n, T* __restrict__ pool) {
+  for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+    if (morton_row(key[t]) != morton_col(key[t])) continue;
+    T* b = pool + t * 1024;
+    const int e = threadIdx.x, r = e >> 4, c = e & 15;
+    b[swz<T>(16 + r, c)] = T(0);
   }
 }
 
@@ -441,21 +502,70 @@ int64_t compact_sub16(qt_ctx ctx, const uint8_t* keep, const int32_t* incl, cons
 }
 
 void cmask16(qt_ctx ctx, int64_t ntiles, const int32_t* ts, const int32_t* pa, const int32_t* pb, const int4* cA,
-             const int4* cB, const int4* cC, const uint8_t* subA, const uint8_t* subB, int trans, uint8_t* subC,
-             int64_t nc, int64_t out[4]) {
+             const int4* cB, const int4* cC, const uint8_t* subA, const uint8_t* subB, int trans,
+             const uint64_t* keyC, uint8_t* subC, int64_t nc, int64_t out[4]) {
   cudaStream_t st = ctx->stream;
   DevBuf cnt(32, st);
   QT_CUDA(cudaMemsetAsync(cnt.p, 0, 32, st));
   QT_CUDA(cudaMemsetAsync(subC, 0, std::max<int64_t>(nc, 1), st));
   if (ntiles > 0) {
-    k_cmask16<<<(unsigned)((ntiles + 7) / 8), 256, 0, st>>>(ts, pa, pb, ntiles, cA, cB, cC, subA, subB, trans, subC,
-                                                           cnt.as<unsigned long long>());
+    k_cmask16<<<(unsigned)((ntiles + 7) / 8), 256, 0, st>>>(ts, pa, pb, ntiles, cA, cB, cC, subA, subB, trans, keyC,
+                                                           subC, cnt.as<unsigned long long>());
     QT_LAUNCH_CHECK(ctx);
   }
   unsigned long long h[4];
   QT_CUDA(cudaMemcpyAsync(h, cnt.p, 32, cudaMemcpyDeviceToHost, st));
   QT_CUDA(cudaStreamSynchronize(st));
   for (int i = 0; i < 4; ++i) out[i] = (int64_t)h[i];
+}
+
+void check_upper16(qt_mat M) {
+  qt_ctx ctx = M->ctx;
+  if (M->nb == 0) return;
+  unsigned long long* bad = ctx->counters.as<unsigned long long>();
+  QT_CUDA(cudaMemsetAsync(bad, 0xff, 8, ctx->stream));
+  k_lower16<<<gfor(M->nb), kT, 0, ctx->stream>>>(M->key.as<uint64_t>(), M->sub.as<uint8_t>(), M->nb, bad);
+  QT_LAUNCH_CHECK(ctx);
+  const unsigned long long b = read_scalar(ctx, bad);
+  if (b != ~0ull) {
+    uint64_t k;
+    uint8_t m;
+    QT_CUDA(cudaMemcpy(&k, M->key.as<uint64_t>() + b, 8, cudaMemcpyDeviceToHost));
+    QT_CUDA(cudaMemcpy(&m, M->sub.as<uint8_t>() + b, 1, cudaMemcpyDeviceToHost));
+    const uint32_t R = morton_row(k), C = morton_col(k);
+    const int q = R > C ? __builtin_ctz(m) : 2;
+    fail(QT_EINVAL, "symmetric square needs upper-triangular block storage; block (brow=%u, bcol=%u) is below "
+         "the diagonal", 2 * R + (q >> 1), 2 * C + (q & 1));
+  }
+}
+
+qt_mat symm_prepare16(qt_mat U) {
+  qt_ctx ctx = U->ctx;
+  DevBuf keep(std::max<int64_t>(U->nb, 1), ctx->stream);
+  if (U->nb > 0) QT_CUDA(cudaMemsetAsync(keep.p, 1, U->nb, ctx->stream));
+  qt_mat X = select_blocks(U, keep.as<uint8_t>());  // a copy (U itself stays as the caller gave it)
+  if (X->nb > 0) {
+    const unsigned g = (unsigned)std::min<int64_t>(X->nb, 148 * 16);
+    if (X->dtype == QT_F64)
+      k_complete_diag16<double><<<g, 256, 0, ctx->stream>>>(X->key.as<uint64_t>(), X->sub.as<uint8_t>(), X->nb,
+                                                            X->pool.as<double>());
+    else
+      k_complete_diag16<float><<<g, 256, 0, ctx->stream>>>(X->key.as<uint64_t>(), X->sub.as<uint8_t>(), X->nb,
+                                                           X->pool.as<float>());
+    QT_LAUNCH_CHECK(ctx);
+  }
+  return X;
+}
+
+void symm_finish16(qt_mat C) {
+  qt_ctx ctx = C->ctx;
+  if (C->nb == 0) return;
+  const unsigned g = (unsigned)std::min<int64_t>(C->nb, 148 * 16);
+  if (C->dtype == QT_F64)
+    k_drop_lower16<double><<<g, 256, 0, ctx->stream>>>(C->key.as<uint64_t>(), C->nb, C->pool.as<double>());
+  else
+    k_drop_lower16<float><<<g, 256, 0, ctx->stream>>>(C->key.as<uint64_t>(), C->nb, C->pool.as<float>());
+  QT_LAUNCH_CHECK(ctx);
 }
 
 qt_mat drop_empty16(qt_mat C) {

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "../../include/qt.h"
@@ -152,6 +153,10 @@ struct qt_mat_s {
   qt::DevBuf rm_inv;   // pool index -> position in row-major (brow, bcol) order (qt_update_values; lazy)
   qt::DevBuf sub;      // ubs == 16: uint8 [nb] quadrant occupancy (bit 2i+j), indexed like the pool
   int64_t nb16 = 0;    // ubs == 16: the caller's blocks (set quadrants)
+  // ubs == 16 symmetric square: the copy with completed diagonal containers
+  // (symm_prepare16), made on the first call and kept (values never change
+  // in place at bs 16: qt_update_values is bs 32 only)
+  std::unique_ptr<qt_mat_s> sym16;
   // B_ext of a multi-rank multiply: pool1 overrides pool.p (a borrowed view of
   // the local pool); block ids >= split live in pool2 (the received blocks).
   const void* pool1 = nullptr;
@@ -208,9 +213,14 @@ int64_t compact_sub16(qt_ctx ctx, const uint8_t* keep, const int32_t* incl, cons
 // C's quadrant masks from the level L-1 task list; out = {16-block products, C 16-blocks, empty
 // containers, non-NIL container pairs (the level-L task count)}
 void cmask16(qt_ctx ctx, int64_t ntiles, const int32_t* ts, const int32_t* pa, const int32_t* pb, const int4* cA,
-             const int4* cB, const int4* cC, const uint8_t* subA, const uint8_t* subB, int trans, uint8_t* subC,
-             int64_t nc, int64_t out[4]);
+             const int4* cB, const int4* cC, const uint8_t* subA, const uint8_t* subB, int trans,
+             const uint64_t* keyC, uint8_t* subC, int64_t nc, int64_t out[4]);
 qt_mat drop_empty16(qt_mat C);
+// symmetric square at bs 16: upper-storage check, U with completed diagonal
+// containers, and C's lower quadrants of diagonal containers removed
+void check_upper16(qt_mat M);
+qt_mat symm_prepare16(qt_mat U);
+void symm_finish16(qt_mat C);
 // keep flags per user block -> per internal block
 void expand_keep(qt_mat M, const uint8_t* keep_user, DevBuf& keep32);
 // truncate (reading C-16): local terms, global decision, single-rank driver

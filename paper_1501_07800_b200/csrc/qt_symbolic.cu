@@ -93,10 +93,10 @@ struct Screen {
 };
 __device__ __forceinline__ bool pair_ok(int ar, int br, const Screen& sc, bool sym) {
   if (ar < 0 || br < 0) return false;
-  if (sc.ma) {
-    int x = sc.ma[ar], y = sc.mb[br];
-    if (sc.tr & 1) x = mask_t(x);
-    if (sc.tr & 2) y = mask_t(y);
+  if (sc.ma) {  // (symmetric square: references into U carry the transpose bit)
+    int x = sc.ma[sym ? (ar >> 2) : ar], y = sc.mb[sym ? (br >> 2) : br];
+    if (sym ? (ar & 1) : (sc.tr & 1)) x = mask_t(x);
+    if (sym ? (br & 1) : (sc.tr & 2)) y = mask_t(y);
     return mask_meet(x, y);
   }
   if (!sc.na) return true;
@@ -729,6 +729,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       sa.tau2 = tau2;
       sa.row_lo = row_lo;
       sa.row_hi = row_hi;
+      // (bs 16: container pairs whose quadrant masks never meet are pruned)
       sa.subA = A->ubs == 16 ? A->sub.as<uint8_t>() : nullptr;
       sa.subB = A->ubs == 16 ? B->sub.as<uint8_t>() : nullptr;
       for (int l = 0; l <= L && l < QT_MAX_LEVELS; ++l) {
@@ -936,7 +937,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       na.normA = screen ? A->norm2[L].as<double>() : nullptr;
       na.normB = screen ? B->norm2[L].as<double>() : nullptr;
       na.tau2 = tau2;
-      if (A->ubs == 16) {
+      if (A->ubs == 16 && !sym) {
         na.subA = A->sub.as<uint8_t>();
         na.subB = B->sub.as<uint8_t>();
       }
@@ -1018,8 +1019,10 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         C->sub.alloc(std::max<int64_t>(C->nb, 1), st);
         int64_t r16[4];
         cmask16(ctx, ns[L - 1], cstart.as<int32_t>(), pa.as<int32_t>(), pb.as<int32_t>(), A->child[L - 1].as<int4>(),
-                B->child[L - 1].as<int4>(), cchild.as<int4>(), A->sub.as<uint8_t>(), B->sub.as<uint8_t>(), trans & 3,
-                C->sub.as<uint8_t>(), C->nb, r16);
+                B->child[L - 1].as<int4>(), cchild.as<int4>(), A->sub.as<uint8_t>(), B->sub.as<uint8_t>(), trans & 7,
+                C->key.as<uint64_t>(), C->sub.as<uint8_t>(), C->nb, r16);
+        tr.mark("cmask16");
+        if (sym) symm_finish16(C);
         C->nb16 = r16[1];
         S.level_tasks[L] = r16[3];  // all non-NIL container pairs (the BFS kept those with a 16-block product)
         S.level_tasks[L + 1] = r16[0];
@@ -1029,6 +1032,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
           qt_mat D = drop_empty16(C);
           delete C;
           C = D;
+          tr.mark("drop_empty16");
         }
       }
       if (plan && C->nb > 0 && !two_phase && C->pool.p == plan_pool_c) {  // keep the launch for qt_plan_execute

@@ -84,10 +84,15 @@ def test_bs16_errors(qt, ctx):
     with pytest.raises(qt.QtError) as e:      # n must be a multiple of 32 (reading C-27)
         qt.Matrix.from_blocks(ctx, 48, 32, 16, np.array([0], np.int32), np.array([0], np.int32), v[:1])
     assert e.value.name == "QT_EINVAL"
-    U = qt.Matrix.from_blocks(ctx, 128, 64, 16, np.array([0], np.int32), np.array([1], np.int32), v[:1])
+    # symmetric square: the (1,0) 16-block of a diagonal 32-container is below the diagonal
+    U = qt.Matrix.from_blocks(ctx, 128, 64, 16, np.array([0, 5], np.int32), np.array([1, 4], np.int32), v)
     with pytest.raises(qt.QtError) as e:
         U.symm_square()
-    assert e.value.name == "QT_EBS"
+    assert e.value.name == "QT_EINVAL" and "brow=5, bcol=4" in str(e.value)
+    U = qt.Matrix.from_blocks(ctx, 128, 64, 16, np.array([0, 6], np.int32), np.array([1, 1], np.int32), v)
+    with pytest.raises(qt.QtError) as e:
+        U.symm_square()
+    assert e.value.name == "QT_EINVAL" and "brow=6, bcol=1" in str(e.value)
 
 
 @pytest.mark.parametrize("nbr,p,leaf", [(2, 1.0, 32), (8, 1.0, 64), (14, 0.5, 64), (38, 0.15, 128),
@@ -231,3 +236,79 @@ def test_bs16_loopback_two_ranks(qt, ctx):
         assert (info["row_lo"], info["row_hi"]) == (bounds[g], bounds[g + 1])
         mt = (tr[0] >= bounds[g]) & (tr[0] < bounds[g + 1])
         assert np.array_equal(tr_r, tr[0][mt]) and np.array_equal(tr_c, tr[1][mt])
+
+
+def random_upper16(rng, nbr, p, kind, leaf, dtype=np.float64):
+    """Upper block triangle at 16-block granularity, symmetric diagonal blocks."""
+    m = np.triu(rng.random((nbr, nbr)) < p)
+    M = random_bm16(rng, nbr, p, kind, leaf, dtype, mask=m)
+    for t in range(M.nb):
+        if M.brow[t] == M.bcol[t]:
+            M.vals[t] = np.triu(M.vals[t]) + np.triu(M.vals[t], 1).T
+    return M
+
+
+@pytest.mark.parametrize("nbr,p,leaf", [(2, 1.0, 32), (8, 1.0, 64), (14, 0.5, 64), (38, 0.15, 128),
+                                        (64, 0.05, 256)])
+@pytest.mark.parametrize("kind,dtype", [("int", np.float64), ("uniform", np.float64), ("int", np.float32)])
+def test_bs16_symm_square(qt, ctx, nbr, p, leaf, kind, dtype):
+    """Reading C-28: C = A^2 from A's upper 16-block triangle; the oracle
+    expands U to the full symmetric matrix and multiplies at bs 16.  The
+    16-block products counted are those of C's upper triangle (brute-force
+    coarsening count, oracle.level_task_counts_sym), i.e. the (1,0) quadrants
+    of diagonal containers are neither stored nor counted."""
+    rng = np.random.default_rng(1700 + nbr + 3 * (kind == "int") + 7 * (dtype == np.float32))
+    Um = random_upper16(rng, nbr, p, kind, leaf, dtype)
+    U = mk(qt, ctx, Um)
+    C, st = U.symm_square()
+    got = C.to_blocks()
+    ref = oracle.symm_square(nbr, 16, tup(Um))
+    assert np.all(got[0] <= got[1])
+    if kind == "int":
+        check(got, ref, None, None, nbr, "int")
+    else:
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+        full = oracle.expand_symmetric(*tup(Um))
+        d = got[2] - ref[2]
+        assert np.linalg.norm(d) <= REL_FRO_F64 * np.linalg.norm(ref[2])
+        br, bc, bound = oracle.higham_bound(nbr, 16, full, full, nbr * 16)
+        assert np.all(np.abs(d) <= bound[br <= bc] + 1e-300)   # (bound of the full product, upper blocks)
+    assert C.nblocks == len(ref[0]) and st.c_blocks == len(ref[0])
+    L, _ = oracle.tree_levels(Um.n, 16, leaf)
+    assert st.block_products == oracle.level_task_counts_sym(L, (Um.brow, Um.bcol))[-1]
+    # the stored U is untouched (the diagonal completion works on a copy)
+    r, c, v = U.to_blocks()
+    o = np.lexsort((Um.bcol, Um.brow))
+    assert np.array_equal(v, Um.vals[o])
+    # C is again upper-triangular bs-16 storage: square it once more
+    C2 = C.symm_square()[0].to_blocks()
+    ref2 = oracle.symm_square(nbr, 16, ref)
+    assert np.array_equal(C2[0], ref2[0]) and np.array_equal(C2[1], ref2[1])
+    if kind == "int" and dtype == np.float64:     # (|C^2| < 2^53: exact)
+        assert np.array_equal(C2[2], ref2[2])
+
+
+def test_bs16_symm_square_matches_full_multiply(qt, ctx):
+    """The symmetric square equals the upper triangle of the full multiply of
+    the expanded matrix computed by the library itself (integer values: exact),
+    and needs fewer 16-block products."""
+    rng = np.random.default_rng(1777)
+    nbr = 96
+    Um = random_upper16(rng, nbr, 0.08, "int", 256)
+    fr, fc, fv = oracle.expand_symmetric(Um.brow, Um.bcol, Um.vals)
+    F = qt.Matrix.from_blocks(ctx, Um.n, 256, 16, fr, fc, fv)
+    Cf, sf = F.multiply(F)
+    r, c, v = Cf.to_blocks()
+    keep = r <= c
+    Cs, ss = mk(qt, ctx, Um).symm_square()
+    gr, gc, gv = Cs.to_blocks()
+    assert np.array_equal(gr, r[keep]) and np.array_equal(gc, c[keep]) and np.array_equal(gv, v[keep])
+    assert ss.block_products < 0.6 * sf.block_products
+
+
+def test_bs16_symm_square_multi_rank_rejected(qt, ctx):
+    rng = np.random.default_rng(1778)
+    Um = random_upper16(rng, 8, 0.5, "int", 64)
+    with pytest.raises(qt.QtError) as e:
+        mk(qt, ctx, Um).symm_square_virtual(2, 0, [0, 4, 8])
+    assert e.value.name == "QT_EBS"

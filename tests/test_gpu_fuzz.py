@@ -1,7 +1,7 @@
 """Seeded randomized sweep over the entry points (needs a B200): random grid
 sizes (ragged against the 2x2 / 4x4 tiles and the leaves), densities from
 empty to full, leaf sizes, block sizes 16/32/64, FP64/FP32, transposed
-operands, the symmetric square, the screened product and virtual ranks —
+operands, the symmetric square (block sizes 32 and 16), the screened product and virtual ranks —
 every result against the oracle on the same inputs (integer values: exact).
 A 2000-case sweep (QT_FUZZ_MUL=1200 QT_FUZZ_MISC=400 QT_FUZZ_NBR=80) passed."""
 import os
@@ -116,6 +116,19 @@ def test_fuzz_symm_screen_truncate_virtual(qt, ctx, seed):
         ms = (sref[0] >= bounds[g]) & (sref[0] < bounds[g + 1])
         r, c, v = Sg.to_blocks()
         assert np.array_equal(r, sref[0][ms]) and np.array_equal(v, sref[2][ms])
+
+
+@pytest.mark.parametrize("seed", range(N_MISC))
+def test_fuzz_symm16(qt, ctx, seed):
+    """Symmetric square at block size 16 (reading C-28) on random upper
+    16-block triangles."""
+    rng = np.random.default_rng(8500 + seed)
+    dtype = np.float64 if seed % 3 else np.float32
+    nbr = 2 * int(rng.integers(1, NBR_MAX // 2))
+    p = float(rng.choice([0.0, 0.05, 0.2, 0.6, 1.0]))
+    leaf = 32 * int(2 ** rng.integers(0, 4))
+    U = rand_int_bm(rng, nbr, p, 16, leaf, dtype, upper=True)
+    same(mk(qt, ctx, U).symm_square()[0].to_blocks(), oracle.symm_square(nbr, 16, t64(U)))
 
 
 @pytest.mark.parametrize("seed", range(N_MISC))

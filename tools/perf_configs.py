@@ -48,6 +48,51 @@ def run_sym(ctx, stream, name, full, steps=20):
     print(json.dumps({"config": name, **out}), flush=True)
 
 
+def run_sym16(ctx, stream, steps=10):
+    """The paper's S^2 shape at block size 16 (reading C-28): a
+    symmetric banded pattern of 16-blocks (half-width 48 blocks, fill 0.5),
+    N = 16384; symmetric square of the upper triangle vs the full multiply."""
+    rng = np.random.default_rng(1007)
+    nbr, w = 1024, 48
+    I, J = np.meshgrid(np.arange(nbr), np.arange(nbr), indexing="ij")
+    m = np.triu((np.abs(I - J) <= w) & (rng.random((nbr, nbr)) < 0.5))
+    np.fill_diagonal(m, True)
+    ur, uc = np.nonzero(m)
+    uv = rng.uniform(-1, 1, size=(len(ur), 16, 16))
+    d = ur == uc
+    uv[d] = (uv[d] + uv[d].transpose(0, 2, 1)) / 2
+    off = ~d
+    fr = np.concatenate([ur, uc[off]]).astype(np.int32)
+    fc = np.concatenate([uc, ur[off]]).astype(np.int32)
+    fv = np.concatenate([uv, uv[off].transpose(0, 2, 1)])
+    A = qtmm.Matrix.from_blocks(ctx, nbr * 16, 2048, 16, fr, fc, fv)
+    Au = qtmm.Matrix.from_blocks(ctx, nbr * 16, 2048, 16, ur.astype(np.int32), uc.astype(np.int32), uv)
+    out = {}
+    for label, fn in (("full", lambda: A.multiply(A)), ("symm", lambda: Au.symm_square())):
+        for _ in range(3):
+            C, st = fn()
+            C.close()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sts = []
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(steps):
+            C, st = fn()
+            sts.append(st)
+            C.close()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        out[label] = {"ms_step": round(ms, 4), "block_products_16": sts[-1].block_products,
+                      "c_blocks_16": sts[-1].c_blocks,
+                      "ms_symbolic": round(statistics.mean(s.ms_symbolic for s in sts), 4),
+                      "ms_numeric": round(statistics.mean(s.ms_numeric for s in sts), 4),
+                      "gflops_effective_16": round(sts[-1].block_products * 2 * 16 ** 3 / ms / 1e6, 1)}
+    out["speedup"] = round(out["full"]["ms_step"] / out["symm"]["ms_step"], 3)
+    print(json.dumps({"config": "S^2 bs16 banded N=16384 (w=48 blocks, fill 0.5): symm_square vs full", **out}),
+          flush=True)
+
+
 def run(ctx, stream, name, c, steps=20):
     Am = c["A"]
     A = qtmm.Matrix.from_blocks(ctx, Am.n, Am.leaf_dim, 32, Am.brow, Am.bcol, Am.vals)
@@ -268,6 +313,8 @@ def main():
             M = qtgen.config(5, P=1, symmetric=True)["A"]
             run_sym(ctx, stream, "cfg5 banded symmetric FP32: symm_square vs full",
                     qtgen.BlockMatrix(M.n, M.leaf_dim, 32, M.brow, M.bcol, M.vals.astype(np.float32)))
+        elif w == "sym16":
+            run_sym16(ctx, stream)
         elif w == "sym4":
             run_sym(ctx, stream, "cfg4 ES-like symmetric (S^2): symm_square vs full",
                     qtgen.config(4, symmetric=True)["A"], steps=5)
