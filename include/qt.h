@@ -187,7 +187,7 @@ qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_sta
  * (QT_EINVAL) and is filled in as (0,1)^T on a copy of U, C's diagonal
  * containers are computed whole and their (1,0) 16-blocks dropped
  * (DESIGN reading C-28); block_products counts 16-block products.
- * Multi-rank (world > 1, block_size 32; collective): each rank passes its
+ * Multi-rank (world > 1, block_size 16 or 32; collective): each rank passes its
  * block rows of U (the bounds given at create time) and gets its block rows
  * of C, upper triangle.  Rank g receives from the others every block of U
  * that a product of its C rows reads, and no other — the rows and columns its
@@ -195,8 +195,10 @@ qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_sta
  * rows below it that reach into it (DESIGN reading C-26; bytes in `st`,
  * oracle.exchange_plan_symm) — and runs the
  * symmetric-square BFS on its blocks + the received ones, pruned to its rows.
+ * At block size 16 the exchange moves 32-containers (completed diagonal
+ * ones) + one mask byte each.
  * Errors: QT_EINVAL (a block below the diagonal), QT_EBS (world > 1 with
- * block_size 16 or 64), QT_ENOMEM, QT_ECUDA, QT_ENCCL. */
+ * block_size 64), QT_ENOMEM, QT_ECUDA, QT_ENCCL. */
 qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st);
 
 /* Frobenius-norm truncation (reading C-16): remove the longest
@@ -332,7 +334,7 @@ qt_status qt_plan_strips(qt_ctx ctx, int64_t n, int32_t block_size, int32_t alig
  * block rows are [row_bounds[g], row_bounds[g+1]); the blocks it would receive
  * are selected from U by the rule of qt_symm_square and the same pruned BFS
  * runs.  C holds rank g's rows of A^2 (upper triangle); `st` reports what
- * rank g would receive.  block_size 32.  Errors: as qt_multiply_virtual,
+ * rank g would receive.  block_size 16 (even row_bounds) or 32.  Errors: as qt_multiply_virtual,
  * QT_EINVAL (a block below the diagonal), QT_EBS (block_size 64). */
 qt_status qt_symm_square_virtual(qt_mat A, int32_t P, int32_t g, const int32_t* row_bounds, qt_mat* C,
                                  qt_stats* st);

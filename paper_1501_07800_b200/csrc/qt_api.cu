@@ -618,7 +618,7 @@ qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
   *C = nullptr;
   qt_ctx ctx = A->ctx;
   QT_CUDA(cudaSetDevice(ctx->device));
-  if (ctx->world > 1 && A->ubs != 32) fail(QT_EBS, "the multi-rank symmetric square needs block_size 32");
+  if (ctx->world > 1 && A->ubs == 64) fail(QT_EBS, "the multi-rank symmetric square needs block_size 16 or 32");
   if (A->ubs == 16)
     check_upper16(A);
   else
@@ -631,7 +631,10 @@ qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
   float ms_sym = 0, ms_num = 0;
   qt_mat R;
   if (ctx->world > 1) {
-    R = symm_square_dist(A, &S);
+    // (block size 16: the exchange moves the completed containers of each
+    // rank's copy, so received diagonal containers arrive complete)
+    if (A->ubs == 16 && !A->sym16) A->sym16.reset(symm_prepare16(A));
+    R = symm_square_dist(A->ubs == 16 ? A->sym16.get() : A, &S);
     ms_sym = S.ms_symbolic;
     ms_num = S.ms_numeric;
   } else if (A->ubs == 64) {
@@ -876,20 +879,30 @@ qt_status qt_symm_square_virtual(qt_mat A, int32_t P, int32_t g, const int32_t* 
   if (!A || !C || !row_bounds) fail(QT_EINVAL, "NULL argument");
   *C = nullptr;
   if (A->ctx->world != 1) fail(QT_ESTATE, "virtual ranks need a single-rank context");
-  if (A->ubs != 32) fail(QT_EBS, "the multi-rank symmetric square needs block_size 32");
+  if (A->ubs == 64) fail(QT_EBS, "the multi-rank symmetric square needs block_size 16 or 32");
   if (P < 1 || g < 0 || g >= P) fail(QT_EINVAL, "bad P=%d / g=%d", P, g);
-  std::vector<int32_t> b(row_bounds, row_bounds + P + 1);
-  if (b[0] != 0 || b[P] != A->nbr) fail(QT_EINVAL, "row_bounds must span [0,%d]", A->nbr);
+  std::vector<int32_t> b(P + 1);
+  for (int q = 0; q <= P; ++q) {  // caller's block rows -> 32-rows
+    if (A->ubs == 16 && (row_bounds[q] & 1)) fail(QT_EINVAL, "block_size 16: row_bounds must be even");
+    b[q] = rows_to_internal(row_bounds[q], A->ubs);
+  }
+  if (b[0] != 0 || b[P] != A->nbr)
+    fail(QT_EINVAL, "row_bounds must span [0,%d]", rows_to_user(A->nbr, A->ubs));
   for (int q = 0; q < P; ++q)
     if (b[q + 1] < b[q]) fail(QT_EINVAL, "row_bounds not non-decreasing");
   qt_ctx ctx = A->ctx;
   QT_CUDA(cudaSetDevice(ctx->device));
-  check_upper(A);
+  if (A->ubs == 16) {
+    check_upper16(A);
+    if (!A->sym16) A->sym16.reset(symm_prepare16(A));
+  } else {
+    check_upper(A);
+  }
   qt_stats local;
   qt_stats& S = st ? *st : local;
   memset(&S, 0, sizeof(S));
   QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
-  qt_mat R = symm_square_virtual(A, b.data(), P, g, &S);
+  qt_mat R = symm_square_virtual(A->ubs == 16 ? A->sym16.get() : A, b.data(), P, g, &S);
   QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
   QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));

@@ -1008,19 +1008,21 @@ __global__ void k_sym_keep(const uint64_t* __restrict__ key, int64_t nb, int32_t
 // one warp per listed block: its key and values into the packed buffers
 __global__ void k_pack_sel(const int32_t* __restrict__ ids, int64_t n, const uint64_t* __restrict__ key,
                            const uint4* __restrict__ pool, int vpb, uint64_t* __restrict__ okey,
-                           uint4* __restrict__ opay) {
+                           uint4* __restrict__ opay, const uint8_t* __restrict__ sub, uint8_t* __restrict__ omask) {
   const int lane = threadIdx.x & 31;
   const int64_t w = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
   if (w >= n) return;
   const int32_t id = ids[w];
   if (lane == 0) okey[w] = key[id];
+  if (lane == 0 && sub) omask[w] = sub[id];
   const uint4* sp = pool + (int64_t)id * vpb;
   uint4* dp = opay + w * vpb;
   for (int e = lane; e < vpb; e += 32) dp[e] = sp[e];
 }
 
-// U_ext = U's local blocks + nr received blocks (keys, values): one pool
-qt_mat make_u_ext(qt_mat U, int64_t nr, const uint64_t* rkeys, const void* rpay) {
+// U_ext = U's local blocks + nr received blocks (keys, values, block size
+// 16: quadrant masks): one pool
+qt_mat make_u_ext(qt_mat U, int64_t nr, const uint64_t* rkeys, const void* rpay, const uint8_t* rmask) {
   qt_ctx ctx = U->ctx;
   cudaStream_t st = ctx->stream;
   const size_t bb = 1024 * elem_size(U->dtype);
@@ -1044,6 +1046,11 @@ qt_mat make_u_ext(qt_mat U, int64_t nr, const uint64_t* rkeys, const void* rpay)
     if (nl > 0) QT_CUDA(cudaMemcpyAsync(X->pool.p, U->pool_ptr(), bb * nl, cudaMemcpyDeviceToDevice, st));
     if (nr > 0)
       QT_CUDA(cudaMemcpyAsync((char*)X->pool.p + bb * nl, rpay, bb * nr, cudaMemcpyDeviceToDevice, st));
+    if (U->ubs == 16) {  // (masks indexed like the pool)
+      X->sub.alloc(nt, st);
+      if (nl > 0) QT_CUDA(cudaMemcpyAsync(X->sub.p, U->sub.p, nl, cudaMemcpyDeviceToDevice, st));
+      if (nr > 0) QT_CUDA(cudaMemcpyAsync(X->sub.as<uint8_t>() + nl, rmask, nr, cudaMemcpyDeviceToDevice, st));
+    }
     build_levels(X, sids.as<int32_t>());
   } catch (...) {
     delete X;
@@ -1156,11 +1163,14 @@ qt_mat symm_square_dist(qt_mat U, qt_stats* S) {
   const int64_t n_out = out_off[P], n_in = in_off[P];
   DevBuf okey(8 * std::max<int64_t>(n_out, 1), st), opay(bb * std::max<int64_t>(n_out, 1), st);
   DevBuf ikey(8 * std::max<int64_t>(n_in, 1), st), ipay(bb * std::max<int64_t>(n_in, 1), st);
+  const bool m16 = U->ubs == 16;  // block size 16: one quadrant-mask byte per block travels too
+  DevBuf omask(m16 ? std::max<int64_t>(n_out, 1) : 0, st), imask(m16 ? std::max<int64_t>(n_in, 1) : 0, st);
   for (int q = 0; q < P; ++q) {
     if (q == g || out_cnt[q] == 0) continue;
     k_pack_sel<<<(unsigned)((out_cnt[q] + 7) / 8), 256, 0, st>>>(
         sel[q].as<int32_t>(), out_cnt[q], U->key.as<uint64_t>(), static_cast<const uint4*>(U->pool_ptr()), vpb,
-        okey.as<uint64_t>() + out_off[q], opay.as<uint4>() + out_off[q] * vpb);
+        okey.as<uint64_t>() + out_off[q], opay.as<uint4>() + out_off[q] * vpb,
+        m16 ? U->sub.as<uint8_t>() : nullptr, m16 ? omask.as<uint8_t>() + out_off[q] : nullptr);
     QT_LAUNCH_CHECK(ctx);
   }
   X->group_start();
@@ -1169,22 +1179,24 @@ qt_mat symm_square_dist(qt_mat U, qt_stats* S) {
     if (out_cnt[q] > 0) {
       X->send(okey.as<uint64_t>() + out_off[q], 8ll * out_cnt[q], q);
       X->send((char*)opay.p + bb * out_off[q], bb * out_cnt[q], q);
+      if (m16) X->send(omask.as<uint8_t>() + out_off[q], out_cnt[q], q);
     }
     if (in_cnt[q] > 0) {
       X->recv(ikey.as<uint64_t>() + in_off[q], 8ll * in_cnt[q], q);
       X->recv((char*)ipay.p + bb * in_off[q], bb * in_cnt[q], q);
+      if (m16) X->recv(imask.as<uint8_t>() + in_off[q], in_cnt[q], q);
     }
   }
   X->group_end();
-  qt_mat Ux = make_u_ext(U, n_in, ikey.as<uint64_t>(), ipay.p);
+  qt_mat Ux = make_u_ext(U, n_in, ikey.as<uint64_t>(), ipay.p, m16 ? imask.as<uint8_t>() : nullptr);
   QT_CUDA(cudaEventRecord(ctx->ev[6], st));
   int64_t lists_in = 0;
   for (int q = 0; q < g; ++q) lists_in += nr_all[q];
   S->blocks_recv = n_in;
   S->bytes_recv_payload = n_in * (int64_t)bb;
-  S->bytes_recv_meta = 8 * n_in + 4ll * (P - 1) + 4 * lists_in;
+  S->bytes_recv_meta = 8 * n_in + 4ll * (P - 1) + 4 * lists_in + (m16 ? n_in : 0);
   S->bytes_sent_payload = n_out * (int64_t)bb;
-  S->bytes_sent_meta = 8 * n_out + 4ll * (P - 1) + 4 * nreq * (P - 1 - g);
+  S->bytes_sent_meta = 8 * n_out + 4ll * (P - 1) + 4 * nreq * (P - 1 - g) + (m16 ? n_out : 0);
   qt_mat C;
   try {
     C = symm_finish(Ux, lo, hi, S);
@@ -1230,7 +1242,7 @@ qt_mat symm_square_virtual(qt_mat U, const int32_t* bounds, int P, int g, qt_sta
     const int64_t n_in = Ux->nb - Ul->nb;
     S->blocks_recv = n_in;
     S->bytes_recv_payload = n_in * (int64_t)bb;
-    S->bytes_recv_meta = 8 * n_in + 4ll * (P - 1) + 4 * lists_in;
+    S->bytes_recv_meta = 8 * n_in + 4ll * (P - 1) + 4 * lists_in + (U->ubs == 16 ? n_in : 0);  // (+ mask bytes)
     S->bytes_sent_meta = 4 * nreq * (P - 1 - g);
     C = symm_finish(Ux, lo, hi, S);
     QT_CUDA(cudaEventElapsedTime(&S->ms_exchange, ctx->ev[5], ctx->ev[6]));

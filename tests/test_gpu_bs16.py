@@ -306,9 +306,72 @@ def test_bs16_symm_square_matches_full_multiply(qt, ctx):
     assert ss.block_products < 0.6 * sf.block_products
 
 
-def test_bs16_symm_square_multi_rank_rejected(qt, ctx):
-    rng = np.random.default_rng(1778)
-    Um = random_upper16(rng, 8, 0.5, "int", 64)
+def _containers(M):
+    k = np.unique(np.stack([M.brow // 2, M.bcol // 2], 1), axis=0)
+    return k[:, 0], k[:, 1]
+
+
+@pytest.mark.parametrize("P,bounds", [(2, [0, 16, 40]), (3, [0, 6, 22, 40]), (4, [0, 0, 10, 30, 40])])
+def test_bs16_symm_square_virtual_ranks(qt, ctx, P, bounds):
+    """Rank g of the P-rank symmetric square at block size 16 (C-26 at
+    container granularity, C-28): its rows equal the single-rank result's,
+    bitwise; the containers received are oracle.exchange_plan_symm's on the
+    container pattern (8 KiB each) plus one mask byte per container."""
+    rng = np.random.default_rng(1790 + P)
+    Um = random_upper16(rng, 40, 0.15, "uniform", 128)
+    U = mk(qt, ctx, Um)
+    full = U.symm_square()[0].to_blocks()
+    plan = oracle.exchange_plan_symm([b // 2 for b in bounds], _containers(Um), 8192)
+    for g in range(P):
+        Cg, st = U.symm_square_virtual(P, g, bounds)
+        r, c, v = Cg.to_blocks()
+        m = (full[0] >= bounds[g]) & (full[0] < bounds[g + 1])
+        assert np.array_equal(r, full[0][m]) and np.array_equal(c, full[1][m]) and np.array_equal(v, full[2][m])
+        assert st.bytes_recv_payload == plan[g]["payload_bytes"]
+        assert st.bytes_recv_meta == plan[g]["meta_bytes"] + plan[g]["blocks_received"]
     with pytest.raises(qt.QtError) as e:
-        mk(qt, ctx, Um).symm_square_virtual(2, 0, [0, 4, 8])
-    assert e.value.name == "QT_EBS"
+        U.symm_square_virtual(2, 0, [0, 15, 40])
+    assert e.value.name == "QT_EINVAL"
+
+
+def test_bs16_symm_square_loopback_two_ranks(qt, ctx):
+    import threading
+    import torch
+    rng = np.random.default_rng(1795)
+    Um = random_upper16(rng, 48, 0.12, "int", 128)
+    full = mk(qt, ctx, Um).symm_square()[0].to_blocks()
+    bounds = [0, 20, 48]
+    plan = oracle.exchange_plan_symm([b // 2 for b in bounds], _containers(Um), 8192)
+    hub = qt.LoopbackHub(2)
+    out, errs = [None] * 2, []
+
+    def rank_fn(g):
+        try:
+            torch.cuda.set_device(0)
+            c = qt.Context(0, stream=torch.cuda.Stream(), loopback=(hub, g, 2))
+            m = (Um.brow >= bounds[g]) & (Um.brow < bounds[g + 1])
+            A = qt.Matrix.from_blocks(c, Um.n, Um.leaf_dim, 16, Um.brow[m], Um.bcol[m], Um.vals[m],
+                                      row_bounds=bounds)
+            C, st = A.symm_square()
+            out[g] = (C.to_blocks(), st.bytes_recv_payload, st.bytes_recv_meta)
+            C.close()
+            A.close()
+            c.close()
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=rank_fn, args=(g,)) for g in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    hub.close()
+    assert not errs, errs
+    ref = oracle.symm_square(48, 16, tup(Um))
+    assert np.array_equal(full[0], ref[0]) and np.array_equal(full[2], ref[2])
+    for g in range(2):
+        (r, c, v), pay, meta = out[g]
+        m = (full[0] >= bounds[g]) & (full[0] < bounds[g + 1])
+        assert np.array_equal(r, full[0][m]) and np.array_equal(c, full[1][m]) and np.array_equal(v, full[2][m])
+        assert pay == plan[g]["payload_bytes"]
+        assert meta == plan[g]["meta_bytes"] + plan[g]["blocks_received"]
