@@ -128,7 +128,17 @@ def test_fuzz_symm16(qt, ctx, seed):
     p = float(rng.choice([0.0, 0.05, 0.2, 0.6, 1.0]))
     leaf = 32 * int(2 ** rng.integers(0, 4))
     U = rand_int_bm(rng, nbr, p, 16, leaf, dtype, upper=True)
-    same(mk(qt, ctx, U).symm_square()[0].to_blocks(), oracle.symm_square(nbr, 16, t64(U)))
+    Au = mk(qt, ctx, U)
+    ref = oracle.symm_square(nbr, 16, t64(U))
+    same(Au.symm_square()[0].to_blocks(), ref)
+    P = int(rng.integers(2, 5))
+    cuts = np.sort(rng.choice(np.arange(0, nbr // 2 + 1), size=P - 1)) * 2
+    bounds = [0, *cuts.tolist(), nbr]
+    for g in range(P):      # virtual ranks: rank g's rows of the same C
+        r, c, v = Au.symm_square_virtual(P, g, bounds)[0].to_blocks()
+        m = (ref[0] >= bounds[g]) & (ref[0] < bounds[g + 1])
+        assert np.array_equal(r, ref[0][m]) and np.array_equal(c, ref[1][m])
+        assert np.array_equal(v.astype(np.float64), ref[2][m])
 
 
 @pytest.mark.parametrize("seed", range(N_MISC))
