@@ -2,19 +2,24 @@
 """Benchmark: effective FP64 GFLOP/s of C = A*A (block-sparse quadtree multiply)
 at N GPUs, plus bytes received per GPU (BASELINE.json metric).
 
-Workload:
-  N = 1  : BASELINE config 2 — banded N=16384, a_ij != 0 iff |i-j| <= 1024,
-           uniform[-1,1], leaf 1024, block 32, C = A*A (FP64).
-  N > 1  : BASELINE config 5 — weak-scaling banded N = 16384*P, bandwidth 1024,
-           leaf 2048, block 32; rank g generates and owns block rows
-           [512g, 512(g+1)) (counter-based generator: no data moves to set up).
+Workload: BASELINE config 5 at every N — the weak-scaling
+banded matrix N = 16384*P, a_ij != 0 iff |i-j| <= 1024, uniform[-1,1], leaf
+2048, block 32, C = A*A (FP64), P = N; rank g generates and owns block rows
+[512g, 512(g+1)) (counter-based generator: no data moves to set up).  N = 1
+is the same matrix as config 2 (which has leaf 1024; it is reported as the
+extra key "cfg2").  1/2/4/8 GPUs are therefore one weak-scaling series.
 A step = one qt_multiply (symbolic BFS + [exchange] + numeric kernel) on
 device-resident inputs.  value = total nonzero block products * 2*32^3 /
 max-over-ranks device time.  Inputs (A 264 MB + C 507 MB per GPU) exceed the
 126 MB L2, so no explicit flush is done between steps.
 
+Launch: `python bench.py --gpus N` with N > 1 and no torchrun environment
+re-launches itself under torch.distributed.run (one rank per GPU, NCCL);
+under torchrun WORLD_SIZE must equal --gpus (exit 2 otherwise).
+
 `--impl reference` times the oracle (plain CPU block-CSR multiply, the
 reference arm of this tier) on a bounded sample of the same workload.
+`--dry-run` exercises the launcher and the rank plumbing (gloo, no GPU).
 """
 from __future__ import annotations
 
@@ -52,7 +57,30 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
     ap.add_argument("--no-symm", action="store_true")
+    ap.add_argument("--no-cfg2", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher + rank plumbing only (gloo, CPU): no GPU work, value null")
     return ap.parse_args()
+
+
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: run N ranks of this script
+    under torch.distributed.run (one process per GPU, rendezvous on
+    127.0.0.1); rank 0 prints the JSON line.  Returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
 
 
 def dist_env():
@@ -63,14 +91,21 @@ def dist_env():
 
 
 def workload(P: int, rank: int):
-    """Inputs of this rank: (config dict, description)."""
-    if P == 1:
-        c = qtgen.config(2)
-        desc = "cfg2 banded C=A*A N=16384 d=1024 (bandwidth 2049) leaf 1024 bs 32 FP64"
-    else:
-        c = qtgen.config(5, P=P, rank=rank)
-        desc = f"cfg5 weak-scaling banded C=A*A N=16384*{P} d=1024 leaf 2048 bs 32 FP64, row strips"
+    """Inputs of this rank: (config dict, description).  Config 5 at every P
+    (P = 1 is config 2's matrix with leaf 2048)."""
+    c = qtgen.config(5, P=P, rank=rank)
+    desc = (f"cfg5 weak-scaling banded C=A*A N=16384*{P} d=1024 (bandwidth 2049) leaf 2048 bs 32 FP64"
+            + (", row strips" if P > 1 else ""))
     return c, desc
+
+
+def oracle_workload(P: int):
+    """The rows the cpu_baseline / reference legs sample: rank 0's strip of
+    config 5 (plus the B rows its products read), i.e. the same matrix rows
+    rank 0 multiplies."""
+    if P == 1:
+        return qtgen.config(5, P=1, rank=0)
+    return qtgen.config(5, P=P, rows=(0, 512 + 32))
 
 
 def aggregate(dist, vals, device, world: int):
@@ -147,8 +182,10 @@ class ClockSampler:
 # ----------------------------------------------------------------- oracle legs
 
 
-def oracle_sample(c: dict, target_s: float = 12.0, max_rows: int | None = None):
-    """Time the oracle (as it stands) on block rows of the same workload.
+def oracle_sample(c: dict, target_s: float = 12.0, row_cap: int | None = None):
+    """Time the oracle (as it stands) on block rows of the same workload,
+    starting in the middle of the generated rows and never past `row_cap`
+    (rows whose products read B rows that were not generated).
     Returns (GFLOP/s, threads, description, seconds)."""
     import oracle
     A = c["A"]
@@ -161,8 +198,9 @@ def oracle_sample(c: dict, target_s: float = 12.0, max_rows: int | None = None):
     a = (A.brow, A.bcol, A.vals)
     b = (Bm.brow, Bm.bcol, Bm.vals)
     lo = int(A.brow.min()) if A.nb else 0
-    mid = lo + (int(A.brow.max()) - lo) // 2 if A.nb else 0
-    rows = max(nt, 4)
+    hi = min(int(A.brow.max()) + 1 if A.nb else 0, row_cap if row_cap is not None else nbr)
+    mid = lo + (hi - 1 - lo) // 2 if A.nb else 0
+    rows = max(1, min(max(nt, 4), hi - mid))
     t0 = time.perf_counter()
     oracle.spgemm(nbr, BS, a, b, nthreads=nt, rows=(mid, mid + rows))
     dt = time.perf_counter() - t0
@@ -170,7 +208,7 @@ def oracle_sample(c: dict, target_s: float = 12.0, max_rows: int | None = None):
     want = int(target_s * rate)
     r1 = mid
     acc = 0
-    while r1 < nbr and acc < want and (max_rows is None or r1 - mid < max_rows):
+    while r1 < hi and acc < want:
         acc += prod_row[r1]
         r1 += 1
     r1 = max(r1, mid + 1)
@@ -195,22 +233,26 @@ def cpu_info():
     return {"cpu_model": model, "nproc": os.cpu_count(), "oracle_flags": "gcc -O2 -ffp-contract=off, pthreads"}
 
 
+def oracle_cap(P: int):
+    """Last block row (exclusive) the oracle may sample from oracle_workload(P):
+    at P > 1 the rows generated beyond rank 0's strip only serve as B rows."""
+    return None if P == 1 else 512
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
     P = args.gpus
-    if P == 1:
-        c, desc = workload(1, 0)
-    else:  # rank 0's strip plus its halo rows (the sample stays inside the strip)
-        c = qtgen.config(5, P=P, rows=(0, 512 + 32))
-        desc = f"cfg5 weak-scaling banded N=16384*{P} d=1024 leaf 2048 bs 32 FP64 (rank 0's rows)"
+    c = oracle_workload(P)
+    desc = (workload(1, 0)[1] if P == 1 else
+            f"cfg5 weak-scaling banded C=A*A N=16384*{P} d=1024 leaf 2048 bs 32 FP64 (rank 0's rows)")
     per_step_s = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     times, rates = [], []
     nt = 1
     sample = ""
     for i in range(args.warmup + args.steps):
-        gf, nt, sample, dt = oracle_sample(c, target_s=per_step_s)
+        gf, nt, sample, dt = oracle_sample(c, target_s=per_step_s, row_cap=oracle_cap(P))
         if i >= args.warmup:
             rates.append(gf)
             times.append(dt)
@@ -231,26 +273,82 @@ def run_reference(args):
 # ----------------------------------------------------------------- product leg
 
 
+def dry_run(args, rank: int, world: int):
+    """Launcher and rank plumbing without a GPU (CPU test of the N > 1 path):
+    gloo process group, this rank's workload strip, the max/sum aggregation
+    and the JSON line shape; value is null (nothing is multiplied)."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    c, desc = workload(world, rank)
+    Am = c["A"]
+    bounds = row_bounds(Am.nbr, world)
+    allv = aggregate(dist, [float(rank), float(Am.nb), float(Am.brow.min()), float(Am.brow.max())],
+                     "cpu", world)
+    if rank == 0:
+        line = {"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "dry_run": True,
+                "config": {"workload": desc, "row_bounds": bounds,
+                           "blocks_per_rank": [int(x) for x in allv[:, 1]],
+                           "rows_per_rank": [[int(x), int(y)] for x, y in allv[:, 2:4]]},
+                "ranks_seen": [int(x) for x in allv[:, 0]]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def timed_steps(stream, step, steps, barrier):
+    """K steps between a barrier + synchronize on both sides; CUDA events on
+    the library's stream.  Returns (ms per step, [qt_stats])."""
+    import torch
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    stats = []
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(steps):
+        stats.append(step())
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    return ev0.elapsed_time(ev1) / steps, stats
+
+
 def main():
     args = parse()
+    rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        sys.exit(relaunch(args))
     if args.impl == "reference":
         run_reference(args)
+        return
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: one rank per GPU is required\n")
+        sys.exit(2)
+    if args.dry_run:
+        dry_run(args, rank, world)
         return
     import torch
     import torch.distributed as dist
 
-    rank, world, local = dist_env()
     P = world
+    if torch.cuda.device_count() < (local + 1):
+        sys.stderr.write(f"bench.py: rank {rank} needs cuda:{local}, {torch.cuda.device_count()} visible\n")
+        sys.exit(2)
+    torch.cuda.set_device(local)
     if world > 1:
-        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
     from paper_1501_07800_b200 import qtmm
 
     stream = torch.cuda.Stream(dev)
     ctx = qtmm.Context(dev, stream=stream)
+    cinfo = ctx.info()
+    if cinfo["comm_ranks"] != P:
+        sys.stderr.write(f"bench.py: the library communicator has {cinfo['comm_ranks']} ranks, expected {P}\n")
+        sys.exit(2)
     c, desc = workload(P, rank)
     Am = c["A"]
     bounds = row_bounds(Am.nbr, P) if P > 1 else None
@@ -271,42 +369,34 @@ def main():
     # FP64 peak for the roofline denominator (MEASURED_PEAKS.json has no FP64 entry)
     # (the best of three 100 ms runs: a single run varies by ~1.5 %)
     peak_dmma = max(ctx.fp64_peak("dmma", 100.0) for _ in range(3))
-    barrier()
-    torch.cuda.synchronize()
     sampler = ClockSampler(dev)
     sampler.start()
     l0 = ctx.kernel_launches
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    stats = []
-    barrier()
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        stats.append(step())
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    ms, stats = timed_steps(stream, step, args.steps, barrier)
     clocks = sampler.stop()
     launches = ctx.kernel_launches - l0
-    ms = ev0.elapsed_time(ev1) / args.steps
     products = stats[-1].block_products
     ms_num = statistics.mean(s.ms_numeric for s in stats)
     ms_sym = statistics.mean(s.ms_symbolic for s in stats)
     ms_exch = statistics.mean(s.ms_exchange for s in stats)
+    ms_pay = statistics.mean(s.ms_payload for s in stats)
     recv = stats[-1].bytes_recv_payload
     recv_meta = stats[-1].bytes_recv_meta
-    allv = aggregate(dist, [ms, float(products), float(recv), float(recv_meta), float(launches)],
-                     "cuda", world)
+    allv = aggregate(dist, [ms, float(products), float(recv), float(recv_meta), float(launches), ms_num,
+                            float(stats[-1].blocks_recv), ms_exch, ms_pay], "cuda", world)
     ms_max = float(allv[:, 0].max())
     total_products = float(allv[:, 1].sum())
     recv_all = allv[:, 2]
+    meta_all = allv[:, 3]
     launches_total = int(allv[:, 4].sum())
     value = total_products * FLOP_PER_PRODUCT / (ms_max * 1e-3) / 1e9
     # dominant kernel: the numeric kernel, timed with events on its stream (qt_stats)
     flops_launch = products * FLOP_PER_PRODUCT
     achieved = flops_launch / (ms_num * 1e-3) / 1e12
 
+    cfg2 = None
+    if P == 1 and not args.no_cfg2:
+        cfg2 = measure_cfg2(qtmm, ctx, stream, args)
     symm = None
     if P == 1 and not args.no_symm:
         symm = measure_symm(qtmm, ctx, stream, args)
@@ -319,14 +409,16 @@ def main():
     if not args.no_e2e:
         e2e = measure_e2e(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier)
     cpu = None
-    if rank == 0 and P == 1 and not args.no_cpu_baseline:
-        gf, nt, sample, _ = oracle_sample(c, target_s=12.0)
-        cpu = {"value": round(gf, 3), "unit": UNIT, "cores": nt, "kind": "oracle", "sample": sample, **cpu_info()}
+    if rank == 0 and not args.no_cpu_baseline:
+        gf, nt, sample, _ = oracle_sample(oracle_workload(P), target_s=12.0, row_cap=oracle_cap(P))
+        cpu = {"value": round(gf, 3), "unit": UNIT, "cores": nt, "kind": "oracle",
+               "sample": sample + (" (rank 0's strip)" if P > 1 else ""), **cpu_info()}
 
     if rank == 0:
+        # SpSUMMA: 2 m k sqrt(p) elements per process with m = nonzeros per
+        # row (2d+1) and k = 16384 rows per process (the paper's weak-scaling setup)
         m_nnz_row = 2 * 1024 + 1
         k = 16384
-        spsumma = [2 * m_nnz_row * k * (p ** 0.5) * 8 for p in [P]]
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": P,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_max, 4),
@@ -334,8 +426,10 @@ def main():
             "data": "synthetic (qtgen counter-based generator, uniform[-1,1])",
             "config": {"workload": desc, "n": Am.n, "leaf_dim": Am.leaf_dim, "block": BS,
                        "global_block_products": int(total_products),
+                       "block_products_per_rank": [int(x) for x in allv[:, 1]],
                        "l2": "no flush: inputs larger than L2 (A 264 MB + C 507 MB per GPU > 126 MB)",
-                       "parallelism": f"row strips x{P}" if P > 1 else "single GPU"},
+                       "parallelism": f"row strips x{P} (NCCL, {cinfo['comm_ranks']}-rank communicator)"
+                       if P > 1 else "single GPU"},
             "roofline": {"bound": "tensor", "kernel": "k_numeric_f64 (DMMA m8n8k4 f64)",
                          "achieved": round(achieved, 3), "peak": round(peak_dmma / 1e12, 3),
                          "unit": "TFLOP/s", "frac": round(achieved / (peak_dmma / 1e12), 4),
@@ -344,16 +438,26 @@ def main():
                                         "MEASURED_PEAKS.json has no FP64 entry; nominal 37.2 TF "
                                         "= 148 SM x 64 FMA x 2 x 1.965 GHz",
                          "ms_numeric": round(ms_num, 4), "ms_symbolic": round(ms_sym, 4),
+                         "ms_numeric_per_rank": [round(float(x), 4) for x in allv[:, 5]],
                          "ms_call_median": round(statistics.median(s.ms_total for s in stats), 4),
                          "ms_call_min": round(min(s.ms_total for s in stats), 4),
                          "ms_exchange": round(ms_exch, 4),
-                         "ms_payload_overlapped": round(statistics.mean(s.ms_payload for s in stats), 4),
+                         "ms_exchange_max": round(float(allv[:, 7].max()), 4),
+                         "ms_payload_overlapped": round(ms_pay, 4),
+                         "ms_payload_max": round(float(allv[:, 8].max()), 4),
                          "tiles_overlapped_after": [int(stats[-1].tiles_overlapped), int(stats[-1].tiles_after)],
                          "numeric_share": round(ms_num / ms_max, 4)},
             "bytes_recv_per_gpu": {"max": int(recv_all.max()), "avg": float(recv_all.mean()),
-                                   "min": int(recv_all.min()), "unit": "bytes (FP64 payload)",
-                                   "spsumma_comparator": spsumma[0] if P > 1 else 0},
+                                   "min": int(recv_all.min()), "per_rank": [int(x) for x in recv_all],
+                                   "meta_max": int(meta_all.max()),
+                                   "blocks_recv_per_rank": [int(x) for x in allv[:, 6]],
+                                   "unit": "bytes (FP64 payload)",
+                                   "spsumma_comparator": 2 * m_nnz_row * k * (P ** 0.5) * 8,
+                                   "spsumma_note": "2mk*sqrt(p)*8 B per process (P:726-728), m=2049, k=16384; "
+                                                   "a formula, not measured (at P=1 nothing moves)"},
+            "nccl": cinfo,
             "cpu_baseline": cpu,
+            "cfg2": cfg2,
             "fp32_variant": fp32,
             "symm_square": symm,
             "e2e": e2e,
@@ -361,9 +465,34 @@ def main():
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
+    A.close()
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_cfg2(qtmm, ctx, stream, args):
+    """BASELINE config 2 (the N=1 matrix with leaf 1024 instead of 2048): the
+    same step timed on its own, reported beside the config-5 headline."""
+    c = qtgen.config(2)["A"]
+    A = qtmm.Matrix.from_blocks(ctx, c.n, c.leaf_dim, BS, c.brow, c.bcol, c.vals)
+
+    def step():
+        C, st = A.multiply(A)
+        C.close()
+        return st
+
+    for _ in range(3):
+        step()
+    ms, sts = timed_steps(stream, step, args.steps, lambda: None)
+    A.close()
+    prods = sts[-1].block_products
+    ms_num = statistics.mean(s.ms_numeric for s in sts)
+    return {"workload": "cfg2 banded C=A*A N=16384 d=1024 leaf 1024 bs 32 FP64",
+            "value": round(prods * FLOP_PER_PRODUCT / (ms * 1e-3) / 1e9, 2), "unit": UNIT,
+            "ms_per_step": round(ms, 4), "ms_numeric": round(ms_num, 4),
+            "ms_symbolic": round(statistics.mean(s.ms_symbolic for s in sts), 4),
+            "block_products": int(prods)}
 
 
 def measure_fp32(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier):
@@ -463,7 +592,7 @@ def traffic_from_profiles(P: int):
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get("cfg2" if P == 1 else "cfg5")
+        return d.get("cfg5_P1" if P == 1 else "cfg5_interior")
     except Exception:
         return None
 

@@ -98,6 +98,14 @@ qt_status qt_ctx_create(int device, void* cuda_stream, int rank, int world,
                         const void* nccl_unique_id, qt_ctx* out);
 qt_status qt_ctx_destroy(qt_ctx ctx);
 
+/* Describe a context: this process's rank, the world size it was created
+ * with, and the number of ranks of the communicator the library actually
+ * built (NCCL: ncclCommCount on the library's own communicator; loopback: the
+ * hub's rank count; 1 when world == 1), and the transport kind (0 none, 1
+ * NCCL, 2 loopback).  Any output pointer may be NULL.  Errors: QT_EINVAL,
+ * QT_ENCCL. */
+qt_status qt_ctx_info(qt_ctx ctx, int32_t* rank, int32_t* world, int32_t* comm_ranks, int32_t* transport);
+
 /* Write a fresh 128-byte ncclUniqueId into `out128` (loads NCCL on demand).
  * Errors: QT_ENCCL when libnccl.so.2 cannot be loaded. */
 qt_status qt_nccl_unique_id(void* out128);
@@ -112,15 +120,23 @@ qt_status qt_nccl_unique_id(void* out128);
  * device pointers; order of blocks is arbitrary.  Zero submatrices are never
  * stored: only the listed blocks exist, a listed all-zero block is
  * kept (reading C-2).
- * The quadtree is uniform: 2^L x 2^L blocks with 2^L >= max(4, ceil(n/bs)),
- * padded children are NIL (reading C-3); the leaf level is
- * L - log2(leaf_dim/bs) (leaves are block-sparse submatrices, §4.1).
- * Requirements: block_size 32 or 64 (the leaf block size; "16-64").
- * A 64x64 block is held internally as a 2x2 quad of 32x32 blocks — the
- * kernels' block size — so the quadtree simply continues one level below the
- * caller's blocks; statistics, read-back, truncation and info are reported in
- * the caller's blocks.  leaf_dim a power-of-two multiple of block_size,
- * n % block_size == 0 (reading C-4), nblocks >= 0 (0 gives the NIL matrix).
+ * The quadtree is uniform: 2^L x 2^L blocks with 2^L the smallest power of
+ * two >= ceil(n/bs) — the matrix is split "as far as possible" into a uniform
+ * block size per level — padded children are NIL (reading C-3);
+ * the leaf level is L - log2(leaf_dim/bs) clipped at 0 (leaves are
+ * block-sparse submatrices, §4.1).  (Internally the kernels need at least
+ * 4x4 32-blocks: smaller matrices get a chain of single-child levels above
+ * the root, which statistics and qt_level_nodes do not report.)
+ * Requirements: block_size 16, 32 or 64 (the leaf block size; P:378-379
+ * "16-64").  A 64x64 block is held internally as a 2x2 quad of 32x32 blocks —
+ * the kernels' block size — so the quadtree simply continues one level below
+ * the caller's blocks.  16x16 blocks are held as the quadrants of 32x32
+ * "containers" with a 4-bit occupancy mask (DESIGN reading C-27): n and
+ * leaf_dim must then be multiples of 32 and multi-rank row_bounds even.
+ * Statistics, read-back, truncation and info are reported in the caller's
+ * blocks.  leaf_dim a power-of-two multiple of max(block_size, 32),
+ * n % max(block_size, 32) == 0 (reading C-4), nblocks >= 0 (0 gives the NIL
+ * matrix).
  * Multi-rank (world > 1): collective; each rank passes the blocks of its own
  * block-row range.  `row_bounds` (host, world+1 non-decreasing block-row
  * boundaries, first 0 and last ceil(n/bs)) gives the ranges; NULL means equal

@@ -29,7 +29,7 @@ S:nnn = SPEC.md line; readings C-n are listed in DESIGN.md):
                   (A-node, B-node) pairs with both non-NIL at level l
                   (§5.1; C-19).  Levels run from the root (l=0) to the
                   block level, "merging the lowest levels".
-* ``tree_levels`` quadtree geometry: 2^L blocks per side, L >= 2 (C-3).
+* ``tree_levels`` quadtree geometry: 2^L blocks per side, 2^L >= block rows (C-3).
 * ``exchange_plan``     bytes each rank receives under block-row strips
                   (A-stationary) — the paper's "data received by each process"
                   (P:1153-1155); protocol in DESIGN.md §Multi-GPU.
@@ -239,12 +239,14 @@ def pattern_product(nbr: int, a_rc, b_rc):
 
 
 def tree_levels(n: int, bs: int, leaf_dim: int):
-    """(L, leaf_level): the quadtree covers 2^L x 2^L blocks with 2^L >= max(4,
-    ceil(n/bs)) (reading C-3: pad to a power of two, padded children are NIL);
-    level 0 is the root, level L the blocks, leaf level = L - log2(leaf/bs)
-    clipped at 0."""
+    """(L, leaf_level): the quadtree covers 2^L x 2^L blocks with 2^L the
+    smallest power of two >= ceil(n/bs) — the matrix is split "as far as
+    possible" into a uniform block size per level (reading C-3:
+    pad to a power of two, padded children are NIL).  Level 0 is the root,
+    level L the blocks, leaf level = L - log2(leaf/bs) clipped at 0.  A matrix
+    of a single block has L = 0 (the root is the block)."""
     nbr = -(-n // bs)
-    L = 2
+    L = 0
     while (1 << L) < nbr:
         L += 1
     per_leaf = leaf_dim // bs

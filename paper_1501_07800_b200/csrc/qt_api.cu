@@ -44,14 +44,62 @@ static qt_status handle_exception() {
   }
 }
 
+// Multi-rank validation: a check or preparation that may fail on some ranks
+// only (a block outside the rank's strip, a duplicate, a block below the
+// diagonal, out of memory) must not leave the other ranks blocked in the next
+// collective.  `local` runs on every rank; then one int64 allgather tells
+// every rank whether any rank failed, and all of them fail with the same
+// status (the failing rank keeps its own message).  `extra` (may be null) is
+// sent along: the caller's per-rank payload of the same allgather.
+template <class F>
+static void collective_check(qt_ctx ctx, F&& local, int64_t* extra = nullptr, int64_t* extra_all = nullptr) {
+  qt_status mine = QT_OK;
+  std::string msg;
+  try {
+    local();
+  } catch (const Error& e) {
+    mine = e.status;
+    msg = e.what();
+  } catch (const std::bad_alloc&) {
+    mine = QT_ENOMEM;
+    msg = "host allocation failed";
+  }
+  if (ctx->world > 1) {
+    int64_t send[2] = {(int64_t)mine, extra ? *extra : 0};
+    std::vector<int64_t> all(2 * ctx->world);
+    allgather_i64(ctx, send, all.data(), 2);
+    if (extra_all)
+      for (int g = 0; g < ctx->world; ++g) extra_all[g] = all[2 * g + 1];
+    if (mine == QT_OK)
+      for (int g = 0; g < ctx->world; ++g)
+        if (all[2 * g] != QT_OK)
+          fail((qt_status)all[2 * g], "rank %d failed (status %lld); see its qt_last_error()", g,
+               (long long)all[2 * g]);
+  }
+  if (mine != QT_OK) throw Error(mine, msg);
+}
+
 // ---------------------------------------------------------------- allocator
 
 namespace {
 struct StreamCache {
   std::unordered_map<size_t, std::vector<void*>> free;
 };
+// Free lists are per (device, stream): the legacy default stream has the same
+// handle (0) on every device, so the stream alone would let a block of one
+// device be handed to a context of another.
+struct CacheKey {
+  int dev;
+  cudaStream_t s;
+  bool operator==(const CacheKey& o) const { return dev == o.dev && s == o.s; }
+};
+struct CacheKeyHash {
+  size_t operator()(const CacheKey& k) const {
+    return std::hash<const void*>()(k.s) ^ (size_t(k.dev) * 0x9E3779B97F4A7C15ull);
+  }
+};
 std::mutex g_cache_mu;
-std::unordered_map<cudaStream_t, StreamCache> g_cache;
+std::unordered_map<CacheKey, StreamCache, CacheKeyHash> g_cache;
 
 size_t size_class(size_t b) {
   if (b <= 512) return 512;
@@ -64,22 +112,34 @@ size_t size_class(size_t b) {
   return (b + g - 1) / g * g;
 }
 
-void flush_all_caches() {
-  // called on out-of-memory: make sure no stream still uses a cached block
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+void flush_device_caches(int dev) {
+  // called on out-of-memory on `dev`: make sure no stream of that device still
+  // uses a cached block, then return that device's cached blocks
   cudaDeviceSynchronize();
-  for (auto& kv : g_cache)
-    for (auto& fv : kv.second.free)
+  for (auto it = g_cache.begin(); it != g_cache.end();) {
+    if (it->first.dev != dev) {
+      ++it;
+      continue;
+    }
+    for (auto& fv : it->second.free)
       for (void* q : fv.second) cudaFree(q);
-  g_cache.clear();
+    it = g_cache.erase(it);
+  }
 }
 }  // namespace
 
-void* cache_alloc(size_t bytes, cudaStream_t s, size_t* granted) {
+void* cache_alloc(size_t bytes, cudaStream_t s, int dev, size_t* granted) {
   const size_t c = size_class(bytes);
   *granted = c;
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    auto it = g_cache.find(s);
+    auto it = g_cache.find(CacheKey{dev, s});
     if (it != g_cache.end()) {
       auto f = it->second.free.find(c);
       if (f != it->second.free.end() && !f->second.empty()) {
@@ -94,7 +154,7 @@ void* cache_alloc(size_t bytes, cudaStream_t s, size_t* granted) {
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    flush_all_caches();
+    flush_device_caches(dev);
     e = cudaMalloc(&q, c);
   }
   if (e != cudaSuccess) {
@@ -104,19 +164,44 @@ void* cache_alloc(size_t bytes, cudaStream_t s, size_t* granted) {
   return q;
 }
 
-void cache_free(void* p, size_t granted, cudaStream_t s) {
+void cache_free(void* p, size_t granted, cudaStream_t s, int dev) {
   std::lock_guard<std::mutex> lk(g_cache_mu);
-  g_cache[s].free[granted].push_back(p);
+  g_cache[CacheKey{dev, s}].free[granted].push_back(p);
 }
 
-void cache_release_stream(cudaStream_t s) {
+void cache_release_stream(cudaStream_t s, int dev) {
   cudaStreamSynchronize(s);
   std::lock_guard<std::mutex> lk(g_cache_mu);
-  auto it = g_cache.find(s);
+  auto it = g_cache.find(CacheKey{dev, s});
   if (it == g_cache.end()) return;
   for (auto& fv : it->second.free)
     for (void* q : fv.second) cudaFree(q);
   g_cache.erase(it);
+}
+
+int cache_device() { return current_device(); }
+
+// Internal padding levels: the kernels need at least 4x4 32-blocks (the FP32
+// kernel tiles 4x4 blocks), so a matrix of fewer block rows gets a quadtree
+// of 2^L >= 4 blocks per side whose top levels are a chain of single nodes.
+// The paper's quadtree (split "as far as possible") starts at the
+// smallest 2^Lp >= the block rows; statistics and level counts are reported
+// in that geometry, i.e. without the `pad` chain levels above its root.
+static int pad_levels(const qt_mat_s* M) {
+  int lp = 0;
+  while ((1ll << lp) < M->nbr) ++lp;
+  return M->L - lp;
+}
+
+static void shift_levels(qt_stats& S, int pad) {
+  if (pad <= 0) return;
+  for (int l = 0; l + pad < QT_MAX_LEVELS; ++l) {
+    S.level_tasks[l] = S.level_tasks[l + pad];
+    S.level_c_nodes[l] = S.level_c_nodes[l + pad];
+  }
+  for (int l = QT_MAX_LEVELS - pad; l < QT_MAX_LEVELS; ++l) S.level_tasks[l] = S.level_c_nodes[l] = 0;
+  S.nlevels -= pad;
+  S.leaf_level = std::max(0, S.leaf_level - pad);
 }
 
 // statistics at the caller's block size: for 64-blocks the 32-block level is
@@ -124,16 +209,16 @@ void cache_release_stream(cudaStream_t s) {
 static void user_stats(qt_mat R, qt_stats& S) {
   if (R->ubs == 16) {  // levels and products at 16-block granularity were set by the multiply
     S.c_blocks = R->nb16;
-    return;
+  } else if (R->ubs == 64) {
+    const int L = R->L;
+    S.nlevels = L;  // levels 0 .. L-1
+    S.block_products = S.level_tasks[L - 1];
+    S.c_blocks = user_nblocks(R);
+    S.level_tasks[L] = 0;
+    S.level_c_nodes[L] = 0;
+    if (S.leaf_level > L - 1) S.leaf_level = L - 1;
   }
-  if (R->ubs != 64) return;
-  const int L = R->L;
-  S.nlevels = L;  // levels 0 .. L-1
-  S.block_products = S.level_tasks[L - 1];
-  S.c_blocks = user_nblocks(R);
-  S.level_tasks[L] = 0;
-  S.level_c_nodes[L] = 0;
-  if (S.leaf_level > L - 1) S.leaf_level = L - 1;
+  shift_levels(S, pad_levels(R));
 }
 
 static int ilog2(int64_t x) {
@@ -211,6 +296,18 @@ qt_status qt_ctx_create(int device, void* cuda_stream, int rank, int world,
   API_CATCH
 }
 
+qt_status qt_ctx_info(qt_ctx ctx, int32_t* rank, int32_t* world, int32_t* comm_ranks, int32_t* transport) {
+  API_TRY
+  if (!ctx) fail(QT_EINVAL, "NULL context");
+  int kind = 0;
+  const int n = transport_info(ctx, &kind);
+  if (rank) *rank = ctx->rank;
+  if (world) *world = ctx->world;
+  if (comm_ranks) *comm_ranks = n;
+  if (transport) *transport = kind;
+  API_CATCH
+}
+
 qt_status qt_loopback_hub_create(int32_t world, void** hub) {
   API_TRY
   if (!hub || world < 1) fail(QT_EINVAL, "bad arguments");
@@ -241,7 +338,7 @@ qt_status qt_ctx_destroy(qt_ctx ctx) {
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->h2d_stream) {
     cudaStreamSynchronize(ctx->h2d_stream);
-    cache_release_stream(ctx->h2d_stream);
+    cache_release_stream(ctx->h2d_stream, ctx->device);
     cudaStreamDestroy(ctx->h2d_stream);
     cudaEventDestroy(ctx->h2d_done);
   }
@@ -261,7 +358,7 @@ qt_status qt_ctx_destroy(qt_ctx ctx) {
     std::lock_guard<std::mutex> lk(g_ctx_mu);
     if (--g_stream_refs[ctx->stream] == 0) {
       g_stream_refs.erase(ctx->stream);
-      cache_release_stream(ctx->stream);
+      cache_release_stream(ctx->stream, ctx->device);
     }
   }
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -307,79 +404,84 @@ qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
     while ((1ll << L) < nbr) ++L;
     M->L = L;
     M->leaf_level = std::max(0, L - ilog2(leaf_dim / 32));
-    // block-row ownership
-    M->bounds.assign(ctx->world + 1, 0);
-    if (ctx->world == 1) {
-      M->bounds[1] = (int32_t)nbr;
-    } else if (row_bounds) {
-      for (int g = 0; g <= ctx->world; ++g) {
-        if (block_size == 16 && (row_bounds[g] & 1)) fail(QT_EINVAL, "block_size 16: row_bounds must be even");
-        M->bounds[g] = rows_to_internal(row_bounds[g], block_size);
-      }
-      if (M->bounds[0] != 0 || M->bounds[ctx->world] != nbr)
-        fail(QT_EINVAL, "row_bounds must start at 0 and end at %lld",
-             (long long)rows_to_user((int32_t)nbr, block_size));
-      for (int g = 0; g < ctx->world; ++g)
-        if (M->bounds[g + 1] < M->bounds[g]) fail(QT_EINVAL, "row_bounds not non-decreasing");
-    } else {
-      const int64_t nu = std::max<int64_t>(1, nbr / std::max(f, 1)),
-                    per = (nu + ctx->world - 1) / ctx->world;
-      for (int g = 0; g <= ctx->world; ++g)
-        M->bounds[g] = (int32_t)(std::min<int64_t>(nu, per * g) * std::max(f, 1));
-    }
-    M->row_lo = M->bounds[ctx->rank];
-    M->row_hi = M->bounds[ctx->rank + 1];
-    // inputs to the device (stream-ordered copies from host, pinned or pageable)
+    // every rank validates its own blocks; all ranks learn whether any failed
+    // (and each rank's block count) in one allgather, so a rank-local
+    // QT_ERANGE / QT_EDUP / QT_ENOMEM never leaves the others blocked
     cudaStream_t st = ctx->stream;
-    size_t es = elem_size(dtype);
-    DevBuf dr, dc, dv;
-    const int32_t* pr = brow;
-    const int32_t* pc = bcol;
-    const void* pv = values;
-    if (nblocks > 0) {
-      if (!is_device_ptr(brow)) {
-        dr.alloc(nblocks * 4, st);
-        QT_CUDA(cudaMemcpyAsync(dr.p, brow, nblocks * 4, cudaMemcpyHostToDevice, st));
-        pr = dr.as<int32_t>();
-      }
-      if (!is_device_ptr(bcol)) {
-        dc.alloc(nblocks * 4, st);
-        QT_CUDA(cudaMemcpyAsync(dc.p, bcol, nblocks * 4, cudaMemcpyHostToDevice, st));
-        pc = dc.as<int32_t>();
-      }
-      const size_t vb = (size_t)nblocks * block_size * block_size * es;
-      if (!is_device_ptr(values)) {
-        // the values (the bulk) come in on the context's H2D stream, into a
-        // staging buffer of that stream's cache: the copy can start while the
-        // context stream still runs earlier work (e.g. the previous
-        // qt_multiply_async); the build waits for it through an event
-        if (!ctx->h2d_stream) {
-          QT_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
-          QT_CUDA(cudaEventCreateWithFlags(&ctx->h2d_done, cudaEventDisableTiming));
+    int64_t mine_nb = 0;
+    std::vector<int64_t> all_nb(ctx->world, 0);
+    collective_check(ctx, [&] {
+      // block-row ownership
+      M->bounds.assign(ctx->world + 1, 0);
+      if (ctx->world == 1) {
+        M->bounds[1] = (int32_t)nbr;
+      } else if (row_bounds) {
+        for (int g = 0; g <= ctx->world; ++g) {
+          if (block_size == 16 && (row_bounds[g] & 1)) fail(QT_EINVAL, "block_size 16: row_bounds must be even");
+          M->bounds[g] = rows_to_internal(row_bounds[g], block_size);
         }
-        dv.alloc(vb, ctx->h2d_stream);
-        QT_CUDA(cudaMemcpyAsync(dv.p, values, vb, cudaMemcpyHostToDevice, ctx->h2d_stream));
-        QT_CUDA(cudaEventRecord(ctx->h2d_done, ctx->h2d_stream));
-        QT_CUDA(cudaStreamWaitEvent(st, ctx->h2d_done, 0));
-        pv = dv.p;
+        if (M->bounds[0] != 0 || M->bounds[ctx->world] != nbr)
+          fail(QT_EINVAL, "row_bounds must start at 0 and end at %lld",
+               (long long)rows_to_user((int32_t)nbr, block_size));
+        for (int g = 0; g < ctx->world; ++g)
+          if (M->bounds[g + 1] < M->bounds[g]) fail(QT_EINVAL, "row_bounds not non-decreasing");
+      } else {
+        const int64_t nu = std::max<int64_t>(1, nbr / std::max(f, 1)),
+                      per = (nu + ctx->world - 1) / ctx->world;
+        for (int g = 0; g <= ctx->world; ++g)
+          M->bounds[g] = (int32_t)(std::min<int64_t>(nu, per * g) * std::max(f, 1));
       }
-    }
-    if (block_size == 16) {
-      build_from_blocks16(M, nblocks, pr, pc, pv, 2 * M->row_lo, 2 * M->row_hi);
-    } else if (f == 2 && nblocks > 0) {
-      DevBuf sr, sc, sv;
-      split64(ctx, dtype, nblocks, pr, pc, pv, sr, sc, sv);
-      build_from_blocks(M, 4 * nblocks, sr.as<int32_t>(), sc.as<int32_t>(), sv.p, M->row_lo, M->row_hi);
-    } else {
-      build_from_blocks(M, nblocks, pr, pc, pv, M->row_lo, M->row_hi);
-    }
-    M->global_nb = user_nblocks(M);
+      M->row_lo = M->bounds[ctx->rank];
+      M->row_hi = M->bounds[ctx->rank + 1];
+      // inputs to the device (stream-ordered copies from host, pinned or pageable)
+        size_t es = elem_size(dtype);
+      DevBuf dr, dc, dv;
+      const int32_t* pr = brow;
+      const int32_t* pc = bcol;
+      const void* pv = values;
+      if (nblocks > 0) {
+        if (!is_device_ptr(brow)) {
+          dr.alloc(nblocks * 4, st);
+          QT_CUDA(cudaMemcpyAsync(dr.p, brow, nblocks * 4, cudaMemcpyHostToDevice, st));
+          pr = dr.as<int32_t>();
+        }
+        if (!is_device_ptr(bcol)) {
+          dc.alloc(nblocks * 4, st);
+          QT_CUDA(cudaMemcpyAsync(dc.p, bcol, nblocks * 4, cudaMemcpyHostToDevice, st));
+          pc = dc.as<int32_t>();
+        }
+        const size_t vb = (size_t)nblocks * block_size * block_size * es;
+        if (!is_device_ptr(values)) {
+          // the values (the bulk) come in on the context's H2D stream, into a
+          // staging buffer of that stream's cache: the copy can start while the
+          // context stream still runs earlier work (e.g. the previous
+          // qt_multiply_async); the build waits for it through an event
+          if (!ctx->h2d_stream) {
+            QT_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+            QT_CUDA(cudaEventCreateWithFlags(&ctx->h2d_done, cudaEventDisableTiming));
+          }
+          dv.alloc(vb, ctx->h2d_stream);
+          QT_CUDA(cudaMemcpyAsync(dv.p, values, vb, cudaMemcpyHostToDevice, ctx->h2d_stream));
+          QT_CUDA(cudaEventRecord(ctx->h2d_done, ctx->h2d_stream));
+          QT_CUDA(cudaStreamWaitEvent(st, ctx->h2d_done, 0));
+          pv = dv.p;
+        }
+      }
+      if (block_size == 16) {
+        build_from_blocks16(M, nblocks, pr, pc, pv, 2 * M->row_lo, 2 * M->row_hi);
+      } else if (f == 2 && nblocks > 0) {
+        DevBuf sr, sc, sv;
+        split64(ctx, dtype, nblocks, pr, pc, pv, sr, sc, sv);
+        build_from_blocks(M, 4 * nblocks, sr.as<int32_t>(), sc.as<int32_t>(), sv.p, M->row_lo, M->row_hi);
+      } else {
+        build_from_blocks(M, nblocks, pr, pc, pv, M->row_lo, M->row_hi);
+      }
+      mine_nb = user_nblocks(M);
+    }, &mine_nb, all_nb.data());
+    M->global_nb = mine_nb;
     if (ctx->world > 1) {
-      std::vector<int64_t> all(ctx->world);
-      int64_t mine = user_nblocks(M);
-      allgather_i64(ctx, &mine, all.data(), 1);
       M->global_nb = 0;
-      for (auto v : all) M->global_nb += v;
+      for (auto v : all_nb) M->global_nb += v;
     }
     QT_CUDA(cudaStreamSynchronize(st));
   } catch (...) {
@@ -608,6 +710,7 @@ qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_sta
   QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
   QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
   R->global_nb = user_nblocks(R);
+  user_stats(R, S);
   *C = R;
   API_CATCH
 }
@@ -619,11 +722,17 @@ qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
   qt_ctx ctx = A->ctx;
   QT_CUDA(cudaSetDevice(ctx->device));
   if (ctx->world > 1 && A->ubs == 64) fail(QT_EBS, "the multi-rank symmetric square needs block_size 16 or 32");
-  if (A->ubs == 16)
-    check_upper16(A);
-  else
-    check_upper(A);
-  ensure_levels(A);
+  // rank-local checks (a block below the diagonal in this rank's strip, out
+  // of memory preparing the completed copy) are agreed on by all ranks before
+  // the first exchange step
+  collective_check(ctx, [&] {
+    if (A->ubs == 16)
+      check_upper16(A);
+    else
+      check_upper(A);
+    ensure_levels(A);
+    if (ctx->world > 1 && A->ubs == 16 && !A->sym16) A->sym16.reset(symm_prepare16(A));
+  });
   qt_stats local;
   qt_stats& S = st ? *st : local;
   memset(&S, 0, sizeof(S));
@@ -710,8 +819,9 @@ qt_status qt_level_nodes(qt_mat A, int64_t* counts, int32_t cap, int32_t* nlevel
   QT_CUDA(cudaSetDevice(A->ctx->device));
   ensure_levels(A);
   const int top = A->ubs == 64 ? A->L - 1 : A->ubs == 16 ? A->L + 1 : A->L;  // the caller's block level
-  if (nlevels) *nlevels = top + 1;
-  for (int l = 0; l <= top && l < cap; ++l) counts[l] = l <= A->L ? A->cnt[l] : A->nb16;
+  const int pad = pad_levels(A);  // chain levels above the paper's root (not reported)
+  if (nlevels) *nlevels = top + 1 - pad;
+  for (int l = pad; l <= top && l - pad < cap; ++l) counts[l - pad] = l <= A->L ? A->cnt[l] : A->nb16;
   API_CATCH
 }
 

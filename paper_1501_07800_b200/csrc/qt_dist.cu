@@ -54,6 +54,7 @@ struct NcclApi {
   decltype(&ncclAllGather) AllGather = nullptr;
   decltype(&ncclAllReduce) AllReduce = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  decltype(&ncclCommCount) CommCount = nullptr;
 };
 
 static NcclApi& nccl() {
@@ -86,6 +87,7 @@ static NcclApi& nccl() {
   LOAD(AllGather)
   LOAD(AllReduce)
   LOAD(GetErrorString)
+  LOAD(CommCount)
 #undef LOAD
   api.ok = true;
   return api;
@@ -112,6 +114,9 @@ struct Transport {
   virtual void send(const void* buf, size_t bytes, int peer) = 0;
   virtual void recv(void* buf, size_t bytes, int peer) = 0;
   virtual void group_end() = 0;
+  // ranks of the underlying communicator (NCCL: ncclCommCount) and kind (1 NCCL, 2 loopback)
+  virtual int comm_size() = 0;
+  virtual int kind() const = 0;
   // stream the following send/recv groups are ordered on (null: the ctx stream)
   void set_stream(cudaStream_t s) { cur_ = s; }
   cudaStream_t cur(qt_ctx ctx) const { return cur_ ? cur_ : ctx->stream; }
@@ -149,6 +154,12 @@ struct NcclTransport : Transport {
     NCCL_CALL(nccl().Recv(buf, bytes, ncclInt8, peer, comm, cur(ctx)));
   }
   void group_end() override { NCCL_CALL(nccl().GroupEnd()); }
+  int comm_size() override {
+    int n = 0;
+    NCCL_CALL(nccl().CommCount(comm, &n));
+    return n;
+  }
+  int kind() const override { return 1; }
 };
 
 // Shared state of the loopback ranks (one per process, created by the caller).
@@ -177,6 +188,8 @@ struct LoopTransport : Transport {
   std::vector<std::shared_ptr<LoopHub::Msg>> posted;
   std::vector<std::tuple<void*, size_t, int>> pending;
   LoopTransport(qt_ctx c, LoopHub* h) : ctx(c), hub(h) {}
+  int comm_size() override { return hub->P; }
+  int kind() const override { return 2; }
   void allgather_i64(const int64_t* send_host, int64_t* recv_host, int count) override {
     std::unique_lock<std::mutex> lk(hub->mu);
     // wait until the previous allgather has been fully consumed
@@ -272,6 +285,15 @@ void dist_init_loopback(qt_ctx ctx, void* hub) {
 void dist_finalize(qt_ctx ctx) {
   delete T(ctx);
   ctx->transport = nullptr;
+}
+
+int transport_info(qt_ctx ctx, int* kind) {
+  if (!ctx->transport) {
+    *kind = 0;
+    return 1;
+  }
+  *kind = T(ctx)->kind();
+  return T(ctx)->comm_size();
 }
 
 void* loop_hub_create(int P) { return new LoopHub(P); }

@@ -51,20 +51,24 @@ struct Error : std::runtime_error {
 // misses call cudaMalloc, and on out-of-memory the caches are flushed and the
 // allocation retried.  In steady state (repeated multiplies) no CUDA allocator
 // call happens at all.
-void* cache_alloc(size_t bytes, cudaStream_t s, size_t* granted);
-void cache_free(void* p, size_t granted, cudaStream_t s);
-void cache_release_stream(cudaStream_t s);
+// Free lists are keyed by (device, stream); `dev` is the current device at
+// allocation time (every entry point sets its context's device first).
+void* cache_alloc(size_t bytes, cudaStream_t s, int dev, size_t* granted);
+void cache_free(void* p, size_t granted, cudaStream_t s, int dev);
+void cache_release_stream(cudaStream_t s, int dev);
+int cache_device();
 
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   size_t granted = 0;
   cudaStream_t s = nullptr;
+  int dev = 0;
   DevBuf() = default;
   DevBuf(size_t b, cudaStream_t st) { alloc(b, st); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), granted(o.granted), s(o.s) {
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), granted(o.granted), s(o.s), dev(o.dev) {
     o.p = nullptr;
     o.bytes = o.granted = 0;
   }
@@ -75,6 +79,7 @@ struct DevBuf {
       bytes = o.bytes;
       granted = o.granted;
       s = o.s;
+      dev = o.dev;
       o.p = nullptr;
       o.bytes = o.granted = 0;
     }
@@ -86,10 +91,11 @@ struct DevBuf {
     s = st;
     bytes = b;
     if (b == 0) return;
-    p = cache_alloc(b, st, &granted);
+    dev = cache_device();
+    p = cache_alloc(b, st, dev, &granted);
   }
   void release() {
-    if (p) cache_free(p, granted, s);
+    if (p) cache_free(p, granted, s, dev);
     p = nullptr;
     bytes = granted = 0;
   }
@@ -344,6 +350,8 @@ void* loop_hub_create(int P);
 void loop_hub_destroy(void* hub);
 void nccl_unique_id(void* out128);
 void dist_finalize(qt_ctx ctx);
+// ranks of the context's communicator; *kind = 0 none (world 1), 1 NCCL, 2 loopback
+int transport_info(qt_ctx ctx, int* kind);
 // tau >= 0: the norm-screened product (B_ext's norms from both of its pools)
 qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* st, double tau = -1.0);
 // the same path for virtual rank g of P on one device (D2D copies stand in for

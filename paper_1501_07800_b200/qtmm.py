@@ -67,6 +67,7 @@ def _load():
     sig = {
         "qt_ctx_create": [ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P, P],
         "qt_ctx_destroy": [P],
+        "qt_ctx_info": [P, P, P, P, P],
         "qt_nccl_unique_id": [P],
         "qt_create": [P, i64, i32, i32, ctypes.c_int, i64, P, P, P, P, P],
         "qt_multiply": [P, P, P, P],
@@ -107,7 +108,7 @@ def _load():
 
 
 _lib = _load()
-EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_nccl_unique_id", "qt_create", "qt_multiply",
+EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_ctx_info", "qt_nccl_unique_id", "qt_create", "qt_multiply",
             "qt_multiply_async",
             "qt_multiply_ex", "qt_symm_square", "qt_multiply_screened",
             "qt_multiply_virtual", "qt_symm_square_virtual", "qt_plan_strips", "qt_multiply_plan",
@@ -189,6 +190,13 @@ class Context:
     @property
     def kernel_launches(self) -> int:
         return int(_lib.qt_kernel_launches(self._h))
+
+    def info(self) -> dict:
+        """qt_ctx_info: rank, world, the library communicator's rank count and transport."""
+        r, w, n, t = (ctypes.c_int32() for _ in range(4))
+        _check(_lib.qt_ctx_info(self._h, ctypes.byref(r), ctypes.byref(w), ctypes.byref(n), ctypes.byref(t)))
+        return {"rank": r.value, "world": w.value, "comm_ranks": n.value,
+                "transport": {0: "none", 1: "nccl", 2: "loopback"}[t.value]}
 
     def synchronize(self):
         """Wait for all enqueued work, including qt_read_back_async copies."""

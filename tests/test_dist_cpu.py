@@ -203,3 +203,38 @@ def _protocol(rank, world, cfg_idx):
 def test_row_strip_protocol_gloo(world, cfg):
     res = _run(world, _protocol, cfg)
     assert len(res) == world
+
+
+# --------------------------------------------------------------------- bench launcher
+
+
+def _bench(*argv, env=None):
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    e.update(env or {})
+    return subprocess.run([sys.executable, os.path.join(root, "bench.py"), *argv], capture_output=True,
+                          text=True, env=e, timeout=240)
+
+
+def test_bench_relaunches_n_ranks_gloo_dry_run():
+    """`bench.py --gpus 2` with no torchrun environment launches 2 ranks itself
+    (torch.distributed.run, 127.0.0.1) and rank 0 prints one line with n_gpus 2
+    and both ranks' config-5 strips (dry run: gloo, no GPU)."""
+    import json
+    r = _bench("--gpus", "2", "--dry-run", "--steps", "2")
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["ranks_seen"] == [0, 1]
+    assert d["config"]["row_bounds"] == [0, 512, 1024]
+    assert d["config"]["rows_per_rank"] == [[0, 511], [512, 1023]]
+    # config 5 at P=2: both ranks are edge ranks with 512 rows and a 33-block half-band
+    assert d["config"]["blocks_per_rank"][0] == d["config"]["blocks_per_rank"][1] > 0
+
+
+def test_bench_rejects_world_mismatch():
+    r = _bench("--gpus", "2", "--dry-run", env={"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode == 2 and "WORLD_SIZE=1" in r.stderr

@@ -118,8 +118,11 @@ def test_fp32_cfg5_small_full_oracle(qt, ctx, kind):
     check(got, oracle.spgemm(Am.nbr, 32, ref64(Am), ref64(Am)), kind)
 
 
-def test_fp32_cfg5_full_size_sampled(qt, ctx):
-    c = qtgen.config(5, P=1)
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_fp32_cfg5_full_size_sampled(qt, ctx, kind):
+    """BASELINE config 5's FP32 variant at full size (P = 1): integer inputs
+    bit-exact (|partial sums| <= 33 280 < 2^24, pin P-12), uniform within 1e-5."""
+    c = qtgen.config(5, kind, P=1)
     Am = f32(c["A"])
     A = mk(qt, ctx, Am)
     C, st = A.multiply(A)
@@ -128,7 +131,26 @@ def test_fp32_cfg5_full_size_sampled(qt, ctx):
     for lo, hi in [(0, 6), (300, 306), (506, 512)]:
         ref = oracle.spgemm(Am.nbr, 32, ref64(Am), ref64(Am), rows=(lo, hi))
         m = (got[0] >= lo) & (got[0] < hi)
-        check((got[0][m], got[1][m], got[2][m]), ref, "uniform")
+        check((got[0][m], got[1][m], got[2][m]), ref, kind)
+
+
+def test_fp32_cfg5_virtual_rank_full_size_int(qt, ctx):
+    """FP32 config 5 at P = 4, interior rank 1 (virtual ranks): sampled rows
+    bit-exact against the oracle, bytes = the exchange plan at 4 KiB per block."""
+    P, g = 4, 1
+    lo, hi = 512 * g, 512 * (g + 1)
+    c = qtgen.config(5, "int", P=P, rows=(lo - 32, hi + 32))
+    Am = f32(c["A"])
+    A = mk(qt, ctx, Am)
+    bounds = [512 * q for q in range(P + 1)]
+    Cg, st = A.multiply_virtual(A, P, g, bounds)
+    plan = oracle.exchange_plan(bounds, (Am.brow, Am.bcol), (Am.brow, Am.bcol), 4096)[g]
+    assert st.bytes_recv_payload == plan["payload_bytes"]
+    got = Cg.to_blocks()
+    for rlo, rhi in ((lo, lo + 3), (hi - 3, hi)):
+        ref = oracle.spgemm(512 * P, 32, ref64(Am), ref64(Am), rows=(rlo, rhi))
+        m = (got[0] >= rlo) & (got[0] < rhi)
+        check((got[0][m], got[1][m], got[2][m]), ref, "int")
 
 
 def test_fp32_cfg4_small(qt, ctx):

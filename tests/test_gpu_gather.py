@@ -2,11 +2,13 @@
 (the NCCL code path with rank threads on one device).  Needs a B200.
 
 Each rank computes its block rows of C = A·A; the root gathers every rank's
-blocks and must hold exactly the single-rank product (bitwise: each C block
-is computed on one rank in the same k order)."""
+blocks and must hold exactly the oracle's product (integer-valued inputs:
+exact in every dtype, pin P-12) and the single-rank product (bitwise: each C
+block is computed on one rank in the same k order, pin P-10)."""
 import numpy as np
 import pytest
 
+import oracle
 import qtgen
 
 pytestmark = pytest.mark.gpu
@@ -38,6 +40,10 @@ def test_gather_equals_single_rank_product(qt, bs, dtype, P, root):
     ctx0 = qt.Context(0)
     A0 = qt.Matrix.from_blocks(ctx0, M.n, M.leaf_dim, bs, M.brow, M.bcol, M.vals)
     full = (A0 @ A0).to_blocks()
+    t = (M.brow, M.bcol, M.vals.astype(np.float64))
+    ref = oracle.spgemm(nbr, bs, t, t)
+    assert np.array_equal(full[0], ref[0]) and np.array_equal(full[1], ref[1])
+    assert np.array_equal(full[2].astype(np.float64), ref[2])
     step = (nbr // P) // 2 * 2
     bounds = [g * step for g in range(P)] + [nbr]
     hub = qt.LoopbackHub(P)
@@ -68,7 +74,9 @@ def test_gather_equals_single_rank_product(qt, bs, dtype, P, root):
         if g != root:
             assert out[g] is None
     r, c, v = out[root]
-    assert np.array_equal(r, full[0]) and np.array_equal(c, full[1]) and np.array_equal(v, full[2])
+    assert np.array_equal(r, ref[0]) and np.array_equal(c, ref[1])
+    assert np.array_equal(v.astype(np.float64), ref[2])                  # the oracle's product
+    assert np.array_equal(v, full[2])                                    # bitwise = single rank
 
 
 @pytest.mark.parametrize("P,frac", [(2, 0.0), (2, 0.5), (3, 1.0)])
@@ -90,6 +98,9 @@ def test_screened_multi_rank_loopback(qt, P, frac):
     if frac > 0:
         assert st_ref.block_products < full.block_products
     ref = ref.to_blocks()
+    t = (M.brow, M.bcol, M.vals)
+    orc = oracle.spgemm(nbr, 32, t, t, tau=tau)                          # integer inputs: exact
+    assert np.array_equal(ref[0], orc[0]) and np.array_equal(ref[1], orc[1]) and np.array_equal(ref[2], orc[2])
     bounds = [g * (nbr // P) for g in range(P)] + [nbr]
     hub = qt.LoopbackHub(P)
     out, errs = [None] * P, []

@@ -7,7 +7,8 @@ What is checked, on the virtual-rank path and on the loopback transport (the
 NCCL code path with rank threads on one device):
 * C is bitwise identical with the overlap on and off (each C tile is computed
   wholly in one of the two launches, in the same k order), and equal to the
-  rank's rows of the single-rank product;
+  rank's rows of the oracle's product (integer-valued inputs: exact in FP64
+  and FP32, pin P-12);
 * the tile split is the one the row-strip rule fixes: a tile (a C node at the
   numeric kernel's tile level: 2x2 blocks for FP64, 4x4 for FP32) runs behind
   the payload iff one of its tasks (A node, B_ext node) has a B_ext node that
@@ -70,10 +71,16 @@ def expected_tiles(M, bounds, g, s):
     return tiles, behind, int(remote.sum())
 
 
+def oracle_full(M):
+    """The oracle's C = M·M (double; the inputs are integers, so exact)."""
+    t = (M.brow, M.bcol, M.vals.astype(np.float64))
+    return oracle.spgemm(M.nbr, 32, t, t)
+
+
 def random_pattern(rng, nbr, p, leaf):
     mask = rng.random((nbr, nbr)) < p
     br, bc = np.nonzero(mask)
-    v = rng.uniform(-1, 1, size=(len(br), 32, 32))
+    v = rng.integers(-4, 5, size=(len(br), 32, 32)).astype(np.float64)
     return qtgen.BlockMatrix(nbr * 32, leaf, 32, br.astype(np.int32), bc.astype(np.int32), v)
 
 
@@ -87,9 +94,9 @@ GROUPED = {"random"}                             # FP64: one launch if the tile 
 
 def _matrix(case, P):
     if case == "cfg5":
-        return qtgen.config(5, P=P, small=True)["A"]
+        return qtgen.config(5, "int", P=P, small=True)["A"]
     if case == "cfg4":
-        return qtgen.config(4, small=True)["A"]
+        return qtgen.config(4, "int", small=True)["A"]
     return random_pattern(np.random.default_rng(5), 64, 0.08, 256)
 
 
@@ -110,7 +117,7 @@ def test_virtual_overlap_split_and_bitwise(qt, ctx, monkeypatch, case, P, spec, 
     bounds = _bounds(M, P, spec)
     s = 2 if dtype == "f64" else 4
     A = mk(qt, ctx, M)
-    full = (A @ A).to_blocks()
+    full = oracle_full(M)
     some_behind = 0
     for g in range(P):
         monkeypatch.setenv("QT_OVERLAP", "0")
@@ -138,11 +145,11 @@ def test_virtual_overlap_split_and_bitwise(qt, ctx, monkeypatch, case, P, spec, 
 def test_loopback_overlap(qt, ctx, monkeypatch, P, dtype):
     import threading
     import torch
-    M = qtgen.config(5, P=P, small=True)["A"]
+    M = qtgen.config(5, "int", P=P, small=True)["A"]
     if dtype == "f32":
         M = f32(M)
     s = 2 if dtype == "f64" else 4
-    full = (mk(qt, ctx, M) @ mk(qt, ctx, M)).to_blocks()
+    full = oracle_full(M)
     bounds = [g * (M.nbr // P) for g in range(P)] + [M.nbr]
     plan = oracle.exchange_plan(bounds, (M.brow, M.bcol), (M.brow, M.bcol), 8192 if dtype == "f64" else 4096)
     res = {}

@@ -174,7 +174,7 @@ def test_disjoint_k_gives_empty(qt, ctx):
                               np.ones((1, 32, 32)))
     C, st = A.multiply(B)
     assert C.nblocks == 0 and st.block_products == 0
-    assert C.level_nodes() == [0, 0, 0]
+    assert C.level_nodes() == [0, 0]  # 2x2 blocks: levels 0 (root) and 1 (blocks)
 
 
 def test_errors(qt, ctx):
@@ -285,14 +285,30 @@ def test_cfg2_banded_full_size_sampled(qt, ctx, kind):
     assert st.block_products == 2048800 and st.c_blocks == 61888
 
 
-def test_cfg3_random_full_size_sampled(qt, ctx):
-    c = qtgen.config(3)
-    _sampled_rows_check(qt, ctx, c, [(0, 16), (1000, 1024)], "uniform")
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_cfg3_random_full_size_sampled(qt, ctx, kind):
+    """Config 3 at full size: full pattern = the boolean product; sampled
+    block rows bit-exact (integer variant) / within the FP64 bar (uniform)."""
+    c = qtgen.config(3, kind)
+    _sampled_rows_check(qt, ctx, c, [(0, 16), (500, 520), (1000, 1024)], kind)
 
 
-def test_cfg4_eslike_full_size_sampled(qt, ctx):
-    c = qtgen.config(4)
-    _sampled_rows_check(qt, ctx, c, [(0, 4), (1500, 1504), (3068, 3072)], "uniform")
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_cfg4_eslike_full_size_sampled(qt, ctx, kind):
+    """Config 4 at full size (3072 atoms): full pattern and per-level task
+    counts vs the oracle; sampled atom rows bit-exact on integer values."""
+    c = qtgen.config(4, kind)
+    _sampled_rows_check(qt, ctx, c, [(0, 4), (1500, 1504), (3068, 3072)], kind)
+
+
+def test_cfg1_2_3_4_int_every_config_once(qt, ctx):
+    """The integer variants of configs 1-4 in one place (north star: bit-exact
+    on small-integer inputs for all five configs; config 5 is checked per
+    rank in test_virtual_ranks_cfg5_full_size_int_values)."""
+    for idx in (1, 2, 3, 4):
+        c = qtgen.config(idx, "int")
+        nbr = c["A"].nbr
+        _sampled_rows_check(qt, ctx, c, [(nbr // 2 - 2, nbr // 2 + 2)], "int")
 
 
 def test_cfg4_small_full_oracle(qt, ctx):
@@ -387,9 +403,15 @@ def _loopback_run(qt, P, c, bounds):
 
 @pytest.mark.parametrize("P", [2, 4])
 def test_loopback_ranks_nccl_path(qt, ctx, P):
-    c = qtgen.config(5, P=P, small=True)
+    """Rank threads on the loopback transport run the NCCL code path; each
+    rank's rows equal the oracle's (integer inputs: exact) and the
+    single-rank product's (bitwise, pin P-10)."""
+    c = qtgen.config(5, "int", P=P, small=True)
     Am = c["A"]
     full = (mk(qt, ctx, Am) @ mk(qt, ctx, Am)).to_blocks()
+    ref = oracle.spgemm(Am.nbr, 32, as_tuple(Am), as_tuple(Am))
+    assert_same_pattern(full, ref)
+    assert np.array_equal(full[2], ref[2])
     per = Am.nbr // P
     bounds = [g * per for g in range(P)] + [Am.nbr]
     plan = oracle.exchange_plan(bounds, (Am.brow, Am.bcol), (Am.brow, Am.bcol), 8192)
@@ -409,9 +431,9 @@ def test_loopback_ranks_nccl_path(qt, ctx, P):
 
 
 def test_loopback_cfg4_small_two_ranks(qt, ctx):
-    c = qtgen.config(4, small=True)
+    c = qtgen.config(4, "int", small=True)
     Am = c["A"]
-    full = (mk(qt, ctx, Am) @ mk(qt, ctx, Am)).to_blocks()
+    full = oracle.spgemm(Am.nbr, 32, as_tuple(Am), as_tuple(Am))
     bounds = [0, Am.nbr // 3, Am.nbr]   # uneven strips
     out = _loopback_run(qt, 2, c, bounds)
     for g in range(2):
@@ -460,6 +482,35 @@ def test_loopback_truncate_matches_single_rank(qt, ctx, P, tau):
     v = np.concatenate([o[0][2] for o in out])
     assert np.array_equal(r, ref[0]) and np.array_equal(c_, ref[1]) and np.array_equal(v, ref[2])
     assert all(o[1]["global_nblocks"] == len(ref[0]) for o in out)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_virtual_ranks_cfg5_full_size_int_values(qt, ctx, P):
+    """Config 5 at full size, integer variant, every rank of P = 2/4/8 (the
+    weak-scaling run): rank g's C rows are bit-exact against the oracle on
+    sampled block rows (its first, middle and last rows, which read the halo
+    received from both neighbours), and the bytes it receives equal the
+    oracle's exchange plan.  Each rank's strip is generated with its halo
+    rows only (the rows its products read)."""
+    nbr = 512 * P
+    bounds = [512 * q for q in range(P + 1)]
+    for g in range(P):
+        lo, hi = 512 * g, 512 * (g + 1)
+        c = qtgen.config(5, "int", P=P, rows=(max(0, lo - 32), min(nbr, hi + 32)))
+        Am = c["A"]
+        A = mk(qt, ctx, Am)
+        Cg, st = A.multiply_virtual(A, P, g, bounds)
+        plan = oracle.exchange_plan(bounds, (Am.brow, Am.bcol), (Am.brow, Am.bcol), 8192)[g]
+        assert st.bytes_recv_payload == plan["payload_bytes"]
+        got = Cg.to_blocks()
+        assert got[0].min() >= lo and got[0].max() < hi
+        for rlo, rhi in ((lo, lo + 3), (lo + 254, lo + 258), (hi - 3, hi)):
+            ref = oracle.spgemm(nbr, 32, as_tuple(Am), as_tuple(Am), rows=(rlo, rhi))
+            m = (got[0] >= rlo) & (got[0] < rhi)
+            assert_same_pattern((got[0][m], got[1][m]), ref)
+            assert np.array_equal(got[2][m], ref[2])
+        A.close()
+        Cg.close()
 
 
 @pytest.mark.parametrize("P,g,expect", [(2, 0, 17039360), (4, 1, 34078720), (8, 5, 34078720)])

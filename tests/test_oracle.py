@@ -207,8 +207,18 @@ def test_tree_levels_configs():
     assert oracle.tree_levels(32768, 32, 2048) == (10, 4)    # cfg3
     assert oracle.tree_levels(98304, 32, 4096) == (12, 5)    # cfg4 (padded to 4096 blocks)
     assert oracle.tree_levels(4, 1, 2) == (2, 1)
-    assert oracle.tree_levels(32, 32, 32) == (2, 2)          # single block: padded to 4x4 (L >= 2)
+    assert oracle.tree_levels(32, 32, 32) == (0, 0)          # single block: the root is the block
+    assert oracle.tree_levels(64, 32, 32) == (1, 1)          # 2x2 blocks
+    assert oracle.tree_levels(96, 32, 64) == (2, 1)          # 3x3 blocks padded to 4x4 (C-3)
     assert oracle.tree_levels(128, 32, 64) == (2, 1)
+
+
+def test_single_block_level_counts():
+    """A 1x1-block product is one task at the single level (the root = the block)."""
+    assert oracle.level_task_counts(0, ([0], [0]), ([0], [0])) == [1]
+    assert oracle.level_node_counts(0, ([0], [0])) == [1]
+    # 2x2 blocks, A = diag, B = dense: root task, then 4 block products
+    assert oracle.level_task_counts(1, ([0, 1], [0, 1]), ([0, 0, 1, 1], [0, 1, 0, 1])) == [1, 4]
 
 
 def test_dense_two_level_spec_s90():
