@@ -59,7 +59,8 @@ struct __align__(16) StageHdr {
   int b[2];      // slot of B(k,J0), B(k,J1)
   int c[4];      // F_STORE: C block indices of the tile (slot 2i+j; -1 = none)
   int flags;
-  int pad0;
+  int sub;       // block size 16: quadrant masks of the staged blocks as read (op applied):
+                 // bits 0-3 A(I0,k), 4-7 A(I1,k), 8-11 B(k,J0), 12-15 B(k,J1)
   int pmask;     // bit 2i+j: product A(i,k)*B(k,j) at this step
   int slot_end;  // producer bookkeeping: slots allocated up to and including this step
 };
@@ -68,14 +69,15 @@ struct __align__(16) StageHdr {
 // (block size 16: "screening" by the quadrant masks — a product whose
 // quadrants never meet adds only zeros and is skipped, as in the BFS)
 // kScreen: 0 none, 1 norms, 2 block-size-16 quadrant masks
+// (ta/tb: the block is read transposed — a symmetric square's reference into U)
 template <bool kTA, bool kTB, int kScreen>
-__device__ __forceinline__ bool prod_ok(int a, int b, const NumericArgs& na) {
+__device__ __forceinline__ bool prod_ok(int a, int b, const NumericArgs& na, int ta = 0, int tb = 0) {
   if (a < 0 || b < 0) return false;
   if (kScreen == 0) return true;
   if (kScreen == 2) {
     int x = na.subA[a], y = na.subB[b];
-    if (kTA) x = mask_t(x);
-    if (kTB) y = mask_t(y);
+    if (kTA || ta) x = mask_t(x);
+    if (kTB || tb) y = mask_t(y);
     return mask_meet(x, y);
   }
   return __dmul_rn(na.normA[a], na.normB[b]) >= na.tau2;
@@ -163,7 +165,11 @@ __device__ __forceinline__ int off_k(int q, int m, int ks, int g, int t4) {
 // those of column j.  PM is a template parameter so that only the step's own
 // loads and DMMAs are issued (a predicated-off DMMA still occupies the pipe).
 // tA/tB: per-block transposes (bit 0: block 0, bit 1: block 1).
-template <int PM>
+// KS0/NKS: the k-slices [KS0, KS0+NKS) of 4 columns each — the whole block
+// (0, 8), or one 16-column half (0, 4) / (4, 4) at block size 16, where the
+// k-half h of a product is skipped when the A(Ii,k) quadrant (qi,h) or the
+// B(k,Jj) quadrant (h,qj) is absent (reading C-27).
+template <int PM, int KS0, int NKS>
 __device__ __forceinline__ void warp_step_mma(double (&acc)[4][2][2][2], const double* __restrict__ A0,
                                               const double* __restrict__ A1, const double* __restrict__ B0,
                                               const double* __restrict__ B1, int tA, int tB, int qi,
@@ -171,7 +177,7 @@ __device__ __forceinline__ void warp_step_mma(double (&acc)[4][2][2][2], const d
   constexpr bool ua0 = PM & 3, ua1 = PM & 12, ub0 = PM & 5, ub1 = PM & 10;
   const int g = lane >> 2, t4 = lane & 3;
 #pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
+  for (int ks = KS0; ks < KS0 + NKS; ++ks) {
     double af[2][2], bf[2][2];
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
@@ -198,26 +204,44 @@ __device__ __forceinline__ void warp_step_mma(double (&acc)[4][2][2][2], const d
   }
 }
 
+template <int KS0 = 0, int NKS = 8>
 __device__ __forceinline__ void warp_step(double (&acc)[4][2][2][2], const double* A0, const double* A1,
                                           const double* B0, const double* B1, int pm, int tA, int tB,
                                           int qi, int qj, int lane) {
+#define QT_STEP(P) warp_step_mma<P, KS0, NKS>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane)
   switch (pm) {
-    case 1: warp_step_mma<1>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    case 2: warp_step_mma<2>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    case 3: warp_step_mma<3>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    case 4: warp_step_mma<4>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    case 5: warp_step_mma<5>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    case 6: warp_step_mma<6>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    case 7: warp_step_mma<7>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    case 8: warp_step_mma<8>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    case 9: warp_step_mma<9>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    case 10: warp_step_mma<10>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    case 11: warp_step_mma<11>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    case 12: warp_step_mma<12>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    case 13: warp_step_mma<13>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    case 14: warp_step_mma<14>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
-    default: warp_step_mma<15>(acc, A0, A1, B0, B1, tA, tB, qi, qj, lane); break;
+    case 0: break;
+    case 1: QT_STEP(1); break;
+    case 2: QT_STEP(2); break;
+    case 3: QT_STEP(3); break;
+    case 4: QT_STEP(4); break;
+    case 5: QT_STEP(5); break;
+    case 6: QT_STEP(6); break;
+    case 7: QT_STEP(7); break;
+    case 8: QT_STEP(8); break;
+    case 9: QT_STEP(9); break;
+    case 10: QT_STEP(10); break;
+    case 11: QT_STEP(11); break;
+    case 12: QT_STEP(12); break;
+    case 13: QT_STEP(13); break;
+    case 14: QT_STEP(14); break;
+    default: QT_STEP(15); break;
   }
+#undef QT_STEP
+}
+
+// Block size 16: the products p = 2i+j of the step's mask `pm` whose k-half h
+// exists for this warp's quadrant (qi, qj): A(Ii,k) has quadrant (qi,h) and
+// B(k,Jj) has quadrant (h,qj) (masks as read, bit 2r+c = quadrant (r,c)).
+__device__ __forceinline__ int half_mask(int pm, int sub, int qi, int qj, int h) {
+  int out = 0;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int i = p >> 1, j = p & 1;
+    const int ma = (sub >> (4 * i)) & 15, mb = (sub >> (8 + 4 * j)) & 15;
+    if (((pm >> p) & 1) && ((ma >> (2 * qi + h)) & 1) && ((mb >> (2 * h + qj)) & 1)) out |= 1 << p;
+  }
+  return out;
 }
 
 // The two steps (kb = 0, 1) of task p at level L-1: the staged blocks
@@ -226,7 +250,7 @@ __device__ __forceinline__ void warp_step(double (&acc)[4][2][2][2], const doubl
 // producer's serial per-step path is only shuffles, the ring wait and the
 // TMA issue.
 struct StepDesc {
-  int a0, a1, b0, b1, meta;
+  int a0, a1, b0, b1, meta, sub;  // sub: block size 16 quadrant masks (StageHdr::sub)
 };
 template <bool kTA, bool kTB, bool kSym, int kScreen>
 __device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, int keep, const NumericArgs& a) {
@@ -236,8 +260,10 @@ __device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, int keep
   const int b0 = blk<kSym>(kb ? B4.z : B4.x, tb0), b1 = blk<kSym>(kb ? B4.w : B4.y, tb1);
   // products of this step: both blocks present and, when screening,
   // ||A(i,k)||^2 * ||B(k,j)||^2 >= tau^2 (the symbolic pass's test)
-  const int pm = ((prod_ok<kTA, kTB, kScreen>(a0, b0, a) ? 1 : 0) | (prod_ok<kTA, kTB, kScreen>(a0, b1, a) ? 2 : 0) |
-                  (prod_ok<kTA, kTB, kScreen>(a1, b0, a) ? 4 : 0) | (prod_ok<kTA, kTB, kScreen>(a1, b1, a) ? 8 : 0)) &
+  const int pm = ((prod_ok<kTA, kTB, kScreen>(a0, b0, a, ta0, tb0) ? 1 : 0) |
+                  (prod_ok<kTA, kTB, kScreen>(a0, b1, a, ta0, tb1) ? 2 : 0) |
+                  (prod_ok<kTA, kTB, kScreen>(a1, b0, a, ta1, tb0) ? 4 : 0) |
+                  (prod_ok<kTA, kTB, kScreen>(a1, b1, a, ta1, tb1) ? 8 : 0)) &
                  keep;
   StepDesc d;
   d.a0 = (pm & 3) ? a0 : -1;
@@ -245,6 +271,16 @@ __device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, int keep
   d.b0 = (pm & 5) ? b0 : -1;
   d.b1 = (pm & 10) ? b1 : -1;
   d.meta = pm | ((ta0 | (ta1 << 1) | (tb0 << 2) | (tb1 << 3)) << 4);
+  d.sub = 0;
+  if (kScreen == 2) {  // the operands' quadrant masks as the consumers read them
+    auto m = [&](const uint8_t* sub, int idx, bool tr) {
+      if (idx < 0) return 0;
+      const int x = sub[idx];
+      return tr ? mask_t(x) : x;
+    };
+    d.sub = m(a.subA, d.a0, kTA || ta0) | (m(a.subA, d.a1, kTA || ta1) << 4) |
+            (m(a.subB, d.b0, kTB || tb0) << 8) | (m(a.subB, d.b1, kTB || tb1) << 12);
+  }
   return d;
 }
 
@@ -313,7 +349,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
     int n_keep = 15, g_keep = 15;  // product mask of the work item (split mode: one C child)
     bool n_newgroup = true, n_valid = false;
     int4 n_cc = make_int4(-1, -1, -1, -1), n_ra = n_cc, n_rb = n_cc;
-    StepDesc n_d0{-1, -1, -1, -1, 0}, n_d1{-1, -1, -1, -1, 0};
+    StepDesc n_d0{-1, -1, -1, -1, 0, 0}, n_d1{-1, -1, -1, -1, 0, 0};
     auto issue_tasks = [&]() {  // node ids of the next batch
       const int p = n_pb0 + lane;
       n_pa = p < n_pend ? a.pa[p] : -1;
@@ -374,7 +410,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
             n_d0 = make_step<kTA, kTB, kSym, kScreen>(ca, cb, 0, keep, a);
             n_d1 = make_step<kTA, kTB, kSym, kScreen>(ca, cb, 1, keep, a);
           } else {
-            n_d0 = StepDesc{-1, -1, -1, -1, 0};
+            n_d0 = StepDesc{-1, -1, -1, -1, 0, 0};
             n_d1 = n_d0;
           }
           n_state = 5;
@@ -470,6 +506,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
           const int la1 = __shfl_sync(0xffffffffu, d.a1, u);
           const int lb0 = __shfl_sync(0xffffffffu, d.b0, u);
           const int lb1 = __shfl_sync(0xffffffffu, d.b1, u);
+          const int sub = kScreen == 2 ? __shfl_sync(0xffffffffu, d.sub, u) : 0;
           adv();
           const int n = (la0 >= 0) + (la1 >= 0) + (lb0 >= 0) + (lb1 >= 0);
           reserve(n);
@@ -488,6 +525,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
             h.b[0] = s2;
             h.b[1] = s3;
             h.flags = F_COMPUTE;
+            h.sub = sub;
             h.pmask = meta & 15;
             h.slot_end = head + n;
             uint64_t* fb = &full[hpos];
@@ -567,7 +605,13 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         const double* B0 = data + h.b[0] * kBlockElems;
         const double* B1 = data + h.b[1] * kBlockElems;
         const int tA = kTA ? 3 : 0, tB = kTB ? 3 : 0;
-        warp_step(acc, A0, A1, B0, B1, pm, tA, tB, qi, qj, lane);
+        if (kScreen == 2) {  // block size 16: only the k-halves whose quadrants exist
+          const int sub = h.sub;
+          warp_step<0, 4>(acc, A0, A1, B0, B1, half_mask(pm, sub, qi, qj, 0), tA, tB, qi, qj, lane);
+          warp_step<4, 4>(acc, A0, A1, B0, B1, half_mask(pm, sub, qi, qj, 1), tA, tB, qi, qj, lane);
+        } else {
+          warp_step(acc, A0, A1, B0, B1, pm, tA, tB, qi, qj, lane);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[hi]);
       }
@@ -674,8 +718,11 @@ void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
       launch_numeric_t<false, false, false, 1, true>(ctx, a, grid);
     else
       launch_numeric_t<false, false, false, 0, true>(ctx, a, grid);
-  } else if (a.trans & 4) {  // symmetric square
-    launch_numeric_t<false, false, true>(ctx, a, grid);
+  } else if (a.trans & 4) {  // symmetric square (block size 16: k-halves by the quadrant masks)
+    if (a.subA)
+      launch_numeric_t<false, false, true, 2>(ctx, a, grid);
+    else
+      launch_numeric_t<false, false, true>(ctx, a, grid);
   } else if (a.normA) {  // norm-screened product
     switch (a.trans & 3) {
       case 0: launch_numeric_t<false, false, false, 1>(ctx, a, grid); break;

@@ -937,7 +937,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       na.normA = screen ? A->norm2[L].as<double>() : nullptr;
       na.normB = screen ? B->norm2[L].as<double>() : nullptr;
       na.tau2 = tau2;
-      if (A->ubs == 16 && !sym) {
+      if (A->ubs == 16 && !f32) {  // block size 16: only the 16-block products that exist
         na.subA = A->sub.as<uint8_t>();
         na.subB = B->sub.as<uint8_t>();
       }

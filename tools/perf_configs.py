@@ -227,8 +227,11 @@ def leaf_sweep(ctx, stream):
     block products (2 bs^3 each).  Block size 16 runs as quadrants of the
     32-blocks (reading C-27): only its 16-block products are counted."""
     n = 4096
-    for dtype in (np.float64, np.float32):
-        for bs in (16, 32, 64):
+    dts = [d for d in (np.float64, np.float32) if os.environ.get("QT_SWEEP_DT", "f64,f32").find(
+        "f64" if d == np.float64 else "f32") >= 0]
+    bss = [int(x) for x in os.environ.get("QT_SWEEP_BS", "16,32,64").split(",")]
+    for dtype in dts:
+        for bs in bss:
             nb = n // bs
             for fill in (0.01, 0.02, 0.05, 0.1, 0.2, 0.5, 1.0):
                 rng = np.random.default_rng(int(1000 * fill) + bs)
@@ -352,6 +355,16 @@ def main():
                       flush=True)
         elif w == "virt8":
             run_virtual(ctx, stream, "cfg5 P=8 banded (virtual ranks)", qtgen.config(5, P=8)["A"], 8, [0, 3])
+        elif w == "virt8r3":  # interior rank 3 of P=8, one numeric launch per multiply (ncu traffic)
+            M = qtgen.config(5, P=8, rows=(3 * 512 - 32, 4 * 512 + 32))["A"]
+            A = qtmm.Matrix.from_blocks(ctx, M.n, M.leaf_dim, 32, M.brow, M.bcol, M.vals)
+            os.environ["QT_OVERLAP"] = "0"
+            for _ in range(4):
+                C, st = A.multiply_virtual(A, 8, 3, [512 * g for g in range(9)])
+                C.close()
+            print(json.dumps({"config": "cfg5 P=8 rank 3 (virtual, overlap off)", "block_products": st.block_products,
+                              "ms_numeric": round(st.ms_numeric, 4), "bytes_recv_payload": st.bytes_recv_payload}))
+            os.environ.pop("QT_OVERLAP", None)
         elif w == "virt8f32":
             M = qtgen.config(5, P=8)["A"]
             run_virtual(ctx, stream, "cfg5 P=8 banded FP32 (virtual ranks)",
