@@ -297,6 +297,10 @@ struct NumericArgs {
   int phase = 0;
   const int32_t* tile_map = nullptr;
   const int32_t* nsel = nullptr;
+  // sync-free multiply: the actual tile count on the device (ntiles is then an
+  // upper bound used for the launch shape only)
+  const int32_t* ntiles_dev = nullptr;
+  bool counter_ready = false;  // the scheduler counter is already zero (no memset before the launch)
 };
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a);
 void launch_transpose_blocks(qt_ctx ctx, const void* in, void* out, int64_t nb);
@@ -327,6 +331,7 @@ struct NumericArgs32 {
   int phase = 0;                   // overlap phases, as in NumericArgs
   const int32_t* tile_map = nullptr;
   const int32_t* nsel = nullptr;
+  bool counter_ready = false;      // as in NumericArgs
 };
 void launch_numeric_f32(qt_ctx ctx, const NumericArgs32& a);
 

@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
     // (a separate instantiation: the runtime checks cost the plain kernel 2-5 %
     // on sparse patterns)
     int ntiles = (int)a.ntiles, t_off = 0;
+    if (a.ntiles_dev) ntiles = *a.ntiles_dev * (a.split ? 4 : 1);  // sync-free: the BFS's count
     if (kPhase) {
       const int ns = *a.nsel;
       const int nt = a.split ? (int)a.ntiles / 4 : (int)a.ntiles;
@@ -419,9 +420,17 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         default: break;
       }
     };
+    // Few equal work items (split mode: one C block each): a static
+    // round-robin over the SMs — item b + G*(stream + 3*k) — so that no SM
+    // holds more than ceil(items / SMs) of them (with the atomic, the CTAs
+    // that start first take three items each and the others none).
+    int n_grabs = 0;
     auto grab = [&]() {  // start fetching the next group
       n_newgroup = true;
-      if (lane == 0) n_tl = atomicAdd(a.counter, G);
+      if (a.split && !kPhase)
+        n_tl = blockIdx.x + gridDim.x * (sid + kStreams * n_grabs++);
+      else if (lane == 0)
+        n_tl = atomicAdd(a.counter, G);
       n_state = 1;
     };
     int posted = 0, released = 0;  // steps posted / known released by the consumers
@@ -696,7 +705,7 @@ static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
 
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
   if (dt != QT_F64) fail(QT_EDTYPE, "launch_numeric is the FP64 kernel");
-  QT_CUDA(cudaMemsetAsync(a0.counter, 0, sizeof(int), a0.stream ? a0.stream : ctx->stream));
+  if (!a0.counter_ready) QT_CUDA(cudaMemsetAsync(a0.counter, 0, sizeof(int), a0.stream ? a0.stream : ctx->stream));
   // Few tiles (fewer than half the tile streams of the GPU): every C block of
   // a tile becomes its own work item, so more streams share the work — a lone
   // stream per SM is latency bound (its 9-slot ring covers ~2 steps of TMA

@@ -721,7 +721,7 @@ static void launch_f32_t(qt_ctx ctx, const NumericArgs32& a, int grid) {
 }
 
 void launch_numeric_f32(qt_ctx ctx, const NumericArgs32& a) {
-  QT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), a.stream ? a.stream : ctx->stream));
+  if (!a.counter_ready) QT_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), a.stream ? a.stream : ctx->stream));
   const int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
   if (a.trans & 4) {  // symmetric square
     launch_f32_t<false, false, true>(ctx, a, grid);

@@ -28,6 +28,7 @@
 // scans; the large levels in ONE persistent cooperative kernel whose phases
 // are separated by grid-wide barriers.  One host sync remains, before the
 // numeric kernel (to size C's block pool).
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cub/cub.cuh>
@@ -164,93 +165,163 @@ struct SmallBfsArgs {
   int32_t row_lo, row_hi;  // C row window (block rows)
   const uint8_t* subA;     // block size 16: quadrant masks (pair test at the block level)
   const uint8_t* subB;
+  unsigned long long* prof;  // QT_BFS_PROF: per-phase %globaltimer marks (diagnostics), or null
+  int* zero;                 // the numeric kernel's scheduler counters, zeroed here (saves a memset launch)
+  int32_t nodesA[QT_MAX_LEVELS];  // child-table rows per level (L2 prefetch at kernel start)
+  int32_t nodesB[QT_MAX_LEVELS];
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // kExt: the block-size-16 pair test and the C row window (multi-rank
 // symmetric square) are compiled in only for the launches that use them — the
 // runtime checks cost the plain BFS ~10 % (cfg4)
-template <bool kExt>
+// kSmem: the frontiers of the levels nobody reads after the kernel (all but
+// level l_end, and level L-1 when the kernel runs to the block level), the
+// scan scratch `off` and the (s,q) -> group map live in shared memory
+// (dynamic, kTinyF tasks / groups per level), so a level costs the child-table
+// gathers and block barriers only, not ~7 dependent round trips to L2.
+constexpr int kTinyF = 2048;
+constexpr size_t kTinySmem = 2 * (3 * 4 + 4 + 8) * (size_t)kTinyF + 4 * 2 * (size_t)kTinyF + 4 * 4 * (size_t)kTinyF +
+                             4 * 4 * (size_t)kTinyF + 64;
+
+template <bool kExt, bool kSmem>
 __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) {
-  using BS = cub::BlockScan<int, kSmallThreads>;
+  // the tiny variant runs 256 threads: its levels have <= kTinyF tasks and
+  // its cost is the latency of block scans and barriers, cheaper with 8 warps
+  constexpr int kT = kSmem ? 256 : kSmallThreads;
+  using BS = cub::BlockScan<int, kT>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ int s_F, s_ns;
+  extern __shared__ __align__(16) uint8_t tiny[];
   const int tid = threadIdx.x;
   const bool sym = a.trans & 4;
+  // per-level buffers: shared memory unless the level is read after the kernel
+  uint64_t* ck0 = reinterpret_cast<uint64_t*>(tiny);
+  int32_t* base = reinterpret_cast<int32_t*>(ck0 + 2 * kTinyF);
+  int32_t* off = kSmem ? base + 8 * kTinyF + 8 : a.off;
+  int32_t* gidx_s = kSmem ? off + 4 * kTinyF : a.gidx;
+  auto glob = [&](int l) { return !kSmem || l == a.l_end || (a.l_end == a.L && l == a.L - 1); };
+  auto PA = [&](int l) { return glob(l) ? a.pa[l & 1] : base + (l & 1) * kTinyF; };
+  auto PB = [&](int l) { return glob(l) ? a.pb[l & 1] : base + (2 + (l & 1)) * kTinyF; };
+  auto PC = [&](int l) { return glob(l) ? a.pc[l & 1] : base + (4 + (l & 1)) * kTinyF; };
+  auto CS = [&](int l) { return glob(l) ? a.cstart[l & 1] : base + 6 * kTinyF + (l & 1) * (kTinyF + 4); };
+  auto CK = [&](int l) { return glob(l) ? a.ckey[l & 1] : ck0 + (l & 1) * kTinyF; };
+  int np = 0;
+  auto mark = [&]() {
+    if (a.prof && tid == 0 && np < 40) a.prof[np] = gtimer();
+    ++np;
+  };
+  mark();
+  // one DRAM round trip for every child table the kernel will gather from
+  // (they were evicted from L2 by the previous numeric pass), instead of one
+  // per level
+  for (int l = 0; l < a.l_end; ++l) {
+    const char* ta = reinterpret_cast<const char*>(a.childA[l]);
+    const char* tb = reinterpret_cast<const char*>(a.childB[l]);
+    for (int i = tid; i < a.nodesA[l] / 8 + 1; i += kT)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(ta + 128 * (size_t)i));
+    if (tb != ta)
+      for (int i = tid; i < a.nodesB[l] / 8 + 1; i += kT)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(tb + 128 * (size_t)i));
+  }
+  // per-level table pointers copied to shared memory once: indexing the
+  // (large) parameter block by the level is a constant-cache miss per level
+  __shared__ const int4* s_cA[QT_MAX_LEVELS];
+  __shared__ const int4* s_cB[QT_MAX_LEVELS];
+  __shared__ const double* s_nA[QT_MAX_LEVELS];
+  __shared__ const double* s_nB[QT_MAX_LEVELS];
+  if (tid < QT_MAX_LEVELS) {
+    s_cA[tid] = a.childA[tid];
+    s_cB[tid] = a.childB[tid];
+    s_nA[tid] = a.normA[tid];
+    s_nB[tid] = a.normB[tid];
+  }
+  if (tid < 2) a.zero[tid] = 0;
   if (tid == 0) {
-    a.pa[0][0] = sym ? 2 : 0;  // the root (a diagonal node in the symmetric square)
-    a.pb[0][0] = sym ? 2 : 0;
-    a.pc[0][0] = 0;
+    PA(0)[0] = sym ? 2 : 0;  // the root (a diagonal node in the symmetric square)
+    PB(0)[0] = sym ? 2 : 0;
+    PC(0)[0] = 0;
     a.f_out[0] = 1;
-    a.cstart[0][0] = 0;
-    a.cstart[0][1] = 1;
-    a.ckey[0][0] = 0;
+    CS(0)[0] = 0;
+    CS(0)[1] = 1;
+    CK(0)[0] = 0;
     a.ns_out[0] = 1;
     s_F = 1;
     s_ns = 1;
   }
   __syncthreads();
   for (int l = 0; l < a.l_end; ++l) {
-    const int cur = l & 1, nxt = cur ^ 1;
     const bool prune = sym && l < (a.trans >> 8);  // C below the diagonal is not computed
     const int F = s_F, ns = s_ns;
-    const int32_t* pa = a.pa[cur];
-    const int32_t* pb = a.pb[cur];
-    const int32_t* pc = a.pc[cur];
-    const int32_t* cs = a.cstart[cur];
-    const uint64_t* ck = a.ckey[cur];
-    const int4* cA = a.childA[l];
-    const int4* cB = a.childB[l];
+    const int32_t* pa = PA(l);
+    const int32_t* pb = PB(l);
+    const int32_t* pc = PC(l);
+    const int32_t* cs = CS(l);
+    const uint64_t* ck = CK(l);
+    int32_t* csn = CS(l + 1);
+    uint64_t* ckn = CK(l + 1);
+    // the group map of the last transition is C's child table when the kernel reaches the blocks
+    int32_t* gidx = (!kSmem || (a.l_end == a.L && l == a.L - 1)) ? a.gidx : gidx_s;
+    const int4* cA = s_cA[l];
+    const int4* cB = s_cB[l];
     const bool lastl = kExt && l + 1 == a.L && a.subA;
-    const Screen sc{a.normA[l + 1], a.normB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
+    const Screen sc{s_nA[l + 1], s_nB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
                     a.trans & 3};
     const int32_t rlo = kExt ? a.row_lo : 0, rhi = kExt ? a.row_hi : INT32_MAX;
     // 1. child-task counts per (task, C child), group-major
-    for (int p = tid; p < F; p += kSmallThreads) {
+    for (int p = tid; p < F; p += kT) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
       int c[4];
-      child_counts(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym), c,
-                   sc, sym);
+      const int4 rA = op_children(cA, pa[p], a.trans & 1, sym), rB = op_children(cB, pb[p], a.trans & 2, sym);
+      child_counts(rA, rB, c, sc, sym);
       const int cm = cmask(ck + s, l, a.L, prune, rlo, rhi);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         if (!((cm >> q) & 1)) c[q] = 0;
       const int64_t base = 4ll * c0 + (p - c0);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) a.off[base + (int64_t)q * m] = c[q];
+      for (int q = 0; q < 4; ++q) off[base + (int64_t)q * m] = c[q];
     }
     __syncthreads();
+    mark();
     // 2. exclusive scan in place
     int carry = 0;
-    for (int b0 = 0; b0 < 4 * F; b0 += kSmallThreads) {
+    for (int b0 = 0; b0 < 4 * F; b0 += kT) {
       const int i = b0 + tid;
-      const int v = i < 4 * F ? a.off[i] : 0;
+      const int v = i < 4 * F ? off[i] : 0;
       int ex, agg;
       BS(tmp).ExclusiveSum(v, ex, agg);
-      if (i < 4 * F) a.off[i] = carry + ex;
+      if (i < 4 * F) off[i] = carry + ex;
       carry += agg;
       __syncthreads();
     }
     const int Fn = carry;
+    mark();
     // 3. new groups (non-empty (s,q)), their starts and keys
     int ncarry = 0;
-    for (int b0 = 0; b0 < 4 * ns; b0 += kSmallThreads) {
+    for (int b0 = 0; b0 < 4 * ns; b0 += kT) {
       const int x = b0 + tid;
       int flag = 0, gst = 0;
       if (x < 4 * ns) {
         const int s = x >> 2, q = x & 3, c0 = cs[s], m = cs[s + 1] - c0;
         const int lo = 4 * c0 + q * m, hi = lo + m;
-        gst = a.off[lo];
-        const int en = hi < 4 * F ? a.off[hi] : Fn;
+        gst = off[lo];
+        const int en = hi < 4 * F ? off[hi] : Fn;
         flag = en > gst;
       }
       int ex, agg;
       BS(tmp).ExclusiveSum(flag, ex, agg);
       if (x < 4 * ns) {
         const int t = flag ? ncarry + ex : -1;
-        a.gidx[x] = t;
+        gidx[x] = t;
         if (flag) {
-          a.cstart[nxt][t] = gst;
-          a.ckey[nxt][t] = (ck[x >> 2] << 2) | (uint64_t)(x & 3);
+          csn[t] = gst;
+          ckn[t] = (ck[x >> 2] << 2) | (uint64_t)(x & 3);
         }
       }
       ncarry += agg;
@@ -258,19 +329,18 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     }
     const int nsn = ncarry;
     if (tid == 0) {
-      a.cstart[nxt][nsn] = Fn;
+      csn[nsn] = Fn;
       a.ns_out[l + 1] = nsn;
       a.f_out[l + 1] = Fn;
     }
     __syncthreads();
+    mark();
     // 4. emit the child tasks (none below the block level)
-    for (int p = tid; p < F && l + 1 < a.L; p += kSmallThreads) {
+    for (int p = tid; p < F && l + 1 < a.L; p += kT) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
       emit_task(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym),
-                4ll * c0 + (p - c0), m, s, cmask(ck + s, l, a.L, prune, rlo, rhi), sc, sym, a.off,
-                a.gidx, a.pa[nxt],
-                a.pb[nxt],
-                a.pc[nxt]);
+                4ll * c0 + (p - c0), m, s, cmask(ck + s, l, a.L, prune, rlo, rhi), sc, sym, off,
+                gidx, PA(l + 1), PB(l + 1), PC(l + 1));
     }
     __syncthreads();
     if (tid == 0) {
@@ -278,7 +348,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
       s_ns = nsn;
     }
     __syncthreads();
+    mark();
   }
+  if (a.prof && tid == 0) a.prof[63] = np;
 }
 
 // ------------------------------------------------------------ large levels (one persistent kernel)
@@ -610,6 +682,15 @@ int large_bfs_grid(qt_ctx ctx) {
 }
 
 
+// Largest transient C pool (bytes) the sync-free mode may allocate by its upper bound.
+size_t syncfree_cap() {
+  static size_t cap = [] {
+    const char* e = getenv("QT_SYNCFREE_MB");
+    return (size_t)(e ? atoll(e) : 1024) << 20;
+  }();
+  return cap;
+}
+
 }  // namespace
 
 // Optional host-side phase trace (QT_TRACE=1): wall-clock marks to stderr.
@@ -704,9 +785,9 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       // upper bounds of the group counts: ns_{l+1} <= min(4 ns_l, F_{l+1})
       std::vector<int64_t> nsb(L + 1, 1);
       for (int l = 0; l < L; ++l) nsb[l + 1] = std::min<int64_t>(4 * nsb[l], F[l + 1]);
-      DevBuf ns_dev(4 * (L + 1), st), f_dev(4 * (L + 1), st);
-      int32_t* nsd = ns_dev.as<int32_t>();
-      int32_t* fd = f_dev.as<int32_t>();
+      DevBuf cnt_dev(8 * (L + 1), st);  // [ns(L+1) | F(L+1)]: one D2H copy
+      int32_t* nsd = cnt_dev.as<int32_t>();
+      int32_t* fd = nsd + (L + 1);
       // --- small levels in one CTA
       const bool f32 = C->dtype == QT_F32;
       int l_end = 0;
@@ -739,6 +820,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       for (int l = 0; l < L; ++l) {
         sa.childA[l] = A->child[l].as<int4>();
         sa.childB[l] = B->child[l].as<int4>();
+        sa.nodesA[l] = (int32_t)std::min<int64_t>(A->cnt[l], INT32_MAX);
+        sa.nodesB[l] = (int32_t)std::min<int64_t>(B->cnt[l], INT32_MAX);
       }
       for (int b = 0; b < 2; ++b) {
         sp[b].alloc(4 * maxF, st);
@@ -757,13 +840,48 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       sa.gidx = sg.as<int32_t>();
       sa.ns_out = nsd;
       sa.f_out = fd;
+      sa.zero = ctx->counters.as<int>() + 16;  // the numeric kernels' scheduler counters (16, 17)
       tr.mark("small_alloc");
       const bool ext = sa.subA || row_lo > 0 || row_hi < INT32_MAX;
-      if (ext)
-        k_bfs_small<true><<<1, kSmallThreads, 0, st>>>(sa);
-      else
-        k_bfs_small<false><<<1, kSmallThreads, 0, st>>>(sa);
+      static const bool bfs_prof = getenv("QT_BFS_PROF") != nullptr;
+      DevBuf profbuf;
+      sa.prof = nullptr;
+      if (bfs_prof) {
+        profbuf.alloc(64 * 8, st);
+        QT_CUDA(cudaMemsetAsync(profbuf.p, 0, 64 * 8, st));
+        sa.prof = profbuf.as<unsigned long long>();
+      }
+      // the intermediate small levels in shared memory when every one fits
+      bool tiny = true;
+      for (int l = 0; l < l_end; ++l) tiny = tiny && F[l] <= kTinyF;
+      if (tiny) {
+        static std::atomic<unsigned long long> attr_set{0};  // per device (bit d)
+        const unsigned long long bit = 1ull << (ctx->device & 63);
+        if (!(attr_set.load(std::memory_order_acquire) & bit)) {
+          QT_CUDA(cudaFuncSetAttribute(k_bfs_small<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kTinySmem));
+          QT_CUDA(cudaFuncSetAttribute(k_bfs_small<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kTinySmem));
+          attr_set.fetch_or(bit, std::memory_order_release);
+        }
+        if (ext)
+          k_bfs_small<true, true><<<1, 256, kTinySmem, st>>>(sa);
+        else
+          k_bfs_small<false, true><<<1, 256, kTinySmem, st>>>(sa);
+      } else if (ext) {
+        k_bfs_small<true, false><<<1, kSmallThreads, 0, st>>>(sa);
+      } else {
+        k_bfs_small<false, false><<<1, kSmallThreads, 0, st>>>(sa);
+      }
       QT_LAUNCH_CHECK(ctx);
+      if (bfs_prof) {
+        unsigned long long h[64];
+        QT_CUDA(cudaMemcpyAsync(h, profbuf.p, 64 * 8, cudaMemcpyDeviceToHost, st));
+        QT_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "[qt bfs_small] l_end=%d tiny=%d marks(ns):", l_end, (int)tiny);
+        for (int i = 1; i < (int)h[63] && i < 40; ++i) fprintf(stderr, " %llu", h[i] - h[i - 1]);
+        fprintf(stderr, "\n");
+      }
       const bool all_small = l_end == L;
       const int cb = (all_small ? L - 1 : l_end) & 1;
       DevBuf pa = std::move(sp[cb]), pb = std::move(sb[cb]), pc = std::move(sc[cb]);
@@ -868,22 +986,41 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
           cstart = std::move(qcs[set(L - 1)]);
         }
       }
-      // --- group counts of every level (the one remaining sync): C's block count
+      // --- group counts of every level: C's block count.  Sync-free mode
+      // (small problems, where a host round trip between the BFS and the
+      // numeric kernel is a large share of the call): C's pool is sized by
+      // the upper bound nsb[L] (transient over-allocation <= QT_SYNCFREE_MB,
+      // default 1024 MiB), the numeric kernel reads the tile count from the
+      // device, and the counts come back with the call's one final sync.
       tr.mark("levels_launched");
       std::vector<int32_t> ns(L + 1, 0), Fa(L + 1, 0);
-      QT_CUDA(cudaMemcpyAsync(ns.data(), nsd, 4 * (L + 1), cudaMemcpyDeviceToHost, st));
-      QT_CUDA(cudaMemcpyAsync(Fa.data(), fd, 4 * (L + 1), cudaMemcpyDeviceToHost, st));
-      QT_CUDA(cudaStreamSynchronize(st));
-      tr.mark("levels_done");
-      for (int l = 0; l <= L; ++l) {
-        S.level_c_nodes[l] = ns[l];
-        S.level_tasks[l] = Fa[l];  // actual counts (== F for regular products)
-        F[l] = Fa[l];
+      const size_t cbound = (size_t)nsb[L] * 1024 * elem_size(C->dtype);
+      const bool syncfree = !f32 && A->ubs != 16 && !ov && !plan && !ctx->async_multiply && !B->pool2 &&
+                            cbound <= syncfree_cap();
+      int32_t* h_counts = static_cast<int32_t*>(ctx->pinned);  // [ns(L+1) | F(L+1)]
+      if (syncfree) {
+        for (int l = 0; l <= L; ++l) ns[l] = (int32_t)nsb[l];  // upper bounds until the final sync
+        C->nb = nsb[L];
+        C->pool.alloc(cbound, st);
+        tr.mark("c_alloc_bound");
+      } else {
+        QT_CUDA(cudaMemcpyAsync(h_counts, nsd, 8 * (L + 1), cudaMemcpyDeviceToHost, st));
+        QT_CUDA(cudaStreamSynchronize(st));
+        for (int l = 0; l <= L; ++l) {
+          ns[l] = h_counts[l];
+          Fa[l] = h_counts[L + 1 + l];
+        }
+        tr.mark("levels_done");
+        for (int l = 0; l <= L; ++l) {
+          S.level_c_nodes[l] = ns[l];
+          S.level_tasks[l] = Fa[l];  // actual counts (== F for regular products)
+          F[l] = Fa[l];
+        }
+        S.block_products = Fa[L];
+        C->nb = ns[L];
+        C->pool.alloc((size_t)C->nb * 1024 * elem_size(C->dtype), st);
+        tr.mark("c_alloc");
       }
-      S.block_products = Fa[L];
-      C->nb = ns[L];
-      C->pool.alloc((size_t)C->nb * 1024 * elem_size(C->dtype), st);
-      tr.mark("c_alloc");
       // tiles per scheduler grab (FP64): ~32 tasks per grab, at most 16 tiles
       int group = 1;
       {
@@ -942,6 +1079,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         na.subB = B->sub.as<uint8_t>();
       }
       na.group = group;
+      na.counter_ready = true;  // zeroed by the small BFS kernel
+      if (syncfree) na.ntiles_dev = nsd + (L - 1);  // the actual tile count (na.ntiles: its bound)
       DevBuf poolT;  // symmetric square: blocks of U read transposed come from U^T's copy
       if (C->nb > 0 && sym) {
         poolT.alloc((size_t)A->nb * 1024 * elem_size(C->dtype), st);
@@ -995,6 +1134,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         nb.poolC = C->pool.p;
         nb.zeros = ctx->zeros.p;
         nb.counter = ctx->counters.as<int>() + 16;
+        nb.counter_ready = true;
         nb.trans = trans & 7;
         nb.poolT = poolT.p;
         if (two_phase)
@@ -1002,11 +1142,25 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         else
           launch_numeric_f32(ctx, nb);
       }
+      if (syncfree) {  // the BFS's counts ride back with the final sync
+        QT_CUDA(cudaMemcpyAsync(h_counts, nsd, 8 * (L + 1), cudaMemcpyDeviceToHost, st));
+      }
       QT_CUDA(cudaEventRecord(ctx->ev[4], st));
       tr.mark("numeric_launched");
       // (the frontier buffers go back to this stream's cache: stream-ordered reuse)
       if (!ctx->async_multiply) QT_CUDA(cudaEventSynchronize(ctx->ev[4]));
       tr.mark("numeric_done");
+      if (syncfree) {
+        for (int l = 0; l <= L; ++l) {
+          ns[l] = h_counts[l];
+          Fa[l] = h_counts[L + 1 + l];
+          S.level_c_nodes[l] = ns[l];
+          S.level_tasks[l] = Fa[l];
+          F[l] = Fa[l];
+        }
+        S.block_products = Fa[L];
+        C->nb = ns[L];  // (the pool keeps its bound-sized allocation)
+      }
       if (two_phase && !ctx->async_multiply) {
         int32_t h = 0;
         QT_CUDA(cudaMemcpyAsync(&h, tnsel.p, 4, cudaMemcpyDeviceToHost, st));
@@ -1059,6 +1213,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
           nb.counter = ctx->counters.as<int>() + 16;
           nb.trans = trans & 7;
           nb.poolT = poolT.p;
+          nb.counter_ready = false;  // re-executions zero the counter themselves
           plan->nb = nb;
           plan->keep[0] = std::move(t2_cstart);
           plan->keep[1] = std::move(t2_pa);
@@ -1067,6 +1222,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
           plan->keep[4] = std::move(cchild);
         } else {
           plan->na = na;
+          plan->na.counter_ready = false;  // re-executions zero the counter themselves
           plan->keep[0] = std::move(cstart);
           plan->keep[1] = std::move(pa);
           plan->keep[2] = std::move(pb);
