@@ -181,11 +181,19 @@ qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, q
  * kernel skips the same block products.  ||C - C~||_F <= sum of the skipped
  * ||A(I,K)|| ||B(K,J)||.  tau = 0 gives qt_multiply's result.  Squared block
  * norms are summed row-major with separate multiply/add roundings (the
- * oracle's order, so both take identical decisions).  FP64, block_size 32.
+ * oracle's order, so both take identical decisions).
+ * Block size 16 (the paper screens its S^2 runs at block size 16):
+ * the test is per 16-block product with 16-block norms; a container's norm
+ * is the sum of its quadrants' (pruning above stays exact), and the consumer
+ * warps skip the k-halves whose 16-block product fails.  block_products
+ * counts the surviving 16-block products.
+ * FP32 (reading C-29): the screened product runs on FP64 copies of A and B
+ * (exact conversion) through the FP64 kernel and C is rounded to FP32 — a
+ * tcgen05 tile MMA cannot skip single block products.
  * Multi-rank (collective): each rank fetches the B rows of the full product
  * (qt_multiply's exchange) and screens its own strip; C is bitwise the
  * single-rank screened product's rows.  Errors: QT_EINVAL (tau < 0), QT_EDIM,
- * QT_EBS, QT_EDTYPE, QT_ENOMEM, QT_ECUDA, QT_ENCCL. */
+ * QT_EBS (block_size 64), QT_EDTYPE, QT_ENOMEM, QT_ECUDA, QT_ENCCL. */
 qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_stats* st);
 
 /* Symmetric matrix square C = A^2 (§3.3): A is symmetric and given

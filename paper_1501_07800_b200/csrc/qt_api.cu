@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <unordered_map>
@@ -693,24 +694,43 @@ qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_sta
   if (A->n != B->n) fail(QT_EDIM, "dimension mismatch");
   if (A->leaf_dim != B->leaf_dim || A->ubs != B->ubs) fail(QT_EBS, "leaf_dim/block_size mismatch");
   if (A->dtype != B->dtype) fail(QT_EDTYPE, "dtype mismatch");
-  if (A->dtype != QT_F64) fail(QT_EDTYPE, "norm screening is FP64-only (the FP32 tile MMA cannot skip single products)");
-  if (A->ubs != 32) fail(QT_EBS, "norm screening is built for block_size 32");
+  if (A->ubs == 64) fail(QT_EBS, "norm screening is built for block_size 16 and 32");
   qt_ctx ctx = A->ctx;
   QT_CUDA(cudaSetDevice(ctx->device));
   ensure_levels(A);
   ensure_levels(B);
+  // FP32 (reading C-29): a tcgen05 tile MMA cannot skip single block
+  // products, so the screened FP32 product runs on FP64 copies of A and B
+  // (exact conversion) through the FP64 kernel and C is rounded to FP32 —
+  // the oracle is the double product of the same FP32 values
+  std::unique_ptr<qt_mat_s> A64, B64;
+  qt_mat a = A, b = B;
+  if (A->dtype == QT_F32) {
+    A64.reset(convert_dtype(A, QT_F64));
+    a = A64.get();
+    if (B == A) {
+      b = a;
+    } else {
+      B64.reset(convert_dtype(B, QT_F64));
+      b = B64.get();
+    }
+  }
   qt_stats local;
   qt_stats& S = st ? *st : local;
   memset(&S, 0, sizeof(S));
   QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   qt_mat R;
   if (ctx->world > 1) {  // the exchange of the full product, then the screened multiply on B_ext
-    R = multiply_dist(A, B, &S, tau);
+    R = multiply_dist(a, b, &S, tau);
   } else {
     float ms_sym = 0, ms_num = 0;
-    R = multiply_local(A, B, &S, &ms_sym, &ms_num, 0, tau);
+    R = multiply_local(a, b, &S, &ms_sym, &ms_num, 0, tau);
     S.ms_symbolic = ms_sym;
     S.ms_numeric = ms_num;
+  }
+  if (A->dtype == QT_F32) {
+    std::unique_ptr<qt_mat_s> R64(R);
+    R = convert_dtype(R64.get(), QT_F32);
   }
   QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   QT_CUDA(cudaEventSynchronize(ctx->ev[1]));

@@ -215,7 +215,8 @@ __global__ void k_cmask16(const int32_t* __restrict__ ts, const int32_t* __restr
                           int64_t ntiles, const int4* __restrict__ cA, const int4* __restrict__ cB,
                           const int4* __restrict__ cC, const uint8_t* __restrict__ subA,
                           const uint8_t* __restrict__ subB, int trans, const uint64_t* __restrict__ keyC,
-                          uint8_t* __restrict__ subC, unsigned long long* __restrict__ counts) {
+                          uint8_t* __restrict__ subC, unsigned long long* __restrict__ counts,
+                          const double* __restrict__ n16A, const double* __restrict__ n16B, double tau2) {
   // symmetric square (trans bit 2): node and block entries are references
   // into U (index << 2 | diagonal << 1 | transposed), see op_children; the
   // (1,0) quadrant of a diagonal C container, and every container below the
@@ -256,7 +257,17 @@ __global__ void k_cmask16(const int32_t* __restrict__ ts, const int32_t* __restr
           if (trans & 1) ma = mask_t(ma);
           if (trans & 2) mb = mask_t(mb);
         }
-        m[q] |= mask_mul(ma, mb, np, keep[q]);
+        if (n16A) {  // norm screening (plain product): the 16-block products that pass
+          const int pm = screen16(ma, mb, n16A + 4 * (int64_t)x, n16B + 4 * (int64_t)y, tau2);
+#pragma unroll
+          for (int cq = 0; cq < 4; ++cq) {
+            const int nq = ((pm >> (2 * cq)) & 1) + ((pm >> (2 * cq + 1)) & 1);
+            np += nq;
+            if (nq) m[q] |= 1 << cq;
+          }
+        } else {
+          m[q] |= mask_mul(ma, mb, np, keep[q]);
+        }
       }
     }
   }
@@ -503,14 +514,15 @@ int64_t compact_sub16(qt_ctx ctx, const uint8_t* keep, const int32_t* incl, cons
 
 void cmask16(qt_ctx ctx, int64_t ntiles, const int32_t* ts, const int32_t* pa, const int32_t* pb, const int4* cA,
              const int4* cB, const int4* cC, const uint8_t* subA, const uint8_t* subB, int trans,
-             const uint64_t* keyC, uint8_t* subC, int64_t nc, int64_t out[4]) {
+             const uint64_t* keyC, uint8_t* subC, int64_t nc, int64_t out[4], const double* n16A,
+             const double* n16B, double tau2) {
   cudaStream_t st = ctx->stream;
   DevBuf cnt(32, st);
   QT_CUDA(cudaMemsetAsync(cnt.p, 0, 32, st));
   QT_CUDA(cudaMemsetAsync(subC, 0, std::max<int64_t>(nc, 1), st));
   if (ntiles > 0) {
     k_cmask16<<<(unsigned)((ntiles + 7) / 8), 256, 0, st>>>(ts, pa, pb, ntiles, cA, cB, cC, subA, subB, trans, keyC,
-                                                           subC, cnt.as<unsigned long long>());
+                                                           subC, cnt.as<unsigned long long>(), n16A, n16B, tau2);
     QT_LAUNCH_CHECK(ctx);
   }
   unsigned long long h[4];

@@ -104,4 +104,22 @@ __host__ __device__ __forceinline__ bool mask_meet(int x, int y) {
   return ((x & 5) && (y & 3)) || ((x & 10) && (y & 12));
 }
 
+// Block size 16 with norm screening: the 16-block products of the container
+// pair (x, y) (masks as read) that exist and pass ||x_rh||^2 ||y_hc||^2 >= tau^2
+// (squared 16-block norms n16x[2r+h], n16y[2h+c]).  bit 2*(2r+c)+h = product
+// x(r,h)·y(h,c) of C quadrant (r,c).
+__device__ __forceinline__ int screen16(int x, int y, const double* __restrict__ nx, const double* __restrict__ ny,
+                                        double tau2) {
+  int out = 0;
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (((x >> (2 * r + h)) & 1) && ((y >> (2 * h + c)) & 1) && __dmul_rn(nx[2 * r + h], ny[2 * h + c]) >= tau2)
+          out |= 1 << (2 * (2 * r + c) + h);
+  return out;
+}
+
 }  // namespace qt

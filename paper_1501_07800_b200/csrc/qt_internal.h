@@ -156,6 +156,7 @@ struct qt_mat_s {
   qt::DevBuf hist;     // int32 per-level node counts per row / per column (see build_levels)
   std::vector<int32_t> hist_host;  // host copy of hist (per-level task counts without a sync)
   std::vector<qt::DevBuf> norm2;  // squared Frobenius norms per node, levels 0..L (screening; lazy)
+  qt::DevBuf norm16;   // ubs == 16 screening: squared norms of the 16-blocks, double [nb][4] (0 if absent; lazy)
   qt::DevBuf rm_inv;   // pool index -> position in row-major (brow, bcol) order (qt_update_values; lazy)
   qt::DevBuf sub;      // ubs == 16: uint8 [nb] quadrant occupancy (bit 2i+j), indexed like the pool
   int64_t nb16 = 0;    // ubs == 16: the caller's blocks (set quadrants)
@@ -220,7 +221,8 @@ int64_t compact_sub16(qt_ctx ctx, const uint8_t* keep, const int32_t* incl, cons
 // containers, non-NIL container pairs (the level-L task count)}
 void cmask16(qt_ctx ctx, int64_t ntiles, const int32_t* ts, const int32_t* pa, const int32_t* pb, const int4* cA,
              const int4* cB, const int4* cC, const uint8_t* subA, const uint8_t* subB, int trans,
-             const uint64_t* keyC, uint8_t* subC, int64_t nc, int64_t out[4]);
+             const uint64_t* keyC, uint8_t* subC, int64_t nc, int64_t out[4], const double* n16A = nullptr,
+             const double* n16B = nullptr, double tau2 = 0.0);
 qt_mat drop_empty16(qt_mat C);
 // symmetric square at bs 16: upper-storage check, U with completed diagonal
 // containers, and C's lower quadrants of diagonal containers removed
@@ -235,6 +237,8 @@ void truncate_decide(qt_ctx ctx, const double* nrm_all, const uint64_t* rm_all, 
                      int64_t n_all, double tau2, int me, uint8_t* keep_local);
 qt_mat truncate(qt_mat A, double tau);
 qt_mat truncate_dist(qt_mat A, double tau);
+// the same matrix with its values converted to `to` (FP32 <-> FP64; plain matrices)
+qt_mat convert_dtype(qt_mat A, qt_dtype to);
 // copy `keep` flagged blocks (Morton order preserved) of A into a new matrix
 qt_mat select_blocks(qt_mat A, const uint8_t* d_keep);
 
@@ -265,7 +269,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* st, float* ms_sym, float* ms
 // when the tiles sit at level L-2 (FP32), else null.  No host sync.
 void split_tiles(qt_ctx ctx, int64_t ntiles, const int32_t* ts, const int32_t* pb, const int4* childB_t,
                  const int4* childB_1, int64_t splitB, int32_t* map, int32_t* nsel);
-// squared Frobenius norms of every quadtree node (levels 0..L) into M->norm2
+// squared Frobenius norms of every quadtree node (levels 0..L) into M->norm2;
+// block size 16: also the 16-blocks' (M->norm16), a container's = the sum of its quadrants'
 void ensure_norms(qt_mat M);
 
 struct NumericArgs {
@@ -291,6 +296,8 @@ struct NumericArgs {
   double tau2 = 0.0;
   const uint8_t* subA = nullptr;  // block size 16: quadrant masks (products whose quadrants never meet are skipped)
   const uint8_t* subB = nullptr;
+  const double* norm16A = nullptr;  // block size 16 + screening: squared 16-block norms [nb][4]
+  const double* norm16B = nullptr;
   cudaStream_t stream = nullptr;  // launch stream (null: the ctx stream)
   // overlap phases (split_tiles): phase 1 = tiles map[0, *nsel), phase 2 =
   // map[*nsel, ntiles); 0 = all tiles in order (tile_map unused).  group == 1.

@@ -69,11 +69,13 @@ struct __align__(16) StageHdr {
 // (block size 16: "screening" by the quadrant masks — a product whose
 // quadrants never meet adds only zeros and is skipped, as in the BFS)
 // kScreen: 0 none, 1 norms, 2 block-size-16 quadrant masks
+// kScreen 3 (block size 16 + norm screening): make_step decides per 16-block
+// product from the quadrant norms (the step's pair mask), prod_ok only checks presence
 // (ta/tb: the block is read transposed — a symmetric square's reference into U)
 template <bool kTA, bool kTB, int kScreen>
 __device__ __forceinline__ bool prod_ok(int a, int b, const NumericArgs& na, int ta = 0, int tb = 0) {
   if (a < 0 || b < 0) return false;
-  if (kScreen == 0) return true;
+  if (kScreen == 0 || kScreen == 3) return true;
   if (kScreen == 2) {
     int x = na.subA[a], y = na.subB[b];
     if (kTA || ta) x = mask_t(x);
@@ -272,6 +274,26 @@ __device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, int keep
   d.b1 = (pm & 10) ? b1 : -1;
   d.meta = pm | ((ta0 | (ta1 << 1) | (tb0 << 2) | (tb1 << 3)) << 4);
   d.sub = 0;
+  if (kScreen == 3) {  // per consumer warp (qi,qj), product p, k-half h: bit 8*(2qi+qj) + 2p + h
+    int pm3 = 0;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int ai = (p >> 1) ? a1 : a0, bj = (p & 1) ? b1 : b0;
+      if (!((pm >> p) & 1)) continue;
+      const int x = a.subA[ai], y = a.subB[bj];
+      const int m = screen16(x, y, a.norm16A + 4 * (int64_t)ai, a.norm16B + 4 * (int64_t)bj, a.tau2);
+#pragma unroll
+      for (int cq = 0; cq < 4; ++cq) {  // C quadrant (r,c) = the consumer warp's quadrant
+        d.sub |= ((m >> (2 * cq)) & 3) << (8 * cq + 2 * p);
+      }
+      if (m) pm3 |= 1 << p;
+    }
+    d.a0 = (pm3 & 3) ? a0 : -1;
+    d.a1 = (pm3 & 12) ? a1 : -1;
+    d.b0 = (pm3 & 5) ? b0 : -1;
+    d.b1 = (pm3 & 10) ? b1 : -1;
+    d.meta = pm3 | (d.meta & ~15);
+  }
   if (kScreen == 2) {  // the operands' quadrant masks as the consumers read them
     auto m = [&](const uint8_t* sub, int idx, bool tr) {
       if (idx < 0) return 0;
@@ -515,7 +537,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
           const int la1 = __shfl_sync(0xffffffffu, d.a1, u);
           const int lb0 = __shfl_sync(0xffffffffu, d.b0, u);
           const int lb1 = __shfl_sync(0xffffffffu, d.b1, u);
-          const int sub = kScreen == 2 ? __shfl_sync(0xffffffffu, d.sub, u) : 0;
+          const int sub = kScreen >= 2 ? __shfl_sync(0xffffffffu, d.sub, u) : 0;
           adv();
           const int n = (la0 >= 0) + (la1 >= 0) + (lb0 >= 0) + (lb1 >= 0);
           reserve(n);
@@ -618,6 +640,16 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
           const int sub = h.sub;
           warp_step<0, 4>(acc, A0, A1, B0, B1, half_mask(pm, sub, qi, qj, 0), tA, tB, qi, qj, lane);
           warp_step<4, 4>(acc, A0, A1, B0, B1, half_mask(pm, sub, qi, qj, 1), tA, tB, qi, qj, lane);
+        } else if (kScreen == 3) {  // ... and pass the norm screen (this warp's 8 bits of the pair mask)
+          const int w8 = (h.sub >> (8 * (2 * qi + qj))) & 255;
+          int h0 = 0, h1 = 0;
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            h0 |= ((w8 >> (2 * p)) & 1) << p;
+            h1 |= ((w8 >> (2 * p + 1)) & 1) << p;
+          }
+          warp_step<0, 4>(acc, A0, A1, B0, B1, h0, tA, tB, qi, qj, lane);
+          warp_step<4, 4>(acc, A0, A1, B0, B1, h1, tA, tB, qi, qj, lane);
         } else {
           warp_step(acc, A0, A1, B0, B1, pm, tA, tB, qi, qj, lane);
         }
@@ -721,7 +753,9 @@ void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
   // grouped grabs (sparse patterns: amortise the scheduler and metadata latency)
   if (a.phase) {  // multi-rank overlap phases: plain (or bs-16 masked) products only
     if (a.trans & 7) fail(QT_EINVAL, "overlap phases are built for the plain product");
-    if (a.subA)
+    if (a.subA && a.norm16A)
+      launch_numeric_t<false, false, false, 3, true>(ctx, a, grid);
+    else if (a.subA)
       launch_numeric_t<false, false, false, 2, true>(ctx, a, grid);
     else if (a.normA)
       launch_numeric_t<false, false, false, 1, true>(ctx, a, grid);
@@ -732,6 +766,9 @@ void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
       launch_numeric_t<false, false, true, 2>(ctx, a, grid);
     else
       launch_numeric_t<false, false, true>(ctx, a, grid);
+  } else if (a.subA && a.norm16A) {  // block size 16, norm-screened (plain product)
+    if (a.trans & 3) fail(QT_EINVAL, "the screened product is built for the plain product");
+    launch_numeric_t<false, false, false, 3>(ctx, a, grid);
   } else if (a.normA) {  // norm-screened product
     switch (a.trans & 3) {
       case 0: launch_numeric_t<false, false, false, 1>(ctx, a, grid); break;

@@ -91,6 +91,8 @@ struct Screen {
   const uint8_t* ma = nullptr;
   const uint8_t* mb = nullptr;
   int tr = 0;
+  const double* n16a = nullptr;  // block size 16 + screening: squared 16-block norms [nb][4]
+  const double* n16b = nullptr;
 };
 __device__ __forceinline__ bool pair_ok(int ar, int br, const Screen& sc, bool sym) {
   if (ar < 0 || br < 0) return false;
@@ -98,6 +100,8 @@ __device__ __forceinline__ bool pair_ok(int ar, int br, const Screen& sc, bool s
     int x = sc.ma[sym ? (ar >> 2) : ar], y = sc.mb[sym ? (br >> 2) : br];
     if (sym ? (ar & 1) : (sc.tr & 1)) x = mask_t(x);
     if (sym ? (br & 1) : (sc.tr & 2)) y = mask_t(y);
+    // screened (plain product only): some 16-block product passes the test
+    if (sc.n16a) return screen16(x, y, sc.n16a + 4 * (int64_t)ar, sc.n16b + 4 * (int64_t)br, sc.tau2) != 0;
     return mask_meet(x, y);
   }
   if (!sc.na) return true;
@@ -165,6 +169,8 @@ struct SmallBfsArgs {
   int32_t row_lo, row_hi;  // C row window (block rows)
   const uint8_t* subA;     // block size 16: quadrant masks (pair test at the block level)
   const uint8_t* subB;
+  const double* n16A;      // block size 16 + screening: squared 16-block norms, or null
+  const double* n16B;
   unsigned long long* prof;  // QT_BFS_PROF: per-phase %globaltimer marks (diagnostics), or null
   int* zero;                 // the numeric kernel's scheduler counters, zeroed here (saves a memset launch)
   int32_t nodesA[QT_MAX_LEVELS];  // child-table rows per level (L2 prefetch at kernel start)
@@ -271,7 +277,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     const int4* cB = s_cB[l];
     const bool lastl = kExt && l + 1 == a.L && a.subA;
     const Screen sc{s_nA[l + 1], s_nB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
-                    a.trans & 3};
+                    a.trans & 3, lastl ? a.n16A : nullptr, lastl ? a.n16B : nullptr};
     const int32_t rlo = kExt ? a.row_lo : 0, rhi = kExt ? a.row_hi : INT32_MAX;
     // 1. child-task counts per (task, C child), group-major
     for (int p = tid; p < F; p += kT) {
@@ -397,6 +403,8 @@ struct LargeBfsArgs {
   int32_t row_lo, row_hi;        // C row window (block rows)
   const uint8_t* subA;           // block size 16: quadrant masks (pair test at the block level)
   const uint8_t* subB;
+  const double* n16A;            // block size 16 + screening: squared 16-block norms, or null
+  const double* n16B;
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -463,7 +471,7 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
     const int mode = (a.trans & 7) | ((sym && l < (a.trans >> 8)) ? 8 : 0);
     const bool lastl = kExt && l + 1 == a.L && a.subA;
     const Screen sc{a.normA[l + 1], a.normB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
-                    a.trans & 3};
+                    a.trans & 3, lastl ? a.n16A : nullptr, lastl ? a.n16B : nullptr};
     const int32_t rlo = kExt ? a.row_lo : 0, rhi = kExt ? a.row_hi : INT32_MAX;
     const int32_t F = a.f_out[l], ns = a.ns_out[l];
     const int32_t* pa = a.pa[l];
@@ -813,6 +821,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       // (bs 16: container pairs whose quadrant masks never meet are pruned)
       sa.subA = A->ubs == 16 ? A->sub.as<uint8_t>() : nullptr;
       sa.subB = A->ubs == 16 ? B->sub.as<uint8_t>() : nullptr;
+      sa.n16A = A->ubs == 16 && screen ? A->norm16.as<double>() : nullptr;
+      sa.n16B = A->ubs == 16 && screen ? B->norm16.as<double>() : nullptr;
       for (int l = 0; l <= L && l < QT_MAX_LEVELS; ++l) {
         sa.normA[l] = screen ? A->norm2[l].as<double>() : nullptr;
         sa.normB[l] = screen ? B->norm2[l].as<double>() : nullptr;
@@ -926,6 +936,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         la.row_hi = row_hi;
         la.subA = sa.subA;
         la.subB = sa.subB;
+        la.n16A = sa.n16A;
+        la.n16B = sa.n16B;
         for (int l = 0; l < L && l < QT_MAX_LEVELS; ++l) {
           la.childA[l] = A->child[l].as<int4>();
           la.childB[l] = B->child[l].as<int4>();
@@ -1071,12 +1083,17 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       na.poolC = C->pool.p;
       na.counter = ctx->counters.as<int>() + 16;
       na.trans = trans & 7;  // bit 2: symmetric square (block refs carry transpose bits)
-      na.normA = screen ? A->norm2[L].as<double>() : nullptr;
-      na.normB = screen ? B->norm2[L].as<double>() : nullptr;
+      // (block size 16: the 16-block test replaces the container norms, below)
+      na.normA = screen && A->ubs != 16 ? A->norm2[L].as<double>() : nullptr;
+      na.normB = screen && A->ubs != 16 ? B->norm2[L].as<double>() : nullptr;
       na.tau2 = tau2;
-      if (A->ubs == 16 && !f32) {  // block size 16: only the 16-block products that exist
+      if (A->ubs == 16 && !f32) {  // block size 16: only the 16-block products that exist (and pass the screen)
         na.subA = A->sub.as<uint8_t>();
         na.subB = B->sub.as<uint8_t>();
+        if (screen) {
+          na.norm16A = A->norm16.as<double>();
+          na.norm16B = B->norm16.as<double>();
+        }
       }
       na.group = group;
       na.counter_ready = true;  // zeroed by the small BFS kernel
@@ -1174,7 +1191,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         int64_t r16[4];
         cmask16(ctx, ns[L - 1], cstart.as<int32_t>(), pa.as<int32_t>(), pb.as<int32_t>(), A->child[L - 1].as<int4>(),
                 B->child[L - 1].as<int4>(), cchild.as<int4>(), A->sub.as<uint8_t>(), B->sub.as<uint8_t>(), trans & 7,
-                C->key.as<uint64_t>(), C->sub.as<uint8_t>(), C->nb, r16);
+                C->key.as<uint64_t>(), C->sub.as<uint8_t>(), C->nb, r16, screen ? A->norm16.as<double>() : nullptr,
+                screen ? B->norm16.as<double>() : nullptr, tau2);
         tr.mark("cmask16");
         if (sym) symm_finish16(C);
         C->nb16 = r16[1];

@@ -458,6 +458,33 @@ __global__ void k_node_norm2(const int4* __restrict__ child, int64_t n, const do
     out[t] = s;
   }
 }
+// Block size 16: the squared norm of each present 16-block (row-major over its
+// 16 x 16 entries with separate roundings: the oracle's order, so screening
+// decisions agree), and the container's = the sum of its quadrants' — a sum of
+// non-negative terms is >= each term under rounding, so container and node
+// pruning stay exact with respect to the 16-block test.
+__global__ void k_quad_norm2(const double* __restrict__ pool, const uint8_t* __restrict__ sub, int64_t nb,
+                             double* __restrict__ out16, double* __restrict__ out32) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nb; t += (int64_t)gridDim.x * blockDim.x) {
+    const double* b = pool + t * 1024;
+    const int m = sub[t];
+    double tot = 0.0;
+    for (int q = 0; q < 4; ++q) {
+      double s = 0.0;
+      if ((m >> q) & 1) {
+        const int r0 = 16 * (q >> 1), c0 = 16 * (q & 1);
+        for (int r = 0; r < 16; ++r)
+          for (int c = 0; c < 16; ++c) {
+            const double v = b[swz64(r0 + r, c0 + c)];
+            s = __dadd_rn(s, __dmul_rn(v, v));
+          }
+      }
+      out16[4 * t + q] = s;
+      tot = __dadd_rn(tot, s);
+    }
+    out32[t] = tot;
+  }
+}
 }  // namespace
 
 void ensure_norms(qt_mat M) {
@@ -467,6 +494,10 @@ void ensure_norms(qt_mat M) {
   cudaStream_t st = ctx->stream;
   std::vector<DevBuf> nv(M->L + 1);
   nv[M->L].alloc(8 * std::max<int64_t>(M->nb, 1), st);
+  if (M->ubs == 16) {
+    if (M->dtype != QT_F64) fail(QT_EDTYPE, "16-block norms are computed on FP64 pools");
+    M->norm16.alloc(32 * std::max<int64_t>(M->nb, 1), st);
+  }
   // block norms indexed like the pool ids (a multi-rank B_ext: ids < split in
   // the local pool, the rest in the received payload)
   const int64_t n1 = std::min<int64_t>(M->nb, M->split), n2 = M->nb - n1;
@@ -476,7 +507,11 @@ void ensure_norms(qt_mat M) {
     if (n <= 0) continue;
     const void* src = part ? M->pool2 : p1;
     double* out = nv[M->L].as<double>() + (part ? n1 : 0);
-    if (M->dtype == QT_F64)
+    if (M->ubs == 16)
+      k_quad_norm2<<<grid_for(n), kThreads, 0, st>>>(static_cast<const double*>(src),
+                                                      M->sub.as<uint8_t>() + (part ? n1 : 0), n,
+                                                      M->norm16.as<double>() + 4 * (part ? n1 : 0), out);
+    else if (M->dtype == QT_F64)
       k_block_norm2_seq<double><<<grid_for(n), kThreads, 0, st>>>(static_cast<const double*>(src), n, out);
     else
       k_block_norm2_seq<float><<<grid_for(n), kThreads, 0, st>>>(static_cast<const float*>(src), n, out);
@@ -716,6 +751,56 @@ qt_mat select_blocks(qt_mat A, const uint8_t* d_keep) {
       k_compact_blocks<<<g, 256, 0, st>>>(d_keep, incl.as<int32_t>(), A->key.as<uint64_t>(),
                                           A->pool.as<uint4>(), n, vpb, M->key.as<uint64_t>(),
                                           M->pool.as<uint4>());
+      QT_LAUNCH_CHECK(ctx);
+    }
+    build_levels(M);
+  } catch (...) {
+    delete M;
+    throw;
+  }
+  return M;
+}
+
+// Pool conversion between the FP32 layout (swz32) and the FP64 layout (swz64),
+// element by element (float -> double is exact; double -> float rounds to
+// nearest).  One 32x32 block per CTA iteration.
+template <class Ti, class To>
+__global__ void k_convert_pool(const Ti* __restrict__ in, To* __restrict__ out, int64_t nb) {
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const Ti* src = in + b * 1024;
+    To* dst = out + b * 1024;
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+      const int r = i >> 5, c = i & 31;
+      dst[sizeof(To) == 8 ? swz64(r, c) : swz32(r, c)] = (To)src[sizeof(Ti) == 8 ? swz64(r, c) : swz32(r, c)];
+    }
+  }
+}
+
+qt_mat convert_dtype(qt_mat A, qt_dtype to) {
+  qt_ctx ctx = A->ctx;
+  cudaStream_t st = ctx->stream;
+  if (A->pool1 || A->split != INT64_MAX) fail(QT_ESTATE, "convert_dtype: a plain matrix is required");
+  qt_mat M = clone_params(A);
+  try {
+    M->dtype = to;
+    M->nb = A->nb;
+    M->nb16 = A->nb16;
+    M->global_nb = A->global_nb;
+    if (A->nb > 0) {
+      M->key.alloc(8 * A->nb, st);
+      QT_CUDA(cudaMemcpyAsync(M->key.p, A->key.p, 8 * A->nb, cudaMemcpyDeviceToDevice, st));
+      if (A->ubs == 16) {
+        M->sub.alloc(A->nb, st);
+        QT_CUDA(cudaMemcpyAsync(M->sub.p, A->sub.p, A->nb, cudaMemcpyDeviceToDevice, st));
+      }
+      M->pool.alloc((size_t)A->nb * 1024 * elem_size(to), st);
+      const unsigned g = (unsigned)std::min<int64_t>(A->nb, 148 * 8);
+      if (A->dtype == QT_F32 && to == QT_F64)
+        k_convert_pool<float, double><<<g, 256, 0, st>>>(A->pool.as<float>(), M->pool.as<double>(), A->nb);
+      else if (A->dtype == QT_F64 && to == QT_F32)
+        k_convert_pool<double, float><<<g, 256, 0, st>>>(A->pool.as<double>(), M->pool.as<float>(), A->nb);
+      else
+        fail(QT_EDTYPE, "convert_dtype: F32 <-> F64 only");
       QT_LAUNCH_CHECK(ctx);
     }
     build_levels(M);

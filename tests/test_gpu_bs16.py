@@ -375,3 +375,75 @@ def test_bs16_symm_square_loopback_two_ranks(qt, ctx):
         assert np.array_equal(r, full[0][m]) and np.array_equal(c, full[1][m]) and np.array_equal(v, full[2][m])
         assert pay == plan[g]["payload_bytes"]
         assert meta == plan[g]["meta_bytes"] + plan[g]["blocks_received"]
+
+
+# ----------------------------------------- norm-screened product at block size 16 (f4)
+
+
+def _taus16(Am, Bm):
+    na = np.sqrt(oracle.block_norm2(Am.vals.astype(np.float64)))
+    nb = np.sqrt(oracle.block_norm2(Bm.vals.astype(np.float64)))
+    prods = np.unique(np.outer(na, nb).ravel())
+    mids = (prods[1:] + prods[:-1]) / 2
+    return [0.0] + [float(mids[int(len(mids) * f)]) for f in (0.2, 0.5, 0.8)]
+
+
+def _screened_count(Am, Bm, tau):
+    """16-block products with ||A_IK||^2 ||B_KJ||^2 >= tau^2 (the oracle's test)."""
+    na2 = oracle.block_norm2(Am.vals.astype(np.float64))
+    nb2 = oracle.block_norm2(Bm.vals.astype(np.float64))
+    n = 0
+    by_row = {}
+    for q in range(Bm.nb):
+        by_row.setdefault(int(Bm.brow[q]), []).append(q)
+    for p in range(Am.nb):
+        for q in by_row.get(int(Am.bcol[p]), []):
+            n += na2[p] * nb2[q] >= tau * tau
+    return n
+
+
+@pytest.mark.parametrize("nbr,p,leaf", [(14, 0.5, 64), (38, 0.15, 128)])
+@pytest.mark.parametrize("kind,dtype", [("int", np.float64), ("uniform", np.float64), ("int", np.float32)])
+def test_bs16_screened_multiply(qt, ctx, nbr, p, leaf, kind, dtype):
+    """qt_multiply_screened at block size 16: each 16-block product is kept iff
+    ||A_IK||_F ||B_KJ||_F >= tau (16-block norms, squared and summed row-major
+    as the oracle does).  Pattern and values equal oracle.spgemm(tau=) at bs 16,
+    block_products equals the number of surviving 16-block products, and
+    ||C - C~||_F <= sum of the skipped products' norm bounds."""
+    rng = np.random.default_rng(500 + nbr + (kind == "int") + (dtype == np.float32))
+    Am = random_bm16(rng, nbr, p, kind, leaf, dtype)
+    Bm = random_bm16(rng, nbr, p, kind, leaf, dtype)
+    Am.vals *= rng.integers(1, 9, size=(Am.nb, 1, 1)).astype(dtype)     # varied 16-block norms
+    Bm.vals *= rng.integers(1, 9, size=(Bm.nb, 1, 1)).astype(dtype)
+    A, B = mk(qt, ctx, Am), mk(qt, ctx, Bm)
+    full = oracle.spgemm(nbr, 16, tup(Am), tup(Bm))
+    for tau in _taus16(Am, Bm):
+        C, st = A.multiply_screened(B, tau)
+        got = C.to_blocks()
+        ref = oracle.spgemm(nbr, 16, tup(Am), tup(Bm), tau=tau)
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+        if kind == "int":
+            assert np.array_equal(got[2].astype(np.float64), ref[2])
+        elif len(ref[0]):
+            assert np.linalg.norm(got[2] - ref[2]) <= REL_FRO_F64 * np.linalg.norm(ref[2])
+        assert st.block_products == _screened_count(Am, Bm, tau)
+        if tau == 0.0:
+            assert np.array_equal(got[0], full[0]) and np.array_equal(got[1], full[1])
+
+
+def test_bs16_screened_eslike_small(qt, ctx):
+    """Config 4's recipe (small) split into 16-blocks, screened at two taus:
+    uniform values within the FP64 gate of the oracle's screened product."""
+    c = qtgen.config(4, small=True)["A"]
+    # each 32-block -> four 16-blocks
+    br = np.repeat(2 * c.brow, 4) + np.tile([0, 0, 1, 1], c.nb)
+    bc = np.repeat(2 * c.bcol, 4) + np.tile([0, 1, 0, 1], c.nb)
+    v = c.vals.reshape(c.nb, 2, 16, 2, 16).transpose(0, 1, 3, 2, 4).reshape(4 * c.nb, 16, 16)
+    M = qtgen.BlockMatrix(c.n, c.leaf_dim, 16, br.astype(np.int32), bc.astype(np.int32), np.ascontiguousarray(v))
+    A = mk(qt, ctx, M)
+    for tau in [1e-3, 5e-2]:
+        C, st = A.multiply_screened(A, tau)
+        got = C.to_blocks()
+        ref = oracle.spgemm(M.nbr, 16, tup(M), tup(M), tau=tau)
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+        assert np.linalg.norm(got[2] - ref[2]) <= REL_FRO_F64 * np.linalg.norm(ref[2])

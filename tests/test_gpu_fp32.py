@@ -236,3 +236,35 @@ def test_fp32_symm_square_cfg5_small(qt, ctx):
     got = C.to_blocks()
     ref = oracle.symm_square(full.nbr, 32, ref64(U))
     check(got, ref, "uniform")
+
+
+# ----------------------------------------- norm-screened product in FP32 (f4; reading C-29)
+
+
+@pytest.mark.parametrize("kind", ["int", "uniform"])
+def test_fp32_screened_multiply(qt, ctx, kind):
+    """FP32 screened product: the FP64 screened multiply of the (exactly
+    converted) FP32 values, C rounded to FP32.  Pattern = oracle.spgemm(tau=)
+    on the same values; integers bit-exact, uniform within 1e-5."""
+    rng = np.random.default_rng(71 + (kind == "int"))
+    nbr = 24
+    mats = []
+    for _ in range(2):
+        m = rng.random((nbr, nbr)) < 0.3
+        br, bc = np.nonzero(m)
+        v = (rng.integers(-4, 5, size=(len(br), 32, 32)) if kind == "int"
+             else rng.uniform(-1, 1, size=(len(br), 32, 32)))
+        v = v * rng.integers(1, 9, size=(len(br), 1, 1))
+        mats.append(qtgen.BlockMatrix(nbr * 32, 128, 32, br.astype(np.int32), bc.astype(np.int32),
+                                      v.astype(np.float32)))
+    Am, Bm = mats
+    A, B = mk(qt, ctx, Am), mk(qt, ctx, Bm)
+    na = np.sqrt(oracle.block_norm2(Am.vals.astype(np.float64)))
+    nb = np.sqrt(oracle.block_norm2(Bm.vals.astype(np.float64)))
+    prods = np.unique(np.outer(na, nb).ravel())
+    mids = (prods[1:] + prods[:-1]) / 2
+    for tau in [0.0, float(mids[len(mids) // 3]), float(mids[2 * len(mids) // 3])]:
+        C, st = A.multiply_screened(B, tau)
+        got = C.to_blocks()
+        ref = oracle.spgemm(nbr, 32, ref64(Am), ref64(Bm), tau=tau)
+        check(got, ref, kind)

@@ -96,9 +96,9 @@ def test_fuzz_symm_screen_truncate_virtual(qt, ctx, seed):
     A = mk(qt, ctx, M)
     full = (A @ A).to_blocks()
     same(full, oracle.spgemm(nbr, 32, t64(M), t64(M)))
+    tau = float(rng.choice([0.0, 50.0, 400.0]))   # (FP32: screened on FP64 copies, reading C-29)
+    same(A.multiply_screened(A, tau)[0].to_blocks(), oracle.spgemm(nbr, 32, t64(M), t64(M), tau=tau))
     if dtype == np.float64:
-        tau = float(rng.choice([0.0, 50.0, 400.0]))
-        same(A.multiply_screened(A, tau)[0].to_blocks(), oracle.spgemm(nbr, 32, t64(M), t64(M), tau=tau))
         tt = float(rng.choice([0.0, 100.0, 1000.0]))
         r, c, v = A.truncate(tt).to_blocks()
         rr, rc, rv = oracle.truncate(M.brow, M.bcol, M.vals, tt)

@@ -520,9 +520,13 @@ def _separating_taus(a, b):
     return [float(mids[len(mids) // 4]), float(mids[len(mids) // 2]), float(mids[3 * len(mids) // 4])]
 
 
-def test_screened_product_vs_bruteforce_enumeration():
-    rng = np.random.default_rng(41)
-    nbr, bs = 8, 4
+@pytest.mark.parametrize("bs", [4, 16])
+def test_screened_product_vs_bruteforce_enumeration(bs):
+    """The screened product (f4) at block sizes 4 and 16 (the paper's S^2 runs
+    screen at block size 16) equals the brute-force enumeration
+    of the block products that pass ||A_IK|| ||B_KJ|| >= tau."""
+    rng = np.random.default_rng(41 + bs)
+    nbr = 8
     a = _scaled_int_matrix(rng, nbr, bs, 0.5)
     b = _scaled_int_matrix(rng, nbr, bs, 0.5)
     na = np.sqrt((a[2] ** 2).sum(axis=(1, 2)))
