@@ -235,7 +235,9 @@ qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st);
  * Errors: QT_EINVAL, QT_ENOMEM, QT_ECUDA, QT_ENCCL. */
 qt_status qt_truncate(qt_mat A, double tau, qt_mat* out);
 
-/* Describe a matrix.  Any output pointer may be NULL.  local_nblocks: blocks
+/* Describe a matrix (the matrix-parameters chunk of §3.1: dimension,
+ * leaf dimension, block size; plus this rank's block counts and rows).  Any
+ * output pointer may be NULL.  local_nblocks: blocks
  * held by this rank; global_nblocks: over all ranks for created and truncated
  * matrices — for the product of a multi-rank multiply it is the local count
  * (summing would cost the multiply a collective; qt_gather's `total` gives
@@ -249,7 +251,8 @@ qt_status qt_info(qt_mat A, int64_t* n, int32_t* leaf_dim, int32_t* block_size,
 qt_status qt_level_nodes(qt_mat A, int64_t* counts, int32_t cap, int32_t* nlevels);
 
 /* Copy this rank's blocks out, sorted by (brow, bcol), values row-major per
- * block.  brow/bcol: local_nblocks int32 each; values: local_nblocks*bs*bs
+ * block — the to_triplets read-back of SPEC S:149-157 at block granularity
+ * (a block list instead of element triplets).  brow/bcol: local_nblocks int32 each; values: local_nblocks*bs*bs
  * elements of the matrix dtype.  Host or device pointers; any may be NULL
  * to skip it.  Synchronises the stream before returning.
  * Errors: QT_EINVAL, QT_ECUDA. */
@@ -319,7 +322,9 @@ qt_status qt_update_values(qt_mat A, const void* values);
  * qt_read_back_async, and release their staging buffers.  Errors: QT_ECUDA. */
 qt_status qt_ctx_synchronize(qt_ctx ctx);
 
-/* Release a matrix (stream-ordered; safe right after the last use). */
+/* Release a matrix (stream-ordered; safe right after the last use).  The
+ * paper's chunks are deleted by their owner when no longer referenced
+ * (single assignment: a handle is never modified, only freed). */
 qt_status qt_destroy(qt_mat A);
 
 /* Message of the last failure on this thread ("" if none). */

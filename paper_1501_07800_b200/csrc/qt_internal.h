@@ -164,6 +164,11 @@ struct qt_mat_s {
   // (symm_prepare16), made on the first call and kept (values never change
   // in place at bs 16: qt_update_values is bs 32 only)
   std::unique_ptr<qt_mat_s> sym16;
+  // symmetric square: U^T's block pool (blocks read transposed), made on the
+  // first call and kept with the immutable handle; poolT_src = the pool it was
+  // made from (qt_update_values drops it)
+  qt::DevBuf poolT_cache;
+  const void* poolT_src = nullptr;
   // B_ext of a multi-rank multiply: pool1 overrides pool.p (a borrowed view of
   // the local pool); block ids >= split live in pool2 (the received blocks).
   const void* pool1 = nullptr;

@@ -1098,14 +1098,32 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       na.group = group;
       na.counter_ready = true;  // zeroed by the small BFS kernel
       if (syncfree) na.ntiles_dev = nsd + (L - 1);  // the actual tile count (na.ntiles: its bound)
-      DevBuf poolT;  // symmetric square: blocks of U read transposed come from U^T's copy
+      // symmetric square: blocks of U read transposed come from U^T's copy —
+      // kept with U (handles are immutable) except for plans, whose execute
+      // refreshes its own copy from U's current values
+      DevBuf poolT;
+      const void* poolTp = nullptr;
       if (C->nb > 0 && sym) {
-        poolT.alloc((size_t)A->nb * 1024 * elem_size(C->dtype), st);
-        if (f32)
-          launch_transpose_blocks_f32(ctx, A->pool_ptr(), poolT.p, A->nb);
-        else
-          launch_transpose_blocks(ctx, A->pool_ptr(), poolT.p, A->nb);
-        na.poolT = poolT.p;
+        const size_t tb = (size_t)A->nb * 1024 * elem_size(C->dtype);
+        auto transpose_into = [&](void* dst) {
+          if (f32)
+            launch_transpose_blocks_f32(ctx, A->pool_ptr(), dst, A->nb);
+          else
+            launch_transpose_blocks(ctx, A->pool_ptr(), dst, A->nb);
+        };
+        if (plan) {
+          poolT.alloc(tb, st);
+          transpose_into(poolT.p);
+          poolTp = poolT.p;
+        } else {
+          if (!A->poolT_cache.p || A->poolT_src != A->pool_ptr()) {
+            A->poolT_cache.alloc(tb, st);
+            transpose_into(A->poolT_cache.p);
+            A->poolT_src = A->pool_ptr();
+          }
+          poolTp = A->poolT_cache.p;
+        }
+        na.poolT = poolTp;
       }
       // phase launches: the local-only tiles on the ctx stream now, the rest
       // on ov->s2 behind the payload; the ctx stream joins s2 afterwards.
@@ -1153,7 +1171,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         nb.counter = ctx->counters.as<int>() + 16;
         nb.counter_ready = true;
         nb.trans = trans & 7;
-        nb.poolT = poolT.p;
+        nb.poolT = poolTp;
         if (two_phase)
           phases(nb, [&](const NumericArgs32& x) { launch_numeric_f32(ctx, x); });
         else
@@ -1230,7 +1248,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
           nb.zeros = ctx->zeros.p;
           nb.counter = ctx->counters.as<int>() + 16;
           nb.trans = trans & 7;
-          nb.poolT = poolT.p;
+          nb.poolT = poolTp;
           nb.counter_ready = false;  // re-executions zero the counter themselves
           plan->nb = nb;
           plan->keep[0] = std::move(t2_cstart);

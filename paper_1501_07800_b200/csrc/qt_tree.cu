@@ -703,7 +703,10 @@ void update_values(qt_mat M, const void* values) {
   else
     k_fill_pool<float><<<g, 256, 0, st>>>((const float*)src, M->rm_inv.as<int32_t>(), nb, M->pool.as<float>());
   QT_LAUNCH_CHECK(ctx);
-  M->norm2.clear();  // (screening norms follow the values)
+  M->norm2.clear();  // (screening norms and U^T's cached pool follow the values)
+  M->norm16.release();
+  M->poolT_cache.release();
+  M->poolT_src = nullptr;
   if (!is_device_ptr(values)) QT_CUDA(cudaStreamSynchronize(st));  // the host buffer may be reused on return
 }
 
