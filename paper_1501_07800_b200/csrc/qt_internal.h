@@ -313,6 +313,7 @@ struct NumericArgs {
   // upper bound used for the launch shape only)
   const int32_t* ntiles_dev = nullptr;
   bool counter_ready = false;  // the scheduler counter is already zero (no memset before the launch)
+  unsigned long long* prof = nullptr;  // QT_NUM_PROF diagnostics (instrumented instantiation only)
 };
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a);
 void launch_transpose_blocks(qt_ctx ctx, const void* in, void* out, int64_t nb);

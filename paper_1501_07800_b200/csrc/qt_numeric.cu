@@ -306,8 +306,10 @@ __device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, int keep
   return d;
 }
 
-template <bool kTA, bool kTB, bool kSym, int kScreen, bool kPhase>
+template <bool kTA, bool kTB, bool kSym, int kScreen, bool kPhase, bool kProf = false, bool kMerge = false>
 __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
+  // kProf (QT_NUM_PROF=1, diagnostics): per-warp clock64 sums of where the time goes
+  unsigned long long pf[5] = {0, 0, 0, 0, 0};
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // warps [0, 4*kStreams): consumers, stream = warp / 4 ; then one producer per stream
@@ -332,6 +334,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
 
   if (producer) {
     // ------------------------------------------------------------ producer
+    const long long pf_t0 = kProf ? clock64() : 0;
     // Work is taken in groups of a.group consecutive tiles (one atomic per
     // group; for groups > 1 the next group's atomic is issued before the
     // current group is streamed, so its latency is hidden).  The tasks of a
@@ -461,12 +464,14 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
     int hpos = 0;                  // posted % kHdrPer
     // wait until a header and n slots are free (consumers release steps in order)
     auto reserve = [&](int n) {
+      const long long t0 = kProf ? clock64() : 0;
       while (posted - released >= kHdrPer || head + n - freed > kSlotsPer) {
         const int ri = released % kHdrPer;
         mbar_wait(&empty[ri], (released / kHdrPer) & 1);
         freed = *reinterpret_cast<volatile int*>(&hdr[ri].slot_end);
         ++released;
       }
+      if (kProf) pf[0] += clock64() - t0;
     };
     auto post = [&](int flags, int4 cc) {
       adv();
@@ -484,6 +489,29 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
       __syncwarp();
       ++posted;
       if (++hpos == kHdrPer) hpos = 0;
+    };
+    // A completed tile's STORE rides on the next compute step's header (the
+    // consumers store, then compute): one header and barrier round trip less
+    // per tile — sparse patterns post about as many tiles as steps.  A tile
+    // with no C block posts nothing unless a step accumulated into it (the
+    // symmetric square's (1,0) products of a diagonal tile are computed and
+    // discarded: the STORE still clears the accumulators).
+    bool pend = false, dirty = false;
+    int4 pend_cc = make_int4(-1, -1, -1, -1);
+    // (kMerge: the instantiation for grouped grabs = sparse tiles only; the
+    // dense-tile instantiation keeps the separate STORE headers)
+    const bool merge = kMerge;
+    auto defer_store = [&](int4 cc) {
+      if (cc.x < 0 && cc.y < 0 && cc.z < 0 && cc.w < 0 && !dirty) return;
+      if (pend) post(F_STORE, pend_cc);
+      if (!merge) {
+        post(F_STORE, cc);
+        dirty = false;
+        return;
+      }
+      pend = true;
+      pend_cc = cc;
+      dirty = false;
     };
     const double* poolT = static_cast<const double*>(a.poolT);
     auto asrc = [&](int la, int t) {
@@ -524,7 +552,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
       for (int u = 0; u < c_nloc; ++u) {
         if (last && n_state == 0 && g_pend - (c_pb0 + u) <= kGrabAhead) grab();
         while (c_pb0 + u >= boundary) {  // tile `cur` is complete
-          post(F_STORE, shfl_int4(g_cc, cur));
+          defer_store(shfl_int4(g_cc, cur));
           ++cur;
           boundary = __shfl_sync(0xffffffffu, g_ts, cur + 1);
         }
@@ -538,9 +566,16 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
           const int lb0 = __shfl_sync(0xffffffffu, d.b0, u);
           const int lb1 = __shfl_sync(0xffffffffu, d.b1, u);
           const int sub = kScreen >= 2 ? __shfl_sync(0xffffffffu, d.sub, u) : 0;
+          long long ta = kProf ? clock64() : 0;
           adv();
+          if (kProf) {
+            const long long t1 = clock64();
+            pf[1] += t1 - ta;
+            ta = t1;
+          }
           const int n = (la0 >= 0) + (la1 >= 0) + (lb0 >= 0) + (lb1 >= 0);
           reserve(n);
+          if (kProf) ta = clock64();
           if (lane == 0) {
             StageHdr& h = hdr[hpos];
             int sp = slot_pos;
@@ -555,7 +590,13 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
             h.a[1] = s1;
             h.b[0] = s2;
             h.b[1] = s3;
-            h.flags = F_COMPUTE;
+            h.flags = pend ? F_COMPUTE | F_STORE : F_COMPUTE;
+            if (pend) {
+              h.c[0] = pend_cc.x;
+              h.c[1] = pend_cc.y;
+              h.c[2] = pend_cc.z;
+              h.c[3] = pend_cc.w;
+            }
             h.sub = sub;
             h.pmask = meta & 15;
             h.slot_end = head + n;
@@ -571,6 +612,9 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
             if (s3 >= 0) bulk_g2s(data + s3 * kBlockElems, kSym ? asrc(lb1, tb & 8) : bsrc(lb1), kBlockBytes, fb);
           }
           __syncwarp();
+          pend = false;
+          dirty = true;
+          if (kProf) pf[2] += clock64() - ta;
           head += n;
           slot_pos += n;
           if (slot_pos >= kSlotsPer) slot_pos -= kSlotsPer;
@@ -579,12 +623,24 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         }
       }
       if (last) {
-        for (; cur < g_n; ++cur) post(F_STORE, shfl_int4(g_cc, cur));
+        for (; cur < g_n; ++cur) defer_store(shfl_int4(g_cc, cur));
         if (n_state == 0) grab();
       }
+      const long long tz = kProf ? clock64() : 0;
       while (n_state < 5) adv();
+      if (kProf) pf[3] += clock64() - tz;
     }
+    if (pend) post(F_STORE, pend_cc);
     post(F_DONE, make_int4(-1, -1, -1, -1));
+    if (kProf && lane == 0) {
+      atomicAdd(a.prof + 4, pf[0]);          // producer: waiting for ring space
+      atomicAdd(a.prof + 6, (unsigned long long)(clock64() - pf_t0));
+      atomicAdd(a.prof + 7, (unsigned long long)posted);
+      atomicAdd(a.prof + 9, 1ull);
+      atomicAdd(a.prof + 11, pf[1]);  // adv() of compute posts
+      atomicAdd(a.prof + 12, pf[2]);  // lane-0 header + TMA issue
+      atomicAdd(a.prof + 13, pf[3]);  // end-of-batch metadata completion
+    }
   } else {
     // ------------------------------------------------------------ consumers
     const int q = warp % kConsumerWarps;
@@ -600,17 +656,26 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
     const int g = lane >> 2, t4 = lane & 3;
     int hi = 0;
     uint32_t phase = 0;
+    const long long c_t0 = kProf ? clock64() : 0;
     for (;;) {
+      long long tw = kProf ? clock64() : 0;
       mbar_wait(&full[hi], phase);
+      if (kProf) {
+        const long long t1 = clock64();
+        pf[0] += t1 - tw;
+        tw = t1;
+      }
       const StageHdr& h = hdr[hi];
       const int flags = h.flags;
       if (flags & F_DONE) break;
-      if (flags & F_STORE) {
+      if (flags & F_STORE) {  // the tile that just ended (possibly before this header's compute step)
         int cb[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) cb[p] = h.c[p];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[hi]);
+        if (!kMerge || !(flags & F_COMPUTE)) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[hi]);
+        }
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
           if (cb[p] >= 0) {
@@ -629,7 +694,13 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
 #pragma unroll
             for (int n = 0; n < 2; ++n) acc[p][m][n][0] = acc[p][m][n][1] = 0.0;
         }
-      } else {
+        if (kProf) {
+          const long long t1 = clock64();
+          pf[2] += t1 - tw;
+          tw = t1;
+        }
+      }
+      if (kMerge ? (flags & F_COMPUTE) : !(flags & F_STORE)) {
         const int pm = h.pmask;
         const double* A0 = data + h.a[0] * kBlockElems;
         const double* A1 = data + h.a[1] * kBlockElems;
@@ -655,11 +726,23 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[hi]);
+        if (kProf) {
+          pf[1] += clock64() - tw;
+          pf[3] += 1;
+        }
       }
       if (++hi == kHdrPer) {
         hi = 0;
         phase ^= 1;
       }
+    }
+    if (kProf && lane == 0) {
+      atomicAdd(a.prof + 0, pf[0]);  // consumers: waiting for staged data
+      atomicAdd(a.prof + 1, pf[1]);  // compute steps (issue of fragment loads + DMMAs)
+      atomicAdd(a.prof + 2, pf[2]);  // tile epilogues (C stores)
+      atomicAdd(a.prof + 3, pf[3]);  // compute steps
+      atomicAdd(a.prof + 8, (unsigned long long)(clock64() - c_t0));
+      atomicAdd(a.prof + 10, 1ull);
     }
   }
 }
@@ -721,18 +804,45 @@ __global__ void k_peak_dfma(double* out, int iters) {
 
 }  // namespace
 
-template <bool TA, bool TB, bool SYM = false, int SCR = 0, bool PH = false>
+template <bool TA, bool TB, bool SYM = false, int SCR = 0, bool PH = false, bool MG = false>
 static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
+  static const bool prof = getenv("QT_NUM_PROF") != nullptr;
+  if (prof && !TA && !TB && !SYM && SCR == 0 && !PH) {  // diagnostics: the instrumented plain kernel
+    static bool set = false;
+    if (!set) {
+      QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<false, false, false, 0, false, true, MG>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+      set = true;
+    }
+    cudaStream_t st = a.stream ? a.stream : ctx->stream;
+    DevBuf pb(16 * 8, st);
+    QT_CUDA(cudaMemsetAsync(pb.p, 0, 16 * 8, st));
+    NumericArgs b = a;
+    b.prof = pb.as<unsigned long long>();
+    k_numeric_f64<false, false, false, 0, false, true, MG><<<grid, kNumThreads, kSmemBytes, st>>>(b);
+    unsigned long long h[16];
+    QT_CUDA(cudaMemcpyAsync(h, pb.p, 16 * 8, cudaMemcpyDeviceToHost, st));
+    QT_CUDA(cudaStreamSynchronize(st));
+    const double nc = (double)h[10], np = (double)h[9];
+    fprintf(stderr,
+            "[qt numeric prof] consumer warps %.0f: total %.0f cyc, wait-data %.0f, compute %.0f, store %.0f, "
+            "steps %.1f | producers %.0f: total %.0f, wait-ring %.0f, posts %.1f, adv %.0f, issue %.0f, "
+            "batch-end %.0f\n",
+            nc, h[8] / nc, h[0] / nc, h[1] / nc, h[2] / nc, h[3] / nc, np, h[6] / np, h[4] / np, h[7] / np,
+            h[11] / np, h[12] / np, h[13] / np);
+    return;
+  }
   // the dynamic shared memory limit is a per-device function attribute: set
   // it once per device (bit d of `attr_set`; concurrent first calls only
   // repeat an idempotent call)
   static std::atomic<unsigned long long> attr_set{0};
   const unsigned long long bit = 1ull << (ctx->device & 63);
   if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<TA, TB, SYM, SCR, PH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<TA, TB, SYM, SCR, PH, false, MG>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
     attr_set.fetch_or(bit, std::memory_order_release);
   }
-  k_numeric_f64<TA, TB, SYM, SCR, PH><<<grid, kNumThreads, kSmemBytes, a.stream ? a.stream : ctx->stream>>>(a);
+  k_numeric_f64<TA, TB, SYM, SCR, PH, false, MG><<<grid, kNumThreads, kSmemBytes, a.stream ? a.stream : ctx->stream>>>(a);
 }
 
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
@@ -785,7 +895,12 @@ void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
     }
   } else {
     switch (a.trans & 3) {
-      case 0: launch_numeric_t<false, false>(ctx, a, grid); break;
+      case 0:  // (grouped grabs: the STORE-merging instantiation)
+        if (a.group > 1)
+          launch_numeric_t<false, false, false, 0, false, true>(ctx, a, grid);
+        else
+          launch_numeric_t<false, false>(ctx, a, grid);
+        break;
       case 1: launch_numeric_t<true, false>(ctx, a, grid); break;
       case 2: launch_numeric_t<false, true>(ctx, a, grid); break;
       default: launch_numeric_t<true, true>(ctx, a, grid); break;

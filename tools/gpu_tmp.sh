@@ -1,4 +1,2 @@
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2> gpurun_out/bench.err; echo "bench rc=$?"
-tail -c 7000 gpurun_out/bench.log; tail -3 gpurun_out/bench.err
-timeout 600 python tools/perf_configs.py 1 3 sym2 sym16 2>&1 | tail -4
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | grep -E "Error|assert|FAILED|passed|failed" | head -30
+for c in 3 4; do QT_NUM_PROF=1 timeout 300 python tools/perf_configs.py $c 2>&1 | grep "numeric prof" | tail -1; done
