@@ -549,7 +549,14 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
       } else if (g_pend - c_pb0 <= kGrabAhead) {
         grab();
       }
-      for (int u = 0; u < c_nloc; ++u) {
+      const long long tu = kProf ? clock64() : 0;
+      // only the tasks with a product at one of their two steps (sparse
+      // patterns: about half of the level L-1 tasks have none); the tiles
+      // they pass are stored on the way
+      unsigned live = __ballot_sync(0xffffffffu, lane < c_nloc && ((c_d0.meta | c_d1.meta) & 15));
+      while (live) {
+        const int u = __ffs(live) - 1;
+        live &= live - 1;
         if (last && n_state == 0 && g_pend - (c_pb0 + u) <= kGrabAhead) grab();
         while (c_pb0 + u >= boundary) {  // tile `cur` is complete
           defer_store(shfl_int4(g_cc, cur));
@@ -622,6 +629,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
           if (++hpos == kHdrPer) hpos = 0;
         }
       }
+      if (kProf) pf[4] += clock64() - tu;
       if (last) {
         for (; cur < g_n; ++cur) defer_store(shfl_int4(g_cc, cur));
         if (n_state == 0) grab();
@@ -640,6 +648,7 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
       atomicAdd(a.prof + 11, pf[1]);  // adv() of compute posts
       atomicAdd(a.prof + 12, pf[2]);  // lane-0 header + TMA issue
       atomicAdd(a.prof + 13, pf[3]);  // end-of-batch metadata completion
+      atomicAdd(a.prof + 14, pf[4]);  // the task loop of the batches
     }
   } else {
     // ------------------------------------------------------------ consumers
@@ -827,9 +836,9 @@ static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
     fprintf(stderr,
             "[qt numeric prof] consumer warps %.0f: total %.0f cyc, wait-data %.0f, compute %.0f, store %.0f, "
             "steps %.1f | producers %.0f: total %.0f, wait-ring %.0f, posts %.1f, adv %.0f, issue %.0f, "
-            "batch-end %.0f\n",
+            "batch-end %.0f, task-loop %.0f\n",
             nc, h[8] / nc, h[0] / nc, h[1] / nc, h[2] / nc, h[3] / nc, np, h[6] / np, h[4] / np, h[7] / np,
-            h[11] / np, h[12] / np, h[13] / np);
+            h[11] / np, h[12] / np, h[13] / np, h[14] / np);
     return;
   }
   // the dynamic shared memory limit is a per-device function attribute: set

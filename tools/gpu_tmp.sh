@@ -1,2 +1,2 @@
 timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | grep -E "Error|assert|FAILED|passed|failed" | head -30
-for c in 3 4; do QT_NUM_PROF=1 timeout 300 python tools/perf_configs.py $c 2>&1 | grep "numeric prof" | tail -1; done
+QT_SWEEP_DT=f64 QT_SWEEP_BS=16,32 timeout 600 python tools/perf_configs.py leafsweep 2>&1 | tail -14 | cut -c1-200
