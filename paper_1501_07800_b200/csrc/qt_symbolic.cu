@@ -295,14 +295,20 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     }
     __syncthreads();
     mark();
-    // 2. exclusive scan in place
+    // 2. exclusive scan in place (kIt consecutive entries per thread: a level
+    // of F tasks takes 4F / (kT kIt) block scans, not 4F / kT)
+    constexpr int kIt = 8;
     int carry = 0;
-    for (int b0 = 0; b0 < 4 * F; b0 += kT) {
-      const int i = b0 + tid;
-      const int v = i < 4 * F ? off[i] : 0;
-      int ex, agg;
+    for (int b0 = 0; b0 < 4 * F; b0 += kT * kIt) {
+      const int i0 = b0 + tid * kIt;
+      int v[kIt], ex[kIt];
+#pragma unroll
+      for (int j = 0; j < kIt; ++j) v[j] = i0 + j < 4 * F ? off[i0 + j] : 0;
+      int agg;
       BS(tmp).ExclusiveSum(v, ex, agg);
-      if (i < 4 * F) off[i] = carry + ex;
+#pragma unroll
+      for (int j = 0; j < kIt; ++j)
+        if (i0 + j < 4 * F) off[i0 + j] = carry + ex[j];
       carry += agg;
       __syncthreads();
     }
@@ -310,24 +316,34 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     mark();
     // 3. new groups (non-empty (s,q)), their starts and keys
     int ncarry = 0;
-    for (int b0 = 0; b0 < 4 * ns; b0 += kT) {
-      const int x = b0 + tid;
-      int flag = 0, gst = 0;
-      if (x < 4 * ns) {
-        const int s = x >> 2, q = x & 3, c0 = cs[s], m = cs[s + 1] - c0;
-        const int lo = 4 * c0 + q * m, hi = lo + m;
-        gst = off[lo];
-        const int en = hi < 4 * F ? off[hi] : Fn;
-        flag = en > gst;
+    for (int b0 = 0; b0 < 4 * ns; b0 += kT * kIt) {
+      const int x0 = b0 + tid * kIt;
+      int flag[kIt], gst[kIt], ex[kIt];
+#pragma unroll
+      for (int j = 0; j < kIt; ++j) {
+        const int x = x0 + j;
+        flag[j] = 0;
+        gst[j] = 0;
+        if (x < 4 * ns) {
+          const int s = x >> 2, q = x & 3, c0 = cs[s], m = cs[s + 1] - c0;
+          const int lo = 4 * c0 + q * m, hi = lo + m;
+          gst[j] = off[lo];
+          const int en = hi < 4 * F ? off[hi] : Fn;
+          flag[j] = en > gst[j];
+        }
       }
-      int ex, agg;
+      int agg;
       BS(tmp).ExclusiveSum(flag, ex, agg);
-      if (x < 4 * ns) {
-        const int t = flag ? ncarry + ex : -1;
-        gidx[x] = t;
-        if (flag) {
-          csn[t] = gst;
-          ckn[t] = (ck[x >> 2] << 2) | (uint64_t)(x & 3);
+#pragma unroll
+      for (int j = 0; j < kIt; ++j) {
+        const int x = x0 + j;
+        if (x < 4 * ns) {
+          const int t = flag[j] ? ncarry + ex[j] : -1;
+          gidx[x] = t;
+          if (flag[j]) {
+            csn[t] = gst[j];
+            ckn[t] = (ck[x >> 2] << 2) | (uint64_t)(x & 3);
+          }
         }
       }
       ncarry += agg;
@@ -799,10 +815,14 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       // --- small levels in one CTA
       const bool f32 = C->dtype == QT_F32;
       int l_end = 0;
-      while (l_end < L - 1 && F[l_end + 1] <= kSmallMaxF) ++l_end;
+      // (block size 16: the container level's mask tests make the single-CTA
+      // kernel slower per task — 4096 measured best for it, 8192 for bs 32)
+      static const int64_t small_env = getenv("QT_SMALL_MAXF") ? atoll(getenv("QT_SMALL_MAXF")) : 0;
+      const int64_t small_max = small_env > 0 ? small_env : (A->ubs == 16 ? kSmallMaxF / 2 : kSmallMaxF);
+      while (l_end < L - 1 && F[l_end + 1] <= small_max) ++l_end;
       // every level small (FP64): the single-CTA kernel also runs the last
       // transition and no cooperative launch is needed
-      if (!f32 && l_end == L - 1 && F[L - 1] <= kSmallMaxF) l_end = L;
+      if (!f32 && l_end == L - 1 && F[L - 1] <= small_max) l_end = L;
       if (f32) l_end = std::min(l_end, L - 2);  // the FP32 tiles need the level L-2 queue
       int64_t maxF = 1, maxNS = 1, maxF4 = 1;
       for (int l = 0; l <= l_end; ++l) {
@@ -888,7 +908,9 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         unsigned long long h[64];
         QT_CUDA(cudaMemcpyAsync(h, profbuf.p, 64 * 8, cudaMemcpyDeviceToHost, st));
         QT_CUDA(cudaStreamSynchronize(st));
-        fprintf(stderr, "[qt bfs_small] l_end=%d tiny=%d marks(ns):", l_end, (int)tiny);
+        fprintf(stderr, "[qt bfs_small] l_end=%d tiny=%d F:", l_end, (int)tiny);
+        for (int l = 0; l <= l_end; ++l) fprintf(stderr, " %lld", (long long)F[l]);
+        fprintf(stderr, " marks(ns):");
         for (int i = 1; i < (int)h[63] && i < 40; ++i) fprintf(stderr, " %llu", h[i] - h[i - 1]);
         fprintf(stderr, "\n");
       }
