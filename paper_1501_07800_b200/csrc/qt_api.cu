@@ -493,6 +493,23 @@ qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
   API_CATCH
 }
 
+// Reading C-30: the FP32 kernel computes whole 4x4-block tiles (16 block
+// products per tile step, absent blocks as zeros); the FP64 kernel computes
+// only the products that exist, at ~1/5 of the FP32 kernel's dense rate.  With
+// steps <= 4 * (tasks at level L-2), the tile density is at least
+// products / (64 * tasks_{L-2}); below QT_F32_DENSITY (default 0.2 = the rate
+// ratio 35 / 178 TFLOP/s measured on B200) the FP64 path is faster.
+static bool fp32_prefers_fp64(qt_mat A, qt_mat B, int trans) {
+  if (A->L < 2 || (trans & 4)) return false;
+  const char* e = getenv("QT_F32_DENSITY");
+  const double thr = e ? atof(e) : 0.2;
+  if (thr <= 0) return false;
+  const std::vector<int64_t> F = level_task_bounds(A, B, trans);
+  const int L = A->L;
+  if (F[L] == 0 || F[L - 2] == 0) return false;
+  return (double)F[L] / (64.0 * (double)F[L - 2]) < thr;
+}
+
 qt_status qt_multiply(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st) {
   return qt_multiply_ex(A, B, 0, 0, C, st);
 }
@@ -521,7 +538,16 @@ qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, q
   memset(&S, 0, sizeof(S));
   QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   qt_mat R;
-  if (ctx->world == 1) {
+  if (ctx->world == 1 && A->dtype == QT_F32 && !ctx->async_multiply && fp32_prefers_fp64(A, B, trans)) {
+    // reading C-30: a sparse FP32 product whose 4x4-block tcgen05 tiles would
+    // be mostly empty runs on FP64 copies through the FP64 kernel (which
+    // skips absent blocks) and C is rounded to FP32
+    float ms_sym = 0, ms_num = 0;
+    R = multiply_local(f64_of(A), f64_of(B), &S, &ms_sym, &ms_num, trans, -1.0, nullptr, 0, INT32_MAX, nullptr,
+                       /*out_f32=*/true);
+    S.ms_symbolic = ms_sym;
+    S.ms_numeric = ms_num;
+  } else if (ctx->world == 1) {
     float ms_sym = 0, ms_num = 0;
     R = multiply_local(A, B, &S, &ms_sym, &ms_num, trans);
     S.ms_symbolic = ms_sym;
@@ -703,17 +729,10 @@ qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_sta
   // products, so the screened FP32 product runs on FP64 copies of A and B
   // (exact conversion) through the FP64 kernel and C is rounded to FP32 —
   // the oracle is the double product of the same FP32 values
-  std::unique_ptr<qt_mat_s> A64, B64;
   qt_mat a = A, b = B;
-  if (A->dtype == QT_F32) {
-    A64.reset(convert_dtype(A, QT_F64));
-    a = A64.get();
-    if (B == A) {
-      b = a;
-    } else {
-      B64.reset(convert_dtype(B, QT_F64));
-      b = B64.get();
-    }
+  if (A->dtype == QT_F32) {  // (the FP64 copies are kept with the handles)
+    a = f64_of(A);
+    b = f64_of(B);
   }
   qt_stats local;
   qt_stats& S = st ? *st : local;

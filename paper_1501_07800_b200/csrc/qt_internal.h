@@ -169,6 +169,9 @@ struct qt_mat_s {
   // made from (qt_update_values drops it)
   qt::DevBuf poolT_cache;
   const void* poolT_src = nullptr;
+  // FP32 matrix: its FP64 copy for the products that run on the FP64 kernel
+  // (readings C-29, C-30), made on first use and kept (qt_update_values drops it)
+  std::unique_ptr<qt_mat_s> f64_copy;
   // B_ext of a multi-rank multiply: pool1 overrides pool.p (a borrowed view of
   // the local pool); block ids >= split live in pool2 (the received blocks).
   const void* pool1 = nullptr;
@@ -244,6 +247,11 @@ qt_mat truncate(qt_mat A, double tau);
 qt_mat truncate_dist(qt_mat A, double tau);
 // the same matrix with its values converted to `to` (FP32 <-> FP64; plain matrices)
 qt_mat convert_dtype(qt_mat A, qt_dtype to);
+// an FP32 matrix's FP64 copy, kept with the handle
+inline qt_mat f64_of(qt_mat A) {
+  if (!A->f64_copy) A->f64_copy.reset(convert_dtype(A, QT_F64));
+  return A->f64_copy.get();
+}
 // copy `keep` flagged blocks (Morton order preserved) of A into a new matrix
 qt_mat select_blocks(qt_mat A, const uint8_t* d_keep);
 
@@ -264,9 +272,14 @@ struct Overlap {
 // [row_lo, row_hi): only C blocks in these block rows are computed (the BFS
 // prunes C nodes outside the window at every level).
 struct NumericPlan;
+// multiply tasks per level 0..L from the occupancy histograms (exact for
+// regular products, an upper bound for the symmetric square)
+std::vector<int64_t> level_task_bounds(qt_mat A, qt_mat B, int trans);
+// out_f32: FP64 operands, C stored as FP32 by the FP64 kernel's epilogue (the
+// FP32 products that run on the FP64 kernel, reading C-30)
 qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* st, float* ms_sym, float* ms_num, int trans = 0,
                       double tau = -1.0, Overlap* ov = nullptr, int32_t row_lo = 0,
-                      int32_t row_hi = INT32_MAX, NumericPlan* plan = nullptr);
+                      int32_t row_hi = INT32_MAX, NumericPlan* plan = nullptr, bool out_f32 = false);
 // Tiles (C nodes of one level with CSR task ranges `ts` over the task array
 // pb) partitioned on the device: map[0, *nsel) = the tiles whose B nodes hold
 // only block ids < splitB (Morton order), map[*nsel, ntiles) = the rest.
@@ -314,6 +327,7 @@ struct NumericArgs {
   const int32_t* ntiles_dev = nullptr;
   bool counter_ready = false;  // the scheduler counter is already zero (no memset before the launch)
   unsigned long long* prof = nullptr;  // QT_NUM_PROF diagnostics (instrumented instantiation only)
+  int out_f32 = 0;             // C pool is FP32 (swz32 layout): the epilogue rounds to nearest
 };
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a);
 void launch_transpose_blocks(qt_ctx ctx, const void* in, void* out, int64_t nb);

@@ -306,7 +306,8 @@ __device__ __forceinline__ StepDesc make_step(int4 A4, int4 B4, int kb, int keep
   return d;
 }
 
-template <bool kTA, bool kTB, bool kSym, int kScreen, bool kPhase, bool kProf = false, bool kMerge = false>
+template <bool kTA, bool kTB, bool kSym, int kScreen, bool kPhase, bool kProf = false, bool kMerge = false,
+          bool kOut32 = false>
 __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
   // kProf (QT_NUM_PROF=1, diagnostics): per-warp clock64 sums of where the time goes
   unsigned long long pf[5] = {0, 0, 0, 0, 0};
@@ -688,15 +689,27 @@ __global__ void __launch_bounds__(kNumThreads, 1) k_numeric_f64(NumericArgs a) {
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
           if (cb[p] >= 0) {
-            double* Cb = poolC + (size_t)cb[p] * kBlockElems;
+            if (kOut32) {  // FP32 C (reading C-30): round to nearest, the FP32 pool layout
+              float* Cb = reinterpret_cast<float*>(poolC) + (size_t)cb[p] * kBlockElems;
 #pragma unroll
-            for (int m = 0; m < 2; ++m)
+              for (int m = 0; m < 2; ++m)
 #pragma unroll
-              for (int n = 0; n < 2; ++n) {
-                const int r = 16 * qi + 8 * m + g, c = 16 * qj + 8 * n + 2 * t4;
-                *reinterpret_cast<double2*>(Cb + swz64(r, c)) =
-                    make_double2(acc[p][m][n][0], acc[p][m][n][1]);
-              }
+                for (int n = 0; n < 2; ++n) {
+                  const int r = 16 * qi + 8 * m + g, c = 16 * qj + 8 * n + 2 * t4;
+                  *reinterpret_cast<float2*>(Cb + swz32(r, c)) =
+                      make_float2(__double2float_rn(acc[p][m][n][0]), __double2float_rn(acc[p][m][n][1]));
+                }
+            } else {
+              double* Cb = poolC + (size_t)cb[p] * kBlockElems;
+#pragma unroll
+              for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int n = 0; n < 2; ++n) {
+                  const int r = 16 * qi + 8 * m + g, c = 16 * qj + 8 * n + 2 * t4;
+                  *reinterpret_cast<double2*>(Cb + swz64(r, c)) =
+                      make_double2(acc[p][m][n][0], acc[p][m][n][1]);
+                }
+            }
           }
 #pragma unroll
           for (int m = 0; m < 2; ++m)
@@ -813,10 +826,10 @@ __global__ void k_peak_dfma(double* out, int iters) {
 
 }  // namespace
 
-template <bool TA, bool TB, bool SYM = false, int SCR = 0, bool PH = false, bool MG = false>
+template <bool TA, bool TB, bool SYM = false, int SCR = 0, bool PH = false, bool MG = false, bool O32 = false>
 static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
   static const bool prof = getenv("QT_NUM_PROF") != nullptr;
-  if (prof && !TA && !TB && !SYM && SCR == 0 && !PH) {  // diagnostics: the instrumented plain kernel
+  if (prof && !TA && !TB && !SYM && SCR == 0 && !PH && !O32) {  // diagnostics: the instrumented plain kernel
     static bool set = false;
     if (!set) {
       QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<false, false, false, 0, false, true, MG>,
@@ -847,11 +860,12 @@ static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
   static std::atomic<unsigned long long> attr_set{0};
   const unsigned long long bit = 1ull << (ctx->device & 63);
   if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<TA, TB, SYM, SCR, PH, false, MG>,
+    QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<TA, TB, SYM, SCR, PH, false, MG, O32>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
     attr_set.fetch_or(bit, std::memory_order_release);
   }
-  k_numeric_f64<TA, TB, SYM, SCR, PH, false, MG><<<grid, kNumThreads, kSmemBytes, a.stream ? a.stream : ctx->stream>>>(a);
+  k_numeric_f64<TA, TB, SYM, SCR, PH, false, MG, O32>
+      <<<grid, kNumThreads, kSmemBytes, a.stream ? a.stream : ctx->stream>>>(a);
 }
 
 void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
@@ -870,7 +884,29 @@ void launch_numeric(qt_ctx ctx, qt_dtype dt, const NumericArgs& a0) {
   const int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
   // a.group: one tile per grab (dense/banded: finest dynamic balance) or
   // grouped grabs (sparse patterns: amortise the scheduler and metadata latency)
-  if (a.phase) {  // multi-rank overlap phases: plain (or bs-16 masked) products only
+  if (a.out_f32) {  // FP32 C from FP64 operands (reading C-30): plain products, any transposes
+    if (a.phase || (a.trans & 4) || a.normA || a.norm16A) fail(QT_EINVAL, "FP32 output: plain products only");
+    if (a.subA) {
+      switch (a.trans & 3) {
+        case 0: launch_numeric_t<false, false, false, 2, false, false, true>(ctx, a, grid); break;
+        case 1: launch_numeric_t<true, false, false, 2, false, false, true>(ctx, a, grid); break;
+        case 2: launch_numeric_t<false, true, false, 2, false, false, true>(ctx, a, grid); break;
+        default: launch_numeric_t<true, true, false, 2, false, false, true>(ctx, a, grid); break;
+      }
+    } else {
+      switch (a.trans & 3) {
+        case 0:
+          if (a.group > 1)
+            launch_numeric_t<false, false, false, 0, false, true, true>(ctx, a, grid);
+          else
+            launch_numeric_t<false, false, false, 0, false, false, true>(ctx, a, grid);
+          break;
+        case 1: launch_numeric_t<true, false, false, 0, false, false, true>(ctx, a, grid); break;
+        case 2: launch_numeric_t<false, true, false, 0, false, false, true>(ctx, a, grid); break;
+        default: launch_numeric_t<true, true, false, 0, false, false, true>(ctx, a, grid); break;
+      }
+    }
+  } else if (a.phase) {  // multi-rank overlap phases: plain (or bs-16 masked) products only
     if (a.trans & 7) fail(QT_EINVAL, "overlap phases are built for the plain product");
     if (a.subA && a.norm16A)
       launch_numeric_t<false, false, false, 3, true>(ctx, a, grid);

@@ -735,8 +735,37 @@ struct Trace {
   }
 };
 
+// Task counts per level from the host copies of the occupancy histograms (no
+// device work, no sync): exact for regular products, an upper bound for the
+// symmetric square (its actual counts come from the BFS).
+std::vector<int64_t> level_task_bounds(qt_mat A, qt_mat B, int trans) {
+  const int L = A->L;
+  const bool sym = trans & 4;
+  std::vector<int64_t> F(L + 1, 0);
+  if (A->nb == 0 || B->nb == 0) return F;
+  const int64_t H = 2ll << L;
+  const int32_t* hA = A->hist_host.data();
+  const int32_t* hB = B->hist_host.data();
+  for (int l = 0; l <= L; ++l) {
+    const int64_t base = (1ll << l) - 1, m = 1ll << l;
+    int64_t f = 0;
+    for (int64_t K = 0; K < m; ++K) {
+      if (sym) {
+        const int64_t c = (int64_t)hA[base + K] + hA[H + base + K];
+        f += c * c;
+      } else {
+        // cols(op(A)_l) . rows(op(B)_l); a transposed operand swaps its row/column histograms
+        f += (int64_t)hA[((trans & 1) ? 0 : H) + base + K] * (int64_t)hB[((trans & 2) ? H : 0) + base + K];
+      }
+    }
+    F[l] = f;
+  }
+  return F;
+}
+
 qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* ms_num, int trans,
-                      double tau, Overlap* ov, int32_t row_lo, int32_t row_hi, NumericPlan* plan) {
+                      double tau, Overlap* ov, int32_t row_lo, int32_t row_hi, NumericPlan* plan,
+                      bool out_f32) {
   const bool screen = tau >= 0.0;
   const double tau2 = tau * tau;
   if (screen) {
@@ -754,7 +783,9 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
   C->n = A->n;
   C->leaf_dim = A->leaf_dim;
   C->bs = A->bs;
-  C->dtype = A->dtype;
+  C->dtype = out_f32 ? QT_F32 : A->dtype;
+  if (out_f32 && (A->dtype != QT_F64 || (trans & 4) || ov || plan))
+    fail(QT_EINVAL, "FP32 output of the FP64 kernel: plain FP64 operands only");
   C->L = L;
   C->leaf_level = A->leaf_level;
   C->nbr = A->nbr;
@@ -772,28 +803,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
   S.leaf_level = A->leaf_level;
   try {
     QT_CUDA(cudaEventRecord(ctx->ev[2], st));
-    std::vector<int64_t> F(L + 1, 0);
+    std::vector<int64_t> F = level_task_bounds(A, B, trans);
     if (A->nb > 0 && B->nb > 0) {
-      // task counts per level from the host copies of the occupancy
-      // histograms (no device work, no sync): exact for regular products, an
-      // upper bound for the symmetric square (its actual counts come from the BFS)
-      const int64_t H = 2ll << L;
-      const int32_t* hA = A->hist_host.data();
-      const int32_t* hB = B->hist_host.data();
-      for (int l = 0; l <= L; ++l) {
-        const int64_t base = (1ll << l) - 1, m = 1ll << l;
-        int64_t f = 0;
-        for (int64_t K = 0; K < m; ++K) {
-          if (sym) {
-            const int64_t c = (int64_t)hA[base + K] + hA[H + base + K];
-            f += c * c;
-          } else {
-            // cols(op(A)_l) . rows(op(B)_l); a transposed operand swaps its row/column histograms
-            f += (int64_t)hA[((trans & 1) ? 0 : H) + base + K] * (int64_t)hB[((trans & 2) ? H : 0) + base + K];
-          }
-        }
-        F[l] = f;
-      }
       tr.mark("counts");
       for (int l = 0; l <= L; ++l)
         if (F[l] >= (1ll << 31) / 4) fail(QT_EINVAL, "level %d has %lld tasks (> 2^29)", l, (long long)F[l]);
@@ -813,7 +824,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       int32_t* nsd = cnt_dev.as<int32_t>();
       int32_t* fd = nsd + (L + 1);
       // --- small levels in one CTA
-      const bool f32 = C->dtype == QT_F32;
+      const bool f32 = A->dtype == QT_F32;  // the FP32 (tcgen05) kernel
       int l_end = 0;
       // (block size 16: the container level's mask tests make the single-CTA
       // kernel slower per task — 4096 measured best for it, 8192 for bs 32)
@@ -1119,6 +1130,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       }
       na.group = group;
       na.counter_ready = true;  // zeroed by the small BFS kernel
+      na.out_f32 = out_f32;
       if (syncfree) na.ntiles_dev = nsd + (L - 1);  // the actual tile count (na.ntiles: its bound)
       // symmetric square: blocks of U read transposed come from U^T's copy —
       // kept with U (handles are immutable) except for plans, whose execute
@@ -1168,9 +1180,9 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       };
       if (C->nb > 0 && !f32) {
         if (two_phase)
-          phases(na, [&](const NumericArgs& x) { launch_numeric(ctx, C->dtype, x); });
+          phases(na, [&](const NumericArgs& x) { launch_numeric(ctx, A->dtype, x); });
         else
-          launch_numeric(ctx, C->dtype, na);
+          launch_numeric(ctx, A->dtype, na);
       }
       if (C->nb > 0 && f32) {
         NumericArgs32 nb;

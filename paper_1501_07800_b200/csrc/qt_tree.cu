@@ -707,6 +707,7 @@ void update_values(qt_mat M, const void* values) {
   M->norm16.release();
   M->poolT_cache.release();
   M->poolT_src = nullptr;
+  M->f64_copy.reset();
   if (!is_device_ptr(values)) QT_CUDA(cudaStreamSynchronize(st));  // the host buffer may be reused on return
 }
 
@@ -806,7 +807,20 @@ qt_mat convert_dtype(qt_mat A, qt_dtype to) {
         fail(QT_EDTYPE, "convert_dtype: F32 <-> F64 only");
       QT_LAUNCH_CHECK(ctx);
     }
-    build_levels(M);
+    // the quadtree is the same: copy it (stream-ordered, no host sync) rather
+    // than rebuilding it; a fresh product's levels stay unbuilt
+    M->levels_built = A->levels_built;
+    if (A->levels_built) {
+      M->cnt = A->cnt;
+      M->hist_host = A->hist_host;
+      auto dup = [&](const DevBuf& src, DevBuf& dst) {
+        dst.alloc(src.bytes, st);
+        if (src.bytes) QT_CUDA(cudaMemcpyAsync(dst.p, src.p, src.bytes, cudaMemcpyDeviceToDevice, st));
+      };
+      dup(A->hist, M->hist);
+      M->child.resize(A->child.size());
+      for (size_t l = 0; l < A->child.size(); ++l) dup(A->child[l], M->child[l]);
+    }
   } catch (...) {
     delete M;
     throw;

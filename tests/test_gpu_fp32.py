@@ -88,7 +88,13 @@ def test_fp32_roundtrip_layout(qt, ctx):
 @pytest.mark.parametrize("nbr,p,leaf", [(1, 1.0, 32), (4, 1.0, 32), (5, 0.6, 64), (16, 0.3, 128),
                                         (37, 0.2, 256), (64, 0.05, 512)])
 @pytest.mark.parametrize("kind", ["int", "uniform"])
-def test_fp32_random_patterns(qt, ctx, nbr, p, leaf, kind):
+@pytest.mark.parametrize("route", ["tcgen05", "auto", "fp64"])
+def test_fp32_random_patterns(qt, ctx, monkeypatch, nbr, p, leaf, kind, route):
+    """FP32 products on the tcgen05 kernel (QT_F32_DENSITY=0), on the FP64
+    kernel over FP64 copies (reading C-30; QT_F32_DENSITY=2 forces it) and
+    with the library's density rule: all equal the oracle's double product of
+    the FP32 inputs (integers bit-exact, uniform within 1e-5)."""
+    monkeypatch.setenv("QT_F32_DENSITY", {"tcgen05": "0", "fp64": "2", "auto": "0.2"}[route])
     rng = np.random.default_rng(nbr * 11 + (kind == "int"))
     Am = random_bm(rng, nbr, p, kind, leaf)
     Bm = random_bm(rng, nbr, p, kind, leaf)
