@@ -275,6 +275,35 @@ def test_cfg2_counts_survey_p7_p8():
     assert len(pr) == 61888 and np.all(np.abs(pr - pc) <= 64)
 
 
+@pytest.mark.parametrize("P,total", [(2, 4212000), (4, 8538400), (8, 17191200)])
+def test_cfg5_products_survey_p7(P, total):
+    """Config 5 (N = 16384 P, half-bandwidth 1024 -> block band 32): the block
+    products of C = A·A over all ranks (SURVEY P-7), from the banded closed
+    form of the per-level counts on the padded quadtree."""
+    nbr = 512 * P
+    br, bc = qtgen.pattern_banded(nbr, qtgen.band_blocks(1024, 32))
+    L, _ = oracle.tree_levels(nbr * 32, 32, 2048)
+    got = oracle.level_task_counts(L, (br, bc), (br, bc))
+    assert got[-1] == total
+    # the paper's banded bound per level, 2^l (2 d_l + 1)^2 with d_l the band at level l (P:578-587)
+    for l, c in enumerate(got):
+        d_l = -(-32 // (1 << (L - l)))
+        assert c <= (1 << l) * (2 * d_l + 1) ** 2
+
+
+def test_cfg4_overlap_growth_survey_p14():
+    """Config 4 (3-D overlap pattern): task counts at least double from level
+    to level below the root (the paper's overlap-matrix argument, P:634-635;
+    SURVEY P-14), measured on the block pattern of the generator."""
+    pos = qtgen.es_geometry()
+    ar, ac, _ = qtgen.pattern_es(pos, 7.0)
+    L, leaf = oracle.tree_levels(len(pos) * 32, 32, 4096)
+    got = oracle.level_task_counts(L, (ar, ac), (ar, ac))
+    assert (L, leaf) == (12, 5) and got[0] == 1
+    assert all(got[l] >= 2 * got[l - 1] for l in range(1, L + 1)), got
+    assert 6.0e6 < got[-1] < 6.6e6          # ~6.3 M block products (C-15 reading)
+
+
 def _random_expectation(L, delta, l):
     # P:517-519 Eq. eq:no_of_mmul_tasks_at_level_random
     n_l = 4 ** (L - l)

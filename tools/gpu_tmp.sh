@@ -1,3 +1,4 @@
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | grep -E "Error|assert|FAILED|passed|failed" | head -20
-QT_SWEEP_DT=f32 QT_SWEEP_BS=16,32 timeout 600 python tools/perf_configs.py leafsweep 2>&1 | tail -14 | cut -c1-200
-timeout 300 python tools/perf_configs.py 2 3 5f32 2>&1 | tail -3 | cut -c1-200
+timeout 300 python tools/perf_configs.py 1 2 3 4 2>&1 | tail -4 | python -c "
+import sys,json
+for l in sys.stdin:
+    d=json.loads(l); print(d['config'][:20], d['ms_step'], d['ms_symbolic'], d['ms_numeric'])"
