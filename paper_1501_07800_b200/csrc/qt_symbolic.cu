@@ -391,7 +391,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
 //   C emit   the child tasks, slot by slot in (parent task, k) order (warp
 //            scans place them), written at their group's start
 // So the scans run over the 4·ns group slots, not the 4·F task slots, and a
-// level costs three barriers.  The launch replaces ~8 kernel launches + 2
+// level costs two grid barriers (A | B C |): phase C of a CTA only reads the
+// positions its own phase B computed.  The launch replaces ~8 kernel launches + 2
 // device scans per level (the large levels were host-launch bound).
 constexpr int kLargeThreads = 1024;
 constexpr int kLargeWarps = kLargeThreads / 32;
@@ -416,6 +417,7 @@ struct LargeBfsArgs {
   int32_t* ns_out;               // groups per level
   int32_t* f_out;                // tasks per level
   unsigned* bar;                 // grid barrier: arrival count (self-resetting), generation
+  unsigned long long* prof;      // QT_BFS_PROF: CTA 0's %globaltimer at each phase boundary, or null
   int32_t row_lo, row_hi;        // C row window (block rows)
   const uint8_t* subA;           // block size 16: quadrant masks (pair test at the block level)
   const uint8_t* subB;
@@ -496,9 +498,14 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
     const uint64_t* ck = a.ckey[l];
     const int4* cA = a.childA[l];
     const int4* cB = a.childB[l];
+    auto pmark = [&](int k) {
+      if (a.prof && blockIdx.x == 0 && threadIdx.x == 0 && l < 16) a.prof[8 * l + k] = gtimer();
+    };
+    pmark(0);
     // this CTA's groups: first task in [b F / G, (b+1) F / G)
     const int32_t g_lo = cta_lower_bound(cs, ns, (int64_t)F * blockIdx.x / gridDim.x);
     const int32_t g_hi = cta_lower_bound(cs, ns, (int64_t)F * (blockIdx.x + 1) / gridDim.x);
+    pmark(1);
     // child counts of task p per C child q (0 for the pruned lower child of a diagonal node)
     auto counts = [&](int32_t p, int32_t sgrp, int (&c)[4]) {
       child_counts(op_children(cA, pa[p], mode & 1, sym), op_children(cB, pb[p], mode & 2, sym), c, sc,
@@ -562,7 +569,9 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
         a.part[gridDim.x + blockIdx.x] = x1;
       }
     }
+    pmark(2);
     grid_sync(a.bar, gen);
+    pmark(3);
     // B. new groups: starts, keys, (s,q) -> group map
     int tpre, Fn, gpre, nsn;
     {
@@ -619,8 +628,13 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
       a.ns_out[l + 1] = nsn;
       a.f_out[l + 1] = Fn;
     }
+    pmark(4);
     if (last) break;
-    grid_sync(a.bar, gen);
+    // (no grid barrier here: phase C of this CTA reads only what its own
+    // phase B wrote — the positions and group ids of its own slots — and the
+    // level-l tasks; the barrier after C orders it before the next level's A)
+    __syncthreads();
+    pmark(5);
     // C. emit the child tasks of level l+1: slot (s,q) lists, for every parent
     // task in order, k = 0 then k = 1 (ascending global k inside the group)
     {
@@ -686,7 +700,9 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
         }
       }
     }
+    pmark(6);
     grid_sync(a.bar, gen);
+    pmark(7);
   }
 }
 
@@ -1004,12 +1020,33 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         la.ns_out = nsd;
         la.f_out = fd;
         la.bar = reinterpret_cast<unsigned*>(ctx->counters.as<int>() + 40);
+        DevBuf lprof;
+        la.prof = nullptr;
+        if (bfs_prof) {
+          lprof.alloc(8 * 128, st);
+          QT_CUDA(cudaMemsetAsync(lprof.p, 0, 8 * 128, st));
+          la.prof = lprof.as<unsigned long long>();
+        }
         void* kargs[] = {&la};
         QT_CUDA(cudaLaunchCooperativeKernel(ext ? (const void*)k_bfs_large<true> : (const void*)k_bfs_large<false>,
                                             dim3(G), dim3(kLargeThreads), kargs, 0,
                                             st));
         ctx->launches += 1;
         QT_LAUNCH_CHECK(ctx);
+        if (bfs_prof) {
+          unsigned long long h[128];
+          QT_CUDA(cudaMemcpyAsync(h, lprof.p, 8 * 128, cudaMemcpyDeviceToHost, st));
+          QT_CUDA(cudaStreamSynchronize(st));
+          fprintf(stderr, "[qt bfs_large] per level (F): lbound A sync B sync C sync (ns)\n");
+          for (int l = l_end; l < L && l < 16; ++l) {
+            const unsigned long long* m = h + 8 * l;
+            fprintf(stderr, "  l=%d (%lld):", l, (long long)F[l]);
+            for (int k = 1; k < 8; ++k)
+              if (m[k] && m[k - 1]) fprintf(stderr, " %llu", m[k] - m[k - 1]);
+            if (l + 1 < L && h[8 * (l + 1)] && m[7]) fprintf(stderr, " | next %llu", h[8 * (l + 1)] - m[7]);
+            fprintf(stderr, "\n");
+          }
+        }
         // hand the queues the numeric kernels consume over
         C->key = std::move(ckeyL);
         cchild = std::move(qgx[set(L - 1)]);

@@ -1,3 +1,4 @@
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | grep -E "Error|assert|FAILED|passed|failed" | head -20
 timeout 300 python tools/perf_configs.py 1 2 3 4 2>&1 | tail -4 | python -c "
 import sys,json
 for l in sys.stdin:
