@@ -3,7 +3,9 @@ sizes (ragged against the 2x2 / 4x4 tiles and the leaves), densities from
 empty to full, leaf sizes, block sizes 16/32/64, FP64/FP32, transposed
 operands, the symmetric square (block sizes 32 and 16), the screened product and virtual ranks —
 every result against the oracle on the same inputs (integer values: exact).
-A 2000-case sweep (QT_FUZZ_MUL=1200 QT_FUZZ_MISC=400 QT_FUZZ_NBR=80) passed."""
+A 2000-case sweep (QT_FUZZ_MUL=1200 QT_FUZZ_MISC=400 QT_FUZZ_NBR=80) passed in
+round 1; round 2 (FP32 products routed by tile density, bs-16 screening):
+1200 cases (QT_FUZZ_MUL=600 QT_FUZZ_MISC=150 QT_FUZZ_NBR=100) passed."""
 import os
 
 import numpy as np
@@ -163,3 +165,22 @@ def test_fuzz_plans(qt, ctx, seed):
                           (Bm.brow[ob], Bm.bcol[ob], vb.astype(np.float64)), ta, tb)
     same(C.to_blocks(), ref)
     plan.close()
+
+
+@pytest.mark.parametrize("seed", range(N_MISC))
+def test_fuzz_screened16(qt, ctx, seed):
+    """Norm-screened product at block size 16 (per 16-block product, reading
+    C-25), FP64 and FP32 (FP64 copies, C-29), random grids, densities and
+    thresholds, against the oracle's screened product at bs 16."""
+    rng = np.random.default_rng(8800 + seed)
+    dtype = np.float64 if seed % 2 else np.float32
+    nbr = 2 * int(rng.integers(1, 24))
+    p = float(rng.choice([0.05, 0.2, 0.5, 1.0]))
+    leaf = 32 * int(2 ** rng.integers(0, 3))
+    Am = rand_int_bm(rng, nbr, p, 16, leaf, dtype)
+    Bm = rand_int_bm(rng, nbr, p, 16, leaf, dtype)
+    Am.vals *= rng.integers(1, 9, size=(Am.nb, 1, 1)).astype(dtype)
+    tau = float(rng.choice([0.0, 60.0, 200.0, 600.0]))
+    A, B = mk(qt, ctx, Am), mk(qt, ctx, Bm)
+    C, st = A.multiply_screened(B, tau)
+    same(C.to_blocks(), oracle.spgemm(nbr, 16, t64(Am), t64(Bm), tau=tau))
