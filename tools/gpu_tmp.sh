@@ -1,3 +1,6 @@
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | grep -E "Error|assert|FAILED|passed|failed" | head -20
-QT_SWEEP_DT=f64 QT_SWEEP_BS=16 timeout 600 python tools/perf_configs.py leafsweep sym16 2>&1 | tail -8 | cut -c1-220
-timeout 300 python tools/perf_configs.py 2 3 2>&1 | tail -2 | cut -c1-200
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | grep -E "passed|failed"
+timeout 300 python tools/perf_configs.py 1 2 3 4 2>&1 | tail -4 | python -c "
+import sys,json
+for l in sys.stdin:
+    d=json.loads(l); print(d['config'][:20], d['ms_step'], d['ms_symbolic'], d['ms_numeric'])"
+QT_NUM_PROF=1 timeout 300 python tools/perf_configs.py 3 2>&1 | grep "numeric prof" | tail -1
