@@ -263,9 +263,14 @@ qt_status qt_read_back(qt_mat A, int32_t* brow, int32_t* bcol, void* values);
  * as soon as its blocks are allocated and the numeric kernel is enqueued on
  * the context stream, so the caller can already enqueue the next step (e.g.
  * qt_create from host, whose value copy runs on the context's H2D stream).
- * The st->ms_* timings are 0; everything else in st is filled.  A and B may
- * be destroyed right after the call (stream-ordered reuse).
- * Errors: as qt_multiply. */
+ * The st->ms_* timings are 0; everything else in st is filled, except for
+ * small products (C's pool sized by the symbolic pass's upper bound, at most
+ * QT_SYNCFREE_MB): these return without any host synchronisation — C's block
+ * count is not known yet, st->c_blocks is -1 and st->level_c_nodes 0 — and
+ * C's count is read when C is first used by any entry point (qt_info,
+ * qt_read_back, as an operand, ...), so back-to-back multiplies pipeline on
+ * the device.  A and B may be destroyed right after the call (stream-ordered
+ * reuse).  Errors: as qt_multiply. */
 qt_status qt_multiply_async(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st);
 
 /* Distributed read-back: collective over the context's ranks.

@@ -228,7 +228,21 @@ static int ilog2(int64_t x) {
   return r;
 }
 
+void resolve_pending(qt_mat M) {
+  qt_ctx ctx = M->ctx;
+  const int slot = M->pend_slot;
+  QT_CUDA(cudaEventSynchronize(ctx->pend_ev[slot]));
+  M->nb = ctx->pend_host[128 * slot + M->L];  // the BFS's group count at the block level
+  M->global_nb = user_nblocks(M);
+  if (ctx->pend_owner[slot] == M) ctx->pend_owner[slot] = nullptr;
+  M->pend_slot = -1;
+}
+
 }  // namespace qt
+
+qt_mat_s::~qt_mat_s() {
+  if (pend_slot >= 0 && ctx && ctx->pend_owner[pend_slot] == this) ctx->pend_owner[pend_slot] = nullptr;
+}
 
 using namespace qt;
 
@@ -274,7 +288,11 @@ static void ctx_create(int device, void* cuda_stream, int rank, int world, const
     c->zeros.alloc(8192, c->stream);
     QT_CUDA(cudaMemsetAsync(c->zeros.p, 0, 8192, c->stream));
     c->pinned_bytes = 1024;  // small D2H staging (the sync-free multiply's level counts)
-    QT_CUDA(cudaMallocHost(&c->pinned, c->pinned_bytes));
+    // (mapped: the BFS kernels write the level counts of sync-free products straight into it)
+    QT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->pend_host), sizeof(int32_t) * 128 * qt_ctx_s::kPendRing,
+                          cudaHostAllocMapped));
+    for (auto& e : c->pend_ev) QT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    QT_CUDA(cudaHostAlloc(&c->pinned, c->pinned_bytes, cudaHostAllocMapped));
     if (world > 1) {
       if (hub) dist_init_loopback(c, hub);
       else dist_init(c, uid);
@@ -363,6 +381,9 @@ qt_status qt_ctx_destroy(qt_ctx ctx) {
     }
   }
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->pend_host) cudaFreeHost(ctx->pend_host);
+  for (auto& e : ctx->pend_ev)
+    if (e) cudaEventDestroy(e);
   delete ctx;
   API_CATCH
 }
@@ -517,6 +538,8 @@ qt_status qt_multiply(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st) {
 qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, qt_mat* C,
                          qt_stats* st) {
   API_TRY
+  resolve(A);
+  resolve(B);
   if (!A || !B || !C) fail(QT_EINVAL, "NULL argument");
   *C = nullptr;
   if (A->ctx != B->ctx) fail(QT_ESTATE, "A and B belong to different contexts");
@@ -536,7 +559,7 @@ qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, q
   qt_stats local;
   qt_stats& S = st ? *st : local;
   memset(&S, 0, sizeof(S));
-  QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  if (!ctx->async_multiply) QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   qt_mat R;
   if (ctx->world == 1 && A->dtype == QT_F32 && !ctx->async_multiply && fp32_prefers_fp64(A, B, trans)) {
     // reading C-30: a sparse FP32 product whose 4x4-block tcgen05 tiles would
@@ -559,12 +582,10 @@ qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, q
     // the numeric kernel's completion event (already waited for) ends the call:
     // no second record + host round trip
     QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[4]));
-  } else {
+  } else if (!ctx->async_multiply) {
     QT_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
-    if (!ctx->async_multiply) {
-      QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
-      QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
-    }
+    QT_CUDA(cudaEventSynchronize(ctx->ev[1]));
+    QT_CUDA(cudaEventElapsedTime(&S.ms_total, ctx->ev[0], ctx->ev[1]));
   }
   R->global_nb = user_nblocks(R);
   user_stats(R, S);
@@ -583,6 +604,8 @@ struct qt_plan_s {
 qt_status qt_multiply_plan(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, qt_plan* plan, qt_mat* C,
                            qt_stats* st) {
   API_TRY
+  resolve(A);
+  resolve(B);
   if (!A || !B || !C || !plan) fail(QT_EINVAL, "NULL argument");
   *C = nullptr;
   *plan = nullptr;
@@ -626,6 +649,7 @@ qt_status qt_multiply_plan(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b,
 
 qt_status qt_symm_square_plan(qt_mat A, qt_plan* plan, qt_mat* C, qt_stats* st) {
   API_TRY
+  resolve(A);
   if (!A || !C || !plan) fail(QT_EINVAL, "NULL argument");
   *C = nullptr;
   *plan = nullptr;
@@ -692,6 +716,7 @@ qt_status qt_plan_destroy(qt_plan plan) {
 
 qt_status qt_update_values(qt_mat A, const void* values) {
   API_TRY
+  resolve(A);
   if (!A) fail(QT_EINVAL, "NULL matrix");
   if (A->ubs != 32) fail(QT_EBS, "qt_update_values is built for block_size 32");
   if (A->nb > 0 && !values) fail(QT_EINVAL, "NULL values");
@@ -713,6 +738,8 @@ qt_status qt_multiply_async(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st) {
 
 qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_stats* st) {
   API_TRY
+  resolve(A);
+  resolve(B);
   if (!A || !B || !C) fail(QT_EINVAL, "NULL argument");
   *C = nullptr;
   if (!(tau >= 0)) fail(QT_EINVAL, "tau must be >= 0");
@@ -762,6 +789,7 @@ qt_status qt_multiply_screened(qt_mat A, qt_mat B, double tau, qt_mat* C, qt_sta
 
 qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
   API_TRY
+  resolve(A);
   if (!A || !C) fail(QT_EINVAL, "NULL argument");
   *C = nullptr;
   qt_ctx ctx = A->ctx;
@@ -826,6 +854,7 @@ qt_status qt_symm_square(qt_mat A, qt_mat* C, qt_stats* st) {
 
 qt_status qt_truncate(qt_mat A, double tau, qt_mat* out) {
   API_TRY
+  resolve(A);
   if (!A || !out) fail(QT_EINVAL, "NULL argument");
   *out = nullptr;
   if (!(tau >= 0)) fail(QT_EINVAL, "tau must be >= 0");
@@ -846,6 +875,7 @@ qt_status qt_info(qt_mat A, int64_t* n, int32_t* leaf_dim, int32_t* block_size, 
                   int64_t* local_nblocks, int64_t* global_nblocks, int32_t* row_lo,
                   int32_t* row_hi) {
   API_TRY
+  resolve(A);
   if (!A) fail(QT_EINVAL, "NULL matrix");
   if (n) *n = A->n;
   if (leaf_dim) *leaf_dim = A->leaf_dim;
@@ -872,6 +902,7 @@ qt_status qt_level_nodes(qt_mat A, int64_t* counts, int32_t cap, int32_t* nlevel
 
 qt_status qt_read_back(qt_mat A, int32_t* brow, int32_t* bcol, void* values) {
   API_TRY
+  resolve(A);
   if (!A) fail(QT_EINVAL, "NULL matrix");
   QT_CUDA(cudaSetDevice(A->ctx->device));
   read_back(A, brow, bcol, values);
@@ -880,6 +911,7 @@ qt_status qt_read_back(qt_mat A, int32_t* brow, int32_t* bcol, void* values) {
 
 qt_status qt_gather(qt_mat A, int32_t root, int32_t* brow, int32_t* bcol, void* values, int64_t* total) {
   API_TRY
+  resolve(A);
   if (!A) fail(QT_EINVAL, "NULL matrix");
   qt_ctx ctx = A->ctx;
   if (root < 0 || root >= ctx->world) fail(QT_EINVAL, "root %d outside [0,%d)", root, ctx->world);
@@ -898,6 +930,7 @@ qt_status qt_gather(qt_mat A, int32_t root, int32_t* brow, int32_t* bcol, void* 
 
 qt_status qt_read_back_async(qt_mat A, int32_t* brow, int32_t* bcol, void* values) {
   API_TRY
+  resolve(A);
   if (!A) fail(QT_EINVAL, "NULL matrix");
   QT_CUDA(cudaSetDevice(A->ctx->device));
   read_back(A, brow, bcol, values, true);
@@ -1031,6 +1064,7 @@ qt_status qt_plan_strips(qt_ctx ctx, int64_t n, int32_t block_size, int32_t alig
 qt_status qt_symm_square_virtual(qt_mat A, int32_t P, int32_t g, const int32_t* row_bounds, qt_mat* C,
                                  qt_stats* st) {
   API_TRY
+  resolve(A);
   if (!A || !C || !row_bounds) fail(QT_EINVAL, "NULL argument");
   *C = nullptr;
   if (A->ctx->world != 1) fail(QT_ESTATE, "virtual ranks need a single-rank context");
@@ -1071,6 +1105,8 @@ qt_status qt_symm_square_virtual(qt_mat A, int32_t P, int32_t g, const int32_t* 
 qt_status qt_multiply_virtual(qt_mat A, qt_mat B, int32_t P, int32_t g, const int32_t* row_bounds,
                               qt_mat* C, qt_stats* st) {
   API_TRY
+  resolve(A);
+  resolve(B);
   if (!A || !B || !C || !row_bounds) fail(QT_EINVAL, "NULL argument");
   *C = nullptr;
   if (A->ctx != B->ctx) fail(QT_ESTATE, "A and B belong to different contexts");

@@ -127,6 +127,14 @@ struct qt_ctx_s {
   cudaStream_t comm_stream = nullptr;  // multi-rank: payload exchange + the remote tiles' numeric launch
   cudaEvent_t ov_ev[4] = {};           // overlap ordering (0, 1) and payload timing (2, 3)
   bool async_multiply = false;         // qt_multiply_async: no final synchronisation
+  // sync-free qt_multiply_async (small products): the BFS's level counts of a
+  // product still in flight land in a pinned ring slot; the product's block
+  // count is read on first use (qt::resolve)
+  static constexpr int kPendRing = 32;
+  int32_t* pend_host = nullptr;        // [kPendRing][128] pinned
+  cudaEvent_t pend_ev[kPendRing] = {};
+  qt_mat_s* pend_owner[kPendRing] = {};
+  int pend_next = 0;
   struct PendingCopy {
     cudaEvent_t done;
     qt::DevBuf bufs[3];  // staging buffers, released when `done` has completed
@@ -177,6 +185,10 @@ struct qt_mat_s {
   const void* pool1 = nullptr;
   const void* pool2 = nullptr;
   int64_t split = INT64_MAX;
+  // a sync-free async product whose block count is still on its way (the
+  // context's ring slot), or -1; nb is the BFS's upper bound until resolved
+  int pend_slot = -1;
+  ~qt_mat_s();
   const void* pool_ptr() const { return pool1 ? pool1 : pool.p; }
 };
 
@@ -198,7 +210,14 @@ void build_from_blocks(qt_mat M, int64_t nb, const int32_t* d_brow, const int32_
 // optional): the pool index of each sorted block, stored in the level L-1
 // child table instead of the sorted position (used by the merged B_ext).
 void build_levels(qt_mat M, const int32_t* leaf_ids = nullptr);
+// a product of a sync-free qt_multiply_async: wait for its level counts and
+// set its block count (every entry point does this before reading nb)
+void resolve_pending(qt_mat M);
+inline void resolve(qt_mat M) {
+  if (M && M->pend_slot >= 0) resolve_pending(M);
+}
 inline void ensure_levels(qt_mat M) {
+  resolve(M);
   if (!M->levels_built) { build_levels(M); M->levels_built = true; }
 }
 // QT_EINVAL unless every (caller-size) block has brow <= bcol (upper block triangle)

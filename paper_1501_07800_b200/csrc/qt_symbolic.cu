@@ -173,6 +173,8 @@ struct SmallBfsArgs {
   const double* n16B;
   unsigned long long* prof;  // QT_BFS_PROF: per-phase %globaltimer marks (diagnostics), or null
   int* zero;                 // the numeric kernel's scheduler counters, zeroed here (saves a memset launch)
+  int tiny_cap;              // the tiny variant's shared-memory frontier capacity
+  int32_t* host_counts;      // sync-free products: [ns(L+1) | F(L+1)] written to mapped host memory, or null
   int32_t nodesA[QT_MAX_LEVELS];  // child-table rows per level (L2 prefetch at kernel start)
   int32_t nodesB[QT_MAX_LEVELS];
 };
@@ -192,8 +194,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // (dynamic, kTinyF tasks / groups per level), so a level costs the child-table
 // gathers and block barriers only, not ~7 dependent round trips to L2.
 constexpr int kTinyF = 2048;
-constexpr size_t kTinySmem = 2 * (3 * 4 + 4 + 8) * (size_t)kTinyF + 4 * 2 * (size_t)kTinyF + 4 * 4 * (size_t)kTinyF +
-                             4 * 4 * (size_t)kTinyF + 64;
+// dynamic shared memory of the tiny variant for levels of <= cap tasks (the
+// launch asks only for what the problem's levels need: a large carve-out
+// costs the launch several microseconds)
+inline size_t tiny_smem(int cap) {
+  return 2 * (3 * 4 + 4 + 8) * (size_t)cap + 4 * 2 * (size_t)cap + 4 * 4 * (size_t)cap + 4 * 4 * (size_t)cap + 64;
+}
 
 template <bool kExt, bool kSmem>
 __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) {
@@ -208,15 +214,16 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
   const bool sym = a.trans & 4;
   // per-level buffers: shared memory unless the level is read after the kernel
   uint64_t* ck0 = reinterpret_cast<uint64_t*>(tiny);
-  int32_t* base = reinterpret_cast<int32_t*>(ck0 + 2 * kTinyF);
-  int32_t* off = kSmem ? base + 8 * kTinyF + 8 : a.off;
-  int32_t* gidx_s = kSmem ? off + 4 * kTinyF : a.gidx;
+  const int T = a.tiny_cap;  // capacity (tasks / groups per level) of the shared-memory frontiers
+  int32_t* base = reinterpret_cast<int32_t*>(ck0 + 2 * T);
+  int32_t* off = kSmem ? base + 8 * T + 8 : a.off;
+  int32_t* gidx_s = kSmem ? off + 4 * T : a.gidx;
   auto glob = [&](int l) { return !kSmem || l == a.l_end || (a.l_end == a.L && l == a.L - 1); };
-  auto PA = [&](int l) { return glob(l) ? a.pa[l & 1] : base + (l & 1) * kTinyF; };
-  auto PB = [&](int l) { return glob(l) ? a.pb[l & 1] : base + (2 + (l & 1)) * kTinyF; };
-  auto PC = [&](int l) { return glob(l) ? a.pc[l & 1] : base + (4 + (l & 1)) * kTinyF; };
-  auto CS = [&](int l) { return glob(l) ? a.cstart[l & 1] : base + 6 * kTinyF + (l & 1) * (kTinyF + 4); };
-  auto CK = [&](int l) { return glob(l) ? a.ckey[l & 1] : ck0 + (l & 1) * kTinyF; };
+  auto PA = [&](int l) { return glob(l) ? a.pa[l & 1] : base + (l & 1) * T; };
+  auto PB = [&](int l) { return glob(l) ? a.pb[l & 1] : base + (2 + (l & 1)) * T; };
+  auto PC = [&](int l) { return glob(l) ? a.pc[l & 1] : base + (4 + (l & 1)) * T; };
+  auto CS = [&](int l) { return glob(l) ? a.cstart[l & 1] : base + 6 * T + (l & 1) * (T + 4); };
+  auto CK = [&](int l) { return glob(l) ? a.ckey[l & 1] : ck0 + (l & 1) * T; };
   int np = 0;
   auto mark = [&]() {
     if (a.prof && tid == 0 && np < 40) a.prof[np] = gtimer();
@@ -373,6 +380,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     mark();
   }
   if (a.prof && tid == 0) a.prof[63] = np;
+  if (a.host_counts && a.l_end == a.L && tid == 0)  // (this kernel produced every level)
+    for (int l = 0; l <= a.L; ++l) {
+      a.host_counts[l] = a.ns_out[l];
+      a.host_counts[a.L + 1 + l] = a.f_out[l];
+    }
 }
 
 // ------------------------------------------------------------ large levels (one persistent kernel)
@@ -418,6 +430,7 @@ struct LargeBfsArgs {
   int32_t* f_out;                // tasks per level
   unsigned* bar;                 // grid barrier: arrival count (self-resetting), generation
   unsigned long long* prof;      // QT_BFS_PROF: CTA 0's %globaltimer at each phase boundary, or null
+  int32_t* host_counts;          // sync-free products: the level counts to mapped host memory, or null
   int32_t row_lo, row_hi;        // C row window (block rows)
   const uint8_t* subA;           // block size 16: quadrant masks (pair test at the block level)
   const uint8_t* subB;
@@ -704,6 +717,12 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
     grid_sync(a.bar, gen);
     pmark(7);
   }
+  // (CTA 0 wrote the counts of this kernel's levels; the small kernel the others)
+  if (a.host_counts && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int l = 0; l <= a.L; ++l) {
+      a.host_counts[l] = a.ns_out[l];
+      a.host_counts[a.L + 1 + l] = a.f_out[l];
+    }
 }
 
 // CTAs of the cooperative BFS launch: every CTA resident (occupancy x SMs)
@@ -818,7 +837,9 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
   S.nlevels = L + 1;
   S.leaf_level = A->leaf_level;
   try {
-    QT_CUDA(cudaEventRecord(ctx->ev[2], st));
+    // (the timing events are skipped by qt_multiply_async, whose ms_* are 0)
+    const bool timed = !ctx->async_multiply;
+    if (timed) QT_CUDA(cudaEventRecord(ctx->ev[2], st));
     std::vector<int64_t> F = level_task_bounds(A, B, trans);
     if (A->nb > 0 && B->nb > 0) {
       tr.mark("counts");
@@ -830,12 +851,36 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
     if (F[L] == 0) {
       // no block product at all: C is the NIL matrix
       C->nb = 0;
-      QT_CUDA(cudaEventRecord(ctx->ev[3], st));
-      QT_CUDA(cudaEventRecord(ctx->ev[4], st));
+      if (timed) {
+        QT_CUDA(cudaEventRecord(ctx->ev[3], st));
+        QT_CUDA(cudaEventRecord(ctx->ev[4], st));
+      }
     } else {
       // upper bounds of the group counts: ns_{l+1} <= min(4 ns_l, F_{l+1})
       std::vector<int64_t> nsb(L + 1, 1);
       for (int l = 0; l < L; ++l) nsb[l + 1] = std::min<int64_t>(4 * nsb[l], F[l + 1]);
+      // Sync-free mode (small problems, where a host round trip between the
+      // BFS and the numeric kernel is a large share of the call): C's pool is
+      // sized by the upper bound nsb[L] (transient over-allocation <=
+      // QT_SYNCFREE_MB, default 1024 MiB), the numeric kernel reads the tile
+      // count from the device, and the last BFS kernel writes the level counts
+      // straight into mapped host memory — the context's staging area (read
+      // after the call's one final sync) or, for qt_multiply_async, a ring
+      // slot read when C is first used (resolve).
+      const size_t cbound = (size_t)nsb[L] * 1024 * elem_size(C->dtype);
+      const bool syncfree =
+          A->dtype != QT_F32 && A->ubs != 16 && !ov && !plan && !B->pool2 && cbound <= syncfree_cap();
+      int32_t* h_counts = static_cast<int32_t*>(ctx->pinned);  // [ns(L+1) | F(L+1)]
+      int pend_slot = -1;
+      int32_t* host_counts = nullptr;
+      if (syncfree && ctx->async_multiply) {
+        pend_slot = ctx->pend_next;
+        ctx->pend_next = (pend_slot + 1) % qt_ctx_s::kPendRing;
+        if (ctx->pend_owner[pend_slot]) resolve(ctx->pend_owner[pend_slot]);  // (ring full: the oldest first)
+        host_counts = ctx->pend_host + 128 * pend_slot;
+      } else if (syncfree) {
+        host_counts = h_counts;
+      }
       DevBuf cnt_dev(8 * (L + 1), st);  // [ns(L+1) | F(L+1)]: one D2H copy
       int32_t* nsd = cnt_dev.as<int32_t>();
       int32_t* fd = nsd + (L + 1);
@@ -898,6 +943,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       sa.ns_out = nsd;
       sa.f_out = fd;
       sa.zero = ctx->counters.as<int>() + 16;  // the numeric kernels' scheduler counters (16, 17)
+      sa.host_counts = host_counts;
       tr.mark("small_alloc");
       const bool ext = sa.subA || row_lo > 0 || row_hi < INT32_MAX;
       static const bool bfs_prof = getenv("QT_BFS_PROF") != nullptr;
@@ -910,21 +956,26 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       }
       // the intermediate small levels in shared memory when every one fits
       bool tiny = true;
-      for (int l = 0; l < l_end; ++l) tiny = tiny && F[l] <= kTinyF;
+      int64_t tiny_max = 1;
+      for (int l = 0; l < l_end; ++l) {
+        tiny = tiny && F[l] <= kTinyF;
+        tiny_max = std::max(tiny_max, F[l]);
+      }
+      sa.tiny_cap = (int)((tiny_max + 127) / 128 * 128);
       if (tiny) {
         static std::atomic<unsigned long long> attr_set{0};  // per device (bit d)
         const unsigned long long bit = 1ull << (ctx->device & 63);
         if (!(attr_set.load(std::memory_order_acquire) & bit)) {
           QT_CUDA(cudaFuncSetAttribute(k_bfs_small<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kTinySmem));
+                                       (int)tiny_smem(kTinyF)));
           QT_CUDA(cudaFuncSetAttribute(k_bfs_small<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kTinySmem));
+                                       (int)tiny_smem(kTinyF)));
           attr_set.fetch_or(bit, std::memory_order_release);
         }
         if (ext)
-          k_bfs_small<true, true><<<1, 256, kTinySmem, st>>>(sa);
+          k_bfs_small<true, true><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
         else
-          k_bfs_small<false, true><<<1, 256, kTinySmem, st>>>(sa);
+          k_bfs_small<false, true><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
       } else if (ext) {
         k_bfs_small<true, false><<<1, kSmallThreads, 0, st>>>(sa);
       } else {
@@ -1020,6 +1071,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         la.ns_out = nsd;
         la.f_out = fd;
         la.bar = reinterpret_cast<unsigned*>(ctx->counters.as<int>() + 40);
+        la.host_counts = host_counts;
         DevBuf lprof;
         la.prof = nullptr;
         if (bfs_prof) {
@@ -1068,18 +1120,9 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
           cstart = std::move(qcs[set(L - 1)]);
         }
       }
-      // --- group counts of every level: C's block count.  Sync-free mode
-      // (small problems, where a host round trip between the BFS and the
-      // numeric kernel is a large share of the call): C's pool is sized by
-      // the upper bound nsb[L] (transient over-allocation <= QT_SYNCFREE_MB,
-      // default 1024 MiB), the numeric kernel reads the tile count from the
-      // device, and the counts come back with the call's one final sync.
+      // --- group counts of every level: C's block count (sync-free mode: above)
       tr.mark("levels_launched");
       std::vector<int32_t> ns(L + 1, 0), Fa(L + 1, 0);
-      const size_t cbound = (size_t)nsb[L] * 1024 * elem_size(C->dtype);
-      const bool syncfree = !f32 && A->ubs != 16 && !ov && !plan && !ctx->async_multiply && !B->pool2 &&
-                            cbound <= syncfree_cap();
-      int32_t* h_counts = static_cast<int32_t*>(ctx->pinned);  // [ns(L+1) | F(L+1)]
       if (syncfree) {
         for (int l = 0; l <= L; ++l) ns[l] = (int32_t)nsb[l];  // upper bounds until the final sync
         C->nb = nsb[L];
@@ -1137,7 +1180,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
                       B->split, tmap.as<int32_t>(), tnsel.as<int32_t>());
         tr.mark("tile_split");
       }
-      QT_CUDA(cudaEventRecord(ctx->ev[3], st));
+      if (timed) QT_CUDA(cudaEventRecord(ctx->ev[3], st));
       NumericArgs na;
       na.ntiles = ns[L - 1];
       na.tile_start = cstart.as<int32_t>();
@@ -1248,15 +1291,19 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         else
           launch_numeric_f32(ctx, nb);
       }
-      if (syncfree) {  // the BFS's counts ride back with the final sync
-        QT_CUDA(cudaMemcpyAsync(h_counts, nsd, 8 * (L + 1), cudaMemcpyDeviceToHost, st));
-      }
-      QT_CUDA(cudaEventRecord(ctx->ev[4], st));
+      if (pend_slot >= 0) QT_CUDA(cudaEventRecord(ctx->pend_ev[pend_slot], st));  // (C's counts are in its ring slot)
+      if (timed) QT_CUDA(cudaEventRecord(ctx->ev[4], st));
       tr.mark("numeric_launched");
       // (the frontier buffers go back to this stream's cache: stream-ordered reuse)
       if (!ctx->async_multiply) QT_CUDA(cudaEventSynchronize(ctx->ev[4]));
       tr.mark("numeric_done");
-      if (syncfree) {
+      if (pend_slot >= 0) {
+        // (stats: the task counts are exact for regular products; C's block
+        // and group counts are unknown until C is resolved)
+        C->pend_slot = pend_slot;
+        ctx->pend_owner[pend_slot] = C;
+        for (int l = 0; l <= L; ++l) S.level_c_nodes[l] = 0;
+      } else if (syncfree) {
         for (int l = 0; l <= L; ++l) {
           ns[l] = h_counts[l];
           Fa[l] = h_counts[L + 1 + l];
@@ -1347,7 +1394,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       QT_CUDA(cudaEventElapsedTime(ms_sym, ctx->ev[2], ctx->ev[3]));
       QT_CUDA(cudaEventElapsedTime(ms_num, ctx->ev[3], ctx->ev[4]));
     }
-    S.c_blocks = C->nb;
+    S.c_blocks = C->pend_slot >= 0 ? -1 : C->nb;  // (-1: a sync-free async product, not known yet)
     if (A->ubs == 16) S.nlevels = L + 2;  // + the 16-block level below the containers
   } catch (...) {
     delete C;

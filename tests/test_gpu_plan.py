@@ -150,3 +150,44 @@ def test_symm_square_plan(qt, ctx, dtype):
         ref = oracle.symm_square(nbr, 32, (br.astype(np.int32), bc.astype(np.int32), v.astype(np.float64)))
         assert np.array_equal(got[0], ref[0]) and np.array_equal(got[2].astype(np.float64), ref[2])
     plan.close()
+
+
+def test_async_small_products_pipeline(qt, ctx):
+    """Sync-free qt_multiply_async (small products): products returned before
+    their block count is known (c_blocks -1) are resolved on first use — as
+    operands of the next multiply, by to_blocks, by close — including more
+    products in flight than the context's 32-slot count ring; every result
+    equals the oracle's (integer values: exact)."""
+    import oracle
+    rng = np.random.default_rng(77)
+    nbr = 12
+    mats = []
+    for _ in range(2):
+        m = rng.random((nbr, nbr)) < 0.4
+        br, bc = np.nonzero(m)
+        v = rng.integers(-2, 3, size=(len(br), 32, 32)).astype(np.float64)
+        mats.append((br.astype(np.int32), bc.astype(np.int32), v))
+    A = qt.Matrix.from_blocks(ctx, nbr * 32, 64, 32, *mats[0])
+    B = qt.Matrix.from_blocks(ctx, nbr * 32, 64, 32, *mats[1])
+    ref_ab = oracle.spgemm(nbr, 32, mats[0], mats[1])
+    # a chain: C1 = A B, C2 = C1 A, C3 = C2 B (each operand still pending)
+    C1, s1 = A.multiply(B, wait=False)
+    assert s1.c_blocks == -1 and s1.block_products > 0
+    C2, _ = C1.multiply(A, wait=False)
+    C3, _ = C2.multiply(B, wait=False)
+    ref2 = oracle.spgemm(nbr, 32, ref_ab, mats[0])
+    ref3 = oracle.spgemm(nbr, 32, ref2, mats[1])
+    for C, ref in ((C1, ref_ab), (C2, ref2), (C3, ref3)):
+        r, c, v = C.to_blocks()
+        assert np.array_equal(r, ref[0]) and np.array_equal(c, ref[1]) and np.array_equal(v, ref[2])
+        assert C.nblocks == len(ref[0])
+    # 80 products in flight (the ring wraps), half of them destroyed unread
+    outs = [A.multiply(B, wait=False)[0] for _ in range(80)]
+    for i, C in enumerate(outs):
+        if i % 2:
+            C.close()
+    for i, C in enumerate(outs):
+        if not i % 2:
+            r, c, v = C.to_blocks()
+            assert np.array_equal(v, ref_ab[2])
+            C.close()

@@ -276,6 +276,26 @@ def main():
             leaf_sweep(ctx, stream)
         elif w == "1":
             run(ctx, stream, "cfg1 dense N=512", qtgen.config(1), steps=200)
+        elif w == "1async":  # config 1 through qt_multiply_async (sync-free: back-to-back on the device)
+            c = qtgen.config(1)
+            A = qtmm.Matrix.from_blocks(ctx, c["A"].n, c["A"].leaf_dim, 32, c["A"].brow, c["A"].bcol, c["A"].vals)
+            B = qtmm.Matrix.from_blocks(ctx, c["B"].n, c["B"].leaf_dim, 32, c["B"].brow, c["B"].bcol, c["B"].vals)
+            for _ in range(20):
+                C, st = A.multiply(B, wait=False)
+                C.close()
+            steps = 400
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(steps):
+                C, st = A.multiply(B, wait=False)
+                C.close()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+            print(json.dumps({"config": "cfg1 dense N=512, qt_multiply_async (pipelined)", "ms_step": round(ms, 4),
+                              "block_products": st.block_products,
+                              "gflops_effective": round(st.block_products * FLOP / ms / 1e6, 1)}), flush=True)
         elif w == "2":
             run(ctx, stream, "cfg2 banded N=16384", qtgen.config(2))
         elif w == "3":
