@@ -378,6 +378,7 @@ struct NumericArgs32 {
   const int32_t* tile_map = nullptr;
   const int32_t* nsel = nullptr;
   bool counter_ready = false;      // as in NumericArgs
+  const int32_t* ntiles_dev = nullptr;  // as in NumericArgs (sync-free products)
 };
 void launch_numeric_f32(qt_ctx ctx, const NumericArgs32& a);
 

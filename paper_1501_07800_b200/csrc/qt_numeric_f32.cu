@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_numeric_f32(NumericArgs32 a) {
     };
     // phase launches of the multi-rank overlap: tiles map[t_off + i]
     int ntiles = (int)a.ntiles, t_off = 0;
+    if (a.ntiles_dev) ntiles = *a.ntiles_dev;  // sync-free product: the BFS's count (a.ntiles: its bound)
     if (a.phase) {
       const int ns = *a.nsel;
       t_off = a.phase == 1 ? 0 : ns;

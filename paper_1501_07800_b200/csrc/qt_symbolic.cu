@@ -869,7 +869,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       // slot read when C is first used (resolve).
       const size_t cbound = (size_t)nsb[L] * 1024 * elem_size(C->dtype);
       const bool syncfree =
-          A->dtype != QT_F32 && A->ubs != 16 && !ov && !plan && !B->pool2 && cbound <= syncfree_cap();
+          A->ubs != 16 && !ov && !plan && !B->pool2 && cbound <= syncfree_cap();
       int32_t* h_counts = static_cast<int32_t*>(ctx->pinned);  // [ns(L+1) | F(L+1)]
       int pend_slot = -1;
       int32_t* host_counts = nullptr;
@@ -1284,6 +1284,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         nb.zeros = ctx->zeros.p;
         nb.counter = ctx->counters.as<int>() + 16;
         nb.counter_ready = true;
+        if (syncfree) nb.ntiles_dev = nsd + (L - 2);  // the actual tile count (nb.ntiles: its bound)
         nb.trans = trans & 7;
         nb.poolT = poolTp;
         if (two_phase)
