@@ -846,10 +846,10 @@ __global__ void k_peak_dfma(double* out, int iters) {
 template <bool TA, bool TB, bool SYM = false, int SCR = 0, bool PH = false, bool MG = false, bool O32 = false>
 static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
   static const bool prof = getenv("QT_NUM_PROF") != nullptr;
-  if (prof && !TA && !TB && !SYM && SCR == 0 && !PH && !O32) {  // diagnostics: the instrumented plain kernel
+  if (prof && !TA && !TB && (SCR == 0 || SCR == 2) && !PH && !O32) {  // diagnostics: the instrumented kernel
     static bool set = false;
     if (!set) {
-      QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<false, false, false, 0, false, true, MG>,
+      QT_CUDA(cudaFuncSetAttribute(k_numeric_f64<false, false, SYM, SCR, false, true, MG>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
       set = true;
     }
@@ -858,7 +858,7 @@ static void launch_numeric_t(qt_ctx ctx, const NumericArgs& a, int grid) {
     QT_CUDA(cudaMemsetAsync(pb.p, 0, 16 * 8, st));
     NumericArgs b = a;
     b.prof = pb.as<unsigned long long>();
-    k_numeric_f64<false, false, false, 0, false, true, MG><<<grid, kNumThreads, kSmemBytes, st>>>(b);
+    k_numeric_f64<false, false, SYM, SCR, false, true, MG><<<grid, kNumThreads, kSmemBytes, st>>>(b);
     unsigned long long h[16];
     QT_CUDA(cudaMemcpyAsync(h, pb.p, 16 * 8, cudaMemcpyDeviceToHost, st));
     QT_CUDA(cudaStreamSynchronize(st));
