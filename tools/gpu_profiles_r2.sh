@@ -23,7 +23,9 @@ full r02_ncu_full_numeric_f32_cfg5 k_numeric_f32 2 5f32
 full r02_ncu_full_bfs_large_cfg3 k_bfs_large 2 3
 full r02_ncu_full_bfs_large_cfg2 k_bfs_large 2 2
 full r02_ncu_full_bfs_small_cfg3 k_bfs_small 2 3
-for c in 3 4; do QT_NUM_PROF=1 timeout 300 python tools/perf_configs.py $c 2>&1 | grep "numeric prof" | tail -1; done > gpurun_out/r02_numeric_prof.txt
+for c in 3 4 sym16; do QT_NUM_PROF=1 timeout 300 python tools/perf_configs.py $c 2>&1 | grep "numeric prof" | tail -1; done > gpurun_out/r02_numeric_prof.txt
+python tools/async_diag.py > gpurun_out/r02_async_cfg1.txt 2>&1
+timeout 300 python tools/perf_configs.py 1async >> gpurun_out/r02_async_cfg1.txt 2>&1
 timeout 1200 python tools/perf_configs.py 1 2 3 4 5 dense4096 5f32 dense4096f32 sym2 sym5f32 sym4 sym16 scr4 virt8 virt8f32 virt4cfg4 virtsym8 virtsym4cfg4 > gpurun_out/r02_perf_configs.jsonl 2>&1; echo "perf rc=$?"
 timeout 900 python tools/perf_configs.py leafsweep > gpurun_out/r02_leaf_sweep.jsonl 2>&1; echo "leaf rc=$?"
 du -sh gpurun_out
