@@ -106,6 +106,16 @@ qt_status qt_ctx_destroy(qt_ctx ctx);
  * QT_ENCCL. */
 qt_status qt_ctx_info(qt_ctx ctx, int32_t* rank, int32_t* world, int32_t* comm_ranks, int32_t* transport);
 
+/* Per-phase device timings of the multiply calls (qt_stats.ms_symbolic,
+ * ms_numeric, ms_total), measured with CUDA events on the context's stream:
+ * on (1, the default) or off (0).  Off skips the event records and the
+ * elapsed-time queries — about 10 us of driver calls per blocking call, a
+ * large share of a small product — and reports 0 for them; results and every
+ * other statistic are unchanged, and a blocking call still returns with its
+ * work complete.  (Measurement only: no passage of the paper.)
+ * Errors: QT_EINVAL (NULL context). */
+qt_status qt_ctx_set_timing(qt_ctx ctx, int32_t on);
+
 /* Write a fresh 128-byte ncclUniqueId into `out128` (loads NCCL on demand).
  * Errors: QT_ENCCL when libnccl.so.2 cannot be loaded. */
 qt_status qt_nccl_unique_id(void* out128);

@@ -127,6 +127,7 @@ struct qt_ctx_s {
   cudaStream_t comm_stream = nullptr;  // multi-rank: payload exchange + the remote tiles' numeric launch
   cudaEvent_t ov_ev[4] = {};           // overlap ordering (0, 1) and payload timing (2, 3)
   bool async_multiply = false;         // qt_multiply_async: no final synchronisation
+  bool timing = true;                  // qt_ctx_set_timing: CUDA-event phase timings in qt_stats
   // sync-free qt_multiply_async (small products): the BFS's level counts of a
   // product still in flight land in a pinned ring slot; the product's block
   // count is read on first use (qt::resolve)
@@ -162,6 +163,11 @@ struct qt_mat_s {
   std::vector<qt::DevBuf> child; // child[l] : int32 [cnt[l]][4], l = 0..L-1 (-1 = NIL)
   bool levels_built = true;     // false for a fresh product: built on first use
   qt::DevBuf hist;     // int32 per-level node counts per row / per column (see build_levels)
+  // dense Morton-indexed node maps of the top levels: int32 [kDenseNodes],
+  // level l (l <= 4, l < L) at offset (4^l - 1) / 3, entry = node index or -1
+  // (the symbolic pass's dense start reads the tasks of level l0 off them)
+  qt::DevBuf dmap;
+  static constexpr int kDenseLevels = 4, kDenseNodes = 341;
   std::vector<int32_t> hist_host;  // host copy of hist (per-level task counts without a sync)
   std::vector<qt::DevBuf> norm2;  // squared Frobenius norms per node, levels 0..L (screening; lazy)
   qt::DevBuf norm16;   // ubs == 16 screening: squared norms of the 16-blocks, double [nb][4] (0 if absent; lazy)

@@ -177,6 +177,9 @@ struct SmallBfsArgs {
   int32_t* host_counts;      // sync-free products: [ns(L+1) | F(L+1)] written to mapped host memory, or null
   int32_t nodesA[QT_MAX_LEVELS];  // child-table rows per level (L2 prefetch at kernel start)
   int32_t nodesB[QT_MAX_LEVELS];
+  int l0 = 0;  // dense start: levels 1..l0 from the dense node maps (0: off)
+  const int32_t* dmapA = nullptr;  // the operands' dense top-level node maps (qt_mat_s::dmap)
+  const int32_t* dmapB = nullptr;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -201,8 +204,11 @@ inline size_t tiny_smem(int cap) {
   return 2 * (3 * 4 + 4 + 8) * (size_t)cap + 4 * 2 * (size_t)cap + 4 * 4 * (size_t)cap + 4 * 4 * (size_t)cap + 64;
 }
 
-template <bool kExt, bool kSmem>
-__global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) {
+// kPlain: a plain or transposed product without screening (no symmetric
+// references, no norm tests): the pair test reduces to two NIL checks and the
+// kernel's code shrinks (the tiny levels are instruction-fetch bound)
+template <bool kExt, bool kSmem, bool kPlain>
+__global__ void __launch_bounds__(kSmem ? 256 : kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) {
   // the tiny variant runs 256 threads: its levels have <= kTinyF tasks and
   // its cost is the latency of block scans and barriers, cheaper with 8 warps
   constexpr int kT = kSmem ? 256 : kSmallThreads;
@@ -211,7 +217,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
   __shared__ int s_F, s_ns;
   extern __shared__ __align__(16) uint8_t tiny[];
   const int tid = threadIdx.x;
-  const bool sym = a.trans & 4;
+  const bool sym = !kPlain && (a.trans & 4);
   // per-level buffers: shared memory unless the level is read after the kernel
   uint64_t* ck0 = reinterpret_cast<uint64_t*>(tiny);
   const int T = a.tiny_cap;  // capacity (tasks / groups per level) of the shared-memory frontiers
@@ -268,7 +274,104 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     s_ns = 1;
   }
   __syncthreads();
-  for (int l = 0; l < a.l_end; ++l) {
+  int l_start = 0;
+  if (kPlain && a.l0 > 0) {
+    // Dense start (plain and transposed products): the tasks of level l0 are
+    // every pair (op(A)(i,k), op(B)(k,j)) of non-NIL level-l0 nodes — the
+    // recursion of §3.2 registers exactly those, a NIL operand at
+    // any coarser level having no non-NIL descendants — so the first l0
+    // transitions are replaced by a lookup in the operands' dense
+    // Morton-indexed node maps of the top l0 levels (4^l nodes at level l,
+    // kept with each matrix: build_levels) and one block scan.
+    // Order as the BFS: groups (C nodes) in Morton order, ascending k inside.
+    constexpr int kDenseMax = 341;  // 1 + 4 + 16 + 64 + 256: levels 0..4
+    __shared__ int32_t sDA[kDenseMax], sDB[kDenseMax];
+    __shared__ int s_lf[8], s_lns[8];
+    const int l0 = a.l0;
+    const int nmap = ((4 << (2 * l0)) - 1) / 3;  // levels 0..l0
+    for (int t = tid; t < nmap; t += kT) {
+      sDA[t] = a.dmapA[t];
+      sDB[t] = a.dmapB[t];
+    }
+    if (tid < 8) s_lf[tid] = s_lns[tid] = 0;
+    __syncthreads();
+    // tasks and C nodes of the levels 1..l0-1 (statistics) and of level l0
+    // (emitted): C node m of level l pairs with k = 0 .. 2^l - 1
+    const bool tA = a.trans & 1, tB = a.trans & 2;
+    // Morton index of (r, c) at a level <= 4: the bits of r and c (< 16) interleaved
+    auto sp4 = [](int x) { return (x & 1) | ((x & 2) << 1) | ((x & 4) << 2) | ((x & 8) << 3); };
+    auto spread_rc = [&](int m, int& ri, int& cj) {  // m -> spread row / column bits
+      ri = (m >> 1) & 0x55;
+      cj = m & 0x55;
+    };
+    unsigned kmask = 0;
+    int cnt0 = 0, rA0 = 0, rB0 = 0;
+    for (int l = 1, o = 1; l <= l0; o += 1 << (2 * l), ++l) {
+      const int K = 1 << l;
+      for (int m = tid; m < K * K; m += kT) {
+        int si, sj;
+        spread_rc(m, si, sj);
+        // op(A)(i,k) at Morton (i,k), or (k,i) transposed; op(B)(k,j) likewise
+        const int ra = tA ? si : si << 1, ka = tA ? 1 : 0;
+        const int rb = tB ? sj << 1 : sj, kb = tB ? 0 : 1;
+        int c = 0;
+        unsigned msk = 0;
+        for (int k = 0; k < K; ++k) {
+          const int sk = sp4(k);
+          const int xa = sDA[o + (ra | (sk << ka))];
+          const int xb = sDB[o + (rb | (sk << kb))];
+          if (xa >= 0 && xb >= 0) {
+            ++c;
+            msk |= 1u << k;
+          }
+        }
+        if (l == l0) {  // (K * K <= kT: one C node per thread)
+          kmask = msk;
+          cnt0 = c;
+          rA0 = ra | (ka << 8);
+          rB0 = rb | (kb << 8);
+        } else if (c > 0) {
+          atomicAdd(&s_lf[l], c);
+          atomicAdd(&s_lns[l], 1);
+        }
+      }
+    }
+    // level l0: packed scan (tasks in the low 16 bits, groups above: <= 4096 / 256)
+    int ex, agg;
+    BS(tmp).ExclusiveSum(cnt0 + ((cnt0 > 0) << 16), ex, agg);
+    const int o0 = ((1 << (2 * l0)) - 1) / 3;  // offset of level l0 in the dense maps
+    if (cnt0 > 0) {
+      int pos = ex & 0xFFFF;
+      const int g = ex >> 16;
+      CS(l0)[g] = pos;
+      CK(l0)[g] = (uint64_t)tid;
+      int32_t *pa0 = PA(l0), *pb0 = PB(l0), *pc0 = PC(l0);
+      for (unsigned msk = kmask; msk; msk &= msk - 1) {
+        const int sk = sp4(__ffs(msk) - 1);
+        pa0[pos] = sDA[o0 + ((rA0 & 0xFF) | (sk << (rA0 >> 8)))];
+        pb0[pos] = sDB[o0 + ((rB0 & 0xFF) | (sk << (rB0 >> 8)))];
+        pc0[pos] = g;
+        ++pos;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const int F0 = agg & 0xFFFF, ns0 = agg >> 16;
+      CS(l0)[ns0] = F0;
+      for (int l = 1; l < l0; ++l) {
+        a.f_out[l] = s_lf[l];
+        a.ns_out[l] = s_lns[l];
+      }
+      a.f_out[l0] = F0;
+      a.ns_out[l0] = ns0;
+      s_F = F0;
+      s_ns = ns0;
+    }
+    __syncthreads();
+    l_start = l0;
+    mark();
+  }
+  for (int l = l_start; l < a.l_end; ++l) {
     const bool prune = sym && l < (a.trans >> 8);  // C below the diagonal is not computed
     const int F = s_F, ns = s_ns;
     const int32_t* pa = PA(l);
@@ -283,14 +386,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     const int4* cA = s_cA[l];
     const int4* cB = s_cB[l];
     const bool lastl = kExt && l + 1 == a.L && a.subA;
-    const Screen sc{s_nA[l + 1], s_nB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
+    const Screen sc{kPlain ? nullptr : s_nA[l + 1], kPlain ? nullptr : s_nB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
                     a.trans & 3, lastl ? a.n16A : nullptr, lastl ? a.n16B : nullptr};
     const int32_t rlo = kExt ? a.row_lo : 0, rhi = kExt ? a.row_hi : INT32_MAX;
     // 1. child-task counts per (task, C child), group-major
-    for (int p = tid; p < F; p += kT) {
+    auto count_task = [&](int p, int4 rA, int4 rB) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
       int c[4];
-      const int4 rA = op_children(cA, pa[p], a.trans & 1, sym), rB = op_children(cB, pb[p], a.trans & 2, sym);
       child_counts(rA, rB, c, sc, sym);
       const int cm = cmask(ck + s, l, a.L, prune, rlo, rhi);
 #pragma unroll
@@ -299,7 +401,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
       const int64_t base = 4ll * c0 + (p - c0);
 #pragma unroll
       for (int q = 0; q < 4; ++q) off[base + (int64_t)q * m] = c[q];
-    }
+    };
+    for (int p = tid; p < F; p += kT)
+      count_task(p, op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym));
     __syncthreads();
     mark();
     // 2. exclusive scan in place (kIt consecutive entries per thread: a level
@@ -365,12 +469,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) 
     __syncthreads();
     mark();
     // 4. emit the child tasks (none below the block level)
-    for (int p = tid; p < F && l + 1 < a.L; p += kT) {
+    auto emit = [&](int p, int4 rA, int4 rB) {
       const int s = pc[p], c0 = cs[s], m = cs[s + 1] - c0;
-      emit_task(op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym),
-                4ll * c0 + (p - c0), m, s, cmask(ck + s, l, a.L, prune, rlo, rhi), sc, sym, off,
-                gidx, PA(l + 1), PB(l + 1), PC(l + 1));
-    }
+      emit_task(rA, rB, 4ll * c0 + (p - c0), m, s, cmask(ck + s, l, a.L, prune, rlo, rhi), sc, sym, off, gidx,
+                PA(l + 1), PB(l + 1), PC(l + 1));
+    };
+    for (int p = tid; p < F && l + 1 < a.L; p += kT)
+      emit(p, op_children(cA, pa[p], a.trans & 1, sym), op_children(cB, pb[p], a.trans & 2, sym));
     __syncthreads();
     if (tid == 0) {
       s_F = Fn;
@@ -766,6 +871,7 @@ struct Trace {
     buf += b;
   }
   ~Trace() {
+    mark("exit");
     if (on) fprintf(stderr, "[qt trace] multiply:%s\n", buf.c_str());
   }
 };
@@ -837,8 +943,9 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
   S.nlevels = L + 1;
   S.leaf_level = A->leaf_level;
   try {
-    // (the timing events are skipped by qt_multiply_async, whose ms_* are 0)
-    const bool timed = !ctx->async_multiply;
+    // (the timing events are skipped by qt_multiply_async and with the
+    // context's timing off: ms_* are 0 then)
+    const bool timed = !ctx->async_multiply && ctx->timing;
     if (timed) QT_CUDA(cudaEventRecord(ctx->ev[2], st));
     std::vector<int64_t> F = level_task_bounds(A, B, trans);
     if (A->nb > 0 && B->nb > 0) {
@@ -946,6 +1053,16 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       sa.host_counts = host_counts;
       tr.mark("small_alloc");
       const bool ext = sa.subA || row_lo > 0 || row_hi < INT32_MAX;
+      // dense start: plain and transposed products without screening (the
+      // other modes prune by rules the dense maps do not carry)
+      static const int dense_env = getenv("QT_DENSE_START") ? atoi(getenv("QT_DENSE_START")) : 4;
+      sa.l0 = (!ext && !sym && !screen && A->dmap.p && B->dmap.p)
+                  ? std::min(std::min(std::min(dense_env, qt_mat_s::kDenseLevels), l_end), L - 1)
+                  : 0;
+      if (sa.l0 < 2) sa.l0 = 0;
+      const bool plain = !ext && !sym && !screen;
+      sa.dmapA = A->dmap.as<int32_t>();
+      sa.dmapB = B->dmap.as<int32_t>();
       static const bool bfs_prof = getenv("QT_BFS_PROF") != nullptr;
       DevBuf profbuf;
       sa.prof = nullptr;
@@ -966,20 +1083,26 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         static std::atomic<unsigned long long> attr_set{0};  // per device (bit d)
         const unsigned long long bit = 1ull << (ctx->device & 63);
         if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-          QT_CUDA(cudaFuncSetAttribute(k_bfs_small<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)tiny_smem(kTinyF)));
-          QT_CUDA(cudaFuncSetAttribute(k_bfs_small<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)tiny_smem(kTinyF)));
+          QT_CUDA(cudaFuncSetAttribute(k_bfs_small<false, true, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiny_smem(kTinyF)));
+          QT_CUDA(cudaFuncSetAttribute(k_bfs_small<false, true, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiny_smem(kTinyF)));
+          QT_CUDA(cudaFuncSetAttribute(k_bfs_small<true, true, false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiny_smem(kTinyF)));
           attr_set.fetch_or(bit, std::memory_order_release);
         }
         if (ext)
-          k_bfs_small<true, true><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
+          k_bfs_small<true, true, false><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
+        else if (plain)
+          k_bfs_small<false, true, true><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
         else
-          k_bfs_small<false, true><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
+          k_bfs_small<false, true, false><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
       } else if (ext) {
-        k_bfs_small<true, false><<<1, kSmallThreads, 0, st>>>(sa);
+        k_bfs_small<true, false, false><<<1, kSmallThreads, 0, st>>>(sa);
+      } else if (plain) {
+        k_bfs_small<false, false, true><<<1, kSmallThreads, 0, st>>>(sa);
       } else {
-        k_bfs_small<false, false><<<1, kSmallThreads, 0, st>>>(sa);
+        k_bfs_small<false, false, false><<<1, kSmallThreads, 0, st>>>(sa);
       }
       QT_LAUNCH_CHECK(ctx);
       if (bfs_prof) {
@@ -1296,7 +1419,10 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       if (timed) QT_CUDA(cudaEventRecord(ctx->ev[4], st));
       tr.mark("numeric_launched");
       // (the frontier buffers go back to this stream's cache: stream-ordered reuse)
-      if (!ctx->async_multiply) QT_CUDA(cudaEventSynchronize(ctx->ev[4]));
+      if (timed)
+        QT_CUDA(cudaEventSynchronize(ctx->ev[4]));
+      else if (!ctx->async_multiply)
+        QT_CUDA(cudaStreamSynchronize(st));
       tr.mark("numeric_done");
       if (pend_slot >= 0) {
         // (stats: the task counts are exact for regular products; C's block
@@ -1390,13 +1516,14 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         }
       }
     }
-    if (!ctx->async_multiply) {
+    if (!ctx->async_multiply && ctx->timing) {
       QT_CUDA(cudaEventSynchronize(ctx->ev[4]));
       QT_CUDA(cudaEventElapsedTime(ms_sym, ctx->ev[2], ctx->ev[3]));
       QT_CUDA(cudaEventElapsedTime(ms_num, ctx->ev[3], ctx->ev[4]));
     }
     S.c_blocks = C->pend_slot >= 0 ? -1 : C->nb;  // (-1: a sync-free async product, not known yet)
     if (A->ubs == 16) S.nlevels = L + 2;  // + the 16-block level below the containers
+    tr.mark("stats");
   } catch (...) {
     delete C;
     throw;

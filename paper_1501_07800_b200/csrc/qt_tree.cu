@@ -72,13 +72,16 @@ __global__ void k_parent_flags(const uint64_t* __restrict__ key, int64_t n,
 
 __global__ void k_link(const uint64_t* __restrict__ key, const int32_t* __restrict__ incl,
                        int64_t n, const int32_t* __restrict__ ids, int32_t* __restrict__ child,
-                       uint64_t* __restrict__ pkey) {
+                       uint64_t* __restrict__ pkey, int32_t* __restrict__ dmap) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
     int32_t p = incl[t] - 1;
     uint64_t k = key[t];
     child[(int64_t)p * 4 + (int)(k & 3)] = ids ? ids[t] : (int32_t)t;
-    if (t == 0 || (k >> 2) != (key[t - 1] >> 2)) pkey[p] = k >> 2;
+    if (t == 0 || (k >> 2) != (key[t - 1] >> 2)) {
+      pkey[p] = k >> 2;
+      if (dmap) dmap[k >> 2] = p;  // (top levels: the parent level's dense map)
+    }
   }
 }
 
@@ -225,6 +228,8 @@ void build_levels(qt_mat M, const int32_t* leaf_ids) {
   M->hist.alloc(8 * H, st);
   QT_CUDA(cudaMemsetAsync(M->hist.p, 0, 8 * H, st));
   M->hist_host.assign(2 * H, 0);
+  M->dmap.alloc(4 * qt_mat_s::kDenseNodes, st);
+  QT_CUDA(cudaMemsetAsync(M->dmap.p, 0xff, 4 * qt_mat_s::kDenseNodes, st));
   if (M->nb == 0) return;
   DevBuf cur_keys(M->nb * 8, st);
   QT_CUDA(cudaMemcpyAsync(cur_keys.p, M->key.p, M->nb * 8, cudaMemcpyDeviceToDevice, st));
@@ -244,7 +249,10 @@ void build_levels(qt_mat M, const int32_t* leaf_ids) {
     DevBuf pkey((size_t)np * 8, st);
     k_link<<<grid_for(n), kThreads, 0, st>>>(cur_keys.as<uint64_t>(), incl.as<int32_t>(), n,
                                              l == M->L - 1 ? leaf_ids : nullptr,
-                                             M->child[l].as<int32_t>(), pkey.as<uint64_t>());
+                                             M->child[l].as<int32_t>(), pkey.as<uint64_t>(),
+                                             l <= qt_mat_s::kDenseLevels
+                                                 ? M->dmap.as<int32_t>() + ((1 << (2 * l)) - 1) / 3
+                                                 : nullptr);
     QT_LAUNCH_CHECK(ctx);
     cur_keys = std::move(pkey);
     k_level_hist<<<grid_for(np), kThreads, 0, st>>>(cur_keys.as<uint64_t>(), np, l, H,
@@ -818,6 +826,7 @@ qt_mat convert_dtype(qt_mat A, qt_dtype to) {
         if (src.bytes) QT_CUDA(cudaMemcpyAsync(dst.p, src.p, src.bytes, cudaMemcpyDeviceToDevice, st));
       };
       dup(A->hist, M->hist);
+      dup(A->dmap, M->dmap);
       M->child.resize(A->child.size());
       for (size_t l = 0; l < A->child.size(); ++l) dup(A->child[l], M->child[l]);
     }

@@ -68,6 +68,7 @@ def _load():
         "qt_ctx_create": [ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P, P],
         "qt_ctx_destroy": [P],
         "qt_ctx_info": [P, P, P, P, P],
+        "qt_ctx_set_timing": [P, i32],
         "qt_nccl_unique_id": [P],
         "qt_create": [P, i64, i32, i32, ctypes.c_int, i64, P, P, P, P, P],
         "qt_multiply": [P, P, P, P],
@@ -108,7 +109,7 @@ def _load():
 
 
 _lib = _load()
-EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_ctx_info", "qt_nccl_unique_id", "qt_create", "qt_multiply",
+EXPORTED = ("qt_ctx_create", "qt_ctx_destroy", "qt_ctx_info", "qt_ctx_set_timing", "qt_nccl_unique_id", "qt_create", "qt_multiply",
             "qt_multiply_async",
             "qt_multiply_ex", "qt_symm_square", "qt_multiply_screened",
             "qt_multiply_virtual", "qt_symm_square_virtual", "qt_plan_strips", "qt_multiply_plan",
@@ -197,6 +198,10 @@ class Context:
         _check(_lib.qt_ctx_info(self._h, ctypes.byref(r), ctypes.byref(w), ctypes.byref(n), ctypes.byref(t)))
         return {"rank": r.value, "world": w.value, "comm_ranks": n.value,
                 "transport": {0: "none", 1: "nccl", 2: "loopback"}[t.value]}
+
+    def set_timing(self, on: bool):
+        """qt_ctx_set_timing: CUDA-event phase timings in the stats (default on)."""
+        _check(_lib.qt_ctx_set_timing(self._h, int(bool(on))))
 
     def synchronize(self):
         """Wait for all enqueued work, including qt_read_back_async copies."""
