@@ -239,7 +239,8 @@ __global__ void __launch_bounds__(kSmem ? 256 : kSmallThreads, 1) k_bfs_small(Sm
   // one DRAM round trip for every child table the kernel will gather from
   // (they were evicted from L2 by the previous numeric pass), instead of one
   // per level
-  for (int l = 0; l < a.l_end; ++l) {
+  // (the dense start's levels are read off the node maps, not gathered)
+  for (int l = kPlain ? a.l0 : 0; l < a.l_end; ++l) {
     const char* ta = reinterpret_cast<const char*>(a.childA[l]);
     const char* tb = reinterpret_cast<const char*>(a.childB[l]);
     for (int i = tid; i < a.nodesA[l] / 8 + 1; i += kT)
@@ -254,11 +255,13 @@ __global__ void __launch_bounds__(kSmem ? 256 : kSmallThreads, 1) k_bfs_small(Sm
   __shared__ const int4* s_cB[QT_MAX_LEVELS];
   __shared__ const double* s_nA[QT_MAX_LEVELS];
   __shared__ const double* s_nB[QT_MAX_LEVELS];
-  if (tid < QT_MAX_LEVELS) {
+  if (tid < QT_MAX_LEVELS && tid <= a.L) {
     s_cA[tid] = a.childA[tid];
     s_cB[tid] = a.childB[tid];
-    s_nA[tid] = a.normA[tid];
-    s_nB[tid] = a.normB[tid];
+    if (!kPlain) {
+      s_nA[tid] = a.normA[tid];
+      s_nB[tid] = a.normB[tid];
+    }
   }
   if (tid < 2) a.zero[tid] = 0;
   if (tid == 0) {
@@ -485,11 +488,13 @@ __global__ void __launch_bounds__(kSmem ? 256 : kSmallThreads, 1) k_bfs_small(Sm
     mark();
   }
   if (a.prof && tid == 0) a.prof[63] = np;
-  if (a.host_counts && a.l_end == a.L && tid == 0)  // (this kernel produced every level)
-    for (int l = 0; l <= a.L; ++l) {
+  if (a.host_counts && a.l_end == a.L) {  // (this kernel produced every level; one level per thread)
+    __syncthreads();
+    for (int l = tid; l <= a.L; l += kT) {
       a.host_counts[l] = a.ns_out[l];
       a.host_counts[a.L + 1 + l] = a.f_out[l];
     }
+  }
 }
 
 // ------------------------------------------------------------ large levels (one persistent kernel)
@@ -823,11 +828,13 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
     pmark(7);
   }
   // (CTA 0 wrote the counts of this kernel's levels; the small kernel the others)
-  if (a.host_counts && blockIdx.x == 0 && threadIdx.x == 0)
-    for (int l = 0; l <= a.L; ++l) {
+  if (a.host_counts && blockIdx.x == 0) {  // (one level per thread)
+    __syncthreads();
+    for (int l = threadIdx.x; l <= a.L; l += blockDim.x) {
       a.host_counts[l] = a.ns_out[l];
       a.host_counts[a.L + 1 + l] = a.f_out[l];
     }
+  }
 }
 
 // CTAs of the cooperative BFS launch: every CTA resident (occupancy x SMs)

@@ -31,7 +31,7 @@ def main():
         for _ in range(20):
             C, _ = A.multiply(B)
             C.close()
-        tm, tc = [], []
+        tm, tc, toff = [], [], []
         for _ in range(200):
             t0 = time.perf_counter()
             C, _ = A.multiply(B)
@@ -40,6 +40,13 @@ def main():
             t2 = time.perf_counter()
             tm.append(t1 - t0)
             tc.append(t2 - t1)
+        ctx.set_timing(False)
+        for _ in range(200):
+            t0 = time.perf_counter()
+            C, _ = A.multiply(B)
+            toff.append(time.perf_counter() - t0)
+            C.close()
+        ctx.set_timing(True)
         raw = []
         h = ctypes.c_void_p()
         stt = qtmm.Stats()
@@ -50,7 +57,8 @@ def main():
             lib.qt_destroy(h)
             raw.append(t1 - t0)
         med = lambda v: round(1e6 * statistics.median(v), 1)
-        print(f"{w}: multiply {med(tm)} us, close {med(tc)} us, raw ctypes qt_multiply {med(raw)} us", flush=True)
+        print(f"{w}: multiply {med(tm)} us (timing off {med(toff)} us), close {med(tc)} us, "
+              f"raw ctypes qt_multiply {med(raw)} us", flush=True)
 
 
 if __name__ == "__main__":

@@ -246,19 +246,31 @@ def leaf_sweep(ctx, stream):
                     C, st = A.multiply(B)
                     C.close()
                 steps = 10
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                torch.cuda.synchronize()
-                e0.record(stream)
-                for _ in range(steps):
-                    C, st = A.multiply(B)
-                    C.close()
-                e1.record(stream)
-                torch.cuda.synchronize()
-                ms = e0.elapsed_time(e1) / steps
+
+                def timed(wait, timing=True):
+                    ctx.set_timing(timing)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    torch.cuda.synchronize()
+                    e0.record(stream)
+                    for _ in range(steps):
+                        C, st = A.multiply(B, wait=wait)
+                        C.close()
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ctx.set_timing(True)
+                    return e0.elapsed_time(e1) / steps, st
+
+                ms, st = timed(True)
+                ms_off, _ = timed(True, timing=False)  # qt_ctx_set_timing(0): no event records / queries
+                ms_async, _ = timed(False)  # qt_multiply_async, calls pipelined
                 flop = st.block_products * 2.0 * bs ** 3
                 print(json.dumps({"config": "leaf sweep N=4096 (one leaf)", "dtype": "f64" if dtype == np.float64 else "f32",
                                   "bs": bs, "fill": fill, "block_products": st.block_products,
-                                  "ms_step": round(ms, 4), "gflops_effective": round(flop / ms / 1e6, 1)}), flush=True)
+                                  "ms_step": round(ms, 4), "gflops_effective": round(flop / ms / 1e6, 1),
+                                  "ms_step_timing_off": round(ms_off, 4),
+                                  "gflops_timing_off": round(flop / ms_off / 1e6, 1),
+                                  "ms_step_async": round(ms_async, 4),
+                                  "gflops_async": round(flop / ms_async / 1e6, 1)}), flush=True)
                 A.close()
                 B.close()
 
@@ -276,6 +288,28 @@ def main():
             leaf_sweep(ctx, stream)
         elif w == "1":
             run(ctx, stream, "cfg1 dense N=512", qtgen.config(1), steps=200)
+        elif w == "1off":  # config 1, blocking calls with the context's timing off (no event records)
+            c = qtgen.config(1)
+            A = qtmm.Matrix.from_blocks(ctx, c["A"].n, c["A"].leaf_dim, 32, c["A"].brow, c["A"].bcol, c["A"].vals)
+            B = qtmm.Matrix.from_blocks(ctx, c["B"].n, c["B"].leaf_dim, 32, c["B"].brow, c["B"].bcol, c["B"].vals)
+            ctx.set_timing(False)
+            for _ in range(20):
+                C, st = A.multiply(B)
+                C.close()
+            steps = 400
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(steps):
+                C, st = A.multiply(B)
+                C.close()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ctx.set_timing(True)
+            ms = e0.elapsed_time(e1) / steps
+            print(json.dumps({"config": "cfg1 dense N=512, blocking qt_multiply, timing off", "ms_step": round(ms, 4),
+                              "block_products": st.block_products,
+                              "gflops_effective": round(st.block_products * FLOP / ms / 1e6, 1)}), flush=True)
         elif w == "1async":  # config 1 through qt_multiply_async (sync-free: back-to-back on the device)
             c = qtgen.config(1)
             A = qtmm.Matrix.from_blocks(ctx, c["A"].n, c["A"].leaf_dim, 32, c["A"].brow, c["A"].bcol, c["A"].vals)
