@@ -40,7 +40,6 @@ namespace qt {
 
 namespace {
 
-constexpr int kThreads = 256;
 constexpr int kSmallThreads = 1024;
 constexpr int64_t kSmallMaxF = 1 << 13;
 
@@ -518,6 +517,7 @@ __global__ void __launch_bounds__(kSmem ? 256 : kSmallThreads, 1) k_bfs_small(Sm
 // device scans per level (the large levels were host-launch bound).
 constexpr int kLargeThreads = 1024;
 constexpr int kLargeWarps = kLargeThreads / 32;
+static_assert(kLargeWarps <= 32, "the CTA sums reduce one warp's worth of warp partials");
 
 struct LargeBfsArgs {
   int l_begin, L;
@@ -572,36 +572,15 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& gen) {
   __syncthreads();
 }
 
-// CTA-wide lower bound: the first index in [0, n] with v[i] >= x (v ascending),
-// by rounds of 1024 parallel samples (__syncthreads_count) instead of a
-// serial binary search — two rounds of loads for up to 1M groups.
-__device__ __forceinline__ int32_t cta_lower_bound(const int32_t* v, int32_t n, int64_t x) {
-  int32_t lo = 0, hi = n;
-  while (lo < hi) {
-    const int32_t span = hi - lo;
-    const int32_t step = (span + kLargeThreads - 1) / kLargeThreads;
-    const int32_t k = (span + step - 1) / step;  // samples lo, lo+step, ... < hi
-    const int32_t pos = lo + (int32_t)threadIdx.x * step;
-    const bool below = (int32_t)threadIdx.x < k && v[pos] < x;
-    const int32_t c = __syncthreads_count(below);
-    const int32_t nlo = c == 0 ? lo : lo + (c - 1) * step + 1;
-    const int32_t nhi = c == k ? hi : lo + c * step;
-    lo = nlo;
-    hi = nhi;
-  }
-  return lo;
-}
-
 template <bool kExt>
 __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) {
   using BS = cub::BlockScan<int, kLargeThreads>;
-  using BR = cub::BlockReduce<int, kLargeThreads>;
   __shared__ union {
     typename BS::TempStorage scan;
-    typename BR::TempStorage red;
   } tmp;
   __shared__ int s_val[4];
-  __shared__ int s_wsum[kLargeWarps][2];
+  __shared__ int s_wsum[kLargeWarps][4];
+  __shared__ int32_t s_g[2];
   unsigned gen = 0;
   if (threadIdx.x == 0) gen = ld_acquire(&a.bar[1]);
   const bool sym = a.trans & 4;
@@ -625,18 +604,31 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
       if (a.prof && blockIdx.x == 0 && threadIdx.x == 0 && l < 16) a.prof[8 * l + k] = gtimer();
     };
     pmark(0);
-    // this CTA's groups: first task in [b F / G, (b+1) F / G)
-    const int32_t g_lo = cta_lower_bound(cs, ns, (int64_t)F * blockIdx.x / gridDim.x);
-    const int32_t g_hi = cta_lower_bound(cs, ns, (int64_t)F * (blockIdx.x + 1) / gridDim.x);
+    // this CTA's groups: first task in [b F / G, (b+1) F / G) — the first
+    // group starting at or after task p0 is the group of p0 (pc) if it starts
+    // there, else the next one: two dependent loads, no search
+    if (threadIdx.x < 2) {
+      const int64_t p0 = (int64_t)F * (blockIdx.x + threadIdx.x) / gridDim.x;
+      int32_t g = ns;
+      if (p0 < F) {
+        const int32_t s0 = a.pc[l][p0];
+        g = cs[s0] == p0 ? s0 : s0 + 1;
+      }
+      s_g[threadIdx.x] = g;
+    }
+    __syncthreads();
+    const int32_t g_lo = s_g[0], g_hi = s_g[1];
     pmark(1);
     // child counts of task p per C child q (0 for the pruned lower child of a diagonal node)
-    auto counts = [&](int32_t p, int32_t sgrp, int (&c)[4]) {
-      child_counts(op_children(cA, pa[p], mode & 1, sym), op_children(cB, pb[p], mode & 2, sym), c, sc,
-                   sym);
+    auto counts_of = [&](int4 rA, int4 rB, int32_t sgrp, int (&c)[4]) {
+      child_counts(rA, rB, c, sc, sym);
       const int cm = cmask(ck + sgrp, l, a.L, mode & 8, rlo, rhi);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         if (!((cm >> q) & 1)) c[q] = 0;
+    };
+    auto counts = [&](int32_t p, int32_t sgrp, int (&c)[4]) {
+      counts_of(op_children(cA, pa[p], mode & 1, sym), op_children(cB, pb[p], mode & 2, sym), sgrp, c);
     };
     // A. child tasks per (s,q).  A group is walked by W lanes (a power of two
     // near half the level's mean group size): random patterns have ~1-task
@@ -682,14 +674,17 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
         s_wsum[warp][1] = vflag;
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
-        int x0 = 0, x1 = 0;
-        for (int w = 0; w < kLargeWarps; ++w) {
-          x0 += s_wsum[w][0];
-          x1 += s_wsum[w][1];
+      if (warp == 0) {
+        int x0 = lane < kLargeWarps ? s_wsum[lane][0] : 0, x1 = lane < kLargeWarps ? s_wsum[lane][1] : 0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+          x0 += __shfl_xor_sync(FULL, x0, d);
+          x1 += __shfl_xor_sync(FULL, x1, d);
         }
-        a.part[blockIdx.x] = x0;
-        a.part[gridDim.x + blockIdx.x] = x1;
+        if (lane == 0) {
+          a.part[blockIdx.x] = x0;
+          a.part[gridDim.x + blockIdx.x] = x1;
+        }
       }
     }
     pmark(2);
@@ -708,12 +703,25 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
           v[2] += y;
         }
       }
+      // the four CTA sums in one pass (warp shuffles, then warp 0 over the warps)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int r = BR(tmp.red).Sum(v[k]);
-        if (threadIdx.x == 0) s_val[k] = r;
-        __syncthreads();
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) v[k] += __shfl_xor_sync(FULL, v[k], d);
+      if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s_wsum[warp][k] = v[k];
+      __syncthreads();
+      if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          int x = lane < kLargeWarps ? s_wsum[lane][k] : 0;
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(FULL, x, d);
+          if (lane == 0) s_val[k] = x;
+        }
       }
+      __syncthreads();
       tpre = s_val[0];
       Fn = s_val[1];
       gpre = s_val[2];
