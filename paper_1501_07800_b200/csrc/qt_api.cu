@@ -389,6 +389,7 @@ qt_status qt_ctx_destroy(qt_ctx ctx) {
   }
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->pend_host) cudaFreeHost(ctx->pend_host);
+  if (ctx->small_host) cudaFreeHost(ctx->small_host);
   for (auto& e : ctx->pend_ev)
     if (e) cudaEventDestroy(e);
   delete ctx;

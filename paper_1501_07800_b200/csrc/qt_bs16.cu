@@ -46,13 +46,7 @@ void incl_sum(qt_ctx ctx, const int32_t* in, int32_t* out, int64_t n) {
   QT_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, in, out, (int)n, ctx->stream));
   ctx->launches += 2;
 }
-template <class T>
-T read_scalar(qt_ctx ctx, const T* d) {
-  T h;
-  QT_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
-  QT_CUDA(cudaStreamSynchronize(ctx->stream));
-  return h;
-}
+
 
 template <class T>
 __device__ __forceinline__ int swz(int r, int c) {
@@ -378,8 +372,7 @@ void build_from_blocks16(qt_mat M, int64_t n, const int32_t* brow, const int32_t
   k_dup16<<<gfor(n), kT, 0, st>>>(k1.as<uint64_t>(), n, err + 1);
   QT_LAUNCH_CHECK(ctx);
   unsigned long long e[2];
-  QT_CUDA(cudaMemcpyAsync(e, err, 16, cudaMemcpyDeviceToHost, st));
-  QT_CUDA(cudaStreamSynchronize(st));
+  read_small(ctx, e, err, 16);
   if (e[0] != ~0ull) {
     int32_t r, c;
     QT_CUDA(cudaMemcpy(&r, brow + e[0], 4, cudaMemcpyDeviceToHost));
@@ -526,8 +519,7 @@ void cmask16(qt_ctx ctx, int64_t ntiles, const int32_t* ts, const int32_t* pa, c
     QT_LAUNCH_CHECK(ctx);
   }
   unsigned long long h[4];
-  QT_CUDA(cudaMemcpyAsync(h, cnt.p, 32, cudaMemcpyDeviceToHost, st));
-  QT_CUDA(cudaStreamSynchronize(st));
+  read_small(ctx, h, cnt.p, 32);
   for (int i = 0; i < 4; ++i) out[i] = (int64_t)h[i];
 }
 

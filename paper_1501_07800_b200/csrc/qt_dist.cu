@@ -142,9 +142,7 @@ struct NcclTransport : Transport {
     DevBuf s(8 * count, ctx->stream), r(8ll * count * ctx->world, ctx->stream);
     QT_CUDA(cudaMemcpyAsync(s.p, send_host, 8 * count, cudaMemcpyHostToDevice, ctx->stream));
     NCCL_CALL(N.AllGather(s.p, r.p, count, ncclInt64, comm, ctx->stream));
-    QT_CUDA(cudaMemcpyAsync(recv_host, r.p, 8ll * count * ctx->world, cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    QT_CUDA(cudaStreamSynchronize(ctx->stream));
+    read_small(ctx, recv_host, r.p, 8ll * count * ctx->world);
   }
   void group_start() override { NCCL_CALL(nccl().GroupStart()); }
   void send(const void* buf, size_t bytes, int peer) override {
@@ -501,16 +499,14 @@ std::vector<int32_t> needed_rows(qt_mat A, int32_t lo, int32_t hi, DevBuf& d_row
   }
   incl_sum(ctx, flag.as<int32_t>(), incl.as<int32_t>(), nbr);
   int32_t n = 0;
-  QT_CUDA(cudaMemcpyAsync(&n, incl.as<int32_t>() + nbr - 1, 4, cudaMemcpyDeviceToHost, st));
-  QT_CUDA(cudaStreamSynchronize(st));
+  read_small(ctx, &n, incl.as<int32_t>() + nbr - 1, 4);
   d_rows.alloc(4ll * std::max(n, 1), st);
   std::vector<int32_t> h(n);
   if (n > 0) {
     k_scatter_flagged<<<gfor(nbr), kT, 0, st>>>(flag.as<int32_t>(), incl.as<int32_t>(), nbr,
                                                 d_rows.as<int32_t>());
     QT_LAUNCH_CHECK(ctx);
-    QT_CUDA(cudaMemcpyAsync(h.data(), d_rows.p, 4ll * n, cudaMemcpyDeviceToHost, st));
-    QT_CUDA(cudaStreamSynchronize(st));
+    read_small(ctx, h.data(), d_rows.p, 4ll * n);
   }
   return h;
 }
@@ -750,12 +746,8 @@ qt_mat multiply_dist(qt_mat A, qt_mat B, qt_stats* S, double tau) {
   X->group_end();
   // offsets on both sides (host copies decide the message sizes)
   std::vector<int32_t> h_out_counts(n_in), h_in_counts(rx.nrows);
-  if (n_in > 0) {
-    QT_CUDA(cudaMemcpyAsync(h_out_counts.data(), d_out_counts.p, 4 * n_in, cudaMemcpyDeviceToHost, st));
-  }
-  if (rx.nrows > 0) {
-    QT_CUDA(cudaMemcpyAsync(h_in_counts.data(), rx.counts.p, 4ll * rx.nrows, cudaMemcpyDeviceToHost, st));
-  }
+  read_small(ctx, h_out_counts.data(), d_out_counts.p, 4 * n_in);
+  read_small(ctx, h_in_counts.data(), rx.counts.p, 4ll * rx.nrows);
   QT_CUDA(cudaStreamSynchronize(st));
   std::vector<int32_t> h_out_offs(n_in + 1, 0), h_in_offs(rx.nrows + 1, 0);
   for (int64_t i = 0; i < n_in; ++i) h_out_offs[i + 1] = h_out_offs[i] + h_out_counts[i];
@@ -943,8 +935,7 @@ qt_mat multiply_virtual(qt_mat A, qt_mat B, const int32_t* bounds, int P, int g,
     build_row_view(B, v);
     pack_counts(B, v, rx.rows.as<int32_t>(), rx.nrows, rx.counts.as<int32_t>());
     std::vector<int32_t> hc(rx.nrows), ho(rx.nrows + 1, 0);
-    if (rx.nrows > 0)
-      QT_CUDA(cudaMemcpyAsync(hc.data(), rx.counts.p, 4ll * rx.nrows, cudaMemcpyDeviceToHost, st));
+    read_small(ctx, hc.data(), rx.counts.p, 4ll * rx.nrows);
     QT_CUDA(cudaStreamSynchronize(st));
     for (int32_t i = 0; i < rx.nrows; ++i) ho[i + 1] = ho[i] + hc[i];
     QT_CUDA(cudaMemcpyAsync(rx.offs.p, ho.data(), 4ll * (rx.nrows + 1), cudaMemcpyHostToDevice, st));
@@ -1173,9 +1164,8 @@ qt_mat symm_square_dist(qt_mat U, qt_stats* S) {
   }
   X->group_end();
   std::vector<int32_t> out_cnt(P), in_cnt(P);
-  QT_CUDA(cudaMemcpyAsync(out_cnt.data(), cnt.p, 4ll * P, cudaMemcpyDeviceToHost, st));
-  QT_CUDA(cudaMemcpyAsync(in_cnt.data(), rcnt.p, 4ll * P, cudaMemcpyDeviceToHost, st));
-  QT_CUDA(cudaStreamSynchronize(st));
+  read_small(ctx, out_cnt.data(), cnt.p, 4ll * P);
+  read_small(ctx, in_cnt.data(), rcnt.p, 4ll * P);
   std::vector<int64_t> out_off(P + 1, 0), in_off(P + 1, 0);
   for (int q = 0; q < P; ++q) {
     out_off[q + 1] = out_off[q] + (q == g ? 0 : out_cnt[q]);

@@ -121,6 +121,11 @@ struct qt_ctx_s {
   qt::DevBuf zeros;    // one zero block (8 KiB) for absent tcgen05 operands
   void* pinned = nullptr;  // small pinned host staging area
   size_t pinned_bytes = 0;
+  // mapped pinned buffer of read_small: small device-to-host reads written by a
+  // kernel, not a copy-engine memcpy (which would queue behind a bulk
+  // qt_read_back_async copy in flight on the same engine)
+  void* small_host = nullptr;
+  static constexpr size_t kSmallHostBytes = 256 << 10;
   cudaStream_t copy_stream = nullptr;  // device-to-host copies of qt_read_back_async
   cudaStream_t h2d_stream = nullptr;   // host-to-device value copies of qt_create
   cudaEvent_t h2d_done = nullptr;
@@ -207,6 +212,18 @@ bool is_device_ptr(const void* p);
 
 // cub temp storage of at least `bytes` on the ctx
 void* scratch(qt_ctx ctx, size_t bytes);
+
+// Read `bytes` of device memory into host memory `dst` on the ctx stream and
+// wait for it: a kernel stores them into the context's mapped pinned buffer
+// (chunks of kSmallHostBytes), so the read never waits for a copy engine
+// busy with a bulk transfer.
+void read_small(qt_ctx ctx, void* dst, const void* src, size_t bytes);
+template <class T>
+T read_scalar(qt_ctx ctx, const T* d) {
+  T h;
+  read_small(ctx, &h, d, sizeof(T));
+  return h;
+}
 
 // ----- kernels / host drivers (qt_tree.cu)
 // keys from coordinates; validation; sort; duplicate check; swizzled pool fill.

@@ -1000,7 +1000,11 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         ctx->pend_next = (pend_slot + 1) % qt_ctx_s::kPendRing;
         if (ctx->pend_owner[pend_slot]) resolve(ctx->pend_owner[pend_slot]);  // (ring full: the oldest first)
         host_counts = ctx->pend_host + 128 * pend_slot;
-      } else if (syncfree) {
+      } else {
+        // (blocking sync-free product: read after the call's final sync;
+        // otherwise right after the BFS — written by the last BFS kernel into
+        // mapped memory either way, not by a copy that could queue behind a
+        // bulk read-back on the copy engine)
         host_counts = h_counts;
       }
       DevBuf cnt_dev(8 * (L + 1), st);  // [ns(L+1) | F(L+1)]: one D2H copy
@@ -1267,8 +1271,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         C->pool.alloc(cbound, st);
         tr.mark("c_alloc_bound");
       } else {
-        QT_CUDA(cudaMemcpyAsync(h_counts, nsd, 8 * (L + 1), cudaMemcpyDeviceToHost, st));
-        QT_CUDA(cudaStreamSynchronize(st));
+        QT_CUDA(cudaStreamSynchronize(st));  // (the BFS wrote h_counts)
         for (int l = 0; l <= L; ++l) {
           ns[l] = h_counts[l];
           Fa[l] = h_counts[L + 1 + l];

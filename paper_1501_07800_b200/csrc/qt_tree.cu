@@ -188,15 +188,34 @@ void cub_incl_sum(qt_ctx ctx, const T* in, T* out, int64_t n) {
   ctx->launches += 2;
 }
 
-template <class T>
-T read_scalar(qt_ctx ctx, const T* d) {
-  T h;
-  QT_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
-  QT_CUDA(cudaStreamSynchronize(ctx->stream));
-  return h;
+__global__ void k_read_small(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, size_t n) {
+  // (16-byte words where both ends allow it, bytes otherwise)
+  const bool v16 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  const size_t nv = v16 ? n / 16 : 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nv; i += (size_t)gridDim.x * blockDim.x)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  for (size_t i = 16 * nv + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
 }
 
 }  // namespace
+
+void read_small(qt_ctx ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return;
+  if (!ctx->small_host) {
+    QT_CUDA(cudaHostAlloc(&ctx->small_host, qt_ctx_s::kSmallHostBytes, cudaHostAllocMapped));
+  }
+  for (size_t o = 0; o < bytes; o += qt_ctx_s::kSmallHostBytes) {
+    const size_t n = std::min(bytes - o, qt_ctx_s::kSmallHostBytes);
+    const unsigned grid = (unsigned)std::min<size_t>(32, (n + 4095) / 4096);
+    k_read_small<<<grid, 256, 0, ctx->stream>>>(static_cast<const uint8_t*>(src) + o,
+                                                 static_cast<uint8_t*>(ctx->small_host), n);
+    QT_LAUNCH_CHECK(ctx);
+    QT_CUDA(cudaStreamSynchronize(ctx->stream));
+    memcpy(static_cast<uint8_t*>(dst) + o, ctx->small_host, n);
+  }
+}
 
 void* scratch(qt_ctx ctx, size_t bytes) {
   if (ctx->scratch.bytes < bytes) {
@@ -260,8 +279,7 @@ void build_levels(qt_mat M, const int32_t* leaf_ids) {
     QT_LAUNCH_CHECK(ctx);
   }
   // host copy: qt_multiply derives its per-level task counts from it
-  QT_CUDA(cudaMemcpyAsync(M->hist_host.data(), M->hist.p, 8 * H, cudaMemcpyDeviceToHost, st));
-  QT_CUDA(cudaStreamSynchronize(st));
+  read_small(ctx, M->hist_host.data(), M->hist.p, 8 * H);
 }
 
 void build_from_blocks(qt_mat M, int64_t nb, const int32_t* d_brow, const int32_t* d_bcol,
@@ -285,8 +303,7 @@ void build_from_blocks(qt_mat M, int64_t nb, const int32_t* d_brow, const int32_
   k_dup<<<grid_for(nb), kThreads, 0, st>>>(M->key.as<uint64_t>(), nb, err + 1);
   QT_LAUNCH_CHECK(ctx);
   unsigned long long e[2];
-  QT_CUDA(cudaMemcpyAsync(e, err, 16, cudaMemcpyDeviceToHost, st));
-  QT_CUDA(cudaStreamSynchronize(st));
+  read_small(ctx, e, err, 16);
   if (e[0] != ~0ull) {
     int32_t r, c;
     QT_CUDA(cudaMemcpy(&r, d_brow + e[0], 4, cudaMemcpyDeviceToHost));
