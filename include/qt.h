@@ -166,6 +166,12 @@ qt_status qt_create(qt_ctx ctx, int64_t n, int32_t leaf_dim, int32_t block_size,
  * numeric block-sparse multiply (each C block = sum over k ascending of
  * A(I,k)*B(k,J), accumulated in registers, no atomics).  The result is a new
  * handle; A and B are unchanged.  `st` may be NULL.
+ * Precision: QT_F64 computes in FP64 (DMMA); QT_F32 in 3xTF32 on tcgen05
+ * (reading C-9), or — a sparse product whose 4x4-block tensor-core tiles
+ * would be mostly empty — on FP64 copies with the result rounded to FP32
+ * (reading C-30).  The FP32 tiles multiply absent blocks as zeros, so FP32
+ * inputs must be finite (an Inf/NaN would reach C blocks the sparse product
+ * leaves finite); FP64 never combines a present block with an absent one.
  * Multi-rank: collective.  C gets A's block-row ranges; each rank receives
  * from the owners exactly the B block rows its A rows reference (NCCL
  * send/recv) and reports the bytes in `st`.
