@@ -91,8 +91,11 @@ typedef struct {
 /* Create a context on CUDA device `device`.  `cuda_stream` is a cudaStream_t
  * (NULL = the legacy default stream).  `rank`/`world`: this process's rank
  * and the number of ranks.  `nccl_unique_id`: the 128-byte ncclUniqueId made
- * by qt_nccl_unique_id() on rank 0 and broadcast by the caller; must be NULL
- * iff world == 1.  Collective when world > 1 (ncclCommInitRank).
+ * by qt_nccl_unique_id() on rank 0 and broadcast by the caller; required
+ * when world > 1.  With world == 1 it may be NULL (no communicator) or a fresh
+ * id: the context then builds a one-rank NCCL communicator (qt_ctx_info
+ * reports it) — the NCCL binding exercised on a single GPU; multiplies take
+ * the single-GPU path either way.  Collective when world > 1 (ncclCommInitRank).
  * Errors: QT_EINVAL (bad rank/world/device), QT_ECUDA, QT_ENCCL. */
 qt_status qt_ctx_create(int device, void* cuda_stream, int rank, int world,
                         const void* nccl_unique_id, qt_ctx* out);

@@ -296,6 +296,8 @@ static void ctx_create(int device, void* cuda_stream, int rank, int world, const
     if (world > 1) {
       if (hub) dist_init_loopback(c, hub);
       else dist_init(c, uid);
+    } else if (uid) {
+      dist_init(c, uid);  // a one-rank NCCL communicator (the binding on one GPU; multiplies stay local)
     }
     QT_CUDA(cudaStreamSynchronize(c->stream));
   } catch (...) {
@@ -309,8 +311,7 @@ static void ctx_create(int device, void* cuda_stream, int rank, int world, const
 qt_status qt_ctx_create(int device, void* cuda_stream, int rank, int world,
                         const void* nccl_unique_id, qt_ctx* out) {
   API_TRY
-  if ((world > 1) != (nccl_unique_id != nullptr))
-    fail(QT_EINVAL, "nccl_unique_id must be non-NULL iff world > 1");
+  if (world > 1 && !nccl_unique_id) fail(QT_EINVAL, "nccl_unique_id is NULL with world > 1");
   ctx_create(device, cuda_stream, rank, world, nccl_unique_id, nullptr, out);
   API_CATCH
 }
@@ -373,7 +374,7 @@ qt_status qt_ctx_destroy(qt_ctx ctx) {
     cudaStreamDestroy(ctx->comm_stream);
     for (auto& e : ctx->ov_ev) cudaEventDestroy(e);
   }
-  if (ctx->world > 1) dist_finalize(ctx);
+  if (ctx->transport) dist_finalize(ctx);
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   ctx->scratch.release();
   ctx->counters.release();

@@ -150,9 +150,11 @@ def _dtype_code(vals) -> int:
 class Context:
     """One per process (rank): device, stream and (world > 1) NCCL communicator."""
 
-    def __init__(self, device: int = 0, stream=None, process_group=None, loopback=None):
+    def __init__(self, device: int = 0, stream=None, process_group=None, loopback=None, nccl_self=False):
         """``loopback=(hub, rank, world)``: a rank thread of the single-device
-        loopback transport (testing only, see LoopbackHub)."""
+        loopback transport (testing only, see LoopbackHub).  ``nccl_self``: a
+        single-rank context that still builds its own one-rank NCCL
+        communicator (qt_ctx_create with world 1 and a unique id)."""
         import torch
         self.device = device
         if stream is None:
@@ -179,6 +181,9 @@ class Context:
                 src = dist.get_global_rank(process_group, 0) if process_group is not None else 0
                 dist.broadcast_object_list(obj, src=src, group=process_group)
                 uid = ctypes.create_string_buffer(obj[0], 128)
+        if nccl_self and world == 1:
+            uid = ctypes.create_string_buffer(128)
+            _check(_lib.qt_nccl_unique_id(uid))
         self.rank, self.world = rank, world
         h = ctypes.c_void_p()
         _check(_lib.qt_ctx_create(device, sptr, rank, world, uid, ctypes.byref(h)))

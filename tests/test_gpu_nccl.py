@@ -118,3 +118,32 @@ def test_bench_two_gpus_self_launch():
     assert d["n_gpus"] == 2 and d["nccl"]["comm_ranks"] == 2 and d["nccl"]["transport"] == "nccl"
     assert d["bytes_recv_per_gpu"]["max"] == 17039360
     assert d["config"]["global_block_products"] == 4212000
+
+
+def test_nccl_binding_one_rank():
+    """Runs on one GPU: the library loads NCCL (dlopen), builds a one-rank
+    communicator from a fresh unique id (ncclCommInitRank), reports it
+    (ncclCommCount) and tears it down; a multiply on that context equals the
+    oracle (integer values: exact)."""
+    import torch
+    import oracle
+    import qtgen
+    from paper_1501_07800_b200 import build
+    build.build()
+    from paper_1501_07800_b200 import qtmm
+    torch.cuda.init()
+    ctx = qtmm.Context(0, stream=torch.cuda.Stream(0), nccl_self=True)
+    try:
+        assert ctx.info() == {"rank": 0, "world": 1, "comm_ranks": 1, "transport": "nccl"}
+        c = qtgen.config(1, "int")
+        A = qtmm.Matrix.from_blocks(ctx, 512, 128, 32, c["A"].brow, c["A"].bcol, c["A"].vals)
+        B = qtmm.Matrix.from_blocks(ctx, 512, 128, 32, c["B"].brow, c["B"].bcol, c["B"].vals)
+        C, st = A.multiply(B)
+        got = C.to_blocks()
+        ref = oracle.spgemm(16, 32, (c["A"].brow, c["A"].bcol, c["A"].vals), (c["B"].brow, c["B"].bcol, c["B"].vals))
+        assert all(np.array_equal(x, y) for x, y in zip(got, ref))
+        assert st.bytes_recv_payload == 0
+        for M in (A, B, C):
+            M.close()
+    finally:
+        ctx.close()
