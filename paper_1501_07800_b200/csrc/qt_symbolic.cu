@@ -1075,11 +1075,14 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       // dense start: plain and transposed products without screening (the
       // other modes prune by rules the dense maps do not carry)
       static const int dense_env = getenv("QT_DENSE_START") ? atoi(getenv("QT_DENSE_START")) : 4;
-      sa.l0 = (!ext && !sym && !screen && A->dmap.p && B->dmap.p)
+      // (block size 16: the quadrant-mask test applies only to the block-level
+      // pairs, below any level the dense start produces; a row window does not)
+      const bool plain = !sym && !screen;
+      const bool window = row_lo > 0 || row_hi < INT32_MAX;
+      sa.l0 = (plain && !window && A->dmap.p && B->dmap.p)
                   ? std::min(std::min(std::min(dense_env, qt_mat_s::kDenseLevels), l_end), L - 1)
                   : 0;
       if (sa.l0 < 2) sa.l0 = 0;
-      const bool plain = !ext && !sym && !screen;
       sa.dmapA = A->dmap.as<int32_t>();
       sa.dmapB = B->dmap.as<int32_t>();
       static const bool bfs_prof = getenv("QT_BFS_PROF") != nullptr;
@@ -1108,14 +1111,20 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiny_smem(kTinyF)));
           QT_CUDA(cudaFuncSetAttribute(k_bfs_small<true, true, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiny_smem(kTinyF)));
+          QT_CUDA(cudaFuncSetAttribute(k_bfs_small<true, true, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiny_smem(kTinyF)));
           attr_set.fetch_or(bit, std::memory_order_release);
         }
-        if (ext)
+        if (ext && plain)
+          k_bfs_small<true, true, true><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
+        else if (ext)
           k_bfs_small<true, true, false><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
         else if (plain)
           k_bfs_small<false, true, true><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
         else
           k_bfs_small<false, true, false><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
+      } else if (ext && plain) {
+        k_bfs_small<true, false, true><<<1, kSmallThreads, 0, st>>>(sa);
       } else if (ext) {
         k_bfs_small<true, false, false><<<1, kSmallThreads, 0, st>>>(sa);
       } else if (plain) {
