@@ -5,7 +5,10 @@ operands, the symmetric square (block sizes 32 and 16), the screened product and
 every result against the oracle on the same inputs (integer values: exact).
 A 2000-case sweep (QT_FUZZ_MUL=1200 QT_FUZZ_MISC=400 QT_FUZZ_NBR=80) passed in
 round 1; round 2 (FP32 products routed by tile density, bs-16 screening):
-1200 cases (QT_FUZZ_MUL=600 QT_FUZZ_MISC=150 QT_FUZZ_NBR=100) passed."""
+1200 cases (QT_FUZZ_MUL=600 QT_FUZZ_MISC=150 QT_FUZZ_NBR=100) passed, and
+again after the symbolic pass's dense start, plain instantiations and the
+asynchronous products added to the sweep (QT_FUZZ_MUL=800 QT_FUZZ_MISC=150
+QT_FUZZ_NBR=160)."""
 import os
 
 import numpy as np
@@ -82,6 +85,10 @@ def test_fuzz_multiply(qt, ctx, seed):
     got2 = (C @ A).to_blocks()
     ref2 = oracle.spgemm(nbr, bs, ref, t64(Am))
     same(got2, ref2)
+    # qt_multiply_async (sync-free for small products: C's count resolved on first use)
+    if not (ta or tb):
+        Ca, _ = A.multiply(B, wait=False)
+        same(Ca.to_blocks(), oracle.spgemm(nbr, bs, t64(Am), t64(Bm)))
 
 
 @pytest.mark.parametrize("seed", range(N_MISC))
