@@ -115,3 +115,30 @@ def test_timing_off_same_results(qt, ctx, case):
     assert s_on.ms_total > 0
     assert s_off.block_products == s_on.block_products and s_off.c_blocks == s_on.c_blocks
     assert list(s_off.level_tasks) == list(s_on.level_tasks)
+
+
+def test_huge_sparse_grid(qt, ctx):
+    """A 2^15 x 2^15 block grid (n = 1 048 576) holding a few hundred blocks:
+    16 quadtree levels, per-level histograms of 512 KiB read back in chunks of
+    the mapped staging buffer (read_small), a deep BFS over nearly empty
+    levels.  Pattern, values, per-level task counts vs the oracle."""
+    rng = np.random.default_rng(15)
+    nbr = 1 << 15
+    mats = []
+    for _ in range(2):
+        # blocks clustered on a few block rows / columns so that products exist
+        rows = rng.integers(0, 64, size=300) * 512 + rng.integers(0, 4, size=300)
+        cols = rng.integers(0, 64, size=300) * 512 + rng.integers(0, 4, size=300)
+        key = np.unique(rows.astype(np.int64) * nbr + cols)
+        br, bc = (key // nbr).astype(np.int32), (key % nbr).astype(np.int32)
+        v = rng.integers(-4, 5, size=(len(br), 32, 32)).astype(np.float64)
+        mats.append(qtgen.BlockMatrix(nbr * 32, 1024, 32, br, bc, v))
+    Am, Bm = mats
+    C, st = mk(qt, ctx, Am).multiply(mk(qt, ctx, Bm))
+    ref = oracle.spgemm(nbr, 32, (Am.brow, Am.bcol, Am.vals), (Bm.brow, Bm.bcol, Bm.vals))
+    got = C.to_blocks()
+    assert len(ref[0]) > 0
+    assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
+    L, _ = oracle.tree_levels(Am.n, 32, 1024)
+    assert L == 15
+    assert list(st.level_tasks[: L + 1]) == oracle.level_task_counts(L, (Am.brow, Am.bcol), (Bm.brow, Bm.bcol))
