@@ -572,7 +572,9 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& gen) {
   __syncthreads();
 }
 
-template <bool kExt>
+// kPlain: as k_bfs_small's — no symmetric references and no norm tests
+// compiled in (the pair test of the count and emit phases is two NIL checks)
+template <bool kExt, bool kPlain>
 __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) {
   using BS = cub::BlockScan<int, kLargeThreads>;
   __shared__ union {
@@ -583,14 +585,14 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
   __shared__ int32_t s_g[2];
   unsigned gen = 0;
   if (threadIdx.x == 0) gen = ld_acquire(&a.bar[1]);
-  const bool sym = a.trans & 4;
+  const bool sym = !kPlain && (a.trans & 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
   for (int l = a.l_begin; l < a.L; ++l) {
     const bool last = l == a.L - 1;
     const int mode = (a.trans & 7) | ((sym && l < (a.trans >> 8)) ? 8 : 0);
     const bool lastl = kExt && l + 1 == a.L && a.subA;
-    const Screen sc{a.normA[l + 1], a.normB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
+    const Screen sc{kPlain ? nullptr : a.normA[l + 1], kPlain ? nullptr : a.normB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
                     a.trans & 3, lastl ? a.n16A : nullptr, lastl ? a.n16B : nullptr};
     const int32_t rlo = kExt ? a.row_lo : 0, rhi = kExt ? a.row_hi : INT32_MAX;
     const int32_t F = a.f_out[l], ns = a.ns_out[l];
@@ -849,11 +851,13 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
 int large_bfs_grid(qt_ctx ctx) {
   static int per_sm = -1;
   if (per_sm < 0) {
-    int n = 0;
-    int n1 = 0;
-    QT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_bfs_large<false>, kLargeThreads, 0));
-    QT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, k_bfs_large<true>, kLargeThreads, 0));
-    n = std::min(n, n1);
+    int n = 1 << 30;
+    for (const void* f : {(const void*)k_bfs_large<false, false>, (const void*)k_bfs_large<true, false>,
+                          (const void*)k_bfs_large<false, true>, (const void*)k_bfs_large<true, true>}) {
+      int m = 0;
+      QT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, f, kLargeThreads, 0));
+      n = std::min(n, m);
+    }
     if (n < 1) fail(QT_ECUDA, "k_bfs_large cannot be resident");
     per_sm = 1;
   }
@@ -1231,7 +1235,9 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
           la.prof = lprof.as<unsigned long long>();
         }
         void* kargs[] = {&la};
-        QT_CUDA(cudaLaunchCooperativeKernel(ext ? (const void*)k_bfs_large<true> : (const void*)k_bfs_large<false>,
+        const void* kfn = ext ? (plain ? (const void*)k_bfs_large<true, true> : (const void*)k_bfs_large<true, false>)
+                              : (plain ? (const void*)k_bfs_large<false, true> : (const void*)k_bfs_large<false, false>);
+        QT_CUDA(cudaLaunchCooperativeKernel(kfn,
                                             dim3(G), dim3(kLargeThreads), kargs, 0,
                                             st));
         ctx->launches += 1;
