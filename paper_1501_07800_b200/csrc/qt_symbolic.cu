@@ -203,11 +203,14 @@ inline size_t tiny_smem(int cap) {
   return 2 * (3 * 4 + 4 + 8) * (size_t)cap + 4 * 2 * (size_t)cap + 4 * 4 * (size_t)cap + 4 * 4 * (size_t)cap + 64;
 }
 
-// kPlain: a plain or transposed product without screening (no symmetric
-// references, no norm tests): the pair test reduces to two NIL checks and the
-// kernel's code shrinks (the tiny levels are instruction-fetch bound)
-template <bool kExt, bool kSmem, bool kPlain>
+// kMode — products without screening get instantiations with no norm tests
+// compiled in: 1 plain or transposed products (kPlain: no symmetric references
+// either, the pair test is two NIL checks; dense start), 2 the symmetric
+// square (symmetric references always); 0 generic (runtime flags).  The tiny
+// levels are latency and instruction-fetch bound, so the smaller code pays.
+template <bool kExt, bool kSmem, int kMode>
 __global__ void __launch_bounds__(kSmem ? 256 : kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) {
+  constexpr bool kPlain = kMode == 1, kNoNorms = kMode != 0;
   // the tiny variant runs 256 threads: its levels have <= kTinyF tasks and
   // its cost is the latency of block scans and barriers, cheaper with 8 warps
   constexpr int kT = kSmem ? 256 : kSmallThreads;
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(kSmem ? 256 : kSmallThreads, 1) k_bfs_small(Sm
   __shared__ int s_F, s_ns;
   extern __shared__ __align__(16) uint8_t tiny[];
   const int tid = threadIdx.x;
-  const bool sym = !kPlain && (a.trans & 4);
+  const bool sym = kMode == 2 || (kMode == 0 && (a.trans & 4));
   // per-level buffers: shared memory unless the level is read after the kernel
   uint64_t* ck0 = reinterpret_cast<uint64_t*>(tiny);
   const int T = a.tiny_cap;  // capacity (tasks / groups per level) of the shared-memory frontiers
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(kSmem ? 256 : kSmallThreads, 1) k_bfs_small(Sm
   if (tid < QT_MAX_LEVELS && tid <= a.L) {
     s_cA[tid] = a.childA[tid];
     s_cB[tid] = a.childB[tid];
-    if (!kPlain) {
+    if (!kNoNorms) {
       s_nA[tid] = a.normA[tid];
       s_nB[tid] = a.normB[tid];
     }
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(kSmem ? 256 : kSmallThreads, 1) k_bfs_small(Sm
     const int4* cA = s_cA[l];
     const int4* cB = s_cB[l];
     const bool lastl = kExt && l + 1 == a.L && a.subA;
-    const Screen sc{kPlain ? nullptr : s_nA[l + 1], kPlain ? nullptr : s_nB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
+    const Screen sc{kNoNorms ? nullptr : s_nA[l + 1], kNoNorms ? nullptr : s_nB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
                     a.trans & 3, lastl ? a.n16A : nullptr, lastl ? a.n16B : nullptr};
     const int32_t rlo = kExt ? a.row_lo : 0, rhi = kExt ? a.row_hi : INT32_MAX;
     // 1. child-task counts per (task, C child), group-major
@@ -572,10 +575,11 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& gen) {
   __syncthreads();
 }
 
-// kPlain: as k_bfs_small's — no symmetric references and no norm tests
-// compiled in (the pair test of the count and emit phases is two NIL checks)
-template <bool kExt, bool kPlain>
+// kMode: as k_bfs_small's (1 plain, 2 symmetric square, 0 generic) — the
+// pair test of the count and emit phases without runtime mode branches
+template <bool kExt, int kMode>
 __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) {
+  constexpr bool kNoNorms = kMode != 0;
   using BS = cub::BlockScan<int, kLargeThreads>;
   __shared__ union {
     typename BS::TempStorage scan;
@@ -585,14 +589,14 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
   __shared__ int32_t s_g[2];
   unsigned gen = 0;
   if (threadIdx.x == 0) gen = ld_acquire(&a.bar[1]);
-  const bool sym = !kPlain && (a.trans & 4);
+  const bool sym = kMode == 2 || (kMode == 0 && (a.trans & 4));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
   for (int l = a.l_begin; l < a.L; ++l) {
     const bool last = l == a.L - 1;
     const int mode = (a.trans & 7) | ((sym && l < (a.trans >> 8)) ? 8 : 0);
     const bool lastl = kExt && l + 1 == a.L && a.subA;
-    const Screen sc{kPlain ? nullptr : a.normA[l + 1], kPlain ? nullptr : a.normB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
+    const Screen sc{kNoNorms ? nullptr : a.normA[l + 1], kNoNorms ? nullptr : a.normB[l + 1], a.tau2, lastl ? a.subA : nullptr, lastl ? a.subB : nullptr,
                     a.trans & 3, lastl ? a.n16A : nullptr, lastl ? a.n16B : nullptr};
     const int32_t rlo = kExt ? a.row_lo : 0, rhi = kExt ? a.row_hi : INT32_MAX;
     const int32_t F = a.f_out[l], ns = a.ns_out[l];
@@ -847,13 +851,25 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
   }
 }
 
+// the single-CTA BFS instantiation for (row-window/bs-16 extensions, tiny
+// shared-memory frontiers, kMode)
+const void* small_fn(bool ext, bool tiny, int mode) {
+#define QT_SMALL(e, t)                                                                        \
+  (mode == 0 ? (const void*)k_bfs_small<e, t, 0>                                              \
+             : mode == 1 ? (const void*)k_bfs_small<e, t, 1> : (const void*)k_bfs_small<e, t, 2>)
+  return ext ? (tiny ? QT_SMALL(true, true) : QT_SMALL(true, false))
+             : (tiny ? QT_SMALL(false, true) : QT_SMALL(false, false));
+#undef QT_SMALL
+}
+
 // CTAs of the cooperative BFS launch: every CTA resident (occupancy x SMs)
 int large_bfs_grid(qt_ctx ctx) {
   static int per_sm = -1;
   if (per_sm < 0) {
     int n = 1 << 30;
-    for (const void* f : {(const void*)k_bfs_large<false, false>, (const void*)k_bfs_large<true, false>,
-                          (const void*)k_bfs_large<false, true>, (const void*)k_bfs_large<true, true>}) {
+    for (const void* f : {(const void*)k_bfs_large<false, 0>, (const void*)k_bfs_large<true, 0>,
+                          (const void*)k_bfs_large<false, 1>, (const void*)k_bfs_large<true, 1>,
+                          (const void*)k_bfs_large<false, 2>, (const void*)k_bfs_large<true, 2>}) {
       int m = 0;
       QT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, f, kLargeThreads, 0));
       n = std::min(n, m);
@@ -1082,6 +1098,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       // (block size 16: the quadrant-mask test applies only to the block-level
       // pairs, below any level the dense start produces; a row window does not)
       const bool plain = !sym && !screen;
+      const int mode = screen ? 0 : (sym ? 2 : 1);  // the BFS kernels' kMode
       const bool window = row_lo > 0 || row_hi < INT32_MAX;
       sa.l0 = (plain && !window && A->dmap.p && B->dmap.p)
                   ? std::min(std::min(std::min(dense_env, qt_mat_s::kDenseLevels), l_end), L - 1)
@@ -1109,32 +1126,16 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         static std::atomic<unsigned long long> attr_set{0};  // per device (bit d)
         const unsigned long long bit = 1ull << (ctx->device & 63);
         if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-          QT_CUDA(cudaFuncSetAttribute(k_bfs_small<false, true, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiny_smem(kTinyF)));
-          QT_CUDA(cudaFuncSetAttribute(k_bfs_small<false, true, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiny_smem(kTinyF)));
-          QT_CUDA(cudaFuncSetAttribute(k_bfs_small<true, true, false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiny_smem(kTinyF)));
-          QT_CUDA(cudaFuncSetAttribute(k_bfs_small<true, true, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiny_smem(kTinyF)));
+          for (const void* f : {small_fn(false, true, 0), small_fn(false, true, 1), small_fn(false, true, 2),
+                                small_fn(true, true, 0), small_fn(true, true, 1), small_fn(true, true, 2)})
+            QT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiny_smem(kTinyF)));
           attr_set.fetch_or(bit, std::memory_order_release);
         }
-        if (ext && plain)
-          k_bfs_small<true, true, true><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
-        else if (ext)
-          k_bfs_small<true, true, false><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
-        else if (plain)
-          k_bfs_small<false, true, true><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
-        else
-          k_bfs_small<false, true, false><<<1, 256, tiny_smem(sa.tiny_cap), st>>>(sa);
-      } else if (ext && plain) {
-        k_bfs_small<true, false, true><<<1, kSmallThreads, 0, st>>>(sa);
-      } else if (ext) {
-        k_bfs_small<true, false, false><<<1, kSmallThreads, 0, st>>>(sa);
-      } else if (plain) {
-        k_bfs_small<false, false, true><<<1, kSmallThreads, 0, st>>>(sa);
+        void* kargs[] = {&sa};
+        QT_CUDA(cudaLaunchKernel(small_fn(ext, true, mode), dim3(1), dim3(256), kargs, tiny_smem(sa.tiny_cap), st));
       } else {
-        k_bfs_small<false, false, false><<<1, kSmallThreads, 0, st>>>(sa);
+        void* kargs[] = {&sa};
+        QT_CUDA(cudaLaunchKernel(small_fn(ext, false, mode), dim3(1), dim3(kSmallThreads), kargs, 0, st));
       }
       QT_LAUNCH_CHECK(ctx);
       if (bfs_prof) {
@@ -1235,8 +1236,9 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
           la.prof = lprof.as<unsigned long long>();
         }
         void* kargs[] = {&la};
-        const void* kfn = ext ? (plain ? (const void*)k_bfs_large<true, true> : (const void*)k_bfs_large<true, false>)
-                              : (plain ? (const void*)k_bfs_large<false, true> : (const void*)k_bfs_large<false, false>);
+        const void* kfn = mode == 0 ? (ext ? (const void*)k_bfs_large<true, 0> : (const void*)k_bfs_large<false, 0>)
+                          : mode == 1 ? (ext ? (const void*)k_bfs_large<true, 1> : (const void*)k_bfs_large<false, 1>)
+                                      : (ext ? (const void*)k_bfs_large<true, 2> : (const void*)k_bfs_large<false, 2>);
         QT_CUDA(cudaLaunchCooperativeKernel(kfn,
                                             dim3(G), dim3(kLargeThreads), kargs, 0,
                                             st));
