@@ -611,10 +611,10 @@ def measure_e2e(qtmm, ctx, stream, Am, bounds, args, world, dist, barrier):
     bcol = torch.from_numpy(Am.bcol).pin_memory()
     vals = torch.from_numpy(Am.vals).pin_memory()
     outs = [None, None]  # double-buffered pinned results (step i writes outs[i % 2])
-    # (a stream of steps: the first step's H2D and multiply fill the pipeline,
-    # after which the steps are bound by the D2H of C — 20 steps keep the
-    # fill's share small and the region ~0.2 s)
-    steps = max(2, min(args.steps, 20))
+    # (a stream of steps, as many as the device-resident leg times (at most
+    # 50, ~0.5 s): the first step's H2D and multiply fill the pipeline, after
+    # which the steps are bound by the D2H of C)
+    steps = max(2, min(args.steps, 50))
 
     def step(i):
         A = qtmm.Matrix.from_blocks(ctx, Am.n, Am.leaf_dim, BS, brow, bcol, vals, row_bounds=bounds)
