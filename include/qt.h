@@ -289,9 +289,8 @@ qt_status qt_read_back(qt_mat A, int32_t* brow, int32_t* bcol, void* values);
  * C's count is read when C is first used by any entry point (qt_info,
  * qt_read_back, as an operand, ...), so back-to-back multiplies pipeline on
  * the device.  A and B may be destroyed right after the call (stream-ordered
- * reuse).  QT_F32 products always take the tcgen05 kernel here (the FP64
- * route of reading C-30 is qt_multiply's choice only); results agree within
- * the FP32 tolerance either way.
+ * reuse).  QT_F32 products are routed as by qt_multiply (reading C-30; the
+ * FP64 copies of the operands are made stream-ordered on first use).
  * Errors: as qt_multiply. */
 qt_status qt_multiply_async(qt_mat A, qt_mat B, qt_mat* C, qt_stats* st);
 

@@ -571,7 +571,7 @@ qt_status qt_multiply_ex(qt_mat A, qt_mat B, int32_t trans_a, int32_t trans_b, q
   const bool timed = !ctx->async_multiply && ctx->timing;
   if (timed) QT_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   qt_mat R;
-  if (ctx->world == 1 && A->dtype == QT_F32 && !ctx->async_multiply && fp32_prefers_fp64(A, B, trans)) {
+  if (ctx->world == 1 && A->dtype == QT_F32 && fp32_prefers_fp64(A, B, trans)) {
     // reading C-30: a sparse FP32 product whose 4x4-block tcgen05 tiles would
     // be mostly empty runs on FP64 copies through the FP64 kernel (which
     // skips absent blocks) and C is rounded to FP32

@@ -98,10 +98,14 @@ def test_fp32_random_patterns(qt, ctx, monkeypatch, nbr, p, leaf, kind, route):
     rng = np.random.default_rng(nbr * 11 + (kind == "int"))
     Am = random_bm(rng, nbr, p, kind, leaf)
     Bm = random_bm(rng, nbr, p, kind, leaf)
-    C, st = mk(qt, ctx, Am).multiply(mk(qt, ctx, Bm))
+    A, B = mk(qt, ctx, Am), mk(qt, ctx, Bm)
+    C, st = A.multiply(B)
     got = C.to_blocks()
     ref = oracle.spgemm(nbr, 32, ref64(Am), ref64(Bm))
     check(got, ref, kind)
+    # qt_multiply_async takes the same route (sync-free for small products)
+    Ca, _ = A.multiply(B, wait=False)
+    check(Ca.to_blocks(), ref, kind)
     L, _ = oracle.tree_levels(Am.n, 32, leaf)
     assert list(st.level_tasks[: L + 1]) == oracle.level_task_counts(
         L, (Am.brow, Am.bcol), (Bm.brow, Bm.bcol))
