@@ -179,6 +179,7 @@ struct SmallBfsArgs {
   int l0 = 0;  // dense start: levels 1..l0 from the dense node maps (0: off)
   const int32_t* dmapA = nullptr;  // the operands' dense top-level node maps (qt_mat_s::dmap)
   const int32_t* dmapB = nullptr;
+  int stage_cap = 0;  // dense start into global memory: tasks staged in shared memory (after the tiny area), or 0
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -199,7 +200,7 @@ constexpr int kTinyF = 2048;
 // dynamic shared memory of the tiny variant for levels of <= cap tasks (the
 // launch asks only for what the problem's levels need: a large carve-out
 // costs the launch several microseconds)
-inline size_t tiny_smem(int cap) {
+__host__ __device__ inline size_t tiny_smem(int cap) {
   return 2 * (3 * 4 + 4 + 8) * (size_t)cap + 4 * 2 * (size_t)cap + 4 * 4 * (size_t)cap + 4 * 4 * (size_t)cap + 64;
 }
 
@@ -345,12 +346,17 @@ __global__ void __launch_bounds__(kSmem ? 256 : kSmallThreads, 1) k_bfs_small(Sm
     int ex, agg;
     BS(tmp).ExclusiveSum(cnt0 + ((cnt0 > 0) << 16), ex, agg);
     const int o0 = ((1 << (2 * l0)) - 1) / 3;  // offset of level l0 in the dense maps
+    // (a level l0 handed to the next kernel is written through a shared-memory
+    // stage: each thread's tasks are contiguous, so direct stores would be
+    // 32 scattered sectors per warp instruction)
+    int32_t* stg = a.stage_cap > 0 ? reinterpret_cast<int32_t*>(tiny + tiny_smem(T)) : nullptr;
     if (cnt0 > 0) {
       int pos = ex & 0xFFFF;
       const int g = ex >> 16;
       CS(l0)[g] = pos;
       CK(l0)[g] = (uint64_t)tid;
-      int32_t *pa0 = PA(l0), *pb0 = PB(l0), *pc0 = PC(l0);
+      int32_t *pa0 = stg ? stg : PA(l0), *pb0 = stg ? stg + a.stage_cap : PB(l0),
+              *pc0 = stg ? stg + 2 * a.stage_cap : PC(l0);
       for (unsigned msk = kmask; msk; msk &= msk - 1) {
         const int sk = sp4(__ffs(msk) - 1);
         pa0[pos] = sDA[o0 + ((rA0 & 0xFF) | (sk << (rA0 >> 8)))];
@@ -360,6 +366,15 @@ __global__ void __launch_bounds__(kSmem ? 256 : kSmallThreads, 1) k_bfs_small(Sm
       }
     }
     __syncthreads();
+    if (stg) {
+      const int F0 = agg & 0xFFFF;
+      int32_t *pa0 = PA(l0), *pb0 = PB(l0), *pc0 = PC(l0);
+      for (int i = tid; i < F0; i += kT) {
+        pa0[i] = stg[i];
+        pb0[i] = stg[a.stage_cap + i];
+        pc0[i] = stg[2 * a.stage_cap + i];
+      }
+    }
     if (tid == 0) {
       const int F0 = agg & 0xFFFF, ns0 = agg >> 16;
       CS(l0)[ns0] = F0;
@@ -1131,8 +1146,15 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
             QT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiny_smem(kTinyF)));
           attr_set.fetch_or(bit, std::memory_order_release);
         }
+        // dense start straight into the next kernel's level: staged (when it fits)
+        size_t smem = tiny_smem(sa.tiny_cap);
+        sa.stage_cap = 0;
+        if (sa.l0 > 0 && sa.l0 == l_end && smem + 12 * (size_t)F[l_end] <= tiny_smem(kTinyF)) {
+          sa.stage_cap = (int)F[l_end];
+          smem += 12 * (size_t)F[l_end];
+        }
         void* kargs[] = {&sa};
-        QT_CUDA(cudaLaunchKernel(small_fn(ext, true, mode), dim3(1), dim3(256), kargs, tiny_smem(sa.tiny_cap), st));
+        QT_CUDA(cudaLaunchKernel(small_fn(ext, true, mode), dim3(1), dim3(256), kargs, smem, st));
       } else {
         void* kargs[] = {&sa};
         QT_CUDA(cudaLaunchKernel(small_fn(ext, false, mode), dim3(1), dim3(kSmallThreads), kargs, 0, st));
