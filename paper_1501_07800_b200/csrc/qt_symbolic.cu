@@ -25,9 +25,11 @@
 // occupancy histograms kept with each matrix — so all frontier buffers are
 // sized exactly and the BFS runs without host round trips.  The top levels
 // (frontiers up to 8K tasks) run in ONE single-CTA kernel with block-wide
-// scans; the large levels in ONE persistent cooperative kernel whose phases
-// are separated by grid-wide barriers.  One host sync remains, before the
-// numeric kernel (to size C's block pool).
+// scans (plain products start at level <= 4 from dense node maps); the large
+// levels in ONE persistent cooperative kernel whose phases are separated by
+// grid-wide barriers.  One host sync remains for large products, before the
+// numeric kernel (to size C's block pool); small products size C by an upper
+// bound and run sync-free (multiply_local).
 #include <atomic>
 #include <chrono>
 #include <cstdlib>
