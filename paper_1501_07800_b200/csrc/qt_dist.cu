@@ -914,6 +914,7 @@ qt_mat truncate_dist(qt_mat A, double tau) {
 // ------------------------------------------------------------ virtual ranks
 
 qt_mat multiply_virtual(qt_mat A, qt_mat B, const int32_t* bounds, int P, int g, qt_stats* S) {
+  if (g < 0 || g >= P) fail(QT_EINVAL, "virtual rank %d not in [0,%d)", g, P);
   qt_ctx ctx = A->ctx;
   cudaStream_t st = ctx->stream;
   const size_t bb = 1024 * elem_size(A->dtype);
