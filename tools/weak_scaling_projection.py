@@ -8,6 +8,8 @@ part of it: its bytes are reported beside the time, and 34 MB at NVLink's
 ~700 GB/s is ~50 us.  A projection, not a multi-GPU measurement.
 
   python tools/weak_scaling_projection.py > profiles/r02_weak_scaling_projection.jsonl
+  python tools/weak_scaling_projection.py cfg4   # strong scaling of config 4 (one fixed
+                                                 # matrix split into P strips by qt_plan_strips)
 """
 import json
 import os
@@ -28,11 +30,17 @@ def main():
     stream = torch.cuda.Stream()
     ctx = qtmm.Context(0, stream=stream)
     os.environ["QT_OVERLAP"] = "0"  # one numeric launch per rank (nothing to overlap on one GPU)
+    strong = len(sys.argv) > 1 and sys.argv[1] == "cfg4"
     base = None
+    M4 = qtgen.config(4)["A"] if strong else None
     for P in (1, 2, 4, 8):
-        M = qtgen.config(5, P=P)["A"]
+        M = M4 if strong else qtgen.config(5, P=P)["A"]
         A = qtmm.Matrix.from_blocks(ctx, M.n, M.leaf_dim, 32, M.brow, M.bcol, M.vals)
-        bounds = [g * (M.nbr // P) for g in range(P)] + [M.nbr]
+        if strong:  # product-balanced strips at leaf rows (the library's planner)
+            b, _ = qtmm.plan_strips(M.n, 32, P, (M.brow, M.bcol), M.brow, align_rows=M.leaf_dim // 32)
+            bounds = [int(x) for x in b]
+        else:
+            bounds = [g * (M.nbr // P) for g in range(P)] + [M.nbr]
         ranks = []
         for g in range(P):
             for _ in range(2):
@@ -52,9 +60,11 @@ def main():
         value = prods * FLOP / (t * 1e-3) / 1e9
         if base is None:
             base = value
-        print(json.dumps({"config": "cfg5 weak scaling, projected from virtual ranks", "P": P,
+        print(json.dumps({"config": ("cfg4 strong scaling" if strong else "cfg5 weak scaling")
+                          + ", projected from virtual ranks", "P": P, "bounds": bounds,
                           "projected_gflops": round(value, 1), "per_gpu_gflops": round(value / P, 1),
                           "efficiency_vs_P1": round(value / (base * P), 4), "slowest_rank_ms": t,
+                          "speedup_vs_P1": round(value / base, 3),
                           "block_products": prods,
                           "bytes_recv_max": max(r["bytes_recv_payload"] for r in ranks),
                           "ranks": ranks}), flush=True)
