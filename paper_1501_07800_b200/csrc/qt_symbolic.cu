@@ -206,14 +206,15 @@ __host__ __device__ inline size_t tiny_smem(int cap) {
   return 2 * (3 * 4 + 4 + 8) * (size_t)cap + 4 * 2 * (size_t)cap + 4 * 4 * (size_t)cap + 4 * 4 * (size_t)cap + 64;
 }
 
-// kMode — products without screening get instantiations with no norm tests
-// compiled in: 1 plain or transposed products (kPlain: no symmetric references
-// either, the pair test is two NIL checks; dense start), 2 the symmetric
-// square (symmetric references always); 0 generic (runtime flags).  The tiny
+// kMode — instantiations without the runtime mode branches: 1 plain or
+// transposed products (kPlain: no symmetric references, no norm tests — the
+// pair test is two NIL checks; dense start), 2 the symmetric square (symmetric
+// references always, no norm tests), 3 screened plain products (norm tests,
+// no symmetric references); 0 generic (runtime flags).  The tiny
 // levels are latency and instruction-fetch bound, so the smaller code pays.
 template <bool kExt, bool kSmem, int kMode>
 __global__ void __launch_bounds__(kSmem ? 256 : kSmallThreads, 1) k_bfs_small(SmallBfsArgs a) {
-  constexpr bool kPlain = kMode == 1, kNoNorms = kMode != 0;
+  constexpr bool kPlain = kMode == 1, kNoNorms = kMode == 1 || kMode == 2;
   // the tiny variant runs 256 threads: its levels have <= kTinyF tasks and
   // its cost is the latency of block scans and barriers, cheaper with 8 warps
   constexpr int kT = kSmem ? 256 : kSmallThreads;
@@ -592,11 +593,11 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& gen) {
   __syncthreads();
 }
 
-// kMode: as k_bfs_small's (1 plain, 2 symmetric square, 0 generic) — the
+// kMode: as k_bfs_small's (1 plain, 2 symmetric square, 3 screened, 0 generic) — the
 // pair test of the count and emit phases without runtime mode branches
 template <bool kExt, int kMode>
 __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) {
-  constexpr bool kNoNorms = kMode != 0;
+  constexpr bool kNoNorms = kMode == 1 || kMode == 2;
   using BS = cub::BlockScan<int, kLargeThreads>;
   __shared__ union {
     typename BS::TempStorage scan;
@@ -872,8 +873,10 @@ __global__ void __launch_bounds__(kLargeThreads, 1) k_bfs_large(LargeBfsArgs a) 
 // shared-memory frontiers, kMode)
 const void* small_fn(bool ext, bool tiny, int mode) {
 #define QT_SMALL(e, t)                                                                        \
-  (mode == 0 ? (const void*)k_bfs_small<e, t, 0>                                              \
-             : mode == 1 ? (const void*)k_bfs_small<e, t, 1> : (const void*)k_bfs_small<e, t, 2>)
+  (mode == 0   ? (const void*)k_bfs_small<e, t, 0>                                            \
+   : mode == 1 ? (const void*)k_bfs_small<e, t, 1>                                            \
+   : mode == 2 ? (const void*)k_bfs_small<e, t, 2>                                            \
+               : (const void*)k_bfs_small<e, t, 3>)
   return ext ? (tiny ? QT_SMALL(true, true) : QT_SMALL(true, false))
              : (tiny ? QT_SMALL(false, true) : QT_SMALL(false, false));
 #undef QT_SMALL
@@ -886,7 +889,8 @@ int large_bfs_grid(qt_ctx ctx) {
     int n = 1 << 30;
     for (const void* f : {(const void*)k_bfs_large<false, 0>, (const void*)k_bfs_large<true, 0>,
                           (const void*)k_bfs_large<false, 1>, (const void*)k_bfs_large<true, 1>,
-                          (const void*)k_bfs_large<false, 2>, (const void*)k_bfs_large<true, 2>}) {
+                          (const void*)k_bfs_large<false, 2>, (const void*)k_bfs_large<true, 2>,
+                          (const void*)k_bfs_large<false, 3>, (const void*)k_bfs_large<true, 3>}) {
       int m = 0;
       QT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, f, kLargeThreads, 0));
       n = std::min(n, m);
@@ -1115,7 +1119,7 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
       // (block size 16: the quadrant-mask test applies only to the block-level
       // pairs, below any level the dense start produces; a row window does not)
       const bool plain = !sym && !screen;
-      const int mode = screen ? 0 : (sym ? 2 : 1);  // the BFS kernels' kMode
+      const int mode = screen ? (sym ? 0 : 3) : (sym ? 2 : 1);  // the BFS kernels' kMode
       const bool window = row_lo > 0 || row_hi < INT32_MAX;
       sa.l0 = (plain && !window && A->dmap.p && B->dmap.p)
                   ? std::min(std::min(std::min(dense_env, qt_mat_s::kDenseLevels), l_end), L - 1)
@@ -1144,7 +1148,8 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
         const unsigned long long bit = 1ull << (ctx->device & 63);
         if (!(attr_set.load(std::memory_order_acquire) & bit)) {
           for (const void* f : {small_fn(false, true, 0), small_fn(false, true, 1), small_fn(false, true, 2),
-                                small_fn(true, true, 0), small_fn(true, true, 1), small_fn(true, true, 2)})
+                                small_fn(false, true, 3), small_fn(true, true, 0), small_fn(true, true, 1),
+                                small_fn(true, true, 2), small_fn(true, true, 3)})
             QT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tiny_smem(kTinyF)));
           attr_set.fetch_or(bit, std::memory_order_release);
         }
@@ -1260,9 +1265,10 @@ qt_mat multiply_local(qt_mat A, qt_mat B, qt_stats* stp, float* ms_sym, float* m
           la.prof = lprof.as<unsigned long long>();
         }
         void* kargs[] = {&la};
-        const void* kfn = mode == 0 ? (ext ? (const void*)k_bfs_large<true, 0> : (const void*)k_bfs_large<false, 0>)
+        const void* kfn = mode == 0   ? (ext ? (const void*)k_bfs_large<true, 0> : (const void*)k_bfs_large<false, 0>)
                           : mode == 1 ? (ext ? (const void*)k_bfs_large<true, 1> : (const void*)k_bfs_large<false, 1>)
-                                      : (ext ? (const void*)k_bfs_large<true, 2> : (const void*)k_bfs_large<false, 2>);
+                          : mode == 2 ? (ext ? (const void*)k_bfs_large<true, 2> : (const void*)k_bfs_large<false, 2>)
+                                      : (ext ? (const void*)k_bfs_large<true, 3> : (const void*)k_bfs_large<false, 3>);
         QT_CUDA(cudaLaunchCooperativeKernel(kfn,
                                             dim3(G), dim3(kLargeThreads), kargs, 0,
                                             st));
